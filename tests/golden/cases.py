@@ -1,0 +1,80 @@
+"""Golden-case definitions shared by the fixture generator (run once, in the
+build container, against the reference) and the tests (run anywhere).
+
+Each case names a mesh, a time degree, a linearization and discretization
+options; inputs come from ``paper_2603_28706_b200.synth`` with a fixed seed
+so the fixture stores only what the reference computed plus the inputs
+needed to recompute them.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from paper_2603_28706_b200.synth import SynthConfig, CONFIGS
+
+
+def forcing_a(x, y, t):
+    """A smooth body force used by the f != 0 residual case; returns (..., 2)."""
+    return np.stack([np.sin(2.0 * x + 1.0) * np.cos(y) + t, x * y - 0.5 * t * np.cos(3.0 * y)], axis=-1)
+
+
+FORCINGS = {"zero": None, "a": forcing_a}
+
+
+def ghat_field(X, Y):
+    """Velocity field whose Q2 interpolant is used as the Nitsche lifting g_hat."""
+    return np.stack([0.3 * np.sin(np.pi * X) * np.cos(0.5 * Y) + 0.1, -0.2 * X * Y + 0.05 * np.cos(2 * X)], axis=-1)
+
+
+@dataclass(frozen=True)
+class Case:
+    name: str
+    cfg: SynthConfig
+    variant: str = "modn"
+    sigma_max: float | None = None  # None -> nu (harness.py:49-58)
+    neumann_sides: tuple = ()  # subset of ("bottom", "right", "top", "left")
+    ghat: bool = False
+    forcing: str = "zero"
+    t_start: float = 0.0
+    patches: bool = False  # also build STMG patches / Vanka / V-cycle
+    surrogate: bool = True
+    min_cells: int = 4
+
+
+def _cfg(name, nx, ny, k, p=1.5, delta=1e-2, nu=1.0, nu_inf=1e-3, modes=4, seed=1, **kw):
+    return SynthConfig(name, nx, ny, k, p, delta, nu, nu_inf, modes, seed, **kw)
+
+
+CASES = [
+    Case("cfg1", CONFIGS["cfg1"], patches=True),
+    Case("cfg1_exact", replace(CONFIGS["cfg1"], name="cfg1_exact"), patches=True, surrogate=False),
+    Case("cfg1_pic", replace(CONFIGS["cfg1"], name="cfg1_pic"), variant="pic"),
+    Case("cfg1_exn", replace(CONFIGS["cfg1"], name="cfg1_exn"), variant="exn"),
+    Case("n1_k0_pic", _cfg("n1_k0_pic", 1, 1, 0, seed=11), variant="pic"),
+    Case("n1_k1_exn", _cfg("n1_k1_exn", 1, 1, 1, seed=12), variant="exn"),
+    Case("n2_k1_modn", _cfg("n2_k1_modn", 2, 2, 1, seed=13, p=1.3, delta=1e-3, nu_inf=0.0)),
+    Case("rect_k2_exn", _cfg("rect_k2_exn", 3, 2, 2, seed=14, extents=(0.0, -0.5, 2.0, 1.0)), variant="exn", t_start=0.3),
+    Case("n4_k0_modn", _cfg("n4_k0_modn", 4, 4, 0, seed=15), sigma_max=0.05),
+    Case("n4_k2_pic", _cfg("n4_k2_pic", 4, 4, 2, seed=16, p=1.1, delta=1e-4, nu_inf=1e-4), variant="pic"),
+    Case("n4_ghat_exn", _cfg("n4_ghat_exn", 4, 4, 1, seed=17), variant="exn", ghat=True),
+    Case("n4_neumann", _cfg("n4_neumann", 4, 4, 1, seed=18), neumann_sides=("right",)),
+    Case("n4_forcing", _cfg("n4_forcing", 4, 4, 1, seed=19), forcing="a", t_start=0.25),
+    Case("n5x3_mixed", _cfg("n5x3_mixed", 5, 3, 1, seed=20, gamma1=1e3, gamma2=5e2, gamma_cip=0.5),
+         variant="exn", neumann_sides=("top", "left"), ghat=True, forcing="a"),
+    # Patch / Vanka / V-cycle cases (levels: 6 -> 3, 8 -> 4).
+    Case("p6_k0_exn", _cfg("p6_k0_exn", 6, 6, 0, seed=21), variant="exn", patches=True),
+    Case("p6_k1_modn", _cfg("p6_k1_modn", 6, 6, 1, seed=22), patches=True),
+    Case("p6_k2_pic_exact", _cfg("p6_k2_pic_exact", 6, 6, 2, seed=23, p=1.3, delta=1e-3), variant="pic",
+         patches=True, surrogate=False),
+    Case("p6_neumann_ghat", _cfg("p6_neumann_ghat", 6, 6, 1, seed=24), variant="exn", patches=True,
+         neumann_sides=("bottom",), ghat=True),
+    Case("p8_k1_exn_rect", _cfg("p8_k1_exn_rect", 8, 4, 1, seed=25, extents=(0.0, 0.0, 2.0, 1.0)), variant="exn",
+         patches=True, min_cells=2),
+]
+
+CASE_BY_NAME = {c.name: c for c in CASES}
+
+TRANSFER_PAIRS = [(1, 1), (2, 2), (3, 3), (4, 2), (4, 4)]  # coarse (nx, ny); fine is 2x

@@ -1,0 +1,54 @@
+"""Shared test helpers: golden fixture loading and oracle construction."""
+
+from __future__ import annotations
+
+import math
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+for p in (ROOT, GOLDEN):
+    if p not in sys.path:
+        sys.path.insert(0, p)
+
+from cases import CASE_BY_NAME, CASES, FORCINGS  # noqa: E402
+from oracle import pdst_oracle as orc  # noqa: E402
+
+
+def load(name):
+    return dict(np.load(os.path.join(GOLDEN, f"{name}.npz")))
+
+
+def variant_of(case):
+    if case.variant == "pic":
+        return orc.Variant("pic")
+    if case.variant == "exn":
+        return orc.Variant("exn")
+    return orc.Variant("modn", case.cfg.nu if case.sigma_max is None else case.sigma_max)
+
+
+def oracle_slab(case, fx):
+    cfg = case.cfg
+    grid = orc.Grid(cfg.nx, cfg.ny, cfg.extents, fx["tags"], cfg.gamma1, cfg.gamma2, cfg.gamma_cip,
+                    fx.get("g_hat"))
+    params = orc.Params(cfg.p, cfg.delta, cfg.nu, cfg.nu_inf)
+    return orc.Slab(grid, params, cfg.k, fx["nodes"], fx["weights"], fx["K_t"], fx["m_t"], cfg.tau,
+                    case.t_start, fx["v_minus"], FORCINGS[case.forcing])
+
+
+def rel_err(a, b):
+    """(relative L2, relative Linf) of a against reference b."""
+    a, b = np.asarray(a).ravel(), np.asarray(b).ravel()
+    nb2 = np.linalg.norm(b)
+    nbi = np.abs(b).max() if b.size else 0.0
+    e2 = np.linalg.norm(a - b) / (nb2 if nb2 > 0 else 1.0)
+    ei = np.abs(a - b).max() / (nbi if nbi > 0 else 1.0) if b.size else 0.0
+    return e2, ei
+
+
+def assert_close(a, b, tol=1e-12, what=""):
+    e2, ei = rel_err(a, b)
+    assert e2 <= tol and ei <= tol, f"{what}: rel L2 {e2:.3e}, rel Linf {ei:.3e} > {tol:.0e}"
