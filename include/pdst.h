@@ -1,0 +1,127 @@
+/* pdst.h — C ABI of the B200 slab hot path (libpdst.so).
+ *
+ * Drop-in boundary for the operator/smoother seam of the reference package
+ * pdflow (arXiv 2603.28706).  Every entry point replaces one reference
+ * interface (file:line into /root/reference/pkg/src/pdflow):
+ *
+ *   pdst_create            SlabContext + Discretization setup      slab.py:71-112, forms.py:135-283
+ *   pdst_set_lifting       DiscretizationConfig.g_hat / lifting     forms.py:60-83, 343-356
+ *   pdst_linearize         SlabJacobian.__init__                    slab.py:183-191, forms.py:527-578
+ *   pdst_jacobian_apply    SlabJacobian.matvec / .apply             slab.py:193-205, forms.py:581-652
+ *   pdst_jacobian_defect   r - level.matvec(d) inside vanka_smooth   solver/multigrid.py:336
+ *   pdst_residual          slab_residual                            slab.py:168-173, forms.py:435-516
+ *   pdst_mass_apply        MassNorm.apply                           solver/newton.py:112-117
+ *   pdst_mass_dot          MassNorm.norm / FGMRES M-inner products  solver/newton.py:119-121, krylov.py:67-68
+ *   pdst_dot               FGMRES Euclidean dots on M-weighted vecs solver/krylov.py:102, 106
+ *   pdst_cell_maps         Discretization.cell_nodes / patch ids    femspace.py:127-140, forms.py:192-196,
+ *                                                                   solver/multigrid.py:273-275
+ *   pdst_hierarchy         MgGeometry.from_fine                     solver/multigrid.py:164-191
+ *   pdst_patches_build     StmgPreconditioner patch setup           solver/multigrid.py:261-299, 475-488
+ *   pdst_patch_matrices    PatchSet.matrices (read back)            solver/multigrid.py:198-209
+ *   pdst_vanka             vanka_smooth                             solver/multigrid.py:327-340
+ *   pdst_level_apply       MgLevel.matvec (coarse Galerkin levels)  solver/multigrid.py:234-248, 302-324
+ *   pdst_restrict          StmgPreconditioner._restrict             solver/multigrid.py:523-532
+ *   pdst_prolong           StmgPreconditioner._prolong              solver/multigrid.py:534-543
+ *   pdst_vcycle            StmgPreconditioner.apply                 solver/multigrid.py:545-578
+ *
+ * Conventions: all arrays are fp64 (integers int64) in the reference layout
+ * — slab vectors are (k+1) node-major blocks of nd = Mv + Mp, velocity dofs
+ * interleaved 2*node + component with nodes row-major (y, x), then 3 P1disc
+ * dofs per cell.  `where` says whether pointers are host memory (copied in
+ * and out, call is synchronous) or device memory on the handle's device
+ * (call is asynchronous on the handle's stream).  The caller owns every
+ * argument buffer; the handle owns all device caches.  A handle is bound to
+ * one device and stream and is not thread safe.
+ */
+#ifndef PDST_H
+#define PDST_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define PDST_OK 0
+#define PDST_EINVAL 1    /* bad argument (maps to ValueError) */
+#define PDST_EDOMAIN 2   /* delta <= 0 etc. (ConstitutiveDomainError) */
+#define PDST_ESINGULAR 3 /* singular patch (SingularPatchError) */
+#define PDST_ECUDA 4     /* CUDA runtime failure */
+#define PDST_ESTATE 5    /* call order (e.g. apply before linearize) */
+#define PDST_ENOTSUP 6   /* unsupported size (k > 3 for the kernels) */
+
+#define PDST_HOST 0
+#define PDST_DEVICE 1
+
+/* linearization kinds (constitutive.py:133-160) */
+#define PDST_PICARD 0
+#define PDST_EXACT_NEWTON 1
+#define PDST_MODIFIED_NEWTON 2
+
+typedef struct pdst_handle pdst_handle;
+
+typedef struct {
+  int32_t nx, ny;              /* cells per direction */
+  double x0, y0, x1, y1;       /* rectangle */
+  const uint8_t* dirichlet;    /* 2(nx+ny) flags, sides bottom,right,top,left; NULL = all Dirichlet */
+} pdst_mesh;
+
+typedef struct {
+  int32_t k;                   /* DG(k) in time, k+1 right Radau nodes */
+  const double* nodes;         /* k+1 */
+  const double* weights;       /* k+1 */
+  const double* K_t;           /* (k+1)^2 row-major */
+  const double* m_t;           /* k+1 */
+} pdst_time;
+
+typedef struct {
+  double gamma1, gamma2, gamma_cip;
+  int32_t enable_viscous, enable_convection, enable_pressure;
+} pdst_disc;
+
+typedef struct {
+  double p, delta, nu, nu_inf;
+} pdst_params;
+
+int pdst_create(const pdst_mesh* mesh, const pdst_time* time, const pdst_disc* disc, const pdst_params* params,
+                double tau, int device, void* stream, pdst_handle** out);
+int pdst_destroy(pdst_handle* h);
+int pdst_set_stream(pdst_handle* h, void* stream);
+int pdst_sizes(const pdst_handle* h, int64_t* mv, int64_t* mp, int64_t* nd, int64_t* ndof);
+
+int pdst_set_lifting(pdst_handle* h, const double* g_hat, int where); /* g_hat: Mv or NULL */
+int pdst_linearize(pdst_handle* h, const double* U, int kind, double sigma_max, int where);
+int pdst_jacobian_apply(pdst_handle* h, const double* x, double* y, int where);
+int pdst_jacobian_defect(pdst_handle* h, const double* x, const double* r, double* y, int where);
+/* f_qp: (k+1, ncells, 16, 2) body force at x-major volume points, or NULL (f = 0);
+   advect: (k+1)*nd lagged state or NULL (= U) */
+int pdst_residual(pdst_handle* h, const double* U, const double* v_minus, const double* f_qp, const double* advect,
+                  double* R, int where);
+int pdst_mass_apply(pdst_handle* h, const double* x, double* y, int where);
+int pdst_mass_dot(pdst_handle* h, const double* a, const double* b, double* out, int where);
+int pdst_dot(pdst_handle* h, const double* a, const double* b, int64_t n, double* out, int where);
+
+/* integer maps, host output: cell_nodes (ncells, 9), patch_ids (ncells, 21(k+1)) */
+int pdst_cell_maps(pdst_handle* h, int64_t* cell_nodes, int64_t* patch_ids);
+
+/* multigrid: levels 0 (coarsest) .. L-1 (finest = the handle mesh) */
+int pdst_hierarchy(pdst_handle* h, int min_cells, int* num_levels);
+int pdst_level_sizes(pdst_handle* h, int level, int32_t* nx, int32_t* ny, int64_t* ndof);
+/* surrogate != 0: finest patches from the blended state at rep_fraction; coarse levels exact.
+   On ESINGULAR, *bad_level / *bad_patch identify the first singular patch. */
+int pdst_patches_build(pdst_handle* h, int surrogate, double rep_fraction, int* bad_level, int64_t* bad_patch);
+int pdst_patch_matrices(pdst_handle* h, int level, double* mats /* host (ncells, D, D) */);
+int pdst_vanka(pdst_handle* h, int level, double* d, const double* r, int steps, double omega, int where);
+int pdst_level_apply(pdst_handle* h, int level, const double* x, double* y, int where);
+int pdst_restrict(pdst_handle* h, int fine_level, const double* r_fine, double* r_coarse, int where);
+int pdst_prolong(pdst_handle* h, int fine_level, const double* e_coarse, double* e_fine, int where);
+int pdst_vcycle(pdst_handle* h, const double* r, double* z, int pre, int post, double omega, int where);
+
+const char* pdst_last_error(void);
+const char* pdst_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PDST_H */

@@ -1,0 +1,116 @@
+// pdst_device.cuh — device-side tables, kernel parameter blocks and the
+// per-cell Q2/P1disc element math shared by the slab Jacobian, residual and
+// patch kernels (sm_100a, fp64).
+//
+// Mathematics follows the reference pdflow package (file:line into
+// /root/reference/pkg/src/pdflow):
+//   tangent coefficients  constitutive.py:323-337
+//   Jacobian action       forms.py:581-652, slab.py:193-201
+//   residual              forms.py:435-516, slab.py:162-173
+//   tables                femspace.py:46-106 (x-major volume points q = 4 qx + qy,
+//                         local node a = 3 jy + ix, interleaved components)
+//
+// Layout conventions (global memory):
+//   slab vectors  (k+1) blocks of nd = Mv + Mp doubles, Mv = 2 (2nx+1)(2ny+1);
+//                 velocity dof of node (X, Y) component d at 2 (Y (2nx+1) + X) + d;
+//                 pressure dof j of cell c at Mv + 3 c + j
+//   qp caches     [mu][q][cell] (structure of arrays, coalesced over cells)
+//   face caches   [mu][bface][q], bface = side offset + index along the side,
+//                 side order bottom, right, top, left
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pdst {
+
+constexpr int MAXK1 = 7;
+
+// 1-D Gauss(4) on [0,1] and Q2 Lagrange tables, filled from the host.
+struct Tables {
+  double s[4];      // Gauss points
+  double w[4];      // Gauss weights
+  double B[4][3];   // L_i(s_q)
+  double G[4][3];   // L_i'(s_q)
+  double M1[3][3];  // 1-D mass sum_q w_q L_i L_j
+  double E[2][3];   // L_i(0), L_i(1)
+  double dE[2][3];  // L_i'(0), L_i'(1)
+};
+
+extern __constant__ Tables c_tab;
+
+struct Geom {
+  int nx, ny;    // cells
+  int nnx, nny;  // Q2 nodes per direction
+  int ncells;
+  int mv, nd;    // velocity dofs, dofs per node block
+  int nbf;       // boundary faces 2 (nx + ny)
+  double hx, hy;
+  const uint8_t* dirichlet;  // nbf flags (device)
+};
+
+struct TimeData {
+  int k1;
+  double tau_w[MAXK1];
+  double K_t[MAXK1 * MAXK1];
+  double m_t[MAXK1];
+};
+
+struct Disc {
+  double gamma1, gamma2, gamma_cip;
+  int viscous, convection, pressure;
+};
+
+struct Model {
+  double p, delta, nu, nu_inf;
+  int kind;  // 0 pic, 1 exn, 2 modn
+  double sigma_max;
+};
+
+// Frozen linearization (per node mu).
+struct Lin {
+  const double* eta;    // [k1][16][nc]
+  const double* gam;    // [k1][16][nc]
+  const double* etaf;   // [k1][nbf][4]
+  const double* gamf;   // [k1][nbf][4]
+  const double* etad;   // [nbf][4]  lifting viscosity (state independent)
+  const double* betad;  // [nbf][4]
+  const double* dg;     // [nbf][4][3] sym grad of the lifting
+  int has_gamma;        // 0 for Picard (gamma == 0)
+};
+
+__host__ __device__ inline int side_offset(const Geom& g, int side) {
+  // bottom, right, top, left
+  return side == 0 ? 0 : side == 1 ? g.nx : side == 2 ? g.nx + g.ny : 2 * g.nx + g.ny;
+}
+
+// (eta, gamma) of T(B) = eta B + gamma (A:B) A at squared norm a_sq.
+// constitutive.py:323-337 (gamma scaled by the clip factor of :311-320 for modn).
+__device__ inline void tangent_coeffs(const Model& m, double a_sq, double& eta, double& gam) {
+  const double dsq = m.delta * m.delta + a_sq;
+  const double mu = m.nu * pow(dsq, (m.p - 2.0) / 2.0);
+  eta = m.nu_inf + mu;
+  if (m.kind == 0) {
+    gam = 0.0;
+    return;
+  }
+  double g = (m.p - 2.0) * mu / dsq;
+  if (m.kind == 2) {
+    const double sigma = mu * sqrt(a_sq);
+    // s = min(1, sigma_max / (sigma > 0 ? sigma : inf)); NaN propagates like np.minimum.
+    const double r = m.sigma_max / (sigma > 0.0 ? sigma : __longlong_as_double(0x7ff0000000000000LL));
+    const double s = (r > 1.0) ? 1.0 : r;
+    g = s * g;
+  }
+  gam = g;
+}
+
+__device__ inline double eta_field(const Model& m, double a_sq) {
+  return m.nu_inf + m.nu * pow(m.delta * m.delta + a_sq, (m.p - 2.0) / 2.0);
+}
+
+__device__ inline double beta_field(const Model& m, double a_sq) {
+  return m.nu * (m.p - 2.0) * pow(m.delta * m.delta + a_sq, (m.p - 4.0) / 2.0);
+}
+
+}  // namespace pdst

@@ -1,0 +1,38 @@
+// pdst_internal.h — host-side launch wrappers shared by the C-ABI layer.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "pdst_device.cuh"
+
+namespace pdst {
+
+cudaError_t set_tables(const Tables& t);
+
+cudaError_t jacobian_apply(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* state,
+                           const double* x, const double* rhs, double* out, cudaStream_t st);
+
+cudaError_t slab_residual(const Geom& g, const TimeData& td, const Disc& ds, const Model& m, const Lin& L,
+                          const double* U, const double* advect, const double* vminus, const double* fqp,
+                          const double* ghat, double* out, cudaStream_t st);
+
+cudaError_t linearize(const Geom& g, const Model& m, int k1, const double* state, double* eta, double* gam,
+                      double* etaf, double* gamf, cudaStream_t st);
+
+cudaError_t lifting(const Geom& g, const Model& m, const double* ghat, double* etad, double* betad, double* dg,
+                    cudaStream_t st);
+
+// Mass-weighted slab products (newton.py:96-121): y = (tau w (x) M) x and
+// the dot <a, M b>; `partials` must hold at least reduce_partials() doubles.
+cudaError_t mass_apply(const Geom& g, const TimeData& td, const double* x, double* y, cudaStream_t st);
+int reduce_partials();
+cudaError_t mass_dot(const Geom& g, const TimeData& td, const double* a, const double* b, double* partials,
+                     double* result, cudaStream_t st);
+cudaError_t dot(const double* a, const double* b, size_t n, double* partials, double* result, cudaStream_t st);
+
+// Strip the velocity components of a slab state into a dense (k1, Mv) copy.
+cudaError_t copy_velocity_blocks(const Geom& g, int k1, const double* U, double* V, cudaStream_t st);
+// V = sum_mu c[mu] U_mu (velocity only)
+cudaError_t blend_velocity(const Geom& g, int k1, const double* coef, const double* U, double* V, cudaStream_t st);
+
+}  // namespace pdst

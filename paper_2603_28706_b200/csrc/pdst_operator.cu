@@ -1,0 +1,1001 @@
+// pdst_operator.cu — linearization, matrix-free slab Jacobian apply and slab
+// residual kernels (sm_100a, fp64).
+//
+// Kernel design:
+//   * one CTA per tile of TX x TY owned cells; the CTA also computes a halo
+//     ring of one cell to the left and below so that every node it owns
+//     receives all of its element contributions inside the CTA
+//     (owner-computes; deterministic, no atomics);
+//   * the tile's Q2 node values (all k+1 Radau nodes of the direction, the
+//     state of the current node) are staged in shared memory with a two-cell
+//     ring so that the CIP jump of every computed cell can be evaluated;
+//   * one thread per cell evaluates the cell's full contribution to its own
+//     9 nodes: volume terms by sum factorisation over the 1-D 4x3 tables,
+//     its boundary sides, the own-side half of its 4 CIP faces and the
+//     K_t (x) M_x temporal coupling (cell mass = hx hy M1 (x) M1);
+//   * contributions are combined per node from shared memory in a fixed
+//     order and written once.
+//
+// Reference: forms.py:581-652 (J x), forms.py:435-516 (residual),
+// slab.py:162-205 (slab composition), constitutive.py:323-337 (tangent).
+#include "pdst_device.cuh"
+#include "pdst_internal.h"
+
+namespace pdst {
+
+__constant__ Tables c_tab;
+
+namespace {
+
+constexpr int TX = 15;           // owned cells per tile, x
+constexpr int TY = 15;           // owned cells per tile, y
+constexpr int CX = TX + 1;       // computed cells (with left halo)
+constexpr int CY = TY + 1;
+constexpr int NT = CX * CY;      // threads per CTA
+constexpr int NC = 2 * (TX + 3) + 1;  // staged node columns
+constexpr int NR = 2 * (TY + 3) + 1;  // staged node rows
+constexpr int PLANE = NR * NC;
+
+struct Plane2 {
+  const double* p0;  // component 0
+  const double* p1;  // component 1
+  __device__ double at(int d, int r, int c) const { return (d == 0 ? p0 : p1)[r * NC + c]; }
+};
+
+// Stage one slab block's velocity into two shared planes (zero outside the domain).
+__device__ void stage_velocity(const Geom& g, const double* __restrict__ v, double* pl0, double* pl1, int X0,
+                               int Y0) {
+  for (int idx = threadIdx.x; idx < PLANE; idx += blockDim.x) {
+    const int r = idx / NC, c = idx - r * NC;
+    const int X = X0 + c, Y = Y0 + r;
+    double a = 0.0, b = 0.0;
+    if (X >= 0 && X < g.nnx && Y >= 0 && Y < g.nny) {
+      const size_t o = 2 * ((size_t)Y * g.nnx + X);
+      a = __ldg(v + o);
+      b = __ldg(v + o + 1);
+    }
+    pl0[idx] = a;
+    pl1[idx] = b;
+  }
+}
+
+// line[t][d] = sum_n coef[n] F(node (n along axis-normal, t along tangent))
+// for the 3x3 node block whose lower-left staged node is (r0, c0).
+__device__ __forceinline__ void line_sums(const Plane2& F, int r0, int c0, int axis, const double* coef,
+                                          double line[3][2]) {
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      double s = 0.0;
+#pragma unroll
+      for (int n = 0; n < 3; ++n) {
+        const double f = axis == 0 ? F.at(d, r0 + t, c0 + n) : F.at(d, r0 + n, c0 + t);
+        s = fma(coef[n], f, s);
+      }
+      line[t][d] = s;
+    }
+  }
+}
+
+__device__ __forceinline__ void side_info(int side, int& axis, int& e, double& n0, double& n1) {
+  // 0 bottom, 1 right, 2 top, 3 left
+  axis = (side == 1 || side == 3) ? 0 : 1;
+  e = (side == 1 || side == 2) ? 1 : 0;
+  n0 = side == 1 ? 1.0 : side == 3 ? -1.0 : 0.0;
+  n1 = side == 2 ? 1.0 : side == 0 ? -1.0 : 0.0;
+}
+
+// Scatter face accumulators RE (value/tangential tests) and RD (normal
+// derivative tests) to the cell's 9 nodes.
+__device__ __forceinline__ void face_scatter(int axis, int e, const double RE[3][2], const double RD[3][2],
+                                             double acc[3][3][2]) {
+#pragma unroll
+  for (int n = 0; n < 3; ++n) {
+    const double en = c_tab.E[e][n], dn = c_tab.dE[e][n];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        const double v = en * RE[t][d] + dn * RD[t][d];
+        if (axis == 0)
+          acc[t][n][d] += v;
+        else
+          acc[n][t][d] += v;
+      }
+    }
+  }
+}
+
+// Own-side half of the CIP term of one interior face of the cell
+// (forms.py:639-650); sgn = +1 for the Jacobian, -1 for the residual
+// (forms.py:415-432).  F = field whose normal-derivative jump is penalised,
+// A = lagged advective field (weights), both staged.
+__device__ void cip_side(const Geom& g, const Disc& ds, int side, const Plane2& F, const Plane2& A, int r0, int c0,
+                         double sgn, double acc[3][3][2]) {
+  int axis, e_own, dummy_e;
+  double n0, n1;
+  side_info(side, axis, dummy_e, n0, n1);
+  e_own = dummy_e;
+  const int e_nbr = 1 - e_own;
+  // neighbour block origin
+  int rn = r0, cn = c0;
+  if (side == 0) rn -= 2;
+  if (side == 2) rn += 2;
+  if (side == 1) cn += 2;
+  if (side == 3) cn -= 2;
+  const double hface = axis == 0 ? g.hy : g.hx;
+  const double hnorm = axis == 0 ? g.hx : g.hy;
+  double own[3][2], nbr[3][2], tr[3][2];
+  line_sums(F, r0, c0, axis, c_tab.dE[e_own], own);
+  line_sums(F, rn, cn, axis, c_tab.dE[e_nbr], nbr);
+  line_sums(A, r0, c0, axis, c_tab.E[e_own], tr);
+  const double coef = sgn * ds.gamma_cip * hface * hface;
+  double RD[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+  const double RE[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    double vt = 0.0, j0 = 0.0, j1 = 0.0;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const double b = c_tab.B[q][t];
+      vt = fma(b, tr[t][axis], vt);
+      j0 = fma(b, own[t][0] - nbr[t][0], j0);
+      j1 = fma(b, own[t][1] - nbr[t][1], j1);
+    }
+    const double wgt = coef * (c_tab.w[q] * hface) * fabs(vt) / (hnorm * hnorm);
+    const double c0v = wgt * j0, c1v = wgt * j1;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      RD[t][0] = fma(c0v, c_tab.B[q][t], RD[t][0]);
+      RD[t][1] = fma(c1v, c_tab.B[q][t], RD[t][1]);
+    }
+  }
+  face_scatter(axis, e_own, RE, RD, acc);
+}
+
+// Evaluate a staged field on a boundary side at face point q:
+// value u[d], gradient ux[d], uy[d].
+struct FaceLines {
+  double E[3][2], D[3][2];
+};
+
+__device__ __forceinline__ void face_point(const FaceLines& L, int axis, int q, double htan, double hnorm, double u[2],
+                                           double ux[2], double uy[2]) {
+#pragma unroll
+  for (int d = 0; d < 2; ++d) {
+    double v = 0, dt = 0, dn = 0;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      v = fma(c_tab.B[q][t], L.E[t][d], v);
+      dt = fma(c_tab.G[q][t], L.E[t][d], dt);
+      dn = fma(c_tab.B[q][t], L.D[t][d], dn);
+    }
+    u[d] = v;
+    if (axis == 0) {
+      ux[d] = dn / hnorm;
+      uy[d] = dt / htan;
+    } else {
+      ux[d] = dt / htan;
+      uy[d] = dn / hnorm;
+    }
+  }
+}
+
+// Jacobian boundary-side terms of one cell side (forms.py:605-637).
+__device__ void jac_boundary_side(const Geom& g, const Disc& ds, const Lin& L, int mu, int side, int bf,
+                                  const Plane2& X, const Plane2& S, int r0, int c0, const double P[3],
+                                  double acc[3][3][2], double accp[3]) {
+  int axis, e;
+  double n0, n1;
+  side_info(side, axis, e, n0, n1);
+  const double htan = axis == 0 ? g.hy : g.hx;
+  const double hnorm = axis == 0 ? g.hx : g.hy;
+  FaceLines LU, LV;
+  line_sums(X, r0, c0, axis, c_tab.E[e], LU.E);
+  line_sums(X, r0, c0, axis, c_tab.dE[e], LU.D);
+  line_sums(S, r0, c0, axis, c_tab.E[e], LV.E);
+  line_sums(S, r0, c0, axis, c_tab.dE[e], LV.D);
+  const bool dm = g.dirichlet[bf] != 0;
+  double RE[3][2] = {{0, 0}, {0, 0}, {0, 0}}, RD[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+  for (int q = 0; q < 4; ++q) {
+    const double wq = c_tab.w[q] * htan;
+    double u[2], ux[2], uy[2], v[2], vx[2], vy[2];
+    face_point(LU, axis, q, htan, hnorm, u, ux, uy);
+    face_point(LV, axis, q, htan, hnorm, v, vx, vy);
+    const double vn = v[0] * n0 + v[1] * n1;
+    const double un = u[0] * n0 + u[1] * n1;
+    double Cv[2] = {0, 0}, Cgx[2] = {0, 0}, Cgy[2] = {0, 0};
+    if (ds.convection) {
+      Cv[0] += vn * u[0] + un * v[0];
+      Cv[1] += vn * u[1] + un * v[1];
+    }
+    if (dm) {
+      if (ds.viscous) {
+        const double a0 = vx[0], a1 = vy[1], a2 = 0.5 * (vy[0] + vx[1]);
+        const double b0 = ux[0], b1 = uy[1], b2 = 0.5 * (uy[0] + ux[1]);
+        const size_t fi = ((size_t)mu * g.nbf + bf) * 4 + q;
+        const double ef = L.etaf[fi];
+        const double gf = L.has_gamma ? L.gamf[fi] : 0.0;
+        const double ab = a0 * b0 + a1 * b1 + 2.0 * a2 * b2;
+        const double t0 = ef * b0 + gf * ab * a0, t1 = ef * b1 + gf * ab * a1, t2 = ef * b2 + gf * ab * a2;
+        Cv[0] -= t0 * n0 + t2 * n1;
+        Cv[1] -= t2 * n0 + t1 * n1;
+        const size_t li = (size_t)bf * 4 + q;
+        const double ed = L.etad[li], bd = L.betad[li];
+        const double g0 = L.dg[li * 3 + 0], g1 = L.dg[li * 3 + 1], g2 = L.dg[li * 3 + 2];
+        const double dgn0 = g0 * n0 + g2 * n1, dgn1 = g2 * n0 + g1 * n1;
+        const double dgnu = dgn0 * u[0] + dgn1 * u[1];
+        Cgx[0] -= 0.5 * ed * (n0 * u[0] + u[0] * n0) + bd * dgnu * g0;
+        Cgx[1] -= 0.5 * ed * (n0 * u[1] + u[0] * n1) + bd * dgnu * g2;
+        Cgy[0] -= 0.5 * ed * (n1 * u[0] + u[1] * n0) + bd * dgnu * g2;
+        Cgy[1] -= 0.5 * ed * (n1 * u[1] + u[1] * n1) + bd * dgnu * g1;
+        const double p1 = ds.gamma1 / htan * ed, p2 = ds.gamma2 / htan * un;
+        Cv[0] += p1 * u[0] + p2 * n0;
+        Cv[1] += p1 * u[1] + p2 * n1;
+      }
+      if (ds.convection) {
+        const double wneg = 0.5 * (fabs(vn) - vn);
+        Cv[0] -= wneg * u[0];
+        Cv[1] -= wneg * u[1];
+      }
+      if (ds.pressure) {
+        const double xh = axis == 0 ? (double)e : c_tab.s[q];
+        const double yh = axis == 0 ? c_tab.s[q] : (double)e;
+        const double dp = P[0] + P[1] * (xh - 0.5) + P[2] * (yh - 0.5);
+        Cv[0] += dp * n0;
+        Cv[1] += dp * n1;
+        accp[0] += wq * un;
+        accp[1] += wq * un * (xh - 0.5);
+        accp[2] += wq * un * (yh - 0.5);
+      }
+    }
+    const double* Ct = axis == 0 ? Cgy : Cgx;
+    const double* Cn = axis == 0 ? Cgx : Cgy;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        RE[t][d] += wq * (Cv[d] * c_tab.B[q][t] + Ct[d] * c_tab.G[q][t] / htan);
+        RD[t][d] += wq * (Cn[d] * c_tab.B[q][t] / hnorm);
+      }
+    }
+  }
+  face_scatter(axis, e, RE, RD, acc);
+}
+
+// Residual boundary-side terms (forms.py:474-507) plus, when a lifting is
+// present, the Nitsche vector B_gamma(g_hat, .) of forms.py:374-412.
+__device__ void res_boundary_side(const Geom& g, const Disc& ds, const Model& m, const Lin& L, int side, int bf,
+                                  const Plane2& S, const Plane2& A, int r0, int c0, const double PI[3],
+                                  const double* ghat_nodes /*9x2 or null*/, double acc[3][3][2], double accp[3]) {
+  int axis, e;
+  double n0, n1;
+  side_info(side, axis, e, n0, n1);
+  const double htan = axis == 0 ? g.hy : g.hx;
+  const double hnorm = axis == 0 ? g.hx : g.hy;
+  FaceLines LV, LA;
+  line_sums(S, r0, c0, axis, c_tab.E[e], LV.E);
+  line_sums(S, r0, c0, axis, c_tab.dE[e], LV.D);
+  line_sums(A, r0, c0, axis, c_tab.E[e], LA.E);
+  line_sums(A, r0, c0, axis, c_tab.dE[e], LA.D);
+  double GE[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+  if (ghat_nodes) {
+#pragma unroll
+    for (int t = 0; t < 3; ++t)
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        double s = 0.0;
+#pragma unroll
+        for (int n = 0; n < 3; ++n) {
+          const int a = axis == 0 ? 3 * t + n : 3 * n + t;
+          s = fma(c_tab.E[e][n], ghat_nodes[2 * a + d], s);
+        }
+        GE[t][d] = s;
+      }
+  }
+  const bool dm = g.dirichlet[bf] != 0;
+  double RE[3][2] = {{0, 0}, {0, 0}, {0, 0}}, RD[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+  for (int q = 0; q < 4; ++q) {
+    const double wq = c_tab.w[q] * htan;
+    double v[2], vx[2], vy[2], a[2], ax_[2], ay_[2];
+    face_point(LV, axis, q, htan, hnorm, v, vx, vy);
+    face_point(LA, axis, q, htan, hnorm, a, ax_, ay_);
+    const double vn = v[0] * n0 + v[1] * n1;
+    double Cv[2] = {0, 0}, Cgx[2] = {0, 0}, Cgy[2] = {0, 0};
+    if (ds.convection) {
+      Cv[0] -= vn * v[0];
+      Cv[1] -= vn * v[1];
+    }
+    if (dm) {
+      const size_t li = (size_t)bf * 4 + q;
+      const double ed = L.etad[li], bd = L.betad[li];
+      const double g0 = L.dg[li * 3 + 0], g1 = L.dg[li * 3 + 1], g2 = L.dg[li * 3 + 2];
+      const double dgn0 = g0 * n0 + g2 * n1, dgn1 = g2 * n0 + g1 * n1;
+      if (ds.viscous) {
+        const double a0 = vx[0], a1 = vy[1], a2 = 0.5 * (vy[0] + vx[1]);
+        const double ef = eta_field(m, a0 * a0 + a1 * a1 + 2.0 * a2 * a2);
+        Cv[0] += ef * (a0 * n0 + a2 * n1);
+        Cv[1] += ef * (a2 * n0 + a1 * n1);
+        const double dgnv = dgn0 * v[0] + dgn1 * v[1];
+        Cgx[0] += 0.5 * ed * (n0 * v[0] + v[0] * n0) + bd * dgnv * g0;
+        Cgx[1] += 0.5 * ed * (n0 * v[1] + v[0] * n1) + bd * dgnv * g2;
+        Cgy[0] += 0.5 * ed * (n1 * v[0] + v[1] * n0) + bd * dgnv * g2;
+        Cgy[1] += 0.5 * ed * (n1 * v[1] + v[1] * n1) + bd * dgnv * g1;
+        const double p1 = ds.gamma1 / htan * ed, p2 = ds.gamma2 / htan * vn;
+        Cv[0] -= p1 * v[0] + p2 * n0;
+        Cv[1] -= p1 * v[1] + p2 * n1;
+      }
+      const double xh = axis == 0 ? (double)e : c_tab.s[q];
+      const double yh = axis == 0 ? c_tab.s[q] : (double)e;
+      if (ds.convection) {
+        const double an = a[0] * n0 + a[1] * n1;
+        const double aneg = 0.5 * (fabs(an) - an);
+        Cv[0] += aneg * v[0];
+        Cv[1] += aneg * v[1];
+      }
+      if (ds.pressure) {
+        const double pf = PI[0] + PI[1] * (xh - 0.5) + PI[2] * (yh - 0.5);
+        Cv[0] -= pf * n0;
+        Cv[1] -= pf * n1;
+        accp[0] -= wq * vn;
+        accp[1] -= wq * vn * (xh - 0.5);
+        accp[2] -= wq * vn * (yh - 0.5);
+      }
+      if (ghat_nodes) {
+        double gv[2];
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+          double s = 0.0;
+#pragma unroll
+          for (int t = 0; t < 3; ++t) s = fma(c_tab.B[q][t], GE[t][d], s);
+          gv[d] = s;
+        }
+        const double gn = gv[0] * n0 + gv[1] * n1;
+        if (ds.viscous) {
+          const double dgng = dgn0 * gv[0] + dgn1 * gv[1];
+          Cgx[0] -= 0.5 * ed * (n0 * gv[0] + gv[0] * n0) + bd * dgng * g0;
+          Cgx[1] -= 0.5 * ed * (n0 * gv[1] + gv[0] * n1) + bd * dgng * g2;
+          Cgy[0] -= 0.5 * ed * (n1 * gv[0] + gv[1] * n0) + bd * dgng * g2;
+          Cgy[1] -= 0.5 * ed * (n1 * gv[1] + gv[1] * n1) + bd * dgng * g1;
+          const double p1 = ds.gamma1 / htan * ed, p2 = ds.gamma2 / htan * gn;
+          Cv[0] += p1 * gv[0] + p2 * n0;
+          Cv[1] += p1 * gv[1] + p2 * n1;
+        }
+        if (ds.convection) {
+          const double gneg = 0.5 * (fabs(gn) - gn);
+          Cv[0] -= gneg * gv[0];
+          Cv[1] -= gneg * gv[1];
+        }
+        if (ds.pressure) {
+          accp[0] += wq * gn;
+          accp[1] += wq * gn * (xh - 0.5);
+          accp[2] += wq * gn * (yh - 0.5);
+        }
+      }
+    }
+    const double* Ct = axis == 0 ? Cgy : Cgx;
+    const double* Cn = axis == 0 ? Cgx : Cgy;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        RE[t][d] += wq * (Cv[d] * c_tab.B[q][t] + Ct[d] * c_tab.G[q][t] / htan);
+        RD[t][d] += wq * (Cn[d] * c_tab.B[q][t] / hnorm);
+      }
+    }
+  }
+  face_scatter(axis, e, RE, RD, acc);
+}
+
+// Stage-1 sums along x for one Q2 row jy at Gauss column qx.
+__device__ __forceinline__ void row_sums(const Plane2& F, int r, int c0, int qx, double sB[2], double sG[2]) {
+#pragma unroll
+  for (int d = 0; d < 2; ++d) {
+    const double f0 = F.at(d, r, c0), f1 = F.at(d, r, c0 + 1), f2 = F.at(d, r, c0 + 2);
+    sB[d] = c_tab.B[qx][0] * f0 + c_tab.B[qx][1] * f1 + c_tab.B[qx][2] * f2;
+    sG[d] = c_tab.G[qx][0] * f0 + c_tab.G[qx][1] * f1 + c_tab.G[qx][2] * f2;
+  }
+}
+
+// acc += s * (M1 (x) M1) XT for the cell, XT = sum_nu K_t[mu,nu] F_nu - mfac * Fm.
+template <int K1>
+__device__ __forceinline__ void add_mass(const Plane2* F, const Plane2* Fm, double mfac, const double* Krow, int r0,
+                                         int c0, double s, double acc[3][3][2]) {
+#pragma unroll
+  for (int jj = 0; jj < 3; ++jj) {  // source row jy'
+    double T1[3][2];
+    double xt[3][2];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        double v = 0.0;
+#pragma unroll
+        for (int nu = 0; nu < K1; ++nu) v = fma(Krow[nu], F[nu].at(d, r0 + jj, c0 + i), v);
+        if (Fm) v -= mfac * Fm->at(d, r0 + jj, c0 + i);
+        xt[i][d] = v;
+      }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int d = 0; d < 2; ++d)
+        T1[i][d] = c_tab.M1[i][0] * xt[0][d] + c_tab.M1[i][1] * xt[1][d] + c_tab.M1[i][2] * xt[2][d];
+#pragma unroll
+    for (int jy = 0; jy < 3; ++jy) {
+      const double m = s * c_tab.M1[jy][jj];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int d = 0; d < 2; ++d) acc[jy][i][d] = fma(m, T1[i][d], acc[jy][i][d]);
+    }
+  }
+}
+
+// Node assembly from per-cell shared slots and the final write.
+__device__ void assemble_and_store(const Geom& g, const double* sacc, int i0, int j0, int mu,
+                                   const double* __restrict__ rhs, double* __restrict__ out) {
+  const bool lastx = (i0 + TX >= g.nx), lasty = (j0 + TY >= g.ny);
+  const int lxe = lastx ? 2 * (g.nx - (i0 - 1)) + 1 : 2 * TX + 2;  // exclusive local node bound
+  const int lye = lasty ? 2 * (g.ny - (j0 - 1)) + 1 : 2 * TY + 2;
+  const int wx = lxe - 2, wy = lye - 2;  // owned local nodes start at 2
+  const int n = wx * wy;
+  const size_t base = (size_t)mu * g.nd;
+  for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+    const int ly = 2 + idx / wx, lx = 2 + idx % wx;
+    double s0 = 0.0, s1 = 0.0;
+    const int cxa = (lx & 1) ? (lx - 1) / 2 : lx / 2 - 1;
+    const int cxb = lx / 2;
+    const int cya = (ly & 1) ? (ly - 1) / 2 : ly / 2 - 1;
+    const int cyb = ly / 2;
+    for (int cy = cya; cy <= cyb; ++cy) {
+      if (cy < 0 || cy >= CY) continue;
+      for (int cx = cxa; cx <= cxb; ++cx) {
+        if (cx < 0 || cx >= CX) continue;
+        const int a = 3 * (ly - 2 * cy) + (lx - 2 * cx);
+        const double* slot = sacc + (cy * CX + cx) * 18 + 2 * a;
+        s0 += slot[0];
+        s1 += slot[1];
+      }
+    }
+    const int X = 2 * (i0 - 1) + lx, Y = 2 * (j0 - 1) + ly;
+    const size_t o = base + 2 * ((size_t)Y * g.nnx + X);
+    if (rhs) {
+      s0 = rhs[o] - s0;
+      s1 = rhs[o + 1] - s1;
+    }
+    out[o] = s0;
+    out[o + 1] = s1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Slab Jacobian apply: out = J x  (or rhs - J x when rhs != null)
+// ---------------------------------------------------------------------------
+template <int K1>
+__global__ void __launch_bounds__(NT) k_jacobian(Geom g, TimeData td, Disc ds, Lin L, const double* __restrict__ state,
+                                                 const double* __restrict__ x, const double* __restrict__ rhs,
+                                                 double* __restrict__ out) {
+  extern __shared__ double smem[];
+  double* xs = smem;                       // [K1][2][PLANE]
+  double* ss = xs + (size_t)K1 * 2 * PLANE;  // [2][PLANE]
+  double* sacc = ss + 2 * PLANE;           // [NT][18]
+  const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
+  const int X0 = 2 * (i0 - 2), Y0 = 2 * (j0 - 2);
+  for (int nu = 0; nu < K1; ++nu)
+    stage_velocity(g, x + (size_t)nu * g.nd, xs + (size_t)nu * 2 * PLANE, xs + (size_t)nu * 2 * PLANE + PLANE, X0,
+                   Y0);
+  Plane2 XP[K1];
+#pragma unroll
+  for (int nu = 0; nu < K1; ++nu) XP[nu] = Plane2{xs + nu * 2 * PLANE, xs + nu * 2 * PLANE + PLANE};
+  const Plane2 SP{ss, ss + PLANE};
+
+  const int tx = threadIdx.x % CX, ty = threadIdx.x / CX;
+  const int ci = i0 - 1 + tx, cj = j0 - 1 + ty;
+  const bool valid = ci >= 0 && ci < g.nx && cj >= 0 && cj < g.ny;
+  const bool owned = valid && tx >= 1 && ty >= 1;
+  const int c = cj * g.nx + ci;
+  const int r0 = 2 + 2 * ty, c0 = 2 + 2 * tx;  // staged origin of the cell's nodes
+  const double W = g.hx * g.hy;
+
+  for (int mu = 0; mu < K1; ++mu) {
+    stage_velocity(g, state + (size_t)mu * g.mv, ss, ss + PLANE, X0, Y0);
+    __syncthreads();
+    double acc[3][3][2];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    double accp[3] = {0.0, 0.0, 0.0};
+    if (valid) {
+      const Plane2& XM = XP[mu];
+      double P[3];
+      const double* xp = x + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
+      P[0] = __ldg(xp);
+      P[1] = __ldg(xp + 1);
+      P[2] = __ldg(xp + 2);
+      // ---- volume (forms.py:589-603) ----
+#pragma unroll 1
+      for (int qx = 0; qx < 4; ++qx) {
+        double xB[3][2], xG[3][2], sB[3][2], sG[3][2];
+#pragma unroll
+        for (int jy = 0; jy < 3; ++jy) {
+          row_sums(XM, r0 + jy, c0, qx, xB[jy], xG[jy]);
+          row_sums(SP, r0 + jy, c0, qx, sB[jy], sG[jy]);
+        }
+        double Pa[3][2] = {{0, 0}, {0, 0}, {0, 0}}, Qa[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+        const double xh = c_tab.s[qx] - 0.5;
+#pragma unroll
+        for (int qy = 0; qy < 4; ++qy) {
+          double u[2], ux[2], uy[2], v[2], vx[2], vy[2];
+#pragma unroll
+          for (int d = 0; d < 2; ++d) {
+            u[d] = c_tab.B[qy][0] * xB[0][d] + c_tab.B[qy][1] * xB[1][d] + c_tab.B[qy][2] * xB[2][d];
+            ux[d] = (c_tab.B[qy][0] * xG[0][d] + c_tab.B[qy][1] * xG[1][d] + c_tab.B[qy][2] * xG[2][d]) / g.hx;
+            uy[d] = (c_tab.G[qy][0] * xB[0][d] + c_tab.G[qy][1] * xB[1][d] + c_tab.G[qy][2] * xB[2][d]) / g.hy;
+            v[d] = c_tab.B[qy][0] * sB[0][d] + c_tab.B[qy][1] * sB[1][d] + c_tab.B[qy][2] * sB[2][d];
+            vx[d] = (c_tab.B[qy][0] * sG[0][d] + c_tab.B[qy][1] * sG[1][d] + c_tab.B[qy][2] * sG[2][d]) / g.hx;
+            vy[d] = (c_tab.G[qy][0] * sB[0][d] + c_tab.G[qy][1] * sB[1][d] + c_tab.G[qy][2] * sB[2][d]) / g.hy;
+          }
+          const int q = 4 * qx + qy;
+          const double wq = c_tab.w[qx] * c_tab.w[qy] * W;
+          double Fx0 = 0, Fx1 = 0, Fy0 = 0, Fy1 = 0;
+          if (ds.viscous) {
+            const size_t ci_ = ((size_t)mu * 16 + q) * g.ncells + c;
+            const double eta = __ldg(L.eta + ci_);
+            const double gam = L.has_gamma ? __ldg(L.gam + ci_) : 0.0;
+            const double a0 = vx[0], a1 = vy[1], a2 = 0.5 * (vy[0] + vx[1]);
+            const double b0 = ux[0], b1 = uy[1], b2 = 0.5 * (uy[0] + ux[1]);
+            const double ab = a0 * b0 + a1 * b1 + 2.0 * a2 * b2;
+            Fx0 = eta * b0 + gam * ab * a0;
+            Fy1 = eta * b1 + gam * ab * a1;
+            Fx1 = Fy0 = eta * b2 + gam * ab * a2;
+          }
+          if (ds.convection) {
+            Fx0 -= u[0] * v[0] + v[0] * u[0];
+            Fx1 -= u[1] * v[0] + v[1] * u[0];
+            Fy0 -= u[0] * v[1] + v[0] * u[1];
+            Fy1 -= u[1] * v[1] + v[1] * u[1];
+          }
+          if (ds.pressure) {
+            const double yh = c_tab.s[qy] - 0.5;
+            const double dp = P[0] + P[1] * xh + P[2] * yh;
+            Fx0 -= dp;
+            Fy1 -= dp;
+            const double dv = wq * (ux[0] + uy[1]);
+            accp[0] -= dv;
+            accp[1] -= dv * xh;
+            accp[2] -= dv * yh;
+          }
+#pragma unroll
+          for (int jy = 0; jy < 3; ++jy) {
+            Pa[jy][0] = fma(wq * Fx0, c_tab.B[qy][jy], Pa[jy][0]);
+            Pa[jy][1] = fma(wq * Fx1, c_tab.B[qy][jy], Pa[jy][1]);
+            Qa[jy][0] = fma(wq * Fy0, c_tab.G[qy][jy], Qa[jy][0]);
+            Qa[jy][1] = fma(wq * Fy1, c_tab.G[qy][jy], Qa[jy][1]);
+          }
+        }
+#pragma unroll
+        for (int jy = 0; jy < 3; ++jy)
+#pragma unroll
+          for (int ix = 0; ix < 3; ++ix)
+#pragma unroll
+            for (int d = 0; d < 2; ++d)
+              acc[jy][ix][d] += c_tab.G[qx][ix] / g.hx * Pa[jy][d] + c_tab.B[qx][ix] / g.hy * Qa[jy][d];
+      }
+      // ---- boundary sides (forms.py:605-637) ----
+      if (ci == 0 || cj == 0 || ci == g.nx - 1 || cj == g.ny - 1) {
+        if (cj == 0) jac_boundary_side(g, ds, L, mu, 0, side_offset(g, 0) + ci, XM, SP, r0, c0, P, acc, accp);
+        if (ci == g.nx - 1) jac_boundary_side(g, ds, L, mu, 1, side_offset(g, 1) + cj, XM, SP, r0, c0, P, acc, accp);
+        if (cj == g.ny - 1) jac_boundary_side(g, ds, L, mu, 2, side_offset(g, 2) + ci, XM, SP, r0, c0, P, acc, accp);
+        if (ci == 0) jac_boundary_side(g, ds, L, mu, 3, side_offset(g, 3) + cj, XM, SP, r0, c0, P, acc, accp);
+      }
+      // ---- CIP own sides (forms.py:639-650) ----
+      if (ds.convection && ds.gamma_cip > 0.0) {
+        if (cj > 0) cip_side(g, ds, 0, XM, SP, r0, c0, 1.0, acc);
+        if (ci < g.nx - 1) cip_side(g, ds, 1, XM, SP, r0, c0, 1.0, acc);
+        if (cj < g.ny - 1) cip_side(g, ds, 2, XM, SP, r0, c0, 1.0, acc);
+        if (ci > 0) cip_side(g, ds, 3, XM, SP, r0, c0, 1.0, acc);
+      }
+      // ---- slab composition (slab.py:197-200) ----
+      const double tw = td.tau_w[mu];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          acc[a][b][0] *= tw;
+          acc[a][b][1] *= tw;
+        }
+      add_mass<K1>(XP, nullptr, 0.0, td.K_t + mu * K1, r0, c0, W, acc);
+      if (owned) {
+        const size_t o = (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const double val = tw * accp[j];
+          out[o + j] = rhs ? rhs[o + j] - val : val;
+        }
+      }
+    }
+    double* slot = sacc + threadIdx.x * 18;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        slot[2 * (3 * a + b)] = acc[a][b][0];
+        slot[2 * (3 * a + b) + 1] = acc[a][b][1];
+      }
+    __syncthreads();
+    assemble_and_store(g, sacc, i0, j0, mu, rhs, out);
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Slab residual: R = tau w F(U) - [(K_t x M)V - (m_t x M) v_minus; 0]
+// ---------------------------------------------------------------------------
+template <int K1>
+__global__ void __launch_bounds__(NT) k_residual(Geom g, TimeData td, Disc ds, Model m, Lin L,
+                                                 const double* __restrict__ U, const double* __restrict__ advect,
+                                                 const double* __restrict__ vminus, const double* __restrict__ fqp,
+                                                 const double* __restrict__ ghat, double* __restrict__ out) {
+  extern __shared__ double smem[];
+  double* us = smem;                          // [K1][2][PLANE] state velocities
+  double* vm = us + (size_t)K1 * 2 * PLANE;   // [2][PLANE] v_minus
+  double* as = vm + 2 * PLANE;                // [2][PLANE] advect (if given)
+  double* sacc = as + 2 * PLANE;              // [NT][18]
+  const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
+  const int X0 = 2 * (i0 - 2), Y0 = 2 * (j0 - 2);
+  for (int nu = 0; nu < K1; ++nu)
+    stage_velocity(g, U + (size_t)nu * g.nd, us + (size_t)nu * 2 * PLANE, us + (size_t)nu * 2 * PLANE + PLANE, X0,
+                   Y0);
+  stage_velocity(g, vminus, vm, vm + PLANE, X0, Y0);
+  Plane2 UP[K1];
+#pragma unroll
+  for (int nu = 0; nu < K1; ++nu) UP[nu] = Plane2{us + nu * 2 * PLANE, us + nu * 2 * PLANE + PLANE};
+  const Plane2 VM{vm, vm + PLANE};
+  const Plane2 AP{as, as + PLANE};
+
+  const int tx = threadIdx.x % CX, ty = threadIdx.x / CX;
+  const int ci = i0 - 1 + tx, cj = j0 - 1 + ty;
+  const bool valid = ci >= 0 && ci < g.nx && cj >= 0 && cj < g.ny;
+  const bool owned = valid && tx >= 1 && ty >= 1;
+  const int c = cj * g.nx + ci;
+  const int r0 = 2 + 2 * ty, c0 = 2 + 2 * tx;
+  const double W = g.hx * g.hy;
+
+  for (int mu = 0; mu < K1; ++mu) {
+    if (advect) stage_velocity(g, advect + (size_t)mu * g.nd, as, as + PLANE, X0, Y0);
+    __syncthreads();
+    const Plane2& SP = UP[mu];
+    const Plane2& AW = advect ? AP : UP[mu];
+    double acc[3][3][2];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    double accp[3] = {0.0, 0.0, 0.0};
+    if (valid) {
+      double PI[3];
+      const double* pp = U + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
+      PI[0] = __ldg(pp);
+      PI[1] = __ldg(pp + 1);
+      PI[2] = __ldg(pp + 2);
+#pragma unroll 1
+      for (int qx = 0; qx < 4; ++qx) {
+        double sB[3][2], sG[3][2];
+#pragma unroll
+        for (int jy = 0; jy < 3; ++jy) row_sums(SP, r0 + jy, c0, qx, sB[jy], sG[jy]);
+        double Pa[3][2] = {{0, 0}, {0, 0}, {0, 0}}, Qa[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+        const double xh = c_tab.s[qx] - 0.5;
+#pragma unroll
+        for (int qy = 0; qy < 4; ++qy) {
+          double v[2], vx[2], vy[2];
+#pragma unroll
+          for (int d = 0; d < 2; ++d) {
+            v[d] = c_tab.B[qy][0] * sB[0][d] + c_tab.B[qy][1] * sB[1][d] + c_tab.B[qy][2] * sB[2][d];
+            vx[d] = (c_tab.B[qy][0] * sG[0][d] + c_tab.B[qy][1] * sG[1][d] + c_tab.B[qy][2] * sG[2][d]) / g.hx;
+            vy[d] = (c_tab.G[qy][0] * sB[0][d] + c_tab.G[qy][1] * sB[1][d] + c_tab.G[qy][2] * sB[2][d]) / g.hy;
+          }
+          const int q = 4 * qx + qy;
+          const double wq = c_tab.w[qx] * c_tab.w[qy] * W;
+          double Fx0 = 0, Fx1 = 0, Fy0 = 0, Fy1 = 0, Fv0 = 0, Fv1 = 0;
+          if (fqp) {
+            const size_t fi = (((size_t)mu * g.ncells + c) * 16 + q) * 2;
+            Fv0 = __ldg(fqp + fi);
+            Fv1 = __ldg(fqp + fi + 1);
+          }
+          if (ds.viscous) {
+            const double a0 = vx[0], a1 = vy[1], a2 = 0.5 * (vy[0] + vx[1]);
+            const double eta = eta_field(m, a0 * a0 + a1 * a1 + 2.0 * a2 * a2);
+            Fx0 -= eta * a0;
+            Fy1 -= eta * a1;
+            Fx1 -= eta * a2;
+            Fy0 -= eta * a2;
+          }
+          if (ds.convection) {
+            Fx0 += v[0] * v[0];
+            Fx1 += v[1] * v[0];
+            Fy0 += v[0] * v[1];
+            Fy1 += v[1] * v[1];
+          }
+          if (ds.pressure) {
+            const double yh = c_tab.s[qy] - 0.5;
+            const double pq = PI[0] + PI[1] * xh + PI[2] * yh;
+            Fx0 += pq;
+            Fy1 += pq;
+            const double dv = wq * (vx[0] + vy[1]);
+            accp[0] += dv;
+            accp[1] += dv * xh;
+            accp[2] += dv * yh;
+          }
+#pragma unroll
+          for (int jy = 0; jy < 3; ++jy) {
+            Pa[jy][0] = fma(wq * Fx0, c_tab.B[qy][jy], Pa[jy][0]);
+            Pa[jy][1] = fma(wq * Fx1, c_tab.B[qy][jy], Pa[jy][1]);
+            Qa[jy][0] = fma(wq * Fy0, c_tab.G[qy][jy] / g.hy, fma(wq * Fv0, c_tab.B[qy][jy], Qa[jy][0]));
+            Qa[jy][1] = fma(wq * Fy1, c_tab.G[qy][jy] / g.hy, fma(wq * Fv1, c_tab.B[qy][jy], Qa[jy][1]));
+          }
+        }
+#pragma unroll
+        for (int jy = 0; jy < 3; ++jy)
+#pragma unroll
+          for (int ix = 0; ix < 3; ++ix)
+#pragma unroll
+            for (int d = 0; d < 2; ++d)
+              acc[jy][ix][d] += c_tab.G[qx][ix] / g.hx * Pa[jy][d] + c_tab.B[qx][ix] * Qa[jy][d];
+      }
+      if (ci == 0 || cj == 0 || ci == g.nx - 1 || cj == g.ny - 1) {
+        double gn[18];
+        const double* gp = nullptr;
+        if (ghat) {
+#pragma unroll
+          for (int a = 0; a < 9; ++a) {
+            const size_t node = (size_t)(2 * cj + a / 3) * g.nnx + 2 * ci + a % 3;
+            gn[2 * a] = ghat[2 * node];
+            gn[2 * a + 1] = ghat[2 * node + 1];
+          }
+          gp = gn;
+        }
+        if (cj == 0) res_boundary_side(g, ds, m, L, 0, side_offset(g, 0) + ci, SP, AW, r0, c0, PI, gp, acc, accp);
+        if (ci == g.nx - 1)
+          res_boundary_side(g, ds, m, L, 1, side_offset(g, 1) + cj, SP, AW, r0, c0, PI, gp, acc, accp);
+        if (cj == g.ny - 1)
+          res_boundary_side(g, ds, m, L, 2, side_offset(g, 2) + ci, SP, AW, r0, c0, PI, gp, acc, accp);
+        if (ci == 0) res_boundary_side(g, ds, m, L, 3, side_offset(g, 3) + cj, SP, AW, r0, c0, PI, gp, acc, accp);
+      }
+      if (ds.convection && ds.gamma_cip > 0.0) {
+        if (cj > 0) cip_side(g, ds, 0, SP, AW, r0, c0, -1.0, acc);
+        if (ci < g.nx - 1) cip_side(g, ds, 1, SP, AW, r0, c0, -1.0, acc);
+        if (cj < g.ny - 1) cip_side(g, ds, 2, SP, AW, r0, c0, -1.0, acc);
+        if (ci > 0) cip_side(g, ds, 3, SP, AW, r0, c0, -1.0, acc);
+      }
+      const double tw = td.tau_w[mu];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          acc[a][b][0] *= tw;
+          acc[a][b][1] *= tw;
+        }
+      add_mass<K1>(UP, &VM, td.m_t[mu], td.K_t + mu * K1, r0, c0, -W, acc);
+      if (owned) {
+        const size_t o = (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) out[o + j] = tw * accp[j];
+      }
+    }
+    double* slot = sacc + threadIdx.x * 18;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        slot[2 * (3 * a + b)] = acc[a][b][0];
+        slot[2 * (3 * a + b) + 1] = acc[a][b][1];
+      }
+    __syncthreads();
+    assemble_and_store(g, sacc, i0, j0, mu, nullptr, out);
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Linearization caches (forms.py:544-571): per cell qp (eta, gamma), per
+// boundary face qp (eta_f, gamma_f), lifting coefficients (eta_d, beta_d, Dg).
+// ---------------------------------------------------------------------------
+__global__ void k_linearize_cells(Geom g, Model m, int k1, const double* __restrict__ state, double* __restrict__ eta,
+                                  double* __restrict__ gam) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int mu = blockIdx.y;
+  if (c >= g.ncells || mu >= k1) return;
+  const int ci = c % g.nx, cj = c / g.nx;
+  const double* sv = state + (size_t)mu * g.mv;
+  double S[3][3][2];
+#pragma unroll
+  for (int jy = 0; jy < 3; ++jy)
+#pragma unroll
+    for (int ix = 0; ix < 3; ++ix) {
+      const size_t node = (size_t)(2 * cj + jy) * g.nnx + 2 * ci + ix;
+      const double2 v = __ldg(reinterpret_cast<const double2*>(sv) + node);
+      S[jy][ix][0] = v.x;
+      S[jy][ix][1] = v.y;
+    }
+  for (int qx = 0; qx < 4; ++qx) {
+    double sB[3][2], sG[3][2];
+#pragma unroll
+    for (int jy = 0; jy < 3; ++jy)
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        sB[jy][d] = c_tab.B[qx][0] * S[jy][0][d] + c_tab.B[qx][1] * S[jy][1][d] + c_tab.B[qx][2] * S[jy][2][d];
+        sG[jy][d] = c_tab.G[qx][0] * S[jy][0][d] + c_tab.G[qx][1] * S[jy][1][d] + c_tab.G[qx][2] * S[jy][2][d];
+      }
+    for (int qy = 0; qy < 4; ++qy) {
+      double vx[2], vy[2];
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        vx[d] = (c_tab.B[qy][0] * sG[0][d] + c_tab.B[qy][1] * sG[1][d] + c_tab.B[qy][2] * sG[2][d]) / g.hx;
+        vy[d] = (c_tab.G[qy][0] * sB[0][d] + c_tab.G[qy][1] * sB[1][d] + c_tab.G[qy][2] * sB[2][d]) / g.hy;
+      }
+      const double a0 = vx[0], a1 = vy[1], a2 = 0.5 * (vy[0] + vx[1]);
+      double e, gm;
+      tangent_coeffs(m, a0 * a0 + a1 * a1 + 2.0 * a2 * a2, e, gm);
+      const size_t o = ((size_t)mu * 16 + 4 * qx + qy) * g.ncells + c;
+      eta[o] = e;
+      gam[o] = gm;
+    }
+  }
+}
+
+// Sym gradient of a nodal field on boundary face bf at face point q.
+__device__ void face_symgrad(const Geom& g, const double* __restrict__ v, int bf, int q, double& a0, double& a1,
+                             double& a2) {
+  int side = 0;
+  while (side < 3 && bf >= side_offset(g, side + 1)) ++side;
+  const int f = bf - side_offset(g, side);
+  int ci, cj;
+  if (side == 0) { ci = f; cj = 0; }
+  else if (side == 1) { ci = g.nx - 1; cj = f; }
+  else if (side == 2) { ci = f; cj = g.ny - 1; }
+  else { ci = 0; cj = f; }
+  const int axis = (side == 1 || side == 3) ? 0 : 1;
+  const int e = (side == 1 || side == 2) ? 1 : 0;
+  const double htan = axis == 0 ? g.hy : g.hx, hnorm = axis == 0 ? g.hx : g.hy;
+  double ux[2], uy[2];
+  for (int d = 0; d < 2; ++d) {
+    double dt = 0.0, dn = 0.0;
+    for (int t = 0; t < 3; ++t) {
+      double le = 0.0, ld = 0.0;
+      for (int n = 0; n < 3; ++n) {
+        const int jy = axis == 0 ? t : n, ix = axis == 0 ? n : t;
+        const double val = v[2 * ((size_t)(2 * cj + jy) * g.nnx + 2 * ci + ix) + d];
+        le = fma(c_tab.E[e][n], val, le);
+        ld = fma(c_tab.dE[e][n], val, ld);
+      }
+      dt = fma(c_tab.G[q][t], le, dt);
+      dn = fma(c_tab.B[q][t], ld, dn);
+    }
+    if (axis == 0) {
+      ux[d] = dn / hnorm;
+      uy[d] = dt / htan;
+    } else {
+      ux[d] = dt / htan;
+      uy[d] = dn / hnorm;
+    }
+  }
+  a0 = ux[0];
+  a1 = uy[1];
+  a2 = 0.5 * (uy[0] + ux[1]);
+}
+
+__global__ void k_linearize_faces(Geom g, Model m, int k1, const double* __restrict__ state, double* __restrict__ etaf,
+                                  double* __restrict__ gamf) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;  // bf*4 + q
+  const int mu = blockIdx.y;
+  if (t >= g.nbf * 4 || mu >= k1) return;
+  const int bf = t / 4, q = t % 4;
+  double a0, a1, a2;
+  face_symgrad(g, state + (size_t)mu * g.mv, bf, q, a0, a1, a2);
+  double e, gm;
+  tangent_coeffs(m, a0 * a0 + a1 * a1 + 2.0 * a2 * a2, e, gm);
+  etaf[(size_t)mu * g.nbf * 4 + t] = e;
+  gamf[(size_t)mu * g.nbf * 4 + t] = gm;
+}
+
+__global__ void k_lifting(Geom g, Model m, const double* __restrict__ ghat, double* __restrict__ etad,
+                          double* __restrict__ betad, double* __restrict__ dg) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= g.nbf * 4) return;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  if (ghat) face_symgrad(g, ghat, t / 4, t % 4, a0, a1, a2);
+  const double a_sq = a0 * a0 + a1 * a1 + 2.0 * a2 * a2;
+  etad[t] = eta_field(m, a_sq);
+  betad[t] = beta_field(m, a_sq);
+  dg[3 * t] = a0;
+  dg[3 * t + 1] = a1;
+  dg[3 * t + 2] = a2;
+}
+
+template <int K1>
+size_t jac_smem() {
+  return ((size_t)K1 * 2 * PLANE + 2 * PLANE + (size_t)NT * 18) * sizeof(double);
+}
+template <int K1>
+size_t res_smem() {
+  return ((size_t)K1 * 2 * PLANE + 4 * PLANE + (size_t)NT * 18) * sizeof(double);
+}
+
+template <int K1>
+cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* state,
+                       const double* x, const double* rhs, double* out, cudaStream_t st) {
+  static bool configured = false;
+  const size_t sm = jac_smem<K1>();
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_jacobian<K1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid((g.nx + TX - 1) / TX, (g.ny + TY - 1) / TY);
+  k_jacobian<K1><<<grid, NT, sm, st>>>(g, td, ds, L, state, x, rhs, out);
+  return cudaGetLastError();
+}
+
+template <int K1>
+cudaError_t launch_res(const Geom& g, const TimeData& td, const Disc& ds, const Model& m, const Lin& L,
+                       const double* U, const double* advect, const double* vminus, const double* fqp,
+                       const double* ghat, double* out, cudaStream_t st) {
+  static bool configured = false;
+  const size_t sm = res_smem<K1>();
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_residual<K1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid((g.nx + TX - 1) / TX, (g.ny + TY - 1) / TY);
+  k_residual<K1><<<grid, NT, sm, st>>>(g, td, ds, m, L, U, advect, vminus, fqp, ghat, out);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t set_tables(const Tables& t) { return cudaMemcpyToSymbol(c_tab, &t, sizeof(Tables)); }
+
+cudaError_t jacobian_apply(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* state,
+                           const double* x, const double* rhs, double* out, cudaStream_t st) {
+  switch (td.k1) {
+    case 1: return launch_jac<1>(g, td, ds, L, state, x, rhs, out, st);
+    case 2: return launch_jac<2>(g, td, ds, L, state, x, rhs, out, st);
+    case 3: return launch_jac<3>(g, td, ds, L, state, x, rhs, out, st);
+    case 4: return launch_jac<4>(g, td, ds, L, state, x, rhs, out, st);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+cudaError_t slab_residual(const Geom& g, const TimeData& td, const Disc& ds, const Model& m, const Lin& L,
+                          const double* U, const double* advect, const double* vminus, const double* fqp,
+                          const double* ghat, double* out, cudaStream_t st) {
+  switch (td.k1) {
+    case 1: return launch_res<1>(g, td, ds, m, L, U, advect, vminus, fqp, ghat, out, st);
+    case 2: return launch_res<2>(g, td, ds, m, L, U, advect, vminus, fqp, ghat, out, st);
+    case 3: return launch_res<3>(g, td, ds, m, L, U, advect, vminus, fqp, ghat, out, st);
+    case 4: return launch_res<4>(g, td, ds, m, L, U, advect, vminus, fqp, ghat, out, st);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+cudaError_t linearize(const Geom& g, const Model& m, int k1, const double* state, double* eta, double* gam,
+                      double* etaf, double* gamf, cudaStream_t st) {
+  dim3 gc((g.ncells + 127) / 128, k1);
+  k_linearize_cells<<<gc, 128, 0, st>>>(g, m, k1, state, eta, gam);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  dim3 gf((g.nbf * 4 + 127) / 128, k1);
+  k_linearize_faces<<<gf, 128, 0, st>>>(g, m, k1, state, etaf, gamf);
+  return cudaGetLastError();
+}
+
+cudaError_t lifting(const Geom& g, const Model& m, const double* ghat, double* etad, double* betad, double* dg,
+                    cudaStream_t st) {
+  k_lifting<<<(g.nbf * 4 + 127) / 128, 128, 0, st>>>(g, m, ghat, etad, betad, dg);
+  return cudaGetLastError();
+}
+
+}  // namespace pdst

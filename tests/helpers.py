@@ -52,3 +52,38 @@ def rel_err(a, b):
 def assert_close(a, b, tol=1e-12, what=""):
     e2, ei = rel_err(a, b)
     assert e2 <= tol and ei <= tol, f"{what}: rel L2 {e2:.3e}, rel Linf {ei:.3e} > {tol:.0e}"
+
+
+def product_ctx(case, fx):
+    """The product's own SlabContext for a golden case (K_t etc. from the fixture)."""
+    from paper_2603_28706_b200 import problem as pb
+    from paper_2603_28706_b200.radau import TimeBasis, TimeMatrices
+
+    cfg = case.cfg
+    mesh = pb.tag_sides(pb.QuadMesh(cfg.nx, cfg.ny, *cfg.extents), case.neumann_sides)
+    disc = pb.Discretization(mesh)
+    config = pb.DiscretizationConfig(cfg.gamma1, cfg.gamma2, cfg.gamma_cip, fx.get("g_hat"))
+    params = pb.ModelParams(cfg.p, cfg.delta, cfg.nu, cfg.nu_inf)
+    basis = TimeBasis(cfg.k, fx["nodes"], fx["weights"])
+    tmat = TimeMatrices(fx["M_t"], fx["K_t"], fx["m_t"])
+    return pb.SlabContext(disc, params, config, pb.ProblemData(f=FORCINGS[case.forcing]), basis, tmat,
+                          case.t_start, cfg.tau, fx["v_minus"])
+
+
+def product_variant(case):
+    from paper_2603_28706_b200 import problem as pb
+
+    if case.variant == "pic":
+        return pb.picard()
+    if case.variant == "exn":
+        return pb.exact_newton()
+    return pb.modified_newton(case.cfg.nu if case.sigma_max is None else case.sigma_max)
+
+
+def cuda_available():
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:
+        return False

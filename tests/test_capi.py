@@ -1,0 +1,30 @@
+"""CPU-side checks of the C ABI: the library loads and exports every symbol
+include/pdst.h declares (no compute calls without a GPU)."""
+
+import os
+import re
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "pdst.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(pdst_\w+)\s*\(", text, re.M)))
+
+
+def test_header_symbols_exported():
+    from paper_2603_28706_b200 import _lib
+
+    lib = _lib.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    assert set(syms) == set(_lib.SIGNATURES), set(syms) ^ set(_lib.SIGNATURES)
+
+
+def test_version_and_error_string():
+    from paper_2603_28706_b200 import _lib
+
+    assert b"sm_100a" in _lib.lib().pdst_version()
+    assert isinstance(_lib.lib().pdst_last_error(), bytes)
