@@ -1,0 +1,340 @@
+"""Benchmark of the B200 slab hot path.
+
+Workload (BASELINE.json configs[1], "cfg2"): 256x256 Q2/P1disc, DG(1) with 2
+right-Radau points, fp64, p=1.3, delta=1e-3, nu=1, nu_inf=0, modified-Newton
+tangent (sigma_max = nu), surrogate Vanka patches frozen at the last Radau
+point, omega = 0.7.  N_dof = 1,445,892.
+
+One step = one matrix-free slab Jacobian apply (y = J x) + one Vanka sweep
+(d <- d + omega sum_K R_K' A_K^-1 R_K (r - J d)) on device-resident vectors.
+metric = GDoF/s = N_dof x ranks / (time per step).  L2 is flushed (256 MiB
+write) between timed steps, outside the events.
+
+  python bench.py [--gpus N --steps K --warmup W]      our arm (one JSON line)
+  python bench.py --impl reference ...                  CPU reference arm (oracle port)
+
+Multi-GPU: one process per GPU; each rank runs an independent replica (the
+cell-partitioned path with NCCL halos is not in this round), "scaling": "weak".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "GDoF/s of matrix-free space-time Jacobian apply + Vanka sweep; HBM % of peak"
+UNIT = "GDoF/s"
+CPU_SAMPLE_N = 64
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = sorted(float(r[0]) for r in rows if r[0].replace(".", "").isdigit())
+        mx = max(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_baseline_single(steps=6):
+    env = dict(os.environ, OPENBLAS_NUM_THREADS="1", OMP_NUM_THREADS="1", MKL_NUM_THREADS="1")
+    out = subprocess.run([sys.executable, "-m", "oracle.cpu_bench", "--n", str(CPU_SAMPLE_N), "--steps", str(steps)],
+                         cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    if out.returncode != 0:
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": "failed: " + out.stderr[-300:]}
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    return {"value": r["gdofs"], "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": (f"oracle/pdst_oracle.py (numpy restatement of pdflow) on a {CPU_SAMPLE_N}x{CPU_SAMPLE_N} "
+                       f"mesh with the cfg2 parameters (N_dof={r['n_dof']}), {steps} x (apply + sweep), 1 thread; "
+                       f"apply {r['t_apply_s']:.3f} s, sweep {r['t_sweep_s']:.3f} s"),
+            "t_apply_s": r["t_apply_s"], "t_sweep_s": r["t_sweep_s"]}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    procs = max(1, min(os.cpu_count() or 1, 64))
+    from oracle.cpu_bench import Pool
+
+    t0 = time.time()
+    pool = Pool(CPU_SAMPLE_N, procs)
+    build = time.time() - t0
+    for _ in range(args.warmup):
+        pool.step()
+    ts = [pool.step() for _ in range(args.steps)]
+    pool.close()
+    t = sum(ts) / len(ts)
+    value = procs * pool.n_dof / t / 1e9
+    sample = (f"{procs} worker processes (all host threads, one numpy oracle each) on {CPU_SAMPLE_N}x{CPU_SAMPLE_N} "
+              f"cfg2-parameter samples (N_dof={pool.n_dof} each); step = apply + sweep on every worker; "
+              f"wall time per step {t:.3f} s; untimed patch build {build:.1f} s")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded modal state, SURVEY.md §8d)",
+            "impl": "reference",
+            "config": {"workload": "cfg2 parameters on bounded CPU samples", "sample_mesh": CPU_SAMPLE_N,
+                       "parallelism": f"{procs} processes"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2603_28706_b200 import _lib as L
+    from paper_2603_28706_b200 import problem as pb
+    from paper_2603_28706_b200.operators import SlabJacobian
+    from paper_2603_28706_b200.smoother import VankaLevel, vanka_smooth
+    from paper_2603_28706_b200.synth import CONFIGS, make_slab_inputs
+
+    cfg = CONFIGS[args.config]
+    params = pb.ModelParams(cfg.p, cfg.delta, cfg.nu, cfg.nu_inf)
+    conf = pb.DiscretizationConfig(cfg.gamma1, cfg.gamma2, cfg.gamma_cip)
+    syn = make_slab_inputs(cfg)
+    ctx = pb.make_context(cfg.nx, cfg.ny, cfg.k, params, cfg.tau, config=conf, v_minus=syn.v_minus)
+    variant = pb.modified_newton(cfg.nu)
+    dev = torch.device("cuda", local)
+    U = torch.as_tensor(syn.U, device=dev)
+    x = torch.as_tensor(syn.x, device=dev)
+    r = x.clone()
+    d0 = torch.as_tensor(syn.d0, device=dev)
+    d = d0.clone()
+    y = torch.empty_like(x)
+    t_setup = time.time()
+    jac = SlabJacobian(ctx, U, variant, device=local)
+    lvl = VankaLevel(ctx, U, variant, surrogate=True, rep_fraction=cfg.rep_fraction, jac=jac)
+    torch.cuda.synchronize()
+    t_setup = time.time() - t_setup
+    N = x.numel()
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+
+    def step():
+        jac.matvec(x, out=y)
+        lvl.smooth(d, r, 1, cfg.omega, inplace=True)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        ev[i][0].record()
+        step()
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+    t_step = sum(a.elapsed_time(b) for a, b in ev) / args.steps / 1e3  # seconds
+    if ws > 1:
+        tt = torch.tensor([t_step], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_step = float(tt.item())
+    value = ws * N / t_step / 1e9
+
+    # -- per-kernel times (CUDA events inside libpdst, same stream) ---------
+    h = jac.dev.h
+    L.lib().pdst_profile(h, 1)
+    nprof = max(3, min(args.steps, 20))
+    for i in range(nprof):
+        flush.fill_(float(i))
+        step()
+    torch.cuda.synchronize()
+    kt = {}
+    for kid, name in ((0, "jacobian"), (1, "vanka_gemv"), (2, "vanka_scatter")):
+        ms, cnt = L.C.c_double(), L.C.c_int64()
+        L.lib().pdst_profile_read(h, kid, L.C.byref(ms), L.C.byref(cnt))
+        kt[name] = (ms.value / max(cnt.value, 1), cnt.value)
+    L.lib().pdst_profile(h, 0)
+    launches_per_step = 4  # apply + (defect apply, gemv, scatter)
+
+    nc, k1 = cfg.nx * cfg.ny, cfg.k + 1
+    D = 21 * k1
+    nd = ctx.disc.ndof
+    mv = ctx.disc.n_velocity
+    nbf = 2 * (cfg.nx + cfg.ny)
+    # algorithmic bytes
+    b_gemv = 8.0 * (nc * D * D + N + nc * D)  # inverses + defect + update
+    b_apply_ours = 8.0 * (2 * N + k1 * mv + 2 * 16 * k1 * nc + 2 * 4 * k1 * nbf)  # x, y, state, eta/gamma, faces
+    b_apply_ref = 8.0 * k1 * (2 * nd + 112 * nc + 56 * nbf + 4 * (2 * cfg.nx * (cfg.nx - 1)))
+    peak, peak_kind = _peaks()
+    t_gemv = kt["vanka_gemv"][0] * 1e-3
+    t_jac = kt["jacobian"][0] * 1e-3
+    ach = b_gemv / t_gemv / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic_r01.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("vanka_gemv")
+        except Exception:
+            traffic = None
+
+    # -- e2e through the public API with host (pinned) buffers ---------------
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+        t.numpy()[...] = a
+        return t.numpy()
+
+    xh, rh, dh = pinned(syn.x), pinned(syn.x), pinned(syn.d0)
+    yh = pinned(np.zeros_like(syn.x))
+
+    def step_host():
+        jac.matvec(xh, out=yh)
+        return vanka_smooth(lvl, dh, rh, 1, cfg.omega)
+
+    for _ in range(2):
+        step_host()
+    n_e2e = max(3, min(args.steps, 10))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(n_e2e):
+        step_host()
+    torch.cuda.synchronize()
+    t_e2e = (time.perf_counter() - t0) / n_e2e
+    if ws > 1:
+        tt = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    e2e = {"value": ws * N / t_e2e / 1e9, "unit": UNIT, "h2d_bytes_per_step": 3 * 8 * N,
+           "d2h_bytes_per_step": 2 * 8 * N, "ms_per_step": t_e2e * 1e3,
+           "note": "SlabJacobian.matvec + vanka_smooth on pinned numpy buffers (libpdst copies in/out), wall clock"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_single(args.cpu_steps)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded 16-mode modal state + 1e-3 noise, SURVEY.md §8d; no dataset)",
+        "config": {"workload": f"{cfg.name}: {cfg.nx}x{cfg.ny} Q2/P1disc, DG({cfg.k}), p={cfg.p}, delta={cfg.delta}, "
+                               f"nu={cfg.nu}, nu_inf={cfg.nu_inf}, modN(sigma_max=nu), surrogate patches at "
+                               f"rep_fraction={cfg.rep_fraction}, omega={cfg.omega}",
+                   "n_dof": N, "step": "1 Jacobian apply + 1 Vanka sweep (1 smoothing step)",
+                   "l2": "flushed between timed steps (256 MiB write, outside events)",
+                   "parallelism": f"replicas x{ws}"},
+        "gpu_launches": launches_per_step * args.steps,
+        "roofline": {"bound": "hbm", "kernel": "vanka_gemv (patch-inverse stream)", "achieved": ach, "peak": peak,
+                     "unit": "GB/s", "frac": ach / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "algorithmic_bytes": b_gemv, "launch_ms": kt["vanka_gemv"][0]},
+        "kernels": {
+            "jacobian_apply": {"ms": kt["jacobian"][0], "gdofs": N / t_jac / 1e9,
+                               "algorithmic_bytes": b_apply_ours, "gbs": b_apply_ours / t_jac / 1e9,
+                               "frac_hbm": b_apply_ours / t_jac / 1e9 / peak,
+                               "reference_cache_bytes": b_apply_ref,
+                               "reference_cache_equiv_gbs": b_apply_ref / t_jac / 1e9},
+            "vanka_gemv": {"ms": kt["vanka_gemv"][0]},
+            "vanka_scatter": {"ms": kt["vanka_scatter"][0]},
+        },
+        "apply_gdofs": N / t_jac / 1e9,
+        "sweep_gdofs": N / (t_jac + t_gemv + kt["vanka_scatter"][0] * 1e-3) / 1e9,
+        "setup_s": t_setup,
+        "clocks": clk,
+        "e2e": e2e,
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--cpu-steps", type=int, default=6)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -118,6 +118,12 @@ int pdst_restrict(pdst_handle* h, int fine_level, const double* r_fine, double* 
 int pdst_prolong(pdst_handle* h, int fine_level, const double* e_coarse, double* e_fine, int where);
 int pdst_vcycle(pdst_handle* h, const double* r, double* z, int pre, int post, double omega, int where);
 
+/* Kernel timing for benchmarks: CUDA events around every launch of class
+   kernel (0 jacobian/defect, 1 vanka gemv, 2 vanka scatter, 3 residual,
+   4 transfers, 5 coarse-level operators) while enabled. */
+int pdst_profile(pdst_handle* h, int enable);
+int pdst_profile_read(pdst_handle* h, int kernel, double* total_ms, int64_t* launches);
+
 const char* pdst_last_error(void);
 const char* pdst_version(void);
 

@@ -952,7 +952,7 @@ class StmgOracle:
                 lv.ids, lv.mats = patch_matrices(lv, lv.j_nodes)
             lv.invs = np.linalg.inv(lv.mats)
         self.levels = levels
-        self._coarse()
+        self.coarse_lu = None  # built on first use (the dense coarse LU is O(N^2) memory)
 
     def _coarse(self):
         lv = self.levels[0]
@@ -978,6 +978,8 @@ class StmgOracle:
 
     def vcycle(self, ell, b):
         if ell == 0:
+            if self.coarse_lu is None:
+                self._coarse()
             return sla.lu_solve(self.coarse_lu, b)
         lv = self.levels[ell]
         d = vanka(lv, np.zeros_like(b), b, self.pre, self.omega)

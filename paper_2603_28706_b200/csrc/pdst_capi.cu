@@ -17,8 +17,9 @@ using namespace pdst;
 
 namespace {
 thread_local std::string g_last_error;
+}  // namespace
 
-int fail(int code, const char* fmt, ...) {
+int pdst::set_error(int code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
   va_start(ap, fmt);
@@ -27,6 +28,9 @@ int fail(int code, const char* fmt, ...) {
   g_last_error = buf;
   return code;
 }
+
+namespace {
+#define fail pdst::set_error
 
 int cuda_fail(cudaError_t e, const char* where) {
   return fail(PDST_ECUDA, "%s: %s", where, cudaGetErrorString(e));
@@ -71,12 +75,6 @@ Tables host_tables() {
   return t;
 }
 
-struct Staging {
-  pdst_handle* h;
-  int where;
-  std::vector<std::pair<double*, const double*>> ins;
-};
-
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -120,7 +118,7 @@ Geom make_geom(int nx, int ny, double x0, double y0, double x1, double y1, const
 }  // namespace pdst
 
 // Copy a caller array to a device scratch buffer when it lives on the host.
-static const double* stage_in(pdst_handle* h, DeviceBuffer& buf, const double* p, size_t n, int where, int* err) {
+const double* pdst::stage_in(pdst_handle* h, DeviceBuffer& buf, const double* p, size_t n, int where, int* err) {
   if (!p) return nullptr;
   if (where == PDST_DEVICE) return p;
   double* d = buf.ensure(n);
@@ -136,18 +134,18 @@ static const double* stage_in(pdst_handle* h, DeviceBuffer& buf, const double* p
   return d;
 }
 
-static double* out_ptr(DeviceBuffer& buf, double* p, size_t n, int where) {
+double* pdst::out_ptr(DeviceBuffer& buf, double* p, size_t n, int where) {
   return where == PDST_DEVICE ? p : buf.ensure(n);
 }
 
-static int finish_out(pdst_handle* h, double* host, const double* dev, size_t n, int where) {
+int pdst::finish_out(pdst_handle* h, double* host, const double* dev, size_t n, int where) {
   if (where == PDST_DEVICE) return PDST_OK;
   CK(cudaMemcpyAsync(host, dev, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   return PDST_OK;
 }
 
-static int check_where(int where) {
+int pdst::check_where(int where) {
   if (where != PDST_HOST && where != PDST_DEVICE) return fail(PDST_EINVAL, "where must be PDST_HOST or PDST_DEVICE");
   return PDST_OK;
 }
@@ -301,19 +299,6 @@ int pdst_linearize(pdst_handle* h, const double* U, int kind, double sigma_max, 
   return PDST_OK;
 }
 
-static Lin lin_of(pdst_handle* h) {
-  Lin L{};
-  L.eta = h->eta.ptr;
-  L.gam = h->gam.ptr;
-  L.etaf = h->etaf.ptr;
-  L.gamf = h->gamf.ptr;
-  L.etad = h->etad.ptr;
-  L.betad = h->betad.ptr;
-  L.dg = h->dg.ptr;
-  L.has_gamma = h->model.kind != 0;
-  return L;
-}
-
 static int jac_common(pdst_handle* h, const double* x, const double* r, double* y, int where) {
   if (!h || !x || !y) return fail(PDST_EINVAL, "null argument");
   if (int e = check_where(where)) return e;
@@ -327,7 +312,7 @@ static int jac_common(pdst_handle* h, const double* x, const double* r, double* 
   if (err) return err;
   double* yd = out_ptr(h->scratch_b, y, n, where);
   if (!yd) return fail(PDST_ECUDA, "out of device memory");
-  CK(jacobian_apply(h->g, h->td, h->ds, lin_of(h), h->state.ptr, xd, rd, yd, h->stream));
+  CK(PDST_TIMED(h, PK_JACOBIAN, jacobian_apply(h->g, h->td, h->ds, lin_of(h), h->state.ptr, xd, rd, yd, h->stream)));
   return finish_out(h, y, yd, n, where);
 }
 
@@ -361,8 +346,9 @@ int pdst_residual(pdst_handle* h, const double* U, const double* v_minus, const 
   double* Rd = out_ptr(h->scratch_b, R, n, where);
   if (!Rd) return fail(PDST_ECUDA, "out of device memory");
   Lin L = lin_of(h);
-  CK(slab_residual(g, h->td, h->ds, h->model, L, Ud, ad, vm, fq, h->has_ghat ? h->ghat.ptr : nullptr, Rd,
-                   h->stream));
+  CK(PDST_TIMED(h, PK_RESIDUAL,
+                slab_residual(g, h->td, h->ds, h->model, L, Ud, ad, vm, fq, h->has_ghat ? h->ghat.ptr : nullptr, Rd,
+                              h->stream)));
   return finish_out(h, R, Rd, n, where);
 }
 
@@ -399,6 +385,27 @@ static int dot_common(pdst_handle* h, const double* a, const double* b, int64_t 
   else
     CK(dot(ad, bd, n, part, res, h->stream));
   return finish_out(h, out, res, 1, where);
+}
+
+int pdst_profile(pdst_handle* h, int enable) {
+  if (!h) return fail(PDST_EINVAL, "null handle");
+  h->prof.drain();
+  for (int k = 0; k < Profiler::NK; ++k) {
+    h->prof.total_ms[k] = 0.0;
+    h->prof.count[k] = 0;
+  }
+  h->prof.on = enable != 0;
+  return PDST_OK;
+}
+
+int pdst_profile_read(pdst_handle* h, int kernel, double* total_ms, int64_t* launches) {
+  if (!h) return fail(PDST_EINVAL, "null handle");
+  if (kernel < 0 || kernel >= Profiler::NK) return fail(PDST_EINVAL, "kernel class %d out of range", kernel);
+  CK(cudaSetDevice(h->device));
+  h->prof.drain();
+  if (total_ms) *total_ms = h->prof.total_ms[kernel];
+  if (launches) *launches = h->prof.count[kernel];
+  return PDST_OK;
 }
 
 int pdst_mass_dot(pdst_handle* h, const double* a, const double* b, double* out, int where) {

@@ -46,6 +46,48 @@ struct Level {
   }
 };
 
+// Optional CUDA-event timing of every kernel launch (bench / roofline).
+struct Profiler {
+  static constexpr int NK = 8;
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[NK];
+  double total_ms[NK] = {0};
+  long long count[NK] = {0};
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+  void drain() {
+    for (int k = 0; k < NK; ++k) {
+      for (auto& pr : pending[k]) {
+        float ms = 0.f;
+        cudaEventSynchronize(pr.second);
+        cudaEventElapsedTime(&ms, pr.first, pr.second);
+        total_ms[k] += ms;
+        count[k] += 1;
+        pool.push_back(pr.first);
+        pool.push_back(pr.second);
+      }
+      pending[k].clear();
+    }
+  }
+  ~Profiler() {
+    for (int k = 0; k < NK; ++k)
+      for (auto& pr : pending[k]) {
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+      }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
 }  // namespace pdst
 
 struct pdst_handle {
@@ -73,8 +115,15 @@ struct pdst_handle {
   pdst::DeviceBuffer scratch_a, scratch_b, scratch_c, scratch_d, scratch_f;
   pdst::DeviceBuffer partials;
 
+  // surrogate (representative-state) linearization and patch scratch
+  pdst::DeviceBuffer state_rep, eta_rep, gam_rep, etaf_rep, gamf_rep;
+  pdst::DeviceBuffer ET, upd, defect, ibuf;
+
+  pdst::Profiler prof;
+
   // multigrid
   std::vector<pdst::Level*> levels;  // 0 = coarsest
+  int min_cells = 0;
   bool patches_valid = false;
 
   ~pdst_handle() {
@@ -82,3 +131,41 @@ struct pdst_handle {
     if (dirichlet) cudaFree(dirichlet);
   }
 };
+
+namespace pdst {
+// Record the message returned by pdst_last_error(); returns `code`.
+int set_error(int code, const char* fmt, ...);
+// Host/device argument staging (where = PDST_HOST copies through the handle).
+const double* stage_in(pdst_handle* h, DeviceBuffer& buf, const double* p, size_t n, int where, int* err);
+double* out_ptr(DeviceBuffer& buf, double* p, size_t n, int where);
+int finish_out(pdst_handle* h, double* host, const double* dev, size_t n, int where);
+int check_where(int where);
+
+// Kernel classes for pdst_profile_read.
+enum { PK_JACOBIAN = 0, PK_VANKA_GEMV = 1, PK_VANKA_SCATTER = 2, PK_RESIDUAL = 3, PK_TRANSFER = 4, PK_LEVEL = 5 };
+
+// Launch `expr` (a cudaError_t expression) bracketed by profiling events when enabled.
+#define PDST_TIMED(h, kid, expr)                                      \
+  ([&]() -> cudaError_t {                                            \
+    if (!(h)->prof.on) return (expr);                                \
+    cudaEvent_t _a = (h)->prof.get(), _b = (h)->prof.get();          \
+    cudaEventRecord(_a, (h)->stream);                                \
+    cudaError_t _r = (expr);                                         \
+    cudaEventRecord(_b, (h)->stream);                                \
+    (h)->prof.pending[(kid)].push_back({_a, _b});                    \
+    return _r;                                                       \
+  }())
+
+inline Lin lin_of(pdst_handle* h) {
+  Lin L{};
+  L.eta = h->eta.ptr;
+  L.gam = h->gam.ptr;
+  L.etaf = h->etaf.ptr;
+  L.gamf = h->gamf.ptr;
+  L.etad = h->etad.ptr;
+  L.betad = h->betad.ptr;
+  L.dg = h->dg.ptr;
+  L.has_gamma = h->model.kind != 0;
+  return L;
+}
+}  // namespace pdst

@@ -19,6 +19,11 @@ cudaError_t slab_residual(const Geom& g, const TimeData& td, const Disc& ds, con
 cudaError_t linearize(const Geom& g, const Model& m, int k1, const double* state, double* eta, double* gam,
                       double* etaf, double* gamf, cudaStream_t st);
 
+// Element matrices (volume + boundary sides, no CIP / mass / tau w) of node
+// slot mu of the linearization L at velocity state (Mv), column-major per cell.
+cudaError_t element_matrices(const Geom& g, const Disc& ds, const Lin& L, int mu, const double* state, double* ET,
+                             cudaStream_t st);
+
 cudaError_t lifting(const Geom& g, const Model& m, const double* ghat, double* etad, double* betad, double* dg,
                     cudaStream_t st);
 
@@ -32,7 +37,8 @@ cudaError_t dot(const double* a, const double* b, size_t n, double* partials, do
 
 // Strip the velocity components of a slab state into a dense (k1, Mv) copy.
 cudaError_t copy_velocity_blocks(const Geom& g, int k1, const double* U, double* V, cudaStream_t st);
-// V = sum_mu c[mu] U_mu (velocity only)
-cudaError_t blend_velocity(const Geom& g, int k1, const double* coef, const double* U, double* V, cudaStream_t st);
+// V = sum_mu c[mu] U_mu (velocity part of blocks of length `stride`)
+cudaError_t blend_velocity(const Geom& g, int k1, const double* coef, const double* U, size_t stride, double* V,
+                           cudaStream_t st);
 
 }  // namespace pdst

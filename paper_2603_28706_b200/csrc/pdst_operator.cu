@@ -61,7 +61,8 @@ __device__ void stage_velocity(const Geom& g, const double* __restrict__ v, doub
 
 // line[t][d] = sum_n coef[n] F(node (n along axis-normal, t along tangent))
 // for the 3x3 node block whose lower-left staged node is (r0, c0).
-__device__ __forceinline__ void line_sums(const Plane2& F, int r0, int c0, int axis, const double* coef,
+template <class FA>
+__device__ __forceinline__ void line_sums(const FA& F, int r0, int c0, int axis, const double* coef,
                                           double line[3][2]) {
 #pragma unroll
   for (int t = 0; t < 3; ++t) {
@@ -111,7 +112,8 @@ __device__ __forceinline__ void face_scatter(int axis, int e, const double RE[3]
 // (forms.py:639-650); sgn = +1 for the Jacobian, -1 for the residual
 // (forms.py:415-432).  F = field whose normal-derivative jump is penalised,
 // A = lagged advective field (weights), both staged.
-__device__ void cip_side(const Geom& g, const Disc& ds, int side, const Plane2& F, const Plane2& A, int r0, int c0,
+template <class FA, class AA>
+__device__ void cip_side(const Geom& g, const Disc& ds, int side, const FA& F, const AA& A, int r0, int c0,
                          double sgn, double acc[3][3][2]) {
   int axis, e_own, dummy_e;
   double n0, n1;
@@ -183,8 +185,9 @@ __device__ __forceinline__ void face_point(const FaceLines& L, int axis, int q, 
 }
 
 // Jacobian boundary-side terms of one cell side (forms.py:605-637).
+template <class XA, class SA>
 __device__ void jac_boundary_side(const Geom& g, const Disc& ds, const Lin& L, int mu, int side, int bf,
-                                  const Plane2& X, const Plane2& S, int r0, int c0, const double P[3],
+                                  const XA& X, const SA& S, int r0, int c0, const double P[3],
                                   double acc[3][3][2], double accp[3]) {
   int axis, e;
   double n0, n1;
@@ -389,7 +392,8 @@ __device__ void res_boundary_side(const Geom& g, const Disc& ds, const Model& m,
 }
 
 // Stage-1 sums along x for one Q2 row jy at Gauss column qx.
-__device__ __forceinline__ void row_sums(const Plane2& F, int r, int c0, int qx, double sB[2], double sG[2]) {
+template <class FA>
+__device__ __forceinline__ void row_sums(const FA& F, int r, int c0, int qx, double sB[2], double sG[2]) {
 #pragma unroll
   for (int d = 0; d < 2; ++d) {
     const double f0 = F.at(d, r, c0), f1 = F.at(d, r, c0 + 1), f2 = F.at(d, r, c0 + 2);
@@ -430,6 +434,93 @@ __device__ __forceinline__ void add_mass(const Plane2* F, const Plane2* Fm, doub
         for (int d = 0; d < 2; ++d) acc[jy][i][d] = fma(m, T1[i][d], acc[jy][i][d]);
     }
   }
+}
+
+// Cell-local Jacobian action (volume + the cell's boundary sides), without the
+// CIP faces, the temporal mass and the tau w_mu scaling.  XA / SA are field
+// accessors (shared-memory planes in the apply, unit vectors / global memory
+// in the element-matrix kernel).  forms.py:589-637.
+template <class XA, class SA>
+__device__ __forceinline__ void jac_cell_local(const Geom& g, const Disc& ds, const Lin& L, int mu, int c, int ci,
+                                               int cj, const XA& XM, const SA& SP, int r0, int c0, const double P[3],
+                                               double acc[3][3][2], double accp[3]) {
+  const double W = g.hx * g.hy;
+      // ---- volume (forms.py:589-603) ----
+#pragma unroll 1
+      for (int qx = 0; qx < 4; ++qx) {
+        double xB[3][2], xG[3][2], sB[3][2], sG[3][2];
+#pragma unroll
+        for (int jy = 0; jy < 3; ++jy) {
+          row_sums(XM, r0 + jy, c0, qx, xB[jy], xG[jy]);
+          row_sums(SP, r0 + jy, c0, qx, sB[jy], sG[jy]);
+        }
+        double Pa[3][2] = {{0, 0}, {0, 0}, {0, 0}}, Qa[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+        const double xh = c_tab.s[qx] - 0.5;
+#pragma unroll
+        for (int qy = 0; qy < 4; ++qy) {
+          double u[2], ux[2], uy[2], v[2], vx[2], vy[2];
+#pragma unroll
+          for (int d = 0; d < 2; ++d) {
+            u[d] = c_tab.B[qy][0] * xB[0][d] + c_tab.B[qy][1] * xB[1][d] + c_tab.B[qy][2] * xB[2][d];
+            ux[d] = (c_tab.B[qy][0] * xG[0][d] + c_tab.B[qy][1] * xG[1][d] + c_tab.B[qy][2] * xG[2][d]) / g.hx;
+            uy[d] = (c_tab.G[qy][0] * xB[0][d] + c_tab.G[qy][1] * xB[1][d] + c_tab.G[qy][2] * xB[2][d]) / g.hy;
+            v[d] = c_tab.B[qy][0] * sB[0][d] + c_tab.B[qy][1] * sB[1][d] + c_tab.B[qy][2] * sB[2][d];
+            vx[d] = (c_tab.B[qy][0] * sG[0][d] + c_tab.B[qy][1] * sG[1][d] + c_tab.B[qy][2] * sG[2][d]) / g.hx;
+            vy[d] = (c_tab.G[qy][0] * sB[0][d] + c_tab.G[qy][1] * sB[1][d] + c_tab.G[qy][2] * sB[2][d]) / g.hy;
+          }
+          const int q = 4 * qx + qy;
+          const double wq = c_tab.w[qx] * c_tab.w[qy] * W;
+          double Fx0 = 0, Fx1 = 0, Fy0 = 0, Fy1 = 0;
+          if (ds.viscous) {
+            const size_t ci_ = ((size_t)mu * 16 + q) * g.ncells + c;
+            const double eta = __ldg(L.eta + ci_);
+            const double gam = L.has_gamma ? __ldg(L.gam + ci_) : 0.0;
+            const double a0 = vx[0], a1 = vy[1], a2 = 0.5 * (vy[0] + vx[1]);
+            const double b0 = ux[0], b1 = uy[1], b2 = 0.5 * (uy[0] + ux[1]);
+            const double ab = a0 * b0 + a1 * b1 + 2.0 * a2 * b2;
+            Fx0 = eta * b0 + gam * ab * a0;
+            Fy1 = eta * b1 + gam * ab * a1;
+            Fx1 = Fy0 = eta * b2 + gam * ab * a2;
+          }
+          if (ds.convection) {
+            Fx0 -= u[0] * v[0] + v[0] * u[0];
+            Fx1 -= u[1] * v[0] + v[1] * u[0];
+            Fy0 -= u[0] * v[1] + v[0] * u[1];
+            Fy1 -= u[1] * v[1] + v[1] * u[1];
+          }
+          if (ds.pressure) {
+            const double yh = c_tab.s[qy] - 0.5;
+            const double dp = P[0] + P[1] * xh + P[2] * yh;
+            Fx0 -= dp;
+            Fy1 -= dp;
+            const double dv = wq * (ux[0] + uy[1]);
+            accp[0] -= dv;
+            accp[1] -= dv * xh;
+            accp[2] -= dv * yh;
+          }
+#pragma unroll
+          for (int jy = 0; jy < 3; ++jy) {
+            Pa[jy][0] = fma(wq * Fx0, c_tab.B[qy][jy], Pa[jy][0]);
+            Pa[jy][1] = fma(wq * Fx1, c_tab.B[qy][jy], Pa[jy][1]);
+            Qa[jy][0] = fma(wq * Fy0, c_tab.G[qy][jy], Qa[jy][0]);
+            Qa[jy][1] = fma(wq * Fy1, c_tab.G[qy][jy], Qa[jy][1]);
+          }
+        }
+#pragma unroll
+        for (int jy = 0; jy < 3; ++jy)
+#pragma unroll
+          for (int ix = 0; ix < 3; ++ix)
+#pragma unroll
+            for (int d = 0; d < 2; ++d)
+              acc[jy][ix][d] += c_tab.G[qx][ix] / g.hx * Pa[jy][d] + c_tab.B[qx][ix] / g.hy * Qa[jy][d];
+      }
+      // ---- boundary sides (forms.py:605-637) ----
+      if (ci == 0 || cj == 0 || ci == g.nx - 1 || cj == g.ny - 1) {
+        if (cj == 0) jac_boundary_side(g, ds, L, mu, 0, side_offset(g, 0) + ci, XM, SP, r0, c0, P, acc, accp);
+        if (ci == g.nx - 1) jac_boundary_side(g, ds, L, mu, 1, side_offset(g, 1) + cj, XM, SP, r0, c0, P, acc, accp);
+        if (cj == g.ny - 1) jac_boundary_side(g, ds, L, mu, 2, side_offset(g, 2) + ci, XM, SP, r0, c0, P, acc, accp);
+        if (ci == 0) jac_boundary_side(g, ds, L, mu, 3, side_offset(g, 3) + cj, XM, SP, r0, c0, P, acc, accp);
+      }
 }
 
 // Node assembly from per-cell shared slots and the final write.
@@ -514,82 +605,7 @@ __global__ void __launch_bounds__(NT) k_jacobian(Geom g, TimeData td, Disc ds, L
       P[0] = __ldg(xp);
       P[1] = __ldg(xp + 1);
       P[2] = __ldg(xp + 2);
-      // ---- volume (forms.py:589-603) ----
-#pragma unroll 1
-      for (int qx = 0; qx < 4; ++qx) {
-        double xB[3][2], xG[3][2], sB[3][2], sG[3][2];
-#pragma unroll
-        for (int jy = 0; jy < 3; ++jy) {
-          row_sums(XM, r0 + jy, c0, qx, xB[jy], xG[jy]);
-          row_sums(SP, r0 + jy, c0, qx, sB[jy], sG[jy]);
-        }
-        double Pa[3][2] = {{0, 0}, {0, 0}, {0, 0}}, Qa[3][2] = {{0, 0}, {0, 0}, {0, 0}};
-        const double xh = c_tab.s[qx] - 0.5;
-#pragma unroll
-        for (int qy = 0; qy < 4; ++qy) {
-          double u[2], ux[2], uy[2], v[2], vx[2], vy[2];
-#pragma unroll
-          for (int d = 0; d < 2; ++d) {
-            u[d] = c_tab.B[qy][0] * xB[0][d] + c_tab.B[qy][1] * xB[1][d] + c_tab.B[qy][2] * xB[2][d];
-            ux[d] = (c_tab.B[qy][0] * xG[0][d] + c_tab.B[qy][1] * xG[1][d] + c_tab.B[qy][2] * xG[2][d]) / g.hx;
-            uy[d] = (c_tab.G[qy][0] * xB[0][d] + c_tab.G[qy][1] * xB[1][d] + c_tab.G[qy][2] * xB[2][d]) / g.hy;
-            v[d] = c_tab.B[qy][0] * sB[0][d] + c_tab.B[qy][1] * sB[1][d] + c_tab.B[qy][2] * sB[2][d];
-            vx[d] = (c_tab.B[qy][0] * sG[0][d] + c_tab.B[qy][1] * sG[1][d] + c_tab.B[qy][2] * sG[2][d]) / g.hx;
-            vy[d] = (c_tab.G[qy][0] * sB[0][d] + c_tab.G[qy][1] * sB[1][d] + c_tab.G[qy][2] * sB[2][d]) / g.hy;
-          }
-          const int q = 4 * qx + qy;
-          const double wq = c_tab.w[qx] * c_tab.w[qy] * W;
-          double Fx0 = 0, Fx1 = 0, Fy0 = 0, Fy1 = 0;
-          if (ds.viscous) {
-            const size_t ci_ = ((size_t)mu * 16 + q) * g.ncells + c;
-            const double eta = __ldg(L.eta + ci_);
-            const double gam = L.has_gamma ? __ldg(L.gam + ci_) : 0.0;
-            const double a0 = vx[0], a1 = vy[1], a2 = 0.5 * (vy[0] + vx[1]);
-            const double b0 = ux[0], b1 = uy[1], b2 = 0.5 * (uy[0] + ux[1]);
-            const double ab = a0 * b0 + a1 * b1 + 2.0 * a2 * b2;
-            Fx0 = eta * b0 + gam * ab * a0;
-            Fy1 = eta * b1 + gam * ab * a1;
-            Fx1 = Fy0 = eta * b2 + gam * ab * a2;
-          }
-          if (ds.convection) {
-            Fx0 -= u[0] * v[0] + v[0] * u[0];
-            Fx1 -= u[1] * v[0] + v[1] * u[0];
-            Fy0 -= u[0] * v[1] + v[0] * u[1];
-            Fy1 -= u[1] * v[1] + v[1] * u[1];
-          }
-          if (ds.pressure) {
-            const double yh = c_tab.s[qy] - 0.5;
-            const double dp = P[0] + P[1] * xh + P[2] * yh;
-            Fx0 -= dp;
-            Fy1 -= dp;
-            const double dv = wq * (ux[0] + uy[1]);
-            accp[0] -= dv;
-            accp[1] -= dv * xh;
-            accp[2] -= dv * yh;
-          }
-#pragma unroll
-          for (int jy = 0; jy < 3; ++jy) {
-            Pa[jy][0] = fma(wq * Fx0, c_tab.B[qy][jy], Pa[jy][0]);
-            Pa[jy][1] = fma(wq * Fx1, c_tab.B[qy][jy], Pa[jy][1]);
-            Qa[jy][0] = fma(wq * Fy0, c_tab.G[qy][jy], Qa[jy][0]);
-            Qa[jy][1] = fma(wq * Fy1, c_tab.G[qy][jy], Qa[jy][1]);
-          }
-        }
-#pragma unroll
-        for (int jy = 0; jy < 3; ++jy)
-#pragma unroll
-          for (int ix = 0; ix < 3; ++ix)
-#pragma unroll
-            for (int d = 0; d < 2; ++d)
-              acc[jy][ix][d] += c_tab.G[qx][ix] / g.hx * Pa[jy][d] + c_tab.B[qx][ix] / g.hy * Qa[jy][d];
-      }
-      // ---- boundary sides (forms.py:605-637) ----
-      if (ci == 0 || cj == 0 || ci == g.nx - 1 || cj == g.ny - 1) {
-        if (cj == 0) jac_boundary_side(g, ds, L, mu, 0, side_offset(g, 0) + ci, XM, SP, r0, c0, P, acc, accp);
-        if (ci == g.nx - 1) jac_boundary_side(g, ds, L, mu, 1, side_offset(g, 1) + cj, XM, SP, r0, c0, P, acc, accp);
-        if (cj == g.ny - 1) jac_boundary_side(g, ds, L, mu, 2, side_offset(g, 2) + ci, XM, SP, r0, c0, P, acc, accp);
-        if (ci == 0) jac_boundary_side(g, ds, L, mu, 3, side_offset(g, 3) + cj, XM, SP, r0, c0, P, acc, accp);
-      }
+      jac_cell_local(g, ds, L, mu, c, ci, cj, XM, SP, r0, c0, P, acc, accp);
       // ---- CIP own sides (forms.py:639-650) ----
       if (ds.convection && ds.gamma_cip > 0.0) {
         if (cj > 0) cip_side(g, ds, 0, XM, SP, r0, c0, 1.0, acc);
@@ -914,6 +930,58 @@ __global__ void k_lifting(Geom g, Model m, const double* __restrict__ ghat, doub
   dg[3 * t + 2] = a2;
 }
 
+// ---------------------------------------------------------------------------
+// Element matrices by applying the cell-local action to unit vectors, so the
+// assembled blocks agree with the matrix-free action to rounding (the
+// property of forms.py:519-525).  ET[c][j][i] = E_c[i][j] (column-major per
+// cell), local dofs i = 2a + d (a = 3 jy + ix) then 18 + pressure j.
+// ---------------------------------------------------------------------------
+struct UnitAcc {
+  int r, c, d;
+  __device__ double at(int dd, int rr, int cc) const { return (dd == d && rr == r && cc == c) ? 1.0 : 0.0; }
+};
+
+struct GlobAcc {
+  const double* v;
+  int nnx, X0, Y0;
+  __device__ double at(int d, int r, int c) const { return __ldg(v + 2 * ((size_t)(Y0 + r) * nnx + X0 + c) + d); }
+};
+
+__global__ void __launch_bounds__(128) k_element_matrices(Geom g, Disc ds, Lin L, int mu, const double* __restrict__ state,
+                                                          double* __restrict__ ET) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t c = t / 21;
+  const int j = (int)(t % 21);
+  if (c >= (size_t)g.ncells) return;
+  const int ci = (int)(c % g.nx), cj = (int)(c / g.nx);
+  const GlobAcc S{state, g.nnx, 2 * ci, 2 * cj};
+  double P[3] = {0.0, 0.0, 0.0};
+  UnitAcc X{-1, -1, -1};
+  if (j < 18) {
+    X.r = (j / 2) / 3;
+    X.c = (j / 2) % 3;
+    X.d = j % 2;
+  } else {
+    P[j - 18] = 1.0;
+  }
+  double acc[3][3][2];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  double accp[3] = {0.0, 0.0, 0.0};
+  jac_cell_local(g, ds, L, mu, (int)c, ci, cj, X, S, 0, 0, P, acc, accp);
+  double* out = ET + (c * 21 + j) * 21;
+#pragma unroll
+  for (int a = 0; a < 9; ++a) {
+    out[2 * a] = acc[a / 3][a % 3][0];
+    out[2 * a + 1] = acc[a / 3][a % 3][1];
+  }
+  out[18] = accp[0];
+  out[19] = accp[1];
+  out[20] = accp[2];
+}
+
 template <int K1>
 size_t jac_smem() {
   return ((size_t)K1 * 2 * PLANE + 2 * PLANE + (size_t)NT * 18) * sizeof(double);
@@ -989,6 +1057,13 @@ cudaError_t linearize(const Geom& g, const Model& m, int k1, const double* state
   if (e != cudaSuccess) return e;
   dim3 gf((g.nbf * 4 + 127) / 128, k1);
   k_linearize_faces<<<gf, 128, 0, st>>>(g, m, k1, state, etaf, gamf);
+  return cudaGetLastError();
+}
+
+cudaError_t element_matrices(const Geom& g, const Disc& ds, const Lin& L, int mu, const double* state, double* ET,
+                             cudaStream_t st) {
+  const size_t n = (size_t)g.ncells * 21;
+  k_element_matrices<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(g, ds, L, mu, state, ET);
   return cudaGetLastError();
 }
 

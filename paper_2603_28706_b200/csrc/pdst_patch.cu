@@ -1,0 +1,343 @@
+// pdst_patch.cu — Vanka patch matrices, batched patch inversion and the
+// additive Vanka sweep (sm_100a, fp64).
+//
+// Reference: solver/multigrid.py:251-299 (patch extraction + np.linalg.inv),
+// :327-340 (vanka_smooth), :475-488 (surrogate finest patches).
+//
+// Patch of cell K = the 21 spatial dofs of K (18 velocity a-major comp-minor,
+// 3 pressure) replicated over the k+1 Radau nodes, D = 21 (k+1):
+//   A_K[(mu,i),(nu,j)] = K_t[mu,nu] (R_K M R_K')_{ij}  (velocity i, j)
+//                      + delta_{mu nu} tau w_mu (R_K J_mu R_K')_{ij}.
+// R_K J R_K' is formed WITHOUT a global matrix: entry (A, B) sums the element
+// matrices of every cell that contains both nodes (up to 4 cells of the 3x3
+// neighbourhood) plus the CIP couplings of every interior face whose two
+// cells contain both nodes (up to 12 faces), evaluated on the fly from the
+// lagged state trace.  The mass block uses the assembled 1-D Q2 mass
+// (M = hx hy M1y (x) M1x (x) I2).
+#include <cuda_runtime.h>
+
+#include "pdst_device.cuh"
+#include "pdst_patch.h"
+
+namespace pdst {
+namespace {
+
+__device__ __forceinline__ double m1g(int X, int Xp, int n) {
+  double s = 0.0;
+  const int lo = max(0, (max(X, Xp) - 1) / 2);
+  for (int c = lo; c <= min(X, Xp) / 2 && c < n; ++c) {
+    const int a = X - 2 * c, b = Xp - 2 * c;
+    if (a >= 0 && a <= 2 && b >= 0 && b <= 2) s += c_tab.M1[a][b];
+  }
+  return s;
+}
+
+__device__ __forceinline__ int ceil_half(int v) { return v <= 0 ? -((-v) / 2) : (v + 1) / 2; }
+__device__ __forceinline__ int floor_half(int v) { return v >= 0 ? v / 2 : -((-v + 1) / 2); }
+
+// Jump of the normal derivative of the global Q2 basis function at node
+// coordinate Xn (normal direction) across the face whose left cell starts at
+// node 2f, times B[q][t] (tangential factor applied by the caller).
+__device__ __forceinline__ double jump_factor(int Xn, int f) {
+  double v = 0.0;
+  const int l = Xn - 2 * f;          // position in the left cell
+  if (l >= 0 && l <= 2) v += c_tab.dE[1][l];
+  const int r = Xn - 2 * f - 2;      // position in the right cell
+  if (r >= 0 && r <= 2) v -= c_tab.dE[0][r];
+  return v;
+}
+
+// Spatial block entry (R_K J R_K')_{ij} of element slot s.
+__device__ double spatial_entry(const PatchArgs& a, int s, int K, int i, int j) {
+  const Geom& g = a.g;
+  const int ki = K % g.nx, kj = K / g.nx;
+  const double* ET = a.ET + (size_t)s * g.ncells * 441;
+  if (i >= 18 || j >= 18) return ET[((size_t)K * 21 + j) * 21 + i];  // pressure couplings are cell-local
+  const int ia = i >> 1, d = i & 1, jb = j >> 1, e = j & 1;
+  const int XA = 2 * ki + ia % 3, YA = 2 * kj + ia / 3;
+  const int XB = 2 * ki + jb % 3, YB = 2 * kj + jb / 3;
+  const int xmin = min(XA, XB), xmax = max(XA, XB), ymin = min(YA, YB), ymax = max(YA, YB);
+  double val = 0.0;
+  // element matrices of every cell containing both nodes
+  for (int cy = max(0, ceil_half(ymax - 2)); cy <= min(g.ny - 1, floor_half(ymin)); ++cy)
+    for (int cx = max(0, ceil_half(xmax - 2)); cx <= min(g.nx - 1, floor_half(xmin)); ++cx) {
+      const int c = cy * g.nx + cx;
+      const int al = 3 * (YA - 2 * cy) + (XA - 2 * cx), bl = 3 * (YB - 2 * cy) + (XB - 2 * cx);
+      val += ET[((size_t)c * 21 + 2 * bl + e) * 21 + 2 * al + d];
+    }
+  if (d != e || !(a.ds.convection && a.ds.gamma_cip > 0.0)) return val;
+  const double* v = a.state + (size_t)s * g.mv;
+  // vertical faces (normal +x) between (fi, fj) and (fi+1, fj)
+  {
+    const double h = g.hy, coef = a.ds.gamma_cip * h * h / (g.hx * g.hx);
+    for (int fj = max(0, ceil_half(ymax - 2)); fj <= min(g.ny - 1, floor_half(ymin)); ++fj)
+      for (int fi = max(0, ceil_half(xmax - 4)); fi <= min(g.nx - 2, floor_half(xmin)); ++fi) {
+        const double ja = jump_factor(XA, fi), jb2 = jump_factor(XB, fi);
+        if (ja == 0.0 || jb2 == 0.0) continue;
+        const int ta = YA - 2 * fj, tb = YB - 2 * fj;
+        double sum = 0.0;
+        for (int q = 0; q < 4; ++q) {
+          double tr = 0.0;
+          for (int t = 0; t < 3; ++t)
+            tr = fma(c_tab.B[q][t], v[2 * ((size_t)(2 * fj + t) * g.nnx + 2 * fi + 2)], tr);
+          sum += (c_tab.w[q] * h) * fabs(tr) * (ja * c_tab.B[q][ta]) * (jb2 * c_tab.B[q][tb]);
+        }
+        val += coef * sum;
+      }
+  }
+  // horizontal faces (normal +y) between (fi, fj) and (fi, fj+1)
+  {
+    const double h = g.hx, coef = a.ds.gamma_cip * h * h / (g.hy * g.hy);
+    for (int fj = max(0, ceil_half(ymax - 4)); fj <= min(g.ny - 2, floor_half(ymin)); ++fj)
+      for (int fi = max(0, ceil_half(xmax - 2)); fi <= min(g.nx - 1, floor_half(xmin)); ++fi) {
+        const double ja = jump_factor(YA, fj), jb2 = jump_factor(YB, fj);
+        if (ja == 0.0 || jb2 == 0.0) continue;
+        const int ta = XA - 2 * fi, tb = XB - 2 * fi;
+        double sum = 0.0;
+        for (int q = 0; q < 4; ++q) {
+          double tr = 0.0;
+          for (int t = 0; t < 3; ++t)
+            tr = fma(c_tab.B[q][t], v[2 * ((size_t)(2 * fj + 2) * g.nnx + 2 * fi + t) + 1], tr);
+          sum += (c_tab.w[q] * h) * fabs(tr) * (ja * c_tab.B[q][ta]) * (jb2 * c_tab.B[q][tb]);
+        }
+        val += coef * sum;
+      }
+  }
+  return val;
+}
+
+__global__ void __launch_bounds__(448) k_patch_fine(PatchArgs a) {
+  const int K = blockIdx.x;
+  const int t = threadIdx.x;
+  if (t >= 441) return;
+  const Geom& g = a.g;
+  const int i = t / 21, j = t % 21;
+  const int k1 = a.td.k1, D = 21 * k1;
+  double M = 0.0;
+  if (i < 18 && j < 18 && (i & 1) == (j & 1)) {
+    const int ki = K % g.nx, kj = K / g.nx;
+    const int ia = i >> 1, jb = j >> 1;
+    M = g.hx * g.hy * (m1g(2 * kj + ia / 3, 2 * kj + jb / 3, g.ny) * m1g(2 * ki + ia % 3, 2 * ki + jb % 3, g.nx));
+  }
+  double Js[MAXK1];
+  for (int s = 0; s < a.nslot; ++s) Js[s] = spatial_entry(a, s, K, i, j);
+  double* A = a.mats + (size_t)K * D * D;
+  for (int mu = 0; mu < k1; ++mu) {
+    const double J = Js[a.nslot == 1 ? 0 : mu];
+    for (int nu = 0; nu < k1; ++nu) {
+      double v = (i < 18 && j < 18) ? a.td.K_t[mu * k1 + nu] * M : 0.0;
+      if (mu == nu) v += a.td.tau_w[mu] * J;
+      A[(size_t)(21 * mu + i) * D + 21 * nu + j] = v;
+    }
+  }
+}
+
+// In-place Gauss-Jordan inversion with partial (row) pivoting, one warp per
+// patch, matrix in shared memory (row stride D+1).  An exactly zero pivot
+// column marks the patch singular (LAPACK getrf info > 0, the condition under
+// which np.linalg.inv raises).  Output is stored transposed: invT[K][j][i].
+template <int D>
+__host__ __device__ constexpr int inv_wpb() { return D > 63 ? 2 : 4; }
+
+template <int D>
+__global__ void __launch_bounds__(128) k_invert(const double* __restrict__ mats, double* __restrict__ invT, int npatch,
+                                                int* __restrict__ bad) {
+  constexpr int WPB = inv_wpb<D>();
+  constexpr int LD = D + 1;
+  extern __shared__ double sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = blockIdx.x * WPB + warp;
+  double* A = sm + (size_t)warp * (D * LD + D);
+  double* col = A + D * LD;
+  __shared__ int perm[WPB][D];
+  if (K >= npatch) return;
+  const double* src = mats + (size_t)K * D * D;
+  for (int idx = lane; idx < D * D; idx += 32) A[(idx / D) * LD + idx % D] = src[idx];
+  __syncwarp();
+  bool singular = false;
+  for (int k = 0; k < D; ++k) {
+    double best = -1.0;
+    int bi = D;
+    for (int i = k + lane; i < D; i += 32) {
+      const double v = fabs(A[i * LD + k]);
+      if (v > best || (v == best && i < bi)) {
+        best = v;
+        bi = i;
+      }
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (ov > best || (ov == best && oi < bi)) {
+        best = ov;
+        bi = oi;
+      }
+    }
+    if (!(best > 0.0)) {
+      singular = true;
+      break;
+    }
+    if (lane == 0) perm[warp][k] = bi;
+    if (bi != k)
+      for (int jj = lane; jj < D; jj += 32) {
+        const double tmp = A[k * LD + jj];
+        A[k * LD + jj] = A[bi * LD + jj];
+        A[bi * LD + jj] = tmp;
+      }
+    __syncwarp();
+    const double pivinv = 1.0 / A[k * LD + k];
+    __syncwarp();
+    for (int jj = lane; jj < D; jj += 32) A[k * LD + jj] = (jj == k ? 1.0 : A[k * LD + jj]) * pivinv;
+    for (int i = lane; i < D; i += 32) col[i] = A[i * LD + k];
+    __syncwarp();
+    for (int idx = lane; idx < D * D; idx += 32) {
+      const int i = idx / D, jj = idx - i * D;
+      if (i == k) continue;
+      const double base = (jj == k) ? 0.0 : A[i * LD + jj];
+      A[i * LD + jj] = base - col[i] * A[k * LD + jj];
+    }
+    __syncwarp();
+  }
+  if (singular) {
+    if (lane == 0) atomicMin(bad, K);
+    return;
+  }
+  // unscramble the columns in reverse pivot order
+  for (int k = D - 1; k >= 0; --k) {
+    const int p = perm[warp][k];
+    if (p != k)
+      for (int i = lane; i < D; i += 32) {
+        const double tmp = A[i * LD + k];
+        A[i * LD + k] = A[i * LD + p];
+        A[i * LD + p] = tmp;
+      }
+    __syncwarp();
+  }
+  double* dst = invT + (size_t)K * D * D;
+  for (int idx = lane; idx < D * D; idx += 32) {
+    const int jj = idx / D, i = idx - jj * D;
+    dst[idx] = A[i * LD + jj];
+  }
+}
+
+// Slab dof of local patch position l of cell K.
+__device__ __forceinline__ size_t patch_dof(const Geom& g, int K, int l) {
+  const int mu = l / 21, s = l % 21;
+  const size_t base = (size_t)mu * g.nd;
+  if (s >= 18) return base + g.mv + 3 * (size_t)K + (s - 18);
+  const int a = s >> 1, d = s & 1;
+  const int ki = K % g.nx, kj = K / g.nx;
+  return base + 2 * ((size_t)(2 * kj + a / 3) * g.nnx + 2 * ki + a % 3) + d;
+}
+
+// upd_K = A_K^{-1} defect[ids_K]; threads (patch, row) read invT columns coalesced.
+template <int D>
+__global__ void __launch_bounds__(256) k_vanka_gemv(Geom g, const double* __restrict__ invT,
+                                                    const double* __restrict__ defect, double* __restrict__ upd) {
+  constexpr int PB = 256 / D;
+  __shared__ double loc[PB][D];
+  const int p = threadIdx.x / D, i = threadIdx.x % D;
+  const int K = blockIdx.x * PB + p;
+  const bool active = p < PB && K < g.ncells;
+  if (active) loc[p][i] = __ldg(defect + patch_dof(g, K, i));
+  __syncthreads();
+  if (!active) return;
+  const double* col = invT + (size_t)K * D * D + i;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int jj = 0;
+#pragma unroll 4
+  for (; jj + 3 < D; jj += 4) {
+    s0 = fma(__ldg(col + (size_t)jj * D), loc[p][jj], s0);
+    s1 = fma(__ldg(col + (size_t)(jj + 1) * D), loc[p][jj + 1], s1);
+    s2 = fma(__ldg(col + (size_t)(jj + 2) * D), loc[p][jj + 2], s2);
+    s3 = fma(__ldg(col + (size_t)(jj + 3) * D), loc[p][jj + 3], s3);
+  }
+  for (; jj < D; ++jj) s0 = fma(__ldg(col + (size_t)jj * D), loc[p][jj], s0);
+  upd[(size_t)K * D + i] = (s0 + s1) + (s2 + s3);
+}
+
+// d[dof] += omega * sum over patches containing dof of upd (node gather).
+__global__ void k_vanka_scatter(Geom g, int k1, const double* __restrict__ upd, double omega, double* __restrict__ d) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int mu = blockIdx.y;
+  const size_t nn = (size_t)g.nnx * g.nny;
+  const int D = 21 * k1;
+  double* dm = d + (size_t)mu * g.nd;
+  if (t < nn) {
+    const int X = (int)(t % g.nnx), Y = (int)(t / g.nnx);
+    double s0 = 0.0, s1 = 0.0;
+    for (int cy = max(0, (Y - 1) / 2); cy <= min(g.ny - 1, Y / 2); ++cy)
+      for (int cx = max(0, (X - 1) / 2); cx <= min(g.nx - 1, X / 2); ++cx) {
+        const int a = 3 * (Y - 2 * cy) + (X - 2 * cx);
+        const double* u = upd + ((size_t)cy * g.nx + cx) * D + 21 * mu + 2 * a;
+        s0 += u[0];
+        s1 += u[1];
+      }
+    dm[2 * t] += omega * s0;
+    dm[2 * t + 1] += omega * s1;
+  } else if (t < nn + (size_t)g.ncells) {
+    const size_t c = t - nn;
+    const double* u = upd + c * D + 21 * mu + 18;
+    double* o = dm + g.mv + 3 * c;
+    o[0] += omega * u[0];
+    o[1] += omega * u[1];
+    o[2] += omega * u[2];
+  }
+}
+
+template <int D>
+cudaError_t launch_invert(const double* mats, double* invT, int np, int* bad, cudaStream_t st) {
+  constexpr int WPB = inv_wpb<D>();
+  const size_t smem = (size_t)WPB * (D * (D + 1) + D) * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_invert<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  k_invert<D><<<(np + WPB - 1) / WPB, 32 * WPB, smem, st>>>(mats, invT, np, bad);
+  return cudaGetLastError();
+}
+
+template <int D>
+cudaError_t launch_gemv(const Geom& g, const double* invT, const double* defect, double* upd, cudaStream_t st) {
+  constexpr int PB = 256 / D;
+  k_vanka_gemv<D><<<(g.ncells + PB - 1) / PB, 256, 0, st>>>(g, invT, defect, upd);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t patch_assemble(const PatchArgs& a, cudaStream_t st) {
+  k_patch_fine<<<a.g.ncells, 448, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t patch_invert(int k1, const double* mats, double* invT, int npatch, int* bad, cudaStream_t st) {
+  switch (k1) {
+    case 1: return launch_invert<21>(mats, invT, npatch, bad, st);
+    case 2: return launch_invert<42>(mats, invT, npatch, bad, st);
+    case 3: return launch_invert<63>(mats, invT, npatch, bad, st);
+    case 4: return launch_invert<84>(mats, invT, npatch, bad, st);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+cudaError_t vanka_gemv(const Geom& g, int k1, const double* invT, const double* defect, double* upd, cudaStream_t st) {
+  switch (k1) {
+    case 1: return launch_gemv<21>(g, invT, defect, upd, st);
+    case 2: return launch_gemv<42>(g, invT, defect, upd, st);
+    case 3: return launch_gemv<63>(g, invT, defect, upd, st);
+    case 4: return launch_gemv<84>(g, invT, defect, upd, st);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+cudaError_t vanka_scatter(const Geom& g, int k1, const double* upd, double omega, double* d, cudaStream_t st) {
+  const size_t n = (size_t)g.nnx * g.nny + g.ncells;
+  dim3 grid((unsigned)((n + 255) / 256), k1);
+  k_vanka_scatter<<<grid, 256, 0, st>>>(g, k1, upd, omega, d);
+  return cudaGetLastError();
+}
+
+}  // namespace pdst

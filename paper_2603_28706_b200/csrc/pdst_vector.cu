@@ -138,11 +138,11 @@ struct Coef7 {
   double c[MAXK1];
 };
 
-__global__ void k_blend(Geom g, int k1, Coef7 cf, const double* __restrict__ U, double* __restrict__ V) {
+__global__ void k_blend(Geom g, int k1, Coef7 cf, const double* __restrict__ U, size_t stride, double* __restrict__ V) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (size_t)g.mv) return;
   double s = 0.0;
-  for (int mu = 0; mu < k1; ++mu) s = fma(cf.c[mu], U[(size_t)mu * g.nd + i], s);
+  for (int mu = 0; mu < k1; ++mu) s = fma(cf.c[mu], U[(size_t)mu * stride + i], s);
   V[i] = s;
 }
 
@@ -176,10 +176,11 @@ cudaError_t copy_velocity_blocks(const Geom& g, int k1, const double* U, double*
   return cudaGetLastError();
 }
 
-cudaError_t blend_velocity(const Geom& g, int k1, const double* coef, const double* U, double* V, cudaStream_t st) {
+cudaError_t blend_velocity(const Geom& g, int k1, const double* coef, const double* U, size_t stride, double* V,
+                           cudaStream_t st) {
   Coef7 cf{};
   for (int i = 0; i < k1 && i < MAXK1; ++i) cf.c[i] = coef[i];
-  k_blend<<<(unsigned)((g.mv + 255) / 256), 256, 0, st>>>(g, k1, cf, U, V);
+  k_blend<<<(unsigned)((g.mv + 255) / 256), 256, 0, st>>>(g, k1, cf, U, stride, V);
   return cudaGetLastError();
 }
 

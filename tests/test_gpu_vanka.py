@@ -1,0 +1,80 @@
+"""GPU parity of the Vanka patches (exact and surrogate) and sweeps against
+the reference golden vectors and the oracle.  Tolerance: relative 1e-12
+(L2 and Linf); patch index sets bit-exact."""
+
+import numpy as np
+import pytest
+
+from helpers import CASES, assert_close, load, oracle_slab, orc, product_ctx, product_variant, rel_err, variant_of
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+PATCH_CASES = [c for c in CASES if c.patches]
+
+
+@pytest.mark.parametrize("case", PATCH_CASES, ids=lambda c: c.name)
+def test_golden_patches_and_sweeps(case):
+    from paper_2603_28706_b200.smoother import VankaLevel, vanka_smooth
+
+    fx = load(case.name)
+    ctx = product_ctx(case, fx)
+    lvl = VankaLevel(ctx, fx["U"], product_variant(case), surrogate=case.surrogate,
+                     rep_fraction=case.cfg.rep_fraction)
+    assert np.array_equal(lvl.patch_ids(), fx["patch_ids"])
+    mats = lvl.patch_matrices()
+    worst = max(rel_err(mats[c], fx["patch_mats"][c])[0] for c in range(mats.shape[0]))
+    assert worst <= TOL, f"worst per-patch rel err {worst:.3e}"
+    om = case.cfg.omega
+    assert_close(vanka_smooth(lvl, fx["d0"], fx["x"], 1, om), fx["vanka_d"], TOL, "vanka 1 step")
+    assert_close(vanka_smooth(lvl, fx["d0"], fx["x"], 2, om), fx["vanka_d2"], TOL, "vanka 2 steps")
+    assert_close(vanka_smooth(lvl, 0 * fx["x"], fx["x"], 1, om), fx["vanka_zero"], TOL, "vanka from zero")
+
+
+@pytest.mark.parametrize("nx,ny,k,surrogate", [(20, 17, 1, True), (16, 31, 2, False), (24, 24, 0, True),
+                                               (17, 12, 3, True)])
+def test_oracle_parity_vanka_sizes(nx, ny, k, surrogate):
+    from test_gpu_operator import _sized_case
+
+    from paper_2603_28706_b200.smoother import VankaLevel, vanka_smooth
+
+    case, fx, syn = _sized_case(nx, ny, k, "exn")
+    ctx = product_ctx(case, fx)
+    s = oracle_slab(case, fx)
+    pre = orc.StmgOracle(s, syn.U, variant_of(case), surrogate=surrogate, rep_fraction=0.5, min_cells=max(nx, ny))
+    fine = pre.levels[-1]
+    lvl = VankaLevel(ctx, syn.U, product_variant(case), surrogate=surrogate, rep_fraction=0.5)
+    mats = lvl.patch_matrices()
+    worst = max(rel_err(mats[c], fine.mats[c])[0] for c in range(mats.shape[0]))
+    assert worst <= TOL, f"worst per-patch rel err {worst:.3e}"
+    assert_close(vanka_smooth(lvl, syn.d0, syn.x, 2, 0.7), orc.vanka(fine, syn.d0, syn.x, 2, 0.7), TOL, "vanka")
+
+
+def test_vanka_identities():
+    """omega = 0 is the identity; k = 0 surrogate == exact patches bitwise."""
+    from paper_2603_28706_b200.smoother import VankaLevel, vanka_smooth
+
+    case = [c for c in CASES if c.name == "p6_k0_exn"][0]
+    fx = load(case.name)
+    ctx = product_ctx(case, fx)
+    a = VankaLevel(ctx, fx["U"], product_variant(case), surrogate=True)
+    b = VankaLevel(ctx, fx["U"], product_variant(case), surrogate=False)
+    assert np.array_equal(a.patch_matrices(), b.patch_matrices())
+    d = vanka_smooth(a, fx["d0"], fx["x"], 3, 0.0)
+    assert np.array_equal(d, fx["d0"])
+
+
+def test_singular_patch_reported():
+    from paper_2603_28706_b200 import problem as pb
+    from paper_2603_28706_b200.errors import SingularPatchError
+    from paper_2603_28706_b200.smoother import VankaLevel
+
+    # Stokes-limit with viscosity switched off and no convection: the velocity
+    # blocks reduce to the tiny time-mass part only when tau is huge... use
+    # disabled viscous + convection + pressure so each patch is K_t (x) M on
+    # velocity and an all-zero pressure block -> exactly singular.
+    conf = pb.DiscretizationConfig(40.0, 40.0, 1.0, None, False, False, False)
+    ctx = pb.make_context(3, 3, 0, pb.ModelParams(1.5, 1e-2, 1.0, 0.0), 0.01, config=conf)
+    U = np.zeros((1, ctx.disc.ndof))
+    with pytest.raises(SingularPatchError) as ei:
+        VankaLevel(ctx, U, pb.picard())
+    assert ei.value.patch == 0
