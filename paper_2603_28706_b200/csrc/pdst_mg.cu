@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "../../include/pdst.h"
@@ -15,9 +17,23 @@
 
 using namespace pdst;
 
+// PDST_DEBUG_SYNC=1 synchronizes after every launch so a fault names its kernel.
+static bool debug_sync() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PDST_DEBUG_SYNC");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 #define CK(expr)                                                                               \
   do {                                                                                         \
     cudaError_t _e = (expr);                                                                   \
+    if (_e == cudaSuccess && debug_sync()) {                                                   \
+      _e = cudaDeviceSynchronize();                                                            \
+      fprintf(stderr, "[pdst] %s -> %s\n", #expr, cudaGetErrorString(_e));                    \
+    }                                                                                          \
     if (_e != cudaSuccess) return set_error(PDST_ECUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
   } while (0)
 
@@ -129,6 +145,7 @@ int pdst_patches_build(pdst_handle* h, int surrogate, double rep_fraction, int* 
   pa.nslot = surrogate ? 1 : k1;
   double* ET = h->ET.ensure((size_t)pa.nslot * nc * 441);
   if (!ET) return set_error(PDST_ECUDA, "out of device memory (element matrices)");
+  pa.ET = ET;
   if (rep) {
     // rep state = sum_mu l_mu(rep_fraction) U_mu (slab.py:105-112), linearized alone
     const std::vector<double> c = lagrange_at(h->nodes, rep_fraction);
