@@ -111,6 +111,8 @@ Geom make_geom(int nx, int ny, double x0, double y0, double x1, double y1, const
   g.nbf = 2 * (nx + ny);
   g.hx = (x1 - x0) / nx;
   g.hy = (y1 - y0) / ny;
+  g.ihx = 1.0 / g.hx;
+  g.ihy = 1.0 / g.hy;
   g.dirichlet = dirichlet_dev;
   return g;
 }

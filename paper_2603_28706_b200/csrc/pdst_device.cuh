@@ -46,6 +46,7 @@ struct Geom {
   int mv, nd;    // velocity dofs, dofs per node block
   int nbf;       // boundary faces 2 (nx + ny)
   double hx, hy;
+  double ihx, ihy;           // 1/hx, 1/hy (the reference's grad_scale, femspace.py:142-143)
   const uint8_t* dirichlet;  // nbf flags (device)
 };
 

@@ -34,18 +34,59 @@ constexpr int CY = TY + 1;
 constexpr int NT = CX * CY;      // threads per CTA
 constexpr int NC = 2 * (TX + 3) + 1;  // staged node columns
 constexpr int NR = 2 * (TY + 3) + 1;  // staged node rows
-constexpr int PLANE = NR * NC;
+constexpr int NC2 = (NC + 1) / 2;     // columns per parity half-row
+constexpr int RS = 2 * NC2;           // staged row stride
+constexpr int PLANE = NR * RS;
+
+// Staged node plane: each row holds the even node columns then the odd ones,
+// so threads of consecutive cells (node columns 2tx+{0,1,2}) read
+// consecutive doubles (conflict-free 64-bit shared loads).
+__host__ __device__ constexpr int pidx(int r, int c) { return r * RS + (c & 1) * NC2 + (c >> 1); }
 
 struct Plane2 {
   const double* p0;  // component 0
   const double* p1;  // component 1
-  __device__ double at(int d, int r, int c) const { return (d == 0 ? p0 : p1)[r * NC + c]; }
+  __device__ double at(int d, int r, int c) const { return (d == 0 ? p0 : p1)[pidx(r, c)]; }
 };
+
+// Accumulators for the cell's 9-node velocity contributions: registers (the
+// element-matrix kernel, the volume phase) or the thread's shared-memory slot
+// (structure of arrays over the CTA's threads, stride NT).
+struct RegAcc {
+  double (*a)[3][2];
+  __device__ __forceinline__ void add(int jy, int ix, int d, double v) const { a[jy][ix][d] += v; }
+};
+struct SmemAcc {
+  double* p;
+  __device__ __forceinline__ void add(int jy, int ix, int d, double v) const { p[(2 * (3 * jy + ix) + d) * NT] += v; }
+};
+
+// Asynchronous 8-byte global->shared copy (LDGSTS); size 0 zero-fills.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  const int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Issue the asynchronous staging of one velocity block (zero outside the
+// domain); the caller waits with cp_async_wait_all() + __syncthreads().
+__device__ __forceinline__ void stage_velocity_async(const Geom& g, const double* __restrict__ v, double* pl0,
+                                                     double* pl1, int X0, int Y0) {
+  for (int idx = threadIdx.x; idx < NR * NC; idx += blockDim.x) {
+    const int r = idx / NC, c = idx - r * NC;
+    const int X = X0 + c, Y = Y0 + r;
+    const bool in = X >= 0 && X < g.nnx && Y >= 0 && Y < g.nny;
+    const double* src = in ? v + 2 * ((size_t)Y * g.nnx + X) : v;
+    cp_async8(pl0 + pidx(r, c), src, in);
+    cp_async8(pl1 + pidx(r, c), in ? src + 1 : v, in);
+  }
+}
 
 // Stage one slab block's velocity into two shared planes (zero outside the domain).
 __device__ void stage_velocity(const Geom& g, const double* __restrict__ v, double* pl0, double* pl1, int X0,
                                int Y0) {
-  for (int idx = threadIdx.x; idx < PLANE; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < NR * NC; idx += blockDim.x) {
     const int r = idx / NC, c = idx - r * NC;
     const int X = X0 + c, Y = Y0 + r;
     double a = 0.0, b = 0.0;
@@ -54,8 +95,8 @@ __device__ void stage_velocity(const Geom& g, const double* __restrict__ v, doub
       a = __ldg(v + o);
       b = __ldg(v + o + 1);
     }
-    pl0[idx] = a;
-    pl1[idx] = b;
+    pl0[pidx(r, c)] = a;
+    pl1[pidx(r, c)] = b;
   }
 }
 
@@ -89,8 +130,9 @@ __device__ __forceinline__ void side_info(int side, int& axis, int& e, double& n
 
 // Scatter face accumulators RE (value/tangential tests) and RD (normal
 // derivative tests) to the cell's 9 nodes.
+template <class ACC>
 __device__ __forceinline__ void face_scatter(int axis, int e, const double RE[3][2], const double RD[3][2],
-                                             double acc[3][3][2]) {
+                                             const ACC& acc) {
 #pragma unroll
   for (int n = 0; n < 3; ++n) {
     const double en = c_tab.E[e][n], dn = c_tab.dE[e][n];
@@ -100,52 +142,54 @@ __device__ __forceinline__ void face_scatter(int axis, int e, const double RE[3]
       for (int d = 0; d < 2; ++d) {
         const double v = en * RE[t][d] + dn * RD[t][d];
         if (axis == 0)
-          acc[t][n][d] += v;
+          acc.add(t, n, d, v);
         else
-          acc[n][t][d] += v;
+          acc.add(n, t, d, v);
       }
     }
   }
 }
 
-// Own-side half of the CIP term of one interior face of the cell
-// (forms.py:639-650); sgn = +1 for the Jacobian, -1 for the residual
-// (forms.py:415-432).  F = field whose normal-derivative jump is penalised,
-// A = lagged advective field (weights), both staged.
+// CIP face term (forms.py:639-650 / 415-432), computed ONCE per interior face:
+// RD[t][d] = gamma_cip h^2 / hn^2 * sum_q (w_q h) |a_L . n| jump_d(q) B[q][t]
+// where jump = d_n u|_L - d_n u|_R (n = +x for axis 0, +y for axis 1) and the
+// weight uses the lagged advective trace of the left/lower cell.  The left /
+// lower cell adds +dE(1) (x) RD to its nodes, the right / upper cell
+// -dE(0) (x) RD (cip_scatter).  (rL, cL) = staged origin of the left block.
 template <class FA, class AA>
-__device__ void cip_side(const Geom& g, const Disc& ds, int side, const FA& F, const AA& A, int r0, int c0,
-                         double sgn, double acc[3][3][2]) {
-  int axis, e_own, dummy_e;
-  double n0, n1;
-  side_info(side, axis, dummy_e, n0, n1);
-  e_own = dummy_e;
-  const int e_nbr = 1 - e_own;
-  // neighbour block origin
-  int rn = r0, cn = c0;
-  if (side == 0) rn -= 2;
-  if (side == 2) rn += 2;
-  if (side == 1) cn += 2;
-  if (side == 3) cn -= 2;
+__device__ __forceinline__ void cip_face(const Geom& g, const Disc& ds, int axis, const FA& F, const AA& A, int rL,
+                                         int cL, double RD[3][2], double scale = 1.0) {
+  const int rR = axis == 1 ? rL + 2 : rL, cR = axis == 0 ? cL + 2 : cL;
   const double hface = axis == 0 ? g.hy : g.hx;
-  const double hnorm = axis == 0 ? g.hx : g.hy;
-  double own[3][2], nbr[3][2], tr[3][2];
-  line_sums(F, r0, c0, axis, c_tab.dE[e_own], own);
-  line_sums(F, rn, cn, axis, c_tab.dE[e_nbr], nbr);
-  line_sums(A, r0, c0, axis, c_tab.E[e_own], tr);
-  const double coef = sgn * ds.gamma_cip * hface * hface;
-  double RD[3][2] = {{0, 0}, {0, 0}, {0, 0}};
-  const double RE[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+  const double ihn = axis == 0 ? g.ihx : g.ihy;
+  double dl[3][2], dr[3][2];
+  line_sums(F, rL, cL, axis, c_tab.dE[1], dl);
+  line_sums(F, rR, cR, axis, c_tab.dE[0], dr);
+  double tr[3];
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    double v = 0.0;
+#pragma unroll
+    for (int n = 0; n < 3; ++n)
+      v = fma(c_tab.E[1][n], axis == 0 ? A.at(0, rL + t, cL + n) : A.at(1, rL + n, cL + t), v);
+    tr[t] = v;
+    dl[t][0] -= dr[t][0];
+    dl[t][1] -= dr[t][1];
+  }
+  const double coef = scale * ds.gamma_cip * hface * hface * (ihn * ihn);
+#pragma unroll
+  for (int t = 0; t < 3; ++t) RD[t][0] = RD[t][1] = 0.0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     double vt = 0.0, j0 = 0.0, j1 = 0.0;
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
       const double b = c_tab.B[q][t];
-      vt = fma(b, tr[t][axis], vt);
-      j0 = fma(b, own[t][0] - nbr[t][0], j0);
-      j1 = fma(b, own[t][1] - nbr[t][1], j1);
+      vt = fma(b, tr[t], vt);
+      j0 = fma(b, dl[t][0], j0);
+      j1 = fma(b, dl[t][1], j1);
     }
-    const double wgt = coef * (c_tab.w[q] * hface) * fabs(vt) / (hnorm * hnorm);
+    const double wgt = coef * (c_tab.w[q] * hface) * fabs(vt);
     const double c0v = wgt * j0, c1v = wgt * j1;
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
@@ -153,7 +197,96 @@ __device__ void cip_side(const Geom& g, const Disc& ds, int side, const FA& F, c
       RD[t][1] = fma(c1v, c_tab.B[q][t], RD[t][1]);
     }
   }
-  face_scatter(axis, e_own, RE, RD, acc);
+}
+
+// acc(n,t) += sgn * f(n) RD[t] with f = dE(1) for the left/lower cell, -dE(0) for the right/upper one.
+template <class ACC>
+__device__ __forceinline__ void cip_scatter(int axis, bool left, double sgn, const double RD[3][2], const ACC& acc) {
+#pragma unroll
+  for (int n = 0; n < 3; ++n) {
+    const double f = sgn * (left ? c_tab.dE[1][n] : -c_tab.dE[0][n]);
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      if (axis == 0) {
+        acc.add(t, n, 0, f * RD[t][0]);
+        acc.add(t, n, 1, f * RD[t][1]);
+      } else {
+        acc.add(n, t, 0, f * RD[t][0]);
+        acc.add(n, t, 1, f * RD[t][1]);
+      }
+    }
+  }
+}
+
+// Own CIP faces of a computed cell: the right and upper faces (shared with the
+// neighbour through fR/fT), plus the left / lower faces of the halo column /
+// row whose left neighbour is outside the tile.
+template <class FA, class AA, class ACC>
+__device__ __forceinline__ void cip_own(const Geom& g, const Disc& ds, const FA& F, const AA& A, int ci, int cj,
+                                        int tx, int ty, int r0, int c0, double sgn, double* fR, double* fT,
+                                        const ACC& acc) {
+  double RD[3][2];
+  if (ci < g.nx - 1) {
+    cip_face(g, ds, 0, F, A, r0, c0, RD);
+    cip_scatter(0, true, sgn, RD, acc);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) fR[k * NT + threadIdx.x] = RD[k / 2][k % 2];
+  }
+  if (cj < g.ny - 1) {
+    cip_face(g, ds, 1, F, A, r0, c0, RD);
+    cip_scatter(1, true, sgn, RD, acc);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) fT[k * NT + threadIdx.x] = RD[k / 2][k % 2];
+  }
+  if (tx == 0 && ci > 0) {
+    cip_face(g, ds, 0, F, A, r0, c0 - 2, RD);
+    cip_scatter(0, false, sgn, RD, acc);
+  }
+  if (ty == 0 && cj > 0) {
+    cip_face(g, ds, 1, F, A, r0 - 2, c0, RD);
+    cip_scatter(1, false, sgn, RD, acc);
+  }
+}
+
+// All four CIP faces of a cell, own side only (no exchange): the face jump is
+// evaluated from the staged neighbour block.  `scale` multiplies the term.
+template <class FA, class AA, class ACC>
+__device__ __forceinline__ void cip_all(const Geom& g, const Disc& ds, const FA& F, const AA& A, int ci, int cj, int r0,
+                                        int c0, double scale, const ACC& acc) {
+  double RD[3][2];
+  if (ci < g.nx - 1) {
+    cip_face(g, ds, 0, F, A, r0, c0, RD, scale);
+    cip_scatter(0, true, 1.0, RD, acc);
+  }
+  if (cj < g.ny - 1) {
+    cip_face(g, ds, 1, F, A, r0, c0, RD, scale);
+    cip_scatter(1, true, 1.0, RD, acc);
+  }
+  if (ci > 0) {
+    cip_face(g, ds, 0, F, A, r0, c0 - 2, RD, scale);
+    cip_scatter(0, false, 1.0, RD, acc);
+  }
+  if (cj > 0) {
+    cip_face(g, ds, 1, F, A, r0 - 2, c0, RD, scale);
+    cip_scatter(1, false, 1.0, RD, acc);
+  }
+}
+
+// After a barrier: the left / lower faces computed by the neighbour thread.
+template <class ACC>
+__device__ __forceinline__ void cip_received(const Geom& g, int ci, int cj, int tx, int ty, double sgn,
+                                             const double* fR, const double* fT, const ACC& acc) {
+  double RD[3][2];
+  if (tx >= 1 && ci > 0) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) RD[k / 2][k % 2] = fR[k * NT + threadIdx.x - 1];
+    cip_scatter(0, false, sgn, RD, acc);
+  }
+  if (ty >= 1 && cj > 0) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) RD[k / 2][k % 2] = fT[k * NT + threadIdx.x - CX];
+    cip_scatter(1, false, sgn, RD, acc);
+  }
 }
 
 // Evaluate a staged field on a boundary side at face point q:
@@ -162,7 +295,7 @@ struct FaceLines {
   double E[3][2], D[3][2];
 };
 
-__device__ __forceinline__ void face_point(const FaceLines& L, int axis, int q, double htan, double hnorm, double u[2],
+__device__ __forceinline__ void face_point(const FaceLines& L, int axis, int q, double ihtan, double ihnorm, double u[2],
                                            double ux[2], double uy[2]) {
 #pragma unroll
   for (int d = 0; d < 2; ++d) {
@@ -175,25 +308,27 @@ __device__ __forceinline__ void face_point(const FaceLines& L, int axis, int q, 
     }
     u[d] = v;
     if (axis == 0) {
-      ux[d] = dn / hnorm;
-      uy[d] = dt / htan;
+      ux[d] = dn * ihnorm;
+      uy[d] = dt * ihtan;
     } else {
-      ux[d] = dt / htan;
-      uy[d] = dn / hnorm;
+      ux[d] = dt * ihtan;
+      uy[d] = dn * ihnorm;
     }
   }
 }
 
 // Jacobian boundary-side terms of one cell side (forms.py:605-637).
-template <class XA, class SA>
-__device__ void jac_boundary_side(const Geom& g, const Disc& ds, const Lin& L, int mu, int side, int bf,
+template <class XA, class SA, class ACC>
+__device__ __noinline__ void jac_boundary_side(const Geom& g, const Disc& ds, const Lin& L, int mu, int side, int bf,
                                   const XA& X, const SA& S, int r0, int c0, const double P[3],
-                                  double acc[3][3][2], double accp[3]) {
+                                  const ACC& acc, double accp[3], double tw) {
   int axis, e;
   double n0, n1;
   side_info(side, axis, e, n0, n1);
   const double htan = axis == 0 ? g.hy : g.hx;
-  const double hnorm = axis == 0 ? g.hx : g.hy;
+  const double ihtan = axis == 0 ? g.ihy : g.ihx;
+  const double ihnorm = axis == 0 ? g.ihx : g.ihy;
+  const double pen1 = ds.gamma1 / htan, pen2 = ds.gamma2 / htan;
   FaceLines LU, LV;
   line_sums(X, r0, c0, axis, c_tab.E[e], LU.E);
   line_sums(X, r0, c0, axis, c_tab.dE[e], LU.D);
@@ -202,10 +337,10 @@ __device__ void jac_boundary_side(const Geom& g, const Disc& ds, const Lin& L, i
   const bool dm = g.dirichlet[bf] != 0;
   double RE[3][2] = {{0, 0}, {0, 0}, {0, 0}}, RD[3][2] = {{0, 0}, {0, 0}, {0, 0}};
   for (int q = 0; q < 4; ++q) {
-    const double wq = c_tab.w[q] * htan;
+    const double wq = c_tab.w[q] * htan * tw;
     double u[2], ux[2], uy[2], v[2], vx[2], vy[2];
-    face_point(LU, axis, q, htan, hnorm, u, ux, uy);
-    face_point(LV, axis, q, htan, hnorm, v, vx, vy);
+    face_point(LU, axis, q, ihtan, ihnorm, u, ux, uy);
+    face_point(LV, axis, q, ihtan, ihnorm, v, vx, vy);
     const double vn = v[0] * n0 + v[1] * n1;
     const double un = u[0] * n0 + u[1] * n1;
     double Cv[2] = {0, 0}, Cgx[2] = {0, 0}, Cgy[2] = {0, 0};
@@ -233,7 +368,7 @@ __device__ void jac_boundary_side(const Geom& g, const Disc& ds, const Lin& L, i
         Cgx[1] -= 0.5 * ed * (n0 * u[1] + u[0] * n1) + bd * dgnu * g2;
         Cgy[0] -= 0.5 * ed * (n1 * u[0] + u[1] * n0) + bd * dgnu * g2;
         Cgy[1] -= 0.5 * ed * (n1 * u[1] + u[1] * n1) + bd * dgnu * g1;
-        const double p1 = ds.gamma1 / htan * ed, p2 = ds.gamma2 / htan * un;
+        const double p1 = pen1 * ed, p2 = pen2 * un;
         Cv[0] += p1 * u[0] + p2 * n0;
         Cv[1] += p1 * u[1] + p2 * n1;
       }
@@ -259,8 +394,8 @@ __device__ void jac_boundary_side(const Geom& g, const Disc& ds, const Lin& L, i
     for (int t = 0; t < 3; ++t) {
 #pragma unroll
       for (int d = 0; d < 2; ++d) {
-        RE[t][d] += wq * (Cv[d] * c_tab.B[q][t] + Ct[d] * c_tab.G[q][t] / htan);
-        RD[t][d] += wq * (Cn[d] * c_tab.B[q][t] / hnorm);
+        RE[t][d] += wq * (Cv[d] * c_tab.B[q][t] + Ct[d] * (c_tab.G[q][t] * ihtan));
+        RD[t][d] += wq * (Cn[d] * (c_tab.B[q][t] * ihnorm));
       }
     }
   }
@@ -269,14 +404,17 @@ __device__ void jac_boundary_side(const Geom& g, const Disc& ds, const Lin& L, i
 
 // Residual boundary-side terms (forms.py:474-507) plus, when a lifting is
 // present, the Nitsche vector B_gamma(g_hat, .) of forms.py:374-412.
-__device__ void res_boundary_side(const Geom& g, const Disc& ds, const Model& m, const Lin& L, int side, int bf,
+template <class ACC>
+__device__ __noinline__ void res_boundary_side(const Geom& g, const Disc& ds, const Model& m, const Lin& L, int side, int bf,
                                   const Plane2& S, const Plane2& A, int r0, int c0, const double PI[3],
-                                  const double* ghat_nodes /*9x2 or null*/, double acc[3][3][2], double accp[3]) {
+                                  const double* ghat_nodes /*9x2 or null*/, const ACC& acc, double accp[3]) {
   int axis, e;
   double n0, n1;
   side_info(side, axis, e, n0, n1);
   const double htan = axis == 0 ? g.hy : g.hx;
-  const double hnorm = axis == 0 ? g.hx : g.hy;
+  const double ihtan = axis == 0 ? g.ihy : g.ihx;
+  const double ihnorm = axis == 0 ? g.ihx : g.ihy;
+  const double pen1 = ds.gamma1 / htan, pen2 = ds.gamma2 / htan;
   FaceLines LV, LA;
   line_sums(S, r0, c0, axis, c_tab.E[e], LV.E);
   line_sums(S, r0, c0, axis, c_tab.dE[e], LV.D);
@@ -302,8 +440,8 @@ __device__ void res_boundary_side(const Geom& g, const Disc& ds, const Model& m,
   for (int q = 0; q < 4; ++q) {
     const double wq = c_tab.w[q] * htan;
     double v[2], vx[2], vy[2], a[2], ax_[2], ay_[2];
-    face_point(LV, axis, q, htan, hnorm, v, vx, vy);
-    face_point(LA, axis, q, htan, hnorm, a, ax_, ay_);
+    face_point(LV, axis, q, ihtan, ihnorm, v, vx, vy);
+    face_point(LA, axis, q, ihtan, ihnorm, a, ax_, ay_);
     const double vn = v[0] * n0 + v[1] * n1;
     double Cv[2] = {0, 0}, Cgx[2] = {0, 0}, Cgy[2] = {0, 0};
     if (ds.convection) {
@@ -325,7 +463,7 @@ __device__ void res_boundary_side(const Geom& g, const Disc& ds, const Model& m,
         Cgx[1] += 0.5 * ed * (n0 * v[1] + v[0] * n1) + bd * dgnv * g2;
         Cgy[0] += 0.5 * ed * (n1 * v[0] + v[1] * n0) + bd * dgnv * g2;
         Cgy[1] += 0.5 * ed * (n1 * v[1] + v[1] * n1) + bd * dgnv * g1;
-        const double p1 = ds.gamma1 / htan * ed, p2 = ds.gamma2 / htan * vn;
+        const double p1 = pen1 * ed, p2 = pen2 * vn;
         Cv[0] -= p1 * v[0] + p2 * n0;
         Cv[1] -= p1 * v[1] + p2 * n1;
       }
@@ -361,7 +499,7 @@ __device__ void res_boundary_side(const Geom& g, const Disc& ds, const Model& m,
           Cgx[1] -= 0.5 * ed * (n0 * gv[1] + gv[0] * n1) + bd * dgng * g2;
           Cgy[0] -= 0.5 * ed * (n1 * gv[0] + gv[1] * n0) + bd * dgng * g2;
           Cgy[1] -= 0.5 * ed * (n1 * gv[1] + gv[1] * n1) + bd * dgng * g1;
-          const double p1 = ds.gamma1 / htan * ed, p2 = ds.gamma2 / htan * gn;
+          const double p1 = pen1 * ed, p2 = pen2 * gn;
           Cv[0] += p1 * gv[0] + p2 * n0;
           Cv[1] += p1 * gv[1] + p2 * n1;
         }
@@ -383,8 +521,8 @@ __device__ void res_boundary_side(const Geom& g, const Disc& ds, const Model& m,
     for (int t = 0; t < 3; ++t) {
 #pragma unroll
       for (int d = 0; d < 2; ++d) {
-        RE[t][d] += wq * (Cv[d] * c_tab.B[q][t] + Ct[d] * c_tab.G[q][t] / htan);
-        RD[t][d] += wq * (Cn[d] * c_tab.B[q][t] / hnorm);
+        RE[t][d] += wq * (Cv[d] * c_tab.B[q][t] + Ct[d] * (c_tab.G[q][t] * ihtan));
+        RD[t][d] += wq * (Cn[d] * (c_tab.B[q][t] * ihnorm));
       }
     }
   }
@@ -403,9 +541,9 @@ __device__ __forceinline__ void row_sums(const FA& F, int r, int c0, int qx, dou
 }
 
 // acc += s * (M1 (x) M1) XT for the cell, XT = sum_nu K_t[mu,nu] F_nu - mfac * Fm.
-template <int K1>
+template <int K1, class ACC>
 __device__ __forceinline__ void add_mass(const Plane2* F, const Plane2* Fm, double mfac, const double* Krow, int r0,
-                                         int c0, double s, double acc[3][3][2]) {
+                                         int c0, double s, const ACC& acc) {
 #pragma unroll
   for (int jj = 0; jj < 3; ++jj) {  // source row jy'
     double T1[3][2];
@@ -431,7 +569,67 @@ __device__ __forceinline__ void add_mass(const Plane2* F, const Plane2* Fm, doub
 #pragma unroll
       for (int i = 0; i < 3; ++i)
 #pragma unroll
-        for (int d = 0; d < 2; ++d) acc[jy][i][d] = fma(m, T1[i][d], acc[jy][i][d]);
+        for (int d = 0; d < 2; ++d) acc.add(jy, i, d, m * T1[i][d]);
+    }
+  }
+}
+
+// acc += s * (M1 (x) M1) F on the cell's 9 nodes of one staged plane pair.
+template <class ACC>
+__device__ __forceinline__ void add_mass_plane(const Plane2& F, int r0, int c0, double s, const ACC& acc) {
+#pragma unroll
+  for (int jj = 0; jj < 3; ++jj) {
+    double T1[3][2];
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      const double f0 = F.at(d, r0 + jj, c0), f1 = F.at(d, r0 + jj, c0 + 1), f2 = F.at(d, r0 + jj, c0 + 2);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) T1[i][d] = c_tab.M1[i][0] * f0 + c_tab.M1[i][1] * f1 + c_tab.M1[i][2] * f2;
+    }
+#pragma unroll
+    for (int jy = 0; jy < 3; ++jy) {
+      const double m = s * c_tab.M1[jy][jj];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int d = 0; d < 2; ++d) acc.add(jy, i, d, m * T1[i][d]);
+    }
+  }
+}
+
+// acc += s * (M1 (x) M1) (sum_nu K_t[mu,nu] x_nu) with the cell's nodal x_nu
+// read from global memory (L1) — the temporal coupling of slab.py:199-200.
+template <int K1, class ACC>
+__device__ __forceinline__ void add_mass_global(const double* __restrict__ x, size_t stride, int nnx, int X0, int Y0,
+                                                const double* Krow, double s, const ACC& acc) {
+#pragma unroll
+  for (int jj = 0; jj < 3; ++jj) {
+    double xt[3][2];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const size_t o = 2 * ((size_t)(Y0 + jj) * nnx + X0 + i);
+      double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+      for (int nu = 0; nu < K1; ++nu) {
+        v0 = fma(Krow[nu], __ldg(x + nu * stride + o), v0);
+        v1 = fma(Krow[nu], __ldg(x + nu * stride + o + 1), v1);
+      }
+      xt[i][0] = v0;
+      xt[i][1] = v1;
+    }
+    double T1[3][2];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int d = 0; d < 2; ++d)
+        T1[i][d] = c_tab.M1[i][0] * xt[0][d] + c_tab.M1[i][1] * xt[1][d] + c_tab.M1[i][2] * xt[2][d];
+#pragma unroll
+    for (int jy = 0; jy < 3; ++jy) {
+      const double m = s * c_tab.M1[jy][jj];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int d = 0; d < 2; ++d) acc.add(jy, i, d, m * T1[i][d]);
     }
   }
 }
@@ -440,14 +638,37 @@ __device__ __forceinline__ void add_mass(const Plane2* F, const Plane2* Fm, doub
 // CIP faces, the temporal mass and the tau w_mu scaling.  XA / SA are field
 // accessors (shared-memory planes in the apply, unit vectors / global memory
 // in the element-matrix kernel).  forms.py:589-637.
-template <class XA, class SA>
-__device__ __forceinline__ void jac_cell_local(const Geom& g, const Disc& ds, const Lin& L, int mu, int c, int ci,
-                                               int cj, const XA& XM, const SA& SP, int r0, int c0, const double P[3],
-                                               double acc[3][3][2], double accp[3]) {
-  const double W = g.hx * g.hy;
+template <class XA, class SA, class ACC>
+__device__ __forceinline__ void jac_volume(const Geom& g, const Disc& ds, const Lin& L, int mu, int c,
+                                           const XA& XM, const SA& SP, int r0, int c0, const double P[3],
+                                           const ACC& acc, double accp[3], double tw = 1.0) {
+  const double W = g.hx * g.hy * tw;
+  // eta / gamma of the next Gauss column are loaded one column ahead
+  const double* pe = L.eta + (size_t)mu * 16 * g.ncells + c;
+  const double* pg = L.gam + (size_t)mu * 16 * g.ncells + c;
+  const bool vis = ds.viscous, hg = L.has_gamma && ds.viscous;
+  double en[4], gn[4];
+#pragma unroll
+  for (int qy = 0; qy < 4; ++qy) {
+    en[qy] = vis ? __ldg(pe + (size_t)qy * g.ncells) : 0.0;
+    gn[qy] = hg ? __ldg(pg + (size_t)qy * g.ncells) : 0.0;
+  }
       // ---- volume (forms.py:589-603) ----
 #pragma unroll 1
       for (int qx = 0; qx < 4; ++qx) {
+        double ec[4], gc[4];
+#pragma unroll
+        for (int qy = 0; qy < 4; ++qy) {
+          ec[qy] = en[qy];
+          gc[qy] = gn[qy];
+        }
+        if (qx < 3) {
+#pragma unroll
+          for (int qy = 0; qy < 4; ++qy) {
+            en[qy] = vis ? __ldg(pe + (size_t)(4 * (qx + 1) + qy) * g.ncells) : 0.0;
+            gn[qy] = hg ? __ldg(pg + (size_t)(4 * (qx + 1) + qy) * g.ncells) : 0.0;
+          }
+        }
         double xB[3][2], xG[3][2], sB[3][2], sG[3][2];
 #pragma unroll
         for (int jy = 0; jy < 3; ++jy) {
@@ -462,19 +683,18 @@ __device__ __forceinline__ void jac_cell_local(const Geom& g, const Disc& ds, co
 #pragma unroll
           for (int d = 0; d < 2; ++d) {
             u[d] = c_tab.B[qy][0] * xB[0][d] + c_tab.B[qy][1] * xB[1][d] + c_tab.B[qy][2] * xB[2][d];
-            ux[d] = (c_tab.B[qy][0] * xG[0][d] + c_tab.B[qy][1] * xG[1][d] + c_tab.B[qy][2] * xG[2][d]) / g.hx;
-            uy[d] = (c_tab.G[qy][0] * xB[0][d] + c_tab.G[qy][1] * xB[1][d] + c_tab.G[qy][2] * xB[2][d]) / g.hy;
+            ux[d] = (c_tab.B[qy][0] * xG[0][d] + c_tab.B[qy][1] * xG[1][d] + c_tab.B[qy][2] * xG[2][d]) * g.ihx;
+            uy[d] = (c_tab.G[qy][0] * xB[0][d] + c_tab.G[qy][1] * xB[1][d] + c_tab.G[qy][2] * xB[2][d]) * g.ihy;
             v[d] = c_tab.B[qy][0] * sB[0][d] + c_tab.B[qy][1] * sB[1][d] + c_tab.B[qy][2] * sB[2][d];
-            vx[d] = (c_tab.B[qy][0] * sG[0][d] + c_tab.B[qy][1] * sG[1][d] + c_tab.B[qy][2] * sG[2][d]) / g.hx;
-            vy[d] = (c_tab.G[qy][0] * sB[0][d] + c_tab.G[qy][1] * sB[1][d] + c_tab.G[qy][2] * sB[2][d]) / g.hy;
+            vx[d] = (c_tab.B[qy][0] * sG[0][d] + c_tab.B[qy][1] * sG[1][d] + c_tab.B[qy][2] * sG[2][d]) * g.ihx;
+            vy[d] = (c_tab.G[qy][0] * sB[0][d] + c_tab.G[qy][1] * sB[1][d] + c_tab.G[qy][2] * sB[2][d]) * g.ihy;
           }
           const int q = 4 * qx + qy;
           const double wq = c_tab.w[qx] * c_tab.w[qy] * W;
           double Fx0 = 0, Fx1 = 0, Fy0 = 0, Fy1 = 0;
           if (ds.viscous) {
-            const size_t ci_ = ((size_t)mu * 16 + q) * g.ncells + c;
-            const double eta = __ldg(L.eta + ci_);
-            const double gam = L.has_gamma ? __ldg(L.gam + ci_) : 0.0;
+            const double eta = ec[qy];
+            const double gam = gc[qy];
             const double a0 = vx[0], a1 = vy[1], a2 = 0.5 * (vy[0] + vx[1]);
             const double b0 = ux[0], b1 = uy[1], b2 = 0.5 * (uy[0] + ux[1]);
             const double ab = a0 * b0 + a1 * b1 + 2.0 * a2 * b2;
@@ -512,14 +732,20 @@ __device__ __forceinline__ void jac_cell_local(const Geom& g, const Disc& ds, co
           for (int ix = 0; ix < 3; ++ix)
 #pragma unroll
             for (int d = 0; d < 2; ++d)
-              acc[jy][ix][d] += c_tab.G[qx][ix] / g.hx * Pa[jy][d] + c_tab.B[qx][ix] / g.hy * Qa[jy][d];
+              acc.add(jy, ix, d, (c_tab.G[qx][ix] * g.ihx) * Pa[jy][d] + (c_tab.B[qx][ix] * g.ihy) * Qa[jy][d]);
       }
-      // ---- boundary sides (forms.py:605-637) ----
+}
+
+// The cell's boundary sides (forms.py:605-637).
+template <class XA, class SA, class ACC>
+__device__ __forceinline__ void jac_sides(const Geom& g, const Disc& ds, const Lin& L, int mu, int ci, int cj,
+                                          const XA& XM, const SA& SP, int r0, int c0, const double P[3],
+                                          const ACC& acc, double accp[3], double tw = 1.0) {
       if (ci == 0 || cj == 0 || ci == g.nx - 1 || cj == g.ny - 1) {
-        if (cj == 0) jac_boundary_side(g, ds, L, mu, 0, side_offset(g, 0) + ci, XM, SP, r0, c0, P, acc, accp);
-        if (ci == g.nx - 1) jac_boundary_side(g, ds, L, mu, 1, side_offset(g, 1) + cj, XM, SP, r0, c0, P, acc, accp);
-        if (cj == g.ny - 1) jac_boundary_side(g, ds, L, mu, 2, side_offset(g, 2) + ci, XM, SP, r0, c0, P, acc, accp);
-        if (ci == 0) jac_boundary_side(g, ds, L, mu, 3, side_offset(g, 3) + cj, XM, SP, r0, c0, P, acc, accp);
+        if (cj == 0) jac_boundary_side(g, ds, L, mu, 0, side_offset(g, 0) + ci, XM, SP, r0, c0, P, acc, accp, tw);
+        if (ci == g.nx - 1) jac_boundary_side(g, ds, L, mu, 1, side_offset(g, 1) + cj, XM, SP, r0, c0, P, acc, accp, tw);
+        if (cj == g.ny - 1) jac_boundary_side(g, ds, L, mu, 2, side_offset(g, 2) + ci, XM, SP, r0, c0, P, acc, accp, tw);
+        if (ci == 0) jac_boundary_side(g, ds, L, mu, 3, side_offset(g, 3) + cj, XM, SP, r0, c0, P, acc, accp, tw);
       }
 }
 
@@ -532,7 +758,25 @@ __device__ void assemble_and_store(const Geom& g, const double* sacc, int i0, in
   const int wx = lxe - 2, wy = lye - 2;  // owned local nodes start at 2
   const int n = wx * wy;
   const size_t base = (size_t)mu * g.nd;
-  for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+  constexpr int MAXIT = ((2 * TX + 1) * (2 * TY + 1) + NT - 1) / NT;
+  double r0v[MAXIT], r1v[MAXIT];
+  if (rhs) {
+#pragma unroll
+    for (int it = 0; it < MAXIT; ++it) {
+      const int idx = threadIdx.x + it * NT;
+      r0v[it] = r1v[it] = 0.0;
+      if (idx < n) {
+        const int ly = 2 + idx / wx, lx = 2 + idx % wx;
+        const size_t o = base + 2 * ((size_t)(2 * (j0 - 1) + ly) * g.nnx + 2 * (i0 - 1) + lx);
+        r0v[it] = __ldg(rhs + o);
+        r1v[it] = __ldg(rhs + o + 1);
+      }
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < MAXIT; ++it) {
+    const int idx = threadIdx.x + it * NT;
+    if (idx >= n) break;
     const int ly = 2 + idx / wx, lx = 2 + idx % wx;
     double s0 = 0.0, s1 = 0.0;
     const int cxa = (lx & 1) ? (lx - 1) / 2 : lx / 2 - 1;
@@ -544,16 +788,16 @@ __device__ void assemble_and_store(const Geom& g, const double* sacc, int i0, in
       for (int cx = cxa; cx <= cxb; ++cx) {
         if (cx < 0 || cx >= CX) continue;
         const int a = 3 * (ly - 2 * cy) + (lx - 2 * cx);
-        const double* slot = sacc + (cy * CX + cx) * 18 + 2 * a;
-        s0 += slot[0];
-        s1 += slot[1];
+        const int cell = cy * CX + cx;
+        s0 += sacc[(2 * a) * NT + cell];
+        s1 += sacc[(2 * a + 1) * NT + cell];
       }
     }
     const int X = 2 * (i0 - 1) + lx, Y = 2 * (j0 - 1) + ly;
     const size_t o = base + 2 * ((size_t)Y * g.nnx + X);
     if (rhs) {
-      s0 = rhs[o] - s0;
-      s1 = rhs[o + 1] - s1;
+      s0 = r0v[it] - s0;
+      s1 = r1v[it] - s1;
     }
     out[o] = s0;
     out[o + 1] = s1;
@@ -564,22 +808,19 @@ __device__ void assemble_and_store(const Geom& g, const double* sacc, int i0, in
 // Slab Jacobian apply: out = J x  (or rhs - J x when rhs != null)
 // ---------------------------------------------------------------------------
 template <int K1>
-__global__ void __launch_bounds__(NT) k_jacobian(Geom g, TimeData td, Disc ds, Lin L, const double* __restrict__ state,
+__global__ void __launch_bounds__(NT, 2) k_jacobian(Geom g, TimeData td, Disc ds, Lin L, const double* __restrict__ state,
                                                  const double* __restrict__ x, const double* __restrict__ rhs,
                                                  double* __restrict__ out) {
   extern __shared__ double smem[];
-  double* xs = smem;                       // [K1][2][PLANE]
-  double* ss = xs + (size_t)K1 * 2 * PLANE;  // [2][PLANE]
-  double* sacc = ss + 2 * PLANE;           // [NT][18]
+  double* xs = smem;              // [2][PLANE]  direction x_mu (two-cell ring)
+  double* ss = xs + 2 * PLANE;    // [2][PLANE]  state v_mu
+  double* ts = ss + 2 * PLANE;    // [2][PLANE]  sum_nu K_t[mu,nu] x_nu (temporal coupling)
+  double* sacc = ts + 2 * PLANE;  // [18][NT]   per-cell node contributions
   const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
   const int X0 = 2 * (i0 - 2), Y0 = 2 * (j0 - 2);
-  for (int nu = 0; nu < K1; ++nu)
-    stage_velocity(g, x + (size_t)nu * g.nd, xs + (size_t)nu * 2 * PLANE, xs + (size_t)nu * 2 * PLANE + PLANE, X0,
-                   Y0);
-  Plane2 XP[K1];
-#pragma unroll
-  for (int nu = 0; nu < K1; ++nu) XP[nu] = Plane2{xs + nu * 2 * PLANE, xs + nu * 2 * PLANE + PLANE};
+  const Plane2 XM{xs, xs + PLANE};
   const Plane2 SP{ss, ss + PLANE};
+  const Plane2 TP{ts, ts + PLANE};
 
   const int tx = threadIdx.x % CX, ty = threadIdx.x / CX;
   const int ci = i0 - 1 + tx, cj = j0 - 1 + ty;
@@ -587,59 +828,55 @@ __global__ void __launch_bounds__(NT) k_jacobian(Geom g, TimeData td, Disc ds, L
   const bool owned = valid && tx >= 1 && ty >= 1;
   const int c = cj * g.nx + ci;
   const int r0 = 2 + 2 * ty, c0 = 2 + 2 * tx;  // staged origin of the cell's nodes
-  const double W = g.hx * g.hy;
+  const bool cip = ds.convection && ds.gamma_cip > 0.0;
+  const SmemAcc slot{sacc + threadIdx.x};
 
   for (int mu = 0; mu < K1; ++mu) {
-    stage_velocity(g, state + (size_t)mu * g.mv, ss, ss + PLANE, X0, Y0);
-    __syncthreads();
-    double acc[3][3][2];
+    const double tw = td.tau_w[mu];
+    stage_velocity_async(g, x + (size_t)mu * g.nd, xs, xs + PLANE, X0, Y0);
+    stage_velocity_async(g, state + (size_t)mu * g.mv, ss, ss + PLANE, X0, Y0);
+    // temporal coupling sum_nu K_t[mu,nu] x_nu on the computed cells' nodes (rows/cols 2..2CX+2)
+    for (int idx = threadIdx.x; idx < (2 * CX + 1) * (2 * CY + 1); idx += NT) {
+      const int r = 2 + idx / (2 * CX + 1), cc = 2 + idx % (2 * CX + 1);
+      const int X = X0 + cc, Y = Y0 + r;
+      double v0 = 0.0, v1 = 0.0;
+      if (X >= 0 && X < g.nnx && Y >= 0 && Y < g.nny) {
+        const size_t o = 2 * ((size_t)Y * g.nnx + X);
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-    double accp[3] = {0.0, 0.0, 0.0};
+        for (int nu = 0; nu < K1; ++nu) {
+          const double k = td.K_t[mu * K1 + nu];
+          v0 = fma(k, __ldg(x + (size_t)nu * g.nd + o), v0);
+          v1 = fma(k, __ldg(x + (size_t)nu * g.nd + o + 1), v1);
+        }
+      }
+      ts[pidx(r, cc)] = v0;
+      ts[PLANE + pidx(r, cc)] = v1;
+    }
+    double P[3] = {0.0, 0.0, 0.0};
     if (valid) {
-      const Plane2& XM = XP[mu];
-      double P[3];
       const double* xp = x + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
       P[0] = __ldg(xp);
       P[1] = __ldg(xp + 1);
       P[2] = __ldg(xp + 2);
-      jac_cell_local(g, ds, L, mu, c, ci, cj, XM, SP, r0, c0, P, acc, accp);
-      // ---- CIP own sides (forms.py:639-650) ----
-      if (ds.convection && ds.gamma_cip > 0.0) {
-        if (cj > 0) cip_side(g, ds, 0, XM, SP, r0, c0, 1.0, acc);
-        if (ci < g.nx - 1) cip_side(g, ds, 1, XM, SP, r0, c0, 1.0, acc);
-        if (cj < g.ny - 1) cip_side(g, ds, 2, XM, SP, r0, c0, 1.0, acc);
-        if (ci > 0) cip_side(g, ds, 3, XM, SP, r0, c0, 1.0, acc);
-      }
-      // ---- slab composition (slab.py:197-200) ----
-      const double tw = td.tau_w[mu];
+    }
 #pragma unroll
-      for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int b = 0; b < 3; ++b) {
-          acc[a][b][0] *= tw;
-          acc[a][b][1] *= tw;
-        }
-      add_mass<K1>(XP, nullptr, 0.0, td.K_t + mu * K1, r0, c0, W, acc);
+    for (int k = 0; k < 18; ++k) sacc[k * NT + threadIdx.x] = 0.0;
+    cp_async_wait_all();
+    __syncthreads();
+    if (valid) {
+      double accp[3] = {0.0, 0.0, 0.0};
+      // tau w_mu J_mu x_mu: volume, boundary sides, CIP faces (weights carry tau w_mu)
+      jac_volume(g, ds, L, mu, c, XM, SP, r0, c0, P, slot, accp, tw);
+      jac_sides(g, ds, L, mu, ci, cj, XM, SP, r0, c0, P, slot, accp, tw);
+      if (cip) cip_all(g, ds, XM, SP, ci, cj, r0, c0, tw, slot);
+      // + M_K sum_nu K_t[mu,nu] x_nu (slab.py:199-200)
+      add_mass_plane(TP, r0, c0, g.hx * g.hy, slot);
       if (owned) {
         const size_t o = (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
 #pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          const double val = tw * accp[j];
-          out[o + j] = rhs ? rhs[o + j] - val : val;
-        }
+        for (int j = 0; j < 3; ++j) out[o + j] = rhs ? rhs[o + j] - accp[j] : accp[j];
       }
     }
-    double* slot = sacc + threadIdx.x * 18;
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        slot[2 * (3 * a + b)] = acc[a][b][0];
-        slot[2 * (3 * a + b) + 1] = acc[a][b][1];
-      }
     __syncthreads();
     assemble_and_store(g, sacc, i0, j0, mu, rhs, out);
     __syncthreads();
@@ -658,7 +895,10 @@ __global__ void __launch_bounds__(NT) k_residual(Geom g, TimeData td, Disc ds, M
   double* us = smem;                          // [K1][2][PLANE] state velocities
   double* vm = us + (size_t)K1 * 2 * PLANE;   // [2][PLANE] v_minus
   double* as = vm + 2 * PLANE;                // [2][PLANE] advect (if given)
-  double* sacc = as + 2 * PLANE;              // [NT][18]
+  double* sacc = as + 2 * PLANE;              // [18][NT]
+  double* fR = sacc + 18 * NT;
+  double* fT = fR + 6 * NT;
+  const bool cip = ds.convection && ds.gamma_cip > 0.0;
   const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
   const int X0 = 2 * (i0 - 2), Y0 = 2 * (j0 - 2);
   for (int nu = 0; nu < K1; ++nu)
@@ -709,8 +949,8 @@ __global__ void __launch_bounds__(NT) k_residual(Geom g, TimeData td, Disc ds, M
 #pragma unroll
           for (int d = 0; d < 2; ++d) {
             v[d] = c_tab.B[qy][0] * sB[0][d] + c_tab.B[qy][1] * sB[1][d] + c_tab.B[qy][2] * sB[2][d];
-            vx[d] = (c_tab.B[qy][0] * sG[0][d] + c_tab.B[qy][1] * sG[1][d] + c_tab.B[qy][2] * sG[2][d]) / g.hx;
-            vy[d] = (c_tab.G[qy][0] * sB[0][d] + c_tab.G[qy][1] * sB[1][d] + c_tab.G[qy][2] * sB[2][d]) / g.hy;
+            vx[d] = (c_tab.B[qy][0] * sG[0][d] + c_tab.B[qy][1] * sG[1][d] + c_tab.B[qy][2] * sG[2][d]) * g.ihx;
+            vy[d] = (c_tab.G[qy][0] * sB[0][d] + c_tab.G[qy][1] * sB[1][d] + c_tab.G[qy][2] * sB[2][d]) * g.ihy;
           }
           const int q = 4 * qx + qy;
           const double wq = c_tab.w[qx] * c_tab.w[qy] * W;
@@ -748,8 +988,8 @@ __global__ void __launch_bounds__(NT) k_residual(Geom g, TimeData td, Disc ds, M
           for (int jy = 0; jy < 3; ++jy) {
             Pa[jy][0] = fma(wq * Fx0, c_tab.B[qy][jy], Pa[jy][0]);
             Pa[jy][1] = fma(wq * Fx1, c_tab.B[qy][jy], Pa[jy][1]);
-            Qa[jy][0] = fma(wq * Fy0, c_tab.G[qy][jy] / g.hy, fma(wq * Fv0, c_tab.B[qy][jy], Qa[jy][0]));
-            Qa[jy][1] = fma(wq * Fy1, c_tab.G[qy][jy] / g.hy, fma(wq * Fv1, c_tab.B[qy][jy], Qa[jy][1]));
+            Qa[jy][0] = fma(wq * Fy0, c_tab.G[qy][jy] * g.ihy, fma(wq * Fv0, c_tab.B[qy][jy], Qa[jy][0]));
+            Qa[jy][1] = fma(wq * Fy1, c_tab.G[qy][jy] * g.ihy, fma(wq * Fv1, c_tab.B[qy][jy], Qa[jy][1]));
           }
         }
 #pragma unroll
@@ -758,7 +998,7 @@ __global__ void __launch_bounds__(NT) k_residual(Geom g, TimeData td, Disc ds, M
           for (int ix = 0; ix < 3; ++ix)
 #pragma unroll
             for (int d = 0; d < 2; ++d)
-              acc[jy][ix][d] += c_tab.G[qx][ix] / g.hx * Pa[jy][d] + c_tab.B[qx][ix] * Qa[jy][d];
+              acc[jy][ix][d] += (c_tab.G[qx][ix] * g.ihx) * Pa[jy][d] + c_tab.B[qx][ix] * Qa[jy][d];
       }
       if (ci == 0 || cj == 0 || ci == g.nx - 1 || cj == g.ny - 1) {
         double gn[18];
@@ -772,19 +1012,18 @@ __global__ void __launch_bounds__(NT) k_residual(Geom g, TimeData td, Disc ds, M
           }
           gp = gn;
         }
-        if (cj == 0) res_boundary_side(g, ds, m, L, 0, side_offset(g, 0) + ci, SP, AW, r0, c0, PI, gp, acc, accp);
+        if (cj == 0) res_boundary_side(g, ds, m, L, 0, side_offset(g, 0) + ci, SP, AW, r0, c0, PI, gp, RegAcc{acc}, accp);
         if (ci == g.nx - 1)
-          res_boundary_side(g, ds, m, L, 1, side_offset(g, 1) + cj, SP, AW, r0, c0, PI, gp, acc, accp);
+          res_boundary_side(g, ds, m, L, 1, side_offset(g, 1) + cj, SP, AW, r0, c0, PI, gp, RegAcc{acc}, accp);
         if (cj == g.ny - 1)
-          res_boundary_side(g, ds, m, L, 2, side_offset(g, 2) + ci, SP, AW, r0, c0, PI, gp, acc, accp);
-        if (ci == 0) res_boundary_side(g, ds, m, L, 3, side_offset(g, 3) + cj, SP, AW, r0, c0, PI, gp, acc, accp);
+          res_boundary_side(g, ds, m, L, 2, side_offset(g, 2) + ci, SP, AW, r0, c0, PI, gp, RegAcc{acc}, accp);
+        if (ci == 0) res_boundary_side(g, ds, m, L, 3, side_offset(g, 3) + cj, SP, AW, r0, c0, PI, gp, RegAcc{acc}, accp);
       }
-      if (ds.convection && ds.gamma_cip > 0.0) {
-        if (cj > 0) cip_side(g, ds, 0, SP, AW, r0, c0, -1.0, acc);
-        if (ci < g.nx - 1) cip_side(g, ds, 1, SP, AW, r0, c0, -1.0, acc);
-        if (cj < g.ny - 1) cip_side(g, ds, 2, SP, AW, r0, c0, -1.0, acc);
-        if (ci > 0) cip_side(g, ds, 3, SP, AW, r0, c0, -1.0, acc);
-      }
+      if (cip) cip_own(g, ds, SP, AW, ci, cj, tx, ty, r0, c0, -1.0, fR, fT, RegAcc{acc});
+    }
+    __syncthreads();
+    if (valid) {
+      if (cip) cip_received(g, ci, cj, tx, ty, -1.0, fR, fT, RegAcc{acc});
       const double tw = td.tau_w[mu];
 #pragma unroll
       for (int a = 0; a < 3; ++a)
@@ -793,20 +1032,19 @@ __global__ void __launch_bounds__(NT) k_residual(Geom g, TimeData td, Disc ds, M
           acc[a][b][0] *= tw;
           acc[a][b][1] *= tw;
         }
-      add_mass<K1>(UP, &VM, td.m_t[mu], td.K_t + mu * K1, r0, c0, -W, acc);
+      add_mass<K1>(UP, &VM, td.m_t[mu], td.K_t + mu * K1, r0, c0, -W, RegAcc{acc});
       if (owned) {
         const size_t o = (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
 #pragma unroll
         for (int j = 0; j < 3; ++j) out[o + j] = tw * accp[j];
       }
     }
-    double* slot = sacc + threadIdx.x * 18;
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
       for (int b = 0; b < 3; ++b) {
-        slot[2 * (3 * a + b)] = acc[a][b][0];
-        slot[2 * (3 * a + b) + 1] = acc[a][b][1];
+        sacc[(2 * (3 * a + b)) * NT + threadIdx.x] = acc[a][b][0];
+        sacc[(2 * (3 * a + b) + 1) * NT + threadIdx.x] = acc[a][b][1];
       }
     __syncthreads();
     assemble_and_store(g, sacc, i0, j0, mu, nullptr, out);
@@ -848,8 +1086,8 @@ __global__ void k_linearize_cells(Geom g, Model m, int k1, const double* __restr
       double vx[2], vy[2];
 #pragma unroll
       for (int d = 0; d < 2; ++d) {
-        vx[d] = (c_tab.B[qy][0] * sG[0][d] + c_tab.B[qy][1] * sG[1][d] + c_tab.B[qy][2] * sG[2][d]) / g.hx;
-        vy[d] = (c_tab.G[qy][0] * sB[0][d] + c_tab.G[qy][1] * sB[1][d] + c_tab.G[qy][2] * sB[2][d]) / g.hy;
+        vx[d] = (c_tab.B[qy][0] * sG[0][d] + c_tab.B[qy][1] * sG[1][d] + c_tab.B[qy][2] * sG[2][d]) * g.ihx;
+        vy[d] = (c_tab.G[qy][0] * sB[0][d] + c_tab.G[qy][1] * sB[1][d] + c_tab.G[qy][2] * sB[2][d]) * g.ihy;
       }
       const double a0 = vx[0], a1 = vy[1], a2 = 0.5 * (vy[0] + vx[1]);
       double e, gm;
@@ -874,7 +1112,7 @@ __device__ void face_symgrad(const Geom& g, const double* __restrict__ v, int bf
   else { ci = 0; cj = f; }
   const int axis = (side == 1 || side == 3) ? 0 : 1;
   const int e = (side == 1 || side == 2) ? 1 : 0;
-  const double htan = axis == 0 ? g.hy : g.hx, hnorm = axis == 0 ? g.hx : g.hy;
+  const double ihtan = axis == 0 ? g.ihy : g.ihx, ihnorm = axis == 0 ? g.ihx : g.ihy;
   double ux[2], uy[2];
   for (int d = 0; d < 2; ++d) {
     double dt = 0.0, dn = 0.0;
@@ -890,11 +1128,11 @@ __device__ void face_symgrad(const Geom& g, const double* __restrict__ v, int bf
       dn = fma(c_tab.B[q][t], ld, dn);
     }
     if (axis == 0) {
-      ux[d] = dn / hnorm;
-      uy[d] = dt / htan;
+      ux[d] = dn * ihnorm;
+      uy[d] = dt * ihtan;
     } else {
-      ux[d] = dt / htan;
-      uy[d] = dn / hnorm;
+      ux[d] = dt * ihtan;
+      uy[d] = dn * ihnorm;
     }
   }
   a0 = ux[0];
@@ -970,7 +1208,8 @@ __global__ void __launch_bounds__(128) k_element_matrices(Geom g, Disc ds, Lin L
 #pragma unroll
     for (int b = 0; b < 3; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   double accp[3] = {0.0, 0.0, 0.0};
-  jac_cell_local(g, ds, L, mu, (int)c, ci, cj, X, S, 0, 0, P, acc, accp);
+  jac_volume(g, ds, L, mu, (int)c, X, S, 0, 0, P, RegAcc{acc}, accp);
+  jac_sides(g, ds, L, mu, ci, cj, X, S, 0, 0, P, RegAcc{acc}, accp);
   double* out = ET + (c * 21 + j) * 21;
 #pragma unroll
   for (int a = 0; a < 9; ++a) {
@@ -984,11 +1223,11 @@ __global__ void __launch_bounds__(128) k_element_matrices(Geom g, Disc ds, Lin L
 
 template <int K1>
 size_t jac_smem() {
-  return ((size_t)K1 * 2 * PLANE + 2 * PLANE + (size_t)NT * 18) * sizeof(double);
+  return ((size_t)6 * PLANE + (size_t)NT * 18) * sizeof(double);
 }
 template <int K1>
 size_t res_smem() {
-  return ((size_t)K1 * 2 * PLANE + 4 * PLANE + (size_t)NT * 18) * sizeof(double);
+  return ((size_t)K1 * 2 * PLANE + 4 * PLANE + (size_t)NT * 30) * sizeof(double);
 }
 
 template <int K1>
