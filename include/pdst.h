@@ -112,6 +112,9 @@ int pdst_level_sizes(pdst_handle* h, int level, int32_t* nx, int32_t* ny, int64_
    On ESINGULAR, *bad_level / *bad_patch identify the first singular patch. */
 int pdst_patches_build(pdst_handle* h, int surrogate, double rep_fraction, int* bad_level, int64_t* bad_patch);
 int pdst_patch_matrices(pdst_handle* h, int level, double* mats /* host (ncells, D, D) */);
+/* storage of a level's factorized patches: D, number of temporally diagonalized
+   complex 21x21 blocks (0 = full real D x D inverses), bytes streamed per patch per sweep */
+int pdst_patch_info(pdst_handle* h, int level, int32_t* D, int32_t* diag_blocks, int64_t* bytes_per_patch);
 int pdst_vanka(pdst_handle* h, int level, double* d, const double* r, int steps, double omega, int where);
 int pdst_level_apply(pdst_handle* h, int level, const double* x, double* y, int where);
 int pdst_restrict(pdst_handle* h, int fine_level, const double* r_fine, double* r_coarse, int where);

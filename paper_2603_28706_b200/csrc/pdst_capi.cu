@@ -314,7 +314,10 @@ static int jac_common(pdst_handle* h, const double* x, const double* r, double* 
   if (err) return err;
   double* yd = out_ptr(h->scratch_b, y, n, where);
   if (!yd) return fail(PDST_ECUDA, "out of device memory");
-  CK(PDST_TIMED(h, PK_JACOBIAN, jacobian_apply(h->g, h->td, h->ds, lin_of(h), h->state.ptr, xd, rd, yd, h->stream)));
+  double* part = h->jpart.ensure(jacobian_scratch(h->g, h->td.k1));
+  if (!part) return fail(PDST_ECUDA, "out of device memory");
+  CK(PDST_TIMED(h, PK_JACOBIAN,
+                jacobian_apply(h->g, h->td, h->ds, lin_of(h), h->state.ptr, xd, rd, yd, part, h->stream)));
   return finish_out(h, y, yd, n, where);
 }
 

@@ -7,6 +7,7 @@
 
 #include "pdst_device.cuh"
 #include "pdst_internal.h"
+#include "pdst_patch.h"
 
 namespace pdst {
 
@@ -39,6 +40,10 @@ struct Level {
   // patches
   DeviceBuffer mats, invs;
   int D = 0;
+  // surrogate patches in temporally diagonalized form (pdst_timediag.cu)
+  bool diag = false;
+  TimeDiag tdiag{};
+  DeviceBuffer spatial, binv;
   // work vectors (k1 * nd each)
   DeviceBuffer w0, w1, w2, w3;
   ~Level() {
@@ -114,6 +119,7 @@ struct pdst_handle {
   // staging for host pointers
   pdst::DeviceBuffer scratch_a, scratch_b, scratch_c, scratch_d, scratch_f;
   pdst::DeviceBuffer partials;
+  pdst::DeviceBuffer jpart;  // Jacobian tile-boundary partial sums
 
   // surrogate (representative-state) linearization and patch scratch
   pdst::DeviceBuffer state_rep, eta_rep, gam_rep, etaf_rep, gamf_rep;

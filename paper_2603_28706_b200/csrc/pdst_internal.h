@@ -9,8 +9,10 @@ namespace pdst {
 
 cudaError_t set_tables(const Tables& t);
 
+// y = J x (rhs == null) or y = rhs - J x; `part` holds jacobian_scratch() doubles.
+size_t jacobian_scratch(const Geom& g, int k1);
 cudaError_t jacobian_apply(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* state,
-                           const double* x, const double* rhs, double* out, cudaStream_t st);
+                           const double* x, const double* rhs, double* out, double* part, cudaStream_t st);
 
 cudaError_t slab_residual(const Geom& g, const TimeData& td, const Disc& ds, const Model& m, const Lin& L,
                           const double* U, const double* advect, const double* vminus, const double* fqp,

@@ -171,15 +171,30 @@ int pdst_patches_build(pdst_handle* h, int surrogate, double rep_fraction, int* 
     pa.state = h->state.ptr;
   }
   double* mats = fl->mats.ensure(nc * D * D);
-  double* invs = fl->invs.ensure(nc * D * D);
   double* bad = h->ibuf.ensure(1);
-  if (!mats || !invs || !bad) return set_error(PDST_ECUDA, "out of device memory (patches)");
+  if (!mats || !bad) return set_error(PDST_ECUDA, "out of device memory (patches)");
   pa.mats = mats;
+  // Surrogate patches share one spatial block across the Radau nodes: keep it
+  // and invert the temporally diagonalized blocks instead of A_K itself.
+  const char* nd_env = getenv("PDST_NO_TIMEDIAG");
+  fl->diag = surrogate && !(nd_env && nd_env[0] == '1') && time_diagonalize(k1, h->td.K_t, h->td.tau_w, fl->tdiag);
+  pa.spatial = nullptr;
+  if (fl->diag) {
+    pa.spatial = fl->spatial.ensure(nc * 441);
+    if (!pa.spatial || !fl->binv.ensure(nc * 441 * 2 * fl->tdiag.nblk))
+      return set_error(PDST_ECUDA, "out of device memory (diagonalized patches)");
+  }
   CK(patch_assemble(pa, h->stream));
   int* badi = reinterpret_cast<int*>(bad);
   const int init = INT_MAX;
   CK(cudaMemcpyAsync(badi, &init, sizeof(int), cudaMemcpyHostToDevice, h->stream));
-  CK(patch_invert(k1, mats, invs, (int)nc, badi, h->stream));
+  if (fl->diag) {
+    CK(patch_invert_diag(g, fl->tdiag, pa.spatial, reinterpret_cast<double2*>(fl->binv.ptr), badi, h->stream));
+  } else {
+    double* invs = fl->invs.ensure(nc * D * D);
+    if (!invs) return set_error(PDST_ECUDA, "out of device memory (patch inverses)");
+    CK(patch_invert(k1, mats, invs, (int)nc, badi, h->stream));
+  }
   int badh = INT_MAX;
   CK(cudaMemcpyAsync(&badh, badi, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
@@ -207,6 +222,18 @@ int pdst_patch_matrices(pdst_handle* h, int level, double* mats) {
   return PDST_OK;
 }
 
+int pdst_patch_info(pdst_handle* h, int level, int32_t* D, int32_t* diag_blocks, int64_t* bytes_per_patch) {
+  if (!h) return set_error(PDST_EINVAL, "null handle");
+  if (int e = check_level(h, level)) return e;
+  Level* l = h->levels[level];
+  if (!l->D) return set_error(PDST_ESTATE, "patches not built");
+  if (D) *D = l->D;
+  if (diag_blocks) *diag_blocks = l->diag ? l->tdiag.nblk : 0;
+  if (bytes_per_patch)
+    *bytes_per_patch = l->diag ? (int64_t)l->tdiag.nblk * 441 * 16 : (int64_t)l->D * l->D * 8;
+  return PDST_OK;
+}
+
 int pdst_vanka(pdst_handle* h, int level, double* d, const double* r, int steps, double omega, int where) {
   if (!h || !d || !r) return set_error(PDST_EINVAL, "null argument");
   if (int e = check_where(where)) return e;
@@ -229,9 +256,15 @@ int pdst_vanka(pdst_handle* h, int level, double* d, const double* r, int steps,
   double* upd = h->upd.ensure((size_t)g.ncells * 21 * k1);
   if (!defect || !upd) return set_error(PDST_ECUDA, "out of device memory");
   const Lin L = lin_of(h);
+  double* part = h->jpart.ensure(jacobian_scratch(g, k1));
+  if (!part) return set_error(PDST_ECUDA, "out of device memory");
   for (int s = 0; s < steps; ++s) {
-    CK(PDST_TIMED(h, PK_JACOBIAN, jacobian_apply(g, h->td, h->ds, L, h->state.ptr, dd, rd, defect, h->stream)));
-    CK(PDST_TIMED(h, PK_VANKA_GEMV, vanka_gemv(g, k1, l->invs.ptr, defect, upd, h->stream)));
+    CK(PDST_TIMED(h, PK_JACOBIAN, jacobian_apply(g, h->td, h->ds, L, h->state.ptr, dd, rd, defect, part, h->stream)));
+    if (l->diag)
+      CK(PDST_TIMED(h, PK_VANKA_GEMV, vanka_gemv_diag(g, l->tdiag, reinterpret_cast<const double2*>(l->binv.ptr),
+                                                       defect, upd, h->stream)));
+    else
+      CK(PDST_TIMED(h, PK_VANKA_GEMV, vanka_gemv(g, k1, l->invs.ptr, defect, upd, h->stream)));
     CK(PDST_TIMED(h, PK_VANKA_SCATTER, vanka_scatter(g, k1, upd, omega, dd, h->stream)));
   }
   return finish_out(h, d, dd, n, where);

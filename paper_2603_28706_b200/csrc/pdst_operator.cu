@@ -807,51 +807,66 @@ __device__ void assemble_and_store(const Geom& g, const double* sacc, int i0, in
 // ---------------------------------------------------------------------------
 // Slab Jacobian apply: out = J x  (or rhs - J x when rhs != null)
 // ---------------------------------------------------------------------------
-template <int K1>
-__global__ void __launch_bounds__(NT, 2) k_jacobian(Geom g, TimeData td, Disc ds, Lin L, const double* __restrict__ state,
-                                                 const double* __restrict__ x, const double* __restrict__ rhs,
-                                                 double* __restrict__ out) {
-  extern __shared__ double smem[];
-  double* xs = smem;              // [2][PLANE]  direction x_mu (two-cell ring)
-  double* ss = xs + 2 * PLANE;    // [2][PLANE]  state v_mu
-  double* ts = ss + 2 * PLANE;    // [2][PLANE]  sum_nu K_t[mu,nu] x_nu (temporal coupling)
-  double* sacc = ts + 2 * PLANE;  // [18][NT]   per-cell node contributions
-  const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
-  const int X0 = 2 * (i0 - 2), Y0 = 2 * (j0 - 2);
-  const Plane2 XM{xs, xs + PLANE};
-  const Plane2 SP{ss, ss + PLANE};
-  const Plane2 TP{ts, ts + PLANE};
+// ---------------------------------------------------------------------------
+// Slab Jacobian apply: out = J x  (or rhs - J x when rhs != null)
+//
+// Tiles of JT x JT cells, one thread per cell, NO redundant halo cells: nodes
+// interior to a tile are complete and written directly; nodes on a tile
+// boundary shared with a neighbour tile are written as partial sums to `part`
+// and combined by k_jac_fixup in a fixed order (deterministic).
+// ---------------------------------------------------------------------------
+constexpr int JT = 16;            // owned cells per tile side
+constexpr int JNT = JT * JT;      // threads per CTA
+constexpr int JPER = 8 * JT;      // perimeter nodes of a tile's node rectangle
+static_assert(2 * (JT + 2) + 1 == NC && 2 * (JT + 2) + 1 == NR, "Jacobian tile must match the staged plane");
+static_assert(JNT == NT, "SmemAcc stride");
 
-  const int tx = threadIdx.x % CX, ty = threadIdx.x / CX;
-  const int ci = i0 - 1 + tx, cj = j0 - 1 + ty;
-  const bool valid = ci >= 0 && ci < g.nx && cj >= 0 && cj < g.ny;
-  const bool owned = valid && tx >= 1 && ty >= 1;
+__host__ __device__ inline int jac_tiles_x(const Geom& g) { return (g.nx + JT - 1) / JT; }
+__host__ __device__ inline int jac_tiles_y(const Geom& g) { return (g.ny + JT - 1) / JT; }
+
+// Canonical perimeter index of node (lx, ly) of a full tile node rectangle.
+__device__ __forceinline__ int perim(int lx, int ly) {
+  if (ly == 0) return lx;
+  if (ly == 2 * JT) return 2 * JT + 1 + lx;
+  if (lx == 0) return 2 * (2 * JT + 1) + ly - 1;
+  return 2 * (2 * JT + 1) + 2 * JT - 1 + ly - 1;
+}
+
+template <int K1>
+__global__ void __launch_bounds__(JNT, 1) k_jacobian(Geom g, TimeData td, Disc ds, Lin L, const double* __restrict__ state,
+                                                  const double* __restrict__ x, const double* __restrict__ rhs,
+                                                  double* __restrict__ out, double* __restrict__ part) {
+  extern __shared__ double smem[];
+  double* xs = smem;                        // [K1][2][PLANE] direction x_nu, all Radau nodes (one-cell ring)
+  double* ss = xs + (size_t)K1 * 2 * PLANE;  // [2][PLANE]     state v_mu
+  double* rs = ss + 2 * PLANE;              // [2][PLANE]     rhs block mu (defect mode)
+  double* sacc = rs + 2 * PLANE;            // [18][JNT]      per-cell node contributions
+  const int bx = blockIdx.x, by = blockIdx.y;
+  const int i0 = bx * JT, j0 = by * JT;
+  const int X0 = 2 * (i0 - 1), Y0 = 2 * (j0 - 1);
+  const int ntx = min(JT, g.nx - i0), nty = min(JT, g.ny - j0);
+  Plane2 XP[K1];
+#pragma unroll
+  for (int nu = 0; nu < K1; ++nu) XP[nu] = Plane2{xs + nu * 2 * PLANE, xs + nu * 2 * PLANE + PLANE};
+  const Plane2 SP{ss, ss + PLANE};
+  const Plane2 RP{rs, rs + PLANE};
+  const int tx = threadIdx.x % JT, ty = threadIdx.x / JT;
+  const int ci = i0 + tx, cj = j0 + ty;
+  const bool valid = tx < ntx && ty < nty;
   const int c = cj * g.nx + ci;
   const int r0 = 2 + 2 * ty, c0 = 2 + 2 * tx;  // staged origin of the cell's nodes
   const bool cip = ds.convection && ds.gamma_cip > 0.0;
   const SmemAcc slot{sacc + threadIdx.x};
+  const size_t ntiles = (size_t)jac_tiles_x(g) * jac_tiles_y(g);
+  const size_t tile = (size_t)by * jac_tiles_x(g) + bx;
 
+  for (int nu = 0; nu < K1; ++nu)
+    stage_velocity_async(g, x + (size_t)nu * g.nd, xs + (size_t)nu * 2 * PLANE, xs + (size_t)nu * 2 * PLANE + PLANE,
+                         X0, Y0);
   for (int mu = 0; mu < K1; ++mu) {
     const double tw = td.tau_w[mu];
-    stage_velocity_async(g, x + (size_t)mu * g.nd, xs, xs + PLANE, X0, Y0);
     stage_velocity_async(g, state + (size_t)mu * g.mv, ss, ss + PLANE, X0, Y0);
-    // temporal coupling sum_nu K_t[mu,nu] x_nu on the computed cells' nodes (rows/cols 2..2CX+2)
-    for (int idx = threadIdx.x; idx < (2 * CX + 1) * (2 * CY + 1); idx += NT) {
-      const int r = 2 + idx / (2 * CX + 1), cc = 2 + idx % (2 * CX + 1);
-      const int X = X0 + cc, Y = Y0 + r;
-      double v0 = 0.0, v1 = 0.0;
-      if (X >= 0 && X < g.nnx && Y >= 0 && Y < g.nny) {
-        const size_t o = 2 * ((size_t)Y * g.nnx + X);
-#pragma unroll
-        for (int nu = 0; nu < K1; ++nu) {
-          const double k = td.K_t[mu * K1 + nu];
-          v0 = fma(k, __ldg(x + (size_t)nu * g.nd + o), v0);
-          v1 = fma(k, __ldg(x + (size_t)nu * g.nd + o + 1), v1);
-        }
-      }
-      ts[pidx(r, cc)] = v0;
-      ts[PLANE + pidx(r, cc)] = v1;
-    }
+    if (rhs) stage_velocity_async(g, rhs + (size_t)mu * g.nd, rs, rs + PLANE, X0, Y0);
     double P[3] = {0.0, 0.0, 0.0};
     if (valid) {
       const double* xp = x + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
@@ -860,27 +875,109 @@ __global__ void __launch_bounds__(NT, 2) k_jacobian(Geom g, TimeData td, Disc ds
       P[2] = __ldg(xp + 2);
     }
 #pragma unroll
-    for (int k = 0; k < 18; ++k) sacc[k * NT + threadIdx.x] = 0.0;
+    for (int k = 0; k < 18; ++k) sacc[k * JNT + threadIdx.x] = 0.0;
     cp_async_wait_all();
     __syncthreads();
     if (valid) {
       double accp[3] = {0.0, 0.0, 0.0};
       // tau w_mu J_mu x_mu: volume, boundary sides, CIP faces (weights carry tau w_mu)
-      jac_volume(g, ds, L, mu, c, XM, SP, r0, c0, P, slot, accp, tw);
-      jac_sides(g, ds, L, mu, ci, cj, XM, SP, r0, c0, P, slot, accp, tw);
-      if (cip) cip_all(g, ds, XM, SP, ci, cj, r0, c0, tw, slot);
+      jac_volume(g, ds, L, mu, c, XP[mu], SP, r0, c0, P, slot, accp, tw);
+      jac_sides(g, ds, L, mu, ci, cj, XP[mu], SP, r0, c0, P, slot, accp, tw);
+      if (cip) cip_all(g, ds, XP[mu], SP, ci, cj, r0, c0, tw, slot);
       // + M_K sum_nu K_t[mu,nu] x_nu (slab.py:199-200)
-      add_mass_plane(TP, r0, c0, g.hx * g.hy, slot);
-      if (owned) {
-        const size_t o = (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
+      add_mass<K1>(XP, nullptr, 0.0, td.K_t + mu * K1, r0, c0, g.hx * g.hy, slot);
+      const size_t o = (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
 #pragma unroll
-        for (int j = 0; j < 3; ++j) out[o + j] = rhs ? rhs[o + j] - accp[j] : accp[j];
+      for (int j = 0; j < 3; ++j) out[o + j] = rhs ? rhs[o + j] - accp[j] : accp[j];
+    }
+    __syncthreads();
+    // node assembly over the tile's node rectangle
+    const int wx = 2 * ntx + 1, wy = 2 * nty + 1;
+    const size_t base = (size_t)mu * g.nd;
+    for (int idx = threadIdx.x; idx < wx * wy; idx += JNT) {
+      const int ly = idx / wx, lx = idx - ly * wx;
+      double s0 = 0.0, s1 = 0.0;
+      const int cxa = (lx & 1) ? (lx - 1) / 2 : lx / 2 - 1;
+      const int cya = (ly & 1) ? (ly - 1) / 2 : ly / 2 - 1;
+      for (int cy = cya; cy <= (ly & 1 ? cya : ly / 2); ++cy) {
+        if (cy < 0 || cy >= nty) continue;
+        for (int cx = cxa; cx <= (lx & 1 ? cxa : lx / 2); ++cx) {
+          if (cx < 0 || cx >= ntx) continue;
+          const int a = 3 * (ly - 2 * cy) + (lx - 2 * cx);
+          const int cell = cy * JT + cx;
+          s0 += sacc[(2 * a) * JNT + cell];
+          s1 += sacc[(2 * a + 1) * JNT + cell];
+        }
+      }
+      const bool shx = (lx == 0 && i0 > 0) || (lx == 2 * JT && i0 + JT < g.nx);
+      const bool shy = (ly == 0 && j0 > 0) || (ly == 2 * JT && j0 + JT < g.ny);
+      if (shx || shy) {
+        double* pp = part + (((size_t)mu * ntiles + tile) * JPER + perim(lx, ly)) * 2;
+        pp[0] = s0;
+        pp[1] = s1;
+      } else {
+        const size_t o = base + 2 * ((size_t)(2 * j0 + ly) * g.nnx + 2 * i0 + lx);
+        if (rhs) {
+          s0 = RP.at(0, ly + 2, lx + 2) - s0;
+          s1 = RP.at(1, ly + 2, lx + 2) - s1;
+        }
+        out[o] = s0;
+        out[o + 1] = s1;
       }
     }
     __syncthreads();
-    assemble_and_store(g, sacc, i0, j0, mu, rhs, out);
-    __syncthreads();
   }
+}
+
+// Shared tile-boundary nodes: sum the (2 or 4) tile partials in fixed order.
+__global__ void k_jac_fixup(Geom g, int k1, const double* __restrict__ part, const double* __restrict__ rhs,
+                            double* __restrict__ out) {
+  const int ntx = jac_tiles_x(g), nty = jac_tiles_y(g);
+  const size_t nv = (size_t)(ntx - 1) * g.nny;  // nodes on interior vertical tile lines
+  const size_t nh = (size_t)(nty - 1) * g.nnx;  // nodes on interior horizontal tile lines
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int mu = blockIdx.y;
+  int X, Y;
+  if (t < nv) {
+    X = 2 * JT * (int)(t / g.nny + 1);
+    Y = (int)(t % g.nny);
+  } else if (t < nv + nh) {
+    const size_t u = t - nv;
+    Y = 2 * JT * (int)(u / g.nnx + 1);
+    X = (int)(u % g.nnx);
+    if (X % (2 * JT) == 0 && X > 0 && X < 2 * JT * ntx && X / (2 * JT) < ntx) return;  // on a vertical line
+  } else {
+    return;
+  }
+  int bxs[2], bys[2], nbx = 0, nby = 0;
+  if (X % (2 * JT) == 0 && X > 0 && X / (2 * JT) < ntx) {
+    bxs[0] = X / (2 * JT) - 1;
+    bxs[1] = X / (2 * JT);
+    nbx = 2;
+  } else {
+    bxs[0] = min(X / (2 * JT), ntx - 1);
+    nbx = 1;
+  }
+  if (Y % (2 * JT) == 0 && Y > 0 && Y / (2 * JT) < nty) {
+    bys[0] = Y / (2 * JT) - 1;
+    bys[1] = Y / (2 * JT);
+    nby = 2;
+  } else {
+    bys[0] = min(Y / (2 * JT), nty - 1);
+    nby = 1;
+  }
+  const size_t ntiles = (size_t)ntx * nty;
+  double s0 = 0.0, s1 = 0.0;
+  for (int b = 0; b < nby; ++b)
+    for (int a = 0; a < nbx; ++a) {
+      const int lx = X - 2 * JT * bxs[a], ly = Y - 2 * JT * bys[b];
+      const double* pp = part + (((size_t)mu * ntiles + (size_t)bys[b] * ntx + bxs[a]) * JPER + perim(lx, ly)) * 2;
+      s0 += pp[0];
+      s1 += pp[1];
+    }
+  const size_t o = (size_t)mu * g.nd + 2 * ((size_t)Y * g.nnx + X);
+  out[o] = rhs ? rhs[o] - s0 : s0;
+  out[o + 1] = rhs ? rhs[o + 1] - s1 : s1;
 }
 
 // ---------------------------------------------------------------------------
@@ -1223,7 +1320,7 @@ __global__ void __launch_bounds__(128) k_element_matrices(Geom g, Disc ds, Lin L
 
 template <int K1>
 size_t jac_smem() {
-  return ((size_t)6 * PLANE + (size_t)NT * 18) * sizeof(double);
+  return ((size_t)(2 * K1 + 4) * PLANE + (size_t)JNT * 18) * sizeof(double);
 }
 template <int K1>
 size_t res_smem() {
@@ -1232,7 +1329,7 @@ size_t res_smem() {
 
 template <int K1>
 cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* state,
-                       const double* x, const double* rhs, double* out, cudaStream_t st) {
+                       const double* x, const double* rhs, double* out, double* part, cudaStream_t st) {
   static bool configured = false;
   const size_t sm = jac_smem<K1>();
   if (!configured) {
@@ -1240,8 +1337,15 @@ cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const 
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid((g.nx + TX - 1) / TX, (g.ny + TY - 1) / TY);
-  k_jacobian<K1><<<grid, NT, sm, st>>>(g, td, ds, L, state, x, rhs, out);
+  dim3 grid(jac_tiles_x(g), jac_tiles_y(g));
+  k_jacobian<K1><<<grid, JNT, sm, st>>>(g, td, ds, L, state, x, rhs, out, part);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const size_t nfix = (size_t)(jac_tiles_x(g) - 1) * g.nny + (size_t)(jac_tiles_y(g) - 1) * g.nnx;
+  if (nfix > 0) {
+    dim3 fg((unsigned)((nfix + 255) / 256), K1);
+    k_jac_fixup<<<fg, 256, 0, st>>>(g, K1, part, rhs, out);
+  }
   return cudaGetLastError();
 }
 
@@ -1265,13 +1369,17 @@ cudaError_t launch_res(const Geom& g, const TimeData& td, const Disc& ds, const 
 
 cudaError_t set_tables(const Tables& t) { return cudaMemcpyToSymbol(c_tab, &t, sizeof(Tables)); }
 
+size_t jacobian_scratch(const Geom& g, int k1) {
+  return (size_t)k1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2;
+}
+
 cudaError_t jacobian_apply(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* state,
-                           const double* x, const double* rhs, double* out, cudaStream_t st) {
+                           const double* x, const double* rhs, double* out, double* part, cudaStream_t st) {
   switch (td.k1) {
-    case 1: return launch_jac<1>(g, td, ds, L, state, x, rhs, out, st);
-    case 2: return launch_jac<2>(g, td, ds, L, state, x, rhs, out, st);
-    case 3: return launch_jac<3>(g, td, ds, L, state, x, rhs, out, st);
-    case 4: return launch_jac<4>(g, td, ds, L, state, x, rhs, out, st);
+    case 1: return launch_jac<1>(g, td, ds, L, state, x, rhs, out, part, st);
+    case 2: return launch_jac<2>(g, td, ds, L, state, x, rhs, out, part, st);
+    case 3: return launch_jac<3>(g, td, ds, L, state, x, rhs, out, part, st);
+    case 4: return launch_jac<4>(g, td, ds, L, state, x, rhs, out, part, st);
     default: return cudaErrorNotSupported;
   }
 }

@@ -15,7 +15,31 @@ struct PatchArgs {
   int nslot;            // k1 (exact patches) or 1 (surrogate)
   const double* state;  // [nslot][Mv] lagged velocity per slot (CIP weights)
   double* mats;         // [ncells][D][D] row-major output
+  double* spatial;      // optional [ncells][21][21] surrogate spatial block R_K J_rep R_K' (row-major)
 };
+
+// Temporal diagonalization of a surrogate patch:
+//   A_K = K_t (x) Mhat + diag(tau w) (x) Jhat,  S = diag(tau w)^-1 K_t = V diag(lam) V^-1,
+//   A_K^-1 e = (V (x) I) blockdiag[(lam_i Mhat + Jhat)^-1] (V^-1 diag(tau w)^-1 (x) I) e.
+// Only one member of each complex-conjugate pair is stored (nblk blocks).
+struct TimeDiag {
+  int k1;
+  int nblk;                    // stored eigen-blocks
+  int pair[MAXK1];             // 1 if block b is one of a conjugate pair (weight 2 Re), 0 if real
+  double lam_re[MAXK1], lam_im[MAXK1];
+  double V_re[MAXK1 * MAXK1], V_im[MAXK1 * MAXK1];        // V[mu][b] for stored blocks b (column b)
+  double Vi_re[MAXK1 * MAXK1], Vi_im[MAXK1 * MAXK1];      // Vinv[b][mu] rows for stored blocks
+  double itw[MAXK1];           // 1 / (tau w_mu)
+};
+
+// Host: diagonalize S = diag(tau w)^-1 K_t (k1 <= 4). Returns false when S is
+// defective / ill-conditioned (the caller keeps the full real inverses).
+bool time_diagonalize(int k1, const double* K_t, const double* tau_w, TimeDiag& out);
+
+cudaError_t patch_invert_diag(const Geom& g, const TimeDiag& td, const double* spatial, double2* binvT, int* bad,
+                              cudaStream_t st);
+cudaError_t vanka_gemv_diag(const Geom& g, const TimeDiag& td, const double2* binvT, const double* defect,
+                            double* upd, cudaStream_t st);
 
 cudaError_t patch_assemble(const PatchArgs& a, cudaStream_t st);
 cudaError_t patch_invert(int k1, const double* mats, double* invT, int npatch, int* bad, cudaStream_t st);

@@ -1,0 +1,425 @@
+// pdst_timediag.cu — temporally diagonalized surrogate Vanka patches.
+//
+// A surrogate patch (solver/multigrid.py:475-488) uses ONE spatial block for
+// every Radau node, so
+//   A_K = K_t (x) Mhat + W (x) Jhat,   W = diag(tau w_mu),
+// with Mhat the 21x21 patch mass (zero pressure rows/cols) and Jhat the
+// 21x21 surrogate spatial block.  With S = W^-1 K_t = V diag(lam) V^-1,
+//   A_K^-1 = (V (x) I) blockdiag_i[(lam_i Mhat + Jhat)^-1] (V^-1 W^-1 (x) I).
+// The Radau eigenvalues of S come in complex-conjugate pairs (plus one real
+// eigenvalue for odd k+1), so each patch stores one complex 21x21 inverse per
+// pair: 882 doubles instead of 42^2 = 1764 for DG(1), 1764 (incl. the real
+// block stored as complex) instead of 63^2 = 3969 for DG(2).  The Vanka sweep
+// then streams half / less than half the bytes.  Mathematically identical to
+// np.linalg.inv(A_K) @ e (multigrid.py:290-291, 338); rounding differs.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <complex>
+
+#include "pdst_device.cuh"
+#include "pdst_patch.h"
+
+namespace pdst {
+
+using cplx = std::complex<double>;
+
+namespace {
+
+// Complex Gauss-Jordan inverse of an n x n matrix (n <= 7), partial pivoting.
+bool cinv(int n, cplx* A /* row-major, in/out */) {
+  int perm[MAXK1];
+  for (int k = 0; k < n; ++k) {
+    int p = k;
+    double best = std::abs(A[k * n + k]);
+    for (int i = k + 1; i < n; ++i)
+      if (std::abs(A[i * n + k]) > best) {
+        best = std::abs(A[i * n + k]);
+        p = i;
+      }
+    if (!(best > 0.0)) return false;
+    perm[k] = p;
+    if (p != k)
+      for (int j = 0; j < n; ++j) std::swap(A[k * n + j], A[p * n + j]);
+    const cplx pinv = 1.0 / A[k * n + k];
+    A[k * n + k] = 1.0;
+    for (int j = 0; j < n; ++j) A[k * n + j] *= pinv;
+    for (int i = 0; i < n; ++i) {
+      if (i == k) continue;
+      const cplx f = A[i * n + k];
+      A[i * n + k] = 0.0;
+      for (int j = 0; j < n; ++j) A[i * n + j] -= f * A[k * n + j];
+    }
+  }
+  for (int k = n - 1; k >= 0; --k)
+    if (perm[k] != k)
+      for (int i = 0; i < n; ++i) std::swap(A[i * n + k], A[i * n + perm[k]]);
+  return true;
+}
+
+// Eigenvalues of a real n x n matrix via Durand-Kerner on the characteristic
+// polynomial (Faddeev-LeVerrier), n <= 7, after scaling to unit magnitude.
+bool eigenvalues(int n, const double* S, cplx* lam) {
+  double scale = 0.0;
+  for (int i = 0; i < n * n; ++i) scale = std::max(scale, std::fabs(S[i]));
+  if (!(scale > 0.0)) return false;
+  double A[MAXK1 * MAXK1], M[MAXK1 * MAXK1], AM[MAXK1 * MAXK1], c[MAXK1 + 1];
+  for (int i = 0; i < n * n; ++i) A[i] = S[i] / scale;
+  // Faddeev-LeVerrier: p(x) = x^n + c1 x^(n-1) + ... + cn
+  for (int i = 0; i < n * n; ++i) M[i] = 0.0;
+  c[0] = 1.0;
+  for (int k = 1; k <= n; ++k) {
+    // M = A M_prev + c_{k-1} I
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        double s = 0.0;
+        for (int l = 0; l < n; ++l) s += A[i * n + l] * M[l * n + j];
+        AM[i * n + j] = s + (i == j ? c[k - 1] : 0.0);
+      }
+    for (int i = 0; i < n * n; ++i) M[i] = AM[i];
+    double tr = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int l = 0; l < n; ++l) tr += A[i * n + l] * M[l * n + i];
+    c[k] = -tr / k;
+  }
+  auto poly = [&](cplx x) {
+    cplx v = 1.0;
+    for (int k = 1; k <= n; ++k) v = v * x + c[k];
+    return v;
+  };
+  cplx z[MAXK1];
+  const cplx seed(0.4, 0.9);
+  z[0] = 1.0;
+  for (int i = 0; i < n; ++i) z[i] = std::pow(seed, i + 1) * 1.5;
+  for (int it = 0; it < 500; ++it) {
+    double delta = 0.0;
+    for (int i = 0; i < n; ++i) {
+      cplx den = 1.0;
+      for (int j = 0; j < n; ++j)
+        if (j != i) den *= (z[i] - z[j]);
+      if (std::abs(den) == 0.0) return false;
+      const cplx dz = poly(z[i]) / den;
+      z[i] -= dz;
+      delta = std::max(delta, std::abs(dz));
+    }
+    if (delta < 1e-17) break;
+  }
+  for (int i = 0; i < n; ++i) lam[i] = z[i] * scale;
+  return true;
+}
+
+}  // namespace
+
+bool time_diagonalize(int k1, const double* K_t, const double* tau_w, TimeDiag& out) {
+  out = TimeDiag{};
+  out.k1 = k1;
+  if (k1 < 1 || k1 > 4) return false;
+  double S[MAXK1 * MAXK1];
+  for (int i = 0; i < k1; ++i) {
+    out.itw[i] = 1.0 / tau_w[i];
+    for (int j = 0; j < k1; ++j) S[i * k1 + j] = K_t[i * k1 + j] / tau_w[i];
+  }
+  cplx lam[MAXK1];
+  if (k1 == 1) {
+    lam[0] = S[0];
+  } else if (!eigenvalues(k1, S, lam)) {
+    return false;
+  }
+  // Newton-polish each eigenvalue on det(S - lam I) via inverse iteration
+  cplx V[MAXK1 * MAXK1];
+  double snorm = 0.0;
+  for (int i = 0; i < k1 * k1; ++i) snorm = std::max(snorm, std::fabs(S[i]));
+  for (int b = 0; b < k1; ++b) {
+    // snap near-real eigenvalues to the real axis
+    if (std::fabs(lam[b].imag()) < 1e-12 * std::abs(lam[b])) lam[b] = cplx(lam[b].real(), 0.0);
+    cplx v[MAXK1];
+    for (int i = 0; i < k1; ++i) v[i] = cplx(1.0 + 0.1 * i, 0.05 * i);
+    for (int it = 0; it < 4; ++it) {
+      cplx A[MAXK1 * MAXK1];
+      const cplx shift = lam[b] + cplx(1e-11 * snorm, 0.0);
+      for (int i = 0; i < k1; ++i)
+        for (int j = 0; j < k1; ++j) A[i * k1 + j] = S[i * k1 + j] - (i == j ? shift : 0.0);
+      if (!cinv(k1, A)) return false;
+      cplx w[MAXK1];
+      double nrm = 0.0;
+      for (int i = 0; i < k1; ++i) {
+        w[i] = 0.0;
+        for (int j = 0; j < k1; ++j) w[i] += A[i * k1 + j] * v[j];
+        nrm = std::max(nrm, std::abs(w[i]));
+      }
+      for (int i = 0; i < k1; ++i) v[i] = w[i] / nrm;
+      // Rayleigh-type refinement of lam
+      cplx num = 0.0, den = 0.0;
+      for (int i = 0; i < k1; ++i) {
+        cplx sv = 0.0;
+        for (int j = 0; j < k1; ++j) sv += S[i * k1 + j] * v[j];
+        num += std::conj(v[i]) * sv;
+        den += std::conj(v[i]) * v[i];
+      }
+      if (lam[b].imag() != 0.0) lam[b] = num / den;
+      else lam[b] = cplx((num / den).real(), 0.0);
+    }
+    if (lam[b].imag() == 0.0)
+      for (int i = 0; i < k1; ++i) v[i] = cplx(v[i].real(), 0.0);
+    for (int i = 0; i < k1; ++i) V[i * k1 + b] = v[i];
+  }
+  // enforce exact conjugate pairs: for each lam with Im > 0 find its partner
+  bool used[MAXK1] = {false};
+  int keep[MAXK1], nk = 0, partner[MAXK1];
+  for (int b = 0; b < k1; ++b) partner[b] = -1;
+  for (int b = 0; b < k1; ++b) {
+    if (used[b]) continue;
+    used[b] = true;
+    if (lam[b].imag() == 0.0) {
+      keep[nk++] = b;
+      continue;
+    }
+    int best = -1;
+    double bd = 1e300;
+    for (int c = 0; c < k1; ++c)
+      if (!used[c]) {
+        const double d = std::abs(lam[c] - std::conj(lam[b]));
+        if (d < bd) {
+          bd = d;
+          best = c;
+        }
+      }
+    if (best < 0 || bd > 1e-8 * std::abs(lam[b])) return false;
+    used[best] = true;
+    const int pos = lam[b].imag() > 0.0 ? b : best, neg = pos == b ? best : b;
+    lam[neg] = std::conj(lam[pos]);
+    for (int i = 0; i < k1; ++i) V[i * k1 + neg] = std::conj(V[i * k1 + pos]);
+    keep[nk++] = pos;
+    partner[pos] = neg;
+  }
+  cplx Vi[MAXK1 * MAXK1];
+  for (int i = 0; i < k1 * k1; ++i) Vi[i] = V[i];
+  if (!cinv(k1, Vi)) return false;
+  // residual check |S V - V Lam| and conditioning
+  double res = 0.0, vn = 0.0, vin = 0.0;
+  for (int i = 0; i < k1; ++i)
+    for (int b = 0; b < k1; ++b) {
+      cplx sv = 0.0;
+      for (int j = 0; j < k1; ++j) sv += S[i * k1 + j] * V[j * k1 + b];
+      res = std::max(res, std::abs(sv - lam[b] * V[i * k1 + b]));
+      vn = std::max(vn, std::abs(V[i * k1 + b]));
+      vin = std::max(vin, std::abs(Vi[i * k1 + b]));
+    }
+  if (!(res <= 1e-12 * snorm * vn) || !(vn * vin < 1e6)) return false;
+  out.nblk = nk;
+  for (int s = 0; s < nk; ++s) {
+    const int b = keep[s];
+    out.pair[s] = partner[b] >= 0 ? 1 : 0;
+    out.lam_re[s] = lam[b].real();
+    out.lam_im[s] = lam[b].imag();
+    for (int mu = 0; mu < k1; ++mu) {
+      out.V_re[mu * MAXK1 + s] = V[mu * k1 + b].real();
+      out.V_im[mu * MAXK1 + s] = V[mu * k1 + b].imag();
+      out.Vi_re[s * MAXK1 + mu] = Vi[b * k1 + mu].real();
+      out.Vi_im[s * MAXK1 + mu] = Vi[b * k1 + mu].imag();
+    }
+  }
+  return true;
+}
+
+namespace {
+
+__device__ __forceinline__ double m1g_d(int X, int Xp, int n) {
+  double s = 0.0;
+  const int lo = max(0, (max(X, Xp) - 1) / 2);
+  for (int c = lo; c <= min(X, Xp) / 2 && c < n; ++c) {
+    const int a = X - 2 * c, b = Xp - 2 * c;
+    if (a >= 0 && a <= 2 && b >= 0 && b <= 2) s += c_tab.M1[a][b];
+  }
+  return s;
+}
+
+__device__ __forceinline__ double cabs1(double2 z) { return fabs(z.x) + fabs(z.y); }
+
+// One warp per (patch, stored eigen-block): C = lam Mhat + Jhat (21x21
+// complex) in shared memory, Gauss-Jordan with partial pivoting (izamax /
+// dcabs1 pivot choice as zgetrf), output transposed binvT[K][b][j][r].
+__global__ void __launch_bounds__(128) k_invert_diag(Geom g, TimeDiag td, const double* __restrict__ spatial,
+                                                     double2* __restrict__ binvT, int* __restrict__ bad) {
+  constexpr int N = 21, LD = 22, WPB = 4;
+  __shared__ double2 sm[WPB][N * LD];
+  __shared__ double2 colb[WPB][N];
+  __shared__ int perm[WPB][N];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int task = blockIdx.x * WPB + warp;
+  if (task >= g.ncells * td.nblk) return;
+  const int K = task / td.nblk, b = task % td.nblk;
+  const int ki = K % g.nx, kj = K / g.nx;
+  double2* A = sm[warp];
+  const double lr = td.lam_re[b], li = td.lam_im[b];
+  for (int idx = lane; idx < N * N; idx += 32) {
+    const int i = idx / N, j = idx % N;
+    double m = 0.0;
+    if (i < 18 && j < 18 && (i & 1) == (j & 1)) {
+      const int ia = i >> 1, jb = j >> 1;
+      m = g.hx * g.hy * (m1g_d(2 * kj + ia / 3, 2 * kj + jb / 3, g.ny) * m1g_d(2 * ki + ia % 3, 2 * ki + jb % 3, g.nx));
+    }
+    const double jv = spatial[(size_t)K * 441 + idx];
+    A[i * LD + j] = make_double2(fma(lr, m, jv), li * m);
+  }
+  __syncwarp();
+  bool singular = false;
+  for (int k = 0; k < N; ++k) {
+    double best = -1.0;
+    int bi = N;
+    const int i = k + lane;
+    if (i < N) {
+      best = cabs1(A[i * LD + k]);
+      bi = i;
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (ov > best || (ov == best && oi < bi)) {
+        best = ov;
+        bi = oi;
+      }
+    }
+    if (!(best > 0.0)) {
+      singular = true;
+      break;
+    }
+    if (lane == 0) perm[warp][k] = bi;
+    if (bi != k && lane < N) {
+      const double2 t = A[k * LD + lane];
+      A[k * LD + lane] = A[bi * LD + lane];
+      A[bi * LD + lane] = t;
+    }
+    __syncwarp();
+    const double2 p = A[k * LD + k];
+    const double den = p.x * p.x + p.y * p.y;
+    const double2 pinv = make_double2(p.x / den, -p.y / den);
+    __syncwarp();
+    if (lane < N) {
+      const double2 a = (lane == k) ? make_double2(1.0, 0.0) : A[k * LD + lane];
+      A[k * LD + lane] = make_double2(a.x * pinv.x - a.y * pinv.y, a.x * pinv.y + a.y * pinv.x);
+      colb[warp][lane] = A[lane * LD + k];
+    }
+    __syncwarp();
+    for (int idx = lane; idx < N * N; idx += 32) {
+      const int r = idx / N, j = idx - r * N;
+      if (r == k) continue;
+      const double2 f = colb[warp][r];
+      const double2 base = (j == k) ? make_double2(0.0, 0.0) : A[r * LD + j];
+      const double2 a = A[k * LD + j];
+      A[r * LD + j] = make_double2(base.x - (f.x * a.x - f.y * a.y), base.y - (f.x * a.y + f.y * a.x));
+    }
+    __syncwarp();
+  }
+  if (singular) {
+    if (lane == 0) atomicMin(bad, K);
+    return;
+  }
+  for (int k = N - 1; k >= 0; --k) {
+    const int p = perm[warp][k];
+    if (p != k && lane < N) {
+      const double2 t = A[lane * LD + k];
+      A[lane * LD + k] = A[lane * LD + p];
+      A[lane * LD + p] = t;
+    }
+    __syncwarp();
+  }
+  double2* dst = binvT + ((size_t)K * td.nblk + b) * N * N;
+  for (int idx = lane; idx < N * N; idx += 32) {
+    const int j = idx / N, r = idx - j * N;
+    dst[idx] = A[r * LD + j];
+  }
+}
+
+__device__ __forceinline__ size_t patch_dof_d(const Geom& g, int K, int l) {
+  const int mu = l / 21, s = l % 21;
+  const size_t base = (size_t)mu * g.nd;
+  if (s >= 18) return base + g.mv + 3 * (size_t)K + (s - 18);
+  const int a = s >> 1, d = s & 1;
+  const int ki = K % g.nx, kj = K / g.nx;
+  return base + 2 * ((size_t)(2 * kj + a / 3) * g.nnx + 2 * ki + a % 3) + d;
+}
+
+// upd_K = A_K^-1 e_K via the temporal diagonalization; threads (patch, row r).
+template <int K1, int NB>
+__global__ void __launch_bounds__(252) k_vanka_gemv_diag(Geom g, TimeDiag td, const double2* __restrict__ binvT,
+                                                         const double* __restrict__ defect, double* __restrict__ upd) {
+  constexpr int PB = 12;
+  __shared__ double2 gs[PB][NB][21];
+  const int p = threadIdx.x / 21, r = threadIdx.x % 21;
+  const int K = blockIdx.x * PB + p;
+  const bool active = K < g.ncells;
+  if (active) {
+    double f[K1];
+#pragma unroll
+    for (int mu = 0; mu < K1; ++mu) f[mu] = __ldg(defect + patch_dof_d(g, K, 21 * mu + r)) * td.itw[mu];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      double gr = 0.0, gi = 0.0;
+#pragma unroll
+      for (int mu = 0; mu < K1; ++mu) {
+        gr = fma(td.Vi_re[b * MAXK1 + mu], f[mu], gr);
+        gi = fma(td.Vi_im[b * MAXK1 + mu], f[mu], gi);
+      }
+      gs[p][b][r] = make_double2(gr, gi);
+    }
+  }
+  __syncthreads();
+  if (!active) return;
+  double hr[NB], hi[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const double2* col = binvT + ((size_t)K * NB + b) * 441 + r;
+    double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
+#pragma unroll 7
+    for (int j = 0; j < 21; ++j) {
+      const double2 m = __ldg(col + 21 * j);
+      const double2 v = gs[p][b][j];
+      ar = fma(m.x, v.x, ar);
+      br = fma(m.y, v.y, br);
+      ai = fma(m.x, v.y, ai);
+      bi = fma(m.y, v.x, bi);
+    }
+    hr[b] = ar - br;
+    hi[b] = ai + bi;
+  }
+  double* o = upd + (size_t)K * 21 * K1;
+#pragma unroll
+  for (int mu = 0; mu < K1; ++mu) {
+    double s = 0.0;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const double re = td.V_re[mu * MAXK1 + b] * hr[b] - td.V_im[mu * MAXK1 + b] * hi[b];
+      s += td.pair[b] ? 2.0 * re : re;
+    }
+    o[21 * mu + r] = s;
+  }
+}
+
+}  // namespace
+
+cudaError_t patch_invert_diag(const Geom& g, const TimeDiag& td, const double* spatial, double2* binvT, int* bad,
+                              cudaStream_t st) {
+  const int tasks = g.ncells * td.nblk;
+  k_invert_diag<<<(tasks + 3) / 4, 128, 0, st>>>(g, td, spatial, binvT, bad);
+  return cudaGetLastError();
+}
+
+cudaError_t vanka_gemv_diag(const Geom& g, const TimeDiag& td, const double2* binvT, const double* defect,
+                            double* upd, cudaStream_t st) {
+  const unsigned grid = (unsigned)((g.ncells + 11) / 12);
+  switch (td.k1 * 10 + td.nblk) {
+    case 11: k_vanka_gemv_diag<1, 1><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd); break;
+    case 21: k_vanka_gemv_diag<2, 1><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd); break;
+    case 22: k_vanka_gemv_diag<2, 2><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd); break;
+    case 32: k_vanka_gemv_diag<3, 2><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd); break;
+    case 33: k_vanka_gemv_diag<3, 3><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd); break;
+    case 42: k_vanka_gemv_diag<4, 2><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd); break;
+    case 43: k_vanka_gemv_diag<4, 3><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd); break;
+    case 44: k_vanka_gemv_diag<4, 4><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd); break;
+    default: return cudaErrorNotSupported;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace pdst

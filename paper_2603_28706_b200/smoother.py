@@ -55,6 +55,12 @@ class VankaLevel:
         L.check(L.lib().pdst_patch_matrices(self.dev.h, self.index, L.vptr(out)), "pdst_patch_matrices")
         return out
 
+    def patch_info(self):
+        """(D, diagonalized complex blocks per patch, bytes streamed per patch per sweep)."""
+        D, nb, by = C.c_int32(), C.c_int32(), C.c_int64()
+        L.check(L.lib().pdst_patch_info(self.dev.h, self.index, C.byref(D), C.byref(nb), C.byref(by)), "pdst_patch_info")
+        return D.value, nb.value, by.value
+
     def patch_ids(self) -> np.ndarray:
         nc = self.ncells
         cn = np.empty((nc, 9), dtype=np.int64)
