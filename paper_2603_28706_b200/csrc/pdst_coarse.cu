@@ -1,0 +1,744 @@
+// pdst_coarse.cu — multigrid levels: grid transfers, Galerkin coarse
+// operators in element form, coarse level apply, coarse patches and the
+// coarsest-level dense solve (sm_100a, fp64).
+//
+// Reference (file:line into /root/reference/pkg/src/pdflow):
+//   transfer_build (Q2 nodal interpolation, P1disc child rewrite)  solver/multigrid.py:90-154
+//   _restrict / _prolong (per Radau node)                           solver/multigrid.py:523-543
+//   coarse_operator (Galerkin P' J P per node)                       solver/multigrid.py:302-324
+//   coarse mass P_v' M P_v                                           solver/multigrid.py:459-460
+//   _sparse_level_matvec                                             solver/multigrid.py:234-248
+//   _build_coarse_solver (dense, pressure pinning) / vcycle          solver/multigrid.py:494-578
+//
+// Element form of a level operator (per Radau node mu):
+//   ecell[mu][c][i][j]            21x21 cell block (volume + boundary, plus the
+//                                  CIP couplings of fine faces interior to c)
+//   fv[mu][fj*(nx-1)+fi][sA][sB][a][b]  vertical face (fi,fj)|(fi+1,fj): 9x9 node
+//   fh[mu][fj*nx+fi][sA][sB][a][b]      horizontal face (fi,fj)|(fi,fj+1) blocks,
+//                                  identity in the velocity component (I2).
+// Because the fine values of a child cell depend only on its parent's 9
+// coarse nodes / 3 pressure coefficients, P' J P is exactly the sum of the
+// children's P_K' E_K P_K plus the face blocks mapped the same way.  The
+// coarse mass is the coarse Q2 mass (exact for nested spaces).
+#include <cuda_runtime.h>
+
+#include "pdst_coarse.h"
+#include "pdst_device.cuh"
+
+namespace pdst {
+namespace {
+
+__device__ __forceinline__ double lag(int i, double x) {
+  return i == 0 ? (1.0 - x) * (1.0 - 2.0 * x) : i == 1 ? 4.0 * x * (1.0 - x) : x * (2.0 * x - 1.0);
+}
+
+__device__ __forceinline__ double m1g(int X, int Xp, int n) {
+  double s = 0.0;
+  const int lo = max(0, (max(X, Xp) - 1) / 2);
+  for (int c = lo; c <= min(X, Xp) / 2 && c < n; ++c) {
+    const int a = X - 2 * c, b = Xp - 2 * c;
+    if (a >= 0 && a <= 2 && b >= 0 && b <= 2) s += c_tab.M1[a][b];
+  }
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// Transfers (multigrid.py:90-154): fine node (X, Y) of the half-cell grid lies
+// in coarse cell (min(X/4, ncx-1), min(Y/4, ncy-1)) at local coordinate X/4 - cx.
+// ---------------------------------------------------------------------------
+__global__ void k_prolong(Geom gc, Geom gf, int k1, const double* __restrict__ ec, double* __restrict__ ef) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int mu = blockIdx.y;
+  const size_t nnf = (size_t)gf.nnx * gf.nny;
+  const double* e = ec + (size_t)mu * gc.nd;
+  double* o = ef + (size_t)mu * gf.nd;
+  if (t < nnf) {
+    const int X = (int)(t % gf.nnx), Y = (int)(t / gf.nnx);
+    const int cx = min(X / 4, gc.nx - 1), cy = min(Y / 4, gc.ny - 1);
+    const double xi = X / 4.0 - cx, eta = Y / 4.0 - cy;
+    double s0 = 0.0, s1 = 0.0;
+    for (int jy = 0; jy < 3; ++jy) {
+      const double ly = lag(jy, eta);
+      if (ly == 0.0) continue;
+      for (int jx = 0; jx < 3; ++jx) {
+        const double w = ly * lag(jx, xi);
+        if (w == 0.0) continue;
+        const size_t node = (size_t)(2 * cy + jy) * gc.nnx + 2 * cx + jx;
+        s0 += w * e[2 * node];
+        s1 += w * e[2 * node + 1];
+      }
+    }
+    o[2 * t] = s0;
+    o[2 * t + 1] = s1;
+  } else if (t < nnf + (size_t)gf.ncells) {
+    const int cf = (int)(t - nnf);
+    const int fi = cf % gf.nx, fj = cf / gf.nx;
+    const int ox = fi & 1, oy = fj & 1;
+    const int c = (fj >> 1) * gc.nx + (fi >> 1);
+    const double* pc = e + gc.mv + 3 * (size_t)c;
+    double* pf = o + gf.mv + 3 * (size_t)cf;
+    pf[0] = pc[0] + (2 * ox - 1) / 4.0 * pc[1] + (2 * oy - 1) / 4.0 * pc[2];
+    pf[1] = 0.5 * pc[1];
+    pf[2] = 0.5 * pc[2];
+  }
+}
+
+__global__ void k_restrict(Geom gc, Geom gf, int k1, const double* __restrict__ rf, double* __restrict__ rc) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int mu = blockIdx.y;
+  const size_t nnc = (size_t)gc.nnx * gc.nny;
+  const double* r = rf + (size_t)mu * gf.nd;
+  double* o = rc + (size_t)mu * gc.nd;
+  if (t < nnc) {
+    const int Xc = (int)(t % gc.nnx), Yc = (int)(t / gc.nnx);
+    double s0 = 0.0, s1 = 0.0;
+    for (int Y = max(0, 2 * Yc - 4); Y <= min(gf.nny - 1, 2 * Yc + 4); ++Y) {
+      const int cy = min(Y / 4, gc.ny - 1), my = Yc - 2 * cy;
+      if (my < 0 || my > 2) continue;
+      const double wy = lag(my, Y / 4.0 - cy);
+      if (wy == 0.0) continue;
+      for (int X = max(0, 2 * Xc - 4); X <= min(gf.nnx - 1, 2 * Xc + 4); ++X) {
+        const int cx = min(X / 4, gc.nx - 1), mx = Xc - 2 * cx;
+        if (mx < 0 || mx > 2) continue;
+        const double w = wy * lag(mx, X / 4.0 - cx);
+        if (w == 0.0) continue;
+        const size_t node = (size_t)Y * gf.nnx + X;
+        s0 += w * r[2 * node];
+        s1 += w * r[2 * node + 1];
+      }
+    }
+    o[2 * t] = s0;
+    o[2 * t + 1] = s1;
+  } else if (t < nnc + (size_t)gc.ncells) {
+    const int c = (int)(t - nnc);
+    const int ci = c % gc.nx, cj = c / gc.nx;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int oy = 0; oy < 2; ++oy)
+      for (int ox = 0; ox < 2; ++ox) {
+        const size_t cf = (size_t)(2 * cj + oy) * gf.nx + 2 * ci + ox;
+        const double* pf = r + gf.mv + 3 * cf;
+        s0 += pf[0];
+        s1 += (2 * ox - 1) / 4.0 * pf[0] + 0.5 * pf[1];
+        s2 += (2 * oy - 1) / 4.0 * pf[0] + 0.5 * pf[2];
+      }
+    double* pc = o + gc.mv + 3 * (size_t)c;
+    pc[0] = s0;
+    pc[1] = s1;
+    pc[2] = s2;
+  }
+}
+
+// Local prolongation of child (ox, oy): Pk[i][j] maps the parent's 21 local
+// dofs (j) to the child's 21 local dofs (i).
+__device__ double ploc(int ox, int oy, int i, int j) {
+  if (i < 18 && j < 18) {
+    if ((i & 1) != (j & 1)) return 0.0;
+    const int af = i >> 1, bc = j >> 1;
+    const double xi = (2 * ox + af % 3) / 4.0, eta = (2 * oy + af / 3) / 4.0;
+    return lag(bc % 3, xi) * lag(bc / 3, eta);
+  }
+  if (i >= 18 && j >= 18) {
+    const int fi = i - 18, cj = j - 18;
+    if (fi == 0) return cj == 0 ? 1.0 : cj == 1 ? (2 * ox - 1) / 4.0 : (2 * oy - 1) / 4.0;
+    if (fi == 1) return cj == 1 ? 0.5 : 0.0;
+    return cj == 2 ? 0.5 : 0.0;
+  }
+  return 0.0;
+}
+
+// Fine-level CIP face block entry (on the fly from the lagged state):
+// coef sum_q (w_q h) |a_L . n| gA_a(q) gB_b(q), g^L = +dE(1) B ihn, g^R = -dE(0) B ihn.
+__device__ double cip_block(const Geom& g, const Disc& ds, const double* v, int axis, int fi, int fj, int sA, int a,
+                            int sB, int b) {
+  const double hface = axis == 0 ? g.hy : g.hx;
+  const double ihn = axis == 0 ? g.ihx : g.ihy;
+  const double coef = ds.gamma_cip * hface * hface * ihn * ihn;
+  const int na = axis == 0 ? a % 3 : a / 3, ta = axis == 0 ? a / 3 : a % 3;
+  const int nb = axis == 0 ? b % 3 : b / 3, tb = axis == 0 ? b / 3 : b % 3;
+  const double fa = sA == 0 ? c_tab.dE[1][na] : -c_tab.dE[0][na];
+  const double fb = sB == 0 ? c_tab.dE[1][nb] : -c_tab.dE[0][nb];
+  double s = 0.0;
+  for (int q = 0; q < 4; ++q) {
+    double tr = 0.0;
+    for (int t = 0; t < 3; ++t) {
+      const size_t node = axis == 0 ? (size_t)(2 * fj + t) * g.nnx + 2 * fi + 2 : (size_t)(2 * fj + 2) * g.nnx + 2 * fi + t;
+      tr = fma(c_tab.B[q][t], v[2 * node + axis], tr);
+    }
+    s += (c_tab.w[q] * hface) * fabs(tr) * (fa * c_tab.B[q][ta]) * (fb * c_tab.B[q][tb]);
+  }
+  return coef * s;
+}
+
+// Face block entry of a level (stored for coarse levels, on the fly for the finest).
+__device__ __forceinline__ double face_entry(const LevelOp& op, int mu, int axis, int fi, int fj, int sA, int a, int sB,
+                                             int b) {
+  if (op.fine) {
+    if (!(op.ds.convection && op.ds.gamma_cip > 0.0)) return 0.0;
+    return cip_block(op.g, op.ds, op.state + (size_t)mu * op.g.mv, axis, fi, fj, sA, a, sB, b);
+  }
+  const double* F = axis == 0 ? op.fv + ((size_t)mu * (op.g.nx - 1) * op.g.ny + (size_t)fj * (op.g.nx - 1) + fi) * 324
+                              : op.fh + ((size_t)mu * op.g.nx * (op.g.ny - 1) + (size_t)fj * op.g.nx + fi) * 324;
+  return F[((sA * 2 + sB) * 9 + a) * 9 + b];
+}
+
+__device__ __forceinline__ double cell_entry(const LevelOp& op, int mu, int c, int i, int j) {
+  // finest level: column-major ET[c][j][i]; coarse levels: row-major ecell[c][i][j]
+  const size_t base = ((size_t)mu * op.g.ncells + c) * 441;
+  return op.fine ? op.ecell[base + (size_t)j * 21 + i] : op.ecell[base + (size_t)i * 21 + j];
+}
+
+// Galerkin coarse cell block: one CTA (448 threads) per (coarse cell, mu).
+__global__ void __launch_bounds__(448) k_galerkin_cells(LevelOp f, Geom gc, double* __restrict__ ecell_c) {
+  __shared__ double T[21][22];
+  __shared__ double Pm[4][21][21];
+  __shared__ double F[9][10];
+  const int C = blockIdx.x, mu = blockIdx.y;
+  const int t = threadIdx.x;
+  const int ci = C % gc.nx, cj = C / gc.nx;
+  for (int idx = t; idx < 4 * 441; idx += blockDim.x) {
+    const int k = idx / 441, e = idx % 441;
+    Pm[k][e / 21][e % 21] = ploc(k & 1, k >> 1, e / 21, e % 21);
+  }
+  const int i = t / 21, j = t % 21;
+  double acc = 0.0;
+  __syncthreads();
+  for (int k = 0; k < 4; ++k) {
+    const int ox = k & 1, oy = k >> 1;
+    const int K = (2 * cj + oy) * f.g.nx + 2 * ci + ox;
+    // T = E_K P_K  (rows = child dofs, cols = parent dofs)
+    if (t < 441) {
+      double s = 0.0;
+      for (int m = 0; m < 21; ++m) s = fma(cell_entry(f, mu, K, i, m), Pm[k][m][j], s);
+      T[i][j] = s;
+    }
+    __syncthreads();
+    if (t < 441) {
+      double s = 0.0;
+      for (int m = 0; m < 21; ++m) s = fma(Pm[k][m][i], T[m][j], s);
+      acc += s;
+    }
+    __syncthreads();
+  }
+  // fine faces interior to C: vertical (children (0,oy)|(1,oy)), horizontal ((ox,0)|(ox,1))
+  for (int fidx = 0; fidx < 4; ++fidx) {
+    const int axis = fidx < 2 ? 0 : 1;
+    const int o = fidx & 1;
+    const int kl = axis == 0 ? (o * 2 + 0) : (0 * 2 + o);  // child index k = ox + 2 oy of the left/lower cell
+    const int kr = axis == 0 ? (o * 2 + 1) : (1 * 2 + o);
+    const int fi = 2 * ci + (axis == 0 ? 0 : o), fj = 2 * cj + (axis == 0 ? o : 0);
+    for (int sA = 0; sA < 2; ++sA)
+      for (int sB = 0; sB < 2; ++sB) {
+        if (t < 81) F[t / 9][t % 9] = face_entry(f, mu, axis, fi, fj, sA, t / 9, sB, t % 9);
+        __syncthreads();
+        if (t < 441 && i < 18 && j < 18) {
+          const int kA = sA == 0 ? kl : kr, kB = sB == 0 ? kl : kr;
+          // sum_{a,b} P_kA[2a+d][i] F[a][b] P_kB[2b+d][j]  (I2: component d of i and j must agree)
+          if ((i & 1) == (j & 1)) {
+            const int d = i & 1;
+            double s = 0.0;
+            for (int a = 0; a < 9; ++a) {
+              const double pa = Pm[kA][2 * a + d][i];
+              if (pa == 0.0) continue;
+              double sb = 0.0;
+              for (int b = 0; b < 9; ++b) sb = fma(F[a][b], Pm[kB][2 * b + d][j], sb);
+              s = fma(pa, sb, s);
+            }
+            acc += s;
+          }
+        }
+        __syncthreads();
+      }
+  }
+  if (t < 441) ecell_c[((size_t)mu * gc.ncells + C) * 441 + t] = acc;
+}
+
+// Galerkin coarse face blocks from the two fine faces lying on the coarse face.
+// One CTA (324 threads: sA, sB, a, b) per (coarse face, mu); axis via blockIdx.z.
+__global__ void __launch_bounds__(324) k_galerkin_faces(LevelOp f, Geom gc, double* __restrict__ fv_c,
+                                                        double* __restrict__ fh_c) {
+  __shared__ double Pn[4][9][9];  // node-level prolongation of child k: Pn[k][a_fine][b_coarse]
+  __shared__ double F[2][2][9][9];
+  const int axis = blockIdx.z, mu = blockIdx.y;
+  const int nfx = axis == 0 ? gc.nx - 1 : gc.nx;
+  const int nface = axis == 0 ? (gc.nx - 1) * gc.ny : gc.nx * (gc.ny - 1);
+  const int fc = blockIdx.x;
+  if (fc >= nface) return;
+  const int fi = fc % nfx, fj = fc / nfx;
+  const int t = threadIdx.x;
+  for (int idx = t; idx < 4 * 81; idx += blockDim.x) {
+    const int k = idx / 81, e = idx % 81;
+    Pn[k][e / 9][e % 9] = ploc(k & 1, k >> 1, 2 * (e / 9), 2 * (e % 9));
+  }
+  const int sA = t / 162, sB = (t / 81) % 2, a = (t / 9) % 9, b = t % 9;
+  double acc = 0.0;
+  for (int o = 0; o < 2; ++o) {
+    // fine face: vertical between (2fi+1, 2fj+o) and (2fi+2, 2fj+o); horizontal between (2fi+o, 2fj+1) and (2fi+o, 2fj+2)
+    const int ffi = axis == 0 ? 2 * fi + 1 : 2 * fi + o, ffj = axis == 0 ? 2 * fj + o : 2 * fj + 1;
+    const int kl = axis == 0 ? (1 + 2 * o) : (o + 2 * 1);  // child index in the left/lower coarse cell
+    const int kr = axis == 0 ? (0 + 2 * o) : (o + 2 * 0);  // child index in the right/upper coarse cell
+    __syncthreads();
+    if (t < 324) F[sA][sB][a][b] = face_entry(f, mu, axis, ffi, ffj, sA, a, sB, b);
+    __syncthreads();
+    if (t < 324) {
+      const int kA = sA == 0 ? kl : kr, kB = sB == 0 ? kl : kr;
+      double s = 0.0;
+      for (int p = 0; p < 9; ++p) {
+        const double pa = Pn[kA][p][a];
+        if (pa == 0.0) continue;
+        double sb = 0.0;
+        for (int q = 0; q < 9; ++q) sb = fma(F[sA][sB][p][q], Pn[kB][q][b], sb);
+        s = fma(pa, sb, s);
+      }
+      acc += s;
+    }
+  }
+  if (t < 324) {
+    double* dst = axis == 0 ? fv_c + ((size_t)mu * nface + fc) * 324 : fh_c + ((size_t)mu * nface + fc) * 324;
+    dst[t] = acc;
+  }
+}
+
+// Coarse level apply (node gather, deterministic):
+// y_mu = tau w_mu J_mu x_mu + sum_nu K_t[mu,nu] M x_nu (multigrid.py:234-248);
+// rhs != null gives y = rhs - A x.
+__global__ void k_level_apply(LevelOp op, TimeData td, const double* __restrict__ x, const double* __restrict__ rhs,
+                              double* __restrict__ y) {
+  const Geom& g = op.g;
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int mu = blockIdx.y;
+  const size_t nn = (size_t)g.nnx * g.nny;
+  const double* xm = x + (size_t)mu * g.nd;
+  double out0 = 0.0, out1 = 0.0;
+  size_t o0;
+  if (t < nn) {
+    const int X = (int)(t % g.nnx), Y = (int)(t / g.nnx);
+    o0 = (size_t)mu * g.nd + 2 * t;
+    double j0 = 0.0, j1 = 0.0;
+    for (int cy = max(0, (Y - 1) / 2); cy <= min(g.ny - 1, Y / 2); ++cy)
+      for (int cx = max(0, (X - 1) / 2); cx <= min(g.nx - 1, X / 2); ++cx) {
+        const int c = cy * g.nx + cx;
+        const int a = 3 * (Y - 2 * cy) + (X - 2 * cx);
+        for (int jj = 0; jj < 21; ++jj) {
+          double xv;
+          if (jj < 18) {
+            const int bb = jj >> 1;
+            xv = xm[2 * ((size_t)(2 * cy + bb / 3) * g.nnx + 2 * cx + bb % 3) + (jj & 1)];
+          } else {
+            xv = xm[g.mv + 3 * (size_t)c + jj - 18];
+          }
+          j0 = fma(cell_entry(op, mu, c, 2 * a, jj), xv, j0);
+          j1 = fma(cell_entry(op, mu, c, 2 * a + 1, jj), xv, j1);
+        }
+      }
+    // faces whose two cells contain the node
+    for (int axis = 0; axis < 2; ++axis) {
+      const int nfx = axis == 0 ? g.nx - 1 : g.nx, nfy = axis == 0 ? g.ny : g.ny - 1;
+      const int xr = axis == 0 ? 4 : 2, yr = axis == 0 ? 2 : 4;  // node extent of L u R
+      for (int fj = max(0, (Y - yr + 1) / 2); fj <= min(nfy - 1, Y / 2); ++fj)
+        for (int fi = max(0, (X - xr + 1) / 2); fi <= min(nfx - 1, X / 2); ++fi) {
+          const int cl = fj * g.nx + fi;
+          const int cr = axis == 0 ? cl + 1 : cl + g.nx;
+          for (int sA = 0; sA < 2; ++sA) {
+            const int cA = sA == 0 ? cl : cr;
+            const int ax = X - 2 * (cA % g.nx), ay = Y - 2 * (cA / g.nx);
+            if (ax < 0 || ax > 2 || ay < 0 || ay > 2) continue;
+            const int a = 3 * ay + ax;
+            for (int sB = 0; sB < 2; ++sB) {
+              const int cB = sB == 0 ? cl : cr;
+              const int bxo = 2 * (cB % g.nx), byo = 2 * (cB / g.nx);
+              for (int bb = 0; bb < 9; ++bb) {
+                const double fvv = face_entry(op, mu, axis, fi, fj, sA, a, sB, bb);
+                const size_t nb = (size_t)(byo + bb / 3) * g.nnx + bxo + bb % 3;
+                j0 = fma(fvv, xm[2 * nb], j0);
+                j1 = fma(fvv, xm[2 * nb + 1], j1);
+              }
+            }
+          }
+        }
+    }
+    // temporal mass coupling on the coarse Q2 mass
+    double m0 = 0.0, m1 = 0.0;
+    for (int Yp = max(0, Y - 2); Yp <= min(g.nny - 1, Y + 2); ++Yp) {
+      const double my = m1g(Y, Yp, g.ny);
+      if (my == 0.0) continue;
+      for (int Xp = max(0, X - 2); Xp <= min(g.nnx - 1, X + 2); ++Xp) {
+        const double mx = m1g(X, Xp, g.nx);
+        if (mx == 0.0) continue;
+        const size_t nb = (size_t)Yp * g.nnx + Xp;
+        double x0 = 0.0, x1 = 0.0;
+        for (int nu = 0; nu < td.k1; ++nu) {
+          x0 = fma(td.K_t[mu * td.k1 + nu], x[(size_t)nu * g.nd + 2 * nb], x0);
+          x1 = fma(td.K_t[mu * td.k1 + nu], x[(size_t)nu * g.nd + 2 * nb + 1], x1);
+        }
+        m0 = fma(my * mx, x0, m0);
+        m1 = fma(my * mx, x1, m1);
+      }
+    }
+    const double h = g.hx * g.hy;
+    out0 = td.tau_w[mu] * j0 + h * m0;
+    out1 = td.tau_w[mu] * j1 + h * m1;
+    y[o0] = rhs ? rhs[o0] - out0 : out0;
+    y[o0 + 1] = rhs ? rhs[o0 + 1] - out1 : out1;
+  } else if (t < nn + (size_t)g.ncells) {
+    const int c = (int)(t - nn);
+    const int cx = c % g.nx, cy = c / g.nx;
+    for (int r = 0; r < 3; ++r) {
+      double s = 0.0;
+      for (int jj = 0; jj < 21; ++jj) {
+        double xv;
+        if (jj < 18) {
+          const int bb = jj >> 1;
+          xv = xm[2 * ((size_t)(2 * cy + bb / 3) * g.nnx + 2 * cx + bb % 3) + (jj & 1)];
+        } else {
+          xv = xm[g.mv + 3 * (size_t)c + jj - 18];
+        }
+        s = fma(cell_entry(op, mu, c, 18 + r, jj), xv, s);
+      }
+      const size_t o = (size_t)mu * g.nd + g.mv + 3 * (size_t)c + r;
+      const double v = td.tau_w[mu] * s;
+      y[o] = rhs ? rhs[o] - v : v;
+    }
+  }
+}
+
+__device__ __forceinline__ int ceil_half(int v) { return v <= 0 ? -((-v) / 2) : (v + 1) / 2; }
+__device__ __forceinline__ int floor_half(int v) { return v >= 0 ? v / 2 : -((-v + 1) / 2); }
+
+// (R_K J R_K')_{ij} of a level in element form.
+__device__ double level_spatial_entry(const LevelOp& op, int mu, int K, int i, int j) {
+  const Geom& g = op.g;
+  if (i >= 18 || j >= 18) return cell_entry(op, mu, K, i, j);
+  const int ki = K % g.nx, kj = K / g.nx;
+  const int ia = i >> 1, d = i & 1, jb = j >> 1, e = j & 1;
+  const int XA = 2 * ki + ia % 3, YA = 2 * kj + ia / 3;
+  const int XB = 2 * ki + jb % 3, YB = 2 * kj + jb / 3;
+  const int xmin = min(XA, XB), xmax = max(XA, XB), ymin = min(YA, YB), ymax = max(YA, YB);
+  double val = 0.0;
+  for (int cy = max(0, ceil_half(ymax - 2)); cy <= min(g.ny - 1, floor_half(ymin)); ++cy)
+    for (int cx = max(0, ceil_half(xmax - 2)); cx <= min(g.nx - 1, floor_half(xmin)); ++cx) {
+      const int c = cy * g.nx + cx;
+      const int al = 3 * (YA - 2 * cy) + (XA - 2 * cx), bl = 3 * (YB - 2 * cy) + (XB - 2 * cx);
+      val += cell_entry(op, mu, c, 2 * al + d, 2 * bl + e);
+    }
+  if (d != e) return val;
+  for (int axis = 0; axis < 2; ++axis) {
+    const int nfx = axis == 0 ? g.nx - 1 : g.nx, nfy = axis == 0 ? g.ny : g.ny - 1;
+    const int xr = axis == 0 ? 4 : 2, yr = axis == 0 ? 2 : 4;
+    for (int fj = max(0, ceil_half(ymax - yr)); fj <= min(nfy - 1, floor_half(ymin)); ++fj)
+      for (int fi = max(0, ceil_half(xmax - xr)); fi <= min(nfx - 1, floor_half(xmin)); ++fi) {
+        const int cl = fj * g.nx + fi, cr = axis == 0 ? cl + 1 : cl + g.nx;
+        for (int sA = 0; sA < 2; ++sA) {
+          const int cA = sA == 0 ? cl : cr;
+          const int ax = XA - 2 * (cA % g.nx), ay = YA - 2 * (cA / g.nx);
+          if (ax < 0 || ax > 2 || ay < 0 || ay > 2) continue;
+          for (int sB = 0; sB < 2; ++sB) {
+            const int cB = sB == 0 ? cl : cr;
+            const int bx = XB - 2 * (cB % g.nx), by = YB - 2 * (cB / g.nx);
+            if (bx < 0 || bx > 2 || by < 0 || by > 2) continue;
+            val += face_entry(op, mu, axis, fi, fj, sA, 3 * ay + ax, sB, 3 * by + bx);
+          }
+        }
+      }
+  }
+  return val;
+}
+
+// Exact coarse patches: A_K = sum K_t (x) R_K M R_K' + tau w_mu R_K J_mu R_K'.
+__global__ void __launch_bounds__(448) k_patch_level(LevelOp op, TimeData td, double* __restrict__ mats) {
+  const int K = blockIdx.x;
+  const int t = threadIdx.x;
+  if (t >= 441) return;
+  const Geom& g = op.g;
+  const int i = t / 21, j = t % 21;
+  const int k1 = td.k1, D = 21 * k1;
+  double M = 0.0;
+  if (i < 18 && j < 18 && (i & 1) == (j & 1)) {
+    const int ki = K % g.nx, kj = K / g.nx;
+    const int ia = i >> 1, jb = j >> 1;
+    M = g.hx * g.hy * (m1g(2 * kj + ia / 3, 2 * kj + jb / 3, g.ny) * m1g(2 * ki + ia % 3, 2 * ki + jb % 3, g.nx));
+  }
+  double* A = mats + (size_t)K * D * D;
+  for (int mu = 0; mu < k1; ++mu) {
+    const double J = level_spatial_entry(op, mu, K, i, j);
+    for (int nu = 0; nu < k1; ++nu) {
+      double v = (i < 18 && j < 18) ? td.K_t[mu * k1 + nu] * M : 0.0;
+      if (mu == nu) v += td.tau_w[mu] * J;
+      A[(size_t)(21 * mu + i) * D + 21 * nu + j] = v;
+    }
+  }
+}
+
+// Dense coarsest-level slab matrix (multigrid.py:494-520), one thread per row.
+__global__ void k_dense_assemble(LevelOp op, TimeData td, double* __restrict__ A, int n) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  const Geom& g = op.g;
+  const int mu = row / g.nd, r = row % g.nd;
+  double* Ar = A + (size_t)row * n;
+  for (int c = 0; c < n; ++c) Ar[c] = 0.0;
+  const double tw = td.tau_w[mu];
+  if (r >= g.mv) {
+    const int c = (r - g.mv) / 3, pr = (r - g.mv) % 3;
+    const int cx = c % g.nx, cy = c / g.nx;
+    for (int jj = 0; jj < 21; ++jj) {
+      const int col = jj < 18 ? 2 * ((2 * cy + (jj >> 1) / 3) * g.nnx + 2 * cx + (jj >> 1) % 3) + (jj & 1)
+                              : g.mv + 3 * c + jj - 18;
+      Ar[(size_t)mu * g.nd + col] += tw * cell_entry(op, mu, c, 18 + pr, jj);
+    }
+    return;
+  }
+  const int node = r >> 1, d = r & 1;
+  const int X = node % g.nnx, Y = node / g.nnx;
+  for (int cy = max(0, (Y - 1) / 2); cy <= min(g.ny - 1, Y / 2); ++cy)
+    for (int cx = max(0, (X - 1) / 2); cx <= min(g.nx - 1, X / 2); ++cx) {
+      const int c = cy * g.nx + cx;
+      const int a = 3 * (Y - 2 * cy) + (X - 2 * cx);
+      for (int jj = 0; jj < 21; ++jj) {
+        const int col = jj < 18 ? 2 * ((2 * cy + (jj >> 1) / 3) * g.nnx + 2 * cx + (jj >> 1) % 3) + (jj & 1)
+                                : g.mv + 3 * c + jj - 18;
+        Ar[(size_t)mu * g.nd + col] += tw * cell_entry(op, mu, c, 2 * a + d, jj);
+      }
+    }
+  for (int axis = 0; axis < 2; ++axis) {
+    const int nfx = axis == 0 ? g.nx - 1 : g.nx, nfy = axis == 0 ? g.ny : g.ny - 1;
+    const int xr = axis == 0 ? 4 : 2, yr = axis == 0 ? 2 : 4;
+    for (int fj = max(0, (Y - yr + 1) / 2); fj <= min(nfy - 1, Y / 2); ++fj)
+      for (int fi = max(0, (X - xr + 1) / 2); fi <= min(nfx - 1, X / 2); ++fi) {
+        const int cl = fj * g.nx + fi, cr = axis == 0 ? cl + 1 : cl + g.nx;
+        for (int sA = 0; sA < 2; ++sA) {
+          const int cA = sA == 0 ? cl : cr;
+          const int ax = X - 2 * (cA % g.nx), ay = Y - 2 * (cA / g.nx);
+          if (ax < 0 || ax > 2 || ay < 0 || ay > 2) continue;
+          for (int sB = 0; sB < 2; ++sB) {
+            const int cB = sB == 0 ? cl : cr;
+            for (int bb = 0; bb < 9; ++bb) {
+              const int nb = (2 * (cB / g.nx) + bb / 3) * g.nnx + 2 * (cB % g.nx) + bb % 3;
+              Ar[(size_t)mu * g.nd + 2 * nb + d] += tw * face_entry(op, mu, axis, fi, fj, sA, 3 * ay + ax, sB, bb);
+            }
+          }
+        }
+      }
+  }
+  // K_t (x) M on velocity
+  for (int Yp = max(0, Y - 2); Yp <= min(g.nny - 1, Y + 2); ++Yp) {
+    const double my = m1g(Y, Yp, g.ny);
+    if (my == 0.0) continue;
+    for (int Xp = max(0, X - 2); Xp <= min(g.nnx - 1, X + 2); ++Xp) {
+      const double mx = m1g(X, Xp, g.nx);
+      if (mx == 0.0) continue;
+      const double m = g.hx * g.hy * (my * mx);
+      for (int nu = 0; nu < td.k1; ++nu)
+        Ar[(size_t)nu * g.nd + 2 * (Yp * g.nnx + Xp) + d] += td.K_t[mu * td.k1 + nu] * m;
+    }
+  }
+}
+
+// Add scale * z z' with z the normalized per-node constant-pressure mode
+// (multigrid.py:509-519); one thread per (row, col) pair of the pressure blocks.
+__global__ void k_dense_pin(Geom g, int k1, double* __restrict__ A, int n, double scale) {
+  const int nc = g.ncells;
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t per = (size_t)nc * nc;
+  if (t >= per * k1) return;
+  const int mu = (int)(t / per);
+  const int a = (int)((t % per) / nc), b = (int)(t % nc);
+  // z entries: area on every p0 dof, normalized: 1/sqrt(nc)
+  const double za = 1.0 / sqrt((double)nc);
+  const size_t ra = (size_t)mu * g.nd + g.mv + 3 * (size_t)a, rb = (size_t)mu * g.nd + g.mv + 3 * (size_t)b;
+  A[ra * n + rb] += scale * (za * za);
+}
+
+__global__ void k_diag_abs_sum(const double* __restrict__ A, int n, double* __restrict__ out) {
+  __shared__ double sh[1024];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += fabs(A[(size_t)i * n + i]);
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if (threadIdx.x < off) sh[threadIdx.x] += sh[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0] / n;
+}
+
+// Dense in-place Gauss-Jordan with partial pivoting, one CTA (coarsest level).
+__global__ void __launch_bounds__(1024) k_dense_invert(double* __restrict__ A, int n, int* __restrict__ piv,
+                                                       int* __restrict__ bad) {
+  __shared__ double sv[1024];
+  __shared__ int si[1024];
+  __shared__ double pinv_s;
+  for (int k = 0; k < n; ++k) {
+    double best = -1.0;
+    int bi = n;
+    for (int i = k + threadIdx.x; i < n; i += blockDim.x) {
+      const double v = fabs(A[(size_t)i * n + k]);
+      if (v > best || (v == best && i < bi)) {
+        best = v;
+        bi = i;
+      }
+    }
+    sv[threadIdx.x] = best;
+    si[threadIdx.x] = bi;
+    __syncthreads();
+    for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+      if (threadIdx.x < off) {
+        const double ov = sv[threadIdx.x + off];
+        const int oi = si[threadIdx.x + off];
+        if (ov > sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+          sv[threadIdx.x] = ov;
+          si[threadIdx.x] = oi;
+        }
+      }
+      __syncthreads();
+    }
+    const int p = si[0];
+    if (!(sv[0] > 0.0)) {
+      if (threadIdx.x == 0) *bad = 1;
+      return;
+    }
+    if (threadIdx.x == 0) piv[k] = p;
+    if (p != k)
+      for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const double tmp = A[(size_t)k * n + j];
+        A[(size_t)k * n + j] = A[(size_t)p * n + j];
+        A[(size_t)p * n + j] = tmp;
+      }
+    __syncthreads();
+    if (threadIdx.x == 0) pinv_s = 1.0 / A[(size_t)k * n + k];
+    __syncthreads();
+    const double pinv = pinv_s;
+    for (int j = threadIdx.x; j < n; j += blockDim.x)
+      A[(size_t)k * n + j] = (j == k ? 1.0 : A[(size_t)k * n + j]) * pinv;
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+      const int i = idx / n, j = idx - i * n;
+      if (i == k || j == k) continue;
+      A[(size_t)i * n + j] -= A[(size_t)i * n + k] * A[(size_t)k * n + j];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      if (i != k) A[(size_t)i * n + k] = -A[(size_t)i * n + k] * pinv;
+    __syncthreads();
+  }
+  for (int k = n - 1; k >= 0; --k) {
+    const int p = piv[k];
+    if (p != k)
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double tmp = A[(size_t)i * n + k];
+        A[(size_t)i * n + k] = A[(size_t)i * n + p];
+        A[(size_t)i * n + p] = tmp;
+      }
+    __syncthreads();
+  }
+}
+
+// y = Ainv b (coarsest-level solve), one warp per row.
+__global__ void k_dense_gemv(const double* __restrict__ Ainv, int n, const double* __restrict__ b,
+                             double* __restrict__ y) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  const double* r = Ainv + (size_t)warp * n;
+  double s = 0.0;
+  for (int j = lane; j < n; j += 32) s = fma(r[j], b[j], s);
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+  if (lane == 0) y[warp] = s;
+}
+
+// Remove the mass-weighted mean of the constant pressure mode per node
+// (multigrid.py:557-572); one CTA per Radau node.
+__global__ void k_project_pressure(Geom g, double* __restrict__ z) {
+  __shared__ double sh[1024];
+  const int mu = blockIdx.x;
+  double* p = z + (size_t)mu * g.nd + g.mv;
+  const double area_c = g.hx * g.hy;
+  double s = 0.0;
+  for (int c = threadIdx.x; c < g.ncells; c += blockDim.x) s = fma(area_c, p[3 * (size_t)c], s);
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if (threadIdx.x < off) sh[threadIdx.x] += sh[threadIdx.x + off];
+    __syncthreads();
+  }
+  const double mean = sh[0] / (area_c * g.ncells);
+  __syncthreads();
+  for (int c = threadIdx.x; c < g.ncells; c += blockDim.x) p[3 * (size_t)c] -= mean;
+}
+
+__global__ void k_axpy(size_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] += a * x[i];
+}
+
+}  // namespace
+
+cudaError_t prolong(const Geom& gc, const Geom& gf, int k1, const double* ec, double* ef, cudaStream_t st) {
+  const size_t n = (size_t)gf.nnx * gf.nny + gf.ncells;
+  k_prolong<<<dim3((unsigned)((n + 255) / 256), k1), 256, 0, st>>>(gc, gf, k1, ec, ef);
+  return cudaGetLastError();
+}
+
+cudaError_t restrict_(const Geom& gc, const Geom& gf, int k1, const double* rf, double* rc, cudaStream_t st) {
+  const size_t n = (size_t)gc.nnx * gc.nny + gc.ncells;
+  k_restrict<<<dim3((unsigned)((n + 255) / 256), k1), 256, 0, st>>>(gc, gf, k1, rf, rc);
+  return cudaGetLastError();
+}
+
+cudaError_t galerkin(const LevelOp& fine, const Geom& gc, int k1, double* ecell_c, double* fv_c, double* fh_c,
+                     cudaStream_t st) {
+  k_galerkin_cells<<<dim3(gc.ncells, k1), 448, 0, st>>>(fine, gc, ecell_c);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int nf = max((gc.nx - 1) * gc.ny, gc.nx * (gc.ny - 1));
+  if (nf > 0) k_galerkin_faces<<<dim3(nf, k1, 2), 324, 0, st>>>(fine, gc, fv_c, fh_c);
+  return cudaGetLastError();
+}
+
+cudaError_t level_apply(const LevelOp& op, const TimeData& td, const double* x, const double* rhs, double* y,
+                        cudaStream_t st) {
+  const size_t n = (size_t)op.g.nnx * op.g.nny + op.g.ncells;
+  k_level_apply<<<dim3((unsigned)((n + 127) / 128), td.k1), 128, 0, st>>>(op, td, x, rhs, y);
+  return cudaGetLastError();
+}
+
+cudaError_t patch_assemble_level(const LevelOp& op, const TimeData& td, double* mats, cudaStream_t st) {
+  k_patch_level<<<op.g.ncells, 448, 0, st>>>(op, td, mats);
+  return cudaGetLastError();
+}
+
+cudaError_t dense_build(const LevelOp& op, const TimeData& td, bool pin, double* A, double* scratch, int* piv,
+                        int* bad, cudaStream_t st) {
+  const int n = td.k1 * op.g.nd;
+  k_dense_assemble<<<(n + 127) / 128, 128, 0, st>>>(op, td, A, n);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (pin) {
+    k_diag_abs_sum<<<1, 1024, 0, st>>>(A, n, scratch);
+    double scale = 0.0;
+    e = cudaMemcpyAsync(&scale, scratch, sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return e;
+    const size_t tot = (size_t)op.g.ncells * op.g.ncells * td.k1;
+    k_dense_pin<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(op.g, td.k1, A, n, scale);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  k_dense_invert<<<1, 1024, 0, st>>>(A, n, piv, bad);
+  return cudaGetLastError();
+}
+
+cudaError_t dense_solve(const double* Ainv, int n, const double* b, double* y, cudaStream_t st) {
+  k_dense_gemv<<<(n * 32 + 255) / 256, 256, 0, st>>>(Ainv, n, b, y);
+  return cudaGetLastError();
+}
+
+cudaError_t project_pressure(const Geom& g, int k1, double* z, cudaStream_t st) {
+  k_project_pressure<<<k1, 1024, 0, st>>>(g, z);
+  return cudaGetLastError();
+}
+
+cudaError_t axpy(size_t n, double a, const double* x, double* y, cudaStream_t st) {
+  k_axpy<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, a, x, y);
+  return cudaGetLastError();
+}
+
+}  // namespace pdst

@@ -1,0 +1,38 @@
+// pdst_coarse.h — multigrid level operators (element form), transfers, coarsest solve.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "pdst_device.cuh"
+
+namespace pdst {
+
+// A level operator in element form (see pdst_coarse.cu).  fine == true: the
+// finest level, ecell holds the column-major element matrices ET of every Radau
+// node and the CIP face blocks are evaluated on the fly from `state`.
+struct LevelOp {
+  Geom g;
+  Disc ds;
+  int fine;
+  const double* ecell;  // [k1][ncells][441]
+  const double* fv;     // [k1][(nx-1) ny][324]   (coarse levels)
+  const double* fh;     // [k1][nx (ny-1)][324]
+  const double* state;  // [k1][Mv] lagged velocity (finest level)
+};
+
+cudaError_t prolong(const Geom& gc, const Geom& gf, int k1, const double* ec, double* ef, cudaStream_t st);
+cudaError_t restrict_(const Geom& gc, const Geom& gf, int k1, const double* rf, double* rc, cudaStream_t st);
+cudaError_t galerkin(const LevelOp& fine, const Geom& gc, int k1, double* ecell_c, double* fv_c, double* fh_c,
+                     cudaStream_t st);
+cudaError_t level_apply(const LevelOp& op, const TimeData& td, const double* x, const double* rhs, double* y,
+                        cudaStream_t st);
+cudaError_t patch_assemble_level(const LevelOp& op, const TimeData& td, double* mats, cudaStream_t st);
+// Dense coarsest slab matrix, optional pressure pinning, in-place inverse.
+// scratch: >= 1 double; piv: >= n ints; bad: 1 int (set to 1 when singular).
+cudaError_t dense_build(const LevelOp& op, const TimeData& td, bool pin, double* A, double* scratch, int* piv,
+                        int* bad, cudaStream_t st);
+cudaError_t dense_solve(const double* Ainv, int n, const double* b, double* y, cudaStream_t st);
+cudaError_t project_pressure(const Geom& g, int k1, double* z, cudaStream_t st);
+cudaError_t axpy(size_t n, double a, const double* x, double* y, cudaStream_t st);
+
+}  // namespace pdst

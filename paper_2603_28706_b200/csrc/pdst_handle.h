@@ -44,6 +44,9 @@ struct Level {
   bool diag = false;
   TimeDiag tdiag{};
   DeviceBuffer spatial, binv;
+  // coarsest level: dense inverse of the (pinned) slab matrix
+  DeviceBuffer dense;
+  DeviceBuffer ipiv;
   // work vectors (k1 * nd each)
   DeviceBuffer w0, w1, w2, w3;
   ~Level() {
@@ -130,6 +133,7 @@ struct pdst_handle {
   // multigrid
   std::vector<pdst::Level*> levels;  // 0 = coarsest
   int min_cells = 0;
+  bool coarse_valid = false;  // Galerkin operators / coarse patches / dense solve built
   bool patches_valid = false;
 
   ~pdst_handle() {

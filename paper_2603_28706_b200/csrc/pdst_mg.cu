@@ -6,6 +6,7 @@
 // forms.py:192-196 (dof maps).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -13,6 +14,7 @@
 
 #include "../../include/pdst.h"
 #include "pdst_handle.h"
+#include "pdst_coarse.h"
 #include "pdst_patch.h"
 
 using namespace pdst;
@@ -112,10 +114,42 @@ int pdst_cell_maps(pdst_handle* h, int64_t* cell_nodes, int64_t* patch_ids) {
 
 int pdst_hierarchy(pdst_handle* h, int min_cells, int* num_levels) {
   if (!h) return set_error(PDST_EINVAL, "null handle");
-  finest(h);
-  (void)min_cells;
+  CK(cudaSetDevice(h->device));
+  for (auto* l : h->levels) delete l;
+  h->levels.clear();
+  h->patches_valid = false;
+  h->coarse_valid = false;
+  h->min_cells = min_cells;
+  // coarsen while nx > min_cells and even, same for ny (multigrid.py:170)
+  std::vector<Level*> chain;
+  Level* f = new Level();
+  f->g = h->g;
+  f->dirichlet_host = h->dirichlet_host;
+  chain.push_back(f);
+  while (true) {
+    const Level* m = chain.back();
+    const int nx = m->g.nx, ny = m->g.ny;
+    if (!(nx > min_cells && nx % 2 == 0 && ny > min_cells && ny % 2 == 0)) break;
+    Level* c = new Level();
+    const int cnx = nx / 2, cny = ny / 2;
+    // coarse faces inherit the tag of the first fine face of their side (multigrid.py:174-182)
+    const int off_f[4] = {0, nx, nx + ny, 2 * nx + ny};
+    const int cnt_c[4] = {cnx, cny, cnx, cny};
+    for (int side = 0; side < 4; ++side)
+      for (int i = 0; i < cnt_c[side]; ++i) c->dirichlet_host.push_back(m->dirichlet_host[off_f[side]]);
+    if (cudaMalloc(&c->dirichlet, c->dirichlet_host.size()) != cudaSuccess) return set_error(PDST_ECUDA, "cudaMalloc");
+    CK(cudaMemcpy(c->dirichlet, c->dirichlet_host.data(), c->dirichlet_host.size(), cudaMemcpyHostToDevice));
+    c->g = make_geom(cnx, cny, h->extents[0], h->extents[1], h->extents[2], h->extents[3], c->dirichlet);
+    chain.push_back(c);
+  }
+  for (auto it = chain.rbegin(); it != chain.rend(); ++it) {
+    Level* l = *it;
+    l->all_dirichlet = true;
+    for (auto v : l->dirichlet_host) l->all_dirichlet = l->all_dirichlet && v;
+    h->levels.push_back(l);
+  }
   if (num_levels) *num_levels = (int)h->levels.size();
-  return set_error(PDST_ENOTSUP, "coarse levels not built in this version");
+  return PDST_OK;
 }
 
 int pdst_level_sizes(pdst_handle* h, int level, int32_t* nx, int32_t* ny, int64_t* ndof) {
@@ -129,50 +163,111 @@ int pdst_level_sizes(pdst_handle* h, int level, int32_t* nx, int32_t* ny, int64_
   return PDST_OK;
 }
 
+// Level operator descriptor of level l (element form).
+static LevelOp level_op(pdst_handle* h, int l) {
+  Level* lv = h->levels[l];
+  LevelOp op{};
+  op.g = lv->g;
+  op.ds = h->ds;
+  op.fine = l == (int)h->levels.size() - 1;
+  op.ecell = lv->ecell.ptr;
+  op.fv = lv->efx.ptr;
+  op.fh = lv->efy.ptr;
+  op.state = h->state.ptr;
+  return op;
+}
+
+static int invert_level_patches(pdst_handle* h, int l, int* badi, int* bad_level, int64_t* bad_patch) {
+  Level* lv = h->levels[l];
+  const int k1 = h->td.k1, D = 21 * k1;
+  const size_t nc = lv->g.ncells;
+  const int init = INT_MAX;
+  CK(cudaMemcpyAsync(badi, &init, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  if (lv->diag) {
+    CK(patch_invert_diag(lv->g, lv->tdiag, lv->spatial.ptr, reinterpret_cast<double2*>(lv->binv.ptr), badi,
+                         h->stream));
+  } else {
+    double* invs = lv->invs.ensure(nc * D * D);
+    if (!invs) return set_error(PDST_ECUDA, "out of device memory (patch inverses)");
+    CK(patch_invert(k1, lv->mats.ptr, invs, (int)nc, badi, h->stream));
+  }
+  int badh = INT_MAX;
+  CK(cudaMemcpyAsync(&badh, badi, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  lv->D = D;
+  if (badh != INT_MAX) {
+    if (bad_level) *bad_level = l;
+    if (bad_patch) *bad_patch = badh;
+    return set_error(PDST_ESINGULAR, "singular patch matrix (level %d, patch %d)", l, badh);
+  }
+  return PDST_OK;
+}
+
 int pdst_patches_build(pdst_handle* h, int surrogate, double rep_fraction, int* bad_level, int64_t* bad_patch) {
   if (!h) return set_error(PDST_EINVAL, "null handle");
   if (!h->linearized) return set_error(PDST_ESTATE, "patches built before pdst_linearize");
   CK(cudaSetDevice(h->device));
+  h->patches_valid = false;
+  h->coarse_valid = false;
   Level* fl = finest(h);
+  const int L = (int)h->levels.size();
   const Geom& g = h->g;
   const int k1 = h->td.k1, D = 21 * k1;
   const size_t nc = g.ncells;
+  const bool multilevel = L > 1;
+  double* bad = h->ibuf.ensure(1);
+  if (!bad) return set_error(PDST_ECUDA, "out of device memory");
+  int* badi = reinterpret_cast<int*>(bad);
+
+  // exact per-node element matrices of the finest level (Galerkin input and exact patches)
+  const bool need_exact = multilevel || !surrogate;
+  if (need_exact) {
+    double* ET = fl->ecell.ensure((size_t)k1 * nc * 441);
+    if (!ET) return set_error(PDST_ECUDA, "out of device memory (element matrices)");
+    const Lin L0 = lin_of(h);
+    for (int s = 0; s < k1; ++s)
+      CK(element_matrices(g, h->ds, L0, s, h->state.ptr + (size_t)s * g.mv, ET + (size_t)s * nc * 441, h->stream));
+  }
+
+  // ---- finest-level patches (surrogate or exact), multigrid.py:475-486 ----
   PatchArgs pa{};
   pa.g = g;
   pa.td = h->td;
   pa.ds = h->ds;
-  const bool rep = surrogate && k1 > 1;
   pa.nslot = surrogate ? 1 : k1;
-  double* ET = h->ET.ensure((size_t)pa.nslot * nc * 441);
-  if (!ET) return set_error(PDST_ECUDA, "out of device memory (element matrices)");
-  pa.ET = ET;
-  if (rep) {
-    // rep state = sum_mu l_mu(rep_fraction) U_mu (slab.py:105-112), linearized alone
-    const std::vector<double> c = lagrange_at(h->nodes, rep_fraction);
-    double* sr = h->state_rep.ensure(g.mv);
-    double* er = h->eta_rep.ensure(16 * nc);
-    double* gr = h->gam_rep.ensure(16 * nc);
-    double* efr = h->etaf_rep.ensure((size_t)g.nbf * 4);
-    double* gfr = h->gamf_rep.ensure((size_t)g.nbf * 4);
-    if (!sr || !er || !gr || !efr || !gfr) return set_error(PDST_ECUDA, "out of device memory");
-    CK(blend_velocity(g, k1, c.data(), h->state.ptr, g.mv, sr, h->stream));
-    CK(linearize(g, h->model, 1, sr, er, gr, efr, gfr, h->stream));
-    Lin L = lin_of(h);
-    L.eta = er;
-    L.gam = gr;
-    L.etaf = efr;
-    L.gamf = gfr;
-    CK(element_matrices(g, h->ds, L, 0, sr, ET, h->stream));
-    pa.state = sr;
+  if (surrogate) {
+    double* ET = h->ET.ensure(nc * 441);
+    if (!ET) return set_error(PDST_ECUDA, "out of device memory (element matrices)");
+    pa.ET = ET;
+    if (k1 > 1) {
+      // rep state = sum_mu l_mu(rep_fraction) U_mu (slab.py:105-112), linearized alone
+      const std::vector<double> c = lagrange_at(h->nodes, rep_fraction);
+      double* sr = h->state_rep.ensure(g.mv);
+      double* er = h->eta_rep.ensure(16 * nc);
+      double* gr = h->gam_rep.ensure(16 * nc);
+      double* efr = h->etaf_rep.ensure((size_t)g.nbf * 4);
+      double* gfr = h->gamf_rep.ensure((size_t)g.nbf * 4);
+      if (!sr || !er || !gr || !efr || !gfr) return set_error(PDST_ECUDA, "out of device memory");
+      CK(blend_velocity(g, k1, c.data(), h->state.ptr, g.mv, sr, h->stream));
+      CK(linearize(g, h->model, 1, sr, er, gr, efr, gfr, h->stream));
+      Lin Lr = lin_of(h);
+      Lr.eta = er;
+      Lr.gam = gr;
+      Lr.etaf = efr;
+      Lr.gamf = gfr;
+      CK(element_matrices(g, h->ds, Lr, 0, sr, ET, h->stream));
+      pa.state = sr;
+    } else {
+      // k = 0: the surrogate is node 0 itself (multigrid.py:480)
+      CK(element_matrices(g, h->ds, lin_of(h), 0, h->state.ptr, ET, h->stream));
+      pa.state = h->state.ptr;
+    }
   } else {
-    const Lin L = lin_of(h);
-    for (int s = 0; s < pa.nslot; ++s)
-      CK(element_matrices(g, h->ds, L, s, h->state.ptr + (size_t)s * g.mv, ET + (size_t)s * nc * 441, h->stream));
+    pa.ET = fl->ecell.ptr;
     pa.state = h->state.ptr;
   }
   double* mats = fl->mats.ensure(nc * D * D);
-  double* bad = h->ibuf.ensure(1);
-  if (!mats || !bad) return set_error(PDST_ECUDA, "out of device memory (patches)");
+  if (!mats) return set_error(PDST_ECUDA, "out of device memory (patches)");
   pa.mats = mats;
   // Surrogate patches share one spatial block across the Radau nodes: keep it
   // and invert the temporally diagonalized blocks instead of A_K itself.
@@ -185,28 +280,45 @@ int pdst_patches_build(pdst_handle* h, int surrogate, double rep_fraction, int* 
       return set_error(PDST_ECUDA, "out of device memory (diagonalized patches)");
   }
   CK(patch_assemble(pa, h->stream));
-  int* badi = reinterpret_cast<int*>(bad);
-  const int init = INT_MAX;
-  CK(cudaMemcpyAsync(badi, &init, sizeof(int), cudaMemcpyHostToDevice, h->stream));
-  if (fl->diag) {
-    CK(patch_invert_diag(g, fl->tdiag, pa.spatial, reinterpret_cast<double2*>(fl->binv.ptr), badi, h->stream));
-  } else {
-    double* invs = fl->invs.ensure(nc * D * D);
-    if (!invs) return set_error(PDST_ECUDA, "out of device memory (patch inverses)");
-    CK(patch_invert(k1, mats, invs, (int)nc, badi, h->stream));
-  }
-  int badh = INT_MAX;
-  CK(cudaMemcpyAsync(&badh, badi, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
-  fl->D = D;
-  const int L = (int)h->levels.size();
-  if (badh != INT_MAX) {
-    if (bad_level) *bad_level = L - 1;
-    if (bad_patch) *bad_patch = badh;
-    h->patches_valid = false;
-    return set_error(PDST_ESINGULAR, "singular patch matrix (level %d, patch %d)", L - 1, badh);
+  if (int e = invert_level_patches(h, L - 1, badi, bad_level, bad_patch)) return e;
+
+  // ---- coarse levels: Galerkin operators, exact patches (multigrid.py:435-488) ----
+  for (int l = L - 2; l >= 0; --l) {
+    Level* lv = h->levels[l];
+    const Geom& gc = lv->g;
+    double* ec = lv->ecell.ensure((size_t)k1 * gc.ncells * 441);
+    double* fv = lv->efx.ensure((size_t)k1 * std::max(1, (gc.nx - 1) * gc.ny) * 324);
+    double* fh = lv->efy.ensure((size_t)k1 * std::max(1, gc.nx * (gc.ny - 1)) * 324);
+    if (!ec || !fv || !fh) return set_error(PDST_ECUDA, "out of device memory (coarse operators)");
+    CK(galerkin(level_op(h, l + 1), gc, k1, ec, fv, fh, h->stream));
+    double* m = lv->mats.ensure((size_t)gc.ncells * D * D);
+    if (!m) return set_error(PDST_ECUDA, "out of device memory (coarse patches)");
+    lv->diag = false;
+    CK(patch_assemble_level(level_op(h, l), h->td, m, h->stream));
+    if (int e = invert_level_patches(h, l, badi, bad_level, bad_patch)) return e;
+    const size_t n = (size_t)k1 * gc.nd;
+    if (!lv->w0.ensure(n) || !lv->w1.ensure(n) || !lv->w2.ensure(n) || !lv->w3.ensure(n))
+      return set_error(PDST_ECUDA, "out of device memory (level vectors)");
   }
   h->patches_valid = true;
+
+  // ---- coarsest-level dense solve (multigrid.py:494-520) ----
+  if (multilevel) {
+    Level* c0 = h->levels[0];
+    const int n = k1 * c0->g.nd;
+    if (n > 16384) return set_error(PDST_ENOTSUP, "coarsest level too large for the dense solve (%d dofs)", n);
+    double* A = c0->dense.ensure((size_t)n * n);
+    double* scr = c0->ipiv.ensure((size_t)n / 2 + 2);
+    if (!A || !scr) return set_error(PDST_ECUDA, "out of device memory (coarse solve)");
+    int* piv = reinterpret_cast<int*>(scr + 1);
+    CK(cudaMemsetAsync(bad, 0, sizeof(int), h->stream));
+    CK(dense_build(level_op(h, 0), h->td, c0->all_dirichlet, A, scr, piv, badi, h->stream));
+    int badh = 0;
+    CK(cudaMemcpyAsync(&badh, badi, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (badh) return set_error(PDST_ESINGULAR, "singular coarsest-level matrix");
+    h->coarse_valid = true;
+  }
   return PDST_OK;
 }
 
@@ -234,58 +346,147 @@ int pdst_patch_info(pdst_handle* h, int level, int32_t* D, int32_t* diag_blocks,
   return PDST_OK;
 }
 
+// y = r - A_l x on level l (device pointers).
+static int level_defect(pdst_handle* h, int l, const double* x, const double* r, double* y) {
+  const int L = (int)h->levels.size();
+  if (l == L - 1) {
+    double* part = h->jpart.ensure(jacobian_scratch(h->g, h->td.k1));
+    if (!part) return set_error(PDST_ECUDA, "out of device memory");
+    CK(PDST_TIMED(h, PK_JACOBIAN,
+                  jacobian_apply(h->g, h->td, h->ds, lin_of(h), h->state.ptr, x, r, y, part, h->stream)));
+  } else {
+    CK(PDST_TIMED(h, PK_LEVEL, level_apply(level_op(h, l), h->td, x, r, y, h->stream)));
+  }
+  return PDST_OK;
+}
+
+// `steps` Vanka steps on level l, d updated in place (device pointers).
+static int vanka_level(pdst_handle* h, int l, double* d, const double* r, int steps, double omega) {
+  Level* lv = h->levels[l];
+  const Geom& g = lv->g;
+  const int k1 = h->td.k1;
+  const size_t n = (size_t)k1 * g.nd;
+  double* defect = h->defect.ensure(std::max(n, (size_t)k1 * h->g.nd));
+  double* upd = h->upd.ensure((size_t)h->g.ncells * 21 * k1);
+  if (!defect || !upd) return set_error(PDST_ECUDA, "out of device memory");
+  for (int s = 0; s < steps; ++s) {
+    if (int e = level_defect(h, l, d, r, defect)) return e;
+    if (lv->diag)
+      CK(PDST_TIMED(h, PK_VANKA_GEMV, vanka_gemv_diag(g, lv->tdiag, reinterpret_cast<const double2*>(lv->binv.ptr),
+                                                       defect, upd, h->stream)));
+    else
+      CK(PDST_TIMED(h, PK_VANKA_GEMV, vanka_gemv(g, k1, lv->invs.ptr, defect, upd, h->stream)));
+    CK(PDST_TIMED(h, PK_VANKA_SCATTER, vanka_scatter(g, k1, upd, omega, d, h->stream)));
+  }
+  return PDST_OK;
+}
+
 int pdst_vanka(pdst_handle* h, int level, double* d, const double* r, int steps, double omega, int where) {
   if (!h || !d || !r) return set_error(PDST_EINVAL, "null argument");
   if (int e = check_where(where)) return e;
   if (int e = check_level(h, level)) return e;
   if (!h->patches_valid) return set_error(PDST_ESTATE, "vanka before pdst_patches_build");
   if (steps < 0) return set_error(PDST_EINVAL, "steps must be >= 0");
-  if (level != (int)h->levels.size() - 1) return set_error(PDST_ENOTSUP, "coarse-level Vanka not built");
   CK(cudaSetDevice(h->device));
-  Level* l = h->levels[level];
-  const Geom& g = l->g;
-  const int k1 = h->td.k1;
-  const size_t n = (size_t)k1 * g.nd;
+  const size_t n = (size_t)h->td.k1 * h->levels[level]->g.nd;
   int err = PDST_OK;
   double* dd = where == PDST_DEVICE ? d : h->scratch_b.ensure(n);
   if (!dd) return set_error(PDST_ECUDA, "out of device memory");
   if (where == PDST_HOST) CK(cudaMemcpyAsync(dd, d, n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
   const double* rd = stage_in(h, h->scratch_c, r, n, where, &err);
   if (err) return err;
-  double* defect = h->defect.ensure(n);
-  double* upd = h->upd.ensure((size_t)g.ncells * 21 * k1);
-  if (!defect || !upd) return set_error(PDST_ECUDA, "out of device memory");
-  const Lin L = lin_of(h);
-  double* part = h->jpart.ensure(jacobian_scratch(g, k1));
-  if (!part) return set_error(PDST_ECUDA, "out of device memory");
-  for (int s = 0; s < steps; ++s) {
-    CK(PDST_TIMED(h, PK_JACOBIAN, jacobian_apply(g, h->td, h->ds, L, h->state.ptr, dd, rd, defect, part, h->stream)));
-    if (l->diag)
-      CK(PDST_TIMED(h, PK_VANKA_GEMV, vanka_gemv_diag(g, l->tdiag, reinterpret_cast<const double2*>(l->binv.ptr),
-                                                       defect, upd, h->stream)));
-    else
-      CK(PDST_TIMED(h, PK_VANKA_GEMV, vanka_gemv(g, k1, l->invs.ptr, defect, upd, h->stream)));
-    CK(PDST_TIMED(h, PK_VANKA_SCATTER, vanka_scatter(g, k1, upd, omega, dd, h->stream)));
-  }
+  if (int e = vanka_level(h, level, dd, rd, steps, omega)) return e;
   return finish_out(h, d, dd, n, where);
 }
 
 int pdst_level_apply(pdst_handle* h, int level, const double* x, double* y, int where) {
-  if (!h) return set_error(PDST_EINVAL, "null handle");
+  if (!h || !x || !y) return set_error(PDST_EINVAL, "null argument");
   finest(h);
   if (int e = check_level(h, level)) return e;
   if (level == (int)h->levels.size() - 1) return pdst_jacobian_apply(h, x, y, where);
-  return set_error(PDST_ENOTSUP, "coarse levels not built in this version");
+  if (!h->patches_valid) return set_error(PDST_ESTATE, "coarse operators are built by pdst_patches_build");
+  if (int e = check_where(where)) return e;
+  CK(cudaSetDevice(h->device));
+  const size_t n = (size_t)h->td.k1 * h->levels[level]->g.nd;
+  int err = PDST_OK;
+  const double* xd = stage_in(h, h->scratch_a, x, n, where, &err);
+  if (err) return err;
+  double* yd = out_ptr(h->scratch_b, y, n, where);
+  if (!yd) return set_error(PDST_ECUDA, "out of device memory");
+  CK(PDST_TIMED(h, PK_LEVEL, level_apply(level_op(h, level), h->td, xd, nullptr, yd, h->stream)));
+  return finish_out(h, y, yd, n, where);
 }
 
-int pdst_restrict(pdst_handle*, int, const double*, double*, int) {
-  return set_error(PDST_ENOTSUP, "transfers not built in this version");
+static int transfer_common(pdst_handle* h, int fine_level, const double* in, double* out, int where, bool prol) {
+  if (!h || !in || !out) return set_error(PDST_EINVAL, "null argument");
+  if (int e = check_where(where)) return e;
+  if (fine_level < 1 || fine_level >= (int)h->levels.size())
+    return set_error(PDST_EINVAL, "fine level %d has no coarser level", fine_level);
+  CK(cudaSetDevice(h->device));
+  const Geom& gf = h->levels[fine_level]->g;
+  const Geom& gc = h->levels[fine_level - 1]->g;
+  const int k1 = h->td.k1;
+  const size_t nin = (size_t)k1 * (prol ? gc.nd : gf.nd), nout = (size_t)k1 * (prol ? gf.nd : gc.nd);
+  int err = PDST_OK;
+  const double* id = stage_in(h, h->scratch_a, in, nin, where, &err);
+  if (err) return err;
+  double* od = out_ptr(h->scratch_b, out, nout, where);
+  if (!od) return set_error(PDST_ECUDA, "out of device memory");
+  if (prol)
+    CK(PDST_TIMED(h, PK_TRANSFER, prolong(gc, gf, k1, id, od, h->stream)));
+  else
+    CK(PDST_TIMED(h, PK_TRANSFER, restrict_(gc, gf, k1, id, od, h->stream)));
+  return finish_out(h, out, od, nout, where);
 }
-int pdst_prolong(pdst_handle*, int, const double*, double*, int) {
-  return set_error(PDST_ENOTSUP, "transfers not built in this version");
+
+int pdst_restrict(pdst_handle* h, int fine_level, const double* r_fine, double* r_coarse, int where) {
+  return transfer_common(h, fine_level, r_fine, r_coarse, where, false);
 }
-int pdst_vcycle(pdst_handle*, const double*, double*, int, int, double, int) {
-  return set_error(PDST_ENOTSUP, "V-cycle not built in this version");
+
+int pdst_prolong(pdst_handle* h, int fine_level, const double* e_coarse, double* e_fine, int where) {
+  return transfer_common(h, fine_level, e_coarse, e_fine, where, true);
+}
+
+// One V-cycle on level l with zero initial guess: z = V_l b (multigrid.py:545-555).
+static int vcycle_level(pdst_handle* h, int l, const double* b, double* z, int pre, int post, double omega) {
+  Level* lv = h->levels[l];
+  const int k1 = h->td.k1;
+  const size_t n = (size_t)k1 * lv->g.nd;
+  if (l == 0) {
+    CK(dense_solve(lv->dense.ptr, (int)n, b, z, h->stream));
+    return PDST_OK;
+  }
+  Level* lc = h->levels[l - 1];
+  const Geom& gc = lc->g;
+  double* r = lv == h->levels.back() ? h->scratch_d.ensure(n) : lv->w1.ptr;
+  if (!r) return set_error(PDST_ECUDA, "out of device memory");
+  CK(cudaMemsetAsync(z, 0, n * sizeof(double), h->stream));
+  if (int e = vanka_level(h, l, z, b, pre, omega)) return e;
+  if (int e = level_defect(h, l, z, b, r)) return e;
+  CK(PDST_TIMED(h, PK_TRANSFER, restrict_(gc, lv->g, k1, r, lc->w0.ptr, h->stream)));
+  if (int e = vcycle_level(h, l - 1, lc->w0.ptr, lc->w2.ptr, pre, post, omega)) return e;
+  CK(PDST_TIMED(h, PK_TRANSFER, prolong(gc, lv->g, k1, lc->w2.ptr, r, h->stream)));
+  CK(axpy(n, 1.0, r, z, h->stream));
+  if (int e = vanka_level(h, l, z, b, post, omega)) return e;
+  return PDST_OK;
+}
+
+int pdst_vcycle(pdst_handle* h, const double* r, double* z, int pre, int post, double omega, int where) {
+  if (!h || !r || !z) return set_error(PDST_EINVAL, "null argument");
+  if (int e = check_where(where)) return e;
+  if (!h->patches_valid || !h->coarse_valid)
+    return set_error(PDST_ESTATE, "V-cycle needs pdst_hierarchy (>= 2 levels) and pdst_patches_build");
+  CK(cudaSetDevice(h->device));
+  const int L = (int)h->levels.size();
+  const size_t n = (size_t)h->td.k1 * h->g.nd;
+  int err = PDST_OK;
+  const double* rd = stage_in(h, h->scratch_c, r, n, where, &err);
+  if (err) return err;
+  double* zd = out_ptr(h->scratch_b, z, n, where);
+  if (!zd) return set_error(PDST_ECUDA, "out of device memory");
+  if (int e = vcycle_level(h, L - 1, rd, zd, pre, post, omega)) return e;
+  if (h->levels.back()->all_dirichlet) CK(project_pressure(h->g, h->td.k1, zd, h->stream));
+  return finish_out(h, z, zd, n, where);
 }
 
 }  // extern "C"
