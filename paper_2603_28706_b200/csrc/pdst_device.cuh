@@ -14,7 +14,7 @@
 //   slab vectors  (k+1) blocks of nd = Mv + Mp doubles, Mv = 2 (2nx+1)(2ny+1);
 //                 velocity dof of node (X, Y) component d at 2 (Y (2nx+1) + X) + d;
 //                 pressure dof j of cell c at Mv + 3 c + j
-//   qp caches     [mu][q][cell] (structure of arrays, coalesced over cells)
+//   qp caches     [mu][cell][q] (16 volume points of a cell contiguous)
 //   face caches   [mu][bface][q], bface = side offset + index along the side,
 //                 side order bottom, right, top, left
 #pragma once
@@ -70,8 +70,8 @@ struct Model {
 
 // Frozen linearization (per node mu).
 struct Lin {
-  const double* eta;    // [k1][16][nc]
-  const double* gam;    // [k1][16][nc]
+  const double* eta;    // [k1][nc][16]
+  const double* gam;    // [k1][nc][16]
   const double* etaf;   // [k1][nbf][4]
   const double* gamf;   // [k1][nbf][4]
   const double* etad;   // [nbf][4]  lifting viscosity (state independent)

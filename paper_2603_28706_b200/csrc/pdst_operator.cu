@@ -18,6 +18,8 @@
 //
 // Reference: forms.py:581-652 (J x), forms.py:435-516 (residual),
 // slab.py:162-205 (slab composition), constitutive.py:323-337 (tangent).
+#include <cstdlib>
+
 #include "pdst_device.cuh"
 #include "pdst_internal.h"
 
@@ -59,6 +61,13 @@ struct RegAcc {
 struct SmemAcc {
   double* p;
   __device__ __forceinline__ void add(int jy, int ix, int d, double v) const { p[(2 * (3 * jy + ix) + d) * NT] += v; }
+};
+template <int STRIDE>
+struct SmemAccN {
+  double* p;
+  __device__ __forceinline__ void add(int jy, int ix, int d, double v) const {
+    p[(2 * (3 * jy + ix) + d) * STRIDE] += v;
+  }
 };
 
 // Asynchronous 8-byte global->shared copy (LDGSTS); size 0 zero-fills.
@@ -644,14 +653,14 @@ __device__ __forceinline__ void jac_volume(const Geom& g, const Disc& ds, const 
                                            const ACC& acc, double accp[3], double tw = 1.0) {
   const double W = g.hx * g.hy * tw;
   // eta / gamma of the next Gauss column are loaded one column ahead
-  const double* pe = L.eta + (size_t)mu * 16 * g.ncells + c;
-  const double* pg = L.gam + (size_t)mu * 16 * g.ncells + c;
+  const double* pe = L.eta + ((size_t)mu * g.ncells + c) * 16;
+  const double* pg = L.gam + ((size_t)mu * g.ncells + c) * 16;
   const bool vis = ds.viscous, hg = L.has_gamma && ds.viscous;
   double en[4], gn[4];
 #pragma unroll
   for (int qy = 0; qy < 4; ++qy) {
-    en[qy] = vis ? __ldg(pe + (size_t)qy * g.ncells) : 0.0;
-    gn[qy] = hg ? __ldg(pg + (size_t)qy * g.ncells) : 0.0;
+    en[qy] = vis ? __ldg(pe + qy) : 0.0;
+    gn[qy] = hg ? __ldg(pg + qy) : 0.0;
   }
       // ---- volume (forms.py:589-603) ----
 #pragma unroll 1
@@ -665,8 +674,8 @@ __device__ __forceinline__ void jac_volume(const Geom& g, const Disc& ds, const 
         if (qx < 3) {
 #pragma unroll
           for (int qy = 0; qy < 4; ++qy) {
-            en[qy] = vis ? __ldg(pe + (size_t)(4 * (qx + 1) + qy) * g.ncells) : 0.0;
-            gn[qy] = hg ? __ldg(pg + (size_t)(4 * (qx + 1) + qy) * g.ncells) : 0.0;
+            en[qy] = vis ? __ldg(pe + 4 * (qx + 1) + qy) : 0.0;
+            gn[qy] = hg ? __ldg(pg + 4 * (qx + 1) + qy) : 0.0;
           }
         }
         double xB[3][2], xG[3][2], sB[3][2], sG[3][2];
@@ -824,13 +833,15 @@ static_assert(JNT == NT, "SmemAcc stride");
 __host__ __device__ inline int jac_tiles_x(const Geom& g) { return (g.nx + JT - 1) / JT; }
 __host__ __device__ inline int jac_tiles_y(const Geom& g) { return (g.ny + JT - 1) / JT; }
 
-// Canonical perimeter index of node (lx, ly) of a full tile node rectangle.
-__device__ __forceinline__ int perim(int lx, int ly) {
+// Canonical perimeter index of node (lx, ly) of a full T x T tile node rectangle.
+template <int T>
+__device__ __forceinline__ int perim_t(int lx, int ly) {
   if (ly == 0) return lx;
-  if (ly == 2 * JT) return 2 * JT + 1 + lx;
-  if (lx == 0) return 2 * (2 * JT + 1) + ly - 1;
-  return 2 * (2 * JT + 1) + 2 * JT - 1 + ly - 1;
+  if (ly == 2 * T) return 2 * T + 1 + lx;
+  if (lx == 0) return 2 * (2 * T + 1) + ly - 1;
+  return 2 * (2 * T + 1) + 2 * T - 1 + ly - 1;
 }
+__device__ __forceinline__ int perim(int lx, int ly) { return perim_t<JT>(lx, ly); }
 
 template <int K1>
 __global__ void __launch_bounds__(JNT, 1) k_jacobian(Geom g, TimeData td, Disc ds, Lin L, const double* __restrict__ state,
@@ -930,48 +941,50 @@ __global__ void __launch_bounds__(JNT, 1) k_jacobian(Geom g, TimeData td, Disc d
 }
 
 // Shared tile-boundary nodes: sum the (2 or 4) tile partials in fixed order.
+template <int T>
 __global__ void k_jac_fixup(Geom g, int k1, const double* __restrict__ part, const double* __restrict__ rhs,
                             double* __restrict__ out) {
-  const int ntx = jac_tiles_x(g), nty = jac_tiles_y(g);
+  constexpr int PER = 8 * T;
+  const int ntx = (g.nx + T - 1) / T, nty = (g.ny + T - 1) / T;
   const size_t nv = (size_t)(ntx - 1) * g.nny;  // nodes on interior vertical tile lines
   const size_t nh = (size_t)(nty - 1) * g.nnx;  // nodes on interior horizontal tile lines
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int mu = blockIdx.y;
   int X, Y;
   if (t < nv) {
-    X = 2 * JT * (int)(t / g.nny + 1);
+    X = 2 * T * (int)(t / g.nny + 1);
     Y = (int)(t % g.nny);
   } else if (t < nv + nh) {
     const size_t u = t - nv;
-    Y = 2 * JT * (int)(u / g.nnx + 1);
+    Y = 2 * T * (int)(u / g.nnx + 1);
     X = (int)(u % g.nnx);
-    if (X % (2 * JT) == 0 && X > 0 && X < 2 * JT * ntx && X / (2 * JT) < ntx) return;  // on a vertical line
+    if (X % (2 * T) == 0 && X > 0 && X / (2 * T) < ntx) return;  // on a vertical line
   } else {
     return;
   }
   int bxs[2], bys[2], nbx = 0, nby = 0;
-  if (X % (2 * JT) == 0 && X > 0 && X / (2 * JT) < ntx) {
-    bxs[0] = X / (2 * JT) - 1;
-    bxs[1] = X / (2 * JT);
+  if (X % (2 * T) == 0 && X > 0 && X / (2 * T) < ntx) {
+    bxs[0] = X / (2 * T) - 1;
+    bxs[1] = X / (2 * T);
     nbx = 2;
   } else {
-    bxs[0] = min(X / (2 * JT), ntx - 1);
+    bxs[0] = min(X / (2 * T), ntx - 1);
     nbx = 1;
   }
-  if (Y % (2 * JT) == 0 && Y > 0 && Y / (2 * JT) < nty) {
-    bys[0] = Y / (2 * JT) - 1;
-    bys[1] = Y / (2 * JT);
+  if (Y % (2 * T) == 0 && Y > 0 && Y / (2 * T) < nty) {
+    bys[0] = Y / (2 * T) - 1;
+    bys[1] = Y / (2 * T);
     nby = 2;
   } else {
-    bys[0] = min(Y / (2 * JT), nty - 1);
+    bys[0] = min(Y / (2 * T), nty - 1);
     nby = 1;
   }
   const size_t ntiles = (size_t)ntx * nty;
   double s0 = 0.0, s1 = 0.0;
   for (int b = 0; b < nby; ++b)
     for (int a = 0; a < nbx; ++a) {
-      const int lx = X - 2 * JT * bxs[a], ly = Y - 2 * JT * bys[b];
-      const double* pp = part + (((size_t)mu * ntiles + (size_t)bys[b] * ntx + bxs[a]) * JPER + perim(lx, ly)) * 2;
+      const int lx = X - 2 * T * bxs[a], ly = Y - 2 * T * bys[b];
+      const double* pp = part + (((size_t)mu * ntiles + (size_t)bys[b] * ntx + bxs[a]) * PER + perim_t<T>(lx, ly)) * 2;
       s0 += pp[0];
       s1 += pp[1];
     }
@@ -1189,7 +1202,7 @@ __global__ void k_linearize_cells(Geom g, Model m, int k1, const double* __restr
       const double a0 = vx[0], a1 = vy[1], a2 = 0.5 * (vy[0] + vx[1]);
       double e, gm;
       tangent_coeffs(m, a0 * a0 + a1 * a1 + 2.0 * a2 * a2, e, gm);
-      const size_t o = ((size_t)mu * 16 + 4 * qx + qy) * g.ncells + c;
+      const size_t o = ((size_t)mu * g.ncells + c) * 16 + 4 * qx + qy;
       eta[o] = e;
       gam[o] = gm;
     }
@@ -1344,7 +1357,7 @@ cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const 
   const size_t nfix = (size_t)(jac_tiles_x(g) - 1) * g.nny + (size_t)(jac_tiles_y(g) - 1) * g.nnx;
   if (nfix > 0) {
     dim3 fg((unsigned)((nfix + 255) / 256), K1);
-    k_jac_fixup<<<fg, 256, 0, st>>>(g, K1, part, rhs, out);
+    k_jac_fixup<JT><<<fg, 256, 0, st>>>(g, K1, part, rhs, out);
   }
   return cudaGetLastError();
 }
