@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -211,6 +212,10 @@ int pdst_create(const pdst_mesh* mesh, const pdst_time* time, const pdst_disc* d
   h->ds.viscous = disc->enable_viscous;
   h->ds.convection = disc->enable_convection;
   h->ds.pressure = disc->enable_pressure;
+  {
+    const char* sk = getenv("PDST_SKIP");  // profiling experiments only
+    h->ds.skip = sk ? atoi(sk) : 0;
+  }
   h->model.p = params->p;
   h->model.delta = params->delta;
   h->model.nu = params->nu;
@@ -295,6 +300,13 @@ int pdst_linearize(pdst_handle* h, const double* U, int kind, double sigma_max, 
   h->model.kind = kind;
   h->model.sigma_max = sigma_max;
   CK(linearize(g, h->model, k1, st, eta, gam, etaf, gamf, h->stream));
+  {
+    double* bm = h->bmat.ensure((size_t)k1 * 441 * g.nbf);
+    if (!bm) return fail(PDST_ECUDA, "out of device memory");
+    Lin L = lin_of(h);
+    L.bmat = nullptr;
+    CK(boundary_matrices(g, h->ds, L, k1, st, bm, h->stream));
+  }
   h->linearized = true;
   h->patches_valid = false;
   if (where == PDST_HOST) CK(cudaStreamSynchronize(h->stream));

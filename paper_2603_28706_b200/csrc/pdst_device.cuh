@@ -60,6 +60,7 @@ struct TimeData {
 struct Disc {
   double gamma1, gamma2, gamma_cip;
   int viscous, convection, pressure;
+  int skip;  // profiling only (PDST_SKIP): 1 volume, 2 CIP, 4 sides, 8 mass, 16 assembly
 };
 
 struct Model {
@@ -77,6 +78,7 @@ struct Lin {
   const double* etad;   // [nbf][4]  lifting viscosity (state independent)
   const double* betad;  // [nbf][4]
   const double* dg;     // [nbf][4][3] sym grad of the lifting
+  const double* bmat;   // [k1][21][21][nbf] boundary-side matrices (rows i, cols j), or null
   int has_gamma;        // 0 for Picard (gamma == 0)
 };
 

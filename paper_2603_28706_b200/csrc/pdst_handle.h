@@ -115,6 +115,7 @@ struct pdst_handle {
   pdst::DeviceBuffer state;  // (k1, Mv)
   pdst::DeviceBuffer eta, gam, etaf, gamf;
   pdst::DeviceBuffer etad, betad, dg;
+  pdst::DeviceBuffer bmat;  // boundary-side matrices of the linearization
   pdst::DeviceBuffer ghat;
   bool has_ghat = false;
   bool linearized = false;
@@ -175,6 +176,7 @@ inline Lin lin_of(pdst_handle* h) {
   L.etad = h->etad.ptr;
   L.betad = h->betad.ptr;
   L.dg = h->dg.ptr;
+  L.bmat = h->bmat.ptr;
   L.has_gamma = h->model.kind != 0;
   return L;
 }

@@ -26,6 +26,10 @@ cudaError_t linearize(const Geom& g, const Model& m, int k1, const double* state
 cudaError_t element_matrices(const Geom& g, const Disc& ds, const Lin& L, int mu, const double* state, double* ET,
                              cudaStream_t st);
 
+// Boundary-side matrices [k1][21][21][nbf] of the current linearization (L.bmat ignored).
+cudaError_t boundary_matrices(const Geom& g, const Disc& ds, const Lin& L, int k1, const double* state, double* bmat,
+                              cudaStream_t st);
+
 cudaError_t lifting(const Geom& g, const Model& m, const double* ghat, double* etad, double* betad, double* dg,
                     cudaStream_t st);
 

@@ -843,15 +843,110 @@ __device__ __forceinline__ int perim_t(int lx, int ly) {
 }
 __device__ __forceinline__ int perim(int lx, int ly) { return perim_t<JT>(lx, ly); }
 
+// Boundary-side products of the current direction, one thread per (row i,
+// boundary face, node mu): ybnd[mu][i][bf] = sum_j B[mu][i][j][bf] x_loc[j].
+// Runs before k_jacobian so boundary cells only add 21 precomputed values.
+__global__ void k_boundary_apply(Geom g, int k1, const double* __restrict__ bmat, const double* __restrict__ x,
+                                 double* __restrict__ ybnd) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int mu = blockIdx.y;
+  const int i = (int)(t / g.nbf), bf = (int)(t % g.nbf);
+  if (i >= 21 || mu >= k1) return;
+  int side = 0;
+  while (side < 3 && bf >= side_offset(g, side + 1)) ++side;
+  const int f = bf - side_offset(g, side);
+  int ci, cj;
+  if (side == 0) { ci = f; cj = 0; }
+  else if (side == 1) { ci = g.nx - 1; cj = f; }
+  else if (side == 2) { ci = f; cj = g.ny - 1; }
+  else { ci = 0; cj = f; }
+  const double* xm = x + (size_t)mu * g.nd;
+  const double* Bm = bmat + (size_t)mu * 441 * g.nbf + (size_t)i * 21 * g.nbf + bf;
+  double s = 0.0;
+#pragma unroll
+  for (int a = 0; a < 9; ++a) {
+    const size_t node = (size_t)(2 * cj + a / 3) * g.nnx + 2 * ci + a % 3;
+    s = fma(__ldg(Bm + (size_t)(2 * a) * g.nbf), __ldg(xm + 2 * node), s);
+    s = fma(__ldg(Bm + (size_t)(2 * a + 1) * g.nbf), __ldg(xm + 2 * node + 1), s);
+  }
+  const double* xp = xm + g.mv + 3 * ((size_t)cj * g.nx + ci);
+#pragma unroll
+  for (int r = 0; r < 3; ++r) s = fma(__ldg(Bm + (size_t)(18 + r) * g.nbf), __ldg(xp + r), s);
+  ybnd[((size_t)mu * 21 + i) * g.nbf + bf] = s;
+}
+
+// Add the precomputed boundary-side products of a cell (times tau w_mu).
+template <class ACC>
+__device__ __forceinline__ void jac_sides_pre(const Geom& g, const double* __restrict__ ybnd, int mu, int ci, int cj,
+                                              const ACC& acc, double accp[3], double tw) {
+  if (!(ci == 0 || cj == 0 || ci == g.nx - 1 || cj == g.ny - 1)) return;
+  for (int side = 0; side < 4; ++side) {
+    const bool on = side == 0 ? cj == 0 : side == 1 ? ci == g.nx - 1 : side == 2 ? cj == g.ny - 1 : ci == 0;
+    if (!on) continue;
+    const int bf = side_offset(g, side) + ((side == 0 || side == 2) ? ci : cj);
+    const double* yb = ybnd + (size_t)mu * 21 * g.nbf + bf;
+#pragma unroll
+    for (int i = 0; i < 18; ++i) acc.add((i >> 1) / 3, (i >> 1) % 3, i & 1, tw * __ldg(yb + (size_t)i * g.nbf));
+#pragma unroll
+    for (int r = 0; r < 3; ++r) accp[r] += tw * __ldg(yb + (size_t)(18 + r) * g.nbf);
+  }
+}
+
+// Staging plan of one thread: the (row, col) staged nodes it copies, shared by
+// every plane it stages (precomputed once per kernel).
+constexpr int STG_IT = (NR * NC + JNT - 1) / JNT;
+struct StagePlan {
+  int sidx[STG_IT];   // shared index (pidx) or -1
+  long long gofs[STG_IT];  // 2 * global node index, or -1 outside the domain
+};
+
+__device__ __forceinline__ void stage_plan(const Geom& g, int X0, int Y0, StagePlan& sp) {
+#pragma unroll
+  for (int it = 0; it < STG_IT; ++it) {
+    const int idx = threadIdx.x + it * JNT;
+    sp.sidx[it] = -1;
+    sp.gofs[it] = -1;
+    if (idx < NR * NC) {
+      const int r = idx / NC, c = idx - r * NC;
+      const int X = X0 + c, Y = Y0 + r;
+      sp.sidx[it] = pidx(r, c);
+      if (X >= 0 && X < g.nnx && Y >= 0 && Y < g.nny) sp.gofs[it] = 2 * ((long long)Y * g.nnx + X);
+    }
+  }
+}
+
+__device__ __forceinline__ void stage_planned(const StagePlan& sp, const double* __restrict__ v, double* pl0,
+                                              double* pl1) {
+#pragma unroll
+  for (int it = 0; it < STG_IT; ++it) {
+    if (sp.sidx[it] < 0) continue;
+    const bool in = sp.gofs[it] >= 0;
+    const double* src = in ? v + sp.gofs[it] : v;
+    cp_async8(pl0 + sp.sidx[it], src, in);
+    cp_async8(pl1 + sp.sidx[it], in ? src + 1 : v, in);
+  }
+}
+
+// PIPE (K1 <= 2): every Radau node's state / rhs planes are staged up front and
+// the per-cell slots are double buffered, so the assembly of node mu overlaps
+// the compute of node mu+1 (one barrier per node instead of two).
+template <int K1>
+__host__ __device__ constexpr bool jac_pipe() { return K1 <= 2; }
+template <int K1>
+__host__ __device__ constexpr int jac_nbuf() { return jac_pipe<K1>() ? K1 : 1; }
+
 template <int K1>
 __global__ void __launch_bounds__(JNT, 1) k_jacobian(Geom g, TimeData td, Disc ds, Lin L, const double* __restrict__ state,
                                                   const double* __restrict__ x, const double* __restrict__ rhs,
-                                                  double* __restrict__ out, double* __restrict__ part) {
+                                                  double* __restrict__ out, double* __restrict__ part,
+                                                  const double* __restrict__ ybnd) {
+  constexpr bool PIPE = jac_pipe<K1>();
+  constexpr int NB = jac_nbuf<K1>();
   extern __shared__ double smem[];
-  double* xs = smem;                        // [K1][2][PLANE] direction x_nu, all Radau nodes (one-cell ring)
-  double* ss = xs + (size_t)K1 * 2 * PLANE;  // [2][PLANE]     state v_mu
-  double* rs = ss + 2 * PLANE;              // [2][PLANE]     rhs block mu (defect mode)
-  double* sacc = rs + 2 * PLANE;            // [18][JNT]      per-cell node contributions
+  double* xs = smem;                             // [K1][2][PLANE] direction x_nu, all Radau nodes (one-cell ring)
+  double* ss0 = xs + (size_t)K1 * 2 * PLANE;      // [NB][2][PLANE] state v_mu
+  double* rs0 = ss0 + (size_t)NB * 2 * PLANE;     // [NB][2][PLANE] rhs block mu (defect mode)
+  double* sacc0 = rs0 + (size_t)NB * 2 * PLANE;   // [NB][18][JNT]  per-cell node contributions
   const int bx = blockIdx.x, by = blockIdx.y;
   const int i0 = bx * JT, j0 = by * JT;
   const int X0 = 2 * (i0 - 1), Y0 = 2 * (j0 - 1);
@@ -859,25 +954,42 @@ __global__ void __launch_bounds__(JNT, 1) k_jacobian(Geom g, TimeData td, Disc d
   Plane2 XP[K1];
 #pragma unroll
   for (int nu = 0; nu < K1; ++nu) XP[nu] = Plane2{xs + nu * 2 * PLANE, xs + nu * 2 * PLANE + PLANE};
-  const Plane2 SP{ss, ss + PLANE};
-  const Plane2 RP{rs, rs + PLANE};
   const int tx = threadIdx.x % JT, ty = threadIdx.x / JT;
   const int ci = i0 + tx, cj = j0 + ty;
   const bool valid = tx < ntx && ty < nty;
   const int c = cj * g.nx + ci;
   const int r0 = 2 + 2 * ty, c0 = 2 + 2 * tx;  // staged origin of the cell's nodes
   const bool cip = ds.convection && ds.gamma_cip > 0.0;
-  const SmemAcc slot{sacc + threadIdx.x};
   const size_t ntiles = (size_t)jac_tiles_x(g) * jac_tiles_y(g);
   const size_t tile = (size_t)by * jac_tiles_x(g) + bx;
+  // nodes owned by this cell in the tile: its lower-left 2x2, plus the tile's
+  // last row / column of nodes for the last cell column / row
+  const bool lastx = tx == ntx - 1, lasty = ty == nty - 1;
 
+  StagePlan plan;
+  stage_plan(g, X0, Y0, plan);
   for (int nu = 0; nu < K1; ++nu)
-    stage_velocity_async(g, x + (size_t)nu * g.nd, xs + (size_t)nu * 2 * PLANE, xs + (size_t)nu * 2 * PLANE + PLANE,
-                         X0, Y0);
+    stage_planned(plan, x + (size_t)nu * g.nd, xs + (size_t)nu * 2 * PLANE, xs + (size_t)nu * 2 * PLANE + PLANE);
+  if (PIPE) {
+    for (int nu = 0; nu < K1; ++nu) {
+      stage_planned(plan, state + (size_t)nu * g.mv, ss0 + (size_t)nu * 2 * PLANE, ss0 + (size_t)nu * 2 * PLANE + PLANE);
+      if (rhs)
+        stage_planned(plan, rhs + (size_t)nu * g.nd, rs0 + (size_t)nu * 2 * PLANE, rs0 + (size_t)nu * 2 * PLANE + PLANE);
+    }
+  }
   for (int mu = 0; mu < K1; ++mu) {
     const double tw = td.tau_w[mu];
-    stage_velocity_async(g, state + (size_t)mu * g.mv, ss, ss + PLANE, X0, Y0);
-    if (rhs) stage_velocity_async(g, rhs + (size_t)mu * g.nd, rs, rs + PLANE, X0, Y0);
+    const int buf = PIPE ? mu : 0;
+    double* ss = ss0 + (size_t)buf * 2 * PLANE;
+    double* rs = rs0 + (size_t)buf * 2 * PLANE;
+    double* sacc = sacc0 + (size_t)buf * 18 * JNT;
+    const Plane2 SP{ss, ss + PLANE};
+    const Plane2 RP{rs, rs + PLANE};
+    const SmemAcc slot{sacc + threadIdx.x};
+    if (!PIPE) {
+      stage_planned(plan, state + (size_t)mu * g.mv, ss, ss + PLANE);
+      if (rhs) stage_planned(plan, rhs + (size_t)mu * g.nd, rs, rs + PLANE);
+    }
     double P[3] = {0.0, 0.0, 0.0};
     if (valid) {
       const double* xp = x + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
@@ -887,56 +999,71 @@ __global__ void __launch_bounds__(JNT, 1) k_jacobian(Geom g, TimeData td, Disc d
     }
 #pragma unroll
     for (int k = 0; k < 18; ++k) sacc[k * JNT + threadIdx.x] = 0.0;
-    cp_async_wait_all();
-    __syncthreads();
+    if (!PIPE || mu == 0) {
+      cp_async_wait_all();
+      __syncthreads();
+    }
     if (valid) {
       double accp[3] = {0.0, 0.0, 0.0};
       // tau w_mu J_mu x_mu: volume, boundary sides, CIP faces (weights carry tau w_mu)
-      jac_volume(g, ds, L, mu, c, XP[mu], SP, r0, c0, P, slot, accp, tw);
-      jac_sides(g, ds, L, mu, ci, cj, XP[mu], SP, r0, c0, P, slot, accp, tw);
-      if (cip) cip_all(g, ds, XP[mu], SP, ci, cj, r0, c0, tw, slot);
+      if (!(ds.skip & 1)) jac_volume(g, ds, L, mu, c, XP[mu], SP, r0, c0, P, slot, accp, tw);
+      if (!(ds.skip & 4)) {
+        if (ybnd)
+          jac_sides_pre(g, ybnd, mu, ci, cj, slot, accp, tw);
+        else
+          jac_sides(g, ds, L, mu, ci, cj, XP[mu], SP, r0, c0, P, slot, accp, tw);
+      }
+      if (cip && !(ds.skip & 2)) cip_all(g, ds, XP[mu], SP, ci, cj, r0, c0, tw, slot);
       // + M_K sum_nu K_t[mu,nu] x_nu (slab.py:199-200)
-      add_mass<K1>(XP, nullptr, 0.0, td.K_t + mu * K1, r0, c0, g.hx * g.hy, slot);
+      if (!(ds.skip & 8)) add_mass<K1>(XP, nullptr, 0.0, td.K_t + mu * K1, r0, c0, g.hx * g.hy, slot);
       const size_t o = (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
 #pragma unroll
       for (int j = 0; j < 3; ++j) out[o + j] = rhs ? rhs[o + j] - accp[j] : accp[j];
     }
     __syncthreads();
-    // node assembly over the tile's node rectangle
-    const int wx = 2 * ntx + 1, wy = 2 * nty + 1;
-    const size_t base = (size_t)mu * g.nd;
-    for (int idx = threadIdx.x; idx < wx * wy; idx += JNT) {
-      const int ly = idx / wx, lx = idx - ly * wx;
-      double s0 = 0.0, s1 = 0.0;
-      const int cxa = (lx & 1) ? (lx - 1) / 2 : lx / 2 - 1;
-      const int cya = (ly & 1) ? (ly - 1) / 2 : ly / 2 - 1;
-      for (int cy = cya; cy <= (ly & 1 ? cya : ly / 2); ++cy) {
-        if (cy < 0 || cy >= nty) continue;
-        for (int cx = cxa; cx <= (lx & 1 ? cxa : lx / 2); ++cx) {
-          if (cx < 0 || cx >= ntx) continue;
-          const int a = 3 * (ly - 2 * cy) + (lx - 2 * cx);
-          const int cell = cy * JT + cx;
-          s0 += sacc[(2 * a) * JNT + cell];
-          s1 += sacc[(2 * a + 1) * JNT + cell];
+    // node assembly: each cell writes the nodes it owns (lower-left 2x2 of its
+    // 3x3 block, plus the right column / top row for the tile's last cells),
+    // summing the <= 4 cells that contain a node in a fixed order.
+    if (valid && !(ds.skip & 16)) {
+      const size_t base = (size_t)mu * g.nd;
+      const int nxo = lastx ? 3 : 2, nyo = lasty ? 3 : 2;
+      for (int jy = 0; jy < nyo; ++jy)
+        for (int ix = 0; ix < nxo; ++ix) {
+          const int lx = 2 * tx + ix, ly = 2 * ty + jy;  // tile-local node
+          double s0 = 0.0, s1 = 0.0;
+          // cells containing the node: (tx - [ix==0], ty - [jy==0]) .. (tx + [ix==2]...)
+          const int cxa = ix == 0 ? tx - 1 : (ix == 2 ? tx : tx), cxb = ix == 2 ? tx : tx;
+          const int cya = jy == 0 ? ty - 1 : ty, cyb = ty;
+#pragma unroll
+          for (int cy = cya; cy <= cyb; ++cy) {
+            if (cy < 0) continue;
+#pragma unroll
+            for (int cx = cxa; cx <= cxb; ++cx) {
+              if (cx < 0) continue;
+              const int a = 3 * (ly - 2 * cy) + (lx - 2 * cx);
+              const int cell = cy * JT + cx;
+              s0 += sacc[(2 * a) * JNT + cell];
+              s1 += sacc[(2 * a + 1) * JNT + cell];
+            }
+          }
+          const bool shx = (lx == 0 && i0 > 0) || (lx == 2 * JT && i0 + JT < g.nx);
+          const bool shy = (ly == 0 && j0 > 0) || (ly == 2 * JT && j0 + JT < g.ny);
+          if (shx || shy) {
+            double* pp = part + (((size_t)mu * ntiles + tile) * JPER + perim(lx, ly)) * 2;
+            pp[0] = s0;
+            pp[1] = s1;
+          } else {
+            const size_t o = base + 2 * ((size_t)(2 * j0 + ly) * g.nnx + 2 * i0 + lx);
+            if (rhs) {
+              s0 = RP.at(0, ly + 2, lx + 2) - s0;
+              s1 = RP.at(1, ly + 2, lx + 2) - s1;
+            }
+            out[o] = s0;
+            out[o + 1] = s1;
+          }
         }
-      }
-      const bool shx = (lx == 0 && i0 > 0) || (lx == 2 * JT && i0 + JT < g.nx);
-      const bool shy = (ly == 0 && j0 > 0) || (ly == 2 * JT && j0 + JT < g.ny);
-      if (shx || shy) {
-        double* pp = part + (((size_t)mu * ntiles + tile) * JPER + perim(lx, ly)) * 2;
-        pp[0] = s0;
-        pp[1] = s1;
-      } else {
-        const size_t o = base + 2 * ((size_t)(2 * j0 + ly) * g.nnx + 2 * i0 + lx);
-        if (rhs) {
-          s0 = RP.at(0, ly + 2, lx + 2) - s0;
-          s1 = RP.at(1, ly + 2, lx + 2) - s1;
-        }
-        out[o] = s0;
-        out[o + 1] = s1;
-      }
     }
-    __syncthreads();
+    if (!PIPE) __syncthreads();
   }
 }
 
@@ -1331,9 +1458,51 @@ __global__ void __launch_bounds__(128) k_element_matrices(Geom g, Disc ds, Lin L
   out[20] = accp[2];
 }
 
+// Boundary-side matrices of the linearization: column j of side bf is the
+// side terms of forms.py:605-637 applied to the local unit vector j.  The apply
+// then does one 21x21 mat-vec per boundary side instead of the face evaluation.
+__global__ void __launch_bounds__(128) k_boundary_matrices(Geom g, Disc ds, Lin L, int k1,
+                                                           const double* __restrict__ state,
+                                                           double* __restrict__ bmat) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int mu = blockIdx.y;
+  const int bf = (int)(t / 21), j = (int)(t % 21);
+  if (bf >= g.nbf || mu >= k1) return;
+  int side = 0;
+  while (side < 3 && bf >= side_offset(g, side + 1)) ++side;
+  const int f = bf - side_offset(g, side);
+  int ci, cj;
+  if (side == 0) { ci = f; cj = 0; }
+  else if (side == 1) { ci = g.nx - 1; cj = f; }
+  else if (side == 2) { ci = f; cj = g.ny - 1; }
+  else { ci = 0; cj = f; }
+  const GlobAcc S{state + (size_t)mu * g.mv, g.nnx, 2 * ci, 2 * cj};
+  double P[3] = {0.0, 0.0, 0.0};
+  UnitAcc X{-1, -1, -1};
+  if (j < 18) {
+    X.r = (j / 2) / 3;
+    X.c = (j / 2) % 3;
+    X.d = j % 2;
+  } else {
+    P[j - 18] = 1.0;
+  }
+  double acc[3][3][2];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  double accp[3] = {0.0, 0.0, 0.0};
+  jac_boundary_side(g, ds, L, mu, side, bf, X, S, 0, 0, P, RegAcc{acc}, accp, 1.0);
+  double* col = bmat + (size_t)mu * 441 * g.nbf;
+  for (int a = 0; a < 9; ++a) {
+    col[((size_t)(2 * a) * 21 + j) * g.nbf + bf] = acc[a / 3][a % 3][0];
+    col[((size_t)(2 * a + 1) * 21 + j) * g.nbf + bf] = acc[a / 3][a % 3][1];
+  }
+  for (int r = 0; r < 3; ++r) col[((size_t)(18 + r) * 21 + j) * g.nbf + bf] = accp[r];
+}
+
 template <int K1>
 size_t jac_smem() {
-  return ((size_t)(2 * K1 + 4) * PLANE + (size_t)JNT * 18) * sizeof(double);
+  constexpr int NB = jac_nbuf<K1>();
+  return ((size_t)(2 * K1 + 4 * NB) * PLANE + (size_t)NB * JNT * 18) * sizeof(double);
 }
 template <int K1>
 size_t res_smem() {
@@ -1350,8 +1519,14 @@ cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const 
     if (e != cudaSuccess) return e;
     configured = true;
   }
+  double* ybnd = nullptr;
+  if (L.bmat) {
+    ybnd = part + (size_t)K1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2;
+    const size_t nb = (size_t)21 * g.nbf;
+    k_boundary_apply<<<dim3((unsigned)((nb + 127) / 128), K1), 128, 0, st>>>(g, K1, L.bmat, x, ybnd);
+  }
   dim3 grid(jac_tiles_x(g), jac_tiles_y(g));
-  k_jacobian<K1><<<grid, JNT, sm, st>>>(g, td, ds, L, state, x, rhs, out, part);
+  k_jacobian<K1><<<grid, JNT, sm, st>>>(g, td, ds, L, state, x, rhs, out, part, ybnd);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const size_t nfix = (size_t)(jac_tiles_x(g) - 1) * g.nny + (size_t)(jac_tiles_y(g) - 1) * g.nnx;
@@ -1383,7 +1558,7 @@ cudaError_t launch_res(const Geom& g, const TimeData& td, const Disc& ds, const 
 cudaError_t set_tables(const Tables& t) { return cudaMemcpyToSymbol(c_tab, &t, sizeof(Tables)); }
 
 size_t jacobian_scratch(const Geom& g, int k1) {
-  return (size_t)k1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2;
+  return (size_t)k1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2 + (size_t)k1 * 21 * g.nbf;
 }
 
 cudaError_t jacobian_apply(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* state,
@@ -1424,6 +1599,13 @@ cudaError_t element_matrices(const Geom& g, const Disc& ds, const Lin& L, int mu
                              cudaStream_t st) {
   const size_t n = (size_t)g.ncells * 21;
   k_element_matrices<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(g, ds, L, mu, state, ET);
+  return cudaGetLastError();
+}
+
+cudaError_t boundary_matrices(const Geom& g, const Disc& ds, const Lin& L, int k1, const double* state, double* bmat,
+                              cudaStream_t st) {
+  const size_t n = (size_t)g.nbf * 21;
+  k_boundary_matrices<<<dim3((unsigned)((n + 127) / 128), k1), 128, 0, st>>>(g, ds, L, k1, state, bmat);
   return cudaGetLastError();
 }
 
