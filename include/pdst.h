@@ -64,7 +64,8 @@ typedef struct pdst_handle pdst_handle;
 typedef struct {
   int32_t nx, ny;              /* cells per direction */
   double x0, y0, x1, y1;       /* rectangle */
-  const uint8_t* dirichlet;    /* 2(nx+ny) flags, sides bottom,right,top,left; NULL = all Dirichlet */
+  const uint8_t* dirichlet;    /* 2(nx+ny) tags, sides bottom,right,top,left: 0 Neumann, 1 Dirichlet,
+                                  2 partition cut (interior face of the global mesh); NULL = all Dirichlet */
 } pdst_mesh;
 
 typedef struct {
@@ -116,6 +117,10 @@ int pdst_patch_matrices(pdst_handle* h, int level, double* mats /* host (ncells,
    complex 21x21 blocks (0 = full real D x D inverses), bytes streamed per patch per sweep */
 int pdst_patch_info(pdst_handle* h, int level, int32_t* D, int32_t* diag_blocks, int64_t* bytes_per_patch);
 int pdst_vanka(pdst_handle* h, int level, double* d, const double* r, int steps, double omega, int where);
+/* One Vanka update without the defect: inc = omega sum_K R_K' A_K^-1 R_K defect over the
+   patches of cell rows [row_lo, row_hi) (distributed sweeps combine increments across ranks). */
+int pdst_vanka_increment(pdst_handle* h, int level, const double* defect, double* inc, int row_lo, int row_hi,
+                         double omega, int where);
 int pdst_level_apply(pdst_handle* h, int level, const double* x, double* y, int where);
 int pdst_restrict(pdst_handle* h, int fine_level, const double* r_fine, double* r_coarse, int where);
 int pdst_prolong(pdst_handle* h, int fine_level, const double* e_coarse, double* e_fine, int where);

@@ -67,6 +67,7 @@ SIGNATURES = {
     "pdst_patch_matrices": [P, I, P],
     "pdst_patch_info": [P, I, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(I64)],
     "pdst_vanka": [P, I, P, P, I, D, I],
+    "pdst_vanka_increment": [P, I, P, P, I, I, D, I],
     "pdst_level_apply": [P, I, P, P, I],
     "pdst_restrict": [P, I, P, P, I],
     "pdst_prolong": [P, I, P, P, I],

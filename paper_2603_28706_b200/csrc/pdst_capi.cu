@@ -188,7 +188,10 @@ int pdst_create(const pdst_mesh* mesh, const pdst_time* time, const pdst_disc* d
   const int nbf = 2 * (mesh->nx + mesh->ny);
   std::vector<uint8_t> dir(nbf, 1);
   if (mesh->dirichlet)
-    for (int i = 0; i < nbf; ++i) dir[i] = mesh->dirichlet[i] ? 1 : 0;
+    for (int i = 0; i < nbf; ++i) {
+      if (mesh->dirichlet[i] > 2) return fail(PDST_EINVAL, "boundary tag %d of face %d is not 0, 1 or 2", mesh->dirichlet[i], i);
+      dir[i] = mesh->dirichlet[i];
+    }
   h->dirichlet_host = dir;
   CK(cudaMalloc(&h->dirichlet, nbf));
   CK(cudaMemcpy(h->dirichlet, dir.data(), nbf, cudaMemcpyHostToDevice));

@@ -39,6 +39,10 @@ struct Tables {
 
 extern __constant__ Tables c_tab;
 
+// Boundary-face tags: 0 Neumann, 1 Dirichlet, 2 partition cut (an interior
+// face of the global mesh at the edge of a rank's local mesh: no side terms).
+constexpr uint8_t kCutSide = 2;
+
 struct Geom {
   int nx, ny;    // cells
   int nnx, nny;  // Q2 nodes per direction
@@ -47,7 +51,7 @@ struct Geom {
   int nbf;       // boundary faces 2 (nx + ny)
   double hx, hy;
   double ihx, ihy;           // 1/hx, 1/hy (the reference's grad_scale, femspace.py:142-143)
-  const uint8_t* dirichlet;  // nbf flags (device)
+  const uint8_t* dirichlet;  // nbf tags (device): 0 Neumann, 1 Dirichlet, 2 cut
 };
 
 struct TimeData {

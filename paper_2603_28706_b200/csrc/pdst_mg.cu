@@ -79,7 +79,7 @@ Level* finest(pdst_handle* h) {
     l->g = h->g;  // shares the handle's dirichlet flags (not owned)
     l->dirichlet_host = h->dirichlet_host;
     l->all_dirichlet = true;
-    for (auto f : h->dirichlet_host) l->all_dirichlet = l->all_dirichlet && f;
+    for (auto f : h->dirichlet_host) l->all_dirichlet = l->all_dirichlet && f == 1;
     h->levels.push_back(l);
   }
   return h->levels.back();
@@ -145,7 +145,7 @@ int pdst_hierarchy(pdst_handle* h, int min_cells, int* num_levels) {
   for (auto it = chain.rbegin(); it != chain.rend(); ++it) {
     Level* l = *it;
     l->all_dirichlet = true;
-    for (auto v : l->dirichlet_host) l->all_dirichlet = l->all_dirichlet && v;
+    for (auto v : l->dirichlet_host) l->all_dirichlet = l->all_dirichlet && v == 1;
     h->levels.push_back(l);
   }
   if (num_levels) *num_levels = (int)h->levels.size();
@@ -397,6 +397,33 @@ int pdst_vanka(pdst_handle* h, int level, double* d, const double* r, int steps,
   if (err) return err;
   if (int e = vanka_level(h, level, dd, rd, steps, omega)) return e;
   return finish_out(h, d, dd, n, where);
+}
+
+int pdst_vanka_increment(pdst_handle* h, int level, const double* defect, double* inc, int row_lo, int row_hi,
+                         double omega, int where) {
+  if (!h || !defect || !inc) return set_error(PDST_EINVAL, "null argument");
+  if (int e = check_where(where)) return e;
+  if (int e = check_level(h, level)) return e;
+  if (!h->patches_valid) return set_error(PDST_ESTATE, "vanka before pdst_patches_build");
+  Level* lv = h->levels[level];
+  if (row_lo < 0 || row_hi > lv->g.ny || row_lo > row_hi) return set_error(PDST_EINVAL, "bad cell-row range");
+  CK(cudaSetDevice(h->device));
+  const Geom& g = lv->g;
+  const int k1 = h->td.k1;
+  const size_t n = (size_t)k1 * g.nd;
+  int err = PDST_OK;
+  const double* dd = stage_in(h, h->scratch_a, defect, n, where, &err);
+  if (err) return err;
+  double* od = out_ptr(h->scratch_b, inc, n, where);
+  double* upd = h->upd.ensure((size_t)h->g.ncells * 21 * k1);
+  if (!od || !upd) return set_error(PDST_ECUDA, "out of device memory");
+  if (lv->diag)
+    CK(PDST_TIMED(h, PK_VANKA_GEMV, vanka_gemv_diag(g, lv->tdiag, reinterpret_cast<const double2*>(lv->binv.ptr), dd,
+                                                     upd, h->stream)));
+  else
+    CK(PDST_TIMED(h, PK_VANKA_GEMV, vanka_gemv(g, k1, lv->invs.ptr, dd, upd, h->stream)));
+  CK(PDST_TIMED(h, PK_VANKA_SCATTER, vanka_scatter(g, k1, upd, omega, od, h->stream, row_lo, row_hi, true)));
+  return finish_out(h, inc, od, n, where);
 }
 
 int pdst_level_apply(pdst_handle* h, int level, const double* x, double* y, int where) {

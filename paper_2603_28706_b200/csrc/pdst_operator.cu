@@ -338,12 +338,13 @@ __device__ __noinline__ void jac_boundary_side(const Geom& g, const Disc& ds, co
   const double ihtan = axis == 0 ? g.ihy : g.ihx;
   const double ihnorm = axis == 0 ? g.ihx : g.ihy;
   const double pen1 = ds.gamma1 / htan, pen2 = ds.gamma2 / htan;
+  if (g.dirichlet[bf] == kCutSide) return;  // partition cut: an interior face owned elsewhere
   FaceLines LU, LV;
   line_sums(X, r0, c0, axis, c_tab.E[e], LU.E);
   line_sums(X, r0, c0, axis, c_tab.dE[e], LU.D);
   line_sums(S, r0, c0, axis, c_tab.E[e], LV.E);
   line_sums(S, r0, c0, axis, c_tab.dE[e], LV.D);
-  const bool dm = g.dirichlet[bf] != 0;
+  const bool dm = g.dirichlet[bf] == 1;
   double RE[3][2] = {{0, 0}, {0, 0}, {0, 0}}, RD[3][2] = {{0, 0}, {0, 0}, {0, 0}};
   for (int q = 0; q < 4; ++q) {
     const double wq = c_tab.w[q] * htan * tw;
@@ -424,6 +425,7 @@ __device__ __noinline__ void res_boundary_side(const Geom& g, const Disc& ds, co
   const double ihtan = axis == 0 ? g.ihy : g.ihx;
   const double ihnorm = axis == 0 ? g.ihx : g.ihy;
   const double pen1 = ds.gamma1 / htan, pen2 = ds.gamma2 / htan;
+  if (g.dirichlet[bf] == kCutSide) return;  // partition cut
   FaceLines LV, LA;
   line_sums(S, r0, c0, axis, c_tab.E[e], LV.E);
   line_sums(S, r0, c0, axis, c_tab.dE[e], LV.D);
@@ -444,7 +446,7 @@ __device__ __noinline__ void res_boundary_side(const Geom& g, const Disc& ds, co
         GE[t][d] = s;
       }
   }
-  const bool dm = g.dirichlet[bf] != 0;
+  const bool dm = g.dirichlet[bf] == 1;
   double RE[3][2] = {{0, 0}, {0, 0}, {0, 0}}, RD[3][2] = {{0, 0}, {0, 0}, {0, 0}};
   for (int q = 0; q < 4; ++q) {
     const double wq = c_tab.w[q] * htan;

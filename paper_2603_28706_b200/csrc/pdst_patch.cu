@@ -258,7 +258,11 @@ __global__ void __launch_bounds__(256) k_vanka_gemv(Geom g, const double* __rest
 }
 
 // d[dof] += omega * sum over patches containing dof of upd (node gather).
-__global__ void k_vanka_scatter(Geom g, int k1, const double* __restrict__ upd, double omega, double* __restrict__ d) {
+// d[dof] += omega * sum over patches containing dof of upd (node gather).
+// Only patches of cell rows [row_lo, row_hi) contribute; inc_only writes the
+// increment instead of adding it (distributed sweeps combine increments).
+__global__ void k_vanka_scatter(Geom g, int k1, const double* __restrict__ upd, double omega, double* __restrict__ d,
+                                int row_lo, int row_hi, int inc_only) {
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int mu = blockIdx.y;
   const size_t nn = (size_t)g.nnx * g.nny;
@@ -267,22 +271,33 @@ __global__ void k_vanka_scatter(Geom g, int k1, const double* __restrict__ upd, 
   if (t < nn) {
     const int X = (int)(t % g.nnx), Y = (int)(t / g.nnx);
     double s0 = 0.0, s1 = 0.0;
-    for (int cy = max(0, (Y - 1) / 2); cy <= min(g.ny - 1, Y / 2); ++cy)
+    for (int cy = max(row_lo, (Y - 1) / 2); cy <= min(row_hi - 1, Y / 2); ++cy)
       for (int cx = max(0, (X - 1) / 2); cx <= min(g.nx - 1, X / 2); ++cx) {
         const int a = 3 * (Y - 2 * cy) + (X - 2 * cx);
         const double* u = upd + ((size_t)cy * g.nx + cx) * D + 21 * mu + 2 * a;
         s0 += u[0];
         s1 += u[1];
       }
-    dm[2 * t] += omega * s0;
-    dm[2 * t + 1] += omega * s1;
+    if (inc_only) {
+      dm[2 * t] = omega * s0;
+      dm[2 * t + 1] = omega * s1;
+    } else {
+      dm[2 * t] += omega * s0;
+      dm[2 * t + 1] += omega * s1;
+    }
   } else if (t < nn + (size_t)g.ncells) {
     const size_t c = t - nn;
+    const int cy = (int)(c / g.nx);
+    const bool act = cy >= row_lo && cy < row_hi;
     const double* u = upd + c * D + 21 * mu + 18;
     double* o = dm + g.mv + 3 * c;
-    o[0] += omega * u[0];
-    o[1] += omega * u[1];
-    o[2] += omega * u[2];
+    for (int j = 0; j < 3; ++j) {
+      const double v = act ? omega * u[j] : 0.0;
+      if (inc_only)
+        o[j] = v;
+      else
+        o[j] += v;
+    }
   }
 }
 
@@ -334,10 +349,12 @@ cudaError_t vanka_gemv(const Geom& g, int k1, const double* invT, const double* 
   }
 }
 
-cudaError_t vanka_scatter(const Geom& g, int k1, const double* upd, double omega, double* d, cudaStream_t st) {
+cudaError_t vanka_scatter(const Geom& g, int k1, const double* upd, double omega, double* d, cudaStream_t st,
+                          int row_lo, int row_hi, bool inc_only) {
+  if (row_hi < 0) row_hi = g.ny;
   const size_t n = (size_t)g.nnx * g.nny + g.ncells;
   dim3 grid((unsigned)((n + 255) / 256), k1);
-  k_vanka_scatter<<<grid, 256, 0, st>>>(g, k1, upd, omega, d);
+  k_vanka_scatter<<<grid, 256, 0, st>>>(g, k1, upd, omega, d, row_lo, row_hi, inc_only ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,333 @@
+"""Cell-strip partition of the slab hot path across GPUs.
+
+Rank r owns the cell rows [a_r, b_r) of the nx x ny mesh: the Q2 node rows
+[2 a_r, 2 b_r) (the last rank also the top row 2 ny) and the P1disc dofs of
+its cells.  Its local mesh is the strip plus two ghost cell rows on each side,
+[c_lo, c_hi) = [max(0, a-2), min(ny, b+2)); the sides of the local mesh that
+are interior faces of the global mesh carry the "cut" tag (2), so the kernels
+apply no boundary terms there.  Two ghost rows are what the CIP gradient-jump
+faces need: the face below cell a-1 still touches node row 2a, and the face
+above cell b still touches node row 2b, which belongs to the Vanka patch of
+cell b-1.  With that depth every owned node receives all of its element,
+CIP-face and temporal-mass contributions locally and every owned patch matrix
+is exact: owner computes, no reverse-add for the operator.
+
+Exchanges (one per operator application, contiguous slices of the node-major
+layout, per Radau block):
+  * x halo: node rows [2c_lo, 2a) from rank r-1, [2b, 2b+2] from rank r+1,
+    plus the pressure of the ghost cells below (cells c_lo..a-1) -- the ghost
+    node rows above 2b+2 only feed ghost outputs;
+  * Vanka defect halo: node row 2b (owned by r+1) for the patch of cell b-1;
+  * Vanka increment reverse-add: the increment of node row 2b computed from
+    r's patch of cell b-1 is added by r+1 (and r adds r-1's at row 2a).
+Transports: LocalTransport (several ranks' local vectors in one process,
+e.g. one GPU) and TorchDistTransport (torch.distributed point-to-point:
+NCCL on GPUs, gloo on CPU tensors).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = ["StripPartition", "RankLayout", "LocalTransport", "TorchDistTransport", "DistributedSlab"]
+
+CUT = 2
+
+
+def strip_bounds(ny: int, nranks: int):
+    """Cell-row ranges [a_r, b_r), as even as possible, each >= 2 rows."""
+    if ny < 2 * nranks:
+        raise ValueError(f"{ny} cell rows cannot give {nranks} strips of >= 2 rows")
+    return [(r * ny // nranks, (r + 1) * ny // nranks) for r in range(nranks)]
+
+
+@dataclass(frozen=True)
+class RankLayout:
+    rank: int
+    nranks: int
+    nx: int
+    ny: int  # global cell rows
+    a: int
+    b: int  # owned cell rows [a, b)
+    c_lo: int
+    c_hi: int  # local cell rows [c_lo, c_hi)
+
+    @property
+    def ny_loc(self):
+        return self.c_hi - self.c_lo
+
+    @property
+    def nnx(self):
+        return 2 * self.nx + 1
+
+    @property
+    def mv_loc(self):
+        return 2 * self.nnx * (2 * self.ny_loc + 1)
+
+    @property
+    def nd_loc(self):
+        return self.mv_loc + 3 * self.nx * self.ny_loc
+
+    @property
+    def mv(self):
+        return 2 * self.nnx * (2 * self.ny + 1)
+
+    @property
+    def nd(self):
+        return self.mv + 3 * self.nx * self.ny
+
+    @property
+    def last(self):
+        return self.rank == self.nranks - 1
+
+    # -- node rows (global Y) ----------------------------------------------
+    @property
+    def owned_node_rows(self):
+        return range(2 * self.a, 2 * self.ny + 1 if self.last else 2 * self.b)
+
+    def vel_slice_local(self, Y0: int, Y1: int):
+        """Local velocity slice of global node rows [Y0, Y1)."""
+        y0, y1 = Y0 - 2 * self.c_lo, Y1 - 2 * self.c_lo
+        return slice(2 * y0 * self.nnx, 2 * y1 * self.nnx)
+
+    def prs_slice_local(self, j0: int, j1: int):
+        """Local pressure slice of global cell rows [j0, j1)."""
+        return slice(self.mv_loc + 3 * (j0 - self.c_lo) * self.nx, self.mv_loc + 3 * (j1 - self.c_lo) * self.nx)
+
+    def vel_slice_global(self, Y0: int, Y1: int):
+        return slice(2 * Y0 * self.nnx, 2 * Y1 * self.nnx)
+
+    def prs_slice_global(self, j0: int, j1: int):
+        return slice(self.mv + 3 * j0 * self.nx, self.mv + 3 * j1 * self.nx)
+
+    # -- local mesh description --------------------------------------------
+    def local_tags(self, global_tags: np.ndarray) -> np.ndarray:
+        """uint8 tags of the local mesh's boundary faces (bottom, right, top, left)."""
+        nx, ny = self.nx, self.ny
+        g = np.asarray(global_tags, dtype=np.uint8)
+        bottom = g[0:nx] if self.c_lo == 0 else np.full(nx, CUT, np.uint8)
+        right = g[nx + self.c_lo: nx + self.c_hi]
+        top = g[nx + ny: 2 * nx + ny] if self.c_hi == ny else np.full(nx, CUT, np.uint8)
+        left = g[2 * nx + ny + self.c_lo: 2 * nx + ny + self.c_hi]
+        return np.concatenate([bottom, right, top, left]).astype(np.uint8)
+
+    def local_extents(self, extents):
+        x0, y0, x1, y1 = extents
+        hy = (y1 - y0) / self.ny
+        return (x0, y0 + self.c_lo * hy, x1, y0 + self.c_hi * hy)
+
+    # -- global <-> local vectors (per Radau block) ---------------------------
+    def to_local(self, xg: np.ndarray) -> np.ndarray:
+        """Local block (with ghosts) of a global block vector."""
+        out = np.empty(self.nd_loc, dtype=xg.dtype)
+        out[: self.mv_loc] = xg[self.vel_slice_global(2 * self.c_lo, 2 * self.c_hi + 1)]
+        out[self.mv_loc:] = xg[self.prs_slice_global(self.c_lo, self.c_hi)]
+        return out
+
+    def owned_into_global(self, xl: np.ndarray, xg: np.ndarray):
+        Y0, Y1 = self.owned_node_rows.start, self.owned_node_rows.stop
+        xg[self.vel_slice_global(Y0, Y1)] = xl[self.vel_slice_local(Y0, Y1)]
+        xg[self.prs_slice_global(self.a, self.b)] = xl[self.prs_slice_local(self.a, self.b)]
+
+    # -- exchange plans: lists of (peer, my local slice, peer's local slice) ---
+    def halo_recv(self):
+        """(peer, my ghost slice, peer-owned slice in the peer's local vector) for the x halo."""
+        out = []
+        if self.rank > 0:
+            lo = _layout_of(self, self.rank - 1)
+            out.append((self.rank - 1, self.vel_slice_local(2 * self.c_lo, 2 * self.a),
+                        lo.vel_slice_local(2 * self.c_lo, 2 * self.a)))
+            out.append((self.rank - 1, self.prs_slice_local(self.c_lo, self.a), lo.prs_slice_local(self.c_lo, self.a)))
+        if not self.last:
+            hi = _layout_of(self, self.rank + 1)
+            top = min(2 * self.b + 3, 2 * self.c_hi + 1)
+            out.append((self.rank + 1, self.vel_slice_local(2 * self.b, top), hi.vel_slice_local(2 * self.b, top)))
+        return out
+
+    def defect_recv(self):
+        """The defect of node row 2b (owned by rank+1)."""
+        if self.last:
+            return []
+        hi = _layout_of(self, self.rank + 1)
+        return [(self.rank + 1, self.vel_slice_local(2 * self.b, 2 * self.b + 1),
+                 hi.vel_slice_local(2 * self.b, 2 * self.b + 1))]
+
+    def inc_recv(self):
+        """Increment of node row 2a computed by rank-1 (from its patch of cell a-1)."""
+        if self.rank == 0:
+            return []
+        lo = _layout_of(self, self.rank - 1)
+        return [(self.rank - 1, self.vel_slice_local(2 * self.a, 2 * self.a + 1),
+                 lo.vel_slice_local(2 * self.a, 2 * self.a + 1))]
+
+
+class StripPartition:
+    def __init__(self, nx: int, ny: int, nranks: int):
+        self.nx, self.ny, self.nranks = nx, ny, nranks
+        self.bounds = strip_bounds(ny, nranks)
+
+    def layout(self, rank: int) -> RankLayout:
+        a, b = self.bounds[rank]
+        return RankLayout(rank, self.nranks, self.nx, self.ny, a, b, max(0, a - 2), min(self.ny, b + 2))
+
+
+def _layout_of(lay: RankLayout, rank: int) -> RankLayout:
+    return StripPartition(lay.nx, lay.ny, lay.nranks).layout(rank)
+
+
+# ---------------------------------------------------------------------------
+# Transports
+# ---------------------------------------------------------------------------
+
+
+class LocalTransport:
+    """All ranks' local vectors in one process (same device or host)."""
+
+    def __init__(self, layouts):
+        self.layouts = layouts
+
+    def exchange(self, vectors, plan_name: str, k1: int, add: bool = False):
+        """vectors[r]: rank r's local slab vector (k1 blocks of nd_loc)."""
+        for r, lay in enumerate(self.layouts):
+            for peer, mine, theirs in getattr(lay, plan_name)():
+                nd, ndp = lay.nd_loc, self.layouts[peer].nd_loc
+                for mu in range(k1):
+                    dst = vectors[r][mu * nd + mine.start: mu * nd + mine.stop]
+                    src = vectors[peer][mu * ndp + theirs.start: mu * ndp + theirs.stop]
+                    if add:
+                        dst += src
+                    else:
+                        dst[...] = src
+
+
+class TorchDistTransport:
+    """One rank per process over torch.distributed point-to-point messages.
+
+    For plan entry (peer, mine, theirs) rank r receives into `mine`; the peer
+    sends its slice `theirs` — every rank derives both sides from the
+    partition, so no metadata is exchanged."""
+
+    def __init__(self, layout: RankLayout, part: StripPartition):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.lay = layout
+        self.part = part
+
+    def exchange(self, vec, plan_name: str, k1: int, add: bool = False):
+        import torch
+
+        lay = self.lay
+        ops, recv_bufs = [], []
+        for peer, mine, _ in getattr(lay, plan_name)():
+            buf = torch.empty((k1, mine.stop - mine.start), dtype=vec.dtype, device=vec.device)
+            recv_bufs.append((mine, buf))
+            ops.append(self.dist.P2POp(self.dist.irecv, buf, peer))
+        # what my neighbours receive from me
+        for peer in (lay.rank - 1, lay.rank + 1):
+            if peer < 0 or peer >= lay.nranks:
+                continue
+            pl = self.part.layout(peer)
+            for src_rank, _, theirs in getattr(pl, plan_name)():
+                if src_rank != lay.rank:
+                    continue
+                v2 = vec.view(k1, lay.nd_loc)
+                ops.append(self.dist.P2POp(self.dist.isend, v2[:, theirs].contiguous(), peer))
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+        v2 = vec.view(k1, lay.nd_loc)
+        for mine, buf in recv_bufs:
+            if add:
+                v2[:, mine] += buf
+            else:
+                v2[:, mine] = buf
+
+
+# ---------------------------------------------------------------------------
+# Distributed operators (one local SlabDevice per rank)
+# ---------------------------------------------------------------------------
+
+
+def local_context(ctx, lay: RankLayout):
+    """The reference-style SlabContext of a rank's local mesh (cut tags)."""
+    from .problem import Discretization, QuadMesh, SlabContext, dirichlet_flags
+
+    m = ctx.disc.mesh
+    ext = lay.local_extents((m.x0, m.y0, m.x1, m.y1))
+    tags = lay.local_tags(dirichlet_flags(m))
+    mesh = QuadMesh(m.nx, lay.ny_loc, *ext, boundary_tags=_TagArray(tags))
+    cfg = ctx.config
+    if getattr(cfg, "g_hat", None) is not None:
+        from dataclasses import replace
+
+        cfg = replace(cfg, g_hat=lay.to_local(np.concatenate([np.asarray(cfg.g_hat), np.zeros(3 * m.nx * m.ny)]))[
+            : lay.mv_loc])
+    vm = lay.to_local(np.concatenate([np.asarray(ctx.v_minus), np.zeros(3 * m.nx * m.ny)]))[: lay.mv_loc]
+    return SlabContext(Discretization(mesh), ctx.params, cfg, ctx.data, ctx.basis, ctx.tmat, ctx.t_start, ctx.tau, vm)
+
+
+class _TagArray(np.ndarray):
+    """uint8 tag array understood by problem.dirichlet_flags (0/1/2 verbatim)."""
+
+    def __new__(cls, tags):
+        return np.asarray(tags, dtype=np.uint8).view(cls)
+
+
+class DistributedSlab:
+    """Slab Jacobian + Vanka sweep of one rank of a strip partition."""
+
+    def __init__(self, ctx, U, variant, part: StripPartition, rank: int, transport, device=0, surrogate=True,
+                 rep_fraction=0.5, U_is_local=False):
+        from .operators import SlabJacobian
+        from .smoother import VankaLevel
+
+        self.lay = part.layout(rank)
+        self.k1 = ctx.basis.k + 1
+        self.transport = transport
+        self.ctx = local_context(ctx, self.lay)
+        Ul = U if U_is_local else np.stack([self.lay.to_local(U[mu]) for mu in range(self.k1)])
+        self.jac = SlabJacobian(self.ctx, Ul, variant, device=device)
+        self.level = None
+        self.surrogate, self.rep_fraction = surrogate, rep_fraction
+
+    def build_patches(self):
+        from .smoother import VankaLevel
+
+        self.level = VankaLevel(self.ctx, None, None, surrogate=self.surrogate, rep_fraction=self.rep_fraction,
+                                jac=self.jac)
+        return self.level
+
+    def local(self, xg):
+        """Local (ghosted) slab vector of a global slab vector (numpy)."""
+        nd = self.lay.nd
+        return np.concatenate([self.lay.to_local(xg[mu * nd:(mu + 1) * nd]) for mu in range(self.k1)])
+
+    def owned_into(self, xl, xg):
+        nd, ndl = self.lay.nd, self.lay.nd_loc
+        for mu in range(self.k1):
+            self.lay.owned_into_global(np.asarray(xl[mu * ndl:(mu + 1) * ndl]), xg[mu * nd:(mu + 1) * nd])
+
+
+def distributed_apply(ranks, xs, transport):
+    """y_r = J x on every rank after the x halo exchange (owner computes)."""
+    transport.exchange(xs, "halo_recv", ranks[0].k1)
+    return [rk.jac.matvec(x) for rk, x in zip(ranks, xs)]
+
+
+def distributed_vanka_step(ranks, ds, rs, omega, transport):
+    """One additive Vanka step on every rank; ds updated in place (local)."""
+    k1 = ranks[0].k1
+    transport.exchange(ds, "halo_recv", k1)
+    defects = [rk.jac.defect(d, r) for rk, d, r in zip(ranks, ds, rs)]
+    transport.exchange(defects, "defect_recv", k1)
+    incs = []
+    for rk, df in zip(ranks, defects):
+        lay = rk.lay
+        incs.append(rk.level.increment(df, lay.a - lay.c_lo, lay.b - lay.c_lo, omega))
+    transport.exchange(incs, "inc_recv", k1, add=True)
+    for d, inc in zip(ds, incs):
+        d += inc
+    return ds

@@ -109,11 +109,15 @@ def tag_sides(mesh: QuadMesh, neumann_sides=()) -> QuadMesh:
 
 
 def dirichlet_flags(mesh) -> np.ndarray:
-    """uint8 flags per boundary face (1 = Dirichlet); untagged = all Dirichlet (forms.py:144-145)."""
+    """uint8 tags per boundary face: 1 Dirichlet, 0 Neumann, 2 partition cut
+    (integer tag arrays pass through); untagged = all Dirichlet (forms.py:144-145)."""
     nbf = 2 * (mesh.nx + mesh.ny)
     tags = getattr(mesh, "boundary_tags", None)
     if tags is None:
         return np.ones(nbf, dtype=np.uint8)
+    arr = np.asarray(tags)
+    if arr.dtype.kind in "iu":
+        return arr.astype(np.uint8)
     return np.array([str(t) == DIRICHLET for t in tags], dtype=np.uint8)
 
 
@@ -137,7 +141,7 @@ class Discretization:
 
     @property
     def all_dirichlet(self):
-        return bool(dirichlet_flags(self.mesh).all())
+        return bool((dirichlet_flags(self.mesh) == 1).all())
 
 
 @dataclass

@@ -82,6 +82,16 @@ class VankaLevel:
         return out
 
 
+    def increment(self, defect, row_lo, row_hi, omega):
+        """omega sum_K R_K' A_K^-1 R_K defect over the patches of cell rows [row_lo, row_hi)."""
+        dc = _f64(defect)
+        inc = self.dev.empty_like(dc)
+        w = self.dev.where(dc, inc)
+        L.check(L.lib().pdst_vanka_increment(self.dev.h, self.index, L.vptr(dc), L.vptr(inc), int(row_lo),
+                                             int(row_hi), float(omega), w), "pdst_vanka_increment")
+        return inc
+
+
 def vanka_smooth(level: VankaLevel, d, r, steps: int, omega: float):
     """Damped additive Schwarz sweeps (solver/multigrid.py:327-340)."""
     return level.smooth(d, r, steps, omega)
