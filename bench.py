@@ -13,8 +13,13 @@ write) between timed steps, outside the events.
   python bench.py [--gpus N --steps K --warmup W]      our arm (one JSON line)
   python bench.py --impl reference ...                  CPU reference arm (oracle port)
 
-Multi-GPU: one process per GPU; each rank runs an independent replica (the
-cell-partitioned path with NCCL halos is not in this round), "scaling": "weak".
+Multi-GPU (torchrun, N > 1): weak scaling over the strip partition
+(partition.py).  The global mesh is nx x (N ny) on [0,1]x[0,N]
+(same h as cfg2), rank r owns cell rows [r ny, (r+1) ny) plus two ghost rows per
+side; a step is the distributed apply + Vanka step with the three NCCL
+point-to-point exchanges (x halo, defect row, increment reverse-add).
+``--virtual-ranks P`` runs the same partitioned step with P ranks on one GPU
+(LocalTransport) to exercise the path without NCCL.
 """
 
 from __future__ import annotations
@@ -144,11 +149,160 @@ def run_reference(args):
     return 0
 
 
+def run_distributed(args):
+    """Strip-partitioned step (weak scaling); see the module docstring."""
+    import dataclasses
+
+    import numpy as np
+    import torch
+
+    from paper_2603_28706_b200 import _lib as L
+    from paper_2603_28706_b200 import problem as pb
+    from paper_2603_28706_b200.partition import (DistributedSlab, LocalTransport, StripPartition,
+                                                 TorchDistTransport, distributed_apply, distributed_vanka_step)
+    from paper_2603_28706_b200.synth import CONFIGS, make_slab_inputs
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    P = ws if ws > 1 else args.virtual_ranks
+    base = CONFIGS[args.config]
+    cfg = dataclasses.replace(base, ny=base.ny * P, extents=(0.0, 0.0, 1.0, float(P)))
+    params = pb.ModelParams(cfg.p, cfg.delta, cfg.nu, cfg.nu_inf)
+    conf = pb.DiscretizationConfig(cfg.gamma1, cfg.gamma2, cfg.gamma_cip)
+    syn = make_slab_inputs(cfg)
+    ctx = pb.make_context(cfg.nx, cfg.ny, cfg.k, params, cfg.tau, extents=cfg.extents, config=conf,
+                          v_minus=syn.v_minus)
+    variant = pb.modified_newton(cfg.nu)
+    dev = torch.device("cuda", local)
+    part = StripPartition(cfg.nx, cfg.ny, P)
+    mine = [rank] if ws > 1 else list(range(P))
+    if ws > 1:
+        transport = TorchDistTransport(part.layout(rank), part)
+    else:
+        transport = LocalTransport([part.layout(r) for r in range(P)])
+    t_setup = time.time()
+    ranks = [DistributedSlab(ctx, syn.U, variant, part, r, transport, device=local, rep_fraction=cfg.rep_fraction)
+             for r in mine]
+    for rk in ranks:
+        rk.build_patches()
+    torch.cuda.synchronize()
+    t_setup = time.time() - t_setup
+    xs = [torch.as_tensor(rk.local(syn.x), device=dev) for rk in ranks]
+    rs = [x.clone() for x in xs]
+    ds = [torch.as_tensor(rk.local(syn.d0), device=dev) for rk in ranks]
+    N = syn.x.size
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+
+    def step():
+        distributed_apply(ranks, xs, transport)
+        distributed_vanka_step(ranks, ds, rs, cfg.omega, transport)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    t_end = time.time() + 1.2
+    while time.time() < t_end:
+        step()
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    n_launch0 = L.lib().pdst_launch_count()
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        ev[i][0].record()
+        step()
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    n_launches = L.lib().pdst_launch_count() - n_launch0
+    if dist is not None:
+        dist.barrier()
+    clk = clocks.stop()
+    t_step = sum(a.elapsed_time(b) for a, b in ev) / args.steps / 1e3
+    if dist is not None:
+        tt = torch.tensor([t_step], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step = float(tt.item())
+    value = N / t_step / 1e9
+
+    # e2e: owned inputs from pinned host memory, results back to the host, every step
+    hx = [torch.empty(x.shape, dtype=torch.float64, pin_memory=True) for x in xs]
+    hd = [torch.empty(x.shape, dtype=torch.float64, pin_memory=True) for x in ds]
+    for h, x in zip(hx, xs):
+        h.copy_(x)
+    for h, d in zip(hd, ds):
+        h.copy_(d)
+    hy = [torch.empty_like(h) for h in hx]
+
+    def step_host():
+        for h, x, r in zip(hx, xs, rs):
+            x.copy_(h, non_blocking=True)
+            r.copy_(h, non_blocking=True)
+        for h, d in zip(hd, ds):
+            d.copy_(h, non_blocking=True)
+        ys = distributed_apply(ranks, xs, transport)
+        distributed_vanka_step(ranks, ds, rs, cfg.omega, transport)
+        for h, y in zip(hy, ys):
+            h.copy_(y, non_blocking=True)
+        for h, d in zip(hd, ds):
+            h.copy_(d, non_blocking=True)
+        torch.cuda.synchronize()
+
+    for _ in range(2):
+        step_host()
+    if dist is not None:
+        dist.barrier()
+    n_e2e = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(n_e2e):
+        step_host()
+    t_e2e = (time.perf_counter() - t0) / n_e2e
+    if dist is not None:
+        tt = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    nloc = sum(x.numel() for x in xs)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded 16-mode modal state + 1e-3 noise, SURVEY.md §8d; no dataset)",
+        "config": {"workload": f"{base.name} strips: {cfg.nx}x{cfg.ny} global mesh on [0,1]x[0,{P}], "
+                               f"{base.ny} cell rows per rank + 2 ghost rows per side, DG({cfg.k}), modN, surrogate "
+                               f"patches, omega={cfg.omega}",
+                   "n_dof": N, "step": "distributed Jacobian apply + Vanka step (x halo, defect row, increment "
+                                       "reverse-add exchanges)",
+                   "l2": "flushed between timed steps (256 MiB write, outside events)",
+                   "parallelism": (f"strip partition x{ws} over NCCL send/recv" if ws > 1 else
+                                   f"{P} virtual ranks on one GPU (LocalTransport)")},
+        "gpu_launches": n_launches,
+        "setup_s": t_setup,
+        "clocks": clk,
+        "e2e": {"value": N / t_e2e / 1e9, "unit": UNIT, "h2d_bytes_per_step": 3 * 8 * nloc,
+                "d2h_bytes_per_step": 2 * 8 * nloc, "ms_per_step": t_e2e * 1e3,
+                "note": "per rank: pinned host x, r, d -> device, partitioned step, y and d -> host; wall clock"},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
 def run_ours(args):
     import numpy as np
     import torch
 
     ws, rank, local = dist_env()
+    if ws > 1 or args.virtual_ranks > 1:
+        return run_distributed(args)
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
@@ -199,12 +353,14 @@ def run_ours(args):
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
+    n_launch0 = L.lib().pdst_launch_count()
     for i in range(args.steps):
         flush.fill_(float(i))
         ev[i][0].record()
         step()
         ev[i][1].record()
     torch.cuda.synchronize()
+    n_launches = L.lib().pdst_launch_count() - n_launch0
     if ws > 1:
         torch.distributed.barrier()
     t_end = time.time() + 0.4
@@ -233,7 +389,6 @@ def run_ours(args):
         L.lib().pdst_profile_read(h, kid, L.C.byref(ms), L.C.byref(cnt))
         kt[name] = (ms.value / max(cnt.value, 1), cnt.value)
     L.lib().pdst_profile(h, 0)
-    launches_per_step = 4  # apply + (defect apply, gemv, scatter)
 
     nc, k1 = cfg.nx * cfg.ny, cfg.k + 1
     D = 21 * k1
@@ -268,7 +423,7 @@ def run_ours(args):
 
     def step_host():
         jac.matvec(xh, out=yh)
-        return vanka_smooth(lvl, dh, rh, 1, cfg.omega)
+        return lvl.smooth(dh, rh, 1, cfg.omega, inplace=True)
 
     for _ in range(2):
         step_host()
@@ -285,7 +440,8 @@ def run_ours(args):
         t_e2e = float(tt.item())
     e2e = {"value": ws * N / t_e2e / 1e9, "unit": UNIT, "h2d_bytes_per_step": 3 * 8 * N,
            "d2h_bytes_per_step": 2 * 8 * N, "ms_per_step": t_e2e * 1e3,
-           "note": "SlabJacobian.matvec + vanka_smooth on pinned numpy buffers (libpdst copies in/out), wall clock"}
+           "note": "SlabJacobian.matvec + VankaLevel.smooth(inplace) on pinned numpy buffers through the C ABI "
+                   "(libpdst copies x; d, r in and y; d out), wall clock"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -301,7 +457,7 @@ def run_ours(args):
                    "n_dof": N, "step": "1 Jacobian apply + 1 Vanka sweep (1 smoothing step)",
                    "l2": "flushed between timed steps (256 MiB write, outside events)",
                    "parallelism": f"replicas x{ws}"},
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": n_launches,
         "roofline": {"bound": "hbm", "kernel": f"vanka_gemv (patch-inverse stream, {nblk} complex 21x21 block(s)/patch)",
                      "achieved": ach, "peak": peak,
                      "unit": "GB/s", "frac": ach / peak, "traffic": traffic, "peak_kind": peak_kind,
@@ -339,6 +495,7 @@ def main():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--cpu-steps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--virtual-ranks", type=int, default=1)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -134,6 +134,9 @@ int pdst_profile_read(pdst_handle* h, int kernel, double* total_ms, int64_t* lau
 
 const char* pdst_last_error(void);
 const char* pdst_version(void);
+/* Number of kernels libpdst has launched in this process (all handles); no
+   reference counterpart -- benchmark bookkeeping. */
+int64_t pdst_launch_count(void);
 
 #ifdef __cplusplus
 }

@@ -76,6 +76,7 @@ SIGNATURES = {
     "pdst_profile_read": [P, I, C.POINTER(D), C.POINTER(I64)],
     "pdst_last_error": [],
     "pdst_version": [],
+    "pdst_launch_count": [],
 }
 
 
@@ -89,7 +90,8 @@ def lib():
         for name, args in SIGNATURES.items():
             fn = getattr(L, name)
             fn.argtypes = args
-            fn.restype = C.c_char_p if name in ("pdst_last_error", "pdst_version") else C.c_int
+            fn.restype = (C.c_char_p if name in ("pdst_last_error", "pdst_version") else
+                          C.c_int64 if name == "pdst_launch_count" else C.c_int)
         _lib = L
     return _lib
 

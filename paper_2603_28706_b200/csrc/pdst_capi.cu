@@ -2,6 +2,7 @@
 // host/device pointer staging, argument validation and error reporting.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -153,10 +154,14 @@ int pdst::check_where(int where) {
   return PDST_OK;
 }
 
+static std::atomic<int64_t> g_launches{0};
+void pdst_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 extern "C" {
 
 const char* pdst_last_error(void) { return g_last_error.c_str(); }
 const char* pdst_version(void) { return "pdst-b200 0.1 (sm_100a fp64)"; }
+int64_t pdst_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int pdst_create(const pdst_mesh* mesh, const pdst_time* time, const pdst_disc* disc, const pdst_params* params,
                 double tau, int device, void* stream, pdst_handle** out) {

@@ -673,71 +673,71 @@ __global__ void k_axpy(size_t n, double a, const double* __restrict__ x, double*
 
 cudaError_t prolong(const Geom& gc, const Geom& gf, int k1, const double* ec, double* ef, cudaStream_t st) {
   const size_t n = (size_t)gf.nnx * gf.nny + gf.ncells;
-  k_prolong<<<dim3((unsigned)((n + 255) / 256), k1), 256, 0, st>>>(gc, gf, k1, ec, ef);
+  PDST_LAUNCH(k_prolong<<<dim3((unsigned)((n + 255) / 256), k1), 256, 0, st>>>(gc, gf, k1, ec, ef));
   return cudaGetLastError();
 }
 
 cudaError_t restrict_(const Geom& gc, const Geom& gf, int k1, const double* rf, double* rc, cudaStream_t st) {
   const size_t n = (size_t)gc.nnx * gc.nny + gc.ncells;
-  k_restrict<<<dim3((unsigned)((n + 255) / 256), k1), 256, 0, st>>>(gc, gf, k1, rf, rc);
+  PDST_LAUNCH(k_restrict<<<dim3((unsigned)((n + 255) / 256), k1), 256, 0, st>>>(gc, gf, k1, rf, rc));
   return cudaGetLastError();
 }
 
 cudaError_t galerkin(const LevelOp& fine, const Geom& gc, int k1, double* ecell_c, double* fv_c, double* fh_c,
                      cudaStream_t st) {
-  k_galerkin_cells<<<dim3(gc.ncells, k1), 448, 0, st>>>(fine, gc, ecell_c);
+  PDST_LAUNCH(k_galerkin_cells<<<dim3(gc.ncells, k1), 448, 0, st>>>(fine, gc, ecell_c));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int nf = max((gc.nx - 1) * gc.ny, gc.nx * (gc.ny - 1));
-  if (nf > 0) k_galerkin_faces<<<dim3(nf, k1, 2), 324, 0, st>>>(fine, gc, fv_c, fh_c);
+  if (nf > 0) PDST_LAUNCH(k_galerkin_faces<<<dim3(nf, k1, 2), 324, 0, st>>>(fine, gc, fv_c, fh_c));
   return cudaGetLastError();
 }
 
 cudaError_t level_apply(const LevelOp& op, const TimeData& td, const double* x, const double* rhs, double* y,
                         cudaStream_t st) {
   const size_t n = (size_t)op.g.nnx * op.g.nny + op.g.ncells;
-  k_level_apply<<<dim3((unsigned)((n + 127) / 128), td.k1), 128, 0, st>>>(op, td, x, rhs, y);
+  PDST_LAUNCH(k_level_apply<<<dim3((unsigned)((n + 127) / 128), td.k1), 128, 0, st>>>(op, td, x, rhs, y));
   return cudaGetLastError();
 }
 
 cudaError_t patch_assemble_level(const LevelOp& op, const TimeData& td, double* mats, cudaStream_t st) {
-  k_patch_level<<<op.g.ncells, 448, 0, st>>>(op, td, mats);
+  PDST_LAUNCH(k_patch_level<<<op.g.ncells, 448, 0, st>>>(op, td, mats));
   return cudaGetLastError();
 }
 
 cudaError_t dense_build(const LevelOp& op, const TimeData& td, bool pin, double* A, double* scratch, int* piv,
                         int* bad, cudaStream_t st) {
   const int n = td.k1 * op.g.nd;
-  k_dense_assemble<<<(n + 127) / 128, 128, 0, st>>>(op, td, A, n);
+  PDST_LAUNCH(k_dense_assemble<<<(n + 127) / 128, 128, 0, st>>>(op, td, A, n));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (pin) {
-    k_diag_abs_sum<<<1, 1024, 0, st>>>(A, n, scratch);
+    PDST_LAUNCH(k_diag_abs_sum<<<1, 1024, 0, st>>>(A, n, scratch));
     double scale = 0.0;
     e = cudaMemcpyAsync(&scale, scratch, sizeof(double), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return e;
     const size_t tot = (size_t)op.g.ncells * op.g.ncells * td.k1;
-    k_dense_pin<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(op.g, td.k1, A, n, scale);
+    PDST_LAUNCH(k_dense_pin<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(op.g, td.k1, A, n, scale));
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  k_dense_invert<<<1, 1024, 0, st>>>(A, n, piv, bad);
+  PDST_LAUNCH(k_dense_invert<<<1, 1024, 0, st>>>(A, n, piv, bad));
   return cudaGetLastError();
 }
 
 cudaError_t dense_solve(const double* Ainv, int n, const double* b, double* y, cudaStream_t st) {
-  k_dense_gemv<<<(n * 32 + 255) / 256, 256, 0, st>>>(Ainv, n, b, y);
+  PDST_LAUNCH(k_dense_gemv<<<(n * 32 + 255) / 256, 256, 0, st>>>(Ainv, n, b, y));
   return cudaGetLastError();
 }
 
 cudaError_t project_pressure(const Geom& g, int k1, double* z, cudaStream_t st) {
-  k_project_pressure<<<k1, 1024, 0, st>>>(g, z);
+  PDST_LAUNCH(k_project_pressure<<<k1, 1024, 0, st>>>(g, z));
   return cudaGetLastError();
 }
 
 cudaError_t axpy(size_t n, double a, const double* x, double* y, cudaStream_t st) {
-  k_axpy<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, a, x, y);
+  PDST_LAUNCH(k_axpy<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, a, x, y));
   return cudaGetLastError();
 }
 

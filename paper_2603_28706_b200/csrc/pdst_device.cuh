@@ -22,6 +22,15 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Process-wide count of libpdst kernel launches (pdst_launch_count; the
+// bench's gpu_launches).  Every launch site goes through PDST_LAUNCH.
+void pdst_count_launch();
+#define PDST_LAUNCH(...)   \
+  do {                     \
+    __VA_ARGS__;           \
+    pdst_count_launch();   \
+  } while (0)
+
 namespace pdst {
 
 constexpr int MAXK1 = 7;

@@ -14,6 +14,7 @@
 
 #include "../../include/pdst.h"
 #include "pdst_handle.h"
+#include "pdst_device.cuh"
 #include "pdst_coarse.h"
 #include "pdst_patch.h"
 
@@ -102,7 +103,7 @@ int pdst_cell_maps(pdst_handle* h, int64_t* cell_nodes, int64_t* patch_ids) {
   int64_t* dev = nullptr;
   const size_t n1 = (size_t)g.ncells * 9, n2 = (size_t)g.ncells * 21 * k1;
   CK(cudaMalloc(&dev, (n1 + n2) * sizeof(int64_t)));
-  k_cell_maps<<<(g.ncells + 127) / 128, 128, 0, h->stream>>>(g.nx, g.ny, g.nd, k1, dev, dev + n1);
+  PDST_LAUNCH(k_cell_maps<<<(g.ncells + 127) / 128, 128, 0, h->stream>>>(g.nx, g.ny, g.nd, k1, dev, dev + n1));
   cudaError_t e = cudaMemcpyAsync(cell_nodes, dev, n1 * sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(patch_ids, dev + n1, n2 * sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream);

@@ -77,6 +77,7 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool v
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(sz) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p)); }
 
 // Issue the asynchronous staging of one velocity block (zero outside the
 // domain); the caller waits with cp_async_wait_all() + __syncthreads().
@@ -665,6 +666,11 @@ __device__ __forceinline__ void jac_volume(const Geom& g, const Disc& ds, const 
     gn[qy] = hg ? __ldg(pg + qy) : 0.0;
   }
       // ---- volume (forms.py:589-603) ----
+  double R[3][3][2];
+#pragma unroll
+  for (int jy = 0; jy < 3; ++jy)
+#pragma unroll
+    for (int ix = 0; ix < 3; ++ix) R[jy][ix][0] = R[jy][ix][1] = 0.0;
 #pragma unroll 1
       for (int qx = 0; qx < 4; ++qx) {
         double ec[4], gc[4];
@@ -743,8 +749,14 @@ __device__ __forceinline__ void jac_volume(const Geom& g, const Disc& ds, const 
           for (int ix = 0; ix < 3; ++ix)
 #pragma unroll
             for (int d = 0; d < 2; ++d)
-              acc.add(jy, ix, d, (c_tab.G[qx][ix] * g.ihx) * Pa[jy][d] + (c_tab.B[qx][ix] * g.ihy) * Qa[jy][d]);
+              R[jy][ix][d] += (c_tab.G[qx][ix] * g.ihx) * Pa[jy][d] + (c_tab.B[qx][ix] * g.ihy) * Qa[jy][d];
       }
+#pragma unroll
+  for (int jy = 0; jy < 3; ++jy)
+#pragma unroll
+    for (int ix = 0; ix < 3; ++ix)
+#pragma unroll
+      for (int d = 0; d < 2; ++d) acc.add(jy, ix, d, R[jy][ix][d]);
 }
 
 // The cell's boundary sides (forms.py:605-637).
@@ -929,16 +941,18 @@ __device__ __forceinline__ void stage_planned(const StagePlan& sp, const double*
   }
 }
 
-// PIPE (K1 <= 2): every Radau node's state / rhs planes are staged up front and
-// the per-cell slots are double buffered, so the assembly of node mu overlaps
-// the compute of node mu+1 (one barrier per node instead of two).
+// Two CTAs per SM (<= 128 registers, ~105 KB shared for K1 = 2) so that a
+// 256x256 mesh (256 tiles) runs in one wave on 148 SMs and one CTA's barriers
+// are covered by the other's compute.  That budget has no room for the
+// double-buffered "PIPE" variant (all Radau nodes' state planes staged up
+// front, two slot buffers), which is kept compiled out.
 template <int K1>
-__host__ __device__ constexpr bool jac_pipe() { return K1 <= 2; }
+__host__ __device__ constexpr bool jac_pipe() { return false; }
 template <int K1>
 __host__ __device__ constexpr int jac_nbuf() { return jac_pipe<K1>() ? K1 : 1; }
 
 template <int K1>
-__global__ void __launch_bounds__(JNT, 1) k_jacobian(Geom g, TimeData td, Disc ds, Lin L, const double* __restrict__ state,
+__global__ void __launch_bounds__(JNT, 2) k_jacobian(Geom g, TimeData td, Disc ds, Lin L, const double* __restrict__ state,
                                                   const double* __restrict__ x, const double* __restrict__ rhs,
                                                   double* __restrict__ out, double* __restrict__ part,
                                                   const double* __restrict__ ybnd) {
@@ -947,8 +961,7 @@ __global__ void __launch_bounds__(JNT, 1) k_jacobian(Geom g, TimeData td, Disc d
   extern __shared__ double smem[];
   double* xs = smem;                             // [K1][2][PLANE] direction x_nu, all Radau nodes (one-cell ring)
   double* ss0 = xs + (size_t)K1 * 2 * PLANE;      // [NB][2][PLANE] state v_mu
-  double* rs0 = ss0 + (size_t)NB * 2 * PLANE;     // [NB][2][PLANE] rhs block mu (defect mode)
-  double* sacc0 = rs0 + (size_t)NB * 2 * PLANE;   // [NB][18][JNT]  per-cell node contributions
+  double* sacc0 = ss0 + (size_t)NB * 2 * PLANE;   // [NB][18][JNT]  per-cell node contributions
   const int bx = blockIdx.x, by = blockIdx.y;
   const int i0 = bx * JT, j0 = by * JT;
   const int X0 = 2 * (i0 - 1), Y0 = 2 * (j0 - 1);
@@ -968,30 +981,32 @@ __global__ void __launch_bounds__(JNT, 1) k_jacobian(Geom g, TimeData td, Disc d
   // last row / column of nodes for the last cell column / row
   const bool lastx = tx == ntx - 1, lasty = ty == nty - 1;
 
-  StagePlan plan;
-  stage_plan(g, X0, Y0, plan);
-  for (int nu = 0; nu < K1; ++nu)
-    stage_planned(plan, x + (size_t)nu * g.nd, xs + (size_t)nu * 2 * PLANE, xs + (size_t)nu * 2 * PLANE + PLANE);
-  if (PIPE) {
-    for (int nu = 0; nu < K1; ++nu) {
-      stage_planned(plan, state + (size_t)nu * g.mv, ss0 + (size_t)nu * 2 * PLANE, ss0 + (size_t)nu * 2 * PLANE + PLANE);
-      if (rhs)
-        stage_planned(plan, rhs + (size_t)nu * g.nd, rs0 + (size_t)nu * 2 * PLANE, rs0 + (size_t)nu * 2 * PLANE + PLANE);
+  // pull this cell's eta / gamma lines (128 B each per Radau node) towards L2
+  // now; the volume loop reads them one Gauss column at a time
+  if (valid && ds.viscous) {
+#pragma unroll
+    for (int mu = 0; mu < K1; ++mu) {
+      prefetch_l2(L.eta + ((size_t)mu * g.ncells + c) * 16);
+      if (L.has_gamma) prefetch_l2(L.gam + ((size_t)mu * g.ncells + c) * 16);
     }
+  }
+  for (int nu = 0; nu < K1; ++nu)
+    stage_velocity_async(g, x + (size_t)nu * g.nd, xs + (size_t)nu * 2 * PLANE, xs + (size_t)nu * 2 * PLANE + PLANE,
+                         X0, Y0);
+  if (PIPE) {
+    for (int nu = 0; nu < K1; ++nu)
+      stage_velocity_async(g, state + (size_t)nu * g.mv, ss0 + (size_t)nu * 2 * PLANE,
+                           ss0 + (size_t)nu * 2 * PLANE + PLANE, X0, Y0);
   }
   for (int mu = 0; mu < K1; ++mu) {
     const double tw = td.tau_w[mu];
     const int buf = PIPE ? mu : 0;
     double* ss = ss0 + (size_t)buf * 2 * PLANE;
-    double* rs = rs0 + (size_t)buf * 2 * PLANE;
     double* sacc = sacc0 + (size_t)buf * 18 * JNT;
     const Plane2 SP{ss, ss + PLANE};
-    const Plane2 RP{rs, rs + PLANE};
     const SmemAcc slot{sacc + threadIdx.x};
-    if (!PIPE) {
-      stage_planned(plan, state + (size_t)mu * g.mv, ss, ss + PLANE);
-      if (rhs) stage_planned(plan, rhs + (size_t)mu * g.nd, rs, rs + PLANE);
-    }
+    if (!PIPE) stage_velocity_async(g, state + (size_t)mu * g.mv, ss, ss + PLANE, X0, Y0);
+    const Plane2 XM{xs + (size_t)mu * 2 * PLANE, xs + (size_t)mu * 2 * PLANE + PLANE};
     double P[3] = {0.0, 0.0, 0.0};
     if (valid) {
       const double* xp = x + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
@@ -1008,14 +1023,14 @@ __global__ void __launch_bounds__(JNT, 1) k_jacobian(Geom g, TimeData td, Disc d
     if (valid) {
       double accp[3] = {0.0, 0.0, 0.0};
       // tau w_mu J_mu x_mu: volume, boundary sides, CIP faces (weights carry tau w_mu)
-      if (!(ds.skip & 1)) jac_volume(g, ds, L, mu, c, XP[mu], SP, r0, c0, P, slot, accp, tw);
+      if (!(ds.skip & 1)) jac_volume(g, ds, L, mu, c, XM, SP, r0, c0, P, slot, accp, tw);
       if (!(ds.skip & 4)) {
         if (ybnd)
           jac_sides_pre(g, ybnd, mu, ci, cj, slot, accp, tw);
         else
-          jac_sides(g, ds, L, mu, ci, cj, XP[mu], SP, r0, c0, P, slot, accp, tw);
+          jac_sides(g, ds, L, mu, ci, cj, XM, SP, r0, c0, P, slot, accp, tw);
       }
-      if (cip && !(ds.skip & 2)) cip_all(g, ds, XP[mu], SP, ci, cj, r0, c0, tw, slot);
+      if (cip && !(ds.skip & 2)) cip_all(g, ds, XM, SP, ci, cj, r0, c0, tw, slot);
       // + M_K sum_nu K_t[mu,nu] x_nu (slab.py:199-200)
       if (!(ds.skip & 8)) add_mass<K1>(XP, nullptr, 0.0, td.K_t + mu * K1, r0, c0, g.hx * g.hy, slot);
       const size_t o = (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
@@ -1057,8 +1072,8 @@ __global__ void __launch_bounds__(JNT, 1) k_jacobian(Geom g, TimeData td, Disc d
           } else {
             const size_t o = base + 2 * ((size_t)(2 * j0 + ly) * g.nnx + 2 * i0 + lx);
             if (rhs) {
-              s0 = RP.at(0, ly + 2, lx + 2) - s0;
-              s1 = RP.at(1, ly + 2, lx + 2) - s1;
+              s0 = __ldg(rhs + o) - s0;
+              s1 = __ldg(rhs + o + 1) - s1;
             }
             out[o] = s0;
             out[o + 1] = s1;
@@ -1504,7 +1519,7 @@ __global__ void __launch_bounds__(128) k_boundary_matrices(Geom g, Disc ds, Lin 
 template <int K1>
 size_t jac_smem() {
   constexpr int NB = jac_nbuf<K1>();
-  return ((size_t)(2 * K1 + 4 * NB) * PLANE + (size_t)NB * JNT * 18) * sizeof(double);
+  return ((size_t)(2 * K1 + 2 * NB) * PLANE + (size_t)NB * JNT * 18) * sizeof(double);
 }
 template <int K1>
 size_t res_smem() {
@@ -1525,16 +1540,16 @@ cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const 
   if (L.bmat) {
     ybnd = part + (size_t)K1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2;
     const size_t nb = (size_t)21 * g.nbf;
-    k_boundary_apply<<<dim3((unsigned)((nb + 127) / 128), K1), 128, 0, st>>>(g, K1, L.bmat, x, ybnd);
+    PDST_LAUNCH(k_boundary_apply<<<dim3((unsigned)((nb + 127) / 128), K1), 128, 0, st>>>(g, K1, L.bmat, x, ybnd));
   }
   dim3 grid(jac_tiles_x(g), jac_tiles_y(g));
-  k_jacobian<K1><<<grid, JNT, sm, st>>>(g, td, ds, L, state, x, rhs, out, part, ybnd);
+  PDST_LAUNCH(k_jacobian<K1><<<grid, JNT, sm, st>>>(g, td, ds, L, state, x, rhs, out, part, ybnd));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const size_t nfix = (size_t)(jac_tiles_x(g) - 1) * g.nny + (size_t)(jac_tiles_y(g) - 1) * g.nnx;
   if (nfix > 0) {
     dim3 fg((unsigned)((nfix + 255) / 256), K1);
-    k_jac_fixup<JT><<<fg, 256, 0, st>>>(g, K1, part, rhs, out);
+    PDST_LAUNCH(k_jac_fixup<JT><<<fg, 256, 0, st>>>(g, K1, part, rhs, out));
   }
   return cudaGetLastError();
 }
@@ -1551,7 +1566,7 @@ cudaError_t launch_res(const Geom& g, const TimeData& td, const Disc& ds, const 
     configured = true;
   }
   dim3 grid((g.nx + TX - 1) / TX, (g.ny + TY - 1) / TY);
-  k_residual<K1><<<grid, NT, sm, st>>>(g, td, ds, m, L, U, advect, vminus, fqp, ghat, out);
+  PDST_LAUNCH(k_residual<K1><<<grid, NT, sm, st>>>(g, td, ds, m, L, U, advect, vminus, fqp, ghat, out));
   return cudaGetLastError();
 }
 
@@ -1589,31 +1604,31 @@ cudaError_t slab_residual(const Geom& g, const TimeData& td, const Disc& ds, con
 cudaError_t linearize(const Geom& g, const Model& m, int k1, const double* state, double* eta, double* gam,
                       double* etaf, double* gamf, cudaStream_t st) {
   dim3 gc((g.ncells + 127) / 128, k1);
-  k_linearize_cells<<<gc, 128, 0, st>>>(g, m, k1, state, eta, gam);
+  PDST_LAUNCH(k_linearize_cells<<<gc, 128, 0, st>>>(g, m, k1, state, eta, gam));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   dim3 gf((g.nbf * 4 + 127) / 128, k1);
-  k_linearize_faces<<<gf, 128, 0, st>>>(g, m, k1, state, etaf, gamf);
+  PDST_LAUNCH(k_linearize_faces<<<gf, 128, 0, st>>>(g, m, k1, state, etaf, gamf));
   return cudaGetLastError();
 }
 
 cudaError_t element_matrices(const Geom& g, const Disc& ds, const Lin& L, int mu, const double* state, double* ET,
                              cudaStream_t st) {
   const size_t n = (size_t)g.ncells * 21;
-  k_element_matrices<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(g, ds, L, mu, state, ET);
+  PDST_LAUNCH(k_element_matrices<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(g, ds, L, mu, state, ET));
   return cudaGetLastError();
 }
 
 cudaError_t boundary_matrices(const Geom& g, const Disc& ds, const Lin& L, int k1, const double* state, double* bmat,
                               cudaStream_t st) {
   const size_t n = (size_t)g.nbf * 21;
-  k_boundary_matrices<<<dim3((unsigned)((n + 127) / 128), k1), 128, 0, st>>>(g, ds, L, k1, state, bmat);
+  PDST_LAUNCH(k_boundary_matrices<<<dim3((unsigned)((n + 127) / 128), k1), 128, 0, st>>>(g, ds, L, k1, state, bmat));
   return cudaGetLastError();
 }
 
 cudaError_t lifting(const Geom& g, const Model& m, const double* ghat, double* etad, double* betad, double* dg,
                     cudaStream_t st) {
-  k_lifting<<<(g.nbf * 4 + 127) / 128, 128, 0, st>>>(g, m, ghat, etad, betad, dg);
+  PDST_LAUNCH(k_lifting<<<(g.nbf * 4 + 127) / 128, 128, 0, st>>>(g, m, ghat, etad, betad, dg));
   return cudaGetLastError();
 }
 

@@ -311,21 +311,21 @@ cudaError_t launch_invert(const double* mats, double* invT, int np, int* bad, cu
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  k_invert<D><<<(np + WPB - 1) / WPB, 32 * WPB, smem, st>>>(mats, invT, np, bad);
+  PDST_LAUNCH(k_invert<D><<<(np + WPB - 1) / WPB, 32 * WPB, smem, st>>>(mats, invT, np, bad));
   return cudaGetLastError();
 }
 
 template <int D>
 cudaError_t launch_gemv(const Geom& g, const double* invT, const double* defect, double* upd, cudaStream_t st) {
   constexpr int PB = 256 / D;
-  k_vanka_gemv<D><<<(g.ncells + PB - 1) / PB, 256, 0, st>>>(g, invT, defect, upd);
+  PDST_LAUNCH(k_vanka_gemv<D><<<(g.ncells + PB - 1) / PB, 256, 0, st>>>(g, invT, defect, upd));
   return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t patch_assemble(const PatchArgs& a, cudaStream_t st) {
-  k_patch_fine<<<a.g.ncells, 448, 0, st>>>(a);
+  PDST_LAUNCH(k_patch_fine<<<a.g.ncells, 448, 0, st>>>(a));
   return cudaGetLastError();
 }
 
@@ -354,7 +354,7 @@ cudaError_t vanka_scatter(const Geom& g, int k1, const double* upd, double omega
   if (row_hi < 0) row_hi = g.ny;
   const size_t n = (size_t)g.nnx * g.nny + g.ncells;
   dim3 grid((unsigned)((n + 255) / 256), k1);
-  k_vanka_scatter<<<grid, 256, 0, st>>>(g, k1, upd, omega, d, row_lo, row_hi, inc_only ? 1 : 0);
+  PDST_LAUNCH(k_vanka_scatter<<<grid, 256, 0, st>>>(g, k1, upd, omega, d, row_lo, row_hi, inc_only ? 1 : 0));
   return cudaGetLastError();
 }
 

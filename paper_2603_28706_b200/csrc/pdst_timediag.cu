@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(252) k_vanka_gemv_diag(Geom g, TimeDiag td, co
 cudaError_t patch_invert_diag(const Geom& g, const TimeDiag& td, const double* spatial, double2* binvT, int* bad,
                               cudaStream_t st) {
   const int tasks = g.ncells * td.nblk;
-  k_invert_diag<<<(tasks + 3) / 4, 128, 0, st>>>(g, td, spatial, binvT, bad);
+  PDST_LAUNCH(k_invert_diag<<<(tasks + 3) / 4, 128, 0, st>>>(g, td, spatial, binvT, bad));
   return cudaGetLastError();
 }
 
@@ -409,14 +409,14 @@ cudaError_t vanka_gemv_diag(const Geom& g, const TimeDiag& td, const double2* bi
                             double* upd, cudaStream_t st) {
   const unsigned grid = (unsigned)((g.ncells + 11) / 12);
   switch (td.k1 * 10 + td.nblk) {
-    case 11: k_vanka_gemv_diag<1, 1><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd); break;
-    case 21: k_vanka_gemv_diag<2, 1><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd); break;
-    case 22: k_vanka_gemv_diag<2, 2><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd); break;
-    case 32: k_vanka_gemv_diag<3, 2><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd); break;
-    case 33: k_vanka_gemv_diag<3, 3><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd); break;
-    case 42: k_vanka_gemv_diag<4, 2><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd); break;
-    case 43: k_vanka_gemv_diag<4, 3><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd); break;
-    case 44: k_vanka_gemv_diag<4, 4><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd); break;
+    case 11: PDST_LAUNCH(k_vanka_gemv_diag<1, 1><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd)); break;
+    case 21: PDST_LAUNCH(k_vanka_gemv_diag<2, 1><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd)); break;
+    case 22: PDST_LAUNCH(k_vanka_gemv_diag<2, 2><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd)); break;
+    case 32: PDST_LAUNCH(k_vanka_gemv_diag<3, 2><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd)); break;
+    case 33: PDST_LAUNCH(k_vanka_gemv_diag<3, 3><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd)); break;
+    case 42: PDST_LAUNCH(k_vanka_gemv_diag<4, 2><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd)); break;
+    case 43: PDST_LAUNCH(k_vanka_gemv_diag<4, 3><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd)); break;
+    case 44: PDST_LAUNCH(k_vanka_gemv_diag<4, 4><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd)); break;
     default: return cudaErrorNotSupported;
   }
   return cudaGetLastError();

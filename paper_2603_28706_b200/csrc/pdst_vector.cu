@@ -153,26 +153,26 @@ int reduce_partials() { return RPARTS; }
 cudaError_t mass_apply(const Geom& g, const TimeData& td, const double* x, double* y, cudaStream_t st) {
   const size_t n = (size_t)g.nnx * g.nny + g.ncells;
   dim3 grid((unsigned)((n + 255) / 256), td.k1);
-  k_mass_apply<<<grid, 256, 0, st>>>(g, td, x, y);
+  PDST_LAUNCH(k_mass_apply<<<grid, 256, 0, st>>>(g, td, x, y));
   return cudaGetLastError();
 }
 
 cudaError_t mass_dot(const Geom& g, const TimeData& td, const double* a, const double* b, double* partials,
                      double* result, cudaStream_t st) {
-  k_mass_dot_partial<<<RPARTS, RB, 0, st>>>(g, td, a, b, partials);
-  k_finish<<<1, 1024, 0, st>>>(partials, RPARTS, result);
+  PDST_LAUNCH(k_mass_dot_partial<<<RPARTS, RB, 0, st>>>(g, td, a, b, partials));
+  PDST_LAUNCH(k_finish<<<1, 1024, 0, st>>>(partials, RPARTS, result));
   return cudaGetLastError();
 }
 
 cudaError_t dot(const double* a, const double* b, size_t n, double* partials, double* result, cudaStream_t st) {
-  k_dot_partial<<<RPARTS, RB, 0, st>>>(a, b, n, partials);
-  k_finish<<<1, 1024, 0, st>>>(partials, RPARTS, result);
+  PDST_LAUNCH(k_dot_partial<<<RPARTS, RB, 0, st>>>(a, b, n, partials));
+  PDST_LAUNCH(k_finish<<<1, 1024, 0, st>>>(partials, RPARTS, result));
   return cudaGetLastError();
 }
 
 cudaError_t copy_velocity_blocks(const Geom& g, int k1, const double* U, double* V, cudaStream_t st) {
   dim3 grid((unsigned)((g.mv + 255) / 256), k1);
-  k_copy_velocity<<<grid, 256, 0, st>>>(g, k1, U, V);
+  PDST_LAUNCH(k_copy_velocity<<<grid, 256, 0, st>>>(g, k1, U, V));
   return cudaGetLastError();
 }
 
@@ -180,7 +180,7 @@ cudaError_t blend_velocity(const Geom& g, int k1, const double* coef, const doub
                            cudaStream_t st) {
   Coef7 cf{};
   for (int i = 0; i < k1 && i < MAXK1; ++i) cf.c[i] = coef[i];
-  k_blend<<<(unsigned)((g.mv + 255) / 256), 256, 0, st>>>(g, k1, cf, U, stride, V);
+  PDST_LAUNCH(k_blend<<<(unsigned)((g.mv + 255) / 256), 256, 0, st>>>(g, k1, cf, U, stride, V));
   return cudaGetLastError();
 }
 

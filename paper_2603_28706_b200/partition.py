@@ -219,6 +219,8 @@ class TorchDistTransport:
     def exchange(self, vec, plan_name: str, k1: int, add: bool = False):
         import torch
 
+        if isinstance(vec, (list, tuple)):  # the distributed_* helpers pass one vector per local rank
+            (vec,) = vec
         lay = self.lay
         ops, recv_bufs = [], []
         for peer, mine, _ in getattr(lay, plan_name)():

@@ -70,10 +70,15 @@ class VankaLevel:
 
     def smooth(self, d, r, steps, omega, inplace=False):
         """d <- d + omega sum_K R_K' A_K^-1 R_K (r - A d), `steps` times.
-        Returns a new array unless inplace (device tensors only)."""
+        Returns a new array unless inplace (a device tensor, or a C-contiguous
+        writable float64 host array -- e.g. pinned -- updated through the C ABI)."""
         rc_ = _f64(r)
         if _is_torch(d):
             out = d if inplace else d.clone()
+        elif inplace:
+            if not (isinstance(d, np.ndarray) and d.dtype == np.float64 and d.flags.c_contiguous and d.flags.writeable):
+                raise TypeError("inplace smoothing needs a C-contiguous writable float64 array")
+            out = d
         else:
             out = np.array(d, dtype=np.float64, copy=True)
         w = self.dev.where(out, rc_)

@@ -9,7 +9,7 @@ ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
 
 def declared_symbols():
     text = open(os.path.join(ROOT, "include", "pdst.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(pdst_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(pdst_\w+)\s*\(", text, re.M)))
 
 
 def test_header_symbols_exported():
@@ -28,3 +28,9 @@ def test_version_and_error_string():
 
     assert b"sm_100a" in _lib.lib().pdst_version()
     assert isinstance(_lib.lib().pdst_last_error(), bytes)
+
+
+def test_launch_counter_starts_at_zero():
+    from paper_2603_28706_b200 import _lib
+
+    assert _lib.lib().pdst_launch_count() == 0
