@@ -404,13 +404,14 @@ def run_ours(args):
     t_gemv = kt["vanka_gemv"][0] * 1e-3
     t_jac = kt["jacobian"][0] * 1e-3
     ach = b_gemv / t_gemv / 1e9
-    traffic = None
+    traffic = traffic_apply = None
     tp = os.path.join(ROOT, "profiles", "traffic_r01.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp):  # dram bytes per launch from one `ncu --set full` capture (scripts/ncu_traffic.py)
         try:
-            traffic = json.load(open(tp)).get("vanka_gemv")
+            tr = json.load(open(tp))
+            traffic, traffic_apply = tr.get("vanka_gemv"), tr.get("jacobian_apply")
         except Exception:
-            traffic = None
+            traffic = traffic_apply = None
 
     # -- e2e through the public API with host (pinned) buffers ---------------
     def pinned(a):
@@ -458,10 +459,19 @@ def run_ours(args):
                    "l2": "flushed between timed steps (256 MiB write, outside events)",
                    "parallelism": f"replicas x{ws}"},
         "gpu_launches": n_launches,
-        "roofline": {"bound": "hbm", "kernel": f"vanka_gemv (patch-inverse stream, {nblk} complex 21x21 block(s)/patch)",
-                     "achieved": ach, "peak": peak,
-                     "unit": "GB/s", "frac": ach / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "algorithmic_bytes": b_gemv, "launch_ms": kt["vanka_gemv"][0]},
+        # dominant kernel by time: the Jacobian apply (2 launches per step).  Its
+        # algorithmic bytes are SURVEY §8(d)'s B_apply (the reference algorithm's
+        # compulsory traffic: x, y and the per-qp / side / CIP coefficient cache).
+        "roofline": {"bound": "hbm", "kernel": "jacobian apply (k_boundary_apply + k_jacobian + k_jac_fixup)",
+                     "achieved": b_apply_ref / t_jac / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": b_apply_ref / t_jac / 1e9 / peak, "traffic": traffic_apply, "peak_kind": peak_kind,
+                     "algorithmic_bytes": b_apply_ref, "launch_ms": kt["jacobian"][0],
+                     "note": "FP64-issue / latency bound in practice (DESIGN.md §4); bytes actually moved are "
+                             "the minimal x, y, state, eta/gamma set (kernels.jacobian_apply.algorithmic_bytes)"},
+        "roofline_gemv": {"bound": "hbm", "kernel": f"vanka_gemv (patch-inverse stream, {nblk} complex 21x21 "
+                                                    f"block(s)/patch)",
+                          "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
+                          "peak_kind": peak_kind, "algorithmic_bytes": b_gemv, "launch_ms": kt["vanka_gemv"][0]},
         "kernels": {
             "jacobian_apply": {"ms": kt["jacobian"][0], "gdofs": N / t_jac / 1e9,
                                "algorithmic_bytes": b_apply_ours, "gbs": b_apply_ours / t_jac / 1e9,

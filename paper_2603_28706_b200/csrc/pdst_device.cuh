@@ -25,6 +25,30 @@
 // Process-wide count of libpdst kernel launches (pdst_launch_count; the
 // bench's gpu_launches).  Every launch site goes through PDST_LAUNCH.
 void pdst_count_launch();
+// Programmatic dependent launch (PDL): a kernel launched with launch_pdl may
+// start while its stream predecessor is still running once every CTA of the
+// predecessor has called pdl_trigger(); pdl_wait() then blocks until the
+// predecessor has completed and its writes are visible (a no-op for a normal
+// launch).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 #define PDST_LAUNCH(...)   \
   do {                     \
     __VA_ARGS__;           \

@@ -862,6 +862,7 @@ __device__ __forceinline__ int perim(int lx, int ly) { return perim_t<JT>(lx, ly
 // Runs before k_jacobian so boundary cells only add 21 precomputed values.
 __global__ void k_boundary_apply(Geom g, int k1, const double* __restrict__ bmat, const double* __restrict__ x,
                                  double* __restrict__ ybnd) {
+  pdl_trigger();  // k_jacobian may start now; its boundary cells wait for ybnd
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int mu = blockIdx.y;
   const int i = (int)(t / g.nbf), bf = (int)(t % g.nbf);
@@ -981,6 +982,7 @@ __global__ void __launch_bounds__(JNT, 2) k_jacobian(Geom g, TimeData td, Disc d
   // last row / column of nodes for the last cell column / row
   const bool lastx = tx == ntx - 1, lasty = ty == nty - 1;
 
+  pdl_trigger();  // k_jac_fixup may be scheduled; it waits for this grid
   // pull this cell's eta / gamma lines (128 B each per Radau node) towards L2
   // now; the volume loop reads them one Gauss column at a time
   if (valid && ds.viscous) {
@@ -1026,7 +1028,10 @@ __global__ void __launch_bounds__(JNT, 2) k_jacobian(Geom g, TimeData td, Disc d
       if (!(ds.skip & 1)) jac_volume(g, ds, L, mu, c, XM, SP, r0, c0, P, slot, accp, tw);
       if (!(ds.skip & 4)) {
         if (ybnd)
+        {
+          if (ci == 0 || cj == 0 || ci == g.nx - 1 || cj == g.ny - 1) pdl_wait();  // ybnd of k_boundary_apply
           jac_sides_pre(g, ybnd, mu, ci, cj, slot, accp, tw);
+        }
         else
           jac_sides(g, ds, L, mu, ci, cj, XM, SP, r0, c0, P, slot, accp, tw);
       }
@@ -1088,6 +1093,7 @@ __global__ void __launch_bounds__(JNT, 2) k_jacobian(Geom g, TimeData td, Disc d
 template <int T>
 __global__ void k_jac_fixup(Geom g, int k1, const double* __restrict__ part, const double* __restrict__ rhs,
                             double* __restrict__ out) {
+  pdl_wait();  // partials of k_jacobian
   constexpr int PER = 8 * T;
   const int ntx = (g.nx + T - 1) / T, nty = (g.ny + T - 1) / T;
   const size_t nv = (size_t)(ntx - 1) * g.nny;  // nodes on interior vertical tile lines
@@ -1543,13 +1549,20 @@ cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const 
     PDST_LAUNCH(k_boundary_apply<<<dim3((unsigned)((nb + 127) / 128), K1), 128, 0, st>>>(g, K1, L.bmat, x, ybnd));
   }
   dim3 grid(jac_tiles_x(g), jac_tiles_y(g));
-  PDST_LAUNCH(k_jacobian<K1><<<grid, JNT, sm, st>>>(g, td, ds, L, state, x, rhs, out, part, ybnd));
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e;
+  if (ybnd) {  // overlaps k_boundary_apply (only the boundary cells wait for it)
+    PDST_LAUNCH(e = launch_pdl(k_jacobian<K1>, grid, dim3(JNT), sm, st, g, td, ds, L, state, x, rhs, out, part,
+                               (const double*)ybnd));
+  } else {
+    PDST_LAUNCH(k_jacobian<K1><<<grid, JNT, sm, st>>>(g, td, ds, L, state, x, rhs, out, part, ybnd));
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess) return e;
   const size_t nfix = (size_t)(jac_tiles_x(g) - 1) * g.nny + (size_t)(jac_tiles_y(g) - 1) * g.nnx;
   if (nfix > 0) {
     dim3 fg((unsigned)((nfix + 255) / 256), K1);
-    PDST_LAUNCH(k_jac_fixup<JT><<<fg, 256, 0, st>>>(g, K1, part, rhs, out));
+    PDST_LAUNCH(e = launch_pdl(k_jac_fixup<JT>, fg, dim3(256), 0, st, g, K1, (const double*)part, rhs, out));
+    if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }
