@@ -14,7 +14,7 @@ import numpy as np
 from .errors import ConstitutiveDomainError, PdstCudaError, SingularPatchError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpdst.so")
+LIB_PATH = os.environ.get("PDST_LIB") or os.path.join(HERE, "libpdst.so")  # PDST_LIB: experiment builds
 
 OK, EINVAL, EDOMAIN, ESINGULAR, ECUDA, ESTATE, ENOTSUP = range(7)
 HOST, DEVICE = 0, 1

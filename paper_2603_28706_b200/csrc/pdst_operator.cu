@@ -942,18 +942,19 @@ __device__ __forceinline__ void stage_planned(const StagePlan& sp, const double*
   }
 }
 
-// Two CTAs per SM (<= 128 registers, ~105 KB shared for K1 = 2) so that a
-// 256x256 mesh (256 tiles) runs in one wave on 148 SMs and one CTA's barriers
-// are covered by the other's compute.  That budget has no room for the
-// double-buffered "PIPE" variant (all Radau nodes' state planes staged up
-// front, two slot buffers), which is kept compiled out.
+// One CTA per SM with the full register file (~250 registers, no spills):
+// measured faster than two CTAs per SM at 128 registers (75 vs 90 us at cfg2)
+// even though the 256 tiles then take 1.73 waves.  The freed shared memory
+// goes to PIPE (K1 <= 2): every Radau node's state planes are staged up front
+// and the per-cell slots are double buffered, so the assembly of node mu
+// overlaps the compute of node mu+1 (one barrier per node instead of two).
 template <int K1>
-__host__ __device__ constexpr bool jac_pipe() { return false; }
+__host__ __device__ constexpr bool jac_pipe() { return K1 <= 2; }
 template <int K1>
 __host__ __device__ constexpr int jac_nbuf() { return jac_pipe<K1>() ? K1 : 1; }
 
 template <int K1>
-__global__ void __launch_bounds__(JNT, 2) k_jacobian(Geom g, TimeData td, Disc ds, Lin L, const double* __restrict__ state,
+__global__ void __launch_bounds__(JNT, 1) k_jacobian(Geom g, TimeData td, Disc ds, Lin L, const double* __restrict__ state,
                                                   const double* __restrict__ x, const double* __restrict__ rhs,
                                                   double* __restrict__ out, double* __restrict__ part,
                                                   const double* __restrict__ ybnd) {
@@ -1048,42 +1049,74 @@ __global__ void __launch_bounds__(JNT, 2) k_jacobian(Geom g, TimeData td, Disc d
     // summing the <= 4 cells that contain a node in a fixed order.
     if (valid && !(ds.skip & 16)) {
       const size_t base = (size_t)mu * g.nd;
-      const int nxo = lastx ? 3 : 2, nyo = lasty ? 3 : 2;
-      for (int jy = 0; jy < nyo; ++jy)
-        for (int ix = 0; ix < nxo; ++ix) {
-          const int lx = 2 * tx + ix, ly = 2 * ty + jy;  // tile-local node
-          double s0 = 0.0, s1 = 0.0;
-          // cells containing the node: (tx - [ix==0], ty - [jy==0]) .. (tx + [ix==2]...)
-          const int cxa = ix == 0 ? tx - 1 : (ix == 2 ? tx : tx), cxb = ix == 2 ? tx : tx;
-          const int cya = jy == 0 ? ty - 1 : ty, cyb = ty;
-#pragma unroll
-          for (int cy = cya; cy <= cyb; ++cy) {
-            if (cy < 0) continue;
-#pragma unroll
-            for (int cx = cxa; cx <= cxb; ++cx) {
-              if (cx < 0) continue;
-              const int a = 3 * (ly - 2 * cy) + (lx - 2 * cx);
-              const int cell = cy * JT + cx;
-              s0 += sacc[(2 * a) * JNT + cell];
-              s1 += sacc[(2 * a + 1) * JNT + cell];
-            }
+      const int me = ty * JT + tx;
+      const bool hl = tx > 0, hd = ty > 0;
+      // neighbour slots: left, down, down-left cell of this thread's cell
+      const double* sm_ = sacc + me;
+      const double* sl_ = sacc + me - 1;
+      const double* sd_ = sacc + me - JT;
+      const double* sld = sacc + me - JT - 1;
+      auto at = [&](const double* p, int a, int d) { return p[(2 * a + d) * JNT]; };
+      auto emit = [&](int lx, int ly, double s0, double s1) {
+        const bool shx = (lx == 0 && i0 > 0) || (lx == 2 * JT && i0 + JT < g.nx);
+        const bool shy = (ly == 0 && j0 > 0) || (ly == 2 * JT && j0 + JT < g.ny);
+        if (shx || shy) {
+          double* pp = part + (((size_t)mu * ntiles + tile) * JPER + perim(lx, ly)) * 2;
+          pp[0] = s0;
+          pp[1] = s1;
+        } else {
+          const size_t o = base + 2 * ((size_t)(2 * j0 + ly) * g.nnx + 2 * i0 + lx);
+          if (rhs) {
+            s0 = __ldg(rhs + o) - s0;
+            s1 = __ldg(rhs + o + 1) - s1;
           }
-          const bool shx = (lx == 0 && i0 > 0) || (lx == 2 * JT && i0 + JT < g.nx);
-          const bool shy = (ly == 0 && j0 > 0) || (ly == 2 * JT && j0 + JT < g.ny);
-          if (shx || shy) {
-            double* pp = part + (((size_t)mu * ntiles + tile) * JPER + perim(lx, ly)) * 2;
-            pp[0] = s0;
-            pp[1] = s1;
-          } else {
-            const size_t o = base + 2 * ((size_t)(2 * j0 + ly) * g.nnx + 2 * i0 + lx);
-            if (rhs) {
-              s0 = __ldg(rhs + o) - s0;
-              s1 = __ldg(rhs + o + 1) - s1;
-            }
-            out[o] = s0;
-            out[o + 1] = s1;
-          }
+          out[o] = s0;  // (nd may be odd: no 16-byte vector store)
+          out[o + 1] = s1;
         }
+      };
+      const int lx = 2 * tx, ly = 2 * ty;
+      // the cells sharing a node are summed in (row, column) order, lower first
+      {  // node (0,0): cells down-left, down, left, self
+        double s0 = 0.0, s1 = 0.0;
+        if (hl && hd) { s0 += at(sld, 8, 0); s1 += at(sld, 8, 1); }
+        if (hd) { s0 += at(sd_, 6, 0); s1 += at(sd_, 6, 1); }
+        if (hl) { s0 += at(sl_, 2, 0); s1 += at(sl_, 2, 1); }
+        s0 += at(sm_, 0, 0);
+        s1 += at(sm_, 0, 1);
+        emit(lx, ly, s0, s1);
+      }
+      {  // (1,0): down, self
+        double s0 = 0.0, s1 = 0.0;
+        if (hd) { s0 += at(sd_, 7, 0); s1 += at(sd_, 7, 1); }
+        s0 += at(sm_, 1, 0);
+        s1 += at(sm_, 1, 1);
+        emit(lx + 1, ly, s0, s1);
+      }
+      {  // (0,1): left, self
+        double s0 = 0.0, s1 = 0.0;
+        if (hl) { s0 += at(sl_, 5, 0); s1 += at(sl_, 5, 1); }
+        s0 += at(sm_, 3, 0);
+        s1 += at(sm_, 3, 1);
+        emit(lx, ly + 1, s0, s1);
+      }
+      emit(lx + 1, ly + 1, 0.0 + at(sm_, 4, 0), 0.0 + at(sm_, 4, 1));  // (1,1): self only
+      if (lastx) {
+        double s0 = 0.0, s1 = 0.0;  // (2,0): down, self
+        if (hd) { s0 += at(sd_, 8, 0); s1 += at(sd_, 8, 1); }
+        s0 += at(sm_, 2, 0);
+        s1 += at(sm_, 2, 1);
+        emit(lx + 2, ly, s0, s1);
+        emit(lx + 2, ly + 1, 0.0 + at(sm_, 5, 0), 0.0 + at(sm_, 5, 1));
+      }
+      if (lasty) {
+        double s0 = 0.0, s1 = 0.0;  // (0,2): left, self
+        if (hl) { s0 += at(sl_, 8, 0); s1 += at(sl_, 8, 1); }
+        s0 += at(sm_, 6, 0);
+        s1 += at(sm_, 6, 1);
+        emit(lx, ly + 2, s0, s1);
+        emit(lx + 1, ly + 2, 0.0 + at(sm_, 7, 0), 0.0 + at(sm_, 7, 1));
+        if (lastx) emit(lx + 2, ly + 2, 0.0 + at(sm_, 8, 0), 0.0 + at(sm_, 8, 1));
+      }
     }
     if (!PIPE) __syncthreads();
   }
