@@ -877,16 +877,22 @@ __global__ void k_boundary_apply(Geom g, int k1, const double* __restrict__ bmat
   else { ci = 0; cj = f; }
   const double* xm = x + (size_t)mu * g.nd;
   const double* Bm = bmat + (size_t)mu * 441 * g.nbf + (size_t)i * 21 * g.nbf + bf;
-  double s = 0.0;
+  // all 42 loads are issued before the first FMA (one memory latency, not 21)
+  double bv[21], xv[21];
+#pragma unroll
+  for (int j = 0; j < 21; ++j) bv[j] = __ldg(Bm + (size_t)j * g.nbf);
 #pragma unroll
   for (int a = 0; a < 9; ++a) {
     const size_t node = (size_t)(2 * cj + a / 3) * g.nnx + 2 * ci + a % 3;
-    s = fma(__ldg(Bm + (size_t)(2 * a) * g.nbf), __ldg(xm + 2 * node), s);
-    s = fma(__ldg(Bm + (size_t)(2 * a + 1) * g.nbf), __ldg(xm + 2 * node + 1), s);
+    xv[2 * a] = __ldg(xm + 2 * node);
+    xv[2 * a + 1] = __ldg(xm + 2 * node + 1);
   }
   const double* xp = xm + g.mv + 3 * ((size_t)cj * g.nx + ci);
 #pragma unroll
-  for (int r = 0; r < 3; ++r) s = fma(__ldg(Bm + (size_t)(18 + r) * g.nbf), __ldg(xp + r), s);
+  for (int r = 0; r < 3; ++r) xv[18 + r] = __ldg(xp + r);
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < 21; ++j) s = fma(bv[j], xv[j], s);
   ybnd[((size_t)mu * 21 + i) * g.nbf + bf] = s;
 }
 
