@@ -129,6 +129,17 @@ int pdst_vcycle(pdst_handle* h, const double* r, double* z, int pre, int post, d
 /* Kernel timing for benchmarks: CUDA events around every launch of class
    kernel (0 jacobian/defect, 1 vanka gemv, 2 vanka scatter, 3 residual,
    4 transfers, 5 coarse-level operators) while enabled. */
+/* FGMRES block operations (krylov.py:93-126), device pointers only
+   (where must be PDST_DEVICE), asynchronous on the handle's stream:
+   out[i] = <A_i, w> for i < m, basis rows A_i = A + i*lda (length n);
+   w -= sum_i c[i] A_i and, when B != NULL, w2 -= sum_i c[i] B_i (c: m doubles
+   on the device).  Classical Gram-Schmidt applied twice is two
+   multidot + multi_axpy pairs. */
+int pdst_multidot(pdst_handle* h, const double* A, int64_t lda, int m, const double* w, int64_t n, double* out,
+                  int where);
+int pdst_multi_axpy(pdst_handle* h, const double* A, const double* B, int64_t lda, int m, const double* c, double* w,
+                    double* w2, int64_t n, int where);
+
 int pdst_profile(pdst_handle* h, int enable);
 int pdst_profile_read(pdst_handle* h, int kernel, double* total_ms, int64_t* launches);
 

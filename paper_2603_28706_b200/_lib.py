@@ -60,6 +60,8 @@ SIGNATURES = {
     "pdst_mass_apply": [P, P, P, I],
     "pdst_mass_dot": [P, P, P, P, I],
     "pdst_dot": [P, P, P, I64, P, I],
+    "pdst_multidot": [P, P, I64, I, P, I64, P, I],
+    "pdst_multi_axpy": [P, P, P, I64, I, P, P, P, I64, I],
     "pdst_cell_maps": [P, P, P],
     "pdst_hierarchy": [P, I, C.POINTER(I)],
     "pdst_level_sizes": [P, I, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(I64)],

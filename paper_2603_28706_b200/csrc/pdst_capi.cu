@@ -437,6 +437,29 @@ int pdst_mass_dot(pdst_handle* h, const double* a, const double* b, double* out,
   return dot_common(h, a, b, 0, out, where, true);
 }
 
+int pdst_multidot(pdst_handle* h, const double* A, int64_t lda, int m, const double* w, int64_t n, double* out,
+                  int where) {
+  if (!h || !A || !w || !out) return fail(PDST_EINVAL, "null argument");
+  if (where != PDST_DEVICE) return fail(PDST_ENOTSUP, "pdst_multidot takes device pointers only");
+  if (m < 0 || n < 0 || lda < n) return fail(PDST_EINVAL, "bad sizes (m=%d, n=%lld, lda=%lld)", m, (long long)n,
+                                             (long long)lda);
+  CK(cudaSetDevice(h->device));
+  double* part = h->kpartials.ensure(multidot_scratch(m > 0 ? m : 1));
+  if (!part) return fail(PDST_ECUDA, "out of device memory");
+  CK(multidot(A, lda, m, w, n, part, out, h->stream));
+  return PDST_OK;
+}
+
+int pdst_multi_axpy(pdst_handle* h, const double* A, const double* B, int64_t lda, int m, const double* c, double* w,
+                    double* w2, int64_t n, int where) {
+  if (!h || !A || !c || !w || (B && !w2)) return fail(PDST_EINVAL, "null argument");
+  if (where != PDST_DEVICE) return fail(PDST_ENOTSUP, "pdst_multi_axpy takes device pointers only");
+  if (m < 0 || n < 0 || lda < n) return fail(PDST_EINVAL, "bad sizes");
+  CK(cudaSetDevice(h->device));
+  CK(multi_axpy(A, B, lda, m, c, w, w2, n, h->stream));
+  return PDST_OK;
+}
+
 int pdst_dot(pdst_handle* h, const double* a, const double* b, int64_t n, double* out, int where) {
   if (n < 0) return fail(PDST_EINVAL, "negative length");
   return dot_common(h, a, b, n, out, where, false);

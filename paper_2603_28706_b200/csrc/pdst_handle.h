@@ -123,6 +123,7 @@ struct pdst_handle {
   // staging for host pointers
   pdst::DeviceBuffer scratch_a, scratch_b, scratch_c, scratch_d, scratch_f;
   pdst::DeviceBuffer partials;
+  pdst::DeviceBuffer kpartials;  // FGMRES multi-dot partial sums
   pdst::DeviceBuffer jpart;  // Jacobian tile-boundary partial sums
 
   // surrogate (representative-state) linearization and patch scratch

@@ -47,4 +47,13 @@ cudaError_t copy_velocity_blocks(const Geom& g, int k1, const double* U, double*
 cudaError_t blend_velocity(const Geom& g, int k1, const double* coef, const double* U, size_t stride, double* V,
                            cudaStream_t st);
 
+// FGMRES block kernels (pdst_krylov.cu): out[i] = <A_i, w> (i < m, rows lda
+// apart; `partial` holds multidot_scratch(m) doubles) and w -= A^T c,
+// w2 -= B^T c.
+size_t multidot_scratch(int m);
+cudaError_t multidot(const double* A, int64_t lda, int m, const double* w, int64_t n, double* partial, double* out,
+                     cudaStream_t st);
+cudaError_t multi_axpy(const double* A, const double* B, int64_t lda, int m, const double* c, double* w, double* w2,
+                       int64_t n, cudaStream_t st);
+
 }  // namespace pdst

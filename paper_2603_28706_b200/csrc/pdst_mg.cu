@@ -216,12 +216,15 @@ int pdst_patches_build(pdst_handle* h, int surrogate, double rep_fraction, int* 
   const int k1 = h->td.k1, D = 21 * k1;
   const size_t nc = g.ncells;
   const bool multilevel = L > 1;
+  // a hierarchy with a single level (min_cells >= the mesh): the V-cycle is the
+  // dense solve of the whole slab system (multigrid.py:494-547)
+  const bool single_solve = L == 1 && h->min_cells > 0;
   double* bad = h->ibuf.ensure(1);
   if (!bad) return set_error(PDST_ECUDA, "out of device memory");
   int* badi = reinterpret_cast<int*>(bad);
 
   // exact per-node element matrices of the finest level (Galerkin input and exact patches)
-  const bool need_exact = multilevel || !surrogate;
+  const bool need_exact = multilevel || !surrogate || single_solve;
   if (need_exact) {
     double* ET = fl->ecell.ensure((size_t)k1 * nc * 441);
     if (!ET) return set_error(PDST_ECUDA, "out of device memory (element matrices)");
@@ -304,7 +307,7 @@ int pdst_patches_build(pdst_handle* h, int surrogate, double rep_fraction, int* 
   h->patches_valid = true;
 
   // ---- coarsest-level dense solve (multigrid.py:494-520) ----
-  if (multilevel) {
+  if (multilevel || single_solve) {
     Level* c0 = h->levels[0];
     const int n = k1 * c0->g.nd;
     if (n > 16384) return set_error(PDST_ENOTSUP, "coarsest level too large for the dense solve (%d dofs)", n);
@@ -503,7 +506,7 @@ int pdst_vcycle(pdst_handle* h, const double* r, double* z, int pre, int post, d
   if (!h || !r || !z) return set_error(PDST_EINVAL, "null argument");
   if (int e = check_where(where)) return e;
   if (!h->patches_valid || !h->coarse_valid)
-    return set_error(PDST_ESTATE, "V-cycle needs pdst_hierarchy (>= 2 levels) and pdst_patches_build");
+    return set_error(PDST_ESTATE, "V-cycle needs pdst_hierarchy and pdst_patches_build");
   CK(cudaSetDevice(h->device));
   const int L = (int)h->levels.size();
   const size_t n = (size_t)h->td.k1 * h->g.nd;

@@ -232,6 +232,12 @@ class MassNorm:
         L.check(L.lib().pdst_mass_apply(self.dev.h, L.vptr(flat), L.vptr(y), w), "pdst_mass_apply")
         return y.reshape(shape)
 
+    def apply_into(self, x, out):
+        """out = M x for device tensors (no allocation; FGMRES basis rows)."""
+        w = self.dev.where(x, out)
+        L.check(L.lib().pdst_mass_apply(self.dev.h, L.vptr(x), L.vptr(out), w), "pdst_mass_apply")
+        return out
+
     def dot(self, a, b):
         ac, bc = _f64(a).reshape(-1), _f64(b).reshape(-1)
         if _is_torch(ac):

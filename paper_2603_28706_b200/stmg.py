@@ -61,8 +61,8 @@ class StmgPreconditioner:
         bl, bp = C.c_int(-1), C.c_int64(-1)
         rc = L.lib().pdst_patches_build(self.dev.h, int(self.mg.surrogate), float(self.mg.rep_fraction),
                                         C.byref(bl), C.byref(bp))
-        if self.num_levels < 2 and rc == L.OK:
-            raise ValueError("the mesh admits no coarser level (min_cells); use smoother.VankaLevel")
+        # one level (min_cells >= the mesh): the V-cycle is the coarsest dense
+        # solve of the whole slab system, as in the reference (multigrid.py:545-547)
         L.check(rc, "pdst_patches_build", level=bl.value, patch=bp.value)
         self.k1 = self.dev.k1
 
@@ -104,10 +104,10 @@ class StmgPreconditioner:
         return out
 
     # -- the preconditioner ------------------------------------------------------
-    def apply(self, r):
+    def apply(self, r, out=None):
         """z = V-cycle(r), projected off the mean-pressure modes when all-Dirichlet."""
         rc_ = _f64(r).reshape(-1)
-        z = self.dev.empty_like(rc_)
+        z = self.dev.empty_like(rc_) if out is None else out
         w = self.dev.where(rc_, z)
         L.check(L.lib().pdst_vcycle(self.dev.h, L.vptr(rc_), L.vptr(z), int(self.mg.pre_smooth),
                                     int(self.mg.post_smooth), float(self.mg.omega), w), "pdst_vcycle")

@@ -78,3 +78,51 @@ CASES = [
 CASE_BY_NAME = {c.name: c for c in CASES}
 
 TRANSFER_PAIRS = [(1, 1), (2, 2), (3, 3), (4, 2), (4, 4)]  # coarse (nx, ny); fine is 2x
+
+
+@dataclass(frozen=True)
+class SolverCase:
+    """FGMRES / Newton fixtures (f1).
+
+    fgmres: the slab case's Jacobian at the synthetic state, rhs = its
+    residual, STMG preconditioner (or none) and the mass norm.
+    newton: the first slab of the reference's benchmark problem
+    (bench/harness.py:91-115: unit square, manufactured forcing, v0 = 0,
+    default discretization), with a Neumann right side, solved by
+    nonlinear_solve_slab with an STMG factory.  Runs that end in the
+    reference's SlabSolveError are fixtures too (partial statistics + kind)."""
+
+    name: str
+    kind: str  # "fgmres" or "newton"
+    case: Case | None = None  # fgmres
+    tol: float = 1e-8
+    restart: int = 60
+    max_iters: int = 300
+    params: tuple = (1.5, 1e-2, 1.0, 1e-3)  # newton: (p, delta, nu, nu_inf)
+    variant: str = "modn"
+    nx: int = 8
+    k: int = 1
+    tau: float = 0.1
+    min_cells: int = 4
+    rebuild_rho: float = 0.9
+    abs_tol: float = 1e-12
+    rel_tol: float = 1e-10
+
+
+SOLVER_CASES = [
+    # a Neumann side removes the constant-pressure null space of the all-Dirichlet slab
+    SolverCase("fg_p8_modn", "fgmres", Case("fg_p8_modn", _cfg("fg_p8_modn", 8, 8, 1, seed=31, gamma1=1e3,
+                                                                gamma2=1e3), neumann_sides=("right",)),
+               tol=1e-6, restart=20, max_iters=80),
+    SolverCase("fg_p8_exn_noprec", "fgmres", Case("fg_p8_exn_noprec", _cfg("fg_p8_exn_noprec", 8, 8, 0, seed=32),
+                                                  variant="exn", neumann_sides=("top",)),
+               tol=1e-6, restart=30, max_iters=90),
+    # single-level STMG (exact coarse solve), rebuilt every step: converges at abs_tol 1e-6
+    SolverCase("nw_h8_modn_conv", "newton", min_cells=8, rebuild_rho=0.0, abs_tol=1e-6),
+    SolverCase("nw_h8_exn_conv", "newton", variant="exn", params=(1.3, 1e-3, 1.0, 0.0), min_cells=8,
+               rebuild_rho=0.0, abs_tol=1e-6),
+    SolverCase("nw_h8_pic_k0", "newton", variant="pic", k=0, min_cells=8, rebuild_rho=0.0, abs_tol=1e-6),
+    # default tolerances: the reference stops with SlabSolveError("krylov") after 3 steps
+    SolverCase("nw_h8_modn_fail", "newton", min_cells=8, rebuild_rho=0.0),
+]
+SOLVER_BY_NAME = {c.name: c for c in SOLVER_CASES}

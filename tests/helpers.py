@@ -14,7 +14,7 @@ for p in (ROOT, GOLDEN):
     if p not in sys.path:
         sys.path.insert(0, p)
 
-from cases import CASE_BY_NAME, CASES, FORCINGS  # noqa: E402
+from cases import CASE_BY_NAME, CASES, FORCINGS, SOLVER_BY_NAME, SOLVER_CASES  # noqa: E402
 from oracle import pdst_oracle as orc  # noqa: E402
 
 
@@ -87,3 +87,43 @@ def cuda_available():
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+class FixedForcing:
+    """f(x, y, t) replaying forcing values frozen at the quadrature points
+    (fixture `fq`, shape (k+1, nc, 16, 2)); t selects the Radau node."""
+
+    def __init__(self, fq, times):
+        self.fq = np.asarray(fq)
+        self.times = np.asarray(times, dtype=float)
+
+    def __call__(self, x, y, t):
+        mu = int(np.argmin(np.abs(self.times - t)))
+        assert abs(self.times[mu] - t) < 1e-12 and np.shape(x) == self.fq.shape[1:3]
+        return self.fq[mu]
+
+
+def solver_ctx(sc, fx):
+    """Product SlabContext of a SOLVER_CASES entry (fixture fx)."""
+    from paper_2603_28706_b200 import problem as pb
+    from paper_2603_28706_b200.radau import TimeBasis, TimeMatrices
+
+    if sc.kind == "fgmres":
+        fx = dict(fx, M_t=np.diag(fx["weights"]))
+        return product_ctx(sc.case, fx)
+    mesh = pb.tag_sides(pb.QuadMesh(sc.nx, sc.nx), ("right",))
+    disc = pb.Discretization(mesh)
+    g = fx["gammas"]
+    config = pb.DiscretizationConfig(float(g[0]), float(g[1]), float(g[2]))
+    params = pb.ModelParams(*sc.params)
+    basis = TimeBasis(sc.k, fx["nodes"], fx["weights"])
+    tmat = TimeMatrices(np.diag(fx["weights"]), fx["K_t"], fx["m_t"])
+    t0, tau = float(fx["t_start"]), float(fx["tau"])
+    f = FixedForcing(fx["fq"], t0 + tau * np.asarray(fx["nodes"]))
+    return pb.SlabContext(disc, params, config, pb.ProblemData(f=f), basis, tmat, t0, tau, fx["v_minus"])
+
+
+def solver_variant(name, nu):
+    from paper_2603_28706_b200 import problem as pb
+
+    return {"pic": pb.picard(), "exn": pb.exact_newton(), "modn": pb.modified_newton(nu)}[name]

@@ -1,0 +1,68 @@
+"""GPU FGMRES (M-inner product, CGS2 on device) and Newton driver against
+the reference's own solver runs (tests/golden/make_golden_solver.py).
+
+Tolerances: iteration counts, step lengths and failure kinds exact; norms
+and solutions relative 1e-6 (Krylov iterates accumulate rounding over up to
+80 Arnoldi steps; the device orthogonalization is CGS2 instead of MGS2)."""
+
+import numpy as np
+import pytest
+
+from helpers import SOLVER_CASES, load, product_variant, rel_err, solver_ctx, solver_variant
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-6  # block-MGS vs sequential MGS: measured 2e-10 .. 5e-8 on the oracle
+
+
+@pytest.mark.parametrize("sc", [c for c in SOLVER_CASES if c.kind == "fgmres"], ids=lambda c: c.name)
+def test_fgmres_matches_reference(sc):
+    from paper_2603_28706_b200.krylov import KrylovConfig, fgmres
+    from paper_2603_28706_b200.operators import MassNorm, SlabJacobian
+    from paper_2603_28706_b200.stmg import MgConfig, StmgPreconditioner
+
+    fx = load(sc.name)
+    ctx = solver_ctx(sc, fx)
+    var = product_variant(sc.case)
+    jac = SlabJacobian(ctx, fx["U0"], var)
+    pre = None if "noprec" in sc.name else StmgPreconditioner(ctx, fx["U0"], var, MgConfig(min_cells=sc.min_cells))
+    res = fgmres(jac.matvec, fx["rhs"], sc.tol, KrylovConfig(sc.restart, sc.max_iters),
+                 precond=pre.apply if pre else None, mass=MassNorm(ctx, dev=jac.dev))
+    assert res.iterations == int(fx["iterations"])
+    assert res.converged == bool(fx["converged"])
+    assert abs(res.residual_norm - float(fx["residual_norm"])) <= RTOL * float(fx["residual_norm"])
+    assert abs(res.target - float(fx["target"])) <= 1e-12 * float(fx["target"])
+    e2, _ = rel_err(res.x, fx["x"])
+    assert e2 <= RTOL, f"x rel err {e2:.2e}"
+
+
+@pytest.mark.parametrize("sc", [c for c in SOLVER_CASES if c.kind == "newton"], ids=lambda c: c.name)
+def test_newton_matches_reference(sc):
+    from paper_2603_28706_b200.errors import SlabSolveError
+    from paper_2603_28706_b200.krylov import KrylovConfig
+    from paper_2603_28706_b200.newton import NewtonConfig, nonlinear_solve_slab
+    from paper_2603_28706_b200.stmg import MgConfig, StmgFactory
+
+    fx = load(sc.name)
+    ctx = solver_ctx(sc, fx)
+    nc = NewtonConfig(variant=solver_variant(sc.variant, sc.params[2]), abs_tol=sc.abs_tol, rel_tol=sc.rel_tol)
+    fac = StmgFactory(MgConfig(min_cells=sc.min_cells, rebuild_rho=sc.rebuild_rho))
+    kc = KrylovConfig(sc.restart, sc.max_iters)
+    failure = str(fx["failure"])
+    if failure:
+        with pytest.raises(SlabSolveError) as ei:
+            nonlinear_solve_slab(ctx, fx["U0"], nc, kc, fac)
+        assert ei.value.kind == failure
+        stats, U = ei.value.diagnostics, None
+    else:
+        U, stats = nonlinear_solve_slab(ctx, fx["U0"], nc, kc, fac)
+    st = stats.steps
+    assert [s.n_l for s in st] == list(fx["n_l"])
+    assert [s.lam for s in st] == list(fx["lam"])
+    assert [s.rebuilt for s in st] == list(fx["rebuilt"])
+    for key in ("eta", "res_before", "res_after"):
+        got = np.array([getattr(s, key) for s in st])
+        assert np.allclose(got, fx[key], rtol=RTOL, atol=0), (key, got, fx[key])
+    assert abs(stats.initial_res - float(fx["initial_res"])) <= 1e-10 * float(fx["initial_res"])
+    if U is not None:
+        e2, _ = rel_err(U, fx["U"])
+        assert e2 <= RTOL, f"U rel err {e2:.2e}"
