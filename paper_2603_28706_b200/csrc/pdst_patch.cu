@@ -254,49 +254,83 @@ __global__ void __launch_bounds__(256) k_vanka_gemv(Geom g, const double* __rest
     s3 = fma(__ldg(col + (size_t)(jj + 3) * D), loc[p][jj + 3], s3);
   }
   for (; jj < D; ++jj) s0 = fma(__ldg(col + (size_t)jj * D), loc[p][jj], s0);
-  upd[(size_t)K * D + i] = (s0 + s1) + (s2 + s3);
+  upd[(size_t)i * g.ncells + K] = (s0 + s1) + (s2 + s3);  // structure of arrays [D][ncells]
 }
 
-// d[dof] += omega * sum over patches containing dof of upd (node gather).
-// d[dof] += omega * sum over patches containing dof of upd (node gather).
+// d += omega * sum_K R_K' upd_K, one thread per (cell, Radau node, velocity
+// component): the cell writes the nodes it owns (lower-left 2x2 of its 3x3
+// block, plus the last row / column of the mesh) summing the <= 4 patches
+// containing each node in a fixed order (down-left, down, left, self); the
+// component-0 thread also writes the cell's 3 pressure dofs.  upd is structure
+// of arrays [21 k1][ncells], so every read is coalesced; all loads are issued
+// before the first store.
 // Only patches of cell rows [row_lo, row_hi) contribute; inc_only writes the
 // increment instead of adding it (distributed sweeps combine increments).
-__global__ void k_vanka_scatter(Geom g, int k1, const double* __restrict__ upd, double omega, double* __restrict__ d,
-                                int row_lo, int row_hi, int inc_only) {
-  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int mu = blockIdx.y;
-  const size_t nn = (size_t)g.nnx * g.nny;
-  const int D = 21 * k1;
+__global__ void __launch_bounds__(256) k_vanka_scatter(Geom g, int k1, const double* __restrict__ upd, double omega,
+                                                       double* __restrict__ d, int row_lo, int row_hi,
+                                                       int inc_only) {
+  const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int mu = blockIdx.y, dd = blockIdx.z;
+  if (c >= (size_t)g.ncells) return;
+  const int ci = (int)(c % g.nx), cj = (int)(c / g.nx);
+  const size_t nc = g.ncells;
+  const double* u = upd + (size_t)21 * mu * nc + (size_t)dd * nc;  // u[2a * nc + cell] = component dd of node a
   double* dm = d + (size_t)mu * g.nd;
-  if (t < nn) {
-    const int X = (int)(t % g.nnx), Y = (int)(t / g.nnx);
-    double s0 = 0.0, s1 = 0.0;
-    for (int cy = max(row_lo, (Y - 1) / 2); cy <= min(row_hi - 1, Y / 2); ++cy)
-      for (int cx = max(0, (X - 1) / 2); cx <= min(g.nx - 1, X / 2); ++cx) {
-        const int a = 3 * (Y - 2 * cy) + (X - 2 * cx);
-        const double* u = upd + ((size_t)cy * g.nx + cx) * D + 21 * mu + 2 * a;
-        s0 += u[0];
-        s1 += u[1];
-      }
-    if (inc_only) {
-      dm[2 * t] = omega * s0;
-      dm[2 * t + 1] = omega * s1;
-    } else {
-      dm[2 * t] += omega * s0;
-      dm[2 * t + 1] += omega * s1;
-    }
-  } else if (t < nn + (size_t)g.ncells) {
-    const size_t c = t - nn;
-    const int cy = (int)(c / g.nx);
-    const bool act = cy >= row_lo && cy < row_hi;
-    const double* u = upd + c * D + 21 * mu + 18;
-    double* o = dm + g.mv + 3 * c;
+  const bool me = cj >= row_lo && cj < row_hi;
+  const bool hd = cj > 0 && cj - 1 >= row_lo && cj - 1 < row_hi;
+  const bool lastx = ci == g.nx - 1, lasty = cj == g.ny - 1;
+  // neighbour cells (clamped to self when absent; their values are masked to 0)
+  const size_t cl = ci > 0 ? c - 1 : c, cd = cj > 0 ? c - g.nx : c, cld = (ci > 0 && cj > 0) ? c - g.nx - 1 : c;
+  const double ml = (ci > 0 && me) ? 1.0 : 0.0, md = hd ? 1.0 : 0.0, mld = (hd && ci > 0) ? 1.0 : 0.0;
+  const double ms = me ? 1.0 : 0.0;
+  auto U = [&](size_t cell, int a) { return __ldg(u + (size_t)(2 * a) * nc + cell); };
+  double S[9];
+#pragma unroll
+  for (int a = 0; a < 9; ++a) S[a] = U(c, a);
+  const double l2 = U(cl, 2), l5 = U(cl, 5), l8 = U(cl, 8);  // left cell: its local nodes 2, 5, 8
+  const double d6 = U(cd, 6), d7 = U(cd, 7), d8 = U(cd, 8);  // down cell: 6, 7, 8
+  const double ld8 = U(cld, 8);
+  double pv[3] = {0.0, 0.0, 0.0}, po[3] = {0.0, 0.0, 0.0};
+  double* op = dm + g.mv + 3 * c;
+  if (dd == 0) {
+#pragma unroll
     for (int j = 0; j < 3; ++j) {
-      const double v = act ? omega * u[j] : 0.0;
-      if (inc_only)
-        o[j] = v;
-      else
-        o[j] += v;
+      pv[j] = __ldg(upd + (size_t)(21 * mu + 18 + j) * nc + c);
+      if (!inc_only) po[j] = op[j];
+    }
+  }
+  const size_t s2 = 2 * (size_t)g.nnx;
+  double* r0 = dm + 2 * ((size_t)(2 * cj) * g.nnx + 2 * ci) + dd;
+  double* r1 = r0 + s2;
+  double* r2 = r1 + s2;
+  double o[9];
+  if (!inc_only) {
+    o[0] = r0[0], o[1] = r0[2], o[3] = r1[0], o[4] = r1[2];
+    if (lastx) o[2] = r0[4], o[5] = r1[4];
+    if (lasty) {
+      o[6] = r2[0], o[7] = r2[2];
+      if (lastx) o[8] = r2[4];
+    }
+  }
+  auto fin = [&](double* dst, int e, int slot, double sv) { dst[e] = inc_only ? omega * sv : o[slot] + omega * sv; };
+  fin(r0, 0, 0, ((0.0 + mld * ld8) + md * d6) + ml * l2 + ms * S[0]);
+  fin(r0, 2, 1, (0.0 + md * d7) + ms * S[1]);
+  fin(r1, 0, 3, (0.0 + ml * l5) + ms * S[3]);
+  fin(r1, 2, 4, 0.0 + ms * S[4]);
+  if (lastx) {
+    fin(r0, 4, 2, (0.0 + md * d8) + ms * S[2]);
+    fin(r1, 4, 5, 0.0 + ms * S[5]);
+  }
+  if (lasty) {
+    fin(r2, 0, 6, (0.0 + ml * l8) + ms * S[6]);
+    fin(r2, 2, 7, 0.0 + ms * S[7]);
+    if (lastx) fin(r2, 4, 8, 0.0 + ms * S[8]);
+  }
+  if (dd == 0) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const double v = me ? omega * pv[j] : 0.0;
+      op[j] = inc_only ? v : po[j] + v;
     }
   }
 }
@@ -352,8 +386,7 @@ cudaError_t vanka_gemv(const Geom& g, int k1, const double* invT, const double* 
 cudaError_t vanka_scatter(const Geom& g, int k1, const double* upd, double omega, double* d, cudaStream_t st,
                           int row_lo, int row_hi, bool inc_only) {
   if (row_hi < 0) row_hi = g.ny;
-  const size_t n = (size_t)g.nnx * g.nny + g.ncells;
-  dim3 grid((unsigned)((n + 255) / 256), k1);
+  dim3 grid((unsigned)((g.ncells + 255) / 256), k1, 2);
   PDST_LAUNCH(k_vanka_scatter<<<grid, 256, 0, st>>>(g, k1, upd, omega, d, row_lo, row_hi, inc_only ? 1 : 0));
   return cudaGetLastError();
 }

@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(252) k_vanka_gemv_diag(Geom g, TimeDiag td, co
     hr[b] = ar - br;
     hi[b] = ai + bi;
   }
-  double* o = upd + (size_t)K * 21 * K1;
+  double* o = upd + K;  // structure of arrays [21 K1][ncells]
 #pragma unroll
   for (int mu = 0; mu < K1; ++mu) {
     double s = 0.0;
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(252) k_vanka_gemv_diag(Geom g, TimeDiag td, co
       const double re = td.V_re[mu * MAXK1 + b] * hr[b] - td.V_im[mu * MAXK1 + b] * hi[b];
       s += td.pair[b] ? 2.0 * re : re;
     }
-    o[21 * mu + r] = s;
+    o[(size_t)(21 * mu + r) * g.ncells] = s;
   }
 }
 
