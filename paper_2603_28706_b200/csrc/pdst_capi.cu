@@ -44,39 +44,6 @@ int cuda_fail(cudaError_t e, const char* where) {
     if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
   } while (0)
 
-Tables host_tables() {
-  Tables t{};
-  const double s[4] = {0.06943184420297371, 0.33000947820757187, 0.6699905217924281, 0.9305681557970262};
-  const double w[4] = {0.17392742256872679, 0.3260725774312732, 0.3260725774312732, 0.17392742256872679};
-  auto L = [](double x, double out[3]) {
-    out[0] = (1.0 - x) * (1.0 - 2.0 * x);
-    out[1] = 4.0 * x * (1.0 - x);
-    out[2] = x * (2.0 * x - 1.0);
-  };
-  auto dL = [](double x, double out[3]) {
-    out[0] = 4.0 * x - 3.0;
-    out[1] = 4.0 - 8.0 * x;
-    out[2] = 4.0 * x - 1.0;
-  };
-  for (int q = 0; q < 4; ++q) {
-    t.s[q] = s[q];
-    t.w[q] = w[q];
-    L(s[q], t.B[q]);
-    dL(s[q], t.G[q]);
-  }
-  for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j) {
-      double acc = 0.0;
-      for (int q = 0; q < 4; ++q) acc += w[q] * t.B[q][i] * t.B[q][j];
-      t.M1[i][j] = acc;
-    }
-  L(0.0, t.E[0]);
-  L(1.0, t.E[1]);
-  dL(0.0, t.dE[0]);
-  dL(1.0, t.dE[1]);
-  return t;
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -93,6 +60,13 @@ double* DeviceBuffer::ensure(size_t n) {
     cap = n;
   }
   return ptr;
+}
+
+double* DeviceBuffer::ensure_zeroed(size_t n) {
+  if (n <= cap) return ptr;
+  double* p = ensure(n);
+  if (p && cudaMemset(p, 0, n * sizeof(double)) != cudaSuccess) return nullptr;
+  return p;
 }
 
 void DeviceBuffer::release() {
@@ -314,6 +288,9 @@ int pdst_linearize(pdst_handle* h, const double* U, int kind, double sigma_max, 
     Lin L = lin_of(h);
     L.bmat = nullptr;
     CK(boundary_matrices(g, h->ds, L, k1, st, bm, h->stream));
+    double* apc = h->apc.ensure(apply_cache_size(g, k1));
+    if (!apc) return fail(PDST_ECUDA, "out of device memory");
+    CK(apply_cache(g, h->td, h->ds, L, st, apc, h->stream));
   }
   h->linearized = true;
   h->patches_valid = false;
@@ -334,10 +311,10 @@ static int jac_common(pdst_handle* h, const double* x, const double* r, double* 
   if (err) return err;
   double* yd = out_ptr(h->scratch_b, y, n, where);
   if (!yd) return fail(PDST_ECUDA, "out of device memory");
-  double* part = h->jpart.ensure(jacobian_scratch(h->g, h->td.k1));
+  double* part = h->jpart.ensure_zeroed(jacobian_scratch(h->g, h->td.k1));
   if (!part) return fail(PDST_ECUDA, "out of device memory");
   CK(PDST_TIMED(h, PK_JACOBIAN,
-                jacobian_apply(h->g, h->td, h->ds, lin_of(h), h->state.ptr, xd, rd, yd, part, h->stream)));
+                jacobian_apply(h->g, h->td, h->ds, lin_of(h), xd, rd, yd, part, h->stream)));
   return finish_out(h, y, yd, n, where);
 }
 
@@ -466,3 +443,39 @@ int pdst_dot(pdst_handle* h, const double* a, const double* b, int64_t n, double
 }
 
 }  // extern "C"
+
+namespace pdst {
+// 1-D Gauss(4) / Q2 tables (femspace.py:46-75) as the host computes them.
+Tables host_tables() {
+  Tables t{};
+  const double s[4] = {0.06943184420297371, 0.33000947820757187, 0.6699905217924281, 0.9305681557970262};
+  const double w[4] = {0.17392742256872679, 0.3260725774312732, 0.3260725774312732, 0.17392742256872679};
+  auto L = [](double x, double out[3]) {
+    out[0] = (1.0 - x) * (1.0 - 2.0 * x);
+    out[1] = 4.0 * x * (1.0 - x);
+    out[2] = x * (2.0 * x - 1.0);
+  };
+  auto dL = [](double x, double out[3]) {
+    out[0] = 4.0 * x - 3.0;
+    out[1] = 4.0 - 8.0 * x;
+    out[2] = 4.0 * x - 1.0;
+  };
+  for (int q = 0; q < 4; ++q) {
+    t.s[q] = s[q];
+    t.w[q] = w[q];
+    L(s[q], t.B[q]);
+    dL(s[q], t.G[q]);
+  }
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      double acc = 0.0;
+      for (int q = 0; q < 4; ++q) acc += w[q] * t.B[q][i] * t.B[q][j];
+      t.M1[i][j] = acc;
+    }
+  L(0.0, t.E[0]);
+  L(1.0, t.E[1]);
+  dL(0.0, t.dE[0]);
+  dL(1.0, t.dE[1]);
+  return t;
+}
+}  // namespace pdst

@@ -97,7 +97,7 @@ struct TimeData {
 struct Disc {
   double gamma1, gamma2, gamma_cip;
   int viscous, convection, pressure;
-  int skip;  // profiling only (PDST_SKIP): 1 volume, 2 CIP, 4 sides, 8 mass, 16 assembly
+  int skip;  // profiling only (PDST_SKIP): 1 volume, 2 CIP, 4 sides, 8 mass, 16 assembly, 32 boundary kernel, 64 tile fixup
 };
 
 struct Model {
@@ -116,6 +116,7 @@ struct Lin {
   const double* betad;  // [nbf][4]
   const double* dg;     // [nbf][4][3] sym grad of the lifting
   const double* bmat;   // [k1][21][21][nbf] boundary-side matrices (rows i, cols j), or null
+  const double* apc;    // apply cache (pdst_operator.cu, APC_SLOTS), or null
   int has_gamma;        // 0 for Picard (gamma == 0)
 };
 

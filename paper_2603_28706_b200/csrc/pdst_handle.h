@@ -19,6 +19,8 @@ struct DeviceBuffer {
   DeviceBuffer& operator=(const DeviceBuffer&) = delete;
   ~DeviceBuffer() { release(); }
   double* ensure(size_t n);
+  // As ensure(), zero-filling a fresh allocation (counters that must start at 0).
+  double* ensure_zeroed(size_t n);
   void release();
 };
 
@@ -116,6 +118,7 @@ struct pdst_handle {
   pdst::DeviceBuffer eta, gam, etaf, gamf;
   pdst::DeviceBuffer etad, betad, dg;
   pdst::DeviceBuffer bmat;  // boundary-side matrices of the linearization
+  pdst::DeviceBuffer apc;   // apply cache of the linearization (the Jacobian apply's coefficient stream)
   pdst::DeviceBuffer ghat;
   bool has_ghat = false;
   bool linearized = false;
@@ -178,6 +181,7 @@ inline Lin lin_of(pdst_handle* h) {
   L.betad = h->betad.ptr;
   L.dg = h->dg.ptr;
   L.bmat = h->bmat.ptr;
+  L.apc = h->apc.ptr;
   L.has_gamma = h->model.kind != 0;
   return L;
 }

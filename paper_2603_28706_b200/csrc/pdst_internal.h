@@ -8,11 +8,20 @@
 namespace pdst {
 
 cudaError_t set_tables(const Tables& t);
+Tables host_tables();
 
 // y = J x (rhs == null) or y = rhs - J x; `part` holds jacobian_scratch() doubles.
 size_t jacobian_scratch(const Geom& g, int k1);
-cudaError_t jacobian_apply(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* state,
-                           const double* x, const double* rhs, double* out, double* part, cudaStream_t st);
+// Requires the linearization's boundary matrices (L.bmat) and apply cache (L.apc).
+cudaError_t jacobian_apply(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* x,
+                           const double* rhs, double* out, double* part, cudaStream_t st);
+
+// Apply cache of the linearization L at velocity state (k1, Mv): the
+// per-quadrature-point coefficients the Jacobian apply streams
+// (apply_cache_size() doubles).
+size_t apply_cache_size(const Geom& g, int k1);
+cudaError_t apply_cache(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* state,
+                        double* apc, cudaStream_t st);
 
 cudaError_t slab_residual(const Geom& g, const TimeData& td, const Disc& ds, const Model& m, const Lin& L,
                           const double* U, const double* advect, const double* vminus, const double* fqp,

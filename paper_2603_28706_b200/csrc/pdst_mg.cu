@@ -354,10 +354,10 @@ int pdst_patch_info(pdst_handle* h, int level, int32_t* D, int32_t* diag_blocks,
 static int level_defect(pdst_handle* h, int l, const double* x, const double* r, double* y) {
   const int L = (int)h->levels.size();
   if (l == L - 1) {
-    double* part = h->jpart.ensure(jacobian_scratch(h->g, h->td.k1));
+    double* part = h->jpart.ensure_zeroed(jacobian_scratch(h->g, h->td.k1));
     if (!part) return set_error(PDST_ECUDA, "out of device memory");
     CK(PDST_TIMED(h, PK_JACOBIAN,
-                  jacobian_apply(h->g, h->td, h->ds, lin_of(h), h->state.ptr, x, r, y, part, h->stream)));
+                  jacobian_apply(h->g, h->td, h->ds, lin_of(h), x, r, y, part, h->stream)));
   } else {
     CK(PDST_TIMED(h, PK_LEVEL, level_apply(level_op(h, l), h->td, x, r, y, h->stream)));
   }

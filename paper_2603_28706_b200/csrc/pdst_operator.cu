@@ -51,6 +51,11 @@ struct Plane2 {
   __device__ double at(int d, int r, int c) const { return (d == 0 ? p0 : p1)[pidx(r, c)]; }
 };
 
+// A staged plane pair addressed by its offset in the kernel's dynamic shared
+// memory: the accesses stay LDS (a pointer array can be demoted to local
+// memory and turn them into generic loads).
+extern __shared__ double g_dsmem[];
+
 // Accumulators for the cell's 9-node velocity contributions: registers (the
 // element-matrix kernel, the volume phase) or the thread's shared-memory slot
 // (structure of arrays over the CTA's threads, stride NT).
@@ -553,8 +558,8 @@ __device__ __forceinline__ void row_sums(const FA& F, int r, int c0, int qx, dou
 }
 
 // acc += s * (M1 (x) M1) XT for the cell, XT = sum_nu K_t[mu,nu] F_nu - mfac * Fm.
-template <int K1, class ACC>
-__device__ __forceinline__ void add_mass(const Plane2* F, const Plane2* Fm, double mfac, const double* Krow, int r0,
+template <int K1, class ACC, class FA = Plane2>
+__device__ __forceinline__ void add_mass(const FA* F, const FA* Fm, double mfac, const double* Krow, int r0,
                                          int c0, double s, const ACC& acc) {
 #pragma unroll
   for (int jj = 0; jj < 3; ++jj) {  // source row jy'
@@ -838,11 +843,57 @@ __device__ void assemble_and_store(const Geom& g, const double* sacc, int i0, in
 // boundary shared with a neighbour tile are written as partial sums to `part`
 // and combined by k_jac_fixup in a fixed order (deterministic).
 // ---------------------------------------------------------------------------
-constexpr int JT = 16;            // owned cells per tile side
+// Per-CTA phase timeline of the apply (profiling builds only, -DPDST_TRACE).
+#ifdef PDST_TRACE
+__device__ unsigned long long g_trace[8192][16];
+#define TR(i)                                                                                          \
+  do {                                                                                                 \
+    if (threadIdx.x == 0) {                                                                            \
+      unsigned long long t_;                                                                           \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                           \
+      g_trace[blockIdx.y * gridDim.x + blockIdx.x][i] = t_;                                            \
+    }                                                                                                  \
+  } while (0)
+#else
+#define TR(i) \
+  do {        \
+  } while (0)
+#endif
+#ifndef PDST_JT
+#define PDST_JT 16
+#endif
+constexpr int JT = PDST_JT;       // owned cells per tile side
 constexpr int JNT = JT * JT;      // threads per CTA
 constexpr int JPER = 8 * JT;      // perimeter nodes of a tile's node rectangle
-static_assert(2 * (JT + 2) + 1 == NC && 2 * (JT + 2) + 1 == NR, "Jacobian tile must match the staged plane");
-static_assert(JNT == NT, "SmemAcc stride");
+// Staged direction planes of the apply: the tile's nodes with a one-cell ring
+// (CIP jumps of the tile's edge cells), even/odd column split as in pidx.
+constexpr int JNC = 2 * (JT + 2) + 1;
+constexpr int JNC2 = (JNC + 1) / 2;
+constexpr int JRS = 2 * JNC2;
+constexpr int JPLANE = JNC * JRS;
+__host__ __device__ constexpr int jpidx(int r, int c) { return r * JRS + (c & 1) * JNC2 + (c >> 1); }
+using JAcc = SmemAccN<JNT>;
+
+// A staged plane pair addressed by its offset in the kernel's dynamic shared
+// memory: the accesses stay LDS (a pointer array can be demoted to local
+// memory and turn them into generic loads).
+struct PlaneS {
+  int o;  // component 0 at o, component 1 at o + JPLANE
+  __device__ double at(int d, int r, int c) const { return g_dsmem[o + d * JPLANE + jpidx(r, c)]; }
+};
+
+// Issue the asynchronous staging of one velocity block into the apply's plane
+// pair at offset o (zero outside the domain).
+__device__ __forceinline__ void stage_jac_async(const Geom& g, const double* __restrict__ v, int o, int X0, int Y0) {
+  for (int idx = threadIdx.x; idx < JNC * JNC; idx += JNT) {
+    const int r = idx / JNC, c = idx - r * JNC;
+    const int X = X0 + c, Y = Y0 + r;
+    const bool in = X >= 0 && X < g.nnx && Y >= 0 && Y < g.nny;
+    const double* src = in ? v + 2 * ((size_t)Y * g.nnx + X) : v;
+    cp_async8(g_dsmem + o + jpidx(r, c), src, in);
+    cp_async8(g_dsmem + o + JPLANE + jpidx(r, c), in ? src + 1 : v, in);
+  }
+}
 
 __host__ __device__ inline int jac_tiles_x(const Geom& g) { return (g.nx + JT - 1) / JT; }
 __host__ __device__ inline int jac_tiles_y(const Geom& g) { return (g.ny + JT - 1) / JT; }
@@ -948,35 +999,318 @@ __device__ __forceinline__ void stage_planned(const StagePlan& sp, const double*
   }
 }
 
-// One CTA per SM with the full register file (~250 registers, no spills):
-// measured faster than two CTAs per SM at 128 registers (75 vs 90 us at cfg2)
-// even though the 256 tiles then take 1.73 waves.  The freed shared memory
-// goes to PIPE (K1 <= 2): every Radau node's state planes are staged up front
-// and the per-cell slots are double buffered, so the assembly of node mu
-// overlaps the compute of node mu+1 (one barrier per node instead of two).
-template <int K1>
-__host__ __device__ constexpr bool jac_pipe() { return K1 <= 2; }
-template <int K1>
-__host__ __device__ constexpr int jac_nbuf() { return jac_pipe<K1>() ? K1 : 1; }
+// ---------------------------------------------------------------------------
+// Apply cache (built once per linearization by k_apply_cache, read by every
+// apply): the reference's per-quadrature-point linearization cache
+// (forms.py:544-578) in the form the apply consumes, tile-major so that a
+// warp's 32 cells read one contiguous 256-byte row per slot.
+//   apc[((tile * k1 + mu) * APC_SLOTS + s) * JNT + t],  t = cell in tile
+//   volume slots s = (qx * 6 + k) * 4 + qy with wq = tau w_mu hx hy w_qx w_qy:
+//     k = 0   e   = wq eta
+//     k = 1-3 a~  = sqrt(-wq gamma) (a0, a1, a2),  A = sym grad v = [[a0 a2][a2 a1]]
+//             (gamma <= 0 for 1 < p <= 2, so wq T(B) = e B - (a~ : B) a~)
+//     k = 4-5 wq v (convection)
+//   CIP slots 96 + 4 f + q, faces f = right, top, left, bottom: the face
+//     weight tau w_mu gamma_cip h^2 / hn^2 (w_q h) |v_L . n| of cip_face.
+// ---------------------------------------------------------------------------
+constexpr int APC_VOL = 96;
+constexpr int APC_SLOTS = APC_VOL + 16;
 
+// The apply cache streams through a per-thread shared-memory ring of 12
+// doubles (half a Gauss column: 2 points x 6 coefficients), filled with
+// cp.async one half-column ahead of its use.  Each thread touches only its own
+// ring column, so no barrier is involved; a half is copied to registers and
+// used before the refill of the same slots is issued.
+constexpr int RING = 12;
+#ifndef PDST_PF_AHEAD
+#define PDST_PF_AHEAD 3  // halves between the L2 prefetch and the use
+#endif
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// L2 prefetch of half h (further ahead than the ring can hold).
+__device__ __forceinline__ void ring_prefetch_l2(const double* __restrict__ cp, int h) {
+  if (h < 8) {
+    const int qx = h >> 1, qy0 = (h & 1) * 2;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) prefetch_l2(cp + (qx * 24 + k * 4 + qy0 + j) * JNT);
+  } else if (h == 8) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) prefetch_l2(cp + (APC_VOL + i) * JNT);
+  }
+}
+
+// XOR of the high words of the values just read from the ring.  Passed to the
+// refill's cp.async as an operand, it makes the refill wait until those reads
+// have landed in registers: the write-after-read order on the ring slots is
+// then enforced by the register scoreboard, not by timing.
+template <int N>
+__device__ __forceinline__ unsigned ring_dep(const double* v) {
+  unsigned d = 0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) d ^= (unsigned)__double2hiint(v[i]);
+  return d;
+}
+
+__device__ __forceinline__ void cp_async8_dep(double* dst, const double* src, unsigned dep) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src), "r"(dep) : "memory");
+}
+
+// Issue half h (0..7: Gauss column h/2, points 2(h%2), 2(h%2)+1) of a node's
+// cache block into the ring; h == 8 issues the CIP weights of faces 0-2.
+// `dep` = ring_dep of the values the ring slots held.
+__device__ __forceinline__ void ring_issue(const double* __restrict__ cp, int h, double* ring, unsigned dep) {
+  if (h < 8) {
+    const int qx = h >> 1, qy0 = (h & 1) * 2;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) cp_async8_dep(ring + (j * 6 + k) * JNT, cp + (qx * 24 + k * 4 + qy0 + j) * JNT, dep);
+  } else {
+#pragma unroll
+    for (int i = 0; i < RING; ++i) cp_async8_dep(ring + i * JNT, cp + (APC_VOL + i) * JNT, dep);
+  }
+  cp_async_commit();
+}
+
+// 1-D tables of the apply with the mesh scales folded in (kernel parameter:
+// with the Gauss loops unrolled every entry is an immediate constant operand).
+struct JTabs {
+  double B[4][3];    // L_i(s_q)
+  double Gx[4][3];   // L_i'(s_q) / hx
+  double Gy[4][3];   // L_i'(s_q) / hy
+  double w[4];       // w_q
+  double wyh[4];     // w_q (s_q - 1/2)
+  double xh[4];      // s_q - 1/2
+};
+
+// Volume terms (forms.py:589-603) from the apply cache; the first writer of
+// the cell's slot.  On entry half 0 of the node's cache is in flight to the
+// ring; on exit the CIP weights of faces 0-2 are (w3 = face 3 from global).
+template <class XA>
+__device__ __forceinline__ void jac_volume_cached(const JTabs& T, const Disc& ds, const double* __restrict__ cp,
+                                                  const XA& XM, int r0, int c0, const double P[3], double* slot,
+                                                  double* ring, double accp[3], double WT, double w3[4]) {
+#pragma unroll 1
+  for (int qx = 0; qx < 4; ++qx) {
+    double xB[3][2], xG[3][2];
+#pragma unroll
+    for (int jy = 0; jy < 3; ++jy)
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        const double f0 = XM.at(d, r0 + jy, c0), f1 = XM.at(d, r0 + jy, c0 + 1), f2 = XM.at(d, r0 + jy, c0 + 2);
+        xB[jy][d] = T.B[qx][0] * f0 + T.B[qx][1] * f1 + T.B[qx][2] * f2;
+        xG[jy][d] = T.Gx[qx][0] * f0 + T.Gx[qx][1] * f1 + T.Gx[qx][2] * f2;
+      }
+    double Pa[3][2] = {{0, 0}, {0, 0}, {0, 0}}, Qa[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+    const double wxT = T.w[qx] * WT;
+    // pressure along the column: dp(qy) = w_qy A + wyh_qy Bp (times w_qx WT)
+    const double pA = wxT * (P[0] + P[1] * T.xh[qx]), pB = wxT * P[2];
+    double dv0 = 0.0, dv1 = 0.0;
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int h = 2 * qx + hh;
+      cp_async_wait0();
+      double cv[2][6];
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int k = 0; k < 6; ++k) cv[j][k] = ring[(j * 6 + k) * JNT];
+      ring_issue(cp, h + 1, ring, ring_dep<12>(&cv[0][0]));
+      ring_prefetch_l2(cp, h + PDST_PF_AHEAD);
+      if (h == 7) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w3[q] = __ldg(cp + (APC_VOL + 12 + q) * JNT);
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int qy = 2 * hh + j;
+        double u[2], ux[2], uy[2];
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+          u[d] = T.B[qy][0] * xB[0][d] + T.B[qy][1] * xB[1][d] + T.B[qy][2] * xB[2][d];
+          ux[d] = T.B[qy][0] * xG[0][d] + T.B[qy][1] * xG[1][d] + T.B[qy][2] * xG[2][d];
+          uy[d] = T.Gy[qy][0] * xB[0][d] + T.Gy[qy][1] * xB[1][d] + T.Gy[qy][2] * xB[2][d];
+        }
+        const double ce = cv[j][0], ca0 = cv[j][1], ca1 = cv[j][2], ca2 = cv[j][3], cv0 = cv[j][4], cv1 = cv[j][5];
+        // wq T(B) with B = sym grad u (b0, b1, b2 = cc / 2)
+        const double b0 = ux[0], b1 = uy[1], cc = uy[0] + ux[1];
+        const double t = ca0 * b0 + ca1 * b1 + ca2 * cc;
+        double F00 = ce * b0 - t * ca0;
+        double F11 = ce * b1 - t * ca1;
+        double F01 = ce * (0.5 * cc) - t * ca2;
+        // - wq (u (x) v + v (x) u)
+        F00 -= 2.0 * u[0] * cv0;
+        F11 -= 2.0 * u[1] * cv1;
+        F01 -= u[1] * cv0 + u[0] * cv1;
+        if (ds.pressure) {
+          const double dp = T.w[qy] * pA + T.wyh[qy] * pB;
+          F00 -= dp;
+          F11 -= dp;
+          const double div = ux[0] + uy[1];
+          dv0 = fma(T.w[qy], div, dv0);
+          dv1 = fma(T.wyh[qy], div, dv1);
+        }
+#pragma unroll
+        for (int jy = 0; jy < 3; ++jy) {
+          Pa[jy][0] = fma(F00, T.B[qy][jy], Pa[jy][0]);
+          Pa[jy][1] = fma(F01, T.B[qy][jy], Pa[jy][1]);
+          Qa[jy][0] = fma(F01, T.Gy[qy][jy], Qa[jy][0]);
+          Qa[jy][1] = fma(F11, T.Gy[qy][jy], Qa[jy][1]);
+        }
+      }
+    }
+    accp[0] -= wxT * dv0;
+    accp[1] -= (wxT * T.xh[qx]) * dv0;
+    accp[2] -= wxT * dv1;
+    // the column's test-function sums go straight to the cell's slot (the
+    // first column stores): keeps the loop at 128 registers
+#pragma unroll
+    for (int jy = 0; jy < 3; ++jy)
+#pragma unroll
+      for (int ix = 0; ix < 3; ++ix)
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+          const double v = T.Gx[qx][ix] * Pa[jy][d] + T.B[qx][ix] * Qa[jy][d];
+          double* sp = slot + (2 * (3 * jy + ix) + d) * JNT;
+          *sp = qx == 0 ? v : *sp + v;
+        }
+  }
+}
+
+// CIP face with cached weights w[q] (cip_face with A replaced by the
+// precomputed |v_L . n| weights).
+template <class FA>
+__device__ __forceinline__ void cip_face_cached(int axis, const FA& F, int rL, int cL, const double w[4],
+                                                double RD[3][2]) {
+  const int rR = axis == 1 ? rL + 2 : rL, cR = axis == 0 ? cL + 2 : cL;
+  double dl[3][2], dr[3][2];
+  line_sums(F, rL, cL, axis, c_tab.dE[1], dl);
+  line_sums(F, rR, cR, axis, c_tab.dE[0], dr);
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    dl[t][0] -= dr[t][0];
+    dl[t][1] -= dr[t][1];
+    RD[t][0] = RD[t][1] = 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    double j0 = 0.0, j1 = 0.0;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      j0 = fma(c_tab.B[q][t], dl[t][0], j0);
+      j1 = fma(c_tab.B[q][t], dl[t][1], j1);
+    }
+    const double c0v = w[q] * j0, c1v = w[q] * j1;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      RD[t][0] = fma(c0v, c_tab.B[q][t], RD[t][0]);
+      RD[t][1] = fma(c1v, c_tab.B[q][t], RD[t][1]);
+    }
+  }
+}
+
+// The four CIP faces of a cell (right, top, left, bottom), own side only;
+// w[f][q] = cached weights.
+template <class FA, class ACC>
+__device__ __forceinline__ void cip_all_cached(const Geom& g, const FA& F, int ci, int cj, int r0, int c0,
+                                               const double (*w)[4], const ACC& acc) {
+  double RD[3][2];
+  if (ci < g.nx - 1) {
+    cip_face_cached(0, F, r0, c0, w[0], RD);
+    cip_scatter(0, true, 1.0, RD, acc);
+  }
+  if (cj < g.ny - 1) {
+    cip_face_cached(1, F, r0, c0, w[1], RD);
+    cip_scatter(1, true, 1.0, RD, acc);
+  }
+  if (ci > 0) {
+    cip_face_cached(0, F, r0, c0 - 2, w[2], RD);
+    cip_scatter(0, false, 1.0, RD, acc);
+  }
+  if (cj > 0) {
+    cip_face_cached(1, F, r0 - 2, c0, w[3], RD);
+    cip_scatter(1, false, 1.0, RD, acc);
+  }
+}
+
+// Shared tile-boundary nodes: sum the (2 or 4) tile partials in fixed order.
+template <int T>
+__global__ void k_jac_fixup(Geom g, int k1, const double* __restrict__ part, const double* __restrict__ rhs,
+                            double* __restrict__ out) {
+  pdl_wait();  // partials of k_jacobian
+  constexpr int PER = 8 * T;
+  const int ntx = (g.nx + T - 1) / T, nty = (g.ny + T - 1) / T;
+  const size_t nv = (size_t)(ntx - 1) * g.nny;  // nodes on interior vertical tile lines
+  const size_t nh = (size_t)(nty - 1) * g.nnx;  // nodes on interior horizontal tile lines
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int mu = blockIdx.y;
+  int X, Y;
+  if (t < nv) {
+    X = 2 * T * (int)(t / g.nny + 1);
+    Y = (int)(t % g.nny);
+  } else if (t < nv + nh) {
+    const size_t u = t - nv;
+    Y = 2 * T * (int)(u / g.nnx + 1);
+    X = (int)(u % g.nnx);
+    if (X % (2 * T) == 0 && X > 0 && X / (2 * T) < ntx) return;  // on a vertical line
+  } else {
+    return;
+  }
+  int bxs[2], bys[2], nbx = 0, nby = 0;
+  if (X % (2 * T) == 0 && X > 0 && X / (2 * T) < ntx) {
+    bxs[0] = X / (2 * T) - 1;
+    bxs[1] = X / (2 * T);
+    nbx = 2;
+  } else {
+    bxs[0] = min(X / (2 * T), ntx - 1);
+    nbx = 1;
+  }
+  if (Y % (2 * T) == 0 && Y > 0 && Y / (2 * T) < nty) {
+    bys[0] = Y / (2 * T) - 1;
+    bys[1] = Y / (2 * T);
+    nby = 2;
+  } else {
+    bys[0] = min(Y / (2 * T), nty - 1);
+    nby = 1;
+  }
+  const size_t ntiles = (size_t)ntx * nty;
+  double s0 = 0.0, s1 = 0.0;
+  for (int b = 0; b < nby; ++b)
+    for (int a = 0; a < nbx; ++a) {
+      const int lx = X - 2 * T * bxs[a], ly = Y - 2 * T * bys[b];
+      const double* pp = part + (((size_t)mu * ntiles + (size_t)bys[b] * ntx + bxs[a]) * PER + perim_t<T>(lx, ly)) * 2;
+      s0 += pp[0];
+      s1 += pp[1];
+    }
+  const size_t o = (size_t)mu * g.nd + 2 * ((size_t)Y * g.nnx + X);
+  out[o] = rhs ? rhs[o] - s0 : s0;
+  out[o + 1] = rhs ? rhs[o + 1] - s1 : s1;
+}
+
+
+// One thread per cell, two CTAs (16 warps) per SM: the state is not staged —
+// its contribution comes from the apply cache, streamed once per apply — so
+// the CTA holds only the direction planes of all Radau nodes and one set of
+// per-cell node slots.
 template <int K1>
-__global__ void __launch_bounds__(JNT, 1) k_jacobian(Geom g, TimeData td, Disc ds, Lin L, const double* __restrict__ state,
+__global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, TimeData td, Disc ds, Lin L,
                                                   const double* __restrict__ x, const double* __restrict__ rhs,
                                                   double* __restrict__ out, double* __restrict__ part,
-                                                  const double* __restrict__ ybnd) {
-  constexpr bool PIPE = jac_pipe<K1>();
-  constexpr int NB = jac_nbuf<K1>();
-  extern __shared__ double smem[];
-  double* xs = smem;                             // [K1][2][PLANE] direction x_nu, all Radau nodes (one-cell ring)
-  double* ss0 = xs + (size_t)K1 * 2 * PLANE;      // [NB][2][PLANE] state v_mu
-  double* sacc0 = ss0 + (size_t)NB * 2 * PLANE;   // [NB][18][JNT]  per-cell node contributions
+                                                  const double* __restrict__ ybnd, const JTabs T) {
+  double* sacc = g_dsmem + (size_t)K1 * 2 * JPLANE;  // [18][JNT] per-cell node contributions
+  // [K1][2][JPLANE] direction x_nu, all Radau nodes (one-cell ring), in front
+  double* ring = sacc + 18 * JNT + threadIdx.x;  // [RING][JNT] apply-cache ring (this thread's column)
   const int bx = blockIdx.x, by = blockIdx.y;
   const int i0 = bx * JT, j0 = by * JT;
   const int X0 = 2 * (i0 - 1), Y0 = 2 * (j0 - 1);
   const int ntx = min(JT, g.nx - i0), nty = min(JT, g.ny - j0);
-  Plane2 XP[K1];
+  PlaneS XP[K1];
 #pragma unroll
-  for (int nu = 0; nu < K1; ++nu) XP[nu] = Plane2{xs + nu * 2 * PLANE, xs + nu * 2 * PLANE + PLANE};
+  for (int nu = 0; nu < K1; ++nu) XP[nu] = PlaneS{nu * 2 * JPLANE};
   const int tx = threadIdx.x % JT, ty = threadIdx.x / JT;
   const int ci = i0 + tx, cj = j0 + ty;
   const bool valid = tx < ntx && ty < nty;
@@ -988,68 +1322,97 @@ __global__ void __launch_bounds__(JNT, 1) k_jacobian(Geom g, TimeData td, Disc d
   // nodes owned by this cell in the tile: its lower-left 2x2, plus the tile's
   // last row / column of nodes for the last cell column / row
   const bool lastx = tx == ntx - 1, lasty = ty == nty - 1;
+  const double* cbase = L.apc + tile * K1 * APC_SLOTS * JNT + threadIdx.x;
 
+  TR(0);
   pdl_trigger();  // k_jac_fixup may be scheduled; it waits for this grid
-  // pull this cell's eta / gamma lines (128 B each per Radau node) towards L2
-  // now; the volume loop reads them one Gauss column at a time
-  if (valid && ds.viscous) {
-#pragma unroll
-    for (int mu = 0; mu < K1; ++mu) {
-      prefetch_l2(L.eta + ((size_t)mu * g.ncells + c) * 16);
-      if (L.has_gamma) prefetch_l2(L.gam + ((size_t)mu * g.ncells + c) * 16);
-    }
+  if (valid) {
+    ring_issue(cbase, 0, ring, 0u);
+    for (int h = 1; h < PDST_PF_AHEAD; ++h) ring_prefetch_l2(cbase, h);
   }
-  for (int nu = 0; nu < K1; ++nu)
-    stage_velocity_async(g, x + (size_t)nu * g.nd, xs + (size_t)nu * 2 * PLANE, xs + (size_t)nu * 2 * PLANE + PLANE,
-                         X0, Y0);
-  if (PIPE) {
-    for (int nu = 0; nu < K1; ++nu)
-      stage_velocity_async(g, state + (size_t)nu * g.mv, ss0 + (size_t)nu * 2 * PLANE,
-                           ss0 + (size_t)nu * 2 * PLANE + PLANE, X0, Y0);
-  }
+  for (int nu = 0; nu < K1; ++nu) stage_jac_async(g, x + (size_t)nu * g.nd, nu * 2 * JPLANE, X0, Y0);
+  cp_async_wait_all();  // (commits the staging copies and waits for every group)
+  __syncthreads();
+  TR(1);
   for (int mu = 0; mu < K1; ++mu) {
     const double tw = td.tau_w[mu];
-    const int buf = PIPE ? mu : 0;
-    double* ss = ss0 + (size_t)buf * 2 * PLANE;
-    double* sacc = sacc0 + (size_t)buf * 18 * JNT;
-    const Plane2 SP{ss, ss + PLANE};
-    const SmemAcc slot{sacc + threadIdx.x};
-    if (!PIPE) stage_velocity_async(g, state + (size_t)mu * g.mv, ss, ss + PLANE, X0, Y0);
-    const Plane2 XM{xs + (size_t)mu * 2 * PLANE, xs + (size_t)mu * 2 * PLANE + PLANE};
-    double P[3] = {0.0, 0.0, 0.0};
+    const double* cp = cbase + (size_t)mu * APC_SLOTS * JNT;
+    double* slot = sacc + threadIdx.x;
+    const JAcc acc{slot};
+    const PlaneS XM{mu * 2 * JPLANE};
     if (valid) {
+      if (rhs) {  // defect mode: pull this cell's rhs rows towards L2 for the assembly
+        const size_t ob = (size_t)mu * g.nd + 2 * ((size_t)(2 * cj) * g.nnx + 2 * ci);
+        prefetch_l2(rhs + ob);
+        prefetch_l2(rhs + ob + 2 * g.nnx);
+        prefetch_l2(rhs + (size_t)mu * g.nd + g.mv + 3 * (size_t)c);
+      }
+      double P[3];
       const double* xp = x + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
       P[0] = __ldg(xp);
       P[1] = __ldg(xp + 1);
       P[2] = __ldg(xp + 2);
-    }
-#pragma unroll
-    for (int k = 0; k < 18; ++k) sacc[k * JNT + threadIdx.x] = 0.0;
-    if (!PIPE || mu == 0) {
-      cp_async_wait_all();
-      __syncthreads();
-    }
-    if (valid) {
       double accp[3] = {0.0, 0.0, 0.0};
       // tau w_mu J_mu x_mu: volume, boundary sides, CIP faces (weights carry tau w_mu)
-      if (!(ds.skip & 1)) jac_volume(g, ds, L, mu, c, XM, SP, r0, c0, P, slot, accp, tw);
-      if (!(ds.skip & 4)) {
-        if (ybnd)
-        {
-          if (ci == 0 || cj == 0 || ci == g.nx - 1 || cj == g.ny - 1) pdl_wait();  // ybnd of k_boundary_apply
-          jac_sides_pre(g, ybnd, mu, ci, cj, slot, accp, tw);
-        }
-        else
-          jac_sides(g, ds, L, mu, ci, cj, XM, SP, r0, c0, P, slot, accp, tw);
+      double w3[4];
+      if (!(ds.skip & 1))
+        jac_volume_cached(T, ds, cp, XM, r0, c0, P, slot, ring, accp, g.hx * g.hy * tw, w3);
+      else {
+#pragma unroll
+        for (int k = 0; k < 18; ++k) slot[k * JNT] = 0.0;
+        cp_async_wait0();
+        double h0[RING];
+#pragma unroll
+        for (int i = 0; i < RING; ++i) h0[i] = ring[i * JNT];
+        ring_issue(cp, 8, ring, ring_dep<RING>(h0));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w3[q] = __ldg(cp + (APC_VOL + 12 + q) * JNT);
       }
-      if (cip && !(ds.skip & 2)) cip_all(g, ds, XM, SP, ci, cj, r0, c0, tw, slot);
+      TR(2 + 5 * mu);
+      // CIP, temporal mass and boundary sides accumulate in registers (the
+      // volume's registers are free now) and reach the slot in one pass
+      double ra[3][3][2];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) ra[a][b][0] = ra[a][b][1] = 0.0;
+      const RegAcc racc{ra};
+      {
+        double w[4][4];
+        cp_async_wait0();
+#pragma unroll
+        for (int i = 0; i < RING; ++i) w[i / 4][i % 4] = ring[i * JNT];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w[3][q] = w3[q];
+        if (cip && !(ds.skip & 2)) cip_all_cached(g, XM, ci, cj, r0, c0, w, racc);
+        // the next node's first half-column (after the weights are consumed)
+        if (mu + 1 < K1) {
+          ring_issue(cp + APC_SLOTS * JNT, 0, ring, ring_dep<12>(&w[0][0]));
+          for (int h = 1; h < PDST_PF_AHEAD; ++h) ring_prefetch_l2(cp + APC_SLOTS * JNT, h);
+        }
+      }
+      TR(3 + 5 * mu);
       // + M_K sum_nu K_t[mu,nu] x_nu (slab.py:199-200)
-      if (!(ds.skip & 8)) add_mass<K1>(XP, nullptr, 0.0, td.K_t + mu * K1, r0, c0, g.hx * g.hy, slot);
+      if (!(ds.skip & 8)) add_mass<K1>(XP, (const PlaneS*)nullptr, 0.0, td.K_t + mu * K1, r0, c0, g.hx * g.hy, racc);
+      // boundary sides last: k_boundary_apply (PDL predecessor) has had the
+      // whole cell pass to finish
+      if (!(ds.skip & 4)) {
+        if (ci == 0 || cj == 0 || ci == g.nx - 1 || cj == g.ny - 1) pdl_wait();  // ybnd of k_boundary_apply
+        jac_sides_pre(g, ybnd, mu, ci, cj, racc, accp, tw);
+      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+          for (int d = 0; d < 2; ++d) acc.add(a, b, d, ra[a][b][d]);
       const size_t o = (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
 #pragma unroll
       for (int j = 0; j < 3; ++j) out[o + j] = rhs ? rhs[o + j] - accp[j] : accp[j];
     }
+    TR(4 + 5 * mu);
     __syncthreads();
+    TR(5 + 5 * mu);
     // node assembly: each cell writes the nodes it owns (lower-left 2x2 of its
     // 3x3 block, plus the right column / top row for the tile's last cells),
     // summing the <= 4 cells that contain a node in a fixed order.
@@ -1124,62 +1487,9 @@ __global__ void __launch_bounds__(JNT, 1) k_jacobian(Geom g, TimeData td, Disc d
         if (lastx) emit(lx + 2, ly + 2, 0.0 + at(sm_, 8, 0), 0.0 + at(sm_, 8, 1));
       }
     }
-    if (!PIPE) __syncthreads();
+    __syncthreads();  // the slots are rewritten by the next node's volume pass
+    TR(6 + 5 * mu);
   }
-}
-
-// Shared tile-boundary nodes: sum the (2 or 4) tile partials in fixed order.
-template <int T>
-__global__ void k_jac_fixup(Geom g, int k1, const double* __restrict__ part, const double* __restrict__ rhs,
-                            double* __restrict__ out) {
-  pdl_wait();  // partials of k_jacobian
-  constexpr int PER = 8 * T;
-  const int ntx = (g.nx + T - 1) / T, nty = (g.ny + T - 1) / T;
-  const size_t nv = (size_t)(ntx - 1) * g.nny;  // nodes on interior vertical tile lines
-  const size_t nh = (size_t)(nty - 1) * g.nnx;  // nodes on interior horizontal tile lines
-  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int mu = blockIdx.y;
-  int X, Y;
-  if (t < nv) {
-    X = 2 * T * (int)(t / g.nny + 1);
-    Y = (int)(t % g.nny);
-  } else if (t < nv + nh) {
-    const size_t u = t - nv;
-    Y = 2 * T * (int)(u / g.nnx + 1);
-    X = (int)(u % g.nnx);
-    if (X % (2 * T) == 0 && X > 0 && X / (2 * T) < ntx) return;  // on a vertical line
-  } else {
-    return;
-  }
-  int bxs[2], bys[2], nbx = 0, nby = 0;
-  if (X % (2 * T) == 0 && X > 0 && X / (2 * T) < ntx) {
-    bxs[0] = X / (2 * T) - 1;
-    bxs[1] = X / (2 * T);
-    nbx = 2;
-  } else {
-    bxs[0] = min(X / (2 * T), ntx - 1);
-    nbx = 1;
-  }
-  if (Y % (2 * T) == 0 && Y > 0 && Y / (2 * T) < nty) {
-    bys[0] = Y / (2 * T) - 1;
-    bys[1] = Y / (2 * T);
-    nby = 2;
-  } else {
-    bys[0] = min(Y / (2 * T), nty - 1);
-    nby = 1;
-  }
-  const size_t ntiles = (size_t)ntx * nty;
-  double s0 = 0.0, s1 = 0.0;
-  for (int b = 0; b < nby; ++b)
-    for (int a = 0; a < nbx; ++a) {
-      const int lx = X - 2 * T * bxs[a], ly = Y - 2 * T * bys[b];
-      const double* pp = part + (((size_t)mu * ntiles + (size_t)bys[b] * ntx + bxs[a]) * PER + perim_t<T>(lx, ly)) * 2;
-      s0 += pp[0];
-      s1 += pp[1];
-    }
-  const size_t o = (size_t)mu * g.nd + 2 * ((size_t)Y * g.nnx + X);
-  out[o] = rhs ? rhs[o] - s0 : s0;
-  out[o + 1] = rhs ? rhs[o + 1] - s1 : s1;
 }
 
 // ---------------------------------------------------------------------------
@@ -1484,6 +1794,89 @@ struct GlobAcc {
   __device__ double at(int d, int r, int c) const { return __ldg(v + 2 * ((size_t)(Y0 + r) * nnx + X0 + c) + d); }
 };
 
+// Apply cache of the current linearization (layout at APC_SLOTS).  One
+// thread per (cell, Radau node); the quantities and their arithmetic follow
+// jac_volume (state value / sym gradient at the volume points, cached eta /
+// gamma) and cip_face (|v_L . n| on the left / lower trace).
+__global__ void __launch_bounds__(JNT) k_apply_cache(Geom g, TimeData td, Disc ds, Lin L, int k1,
+                                                     const double* __restrict__ state, double* __restrict__ apc) {
+  const int bx = blockIdx.x, by = blockIdx.y, mu = blockIdx.z;
+  const size_t tile = (size_t)by * jac_tiles_x(g) + bx;
+  const int tx = threadIdx.x % JT, ty = threadIdx.x / JT;
+  const int ci = bx * JT + tx, cj = by * JT + ty;
+  double* cp = apc + (tile * k1 + mu) * APC_SLOTS * JNT + threadIdx.x;
+  if (ci >= g.nx || cj >= g.ny) {
+    for (int s = 0; s < APC_SLOTS; ++s) cp[(size_t)s * JNT] = 0.0;
+    return;
+  }
+  const int c = cj * g.nx + ci;
+  const double tw = td.tau_w[mu];
+  const double W = g.hx * g.hy * tw;
+  const double* sv = state + (size_t)mu * g.mv;
+  const GlobAcc S{sv, g.nnx, 2 * ci, 2 * cj};
+  const bool vis = ds.viscous, hg = L.has_gamma && ds.viscous, conv = ds.convection;
+  for (int qx = 0; qx < 4; ++qx) {
+    double sB[3][2], sG[3][2];
+#pragma unroll
+    for (int jy = 0; jy < 3; ++jy) row_sums(S, jy, 0, qx, sB[jy], sG[jy]);
+#pragma unroll
+    for (int qy = 0; qy < 4; ++qy) {
+      double v[2], vx[2], vy[2];
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        v[d] = c_tab.B[qy][0] * sB[0][d] + c_tab.B[qy][1] * sB[1][d] + c_tab.B[qy][2] * sB[2][d];
+        vx[d] = (c_tab.B[qy][0] * sG[0][d] + c_tab.B[qy][1] * sG[1][d] + c_tab.B[qy][2] * sG[2][d]) * g.ihx;
+        vy[d] = (c_tab.G[qy][0] * sB[0][d] + c_tab.G[qy][1] * sB[1][d] + c_tab.G[qy][2] * sB[2][d]) * g.ihy;
+      }
+      const size_t o = ((size_t)mu * g.ncells + c) * 16 + 4 * qx + qy;
+      const double eta = vis ? L.eta[o] : 0.0;
+      const double gam = hg ? L.gam[o] : 0.0;
+      const double wq = c_tab.w[qx] * c_tab.w[qy] * W;
+      const double sg = sqrt(-(wq * gam));  // gamma <= 0 (p <= 2); NaN propagates
+      const double a0 = vx[0], a1 = vy[1], a2 = 0.5 * (vy[0] + vx[1]);
+      double* cq = cp + (size_t)qx * 24 * JNT + qy * JNT;
+      cq[0 * 4 * JNT] = wq * eta;
+      cq[1 * 4 * JNT] = sg * a0;
+      cq[2 * 4 * JNT] = sg * a1;
+      cq[3 * 4 * JNT] = sg * a2;
+      cq[4 * 4 * JNT] = conv ? wq * v[0] : 0.0;
+      cq[5 * 4 * JNT] = conv ? wq * v[1] : 0.0;
+    }
+  }
+  // CIP face weights: right, top (this cell is left / lower), left, bottom
+  // (the neighbour is); zero where the face is not interior.
+  const bool cip = ds.convection && ds.gamma_cip > 0.0;
+  for (int f = 0; f < 4; ++f) {
+    const int axis = f & 1;
+    const bool has = f == 0 ? ci < g.nx - 1 : f == 1 ? cj < g.ny - 1 : f == 2 ? ci > 0 : cj > 0;
+    const int lci = f == 2 ? ci - 1 : ci, lcj = f == 3 ? cj - 1 : cj;
+    double* wp = cp + (size_t)(APC_VOL + 4 * f) * JNT;
+    if (!(has && cip)) {
+      for (int q = 0; q < 4; ++q) wp[q * JNT] = 0.0;
+      continue;
+    }
+    const GlobAcc A{sv, g.nnx, 2 * lci, 2 * lcj};
+    const double hface = axis == 0 ? g.hy : g.hx;
+    const double ihn = axis == 0 ? g.ihx : g.ihy;
+    double tr[3];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      double v = 0.0;
+#pragma unroll
+      for (int n = 0; n < 3; ++n) v = fma(c_tab.E[1][n], axis == 0 ? A.at(0, t, n) : A.at(1, n, t), v);
+      tr[t] = v;
+    }
+    const double coef = tw * ds.gamma_cip * hface * hface * (ihn * ihn);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double vt = 0.0;
+#pragma unroll
+      for (int t = 0; t < 3; ++t) vt = fma(c_tab.B[q][t], tr[t], vt);
+      wp[q * JNT] = coef * (c_tab.w[q] * hface) * fabs(vt);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(128) k_element_matrices(Geom g, Disc ds, Lin L, int mu, const double* __restrict__ state,
                                                           double* __restrict__ ET) {
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1563,8 +1956,7 @@ __global__ void __launch_bounds__(128) k_boundary_matrices(Geom g, Disc ds, Lin 
 
 template <int K1>
 size_t jac_smem() {
-  constexpr int NB = jac_nbuf<K1>();
-  return ((size_t)(2 * K1 + 2 * NB) * PLANE + (size_t)NB * JNT * 18) * sizeof(double);
+  return ((size_t)2 * K1 * JPLANE + (size_t)JNT * (18 + RING)) * sizeof(double);
 }
 template <int K1>
 size_t res_smem() {
@@ -1572,8 +1964,8 @@ size_t res_smem() {
 }
 
 template <int K1>
-cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* state,
-                       const double* x, const double* rhs, double* out, double* part, cudaStream_t st) {
+cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* x,
+                       const double* rhs, double* out, double* part, cudaStream_t st) {
   static bool configured = false;
   const size_t sm = jac_smem<K1>();
   if (!configured) {
@@ -1581,24 +1973,33 @@ cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const 
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  double* ybnd = nullptr;
-  if (L.bmat) {
-    ybnd = part + (size_t)K1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2;
-    const size_t nb = (size_t)21 * g.nbf;
+  if (!L.bmat || !L.apc) return cudaErrorInvalidValue;  // built by pdst_linearize
+  double* ybnd = part + (size_t)K1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2;
+  const size_t nb = (size_t)21 * g.nbf;
+  if (!(ds.skip & 32))
     PDST_LAUNCH(k_boundary_apply<<<dim3((unsigned)((nb + 127) / 128), K1), 128, 0, st>>>(g, K1, L.bmat, x, ybnd));
-  }
   dim3 grid(jac_tiles_x(g), jac_tiles_y(g));
   cudaError_t e;
-  if (ybnd) {  // overlaps k_boundary_apply (only the boundary cells wait for it)
-    PDST_LAUNCH(e = launch_pdl(k_jacobian<K1>, grid, dim3(JNT), sm, st, g, td, ds, L, state, x, rhs, out, part,
-                               (const double*)ybnd));
-  } else {
-    PDST_LAUNCH(k_jacobian<K1><<<grid, JNT, sm, st>>>(g, td, ds, L, state, x, rhs, out, part, ybnd));
-    e = cudaGetLastError();
+  // overlaps k_boundary_apply (only the boundary cells wait for it)
+  JTabs T;
+  {
+    static const Tables tab = host_tables();
+    for (int q = 0; q < 4; ++q) {
+      for (int i = 0; i < 3; ++i) {
+        T.B[q][i] = tab.B[q][i];
+        T.Gx[q][i] = tab.G[q][i] * g.ihx;
+        T.Gy[q][i] = tab.G[q][i] * g.ihy;
+      }
+      T.w[q] = tab.w[q];
+      T.xh[q] = tab.s[q] - 0.5;
+      T.wyh[q] = tab.w[q] * (tab.s[q] - 0.5);
+    }
   }
+  PDST_LAUNCH(e = launch_pdl(k_jacobian<K1>, grid, dim3(JNT), sm, st, g, td, ds, L, x, rhs, out, part,
+                             (const double*)ybnd, T));
   if (e != cudaSuccess) return e;
   const size_t nfix = (size_t)(jac_tiles_x(g) - 1) * g.nny + (size_t)(jac_tiles_y(g) - 1) * g.nnx;
-  if (nfix > 0) {
+  if (nfix > 0 && !(ds.skip & 64)) {
     dim3 fg((unsigned)((nfix + 255) / 256), K1);
     PDST_LAUNCH(e = launch_pdl(k_jac_fixup<JT>, fg, dim3(256), 0, st, g, K1, (const double*)part, rhs, out));
     if (e != cudaSuccess) return e;
@@ -1624,19 +2025,26 @@ cudaError_t launch_res(const Geom& g, const TimeData& td, const Disc& ds, const 
 
 }  // namespace
 
+#ifdef PDST_TRACE
+extern "C" int pdst_debug_trace(unsigned long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, g_trace, (size_t)n * 16 * sizeof(unsigned long long));
+}
+#endif
+
 cudaError_t set_tables(const Tables& t) { return cudaMemcpyToSymbol(c_tab, &t, sizeof(Tables)); }
 
 size_t jacobian_scratch(const Geom& g, int k1) {
+  // tile partials, then the boundary-side products
   return (size_t)k1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2 + (size_t)k1 * 21 * g.nbf;
 }
 
-cudaError_t jacobian_apply(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* state,
-                           const double* x, const double* rhs, double* out, double* part, cudaStream_t st) {
+cudaError_t jacobian_apply(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* x,
+                           const double* rhs, double* out, double* part, cudaStream_t st) {
   switch (td.k1) {
-    case 1: return launch_jac<1>(g, td, ds, L, state, x, rhs, out, part, st);
-    case 2: return launch_jac<2>(g, td, ds, L, state, x, rhs, out, part, st);
-    case 3: return launch_jac<3>(g, td, ds, L, state, x, rhs, out, part, st);
-    case 4: return launch_jac<4>(g, td, ds, L, state, x, rhs, out, part, st);
+    case 1: return launch_jac<1>(g, td, ds, L, x, rhs, out, part, st);
+    case 2: return launch_jac<2>(g, td, ds, L, x, rhs, out, part, st);
+    case 3: return launch_jac<3>(g, td, ds, L, x, rhs, out, part, st);
+    case 4: return launch_jac<4>(g, td, ds, L, x, rhs, out, part, st);
     default: return cudaErrorNotSupported;
   }
 }
@@ -1661,6 +2069,17 @@ cudaError_t linearize(const Geom& g, const Model& m, int k1, const double* state
   if (e != cudaSuccess) return e;
   dim3 gf((g.nbf * 4 + 127) / 128, k1);
   PDST_LAUNCH(k_linearize_faces<<<gf, 128, 0, st>>>(g, m, k1, state, etaf, gamf));
+  return cudaGetLastError();
+}
+
+size_t apply_cache_size(const Geom& g, int k1) {
+  return (size_t)jac_tiles_x(g) * jac_tiles_y(g) * k1 * APC_SLOTS * JNT;
+}
+
+cudaError_t apply_cache(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* state,
+                        double* apc, cudaStream_t st) {
+  dim3 grid(jac_tiles_x(g), jac_tiles_y(g), td.k1);
+  PDST_LAUNCH(k_apply_cache<<<grid, JNT, 0, st>>>(g, td, ds, L, td.k1, state, apc));
   return cudaGetLastError();
 }
 

@@ -25,6 +25,16 @@ e1.record(); torch.cuda.synchronize()
 t = e0.elapsed_time(e1) / n * 1e-3
 N = x.numel()
 print(f"{name}: apply {t*1e6:.1f} us  {N/t/1e9:.2f} GDoF/s  N_dof={N}")
+# cold L2: flush (256 MiB write) before every timed apply
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+ts = []
+for _ in range(20):
+    flush.fill_(1)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(); jac.matvec(x, out=y); b.record()
+    torch.cuda.synchronize(); ts.append(a.elapsed_time(b) * 1e3)
+ts.sort()
+print(f"{name}: apply cold-L2 median {ts[len(ts)//2]:.1f} us  min {ts[0]:.1f} us")
 R = slab_residual(ctx, U); torch.cuda.synchronize()
 e0.record()
 for _ in range(n): slab_residual(ctx, U, dev=jac.dev)

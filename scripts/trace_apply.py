@@ -1,0 +1,34 @@
+"""Phase timeline of k_jacobian per CTA (needs a -DPDST_TRACE build via PDST_LIB)."""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_2603_28706_b200 import problem as pb, _lib
+from paper_2603_28706_b200.operators import SlabJacobian
+from paper_2603_28706_b200.synth import CONFIGS, make_slab_inputs
+
+cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "cfg2"]
+params = pb.ModelParams(cfg.p, cfg.delta, cfg.nu, cfg.nu_inf)
+conf = pb.DiscretizationConfig(cfg.gamma1, cfg.gamma2, cfg.gamma_cip)
+syn = make_slab_inputs(cfg)
+ctx = pb.make_context(cfg.nx, cfg.ny, cfg.k, params, cfg.tau, config=conf, v_minus=syn.v_minus)
+U = torch.as_tensor(syn.U, device="cuda"); x = torch.as_tensor(syn.x, device="cuda")
+jac = SlabJacobian(ctx, U, pb.modified_newton(cfg.nu))
+y = torch.empty_like(x)
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+for _ in range(5): jac.matvec(x, out=y)
+flush.fill_(1)
+jac.matvec(x, out=y)
+torch.cuda.synchronize()
+lib = _lib.lib()
+n = ((cfg.nx + 15) // 16) * ((cfg.ny + 15) // 16)
+buf = np.zeros((8192, 16), dtype=np.uint64)
+lib.pdst_debug_trace(buf.ctypes.data_as(ctypes.c_void_p), 8192)
+t = buf[:n].astype(np.float64)
+t0 = t[:, 0].min()
+names = ["start", "staged"] + [f"mu{m}:{p}" for m in range(cfg.k + 1) for p in ("vol", "cip", "mass+sides", "sync1", "assembled")]
+print(f"{n} CTAs; times in us from the first CTA start (min / median / max over CTAs)")
+for i, nm in enumerate(names):
+    c = (t[:, i] - t0) / 1e3
+    print(f"{i:2d} {nm:18s} {c.min():7.1f} {np.median(c):7.1f} {c.max():7.1f}")
+d = (t[:, len(names) - 1] - t[:, 0]) / 1e3
+print("CTA duration min/median/max", d.min(), np.median(d), d.max())
