@@ -1010,26 +1010,22 @@ __device__ __forceinline__ void stage_planned(const StagePlan& sp, const double*
 //     k = 1-3 a~  = sqrt(-wq gamma) (a0, a1, a2),  A = sym grad v = [[a0 a2][a2 a1]]
 //             (gamma <= 0 for 1 < p <= 2, so wq T(B) = e B - (a~ : B) a~)
 //     k = 4-5 wq v (convection)
-//   CIP slots 96 + 4 f + q, faces f = right, top, left, bottom: the face
-//     weight tau w_mu gamma_cip h^2 / hn^2 (w_q h) |v_L . n| of cip_face.
+//   CIP slots 96 + 6 f + e, the cell's right (f = 0) and top (f = 1) faces:
+//     the symmetric 3x3 face matrix W[t][t'] = sum_q c_q B[q][t] B[q][t']
+//     (e = 00 01 02 11 12 22) with the face weight of cip_face
+//     c_q = tau w_mu gamma_cip h^2 / hn^2 (w_q h) |v_L . n|, so the face term
+//     is RD = W J with J the jump of the normal derivative at the 3 face
+//     nodes.  A cell's left / bottom faces are its neighbours' right / top.
 // ---------------------------------------------------------------------------
 constexpr int APC_VOL = 96;
-constexpr int APC_SLOTS = APC_VOL + 16;
-
-// The apply cache streams through a per-thread shared-memory ring of 12
-// doubles (half a Gauss column: 2 points x 6 coefficients), filled with
-// cp.async one half-column ahead of its use.  Each thread touches only its own
-// ring column, so no barrier is involved; a half is copied to registers and
-// used before the refill of the same slots is issued.
-constexpr int RING = 12;
+constexpr int APC_SLOTS = APC_VOL + 12;
 #ifndef PDST_PF_AHEAD
-#define PDST_PF_AHEAD 3  // halves between the L2 prefetch and the use
+#define PDST_PF_AHEAD 2  // half-columns between the L2 prefetch and the use
 #endif
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-// L2 prefetch of half h (further ahead than the ring can hold).
-__device__ __forceinline__ void ring_prefetch_l2(const double* __restrict__ cp, int h) {
+// L2 prefetch of half h (0..7: Gauss column h/2, points 2(h%2), 2(h%2)+1) of
+// a node's cache block; h == 8 is the CIP block.
+__device__ __forceinline__ void apc_prefetch_l2(const double* __restrict__ cp, int h) {
   if (h < 8) {
     const int qx = h >> 1, qy0 = (h & 1) * 2;
 #pragma unroll
@@ -1038,46 +1034,11 @@ __device__ __forceinline__ void ring_prefetch_l2(const double* __restrict__ cp, 
       for (int k = 0; k < 6; ++k) prefetch_l2(cp + (qx * 24 + k * 4 + qy0 + j) * JNT);
   } else if (h == 8) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) prefetch_l2(cp + (APC_VOL + i) * JNT);
+    for (int i = 0; i < 12; ++i) prefetch_l2(cp + (APC_VOL + i) * JNT);
   }
 }
 
-// XOR of the high words of the values just read from the ring.  Passed to the
-// refill's cp.async as an operand, it makes the refill wait until those reads
-// have landed in registers: the write-after-read order on the ring slots is
-// then enforced by the register scoreboard, not by timing.
-template <int N>
-__device__ __forceinline__ unsigned ring_dep(const double* v) {
-  unsigned d = 0;
-#pragma unroll
-  for (int i = 0; i < N; ++i) d ^= (unsigned)__double2hiint(v[i]);
-  return d;
-}
-
-__device__ __forceinline__ void cp_async8_dep(double* dst, const double* src, unsigned dep) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src), "r"(dep) : "memory");
-}
-
-// Issue half h (0..7: Gauss column h/2, points 2(h%2), 2(h%2)+1) of a node's
-// cache block into the ring; h == 8 issues the CIP weights of faces 0-2.
-// `dep` = ring_dep of the values the ring slots held.
-__device__ __forceinline__ void ring_issue(const double* __restrict__ cp, int h, double* ring, unsigned dep) {
-  if (h < 8) {
-    const int qx = h >> 1, qy0 = (h & 1) * 2;
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int k = 0; k < 6; ++k) cp_async8_dep(ring + (j * 6 + k) * JNT, cp + (qx * 24 + k * 4 + qy0 + j) * JNT, dep);
-  } else {
-#pragma unroll
-    for (int i = 0; i < RING; ++i) cp_async8_dep(ring + i * JNT, cp + (APC_VOL + i) * JNT, dep);
-  }
-  cp_async_commit();
-}
-
-// 1-D tables of the apply with the mesh scales folded in (kernel parameter:
-// with the Gauss loops unrolled every entry is an immediate constant operand).
+// 1-D tables of the apply with the mesh scales folded in (kernel parameter).
 struct JTabs {
   double B[4][3];    // L_i(s_q)
   double Gx[4][3];   // L_i'(s_q) / hx
@@ -1085,15 +1046,16 @@ struct JTabs {
   double w[4];       // w_q
   double wyh[4];     // w_q (s_q - 1/2)
   double xh[4];      // s_q - 1/2
+  double cJ[5];      // normal-derivative jump across a face from the 5 node
+                     // lines of the two cells: L'(1) on the left, -L'(0) on the right
 };
 
 // Volume terms (forms.py:589-603) from the apply cache; the first writer of
-// the cell's slot.  On entry half 0 of the node's cache is in flight to the
-// ring; on exit the CIP weights of faces 0-2 are (w3 = face 3 from global).
+// the cell's slot.
 template <class XA>
 __device__ __forceinline__ void jac_volume_cached(const JTabs& T, const Disc& ds, const double* __restrict__ cp,
                                                   const XA& XM, int r0, int c0, const double P[3], double* slot,
-                                                  double* ring, double accp[3], double WT, double w3[4]) {
+                                                  double accp[3], double WT) {
 #pragma unroll 1
   for (int qx = 0; qx < 4; ++qx) {
     double xB[3][2], xG[3][2];
@@ -1107,24 +1069,18 @@ __device__ __forceinline__ void jac_volume_cached(const JTabs& T, const Disc& ds
       }
     double Pa[3][2] = {{0, 0}, {0, 0}, {0, 0}}, Qa[3][2] = {{0, 0}, {0, 0}, {0, 0}};
     const double wxT = T.w[qx] * WT;
-    // pressure along the column: dp(qy) = w_qy A + wyh_qy Bp (times w_qx WT)
+    // pressure along the column: dp(qy) = w_qy pA + wyh_qy pB
     const double pA = wxT * (P[0] + P[1] * T.xh[qx]), pB = wxT * P[2];
     double dv0 = 0.0, dv1 = 0.0;
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
       const int h = 2 * qx + hh;
-      cp_async_wait0();
       double cv[2][6];
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
-        for (int k = 0; k < 6; ++k) cv[j][k] = ring[(j * 6 + k) * JNT];
-      ring_issue(cp, h + 1, ring, ring_dep<12>(&cv[0][0]));
-      ring_prefetch_l2(cp, h + PDST_PF_AHEAD);
-      if (h == 7) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) w3[q] = __ldg(cp + (APC_VOL + 12 + q) * JNT);
-      }
+        for (int k = 0; k < 6; ++k) cv[j][k] = __ldg(cp + (qx * 24 + k * 4 + 2 * hh + j) * JNT);
+      apc_prefetch_l2(cp, h + PDST_PF_AHEAD);
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int qy = 2 * hh + j;
@@ -1181,61 +1137,55 @@ __device__ __forceinline__ void jac_volume_cached(const JTabs& T, const Disc& ds
   }
 }
 
-// CIP face with cached weights w[q] (cip_face with A replaced by the
-// precomputed |v_L . n| weights).
+// CIP face term (forms.py:639-650) with the cached face matrix W:
+// RD = W J, J[t] = jump of the normal derivative at face line t, from the 5
+// staged node lines of the left / lower cell at (rL, cL) and its neighbour.
 template <class FA>
-__device__ __forceinline__ void cip_face_cached(int axis, const FA& F, int rL, int cL, const double w[4],
-                                                double RD[3][2]) {
-  const int rR = axis == 1 ? rL + 2 : rL, cR = axis == 0 ? cL + 2 : cL;
-  double dl[3][2], dr[3][2];
-  line_sums(F, rL, cL, axis, c_tab.dE[1], dl);
-  line_sums(F, rR, cR, axis, c_tab.dE[0], dr);
+__device__ __forceinline__ void cip_face_w(const JTabs& T, int axis, const FA& F, int rL, int cL, const double W[6],
+                                           double RD[3][2]) {
+  double J[3][2];
 #pragma unroll
-  for (int t = 0; t < 3; ++t) {
-    dl[t][0] -= dr[t][0];
-    dl[t][1] -= dr[t][1];
-    RD[t][0] = RD[t][1] = 0.0;
-  }
+  for (int t = 0; t < 3; ++t)
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    double j0 = 0.0, j1 = 0.0;
+    for (int d = 0; d < 2; ++d) {
+      double v = 0.0;
 #pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      j0 = fma(c_tab.B[q][t], dl[t][0], j0);
-      j1 = fma(c_tab.B[q][t], dl[t][1], j1);
+      for (int m = 0; m < 5; ++m) v = fma(T.cJ[m], axis == 0 ? F.at(d, rL + t, cL + m) : F.at(d, rL + m, cL + t), v);
+      J[t][d] = v;
     }
-    const double c0v = w[q] * j0, c1v = w[q] * j1;
 #pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      RD[t][0] = fma(c0v, c_tab.B[q][t], RD[t][0]);
-      RD[t][1] = fma(c1v, c_tab.B[q][t], RD[t][1]);
-    }
+  for (int d = 0; d < 2; ++d) {
+    RD[0][d] = W[0] * J[0][d] + W[1] * J[1][d] + W[2] * J[2][d];
+    RD[1][d] = W[1] * J[0][d] + W[3] * J[1][d] + W[4] * J[2][d];
+    RD[2][d] = W[2] * J[0][d] + W[4] * J[1][d] + W[5] * J[2][d];
   }
 }
 
 // The four CIP faces of a cell (right, top, left, bottom), own side only;
-// w[f][q] = cached weights.
+// W[f] = the faces' matrices (left / bottom from the neighbours' cache).
 template <class FA, class ACC>
-__device__ __forceinline__ void cip_all_cached(const Geom& g, const FA& F, int ci, int cj, int r0, int c0,
-                                               const double (*w)[4], const ACC& acc) {
+__device__ __forceinline__ void cip_all_w(const JTabs& T, const Geom& g, const FA& F, int ci, int cj, int r0, int c0,
+                                          const double (*W)[6], const ACC& acc) {
   double RD[3][2];
   if (ci < g.nx - 1) {
-    cip_face_cached(0, F, r0, c0, w[0], RD);
+    cip_face_w(T, 0, F, r0, c0, W[0], RD);
     cip_scatter(0, true, 1.0, RD, acc);
   }
   if (cj < g.ny - 1) {
-    cip_face_cached(1, F, r0, c0, w[1], RD);
+    cip_face_w(T, 1, F, r0, c0, W[1], RD);
     cip_scatter(1, true, 1.0, RD, acc);
   }
   if (ci > 0) {
-    cip_face_cached(0, F, r0, c0 - 2, w[2], RD);
+    cip_face_w(T, 0, F, r0, c0 - 2, W[2], RD);
     cip_scatter(0, false, 1.0, RD, acc);
   }
   if (cj > 0) {
-    cip_face_cached(1, F, r0 - 2, c0, w[3], RD);
+    cip_face_w(T, 1, F, r0 - 2, c0, W[3], RD);
     cip_scatter(1, false, 1.0, RD, acc);
   }
 }
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 
 // Shared tile-boundary nodes: sum the (2 or 4) tile partials in fixed order.
 template <int T>
@@ -1303,7 +1253,6 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
                                                   const double* __restrict__ ybnd, const JTabs T) {
   double* sacc = g_dsmem + (size_t)K1 * 2 * JPLANE;  // [18][JNT] per-cell node contributions
   // [K1][2][JPLANE] direction x_nu, all Radau nodes (one-cell ring), in front
-  double* ring = sacc + 18 * JNT + threadIdx.x;  // [RING][JNT] apply-cache ring (this thread's column)
   const int bx = blockIdx.x, by = blockIdx.y;
   const int i0 = bx * JT, j0 = by * JT;
   const int X0 = 2 * (i0 - 1), Y0 = 2 * (j0 - 1);
@@ -1326,27 +1275,24 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
 
   TR(0);
   pdl_trigger();  // k_jac_fixup may be scheduled; it waits for this grid
-  if (valid) {
-    ring_issue(cbase, 0, ring, 0u);
-    for (int h = 1; h < PDST_PF_AHEAD; ++h) ring_prefetch_l2(cbase, h);
-  }
-  for (int nu = 0; nu < K1; ++nu) stage_jac_async(g, x + (size_t)nu * g.nd, nu * 2 * JPLANE, X0, Y0);
+  if (valid)
+    for (int h = 0; h < PDST_PF_AHEAD; ++h) apc_prefetch_l2(cbase, h);
+  // x_0 now; the later nodes' planes after the first barrier (their copies
+  // complete during node 0 and are published by its barriers)
+  stage_jac_async(g, x, 0, X0, Y0);
   cp_async_wait_all();  // (commits the staging copies and waits for every group)
   __syncthreads();
   TR(1);
+  for (int nu = 1; nu < K1; ++nu) stage_jac_async(g, x + (size_t)nu * g.nd, nu * 2 * JPLANE, X0, Y0);
+  cp_async_commit();
   for (int mu = 0; mu < K1; ++mu) {
     const double tw = td.tau_w[mu];
     const double* cp = cbase + (size_t)mu * APC_SLOTS * JNT;
     double* slot = sacc + threadIdx.x;
     const JAcc acc{slot};
     const PlaneS XM{mu * 2 * JPLANE};
+    double rv[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};  // rhs of the own 2x2 nodes (defect mode)
     if (valid) {
-      if (rhs) {  // defect mode: pull this cell's rhs rows towards L2 for the assembly
-        const size_t ob = (size_t)mu * g.nd + 2 * ((size_t)(2 * cj) * g.nnx + 2 * ci);
-        prefetch_l2(rhs + ob);
-        prefetch_l2(rhs + ob + 2 * g.nnx);
-        prefetch_l2(rhs + (size_t)mu * g.nd + g.mv + 3 * (size_t)c);
-      }
       double P[3];
       const double* xp = x + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
       P[0] = __ldg(xp);
@@ -1354,21 +1300,25 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
       P[2] = __ldg(xp + 2);
       double accp[3] = {0.0, 0.0, 0.0};
       // tau w_mu J_mu x_mu: volume, boundary sides, CIP faces (weights carry tau w_mu)
-      double w3[4];
       if (!(ds.skip & 1))
-        jac_volume_cached(T, ds, cp, XM, r0, c0, P, slot, ring, accp, g.hx * g.hy * tw, w3);
-      else {
+        jac_volume_cached(T, ds, cp, XM, r0, c0, P, slot, accp, g.hx * g.hy * tw);
+      else
 #pragma unroll
         for (int k = 0; k < 18; ++k) slot[k * JNT] = 0.0;
-        cp_async_wait0();
-        double h0[RING];
-#pragma unroll
-        for (int i = 0; i < RING; ++i) h0[i] = ring[i * JNT];
-        ring_issue(cp, 8, ring, ring_dep<RING>(h0));
-#pragma unroll
-        for (int q = 0; q < 4; ++q) w3[q] = __ldg(cp + (APC_VOL + 12 + q) * JNT);
-      }
       TR(2 + 5 * mu);
+      // defect mode: the right-hand side of this cell's own nodes (lower-left
+      // 2x2) and pressures, loaded now for the assembly
+      double rp[3] = {0, 0, 0};
+      if (rhs) {
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+          const size_t o = (size_t)mu * g.nd + 2 * ((size_t)(2 * cj + (n >> 1)) * g.nnx + 2 * ci + (n & 1));
+          rv[n][0] = __ldg(rhs + o);
+          rv[n][1] = __ldg(rhs + o + 1);
+        }
+#pragma unroll
+        for (int j = 0; j < 3; ++j) rp[j] = __ldg(rhs + (size_t)mu * g.nd + g.mv + 3 * (size_t)c + j);
+      }
       // CIP, temporal mass and boundary sides accumulate in registers (the
       // volume's registers are free now) and reach the slot in one pass
       double ra[3][3][2];
@@ -1377,23 +1327,60 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
 #pragma unroll
         for (int b = 0; b < 3; ++b) ra[a][b][0] = ra[a][b][1] = 0.0;
       const RegAcc racc{ra};
-      {
-        double w[4][4];
-        cp_async_wait0();
+      if (cip && !(ds.skip & 2)) {
+        // face matrices: own right / top, the left / bottom neighbours' right / top
+        double W[4][6];
+        const double* wl = tx > 0 ? cp - 1 : L.apc + ((tile - 1) * K1 + mu) * APC_SLOTS * JNT + ty * JT + JT - 1;
+        const double* wb = ty > 0 ? cp - JT : L.apc + ((tile - jac_tiles_x(g)) * K1 + mu) * APC_SLOTS * JNT + (JT - 1) * JT + tx;
 #pragma unroll
-        for (int i = 0; i < RING; ++i) w[i / 4][i % 4] = ring[i * JNT];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) w[3][q] = w3[q];
-        if (cip && !(ds.skip & 2)) cip_all_cached(g, XM, ci, cj, r0, c0, w, racc);
-        // the next node's first half-column (after the weights are consumed)
-        if (mu + 1 < K1) {
-          ring_issue(cp + APC_SLOTS * JNT, 0, ring, ring_dep<12>(&w[0][0]));
-          for (int h = 1; h < PDST_PF_AHEAD; ++h) ring_prefetch_l2(cp + APC_SLOTS * JNT, h);
+        for (int e = 0; e < 6; ++e) {
+          W[0][e] = __ldg(cp + (APC_VOL + e) * JNT);
+          W[1][e] = __ldg(cp + (APC_VOL + 6 + e) * JNT);
+          W[2][e] = ci > 0 ? __ldg(wl + (APC_VOL + e) * JNT) : 0.0;
+          W[3][e] = cj > 0 ? __ldg(wb + (APC_VOL + 6 + e) * JNT) : 0.0;
         }
+        cip_all_w(T, g, XM, ci, cj, r0, c0, W, racc);
       }
+      if (mu + 1 < K1)  // the next node's first half-columns towards L2
+        for (int h = 0; h < PDST_PF_AHEAD; ++h) apc_prefetch_l2(cp + APC_SLOTS * JNT, h);
       TR(3 + 5 * mu);
       // + M_K sum_nu K_t[mu,nu] x_nu (slab.py:199-200)
-      if (!(ds.skip & 8)) add_mass<K1>(XP, (const PlaneS*)nullptr, 0.0, td.K_t + mu * K1, r0, c0, g.hx * g.hy, racc);
+      // (planes nu <= mu are staged; later nodes' values come from L2)
+      if (!(ds.skip & 8)) {
+        const double* Krow = td.K_t + mu * K1;
+        const double m = g.hx * g.hy;
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj) {  // source row jy'
+          double xt[3][2];
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int d = 0; d < 2; ++d) {
+              double v = 0.0;
+#pragma unroll
+              for (int nu = 0; nu < K1; ++nu) {
+                const double f = nu <= mu ? XP[nu].at(d, r0 + jj, c0 + i)
+                                          : __ldg(x + (size_t)nu * g.nd + 2 * ((size_t)(2 * cj + jj) * g.nnx + 2 * ci + i) + d);
+                v = fma(Krow[nu], f, v);
+              }
+              xt[i][d] = v;
+            }
+          double T1[3][2];
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int d = 0; d < 2; ++d)
+              T1[i][d] = c_tab.M1[i][0] * xt[0][d] + c_tab.M1[i][1] * xt[1][d] + c_tab.M1[i][2] * xt[2][d];
+#pragma unroll
+          for (int jy = 0; jy < 3; ++jy) {
+            const double mm = m * c_tab.M1[jy][jj];
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+#pragma unroll
+              for (int d = 0; d < 2; ++d) ra[jy][i][d] += mm * T1[i][d];
+          }
+        }
+      }
       // boundary sides last: k_boundary_apply (PDL predecessor) has had the
       // whole cell pass to finish
       if (!(ds.skip & 4)) {
@@ -1408,7 +1395,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
           for (int d = 0; d < 2; ++d) acc.add(a, b, d, ra[a][b][d]);
       const size_t o = (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
 #pragma unroll
-      for (int j = 0; j < 3; ++j) out[o + j] = rhs ? rhs[o + j] - accp[j] : accp[j];
+      for (int j = 0; j < 3; ++j) out[o + j] = rhs ? rp[j] - accp[j] : accp[j];
     }
     TR(4 + 5 * mu);
     __syncthreads();
@@ -1426,7 +1413,8 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
       const double* sd_ = sacc + me - JT;
       const double* sld = sacc + me - JT - 1;
       auto at = [&](const double* p, int a, int d) { return p[(2 * a + d) * JNT]; };
-      auto emit = [&](int lx, int ly, double s0, double s1) {
+      // n = own-node index (lower-left 2x2, rhs preloaded) or -1 (tile edge row / column)
+      auto emit = [&](int lx, int ly, double s0, double s1, int n) {
         const bool shx = (lx == 0 && i0 > 0) || (lx == 2 * JT && i0 + JT < g.nx);
         const bool shy = (ly == 0 && j0 > 0) || (ly == 2 * JT && j0 + JT < g.ny);
         if (shx || shy) {
@@ -1436,8 +1424,8 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
         } else {
           const size_t o = base + 2 * ((size_t)(2 * j0 + ly) * g.nnx + 2 * i0 + lx);
           if (rhs) {
-            s0 = __ldg(rhs + o) - s0;
-            s1 = __ldg(rhs + o + 1) - s1;
+            s0 = (n >= 0 ? rv[n][0] : __ldg(rhs + o)) - s0;
+            s1 = (n >= 0 ? rv[n][1] : __ldg(rhs + o + 1)) - s1;
           }
           out[o] = s0;  // (nd may be odd: no 16-byte vector store)
           out[o + 1] = s1;
@@ -1452,39 +1440,39 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
         if (hl) { s0 += at(sl_, 2, 0); s1 += at(sl_, 2, 1); }
         s0 += at(sm_, 0, 0);
         s1 += at(sm_, 0, 1);
-        emit(lx, ly, s0, s1);
+        emit(lx, ly, s0, s1, 0);
       }
       {  // (1,0): down, self
         double s0 = 0.0, s1 = 0.0;
         if (hd) { s0 += at(sd_, 7, 0); s1 += at(sd_, 7, 1); }
         s0 += at(sm_, 1, 0);
         s1 += at(sm_, 1, 1);
-        emit(lx + 1, ly, s0, s1);
+        emit(lx + 1, ly, s0, s1, 1);
       }
       {  // (0,1): left, self
         double s0 = 0.0, s1 = 0.0;
         if (hl) { s0 += at(sl_, 5, 0); s1 += at(sl_, 5, 1); }
         s0 += at(sm_, 3, 0);
         s1 += at(sm_, 3, 1);
-        emit(lx, ly + 1, s0, s1);
+        emit(lx, ly + 1, s0, s1, 2);
       }
-      emit(lx + 1, ly + 1, 0.0 + at(sm_, 4, 0), 0.0 + at(sm_, 4, 1));  // (1,1): self only
+      emit(lx + 1, ly + 1, 0.0 + at(sm_, 4, 0), 0.0 + at(sm_, 4, 1), 3);  // (1,1): self only
       if (lastx) {
         double s0 = 0.0, s1 = 0.0;  // (2,0): down, self
         if (hd) { s0 += at(sd_, 8, 0); s1 += at(sd_, 8, 1); }
         s0 += at(sm_, 2, 0);
         s1 += at(sm_, 2, 1);
-        emit(lx + 2, ly, s0, s1);
-        emit(lx + 2, ly + 1, 0.0 + at(sm_, 5, 0), 0.0 + at(sm_, 5, 1));
+        emit(lx + 2, ly, s0, s1, -1);
+        emit(lx + 2, ly + 1, 0.0 + at(sm_, 5, 0), 0.0 + at(sm_, 5, 1), -1);
       }
       if (lasty) {
         double s0 = 0.0, s1 = 0.0;  // (0,2): left, self
         if (hl) { s0 += at(sl_, 8, 0); s1 += at(sl_, 8, 1); }
         s0 += at(sm_, 6, 0);
         s1 += at(sm_, 6, 1);
-        emit(lx, ly + 2, s0, s1);
-        emit(lx + 1, ly + 2, 0.0 + at(sm_, 7, 0), 0.0 + at(sm_, 7, 1));
-        if (lastx) emit(lx + 2, ly + 2, 0.0 + at(sm_, 8, 0), 0.0 + at(sm_, 8, 1));
+        emit(lx, ly + 2, s0, s1, -1);
+        emit(lx + 1, ly + 2, 0.0 + at(sm_, 7, 0), 0.0 + at(sm_, 7, 1), -1);
+        if (lastx) emit(lx + 2, ly + 2, 0.0 + at(sm_, 8, 0), 0.0 + at(sm_, 8, 1), -1);
       }
     }
     __syncthreads();  // the slots are rewritten by the next node's volume pass
@@ -1843,37 +1831,42 @@ __global__ void __launch_bounds__(JNT) k_apply_cache(Geom g, TimeData td, Disc d
       cq[5 * 4 * JNT] = conv ? wq * v[1] : 0.0;
     }
   }
-  // CIP face weights: right, top (this cell is left / lower), left, bottom
-  // (the neighbour is); zero where the face is not interior.
+  // CIP face matrices of the right and top faces (this cell is the left /
+  // lower one, whose trace gives the weight); zero where not interior.
   const bool cip = ds.convection && ds.gamma_cip > 0.0;
-  for (int f = 0; f < 4; ++f) {
-    const int axis = f & 1;
-    const bool has = f == 0 ? ci < g.nx - 1 : f == 1 ? cj < g.ny - 1 : f == 2 ? ci > 0 : cj > 0;
-    const int lci = f == 2 ? ci - 1 : ci, lcj = f == 3 ? cj - 1 : cj;
-    double* wp = cp + (size_t)(APC_VOL + 4 * f) * JNT;
-    if (!(has && cip)) {
-      for (int q = 0; q < 4; ++q) wp[q * JNT] = 0.0;
-      continue;
+  for (int f = 0; f < 2; ++f) {
+    const int axis = f;
+    const bool has = f == 0 ? ci < g.nx - 1 : cj < g.ny - 1;
+    double* wp = cp + (size_t)(APC_VOL + 6 * f) * JNT;
+    double W[6] = {0, 0, 0, 0, 0, 0};
+    if (has && cip) {
+      const double hface = axis == 0 ? g.hy : g.hx;
+      const double ihn = axis == 0 ? g.ihx : g.ihy;
+      double tr[3];
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        double v = 0.0;
+#pragma unroll
+        for (int n = 0; n < 3; ++n) v = fma(c_tab.E[1][n], axis == 0 ? S.at(0, t, n) : S.at(1, n, t), v);
+        tr[t] = v;
+      }
+      const double coef = tw * ds.gamma_cip * hface * hface * (ihn * ihn);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        double vt = 0.0;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) vt = fma(c_tab.B[q][t], tr[t], vt);
+        const double wq = coef * (c_tab.w[q] * hface) * fabs(vt);
+        W[0] += wq * c_tab.B[q][0] * c_tab.B[q][0];
+        W[1] += wq * c_tab.B[q][0] * c_tab.B[q][1];
+        W[2] += wq * c_tab.B[q][0] * c_tab.B[q][2];
+        W[3] += wq * c_tab.B[q][1] * c_tab.B[q][1];
+        W[4] += wq * c_tab.B[q][1] * c_tab.B[q][2];
+        W[5] += wq * c_tab.B[q][2] * c_tab.B[q][2];
+      }
     }
-    const GlobAcc A{sv, g.nnx, 2 * lci, 2 * lcj};
-    const double hface = axis == 0 ? g.hy : g.hx;
-    const double ihn = axis == 0 ? g.ihx : g.ihy;
-    double tr[3];
 #pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      double v = 0.0;
-#pragma unroll
-      for (int n = 0; n < 3; ++n) v = fma(c_tab.E[1][n], axis == 0 ? A.at(0, t, n) : A.at(1, n, t), v);
-      tr[t] = v;
-    }
-    const double coef = tw * ds.gamma_cip * hface * hface * (ihn * ihn);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      double vt = 0.0;
-#pragma unroll
-      for (int t = 0; t < 3; ++t) vt = fma(c_tab.B[q][t], tr[t], vt);
-      wp[q * JNT] = coef * (c_tab.w[q] * hface) * fabs(vt);
-    }
+    for (int e = 0; e < 6; ++e) wp[e * JNT] = W[e];
   }
 }
 
@@ -1956,7 +1949,7 @@ __global__ void __launch_bounds__(128) k_boundary_matrices(Geom g, Disc ds, Lin 
 
 template <int K1>
 size_t jac_smem() {
-  return ((size_t)2 * K1 * JPLANE + (size_t)JNT * (18 + RING)) * sizeof(double);
+  return ((size_t)2 * K1 * JPLANE + (size_t)JNT * 18) * sizeof(double);
 }
 template <int K1>
 size_t res_smem() {
@@ -1994,6 +1987,11 @@ cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const 
       T.xh[q] = tab.s[q] - 0.5;
       T.wyh[q] = tab.w[q] * (tab.s[q] - 0.5);
     }
+    T.cJ[0] = tab.dE[1][0];
+    T.cJ[1] = tab.dE[1][1];
+    T.cJ[2] = tab.dE[1][2] - tab.dE[0][0];
+    T.cJ[3] = -tab.dE[0][1];
+    T.cJ[4] = -tab.dE[0][2];
   }
   PDST_LAUNCH(e = launch_pdl(k_jacobian<K1>, grid, dim3(JNT), sm, st, g, td, ds, L, x, rhs, out, part,
                              (const double*)ybnd, T));

@@ -35,6 +35,15 @@ for _ in range(20):
     torch.cuda.synchronize(); ts.append(a.elapsed_time(b) * 1e3)
 ts.sort()
 print(f"{name}: apply cold-L2 median {ts[len(ts)//2]:.1f} us  min {ts[0]:.1f} us")
+r = torch.as_tensor(syn.d0, device="cuda")
+ts = []
+for _ in range(20):
+    flush.fill_(1)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(); jac.defect(x, r, out=y); b.record()
+    torch.cuda.synchronize(); ts.append(a.elapsed_time(b) * 1e3)
+ts.sort()
+print(f"{name}: defect cold-L2 median {ts[len(ts)//2]:.1f} us  min {ts[0]:.1f} us")
 R = slab_residual(ctx, U); torch.cuda.synchronize()
 e0.record()
 for _ in range(n): slab_residual(ctx, U, dev=jac.dev)
