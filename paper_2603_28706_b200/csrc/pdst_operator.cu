@@ -1185,8 +1185,6 @@ __device__ __forceinline__ void cip_all_w(const JTabs& T, const Geom& g, const F
   }
 }
 
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-
 // Shared tile-boundary nodes: sum the (2 or 4) tile partials in fixed order.
 template <int T>
 __global__ void k_jac_fixup(Geom g, int k1, const double* __restrict__ part, const double* __restrict__ rhs,
@@ -1242,6 +1240,235 @@ __global__ void k_jac_fixup(Geom g, int k1, const double* __restrict__ part, con
 }
 
 
+// ---------------------------------------------------------------------------
+// Apply epilogue (one kernel, PDL-launched behind k_jacobian): the nodes the
+// tile pass cannot finish alone.
+//   * tile-line nodes (shared by 2 or 4 tiles): sum of the tiles' partials;
+//   * boundary-strip nodes (in a cell with a boundary side) and the pressures
+//     of boundary cells: + the side terms tau w_mu B_f x_loc of every boundary
+//     face whose cell holds the dof, with the precomputed side matrices B_f
+//     (forms.py:605-637 probed once per linearization, k_boundary_matrices).
+// The tile pass writes these dofs without the right-hand side; here
+// y = rhs - s or y = s with s = (interior sum) + (side terms), summed in a
+// fixed order, so apply and defect agree bitwise.  The side products depend
+// only on x and are evaluated before the wait on the tile pass.
+// ---------------------------------------------------------------------------
+__host__ __device__ inline bool in_strip(const Geom& g, int X, int Y) {
+  return X <= 2 || Y <= 2 || X >= g.nnx - 3 || Y >= g.nny - 3;
+}
+__host__ __device__ inline bool on_tile_line(const Geom& g, int X, int Y) {
+  const int ntx = jac_tiles_x(g), nty = jac_tiles_y(g);
+  return (X % (2 * JT) == 0 && X > 0 && X / (2 * JT) < ntx) || (Y % (2 * JT) == 0 && Y > 0 && Y / (2 * JT) < nty);
+}
+
+// Strip node t -> (X, Y): the rows 0-2 and nny-3..nny-1 in full, then the
+// columns 0-2 and nnx-3..nnx-1 of the rows between.
+struct StripIdx {
+  int nb, nt, ncl, ncr;  // bottom rows, top rows, left cols, right cols
+  __host__ __device__ StripIdx(const Geom& g) {
+    nb = min(3, g.nny);
+    nt = min(3, g.nny - nb);
+    ncl = min(3, g.nnx);
+    ncr = min(3, g.nnx - ncl);
+  }
+  __host__ __device__ size_t count(const Geom& g) const {
+    return (size_t)(nb + nt) * g.nnx + (size_t)(g.nny - nb - nt) * (ncl + ncr);
+  }
+  __device__ void node(const Geom& g, size_t t, int& X, int& Y) const {
+    const size_t full = (size_t)(nb + nt) * g.nnx;
+    if (t < full) {
+      const int r = (int)(t / g.nnx);
+      Y = r < nb ? r : g.nny - nt + (r - nb);
+      X = (int)(t % g.nnx);
+    } else {
+      const size_t u = t - full;
+      const int w = ncl + ncr;
+      Y = nb + (int)(u / w);
+      const int cc = (int)(u % w);
+      X = cc < ncl ? cc : g.nnx - ncr + (cc - ncl);
+    }
+  }
+};
+
+// Side terms of the boundary faces at velocity node (X, Y): b[d].
+__device__ void strip_sides(const Geom& g, int k1, int mu, double tw, const double* __restrict__ bmat,
+                            const double* __restrict__ x, int X, int Y, double b[2]) {
+  b[0] = b[1] = 0.0;
+  const double* xm = x + (size_t)mu * g.nd;
+  for (int side = 0; side < 4; ++side) {
+    // cells of this side that contain (X, Y)
+    const bool horiz = side == 0 || side == 2;
+    const int fixed = side == 0 ? 0 : side == 1 ? g.nx - 1 : side == 2 ? g.ny - 1 : 0;
+    const int off = horiz ? Y - 2 * fixed : X - 2 * fixed;  // node offset across the side's cell row
+    if (off < 0 || off > 2) continue;
+    const int along = horiz ? X : Y, ncell = horiz ? g.nx : g.ny;
+    const int lo = max(0, (along - 1) / 2), hi = min(ncell - 1, along / 2);
+    for (int k = lo; k <= hi; ++k) {
+      const int ci = horiz ? k : fixed, cj = horiz ? fixed : k;
+      const int bf = side_offset(g, side) + k;
+      if (g.dirichlet[bf] == kCutSide) continue;
+      const int a = 3 * (Y - 2 * cj) + (X - 2 * ci);
+      const double* B0 = bmat + (size_t)mu * 441 * g.nbf + (size_t)(2 * a) * 21 * g.nbf + bf;
+      const double* B1 = B0 + (size_t)21 * g.nbf;
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int n = 0; n < 9; ++n) {
+        const size_t node = (size_t)(2 * cj + n / 3) * g.nnx + 2 * ci + n % 3;
+        const double x0 = __ldg(xm + 2 * node), x1 = __ldg(xm + 2 * node + 1);
+        s0 = fma(__ldg(B0 + (size_t)(2 * n) * g.nbf), x0, s0);
+        s0 = fma(__ldg(B0 + (size_t)(2 * n + 1) * g.nbf), x1, s0);
+        s1 = fma(__ldg(B1 + (size_t)(2 * n) * g.nbf), x0, s1);
+        s1 = fma(__ldg(B1 + (size_t)(2 * n + 1) * g.nbf), x1, s1);
+      }
+      const double* xp = xm + g.mv + 3 * ((size_t)cj * g.nx + ci);
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        s0 = fma(__ldg(B0 + (size_t)(18 + r) * g.nbf), __ldg(xp + r), s0);
+        s1 = fma(__ldg(B1 + (size_t)(18 + r) * g.nbf), __ldg(xp + r), s1);
+      }
+      b[0] += tw * s0;
+      b[1] += tw * s1;
+    }
+  }
+}
+
+// Sum of the tile partials at tile-line node (X, Y).
+__device__ void tile_partials(const Geom& g, const double* part, int mu, int X, int Y, double s[2]) {
+  const int ntx = jac_tiles_x(g), nty = jac_tiles_y(g);
+  int bxs[2], bys[2], nbx, nby;
+  if (X % (2 * JT) == 0 && X > 0 && X / (2 * JT) < ntx) {
+    bxs[0] = X / (2 * JT) - 1;
+    bxs[1] = X / (2 * JT);
+    nbx = 2;
+  } else {
+    bxs[0] = min(X / (2 * JT), ntx - 1);
+    nbx = 1;
+  }
+  if (Y % (2 * JT) == 0 && Y > 0 && Y / (2 * JT) < nty) {
+    bys[0] = Y / (2 * JT) - 1;
+    bys[1] = Y / (2 * JT);
+    nby = 2;
+  } else {
+    bys[0] = min(Y / (2 * JT), nty - 1);
+    nby = 1;
+  }
+  const size_t ntiles = (size_t)ntx * nty;
+  s[0] = s[1] = 0.0;
+  for (int b = 0; b < nby; ++b)
+    for (int a = 0; a < nbx; ++a) {
+      const int lx = X - 2 * JT * bxs[a], ly = Y - 2 * JT * bys[b];
+      const double* pp = part + (((size_t)mu * ntiles + (size_t)bys[b] * ntx + bxs[a]) * JPER + perim(lx, ly)) * 2;
+      s[0] += pp[0];
+      s[1] += pp[1];
+    }
+}
+
+// Work items per Radau node: strip nodes, then tile-line nodes off the
+// strips, then boundary cells (pressure).
+__global__ void k_jac_post(Geom g, TimeData td, const double* __restrict__ bmat, const double* __restrict__ x,
+                           const double* __restrict__ part, const double* __restrict__ rhs, double* __restrict__ out) {
+  const int mu = blockIdx.y;
+  const double tw = td.tau_w[mu];
+  const StripIdx si(g);
+  const size_t ns = si.count(g);
+  const int ntx = jac_tiles_x(g), nty = jac_tiles_y(g);
+  const size_t nv = (size_t)(ntx - 1) * g.nny, nh = (size_t)(nty - 1) * g.nnx;
+  const size_t ncb = g.nx == 1 || g.ny == 1 ? (size_t)g.ncells : (size_t)2 * g.nx + 2 * (g.ny - 2);
+  size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t base = (size_t)mu * g.nd;
+  if (t < ns) {
+    int X, Y;
+    si.node(g, t, X, Y);
+    double b[2];
+    strip_sides(g, td.k1, mu, tw, bmat, x, X, Y, b);
+    pdl_wait();
+    double s[2];
+    const size_t o = base + 2 * ((size_t)Y * g.nnx + X);
+    if (on_tile_line(g, X, Y)) {
+      tile_partials(g, part, mu, X, Y, s);
+    } else {
+      s[0] = out[o];
+      s[1] = out[o + 1];
+    }
+    s[0] += b[0];
+    s[1] += b[1];
+    out[o] = rhs ? rhs[o] - s[0] : s[0];
+    out[o + 1] = rhs ? rhs[o + 1] - s[1] : s[1];
+    return;
+  }
+  t -= ns;
+  if (t < nv + nh) {
+    int X, Y;
+    if (t < nv) {
+      X = 2 * JT * (int)(t / g.nny + 1);
+      Y = (int)(t % g.nny);
+    } else {
+      const size_t u = t - nv;
+      Y = 2 * JT * (int)(u / g.nnx + 1);
+      X = (int)(u % g.nnx);
+      if (X % (2 * JT) == 0 && X > 0 && X / (2 * JT) < ntx) return;  // on a vertical line
+    }
+    if (in_strip(g, X, Y)) return;
+    pdl_wait();
+    double s[2];
+    tile_partials(g, part, mu, X, Y, s);
+    const size_t o = base + 2 * ((size_t)Y * g.nnx + X);
+    out[o] = rhs ? rhs[o] - s[0] : s[0];
+    out[o + 1] = rhs ? rhs[o + 1] - s[1] : s[1];
+    return;
+  }
+  t -= nv + nh;
+  if (t < ncb) {
+    // boundary cell t: bottom row, top row, then left / right columns between
+    int ci, cj;
+    if (g.nx == 1 || g.ny == 1) {
+      ci = (int)(t % g.nx);
+      cj = (int)(t / g.nx);
+    } else if (t < (size_t)g.nx) {
+      ci = (int)t;
+      cj = 0;
+    } else if (t < (size_t)2 * g.nx) {
+      ci = (int)(t - g.nx);
+      cj = g.ny - 1;
+    } else {
+      const size_t u = t - 2 * g.nx;
+      cj = 1 + (int)(u / 2);
+      ci = (u % 2) ? g.nx - 1 : 0;
+    }
+    const double* xm = x + base;
+    double bp[3] = {0.0, 0.0, 0.0};
+    for (int side = 0; side < 4; ++side) {
+      const bool on = side == 0 ? cj == 0 : side == 1 ? ci == g.nx - 1 : side == 2 ? cj == g.ny - 1 : ci == 0;
+      if (!on) continue;
+      const int bf = side_offset(g, side) + ((side == 0 || side == 2) ? ci : cj);
+      if (g.dirichlet[bf] == kCutSide) continue;
+      for (int r = 0; r < 3; ++r) {
+        const double* Br = bmat + (size_t)mu * 441 * g.nbf + (size_t)(18 + r) * 21 * g.nbf + bf;
+        double sr = 0.0;
+        for (int n = 0; n < 9; ++n) {
+          const size_t node = (size_t)(2 * cj + n / 3) * g.nnx + 2 * ci + n % 3;
+          sr = fma(__ldg(Br + (size_t)(2 * n) * g.nbf), __ldg(xm + 2 * node), sr);
+          sr = fma(__ldg(Br + (size_t)(2 * n + 1) * g.nbf), __ldg(xm + 2 * node + 1), sr);
+        }
+        const double* xp = xm + g.mv + 3 * ((size_t)cj * g.nx + ci);
+        for (int q = 0; q < 3; ++q) sr = fma(__ldg(Br + (size_t)(18 + q) * g.nbf), __ldg(xp + q), sr);
+        bp[r] += tw * sr;
+      }
+    }
+    pdl_wait();
+    const size_t o = base + g.mv + 3 * ((size_t)cj * g.nx + ci);
+    for (int r = 0; r < 3; ++r) {
+      const double s = out[o + r] + bp[r];
+      out[o + r] = rhs ? rhs[o + r] - s : s;
+    }
+  }
+}
+
+__host__ __device__ inline size_t jac_post_items(const Geom& g) {
+  const size_t ncb = g.nx == 1 || g.ny == 1 ? (size_t)g.ncells : (size_t)2 * g.nx + 2 * (g.ny - 2);
+  return StripIdx(g).count(g) + (size_t)(jac_tiles_x(g) - 1) * g.nny + (size_t)(jac_tiles_y(g) - 1) * g.nnx + ncb;
+}
+
 // One thread per cell, two CTAs (16 warps) per SM: the state is not staged —
 // its contribution comes from the apply cache, streamed once per apply — so
 // the CTA holds only the direction planes of all Radau nodes and one set of
@@ -1250,7 +1477,7 @@ template <int K1>
 __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, TimeData td, Disc ds, Lin L,
                                                   const double* __restrict__ x, const double* __restrict__ rhs,
                                                   double* __restrict__ out, double* __restrict__ part,
-                                                  const double* __restrict__ ybnd, const JTabs T) {
+                                                  const JTabs T) {
   double* sacc = g_dsmem + (size_t)K1 * 2 * JPLANE;  // [18][JNT] per-cell node contributions
   // [K1][2][JPLANE] direction x_nu, all Radau nodes (one-cell ring), in front
   const int bx = blockIdx.x, by = blockIdx.y;
@@ -1277,14 +1504,10 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
   pdl_trigger();  // k_jac_fixup may be scheduled; it waits for this grid
   if (valid)
     for (int h = 0; h < PDST_PF_AHEAD; ++h) apc_prefetch_l2(cbase, h);
-  // x_0 now; the later nodes' planes after the first barrier (their copies
-  // complete during node 0 and are published by its barriers)
-  stage_jac_async(g, x, 0, X0, Y0);
+  for (int nu = 0; nu < K1; ++nu) stage_jac_async(g, x + (size_t)nu * g.nd, nu * 2 * JPLANE, X0, Y0);
   cp_async_wait_all();  // (commits the staging copies and waits for every group)
   __syncthreads();
   TR(1);
-  for (int nu = 1; nu < K1; ++nu) stage_jac_async(g, x + (size_t)nu * g.nd, nu * 2 * JPLANE, X0, Y0);
-  cp_async_commit();
   for (int mu = 0; mu < K1; ++mu) {
     const double tw = td.tau_w[mu];
     const double* cp = cbase + (size_t)mu * APC_SLOTS * JNT;
@@ -1345,7 +1568,6 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
         for (int h = 0; h < PDST_PF_AHEAD; ++h) apc_prefetch_l2(cp + APC_SLOTS * JNT, h);
       TR(3 + 5 * mu);
       // + M_K sum_nu K_t[mu,nu] x_nu (slab.py:199-200)
-      // (planes nu <= mu are staged; later nodes' values come from L2)
       if (!(ds.skip & 8)) {
         const double* Krow = td.K_t + mu * K1;
         const double m = g.hx * g.hy;
@@ -1359,9 +1581,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
               double v = 0.0;
 #pragma unroll
               for (int nu = 0; nu < K1; ++nu) {
-                const double f = nu <= mu ? XP[nu].at(d, r0 + jj, c0 + i)
-                                          : __ldg(x + (size_t)nu * g.nd + 2 * ((size_t)(2 * cj + jj) * g.nnx + 2 * ci + i) + d);
-                v = fma(Krow[nu], f, v);
+                v = fma(Krow[nu], XP[nu].at(d, r0 + jj, c0 + i), v);
               }
               xt[i][d] = v;
             }
@@ -1381,12 +1601,6 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
           }
         }
       }
-      // boundary sides last: k_boundary_apply (PDL predecessor) has had the
-      // whole cell pass to finish
-      if (!(ds.skip & 4)) {
-        if (ci == 0 || cj == 0 || ci == g.nx - 1 || cj == g.ny - 1) pdl_wait();  // ybnd of k_boundary_apply
-        jac_sides_pre(g, ybnd, mu, ci, cj, racc, accp, tw);
-      }
 #pragma unroll
       for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -1395,7 +1609,10 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
           for (int d = 0; d < 2; ++d) acc.add(a, b, d, ra[a][b][d]);
       const size_t o = (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
 #pragma unroll
-      for (int j = 0; j < 3; ++j) out[o + j] = rhs ? rp[j] - accp[j] : accp[j];
+      // boundary cells: raw sum, finished (side terms, rhs) by k_jac_post
+      const bool bcell = ci == 0 || cj == 0 || ci == g.nx - 1 || cj == g.ny - 1;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) out[o + j] = (rhs && !bcell) ? rp[j] - accp[j] : accp[j];
     }
     TR(4 + 5 * mu);
     __syncthreads();
@@ -1423,7 +1640,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
           pp[1] = s1;
         } else {
           const size_t o = base + 2 * ((size_t)(2 * j0 + ly) * g.nnx + 2 * i0 + lx);
-          if (rhs) {
+          if (rhs && !in_strip(g, 2 * i0 + lx, 2 * j0 + ly)) {  // strip nodes: k_jac_post
             s0 = (n >= 0 ? rv[n][0] : __ldg(rhs + o)) - s0;
             s1 = (n >= 0 ? rv[n][1] : __ldg(rhs + o + 1)) - s1;
           }
@@ -1967,13 +2184,8 @@ cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const 
     configured = true;
   }
   if (!L.bmat || !L.apc) return cudaErrorInvalidValue;  // built by pdst_linearize
-  double* ybnd = part + (size_t)K1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2;
-  const size_t nb = (size_t)21 * g.nbf;
-  if (!(ds.skip & 32))
-    PDST_LAUNCH(k_boundary_apply<<<dim3((unsigned)((nb + 127) / 128), K1), 128, 0, st>>>(g, K1, L.bmat, x, ybnd));
   dim3 grid(jac_tiles_x(g), jac_tiles_y(g));
   cudaError_t e;
-  // overlaps k_boundary_apply (only the boundary cells wait for it)
   JTabs T;
   {
     static const Tables tab = host_tables();
@@ -1993,13 +2205,13 @@ cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const 
     T.cJ[3] = -tab.dE[0][1];
     T.cJ[4] = -tab.dE[0][2];
   }
-  PDST_LAUNCH(e = launch_pdl(k_jacobian<K1>, grid, dim3(JNT), sm, st, g, td, ds, L, x, rhs, out, part,
-                             (const double*)ybnd, T));
-  if (e != cudaSuccess) return e;
-  const size_t nfix = (size_t)(jac_tiles_x(g) - 1) * g.nny + (size_t)(jac_tiles_y(g) - 1) * g.nnx;
-  if (nfix > 0 && !(ds.skip & 64)) {
-    dim3 fg((unsigned)((nfix + 255) / 256), K1);
-    PDST_LAUNCH(e = launch_pdl(k_jac_fixup<JT>, fg, dim3(256), 0, st, g, K1, (const double*)part, rhs, out));
+  PDST_LAUNCH(k_jacobian<K1><<<grid, JNT, sm, st>>>(g, td, ds, L, x, rhs, out, part, T));
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (!(ds.skip & 64)) {
+    // the epilogue's side products overlap the tile pass (k_jacobian triggers at its start)
+    const size_t n = jac_post_items(g);
+    dim3 pg((unsigned)((n + 127) / 128), K1);
+    PDST_LAUNCH(e = launch_pdl(k_jac_post, pg, dim3(128), 0, st, g, td, L.bmat, x, (const double*)part, rhs, out));
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
@@ -2032,8 +2244,8 @@ extern "C" int pdst_debug_trace(unsigned long long* out, int n) {
 cudaError_t set_tables(const Tables& t) { return cudaMemcpyToSymbol(c_tab, &t, sizeof(Tables)); }
 
 size_t jacobian_scratch(const Geom& g, int k1) {
-  // tile partials, then the boundary-side products
-  return (size_t)k1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2 + (size_t)k1 * 21 * g.nbf;
+  // tile partials
+  return (size_t)k1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2;
 }
 
 cudaError_t jacobian_apply(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* x,
