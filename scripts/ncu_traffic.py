@@ -2,7 +2,7 @@
 
 Runs on the GPU box:
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
-      -k regex:"k_(jac|bound|vanka)" --csv python scripts/prof_step.py cfg2 3 > gpurun_out/traffic.csv
+      -k regex:"k_(jac|vanka)" --csv python scripts/prof_step.py cfg2 3 > gpurun_out/traffic.csv
 then here:  python scripts/ncu_traffic.py gpurun_out/traffic.csv profiles/traffic_r01.json
 """
 import csv
@@ -16,8 +16,8 @@ iK, iN, iV = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Val
 per = defaultdict(lambda: defaultdict(list))
 for r in rows[1:]:
     k = r[iK]
-    name = ("k_jacobian" if "k_jacobian" in k else "k_jac_fixup" if "k_jac_fixup" in k else
-            "k_boundary_apply" if "k_boundary_apply" in k else "k_vanka_gemv" if "gemv" in k else
+    name = ("k_jacobian" if "k_jacobian" in k else "k_jac_post" if "k_jac_post" in k else
+            "k_vanka_gemv" if "gemv" in k else
             "k_vanka_scatter" if "scatter" in k else k[:40])
     per[name][r[iN]].append(float(r[iV].replace(",", "")))
 out = {}
@@ -28,11 +28,11 @@ for name, m in per.items():
     out[name] = {"launches": n, "dram_bytes_per_launch": rd + wr, "read": rd, "write": wr,
                  "ns_per_launch": sum(m["gpu__time_duration.sum"]) / n}
 res = {"kernels": out,
-       "jacobian_apply": sum(out[k]["dram_bytes_per_launch"] for k in ("k_jacobian", "k_jac_fixup", "k_boundary_apply")
+       "jacobian_apply": sum(out[k]["dram_bytes_per_launch"] for k in ("k_jacobian", "k_jac_post")
                              if k in out),
        "vanka_gemv": out.get("k_vanka_gemv", {}).get("dram_bytes_per_launch"),
        "vanka_scatter": out.get("k_vanka_scatter", {}).get("dram_bytes_per_launch"),
        "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum (cold caches, serialized) on "
-                 "scripts/prof_step.py cfg2 3"}
+                 + (sys.argv[3] if len(sys.argv) > 3 else "scripts/prof_step.py cfg2 3")}
 json.dump(res, open(sys.argv[2], "w"), indent=1)
 print(json.dumps(res, indent=1))
