@@ -953,6 +953,8 @@ class StmgOracle:
             lv.invs = np.linalg.inv(lv.mats)
         self.levels = levels
         self.coarse_lu = None  # built on first use (the dense coarse LU is O(N^2) memory)
+        self.coarse_sweeps = None  # set (with coarse_omega) for the iterative coarse solve
+        self.coarse_omega = omega
 
     def _coarse(self):
         lv = self.levels[0]
@@ -978,6 +980,10 @@ class StmgOracle:
 
     def vcycle(self, ell, b):
         if ell == 0:
+            if self.coarse_sweeps is not None:
+                # iterative coarse solve (the product's MgConfig(coarse_solver="vanka"),
+                # no reference counterpart): Vanka steps from zero on the coarsest level
+                return vanka(self.levels[0], np.zeros_like(b), b, self.coarse_sweeps, self.coarse_omega)
             if self.coarse_lu is None:
                 self._coarse()
             return sla.lu_solve(self.coarse_lu, b)

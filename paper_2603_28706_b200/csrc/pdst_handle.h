@@ -138,6 +138,13 @@ struct pdst_handle {
   // multigrid
   std::vector<pdst::Level*> levels;  // 0 = coarsest
   int min_cells = 0;
+  // coarsest-level solve (pdst_set_coarse_solver): 0 dense (the reference's
+  // LU, <= 16384 dofs), 1 `coarse_sweeps` Vanka steps from zero with
+  // `coarse_omega`, 2 dense when it fits else the sweeps
+  int coarse_kind = 0;
+  int coarse_sweeps = 30;
+  double coarse_omega = 0.7;
+  bool coarse_iterative = false;  // resolved at pdst_patches_build
   bool coarse_valid = false;  // Galerkin operators / coarse patches / dense solve built
   bool patches_valid = false;
 

@@ -178,6 +178,10 @@ static LevelOp level_op(pdst_handle* h, int l) {
   return op;
 }
 
+// Build-only / read-back arrays above this many doubles (2 GiB) are released
+// after the build (the large meshes of configs 3 and 5).
+constexpr size_t kKeepMats = (size_t)1 << 28;
+
 static int invert_level_patches(pdst_handle* h, int l, int* badi, int* bad_level, int64_t* bad_patch) {
   Level* lv = h->levels[l];
   const int k1 = h->td.k1, D = 21 * k1;
@@ -270,13 +274,20 @@ int pdst_patches_build(pdst_handle* h, int surrogate, double rep_fraction, int* 
     pa.ET = fl->ecell.ptr;
     pa.state = h->state.ptr;
   }
-  double* mats = fl->mats.ensure(nc * D * D);
-  if (!mats) return set_error(PDST_ECUDA, "out of device memory (patches)");
-  pa.mats = mats;
   // Surrogate patches share one spatial block across the Radau nodes: keep it
   // and invert the temporally diagonalized blocks instead of A_K itself.
   const char* nd_env = getenv("PDST_NO_TIMEDIAG");
   fl->diag = surrogate && !(nd_env && nd_env[0] == '1') && time_diagonalize(k1, h->td.K_t, h->td.tau_w, fl->tdiag);
+  // the full D x D patch matrices are inverted on the exact path; on the
+  // diagonalized path they are kept only for read-back at moderate sizes
+  double* mats = nullptr;
+  if (!fl->diag || nc * D * D <= kKeepMats) {
+    mats = fl->mats.ensure(nc * D * D);
+    if (!mats) return set_error(PDST_ECUDA, "out of device memory (patches)");
+  } else {
+    fl->mats.release();
+  }
+  pa.mats = mats;
   pa.spatial = nullptr;
   if (fl->diag) {
     pa.spatial = fl->spatial.ensure(nc * 441);
@@ -300,17 +311,33 @@ int pdst_patches_build(pdst_handle* h, int surrogate, double rep_fraction, int* 
     lv->diag = false;
     CK(patch_assemble_level(level_op(h, l), h->td, m, h->stream));
     if (int e = invert_level_patches(h, l, badi, bad_level, bad_patch)) return e;
+    if ((size_t)gc.ncells * D * D > kKeepMats) lv->mats.release();  // only the inverses are used
     const size_t n = (size_t)k1 * gc.nd;
     if (!lv->w0.ensure(n) || !lv->w1.ensure(n) || !lv->w2.ensure(n) || !lv->w3.ensure(n))
       return set_error(PDST_ECUDA, "out of device memory (level vectors)");
   }
   h->patches_valid = true;
+  // build-only element data of the finest level (Galerkin input, surrogate
+  // element matrices, the spatial blocks of the diagonalized inverses)
+  if ((size_t)k1 * nc * 441 > kKeepMats) {
+    fl->ecell.release();
+    h->ET.release();
+    if (fl->diag) fl->spatial.release();
+  }
 
-  // ---- coarsest-level dense solve (multigrid.py:494-520) ----
+  // ---- coarsest-level solve (multigrid.py:494-520) ----
   if (multilevel || single_solve) {
     Level* c0 = h->levels[0];
     const int n = k1 * c0->g.nd;
-    if (n > 16384) return set_error(PDST_ENOTSUP, "coarsest level too large for the dense solve (%d dofs)", n);
+    h->coarse_iterative = h->coarse_kind == PDST_COARSE_VANKA || (h->coarse_kind == PDST_COARSE_AUTO && n > 16384);
+    if (h->coarse_iterative) {
+      c0->dense.release();
+      h->coarse_valid = true;
+      return PDST_OK;
+    }
+    if (n > 16384)
+      return set_error(PDST_ENOTSUP, "coarsest level too large for the dense solve (%d dofs); "
+                                     "use pdst_set_coarse_solver", n);
     double* A = c0->dense.ensure((size_t)n * n);
     double* scr = c0->ipiv.ensure((size_t)n / 2 + 2);
     if (!A || !scr) return set_error(PDST_ECUDA, "out of device memory (coarse solve)");
@@ -331,6 +358,7 @@ int pdst_patch_matrices(pdst_handle* h, int level, double* mats) {
   if (int e = check_level(h, level)) return e;
   Level* l = h->levels[level];
   if (!l->D) return set_error(PDST_ESTATE, "patches not built");
+  if (!l->mats.ptr) return set_error(PDST_ESTATE, "patch matrices of level %d are not retained at this size", level);
   CK(cudaSetDevice(h->device));
   const size_t n = (size_t)l->g.ncells * l->D * l->D;
   CK(cudaMemcpyAsync(mats, l->mats.ptr, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
@@ -343,6 +371,7 @@ int pdst_patch_info(pdst_handle* h, int level, int32_t* D, int32_t* diag_blocks,
   if (int e = check_level(h, level)) return e;
   Level* l = h->levels[level];
   if (!l->D) return set_error(PDST_ESTATE, "patches not built");
+  if (!l->mats.ptr) return set_error(PDST_ESTATE, "patch matrices of level %d are not retained at this size", level);
   if (D) *D = l->D;
   if (diag_blocks) *diag_blocks = l->diag ? l->tdiag.nblk : 0;
   if (bytes_per_patch)
@@ -484,6 +513,10 @@ static int vcycle_level(pdst_handle* h, int l, const double* b, double* z, int p
   const int k1 = h->td.k1;
   const size_t n = (size_t)k1 * lv->g.nd;
   if (l == 0) {
+    if (h->coarse_iterative) {  // Vanka steps from zero on the coarsest level
+      CK(cudaMemsetAsync(z, 0, n * sizeof(double), h->stream));
+      return vanka_level(h, 0, z, b, h->coarse_sweeps, h->coarse_omega);
+    }
     CK(dense_solve(lv->dense.ptr, (int)n, b, z, h->stream));
     return PDST_OK;
   }
@@ -499,6 +532,18 @@ static int vcycle_level(pdst_handle* h, int l, const double* b, double* z, int p
   CK(PDST_TIMED(h, PK_TRANSFER, prolong(gc, lv->g, k1, lc->w2.ptr, r, h->stream)));
   CK(axpy(n, 1.0, r, z, h->stream));
   if (int e = vanka_level(h, l, z, b, post, omega)) return e;
+  return PDST_OK;
+}
+
+int pdst_set_coarse_solver(pdst_handle* h, int kind, int sweeps, double omega) {
+  if (!h) return set_error(PDST_EINVAL, "null handle");
+  if (kind < PDST_COARSE_DENSE || kind > PDST_COARSE_AUTO) return set_error(PDST_EINVAL, "unknown coarse solver %d", kind);
+  if (sweeps < 0) return set_error(PDST_EINVAL, "coarse sweeps must be >= 0");
+  if (!(omega > 0.0 && omega <= 1.0)) return set_error(PDST_EINVAL, "coarse omega must lie in (0, 1]");
+  h->coarse_kind = kind;
+  h->coarse_sweeps = sweeps;
+  h->coarse_omega = omega;
+  h->coarse_valid = false;
   return PDST_OK;
 }
 

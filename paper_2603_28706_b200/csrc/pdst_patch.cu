@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(448) k_patch_fine(PatchArgs a) {
   double Js[MAXK1];
   for (int s = 0; s < a.nslot; ++s) Js[s] = spatial_entry(a, s, K, i, j);
   if (a.spatial) a.spatial[(size_t)K * 441 + t] = Js[0];
+  if (!a.mats) return;  // diagonalized path at scale: the spatial block is all the inverse needs
   double* A = a.mats + (size_t)K * D * D;
   for (int mu = 0; mu < k1; ++mu) {
     const double J = Js[a.nslot == 1 ? 0 : mu];

@@ -23,6 +23,8 @@ from .operators import SlabJacobian, _f64, _is_torch
 
 __all__ = ["MgConfig", "StmgPreconditioner", "StmgFactory", "mg_vcycle"]
 
+_COARSE = {"dense": 0, "vanka": 1, "auto": 2}  # pdst_set_coarse_solver kinds
+
 
 @dataclass
 class MgConfig:
@@ -37,10 +39,25 @@ class MgConfig:
     rebuild_factor: float = 2.0
     coarse_mode: str = "galerkin"
     min_cells: int = 4
+    # coarsest-level solve (no reference counterpart beyond "dense", the
+    # reference's LU of the pinned slab system, multigrid.py:494-520): "vanka"
+    # = coarse_sweeps Vanka steps from zero with coarse_omega (default omega) on
+    # the coarsest level's exact patches; "auto" = dense when it fits (16384
+    # dofs), else the sweeps.  SURVEY.md §8 f2: a 5-level hierarchy of a
+    # 2048^2 mesh ends at 128^2 (362,500 dofs).
+    coarse_solver: str = "dense"
+    coarse_sweeps: int = 30
+    coarse_omega: float | None = None
 
     def __post_init__(self):
         if not 0.0 < self.omega <= 1.0:
             raise ValueError("omega must lie in (0, 1]")
+        if self.coarse_solver not in _COARSE:
+            raise ValueError(f"unknown coarse solver {self.coarse_solver!r}")
+        if self.coarse_sweeps < 0:
+            raise ValueError("coarse_sweeps must be >= 0")
+        if self.coarse_omega is not None and not 0.0 < self.coarse_omega <= 1.0:
+            raise ValueError("coarse_omega must lie in (0, 1]")
         if self.coarse_mode not in ("galerkin", "rediscretize"):
             raise ValueError(f"unknown coarse mode {self.coarse_mode!r}")
         if self.coarse_mode == "rediscretize":
@@ -57,6 +74,9 @@ class StmgPreconditioner:
         self.dev = self.jac.dev
         nl = C.c_int(0)
         L.check(L.lib().pdst_hierarchy(self.dev.h, int(self.mg.min_cells), C.byref(nl)), "pdst_hierarchy")
+        cw = self.mg.coarse_omega if self.mg.coarse_omega is not None else self.mg.omega
+        L.check(L.lib().pdst_set_coarse_solver(self.dev.h, _COARSE[self.mg.coarse_solver], int(self.mg.coarse_sweeps),
+                                               float(cw)), "pdst_set_coarse_solver")
         self.num_levels = nl.value
         bl, bp = C.c_int(-1), C.c_int64(-1)
         rc = L.lib().pdst_patches_build(self.dev.h, int(self.mg.surrogate), float(self.mg.rep_fraction),

@@ -104,3 +104,24 @@ def test_vcycle_matches_oracle_sizes():
         x = np.linspace(-1, 1, pre.level_shape(ell)[2])
         assert_close(pre.level_matvec(ell, x), ref.levels[ell].matvec(x), TOL, f"Galerkin L{ell}")
     assert_close(pre.apply(syn.x), ref.apply(syn.x.copy()), VCYCLE_TOL, "V-cycle")
+
+
+@pytest.mark.parametrize("solver,sweeps", [("vanka", 0), ("vanka", 12), ("auto", 12)])
+def test_vcycle_iterative_coarse_solve(solver, sweeps):
+    """MgConfig(coarse_solver=...): the coarsest level solved by Vanka steps
+    from zero — against the oracle V-cycle with the same coarse
+    sweeps; "auto" on a small hierarchy keeps the dense LU."""
+    from test_gpu_operator import _sized_case
+
+    from paper_2603_28706_b200.stmg import MgConfig, StmgPreconditioner
+
+    case, fx, syn = _sized_case(16, 16, 1, "modn")
+    ctx = product_ctx(case, fx)
+    s = oracle_slab(case, fx)
+    ref = orc.StmgOracle(s, syn.U, variant_of(case), omega=0.7, surrogate=True, rep_fraction=0.5, min_cells=4)
+    if solver == "vanka":
+        ref.coarse_sweeps, ref.coarse_omega = sweeps, 0.6
+    mg = MgConfig(rep_fraction=0.5, min_cells=4, coarse_solver=solver, coarse_sweeps=sweeps, coarse_omega=0.6)
+    pre = StmgPreconditioner(ctx, syn.U, product_variant(case), mg)
+    assert pre.num_levels == 3
+    assert_close(pre.apply(syn.x), ref.apply(syn.x.copy()), VCYCLE_TOL, f"V-cycle coarse={solver}/{sweeps}")

@@ -127,3 +127,4 @@ def test_gloo_world2_exchange():
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}
+
