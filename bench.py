@@ -498,6 +498,94 @@ def run_ours(args):
     return 0
 
 
+def run_solve(args):
+    """BASELINE configs[4] workload: one modified-Newton iteration of the slab
+    system, FGMRES preconditioned by the space-time multigrid V-cycle (5
+    geometric levels, 2 + 2 Vanka sweeps, iterative coarsest-level solve),
+    reporting Krylov iterations and the device time per V-cycle.  Not the
+    driver's headline line (that is the default cfg2 step); evidence for
+    DESIGN.md §9."""
+    import numpy as np
+    import torch
+
+    from paper_2603_28706_b200 import problem as pb
+    from paper_2603_28706_b200.errors import SlabSolveError
+    from paper_2603_28706_b200.krylov import KrylovConfig
+    from paper_2603_28706_b200.newton import NewtonConfig, nonlinear_solve_slab
+    from paper_2603_28706_b200.stmg import MgConfig, StmgFactory
+    from paper_2603_28706_b200.synth import CONFIGS, make_slab_inputs
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    cfg = CONFIGS[args.config]
+    params = pb.ModelParams(cfg.p, cfg.delta, cfg.nu, cfg.nu_inf)
+    conf = pb.DiscretizationConfig(cfg.gamma1, cfg.gamma2, cfg.gamma_cip)
+    syn = make_slab_inputs(cfg)
+    ctx = pb.make_context(cfg.nx, cfg.ny, cfg.k, params, cfg.tau, config=conf, v_minus=syn.v_minus)
+    variant = pb.modified_newton(cfg.nu)
+    U0 = torch.as_tensor(syn.U, device=torch.device("cuda", local))
+    min_cells = max(1, cfg.nx >> (args.levels - 1))
+    mg = MgConfig(pre_smooth=2, post_smooth=2, omega=cfg.omega, surrogate=True, rep_fraction=cfg.rep_fraction,
+                  min_cells=min_cells, coarse_solver="auto", coarse_sweeps=args.coarse_sweeps)
+    vc = {"ms": [], "build_s": []}
+
+    class TimedFactory(StmgFactory):
+        def build(self, ctx_, U_, var_):
+            torch.cuda.synchronize()
+            t0 = time.time()
+            pre = super().build(ctx_, U_, var_)
+            torch.cuda.synchronize()
+            vc["build_s"].append(time.time() - t0)
+            vc["levels"] = pre.num_levels
+            inner = pre.apply
+
+            def apply(r, out=None):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                z = inner(r, out=out)
+                b.record()
+                b.synchronize()
+                vc["ms"].append(a.elapsed_time(b))
+                return z
+
+            pre.apply = apply
+            return pre
+
+    newton = NewtonConfig(variant=variant, max_nonlinear=1)
+    krylov = KrylovConfig(restart=args.restart, max_iters=args.max_krylov)
+    torch.cuda.synchronize()
+    t0 = time.time()
+    stats, status, msg = None, "converged", ""
+    try:
+        _, stats = nonlinear_solve_slab(ctx, U0, newton, krylov, TimedFactory(mg), device=local)
+    except SlabSolveError as e:
+        stats, status, msg = e.diagnostics, e.kind, str(e)
+    torch.cuda.synchronize()
+    wall = time.time() - t0
+    st = stats.steps[0] if stats is not None and stats.steps else None
+    N = U0.numel()
+    line = {
+        "metric": "modified-Newton iteration: FGMRES + space-time multigrid V-cycle (Krylov iterations, ms per "
+                  "V-cycle)", "impl": "ours", "n_gpus": 1, "dtype": "f64", "data": "synthetic (synth.py seeded state)",
+        "config": {"workload": f"{cfg.name}: {cfg.nx}x{cfg.ny} Q2/P1disc, DG({cfg.k}), p={cfg.p}, delta={cfg.delta}, "
+                               f"nu_inf={cfg.nu_inf}; {vc.get('levels')} levels (min_cells={min_cells}), 2+2 Vanka "
+                               f"(omega={cfg.omega}, surrogate patches at rep_fraction={cfg.rep_fraction}), coarsest "
+                               f"level: dense LU up to 4096 dofs, else {args.coarse_sweeps} Vanka steps, "
+                               f"FGMRES(restart={args.restart}, budget {args.max_krylov}) in the M-inner product, "
+                               f"Eisenstat-Walker eta0=1e-2",
+                   "n_dof": N},
+        "krylov_iterations": st.n_l if st else len(vc["ms"]), "newton_status": status, "newton_message": msg,
+        "initial_residual": stats.initial_res if stats is not None else None,
+        "residual_before": st.res_before if st else None, "residual_after": st.res_after if st else None,
+        "linear_residual": st.lin_res if st else None, "line_search_lambda": st.lam if st else None,
+        "vcycles": len(vc["ms"]), "ms_per_vcycle": float(np.median(vc["ms"])) if vc["ms"] else None,
+        "vcycle_gdofs": N / (np.median(vc["ms"]) * 1e6) if vc["ms"] else None,
+        "preconditioner_build_s": vc["build_s"], "newton_iteration_wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -508,11 +596,18 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--virtual-ranks", type=int, default=1)
+    ap.add_argument("--solve", action="store_true", help="one Newton iteration with FGMRES + STMG (configs[4])")
+    ap.add_argument("--levels", type=int, default=5)
+    ap.add_argument("--restart", type=int, default=20)
+    ap.add_argument("--max-krylov", type=int, default=60)
+    ap.add_argument("--coarse-sweeps", type=int, default=30)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.solve:
+        return run_solve(args)
     return run_ours(args)
 
 

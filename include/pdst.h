@@ -127,17 +127,22 @@ int pdst_prolong(pdst_handle* h, int fine_level, const double* e_coarse, double*
 int pdst_vcycle(pdst_handle* h, const double* r, double* z, int pre, int post, double omega, int where);
 
 /* Coarsest-level solve of the V-cycle (takes effect at the next
- * pdst_patches_build).  kind: PDST_COARSE_DENSE (the reference's dense LU of
- * the pinned slab system, multigrid.py:494-520; limited to 16384 dofs),
- * PDST_COARSE_VANKA (`sweeps` Vanka steps with `omega` from a zero guess on the
- * coarsest level's exact patches: the iterative coarse solve a 5-level
- * hierarchy of a 2048^2 mesh needs), PDST_COARSE_AUTO (dense
- * when it fits, else the sweeps).  No reference counterpart beyond the dense
- * mode. */
+ * pdst_patches_build).  kind:
+ *   PDST_COARSE_DENSE   the reference's dense LU of the pinned slab system
+ *                       (multigrid.py:494-520), up to 16384 dofs;
+ *   PDST_COARSE_VANKA   `sweeps` Vanka steps with `omega` from a zero guess;
+ *   PDST_COARSE_FGMRES  FGMRES (Euclidean, classical Gram-Schmidt twice) right-
+ *                       preconditioned by `sweeps` Vanka steps from zero, at
+ *                       most `iters` iterations or until the relative residual
+ *                       reaches `rtol`;
+ *   PDST_COARSE_AUTO    dense up to 4096 dofs, else FGMRES.
+ * A 5-level hierarchy of a 2048^2 mesh ends at 128^2 (362,500 dofs), beyond
+ * the dense LU.  No reference counterpart beyond DENSE. */
 #define PDST_COARSE_DENSE 0
 #define PDST_COARSE_VANKA 1
 #define PDST_COARSE_AUTO 2
-int pdst_set_coarse_solver(pdst_handle* h, int kind, int sweeps, double omega);
+#define PDST_COARSE_FGMRES 3
+int pdst_set_coarse_solver(pdst_handle* h, int kind, int sweeps, double omega, int iters, double rtol);
 
 /* Kernel timing for benchmarks: CUDA events around every launch of class
    kernel (0 jacobian/defect, 1 vanka gemv, 2 vanka scatter, 3 residual,

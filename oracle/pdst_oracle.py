@@ -955,6 +955,7 @@ class StmgOracle:
         self.coarse_lu = None  # built on first use (the dense coarse LU is O(N^2) memory)
         self.coarse_sweeps = None  # set (with coarse_omega) for the iterative coarse solve
         self.coarse_omega = omega
+        self.coarse_fgmres = None  # (sweeps, iters, rtol): coarse FGMRES with Vanka preconditioning
 
     def _coarse(self):
         lv = self.levels[0]
@@ -980,6 +981,8 @@ class StmgOracle:
 
     def vcycle(self, ell, b):
         if ell == 0:
+            if self.coarse_fgmres is not None:
+                return self._coarse_fgmres(b, *self.coarse_fgmres)
             if self.coarse_sweeps is not None:
                 # iterative coarse solve (the product's MgConfig(coarse_solver="vanka"),
                 # no reference counterpart): Vanka steps from zero on the coarsest level
@@ -996,6 +999,51 @@ class StmgOracle:
         e = self.vcycle(ell - 1, rc)
         d = d + (P @ e.reshape(k1, -1).T).T.reshape(-1)
         return vanka(lv, d, b, self.post, self.omega)
+
+    def _coarse_fgmres(self, b, sweeps, iters, rtol):
+        """Restatement of the product's coarsest-level FGMRES (csrc/pdst_mg.cu
+        coarse_fgmres): right preconditioning by `sweeps` Vanka steps from zero,
+        Euclidean, classical Gram-Schmidt twice, Givens rotations."""
+        lv = self.levels[0]
+        beta = float(np.sqrt(b @ b))
+        if not beta > 0.0:
+            return np.zeros_like(b)
+        V = [b / beta]
+        Z = []
+        H = np.zeros((iters + 1, iters))
+        cs, sn = np.zeros(iters), np.zeros(iters)
+        g = np.zeros(iters + 1)
+        g[0] = beta
+        k = 0
+        for j in range(iters):
+            z = vanka(lv, np.zeros_like(b), V[j], sweeps, self.coarse_omega)
+            Z.append(z)
+            w = lv.matvec(z)
+            Vm = np.array(V)
+            for _ in range(2):
+                hc = Vm @ w
+                w = w - Vm.T @ hc
+                H[: j + 1, j] += hc
+            hn = float(np.sqrt(w @ w))
+            H[j + 1, j] = hn
+            if hn > 0.0:
+                V.append(w / hn)
+            for i in range(j):
+                a, c = H[i, j], H[i + 1, j]
+                H[i, j], H[i + 1, j] = cs[i] * a + sn[i] * c, -sn[i] * a + cs[i] * c
+            a, c = H[j, j], H[j + 1, j]
+            r = float(np.hypot(a, c))
+            cs[j], sn[j] = (a / r, c / r) if r > 0.0 else (1.0, 0.0)
+            H[j, j], H[j + 1, j] = r, 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            k = j + 1
+            if abs(g[j + 1]) <= rtol * beta or not hn > 0.0:
+                break
+        y = np.zeros(k)
+        for i in range(k - 1, -1, -1):
+            y[i] = (g[i] - H[i, i + 1:k] @ y[i + 1:]) / H[i, i] if H[i, i] != 0.0 else 0.0
+        return np.array(Z[:k]).T @ y
 
     def apply(self, r):
         z = self.vcycle(len(self.levels) - 1, r)

@@ -74,7 +74,7 @@ SIGNATURES = {
     "pdst_restrict": [P, I, P, P, I],
     "pdst_prolong": [P, I, P, P, I],
     "pdst_vcycle": [P, P, P, I, I, D, I],
-    "pdst_set_coarse_solver": [P, I, I, D],
+    "pdst_set_coarse_solver": [P, I, I, D, I, D],
     "pdst_profile": [P, I],
     "pdst_profile_read": [P, I, C.POINTER(D), C.POINTER(I64)],
     "pdst_last_error": [],

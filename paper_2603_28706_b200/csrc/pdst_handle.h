@@ -51,6 +51,9 @@ struct Level {
   DeviceBuffer ipiv;
   // work vectors (k1 * nd each)
   DeviceBuffer w0, w1, w2, w3;
+  // coarsest-level FGMRES: basis V [(m+1) n], preconditioned directions Z [m n],
+  // work vector, reduction scratch
+  DeviceBuffer kv, kz, kw, ks;
   ~Level() {
     if (dirichlet) cudaFree(dirichlet);
   }
@@ -140,10 +143,13 @@ struct pdst_handle {
   int min_cells = 0;
   // coarsest-level solve (pdst_set_coarse_solver): 0 dense (the reference's
   // LU, <= 16384 dofs), 1 `coarse_sweeps` Vanka steps from zero with
-  // `coarse_omega`, 2 dense when it fits else the sweeps
+  // `coarse_omega`, 2 dense up to 4096 dofs else FGMRES, 3 FGMRES
+  // right-preconditioned by `coarse_sweeps` Vanka steps
   int coarse_kind = 0;
   int coarse_sweeps = 30;
   double coarse_omega = 0.7;
+  int coarse_iters = 30;        // FGMRES iteration cap (PDST_COARSE_FGMRES)
+  double coarse_rtol = 1.0e-6;  // FGMRES relative residual target
   bool coarse_iterative = false;  // resolved at pdst_patches_build
   bool coarse_valid = false;  // Galerkin operators / coarse patches / dense solve built
   bool patches_valid = false;

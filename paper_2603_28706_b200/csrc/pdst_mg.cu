@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -329,7 +330,10 @@ int pdst_patches_build(pdst_handle* h, int surrogate, double rep_fraction, int* 
   if (multilevel || single_solve) {
     Level* c0 = h->levels[0];
     const int n = k1 * c0->g.nd;
-    h->coarse_iterative = h->coarse_kind == PDST_COARSE_VANKA || (h->coarse_kind == PDST_COARSE_AUTO && n > 16384);
+    // (auto: the single-CTA Gauss-Jordan inverse is O(n^3) on one SM, seconds
+    // beyond a few thousand dofs)
+    h->coarse_iterative = h->coarse_kind == PDST_COARSE_VANKA || h->coarse_kind == PDST_COARSE_FGMRES ||
+                          (h->coarse_kind == PDST_COARSE_AUTO && n > 4096);
     if (h->coarse_iterative) {
       c0->dense.release();
       h->coarse_valid = true;
@@ -507,15 +511,106 @@ int pdst_prolong(pdst_handle* h, int fine_level, const double* e_coarse, double*
   return transfer_common(h, fine_level, e_coarse, e_fine, where, true);
 }
 
+// Coarsest-level FGMRES: z ~ A_0^-1 b with right preconditioning by
+// `coarse_sweeps` Vanka steps from zero, Euclidean inner product, classical
+// Gram-Schmidt applied twice (multi-dot + fused update), Givens rotations on
+// the host; stops after `coarse_iters` iterations or at relative residual
+// `coarse_rtol`.  Deterministic (fixed reduction trees).
+static int coarse_fgmres(pdst_handle* h, const double* b, double* z) {
+  Level* lv = h->levels[0];
+  const size_t n = (size_t)h->td.k1 * lv->g.nd;
+  const int m = h->coarse_iters;
+  double* V = lv->kv.ensure((size_t)(m + 1) * n);
+  double* Z = lv->kz.ensure((size_t)m * n);
+  double* w = lv->kw.ensure(n);
+  const size_t nred = std::max(multidot_scratch(m + 1), (size_t)reduce_partials());
+  double* sc = lv->ks.ensure(nred + 2 * (size_t)(m + 2));
+  if (!V || !Z || !w || !sc) return set_error(PDST_ECUDA, "out of device memory (coarse FGMRES)");
+  double* part = sc;
+  double* dvec = sc + nred;  // device coefficients (m + 2)
+  auto sync_read = [&](double* host, const double* dev, int cnt) -> int {
+    CK(cudaMemcpyAsync(host, dev, (size_t)cnt * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return PDST_OK;
+  };
+  auto norm2 = [&](const double* v, double* out) -> int {
+    CK(dot(v, v, n, part, dvec, h->stream));
+    double s2 = 0.0;
+    if (int e = sync_read(&s2, dvec, 1)) return e;
+    *out = std::sqrt(s2);
+    return PDST_OK;
+  };
+  CK(cudaMemsetAsync(z, 0, n * sizeof(double), h->stream));
+  double beta = 0.0;
+  if (int e = norm2(b, &beta)) return e;
+  if (!(beta > 0.0)) return PDST_OK;
+  CK(cudaMemsetAsync(V, 0, n * sizeof(double), h->stream));
+  CK(axpy(n, 1.0 / beta, b, V, h->stream));
+  std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1, 0.0), hc(m + 1);
+  g[0] = beta;
+  int k = 0;
+  for (int j = 0; j < m; ++j) {
+    double* Vj = V + (size_t)j * n;
+    double* Zj = Z + (size_t)j * n;
+    CK(cudaMemsetAsync(Zj, 0, n * sizeof(double), h->stream));
+    if (int e = vanka_level(h, 0, Zj, Vj, h->coarse_sweeps, h->coarse_omega)) return e;
+    CK(PDST_TIMED(h, PK_LEVEL, level_apply(level_op(h, 0), h->td, Zj, nullptr, w, h->stream)));
+    for (int pass = 0; pass < 2; ++pass) {  // CGS2
+      CK(multidot(V, (int64_t)n, j + 1, w, (int64_t)n, part, dvec, h->stream));
+      CK(multi_axpy(V, nullptr, (int64_t)n, j + 1, dvec, w, nullptr, (int64_t)n, h->stream));
+      if (int e = sync_read(hc.data(), dvec, j + 1)) return e;
+      for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] += hc[i];
+    }
+    double hn = 0.0;
+    if (int e = norm2(w, &hn)) return e;
+    H[(size_t)(j + 1) * m + j] = hn;
+    if (hn > 0.0) {
+      double* Vn = V + (size_t)(j + 1) * n;
+      CK(cudaMemsetAsync(Vn, 0, n * sizeof(double), h->stream));
+      CK(axpy(n, 1.0 / hn, w, Vn, h->stream));
+    }
+    for (int i = 0; i < j; ++i) {  // previous rotations on column j
+      const double a = H[(size_t)i * m + j], c = H[(size_t)(i + 1) * m + j];
+      H[(size_t)i * m + j] = cs[i] * a + sn[i] * c;
+      H[(size_t)(i + 1) * m + j] = -sn[i] * a + cs[i] * c;
+    }
+    const double a = H[(size_t)j * m + j], c = H[(size_t)(j + 1) * m + j];
+    const double r = std::hypot(a, c);
+    cs[j] = r > 0.0 ? a / r : 1.0;
+    sn[j] = r > 0.0 ? c / r : 0.0;
+    H[(size_t)j * m + j] = r;
+    H[(size_t)(j + 1) * m + j] = 0.0;
+    g[j + 1] = -sn[j] * g[j];
+    g[j] = cs[j] * g[j];
+    k = j + 1;
+    if (std::fabs(g[j + 1]) <= h->coarse_rtol * beta || !(hn > 0.0)) break;
+  }
+  // y = H^-1 g (upper triangular k x k), z = Z y
+  std::vector<double> y(k, 0.0);
+  for (int i = k - 1; i >= 0; --i) {
+    double s = g[i];
+    for (int l2 = i + 1; l2 < k; ++l2) s -= H[(size_t)i * m + l2] * y[l2];
+    y[i] = H[(size_t)i * m + i] != 0.0 ? s / H[(size_t)i * m + i] : 0.0;
+  }
+  for (int i = 0; i < k; ++i) y[i] = -y[i];  // multi_axpy subtracts
+  CK(cudaMemcpyAsync(dvec, y.data(), (size_t)k * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  CK(multi_axpy(Z, nullptr, (int64_t)n, k, dvec, z, nullptr, (int64_t)n, h->stream));
+  CK(cudaStreamSynchronize(h->stream));  // y lives on the host stack
+  return PDST_OK;
+}
+
 // One V-cycle on level l with zero initial guess: z = V_l b (multigrid.py:545-555).
 static int vcycle_level(pdst_handle* h, int l, const double* b, double* z, int pre, int post, double omega) {
   Level* lv = h->levels[l];
   const int k1 = h->td.k1;
   const size_t n = (size_t)k1 * lv->g.nd;
   if (l == 0) {
-    if (h->coarse_iterative) {  // Vanka steps from zero on the coarsest level
-      CK(cudaMemsetAsync(z, 0, n * sizeof(double), h->stream));
-      return vanka_level(h, 0, z, b, h->coarse_sweeps, h->coarse_omega);
+    if (h->coarse_iterative) {
+      if (h->coarse_kind == PDST_COARSE_VANKA) {  // Vanka steps from zero on the coarsest level
+        CK(cudaMemsetAsync(z, 0, n * sizeof(double), h->stream));
+        return vanka_level(h, 0, z, b, h->coarse_sweeps, h->coarse_omega);
+      }
+      return coarse_fgmres(h, b, z);
     }
     CK(dense_solve(lv->dense.ptr, (int)n, b, z, h->stream));
     return PDST_OK;
@@ -535,14 +630,18 @@ static int vcycle_level(pdst_handle* h, int l, const double* b, double* z, int p
   return PDST_OK;
 }
 
-int pdst_set_coarse_solver(pdst_handle* h, int kind, int sweeps, double omega) {
+int pdst_set_coarse_solver(pdst_handle* h, int kind, int sweeps, double omega, int iters, double rtol) {
   if (!h) return set_error(PDST_EINVAL, "null handle");
-  if (kind < PDST_COARSE_DENSE || kind > PDST_COARSE_AUTO) return set_error(PDST_EINVAL, "unknown coarse solver %d", kind);
+  if (kind < PDST_COARSE_DENSE || kind > PDST_COARSE_FGMRES) return set_error(PDST_EINVAL, "unknown coarse solver %d", kind);
   if (sweeps < 0) return set_error(PDST_EINVAL, "coarse sweeps must be >= 0");
   if (!(omega > 0.0 && omega <= 1.0)) return set_error(PDST_EINVAL, "coarse omega must lie in (0, 1]");
+  if (iters < 1 || iters > 1000) return set_error(PDST_EINVAL, "coarse FGMRES iterations must lie in [1, 1000]");
+  if (!(rtol >= 0.0)) return set_error(PDST_EINVAL, "coarse rtol must be >= 0");
   h->coarse_kind = kind;
   h->coarse_sweeps = sweeps;
   h->coarse_omega = omega;
+  h->coarse_iters = iters;
+  h->coarse_rtol = rtol;
   h->coarse_valid = false;
   return PDST_OK;
 }

@@ -23,7 +23,7 @@ from .operators import SlabJacobian, _f64, _is_torch
 
 __all__ = ["MgConfig", "StmgPreconditioner", "StmgFactory", "mg_vcycle"]
 
-_COARSE = {"dense": 0, "vanka": 1, "auto": 2}  # pdst_set_coarse_solver kinds
+_COARSE = {"dense": 0, "vanka": 1, "auto": 2, "fgmres": 3}  # pdst_set_coarse_solver kinds
 
 
 @dataclass
@@ -40,22 +40,28 @@ class MgConfig:
     coarse_mode: str = "galerkin"
     min_cells: int = 4
     # coarsest-level solve (no reference counterpart beyond "dense", the
-    # reference's LU of the pinned slab system, multigrid.py:494-520): "vanka"
-    # = coarse_sweeps Vanka steps from zero with coarse_omega (default omega) on
-    # the coarsest level's exact patches; "auto" = dense when it fits (16384
-    # dofs), else the sweeps.  SURVEY.md §8 f2: a 5-level hierarchy of a
-    # 2048^2 mesh ends at 128^2 (362,500 dofs).
+    # reference's LU of the pinned slab system, multigrid.py:494-520):
+    #   "vanka"  coarse_sweeps Vanka steps from zero with coarse_omega (default omega);
+    #   "fgmres" FGMRES right-preconditioned by coarse_sweeps Vanka steps, at most
+    #            coarse_iters iterations or relative residual coarse_rtol;
+    #   "auto"   dense up to 4096 dofs, else "fgmres".
+    # a 5-level hierarchy of a 2048^2 mesh ends at 128^2
+    # (362,500 dofs), beyond the dense LU.
     coarse_solver: str = "dense"
-    coarse_sweeps: int = 30
+    coarse_sweeps: int | None = None  # default 30 ("vanka") / 2 ("fgmres", "auto")
     coarse_omega: float | None = None
+    coarse_iters: int = 30
+    coarse_rtol: float = 1.0e-6
 
     def __post_init__(self):
         if not 0.0 < self.omega <= 1.0:
             raise ValueError("omega must lie in (0, 1]")
         if self.coarse_solver not in _COARSE:
             raise ValueError(f"unknown coarse solver {self.coarse_solver!r}")
-        if self.coarse_sweeps < 0:
+        if self.coarse_sweeps is not None and self.coarse_sweeps < 0:
             raise ValueError("coarse_sweeps must be >= 0")
+        if not 1 <= self.coarse_iters <= 1000 or not self.coarse_rtol >= 0.0:
+            raise ValueError("coarse_iters must lie in [1, 1000] and coarse_rtol be >= 0")
         if self.coarse_omega is not None and not 0.0 < self.coarse_omega <= 1.0:
             raise ValueError("coarse_omega must lie in (0, 1]")
         if self.coarse_mode not in ("galerkin", "rediscretize"):
@@ -74,9 +80,11 @@ class StmgPreconditioner:
         self.dev = self.jac.dev
         nl = C.c_int(0)
         L.check(L.lib().pdst_hierarchy(self.dev.h, int(self.mg.min_cells), C.byref(nl)), "pdst_hierarchy")
-        cw = self.mg.coarse_omega if self.mg.coarse_omega is not None else self.mg.omega
-        L.check(L.lib().pdst_set_coarse_solver(self.dev.h, _COARSE[self.mg.coarse_solver], int(self.mg.coarse_sweeps),
-                                               float(cw)), "pdst_set_coarse_solver")
+        mg = self.mg
+        cw = mg.coarse_omega if mg.coarse_omega is not None else mg.omega
+        sw = mg.coarse_sweeps if mg.coarse_sweeps is not None else (30 if mg.coarse_solver == "vanka" else 2)
+        L.check(L.lib().pdst_set_coarse_solver(self.dev.h, _COARSE[mg.coarse_solver], int(sw), float(cw),
+                                               int(mg.coarse_iters), float(mg.coarse_rtol)), "pdst_set_coarse_solver")
         self.num_levels = nl.value
         bl, bp = C.c_int(-1), C.c_int64(-1)
         rc = L.lib().pdst_patches_build(self.dev.h, int(self.mg.surrogate), float(self.mg.rep_fraction),

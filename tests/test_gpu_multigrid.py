@@ -125,3 +125,22 @@ def test_vcycle_iterative_coarse_solve(solver, sweeps):
     pre = StmgPreconditioner(ctx, syn.U, product_variant(case), mg)
     assert pre.num_levels == 3
     assert_close(pre.apply(syn.x), ref.apply(syn.x.copy()), VCYCLE_TOL, f"V-cycle coarse={solver}/{sweeps}")
+
+
+@pytest.mark.parametrize("iters,rtol", [(3, 0.0), (25, 1e-6)])
+def test_vcycle_coarse_fgmres(iters, rtol):
+    """MgConfig(coarse_solver="fgmres"): coarsest level by FGMRES right-preconditioned
+    with 2 Vanka steps (CGS2, Givens) — against the oracle's restatement."""
+    from test_gpu_operator import _sized_case
+
+    from paper_2603_28706_b200.stmg import MgConfig, StmgPreconditioner
+
+    case, fx, syn = _sized_case(16, 16, 1, "modn")
+    ctx = product_ctx(case, fx)
+    s = oracle_slab(case, fx)
+    ref = orc.StmgOracle(s, syn.U, variant_of(case), omega=0.7, surrogate=True, rep_fraction=0.5, min_cells=4)
+    ref.coarse_fgmres, ref.coarse_omega = (2, iters, rtol), 0.7
+    mg = MgConfig(rep_fraction=0.5, min_cells=4, coarse_solver="fgmres", coarse_sweeps=2, coarse_iters=iters,
+                  coarse_rtol=rtol)
+    pre = StmgPreconditioner(ctx, syn.U, product_variant(case), mg)
+    assert_close(pre.apply(syn.x), ref.apply(syn.x.copy()), 1e-8, f"V-cycle coarse fgmres {iters}/{rtol}")
