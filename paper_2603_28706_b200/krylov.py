@@ -90,10 +90,17 @@ class _Block:
                 "pdst_multi_axpy")
 
 
-def fgmres(op, rhs, tol: float, config: KrylovConfig | None = None, precond=None, mass=None, x0=None) -> FgmresResult:
+def fgmres(op, rhs, tol: float, config: KrylovConfig | None = None, precond=None, mass=None, x0=None,
+           comm=None) -> FgmresResult:
     """Solve op(x) = rhs to a relative tolerance in the M-weighted norm
     (krylov.py:46-139).  The iteration count is the number of preconditioned
-    operator applications."""
+    operator applications.
+
+    comm (partition.DistComm): the vectors are one rank's part of a
+    distributed slab vector whose non-owned (ghost) entries are zero; every
+    inner product is the local Euclidean product (with M applied through
+    `mass`, itself halo-aware) summed over the ranks by comm.allreduce_ —
+    one allreduce of a (j+1)-vector per Gram-Schmidt pass."""
     torch = _torch()
     config = config or KrylovConfig()
     dev = _owner_dev(mass, op, precond)
@@ -130,7 +137,11 @@ def fgmres(op, rhs, tol: float, config: KrylovConfig | None = None, precond=None
     scal = torch.empty(1, dtype=torch.float64, device=device)
 
     def mdot(a, b_):
-        if mass is None:
+        if comm is not None:  # <a, M b> = sum over ranks of the owned a . (M b)
+            mb = apply_mass(b_, torch.empty_like(b_)) if mass is not None else b_
+            L.check(L.lib().pdst_dot(dev.h, L.vptr(a), L.vptr(mb), n, L.vptr(scal), L.DEVICE), "pdst_dot")
+            comm.allreduce_(scal)
+        elif mass is None:
             L.check(L.lib().pdst_dot(dev.h, L.vptr(a), L.vptr(b_), n, L.vptr(scal), L.DEVICE), "pdst_dot")
         else:
             L.check(L.lib().pdst_mass_dot(dev.h, L.vptr(a), L.vptr(b_), L.vptr(scal), L.DEVICE), "pdst_mass_dot")
@@ -202,6 +213,8 @@ def fgmres(op, rhs, tol: float, config: KrylovConfig | None = None, precond=None
             # vector is mis-scaled), then w -= V h, mw -= MV h (one fused update)
             for p in range(2):
                 MV.dots(j + 1, w, hdev[: j + 1])
+                if comm is not None:
+                    comm.allreduce_(hdev[: j + 1])
                 c = hdev[: j + 1].cpu().numpy()
                 h = np.empty(j + 1)
                 for i in range(j + 1):
@@ -209,7 +222,7 @@ def fgmres(op, rhs, tol: float, config: KrylovConfig | None = None, precond=None
                 H[: j + 1, j] += h
                 hdev[: j + 1].copy_(torch.from_numpy(h))
                 V.sub(j + 1, hdev[: j + 1], w, MV, mw)
-            hh2 = mdot_plain(dev, w, mw, n, scal)
+            hh2 = mdot_plain(dev, w, mw, n, scal, comm)
             hh = float(np.sqrt(max(hh2, 0.0)))
             H[j + 1, j] = hh
             total_iters += 1
@@ -220,6 +233,8 @@ def fgmres(op, rhs, tol: float, config: KrylovConfig | None = None, precond=None
                 mw.mul_(1.0 / hh)
                 if j + 1 < m:  # Gram row of the new basis vector: G[j+1, l] = <MV_{j+1}, V_l>
                     V.dots(j + 1, mw, hdev[: j + 1])
+                    if comm is not None:
+                        comm.allreduce_(hdev[: j + 1])
                     G[j + 1, : j + 1] = hdev[: j + 1].cpu().numpy()
             for i in range(j):
                 t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
@@ -255,7 +270,9 @@ def _accepts_out(fn):
         return False
 
 
-def mdot_plain(dev, a, b, n, scal):
+def mdot_plain(dev, a, b, n, scal, comm=None):
     """Euclidean <a, b> on the device (the Arnoldi norm <w, M w>, krylov.py:109)."""
     L.check(L.lib().pdst_dot(dev.h, L.vptr(a), L.vptr(b), n, L.vptr(scal), L.DEVICE), "pdst_dot")
+    if comm is not None:
+        comm.allreduce_(scal)
     return float(scal.item())

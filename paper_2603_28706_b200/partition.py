@@ -31,7 +31,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["StripPartition", "RankLayout", "LocalTransport", "TorchDistTransport", "DistributedSlab"]
+__all__ = ["StripPartition", "RankLayout", "LocalTransport", "TorchDistTransport", "DistributedSlab", "DistComm",
+           "distributed_fgmres"]
 
 CUT = 2
 
@@ -222,9 +223,12 @@ class TorchDistTransport:
         if isinstance(vec, (list, tuple)):  # the distributed_* helpers pass one vector per local rank
             (vec,) = vec
         lay = self.lay
+        # gloo moves host tensors only: stage device slices through the host
+        xdev = vec.device if self.dist.get_backend() == "gloo" else None
+        bdev = torch.device("cpu") if xdev is not None and xdev.type == "cuda" else vec.device
         ops, recv_bufs = [], []
         for peer, mine, _ in getattr(lay, plan_name)():
-            buf = torch.empty((k1, mine.stop - mine.start), dtype=vec.dtype, device=vec.device)
+            buf = torch.empty((k1, mine.stop - mine.start), dtype=vec.dtype, device=bdev)
             recv_bufs.append((mine, buf))
             ops.append(self.dist.P2POp(self.dist.irecv, buf, peer))
         # what my neighbours receive from me
@@ -236,12 +240,13 @@ class TorchDistTransport:
                 if src_rank != lay.rank:
                     continue
                 v2 = vec.view(k1, lay.nd_loc)
-                ops.append(self.dist.P2POp(self.dist.isend, v2[:, theirs].contiguous(), peer))
+                ops.append(self.dist.P2POp(self.dist.isend, v2[:, theirs].contiguous().to(bdev), peer))
         if ops:
             for req in self.dist.batch_isend_irecv(ops):
                 req.wait()
         v2 = vec.view(k1, lay.nd_loc)
         for mine, buf in recv_bufs:
+            buf = buf.to(vec.device)
             if add:
                 v2[:, mine] += buf
             else:
@@ -333,3 +338,100 @@ def distributed_vanka_step(ranks, ds, rs, omega, transport):
     for d, inc in zip(ds, incs):
         d += inc
     return ds
+
+
+# ---------------------------------------------------------------------------
+# Distributed Krylov (FGMRES in the M-inner product with allreduced dots)
+# ---------------------------------------------------------------------------
+
+
+class DistComm:
+    """Sum-allreduce of device (or host) tensors over a torch.distributed group
+    (NCCL between GPUs; gloo staged through the host)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.host = dist.get_backend(group) == "gloo"
+
+    def allreduce_(self, t):
+        if self.host and t.is_cuda:
+            h = t.cpu()
+            self.dist.all_reduce(h, group=self.group)
+            t.copy_(h)
+        else:
+            self.dist.all_reduce(t, group=self.group)
+        return t
+
+
+def owned_mask(lay: RankLayout, k1: int, device=None):
+    """1 on the dofs rank `lay` owns, 0 on its ghost dofs (local slab vector)."""
+    import torch
+
+    m = torch.zeros((k1, lay.nd_loc), dtype=torch.float64, device=device)
+    rows = lay.owned_node_rows
+    m[:, lay.vel_slice_local(rows.start, rows.stop)] = 1.0
+    m[:, lay.prs_slice_local(lay.a, lay.b)] = 1.0
+    return m.reshape(-1)
+
+
+def distributed_fgmres(rank: DistributedSlab, transport, comm: DistComm, rhs, tol, config=None, vanka_steps=0,
+                       omega=0.7, x0=None):
+    """FGMRES on the strip-partitioned slab system (krylov.fgmres with comm).
+
+    rhs: this rank's local (ghosted) device vector; its ghost entries are
+    ignored.  Operator: x halo exchange + owner-computes Jacobian; mass: halo +
+    (tau w (x) M); preconditioner (optional): `vanka_steps` distributed Vanka
+    steps from zero (patches of the owned cells, increments reverse-added).
+    Every Krylov vector keeps zero ghost entries, so local Euclidean products
+    are owned-only and one allreduce makes them global.  Returns the
+    FgmresResult with x local (ghosts zero)."""
+    import torch
+
+    from .krylov import fgmres
+    from .operators import MassNorm
+
+    k1 = rank.k1
+    dev = rank.jac.dev
+    device = torch.device("cuda", dev.device)
+    mask = owned_mask(rank.lay, k1, device)
+    mass = MassNorm(rank.ctx, dev=dev)
+    tmp = torch.empty(k1 * rank.lay.nd_loc, dtype=torch.float64, device=device)
+
+    def op(v, out=None):
+        tmp.copy_(v)
+        transport.exchange([tmp], "halo_recv", k1)
+        y = rank.jac.matvec(tmp, out=out)
+        y.mul_(mask)
+        return y
+
+    class _Mass:
+        def apply_into(self, v, out):
+            tmp.copy_(v)
+            transport.exchange([tmp], "halo_recv", k1)
+            mass.apply_into(tmp, out)
+            out.mul_(mask)
+            return out
+
+    precond = None
+    if vanka_steps > 0:
+        if rank.level is None:
+            rank.build_patches()
+
+        def precond(v, out=None):
+            d = torch.zeros_like(v)
+            r = v.clone()
+            transport.exchange([r], "halo_recv", k1)
+            for _ in range(vanka_steps):
+                distributed_vanka_step([rank], [d], [r], omega, transport)
+            d.mul_(mask)
+            if out is not None:
+                out.copy_(d)
+                return out
+            return d
+
+    op.dev = dev
+    b = (rhs if isinstance(rhs, torch.Tensor) else torch.as_tensor(rhs, device=device)).reshape(-1) * mask
+    return fgmres(op, b, tol, config, precond=precond, mass=_Mass(), x0=x0, comm=comm)

@@ -128,3 +128,25 @@ def test_gloo_world2_exchange():
         p.join(timeout=60)
     assert res == {0: True, 1: True}
 
+
+
+@pytest.mark.parametrize("nx,ny,P,k1", [(4, 8, 2, 2), (5, 12, 3, 1), (3, 16, 4, 3)])
+def test_owned_masks_partition_unity(nx, ny, P, k1):
+    """The ranks' owned-dof masks (distributed FGMRES inner products) cover every
+    global dof exactly once."""
+    import torch
+
+    from paper_2603_28706_b200.partition import StripPartition, owned_mask
+
+    part = StripPartition(nx, ny, P)
+    tot = np.zeros(k1 * part.layout(0).nd)
+    for r in range(P):
+        lay = part.layout(r)
+        m = owned_mask(lay, k1).numpy()
+        g = np.zeros(lay.nd)
+        for mu in range(k1):
+            lay.owned_into_global(m[mu * lay.nd_loc:(mu + 1) * lay.nd_loc], g)
+            tot[mu * lay.nd:(mu + 1) * lay.nd] += g
+            g[:] = 0.0
+        assert m.sum() == k1 * (len(lay.owned_node_rows) * lay.nnx * 2 + 3 * nx * (lay.b - lay.a))
+    assert np.array_equal(tot, np.ones_like(tot))
