@@ -375,7 +375,6 @@ int pdst_patch_info(pdst_handle* h, int level, int32_t* D, int32_t* diag_blocks,
   if (int e = check_level(h, level)) return e;
   Level* l = h->levels[level];
   if (!l->D) return set_error(PDST_ESTATE, "patches not built");
-  if (!l->mats.ptr) return set_error(PDST_ESTATE, "patch matrices of level %d are not retained at this size", level);
   if (D) *D = l->D;
   if (diag_blocks) *diag_blocks = l->diag ? l->tdiag.nblk : 0;
   if (bytes_per_patch)
