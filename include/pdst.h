@@ -126,6 +126,19 @@ int pdst_restrict(pdst_handle* h, int fine_level, const double* r_fine, double* 
 int pdst_prolong(pdst_handle* h, int fine_level, const double* e_coarse, double* e_fine, int where);
 int pdst_vcycle(pdst_handle* h, const double* r, double* z, int pre, int post, double omega, int where);
 
+/* Manufactured-solution benchmark problem on the device.
+ * pdst_manufactured_forcing: ManufacturedCase.forcing (bench/manufactured.py:
+ *   121-157) at the residual's volume points of every cell and Radau node
+ *   t_start + tau * node[mu]: fqp (k+1, ncells, 16, 2), the f_qp argument of
+ *   pdst_residual.  Uses the handle's model parameters and mesh extents.
+ * pdst_error_norms: one slab's contribution (squared) to error_norms
+ *   (bench/metrics.py:35-85): sq2 = {e_phi^2, e_div^2} over [t0, t1] with
+ *   `spatial_points`^2 Gauss points per cell and `temporal_points` in time
+ *   (the reference's defaults: 5 and k+2); sq2 is a host double[2]. */
+int pdst_manufactured_forcing(pdst_handle* h, double t_start, double* fqp, int where);
+int pdst_error_norms(pdst_handle* h, const double* U, double t0, double t1, int spatial_points, int temporal_points,
+                     double* sq2, int where);
+
 /* Coarsest-level solve of the V-cycle (takes effect at the next
  * pdst_patches_build).  kind:
  *   PDST_COARSE_DENSE   the reference's dense LU of the pinned slab system

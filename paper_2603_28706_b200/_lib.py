@@ -75,6 +75,8 @@ SIGNATURES = {
     "pdst_prolong": [P, I, P, P, I],
     "pdst_vcycle": [P, P, P, I, I, D, I],
     "pdst_set_coarse_solver": [P, I, I, D, I, D],
+    "pdst_manufactured_forcing": [P, D, P, I],
+    "pdst_error_norms": [P, P, D, D, I, I, P, I],
     "pdst_profile": [P, I],
     "pdst_profile_read": [P, I, C.POINTER(D), C.POINTER(I64)],
     "pdst_last_error": [],

@@ -195,8 +195,18 @@ def slab_residual(ctx, U, advect=None, dev: SlabDevice | None = None, device=0):
     own = dev is None
     dev = dev or SlabDevice(ctx, device)
     try:
+        from .manufactured import device_forcing_case
+
         Uc = _f64(U)
-        fq = forcing_at_qp(ctx)
+        dev_f = device_forcing_case(ctx) is not None
+        # the manufactured problem's forcing is evaluated on the device
+        # (pdst_manufactured_forcing); any other f(x, y, t) on the host, as the
+        # reference does (forms.py:459)
+        fq = dev.empty_like(Uc, shape=(dev.k1 * ctx.disc.mesh.nx * ctx.disc.mesh.ny * 32,)) if dev_f else \
+            forcing_at_qp(ctx)
+        if dev_f:
+            L.check(L.lib().pdst_manufactured_forcing(dev.h, float(ctx.t_start), L.vptr(fq), dev.where(fq)),
+                    "pdst_manufactured_forcing")
         vm = ctx.v_minus
         adv = _f64(advect)
         if _is_torch(Uc):

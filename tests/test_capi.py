@@ -34,3 +34,17 @@ def test_launch_counter_starts_at_zero():
     from paper_2603_28706_b200 import _lib
 
     assert _lib.lib().pdst_launch_count() == 0
+
+
+def test_no_unresolved_library_symbols():
+    """Every pdst:: symbol the library references is defined in it (a -shared
+    link would otherwise defer the failure to the first call on the GPU)."""
+    import shutil
+    import subprocess
+
+    from paper_2603_28706_b200 import _lib
+
+    if not shutil.which("nm"):
+        return
+    out = subprocess.run(["nm", "-C", "-u", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "pdst::" not in out, [l for l in out.splitlines() if "pdst::" in l]
