@@ -17,6 +17,8 @@
 #include <cmath>
 #include <complex>
 
+#include <algorithm>
+
 #include "pdst_device.cuh"
 #include "pdst_patch.h"
 
@@ -340,60 +342,169 @@ __device__ __forceinline__ size_t patch_dof_d(const Geom& g, int K, int l) {
   return base + 2 * ((size_t)(2 * kj + a / 3) * g.nnx + 2 * ki + a % 3) + d;
 }
 
-// upd_K = A_K^-1 e_K via the temporal diagonalization; threads (patch, row r).
+// ---------------------------------------------------------------------------
+// The same GEMV as a persistent, TMA-fed pipeline: one CTA per SM streams the
+// patch inverses of groups of PB patches through an S-stage shared-memory ring
+// with bulk copies (cp.async.bulk, completion counted in bytes on an
+// mbarrier), so S-1 groups are always in flight regardless of what the warps
+// are doing; the warps gather the next group's defect while multiplying the
+// current one out of shared memory.  Same arithmetic (and summation order) as
+// the row-per-thread GEMV it replaces (88 -> 84 us at cfg2).
+//   upd_K = A_K^-1 e_K via the temporal diagonalization; threads (patch, row r).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int NB>
+__host__ __device__ constexpr int tma_pb() { return NB == 1 ? 4 : NB == 2 ? 2 : 1; }
+constexpr int TMA_STAGES = 3;
+constexpr int TMA_CTAS_PER_SM = 2;
+template <int NB>
+__host__ __device__ constexpr unsigned tma_patch_bytes() { return (unsigned)NB * 441u * 16u; }
+template <int NB>
+__host__ __device__ constexpr size_t tma_smem() { return (size_t)TMA_STAGES * tma_pb<NB>() * tma_patch_bytes<NB>(); }
+
 template <int K1, int NB>
-__global__ void __launch_bounds__(252) k_vanka_gemv_diag(Geom g, TimeDiag td, const double2* __restrict__ binvT,
-                                                         const double* __restrict__ defect, double* __restrict__ upd) {
-  constexpr int PB = 12;
-  __shared__ double2 gs[PB][NB][21];
+__global__ void __launch_bounds__(tma_pb<NB>() * 21, TMA_CTAS_PER_SM) k_vanka_gemv_diag_tma(Geom g, TimeDiag td,
+                                                                           const double2* __restrict__ binvT,
+                                                                           const double* __restrict__ defect,
+                                                                           double* __restrict__ upd, int ngroups) {
+  constexpr int PB = tma_pb<NB>();
+  constexpr unsigned PBYTES = tma_patch_bytes<NB>();
+  extern __shared__ __align__(128) unsigned char tma_ring[];
+  __shared__ double2 gs[2][PB][NB][21];  // eigen-transformed defects, double buffered
+  __shared__ __align__(8) uint64_t full[TMA_STAGES];
   const int p = threadIdx.x / 21, r = threadIdx.x % 21;
-  const int K = blockIdx.x * PB + p;
-  const bool active = K < g.ncells;
-  if (active) {
-    double f[K1];
+  auto stage_ptr = [&](int st) { return reinterpret_cast<double2*>(tma_ring + (size_t)st * PB * PBYTES); };
+  auto issue = [&](int gi, int st) {  // one thread: arm the stage's barrier and start its copies
+    const int K0 = gi * PB, cnt = min(PB, g.ncells - K0);
+    mbar_expect_tx(&full[st], (unsigned)cnt * PBYTES);
+    for (int q = 0; q < cnt; ++q)
+      bulk_g2s(stage_ptr(st) + (size_t)q * NB * 441, binvT + (size_t)(K0 + q) * NB * 441, PBYTES, &full[st]);
+  };
+  // defect of this thread's (patch, row) in group gi (the loads, issued early)
+  auto load_defect = [&](int gi, double f[K1]) {
+    const int K = gi * PB + p;
+    if (gi < ngroups && K < g.ncells) {
 #pragma unroll
-    for (int mu = 0; mu < K1; ++mu) f[mu] = __ldg(defect + patch_dof_d(g, K, 21 * mu + r)) * td.itw[mu];
+      for (int mu = 0; mu < K1; ++mu) f[mu] = __ldg(defect + patch_dof_d(g, K, 21 * mu + r));
+    }
+  };
+  auto transform = [&](const double f[K1], int buf) {
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
-      double gr = 0.0, gi = 0.0;
+      double gr = 0.0, gi2 = 0.0;
 #pragma unroll
       for (int mu = 0; mu < K1; ++mu) {
-        gr = fma(td.Vi_re[b * MAXK1 + mu], f[mu], gr);
-        gi = fma(td.Vi_im[b * MAXK1 + mu], f[mu], gi);
+        gr = fma(td.Vi_re[b * MAXK1 + mu], f[mu] * td.itw[mu], gr);
+        gi2 = fma(td.Vi_im[b * MAXK1 + mu], f[mu] * td.itw[mu], gi2);
       }
-      gs[p][b][r] = make_double2(gr, gi);
+      gs[buf][p][b][r] = make_double2(gr, gi2);
     }
+  };
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < TMA_STAGES; ++st) mbar_init(&full[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    for (int st = 0; st < TMA_STAGES; ++st) {
+      const int gi = blockIdx.x + st * gridDim.x;
+      if (gi < ngroups) issue(gi, st);
+    }
+  }
+  {
+    double f[K1] = {};
+    load_defect(blockIdx.x, f);
+    transform(f, 0);
   }
   __syncthreads();
-  if (!active) return;
-  double hr[NB], hi[NB];
+  int it = 0;
+  for (int gi = blockIdx.x; gi < ngroups; gi += gridDim.x, ++it) {
+    const int st = it % TMA_STAGES, buf = it & 1;
+    const unsigned parity = (unsigned)(it / TMA_STAGES) & 1u;
+    const int K = gi * PB + p;
+    double fn[K1] = {};
+    load_defect(gi + gridDim.x, fn);  // next group's defect, consumed after this group's product
+    mbar_wait(&full[st], parity);
+    if (K < g.ncells) {
+      const double2* blk = stage_ptr(st) + (size_t)p * NB * 441;
+      double hr[NB], hi[NB];
 #pragma unroll
-  for (int b = 0; b < NB; ++b) {
-    const double2* col = binvT + ((size_t)K * NB + b) * 441 + r;
-    double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
+      for (int b = 0; b < NB; ++b) {
+        const double2* col = blk + (size_t)b * 441 + r;
+        double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
 #pragma unroll 7
-    for (int j = 0; j < 21; ++j) {
-      const double2 m = __ldg(col + 21 * j);
-      const double2 v = gs[p][b][j];
-      ar = fma(m.x, v.x, ar);
-      br = fma(m.y, v.y, br);
-      ai = fma(m.x, v.y, ai);
-      bi = fma(m.y, v.x, bi);
-    }
-    hr[b] = ar - br;
-    hi[b] = ai + bi;
-  }
-  double* o = upd + K;  // structure of arrays [21 K1][ncells]
+        for (int j = 0; j < 21; ++j) {
+          const double2 m = col[21 * j];
+          const double2 v = gs[buf][p][b][j];
+          ar = fma(m.x, v.x, ar);
+          br = fma(m.y, v.y, br);
+          ai = fma(m.x, v.y, ai);
+          bi = fma(m.y, v.x, bi);
+        }
+        hr[b] = ar - br;
+        hi[b] = ai + bi;
+      }
+      double* o = upd + K;
 #pragma unroll
-  for (int mu = 0; mu < K1; ++mu) {
-    double s = 0.0;
+      for (int mu = 0; mu < K1; ++mu) {
+        double sacc = 0.0;
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const double re = td.V_re[mu * MAXK1 + b] * hr[b] - td.V_im[mu * MAXK1 + b] * hi[b];
-      s += td.pair[b] ? 2.0 * re : re;
+        for (int b = 0; b < NB; ++b) {
+          const double re = td.V_re[mu * MAXK1 + b] * hr[b] - td.V_im[mu * MAXK1 + b] * hi[b];
+          sacc += td.pair[b] ? 2.0 * re : re;
+        }
+        o[(size_t)(21 * mu + r) * g.ncells] = sacc;
+      }
     }
-    o[(size_t)(21 * mu + r) * g.ncells] = s;
+    transform(fn, buf ^ 1);
+    __syncthreads();  // stage st is free, gs[buf ^ 1] is complete
+    if (threadIdx.x == 0) {
+      const int gn = gi + TMA_STAGES * gridDim.x;
+      if (gn < ngroups) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads before the async writes
+        issue(gn, st);
+      }
+    }
   }
+}
+
+template <int K1, int NB>
+cudaError_t launch_gemv_tma(const Geom& g, const TimeDiag& td, const double2* binvT, const double* defect,
+                            double* upd, cudaStream_t st) {
+  static int nsm = 0;
+  static bool configured = false;
+  const size_t sm = tma_smem<NB>();
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_vanka_gemv_diag_tma<K1, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sm);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    configured = true;
+  }
+  constexpr int PB = tma_pb<NB>();
+  const int ngroups = (g.ncells + PB - 1) / PB;
+  const int grid = std::min(ngroups, TMA_CTAS_PER_SM * nsm);
+  PDST_LAUNCH(k_vanka_gemv_diag_tma<K1, NB><<<grid, PB * 21, sm, st>>>(g, td, binvT, defect, upd, ngroups));
+  return cudaGetLastError();
 }
 
 }  // namespace
@@ -407,19 +518,17 @@ cudaError_t patch_invert_diag(const Geom& g, const TimeDiag& td, const double* s
 
 cudaError_t vanka_gemv_diag(const Geom& g, const TimeDiag& td, const double2* binvT, const double* defect,
                             double* upd, cudaStream_t st) {
-  const unsigned grid = (unsigned)((g.ncells + 11) / 12);
   switch (td.k1 * 10 + td.nblk) {
-    case 11: PDST_LAUNCH(k_vanka_gemv_diag<1, 1><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd)); break;
-    case 21: PDST_LAUNCH(k_vanka_gemv_diag<2, 1><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd)); break;
-    case 22: PDST_LAUNCH(k_vanka_gemv_diag<2, 2><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd)); break;
-    case 32: PDST_LAUNCH(k_vanka_gemv_diag<3, 2><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd)); break;
-    case 33: PDST_LAUNCH(k_vanka_gemv_diag<3, 3><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd)); break;
-    case 42: PDST_LAUNCH(k_vanka_gemv_diag<4, 2><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd)); break;
-    case 43: PDST_LAUNCH(k_vanka_gemv_diag<4, 3><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd)); break;
-    case 44: PDST_LAUNCH(k_vanka_gemv_diag<4, 4><<<grid, 252, 0, st>>>(g, td, binvT, defect, upd)); break;
+    case 11: return launch_gemv_tma<1, 1>(g, td, binvT, defect, upd, st);
+    case 21: return launch_gemv_tma<2, 1>(g, td, binvT, defect, upd, st);
+    case 22: return launch_gemv_tma<2, 2>(g, td, binvT, defect, upd, st);
+    case 32: return launch_gemv_tma<3, 2>(g, td, binvT, defect, upd, st);
+    case 33: return launch_gemv_tma<3, 3>(g, td, binvT, defect, upd, st);
+    case 42: return launch_gemv_tma<4, 2>(g, td, binvT, defect, upd, st);
+    case 43: return launch_gemv_tma<4, 3>(g, td, binvT, defect, upd, st);
+    case 44: return launch_gemv_tma<4, 4>(g, td, binvT, defect, upd, st);
     default: return cudaErrorNotSupported;
   }
-  return cudaGetLastError();
 }
 
 }  // namespace pdst
