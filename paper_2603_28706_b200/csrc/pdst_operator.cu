@@ -2,19 +2,19 @@
 // residual kernels (sm_100a, fp64).
 //
 // Kernel design:
-//   * one CTA per tile of TX x TY owned cells; the CTA also computes a halo
-//     ring of one cell to the left and below so that every node it owns
-//     receives all of its element contributions inside the CTA
-//     (owner-computes; deterministic, no atomics);
-//   * the tile's Q2 node values (all k+1 Radau nodes of the direction, the
-//     state of the current node) are staged in shared memory with a two-cell
-//     ring so that the CIP jump of every computed cell can be evaluated;
-//   * one thread per cell evaluates the cell's full contribution to its own
-//     9 nodes: volume terms by sum factorisation over the 1-D 4x3 tables,
-//     its boundary sides, the own-side half of its 4 CIP faces and the
-//     K_t (x) M_x temporal coupling (cell mass = hx hy M1 (x) M1);
-//   * contributions are combined per node from shared memory in a fixed
-//     order and written once.
+//   * Jacobian apply (k_apply_cache once per linearization; k_jacobian +
+//     k_jac_post per apply): the per-quadrature-point coefficients are a
+//     tile-major stream (the reference's linearization cache); one CTA per
+//     16 x 16-cell tile, one thread per cell, the direction's Radau planes
+//     staged in shared memory with a one-cell ring, volume by sum
+//     factorisation, CIP through cached face matrices, temporal mass, fixed-
+//     order node assembly; tile-line nodes and the boundary-face side terms
+//     are finished by the PDL-launched epilogue;
+//   * residual (k_residual): tiles of TX x TY owned cells plus a halo ring of
+//     one cell to the left and below (owner computes), the state staged with a
+//     two-cell ring, nonlinear stress evaluated per point;
+//   * element / boundary-side matrices by probing the cell-local action with
+//     unit vectors (the assembled and matrix-free paths agree to rounding).
 //
 // Reference: forms.py:581-652 (J x), forms.py:435-516 (residual),
 // slab.py:162-205 (slab composition), constitutive.py:323-337 (tangent).
@@ -83,20 +83,6 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool v
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p)); }
-
-// Issue the asynchronous staging of one velocity block (zero outside the
-// domain); the caller waits with cp_async_wait_all() + __syncthreads().
-__device__ __forceinline__ void stage_velocity_async(const Geom& g, const double* __restrict__ v, double* pl0,
-                                                     double* pl1, int X0, int Y0) {
-  for (int idx = threadIdx.x; idx < NR * NC; idx += blockDim.x) {
-    const int r = idx / NC, c = idx - r * NC;
-    const int X = X0 + c, Y = Y0 + r;
-    const bool in = X >= 0 && X < g.nnx && Y >= 0 && Y < g.nny;
-    const double* src = in ? v + 2 * ((size_t)Y * g.nnx + X) : v;
-    cp_async8(pl0 + pidx(r, c), src, in);
-    cp_async8(pl1 + pidx(r, c), in ? src + 1 : v, in);
-  }
-}
 
 // Stage one slab block's velocity into two shared planes (zero outside the domain).
 __device__ void stage_velocity(const Geom& g, const double* __restrict__ v, double* pl0, double* pl1, int X0,
@@ -591,66 +577,6 @@ __device__ __forceinline__ void add_mass(const FA* F, const FA* Fm, double mfac,
   }
 }
 
-// acc += s * (M1 (x) M1) F on the cell's 9 nodes of one staged plane pair.
-template <class ACC>
-__device__ __forceinline__ void add_mass_plane(const Plane2& F, int r0, int c0, double s, const ACC& acc) {
-#pragma unroll
-  for (int jj = 0; jj < 3; ++jj) {
-    double T1[3][2];
-#pragma unroll
-    for (int d = 0; d < 2; ++d) {
-      const double f0 = F.at(d, r0 + jj, c0), f1 = F.at(d, r0 + jj, c0 + 1), f2 = F.at(d, r0 + jj, c0 + 2);
-#pragma unroll
-      for (int i = 0; i < 3; ++i) T1[i][d] = c_tab.M1[i][0] * f0 + c_tab.M1[i][1] * f1 + c_tab.M1[i][2] * f2;
-    }
-#pragma unroll
-    for (int jy = 0; jy < 3; ++jy) {
-      const double m = s * c_tab.M1[jy][jj];
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int d = 0; d < 2; ++d) acc.add(jy, i, d, m * T1[i][d]);
-    }
-  }
-}
-
-// acc += s * (M1 (x) M1) (sum_nu K_t[mu,nu] x_nu) with the cell's nodal x_nu
-// read from global memory (L1) — the temporal coupling of slab.py:199-200.
-template <int K1, class ACC>
-__device__ __forceinline__ void add_mass_global(const double* __restrict__ x, size_t stride, int nnx, int X0, int Y0,
-                                                const double* Krow, double s, const ACC& acc) {
-#pragma unroll
-  for (int jj = 0; jj < 3; ++jj) {
-    double xt[3][2];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const size_t o = 2 * ((size_t)(Y0 + jj) * nnx + X0 + i);
-      double v0 = 0.0, v1 = 0.0;
-#pragma unroll
-      for (int nu = 0; nu < K1; ++nu) {
-        v0 = fma(Krow[nu], __ldg(x + nu * stride + o), v0);
-        v1 = fma(Krow[nu], __ldg(x + nu * stride + o + 1), v1);
-      }
-      xt[i][0] = v0;
-      xt[i][1] = v1;
-    }
-    double T1[3][2];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int d = 0; d < 2; ++d)
-        T1[i][d] = c_tab.M1[i][0] * xt[0][d] + c_tab.M1[i][1] * xt[1][d] + c_tab.M1[i][2] * xt[2][d];
-#pragma unroll
-    for (int jy = 0; jy < 3; ++jy) {
-      const double m = s * c_tab.M1[jy][jj];
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int d = 0; d < 2; ++d) acc.add(jy, i, d, m * T1[i][d]);
-    }
-  }
-}
-
 // Cell-local Jacobian action (volume + the cell's boundary sides), without the
 // CIP faces, the temporal mass and the tau w_mu scaling.  XA / SA are field
 // accessors (shared-memory planes in the apply, unit vectors / global memory
@@ -834,14 +760,12 @@ __device__ void assemble_and_store(const Geom& g, const double* sacc, int i0, in
 
 // ---------------------------------------------------------------------------
 // Slab Jacobian apply: out = J x  (or rhs - J x when rhs != null)
-// ---------------------------------------------------------------------------
-// ---------------------------------------------------------------------------
-// Slab Jacobian apply: out = J x  (or rhs - J x when rhs != null)
 //
 // Tiles of JT x JT cells, one thread per cell, NO redundant halo cells: nodes
 // interior to a tile are complete and written directly; nodes on a tile
 // boundary shared with a neighbour tile are written as partial sums to `part`
-// and combined by k_jac_fixup in a fixed order (deterministic).
+// and combined by k_jac_post in a fixed order (deterministic), which also adds
+// the boundary-face side terms.
 // ---------------------------------------------------------------------------
 // Per-CTA phase timeline of the apply (profiling builds only, -DPDST_TRACE).
 #ifdef PDST_TRACE
@@ -907,97 +831,6 @@ __device__ __forceinline__ int perim_t(int lx, int ly) {
   return 2 * (2 * T + 1) + 2 * T - 1 + ly - 1;
 }
 __device__ __forceinline__ int perim(int lx, int ly) { return perim_t<JT>(lx, ly); }
-
-// Boundary-side products of the current direction, one thread per (row i,
-// boundary face, node mu): ybnd[mu][i][bf] = sum_j B[mu][i][j][bf] x_loc[j].
-// Runs before k_jacobian so boundary cells only add 21 precomputed values.
-__global__ void k_boundary_apply(Geom g, int k1, const double* __restrict__ bmat, const double* __restrict__ x,
-                                 double* __restrict__ ybnd) {
-  pdl_trigger();  // k_jacobian may start now; its boundary cells wait for ybnd
-  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int mu = blockIdx.y;
-  const int i = (int)(t / g.nbf), bf = (int)(t % g.nbf);
-  if (i >= 21 || mu >= k1) return;
-  int side = 0;
-  while (side < 3 && bf >= side_offset(g, side + 1)) ++side;
-  const int f = bf - side_offset(g, side);
-  int ci, cj;
-  if (side == 0) { ci = f; cj = 0; }
-  else if (side == 1) { ci = g.nx - 1; cj = f; }
-  else if (side == 2) { ci = f; cj = g.ny - 1; }
-  else { ci = 0; cj = f; }
-  const double* xm = x + (size_t)mu * g.nd;
-  const double* Bm = bmat + (size_t)mu * 441 * g.nbf + (size_t)i * 21 * g.nbf + bf;
-  // all 42 loads are issued before the first FMA (one memory latency, not 21)
-  double bv[21], xv[21];
-#pragma unroll
-  for (int j = 0; j < 21; ++j) bv[j] = __ldg(Bm + (size_t)j * g.nbf);
-#pragma unroll
-  for (int a = 0; a < 9; ++a) {
-    const size_t node = (size_t)(2 * cj + a / 3) * g.nnx + 2 * ci + a % 3;
-    xv[2 * a] = __ldg(xm + 2 * node);
-    xv[2 * a + 1] = __ldg(xm + 2 * node + 1);
-  }
-  const double* xp = xm + g.mv + 3 * ((size_t)cj * g.nx + ci);
-#pragma unroll
-  for (int r = 0; r < 3; ++r) xv[18 + r] = __ldg(xp + r);
-  double s = 0.0;
-#pragma unroll
-  for (int j = 0; j < 21; ++j) s = fma(bv[j], xv[j], s);
-  ybnd[((size_t)mu * 21 + i) * g.nbf + bf] = s;
-}
-
-// Add the precomputed boundary-side products of a cell (times tau w_mu).
-template <class ACC>
-__device__ __forceinline__ void jac_sides_pre(const Geom& g, const double* __restrict__ ybnd, int mu, int ci, int cj,
-                                              const ACC& acc, double accp[3], double tw) {
-  if (!(ci == 0 || cj == 0 || ci == g.nx - 1 || cj == g.ny - 1)) return;
-  for (int side = 0; side < 4; ++side) {
-    const bool on = side == 0 ? cj == 0 : side == 1 ? ci == g.nx - 1 : side == 2 ? cj == g.ny - 1 : ci == 0;
-    if (!on) continue;
-    const int bf = side_offset(g, side) + ((side == 0 || side == 2) ? ci : cj);
-    const double* yb = ybnd + (size_t)mu * 21 * g.nbf + bf;
-#pragma unroll
-    for (int i = 0; i < 18; ++i) acc.add((i >> 1) / 3, (i >> 1) % 3, i & 1, tw * __ldg(yb + (size_t)i * g.nbf));
-#pragma unroll
-    for (int r = 0; r < 3; ++r) accp[r] += tw * __ldg(yb + (size_t)(18 + r) * g.nbf);
-  }
-}
-
-// Staging plan of one thread: the (row, col) staged nodes it copies, shared by
-// every plane it stages (precomputed once per kernel).
-constexpr int STG_IT = (NR * NC + JNT - 1) / JNT;
-struct StagePlan {
-  int sidx[STG_IT];   // shared index (pidx) or -1
-  long long gofs[STG_IT];  // 2 * global node index, or -1 outside the domain
-};
-
-__device__ __forceinline__ void stage_plan(const Geom& g, int X0, int Y0, StagePlan& sp) {
-#pragma unroll
-  for (int it = 0; it < STG_IT; ++it) {
-    const int idx = threadIdx.x + it * JNT;
-    sp.sidx[it] = -1;
-    sp.gofs[it] = -1;
-    if (idx < NR * NC) {
-      const int r = idx / NC, c = idx - r * NC;
-      const int X = X0 + c, Y = Y0 + r;
-      sp.sidx[it] = pidx(r, c);
-      if (X >= 0 && X < g.nnx && Y >= 0 && Y < g.nny) sp.gofs[it] = 2 * ((long long)Y * g.nnx + X);
-    }
-  }
-}
-
-__device__ __forceinline__ void stage_planned(const StagePlan& sp, const double* __restrict__ v, double* pl0,
-                                              double* pl1) {
-#pragma unroll
-  for (int it = 0; it < STG_IT; ++it) {
-    if (sp.sidx[it] < 0) continue;
-    const bool in = sp.gofs[it] >= 0;
-    const double* src = in ? v + sp.gofs[it] : v;
-    cp_async8(pl0 + sp.sidx[it], src, in);
-    cp_async8(pl1 + sp.sidx[it], in ? src + 1 : v, in);
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Apply cache (built once per linearization by k_apply_cache, read by every
@@ -1184,61 +1017,6 @@ __device__ __forceinline__ void cip_all_w(const JTabs& T, const Geom& g, const F
     cip_scatter(1, false, 1.0, RD, acc);
   }
 }
-
-// Shared tile-boundary nodes: sum the (2 or 4) tile partials in fixed order.
-template <int T>
-__global__ void k_jac_fixup(Geom g, int k1, const double* __restrict__ part, const double* __restrict__ rhs,
-                            double* __restrict__ out) {
-  pdl_wait();  // partials of k_jacobian
-  constexpr int PER = 8 * T;
-  const int ntx = (g.nx + T - 1) / T, nty = (g.ny + T - 1) / T;
-  const size_t nv = (size_t)(ntx - 1) * g.nny;  // nodes on interior vertical tile lines
-  const size_t nh = (size_t)(nty - 1) * g.nnx;  // nodes on interior horizontal tile lines
-  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int mu = blockIdx.y;
-  int X, Y;
-  if (t < nv) {
-    X = 2 * T * (int)(t / g.nny + 1);
-    Y = (int)(t % g.nny);
-  } else if (t < nv + nh) {
-    const size_t u = t - nv;
-    Y = 2 * T * (int)(u / g.nnx + 1);
-    X = (int)(u % g.nnx);
-    if (X % (2 * T) == 0 && X > 0 && X / (2 * T) < ntx) return;  // on a vertical line
-  } else {
-    return;
-  }
-  int bxs[2], bys[2], nbx = 0, nby = 0;
-  if (X % (2 * T) == 0 && X > 0 && X / (2 * T) < ntx) {
-    bxs[0] = X / (2 * T) - 1;
-    bxs[1] = X / (2 * T);
-    nbx = 2;
-  } else {
-    bxs[0] = min(X / (2 * T), ntx - 1);
-    nbx = 1;
-  }
-  if (Y % (2 * T) == 0 && Y > 0 && Y / (2 * T) < nty) {
-    bys[0] = Y / (2 * T) - 1;
-    bys[1] = Y / (2 * T);
-    nby = 2;
-  } else {
-    bys[0] = min(Y / (2 * T), nty - 1);
-    nby = 1;
-  }
-  const size_t ntiles = (size_t)ntx * nty;
-  double s0 = 0.0, s1 = 0.0;
-  for (int b = 0; b < nby; ++b)
-    for (int a = 0; a < nbx; ++a) {
-      const int lx = X - 2 * T * bxs[a], ly = Y - 2 * T * bys[b];
-      const double* pp = part + (((size_t)mu * ntiles + (size_t)bys[b] * ntx + bxs[a]) * PER + perim_t<T>(lx, ly)) * 2;
-      s0 += pp[0];
-      s1 += pp[1];
-    }
-  const size_t o = (size_t)mu * g.nd + 2 * ((size_t)Y * g.nnx + X);
-  out[o] = rhs ? rhs[o] - s0 : s0;
-  out[o + 1] = rhs ? rhs[o + 1] - s1 : s1;
-}
-
 
 // ---------------------------------------------------------------------------
 // Apply epilogue (one kernel, PDL-launched behind k_jacobian): the nodes the
@@ -1501,7 +1279,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
   const double* cbase = L.apc + tile * K1 * APC_SLOTS * JNT + threadIdx.x;
 
   TR(0);
-  pdl_trigger();  // k_jac_fixup may be scheduled; it waits for this grid
+  pdl_trigger();  // k_jac_post may start its side products; it waits for this grid
   if (valid)
     for (int h = 0; h < PDST_PF_AHEAD; ++h) apc_prefetch_l2(cbase, h);
   for (int nu = 0; nu < K1; ++nu) stage_jac_async(g, x + (size_t)nu * g.nd, nu * 2 * JPLANE, X0, Y0);
