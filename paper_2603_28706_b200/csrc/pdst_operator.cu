@@ -1068,46 +1068,97 @@ struct StripIdx {
   }
 };
 
-// Side terms of the boundary faces at velocity node (X, Y): b[d].
-__device__ void strip_sides(const Geom& g, int k1, int mu, double tw, const double* __restrict__ bmat,
-                            const double* __restrict__ x, int X, int Y, double b[2]) {
-  b[0] = b[1] = 0.0;
-  const double* xm = x + (size_t)mu * g.nd;
-  for (int side = 0; side < 4; ++side) {
-    // cells of this side that contain (X, Y)
-    const bool horiz = side == 0 || side == 2;
-    const int fixed = side == 0 ? 0 : side == 1 ? g.nx - 1 : side == 2 ? g.ny - 1 : 0;
-    const int off = horiz ? Y - 2 * fixed : X - 2 * fixed;  // node offset across the side's cell row
-    if (off < 0 || off > 2) continue;
-    const int along = horiz ? X : Y, ncell = horiz ? g.nx : g.ny;
-    const int lo = max(0, (along - 1) / 2), hi = min(ncell - 1, along / 2);
-    for (int k = lo; k <= hi; ++k) {
-      const int ci = horiz ? k : fixed, cj = horiz ? fixed : k;
-      const int bf = side_offset(g, side) + k;
-      if (g.dirichlet[bf] == kCutSide) continue;
-      const int a = 3 * (Y - 2 * cj) + (X - 2 * ci);
-      const double* B0 = bmat + (size_t)mu * 441 * g.nbf + (size_t)(2 * a) * 21 * g.nbf + bf;
-      const double* B1 = B0 + (size_t)21 * g.nbf;
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int n = 0; n < 9; ++n) {
-        const size_t node = (size_t)(2 * cj + n / 3) * g.nnx + 2 * ci + n % 3;
-        const double x0 = __ldg(xm + 2 * node), x1 = __ldg(xm + 2 * node + 1);
-        s0 = fma(__ldg(B0 + (size_t)(2 * n) * g.nbf), x0, s0);
-        s0 = fma(__ldg(B0 + (size_t)(2 * n + 1) * g.nbf), x1, s0);
-        s1 = fma(__ldg(B1 + (size_t)(2 * n) * g.nbf), x0, s1);
-        s1 = fma(__ldg(B1 + (size_t)(2 * n + 1) * g.nbf), x1, s1);
-      }
-      const double* xp = xm + g.mv + 3 * ((size_t)cj * g.nx + ci);
-#pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        s0 = fma(__ldg(B0 + (size_t)(18 + r) * g.nbf), __ldg(xp + r), s0);
-        s1 = fma(__ldg(B1 + (size_t)(18 + r) * g.nbf), __ldg(xp + r), s1);
-      }
-      b[0] += tw * s0;
-      b[1] += tw * s1;
-    }
+// Boundary cells: bottom row, top row, then the left / right cells of the rows
+// between (every cell when the mesh is one cell wide or tall).
+__host__ __device__ inline size_t n_bcells(const Geom& g) {
+  return g.nx == 1 || g.ny == 1 ? (size_t)g.ncells : (size_t)2 * g.nx + 2 * (g.ny - 2);
+}
+__device__ inline void bcell_of(const Geom& g, size_t t, int& ci, int& cj) {
+  if (g.nx == 1 || g.ny == 1) {
+    ci = (int)(t % g.nx);
+    cj = (int)(t / g.nx);
+  } else if (t < (size_t)g.nx) {
+    ci = (int)t;
+    cj = 0;
+  } else if (t < (size_t)2 * g.nx) {
+    ci = (int)(t - g.nx);
+    cj = g.ny - 1;
+  } else {
+    const size_t u = t - 2 * g.nx;
+    cj = 1 + (int)(u / 2);
+    ci = (u % 2) ? g.nx - 1 : 0;
   }
+}
+// index of boundary cell (ci, cj), or -1 for an interior cell
+__device__ inline int bcell_index(const Geom& g, int ci, int cj) {
+  if (g.nx == 1 || g.ny == 1) return cj * g.nx + ci;
+  if (cj == 0) return ci;
+  if (cj == g.ny - 1) return g.nx + ci;
+  if (ci == 0) return 2 * g.nx + 2 * (cj - 1);
+  if (ci == g.nx - 1) return 2 * g.nx + 2 * (cj - 1) + 1;
+  return -1;
+}
+
+// Side products of the boundary cells: sp[mu][r][cb] = sum over the cell's
+// boundary faces f (side order, cut faces skipped) of tau w_mu (B_f x_loc)[r],
+// B_f the side matrices of forms.py:605-637 probed once per linearization
+// (k_boundary_matrices, face-contiguous [mu][bf][21][21]).  One warp per
+// boundary cell, lane r < 21 computes row r; x_loc is loaded once and
+// broadcast by shuffles.  Depends only on x: launched with PDL behind the tile
+// pass, its short-lived CTAs run on the SMs the tile pass leaves half empty;
+// the grid completes after the tile pass, so k_jac_post (launched behind this grid) sees both.
+__global__ void __launch_bounds__(128, 8) k_side_products(Geom g, TimeData td, const double* __restrict__ bmat,
+                                                       const double* __restrict__ x, double* __restrict__ sp) {
+  pdl_trigger();
+  const int mu = blockIdx.y, lane = threadIdx.x & 31;
+  const size_t ncb = n_bcells(g);
+  const size_t cb = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (cb < ncb) {
+    int ci, cj;
+    bcell_of(g, cb, ci, cj);
+    const double* xm = x + (size_t)mu * g.nd;
+    double xj = 0.0;
+    if (lane < 18) {
+      const int n = lane >> 1;
+      xj = __ldg(xm + 2 * ((size_t)(2 * cj + n / 3) * g.nnx + 2 * ci + n % 3) + (lane & 1));
+    } else if (lane < 21) {
+      xj = __ldg(xm + g.mv + 3 * ((size_t)cj * g.nx + ci) + (lane - 18));
+    }
+    const int r = lane < 21 ? lane : 20;
+    const double tw = td.tau_w[mu];
+    double acc = 0.0;
+    for (int side = 0; side < 4; ++side) {
+      const bool on = side == 0 ? cj == 0 : side == 1 ? ci == g.nx - 1 : side == 2 ? cj == g.ny - 1 : ci == 0;
+      const int bf = side_offset(g, side) + ((side == 0 || side == 2) ? ci : cj);
+      if (!on || g.dirichlet[bf] == kCutSide) continue;
+      const double* Br = bmat + ((size_t)mu * g.nbf + bf) * 441 + r * 21;
+      double s = 0.0;
+#pragma unroll
+      for (int col = 0; col < 21; ++col) s = fma(__ldg(Br + col), __shfl_sync(0xffffffffu, xj, col), s);
+      acc += tw * s;
+    }
+    if (lane < 21) sp[((size_t)mu * 21 + lane) * ncb + cb] = acc;
+  }
+  // one CTA waits for the tile pass, so this grid completes after it (the
+  // others retire at once and free their SM slots for more of this grid)
+  if (blockIdx.x == 0 && blockIdx.y == 0) pdl_wait();
+}
+
+// Side terms at velocity node (X, Y): sum of the side products of the
+// boundary cells containing it, (row, column) order.
+__device__ void strip_sides(const Geom& g, const double* __restrict__ sp, int mu, int X, int Y, double b[2]) {
+  b[0] = b[1] = 0.0;
+  const size_t ncb = n_bcells(g);
+  const int jlo = max(0, (Y - 1) / 2), jhi = min(g.ny - 1, Y / 2);
+  const int ilo = max(0, (X - 1) / 2), ihi = min(g.nx - 1, X / 2);
+  for (int cj = jlo; cj <= jhi; ++cj)
+    for (int ci = ilo; ci <= ihi; ++ci) {
+      const int cb = bcell_index(g, ci, cj);
+      if (cb < 0) continue;
+      const int a = 3 * (Y - 2 * cj) + (X - 2 * ci);
+      b[0] += sp[((size_t)mu * 21 + 2 * a) * ncb + cb];
+      b[1] += sp[((size_t)mu * 21 + 2 * a + 1) * ncb + cb];
+    }
 }
 
 // Sum of the tile partials at tile-line node (X, Y).
@@ -1142,26 +1193,26 @@ __device__ void tile_partials(const Geom& g, const double* part, int mu, int X, 
 }
 
 // Work items per Radau node: strip nodes, then tile-line nodes off the
-// strips, then boundary cells (pressure).
-__global__ void k_jac_post(Geom g, TimeData td, const double* __restrict__ bmat, const double* __restrict__ x,
-                           const double* __restrict__ part, const double* __restrict__ rhs, double* __restrict__ out) {
+// strips, then boundary cells (pressure).  Launched with PDL behind the tile
+// pass; every item only waits and sums.
+__global__ void __launch_bounds__(128, 16) k_jac_post(Geom g, TimeData td, const double* __restrict__ part,
+                                                  const double* __restrict__ sp, const double* __restrict__ rhs,
+                                                  double* __restrict__ out) {
   const int mu = blockIdx.y;
-  const double tw = td.tau_w[mu];
   const StripIdx si(g);
   const size_t ns = si.count(g);
   const int ntx = jac_tiles_x(g), nty = jac_tiles_y(g);
   const size_t nv = (size_t)(ntx - 1) * g.nny, nh = (size_t)(nty - 1) * g.nnx;
-  const size_t ncb = g.nx == 1 || g.ny == 1 ? (size_t)g.ncells : (size_t)2 * g.nx + 2 * (g.ny - 2);
+  const size_t ncb = n_bcells(g);
   size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t base = (size_t)mu * g.nd;
   if (t < ns) {
     int X, Y;
     si.node(g, t, X, Y);
-    double b[2];
-    strip_sides(g, td.k1, mu, tw, bmat, x, X, Y, b);
-    pdl_wait();
-    double s[2];
     const size_t o = base + 2 * ((size_t)Y * g.nnx + X);
+    pdl_wait();
+    double b[2], s[2];
+    strip_sides(g, sp, mu, X, Y, b);
     if (on_tile_line(g, X, Y)) {
       tile_partials(g, part, mu, X, Y, s);
     } else {
@@ -1197,53 +1248,19 @@ __global__ void k_jac_post(Geom g, TimeData td, const double* __restrict__ bmat,
   }
   t -= nv + nh;
   if (t < ncb) {
-    // boundary cell t: bottom row, top row, then left / right columns between
     int ci, cj;
-    if (g.nx == 1 || g.ny == 1) {
-      ci = (int)(t % g.nx);
-      cj = (int)(t / g.nx);
-    } else if (t < (size_t)g.nx) {
-      ci = (int)t;
-      cj = 0;
-    } else if (t < (size_t)2 * g.nx) {
-      ci = (int)(t - g.nx);
-      cj = g.ny - 1;
-    } else {
-      const size_t u = t - 2 * g.nx;
-      cj = 1 + (int)(u / 2);
-      ci = (u % 2) ? g.nx - 1 : 0;
-    }
-    const double* xm = x + base;
-    double bp[3] = {0.0, 0.0, 0.0};
-    for (int side = 0; side < 4; ++side) {
-      const bool on = side == 0 ? cj == 0 : side == 1 ? ci == g.nx - 1 : side == 2 ? cj == g.ny - 1 : ci == 0;
-      if (!on) continue;
-      const int bf = side_offset(g, side) + ((side == 0 || side == 2) ? ci : cj);
-      if (g.dirichlet[bf] == kCutSide) continue;
-      for (int r = 0; r < 3; ++r) {
-        const double* Br = bmat + (size_t)mu * 441 * g.nbf + (size_t)(18 + r) * 21 * g.nbf + bf;
-        double sr = 0.0;
-        for (int n = 0; n < 9; ++n) {
-          const size_t node = (size_t)(2 * cj + n / 3) * g.nnx + 2 * ci + n % 3;
-          sr = fma(__ldg(Br + (size_t)(2 * n) * g.nbf), __ldg(xm + 2 * node), sr);
-          sr = fma(__ldg(Br + (size_t)(2 * n + 1) * g.nbf), __ldg(xm + 2 * node + 1), sr);
-        }
-        const double* xp = xm + g.mv + 3 * ((size_t)cj * g.nx + ci);
-        for (int q = 0; q < 3; ++q) sr = fma(__ldg(Br + (size_t)(18 + q) * g.nbf), __ldg(xp + q), sr);
-        bp[r] += tw * sr;
-      }
-    }
-    pdl_wait();
+    bcell_of(g, t, ci, cj);
     const size_t o = base + g.mv + 3 * ((size_t)cj * g.nx + ci);
+    pdl_wait();
     for (int r = 0; r < 3; ++r) {
-      const double s = out[o + r] + bp[r];
+      const double s = out[o + r] + sp[((size_t)mu * 21 + 18 + r) * ncb + t];
       out[o + r] = rhs ? rhs[o + r] - s : s;
     }
   }
 }
 
 __host__ __device__ inline size_t jac_post_items(const Geom& g) {
-  const size_t ncb = g.nx == 1 || g.ny == 1 ? (size_t)g.ncells : (size_t)2 * g.nx + 2 * (g.ny - 2);
+  const size_t ncb = n_bcells(g);
   return StripIdx(g).count(g) + (size_t)(jac_tiles_x(g) - 1) * g.nny + (size_t)(jac_tiles_y(g) - 1) * g.nnx + ncb;
 }
 
@@ -1279,7 +1296,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
   const double* cbase = L.apc + tile * K1 * APC_SLOTS * JNT + threadIdx.x;
 
   TR(0);
-  pdl_trigger();  // k_jac_post may start its side products; it waits for this grid
+  pdl_trigger();  // k_side_products runs under this grid; k_jac_post waits for both
   if (valid)
     for (int h = 0; h < PDST_PF_AHEAD; ++h) apc_prefetch_l2(cbase, h);
   for (int nu = 0; nu < K1; ++nu) stage_jac_async(g, x + (size_t)nu * g.nd, nu * 2 * JPLANE, X0, Y0);
@@ -1934,12 +1951,12 @@ __global__ void __launch_bounds__(128) k_boundary_matrices(Geom g, Disc ds, Lin 
     for (int b = 0; b < 3; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   double accp[3] = {0.0, 0.0, 0.0};
   jac_boundary_side(g, ds, L, mu, side, bf, X, S, 0, 0, P, RegAcc{acc}, accp, 1.0);
-  double* col = bmat + (size_t)mu * 441 * g.nbf;
+  double* col = bmat + ((size_t)mu * g.nbf + bf) * 441 + j;  // [mu][bf][row][col]
   for (int a = 0; a < 9; ++a) {
-    col[((size_t)(2 * a) * 21 + j) * g.nbf + bf] = acc[a / 3][a % 3][0];
-    col[((size_t)(2 * a + 1) * 21 + j) * g.nbf + bf] = acc[a / 3][a % 3][1];
+    col[(2 * a) * 21] = acc[a / 3][a % 3][0];
+    col[(2 * a + 1) * 21] = acc[a / 3][a % 3][1];
   }
-  for (int r = 0; r < 3; ++r) col[((size_t)(18 + r) * 21 + j) * g.nbf + bf] = accp[r];
+  for (int r = 0; r < 3; ++r) col[(18 + r) * 21] = accp[r];
 }
 
 template <int K1>
@@ -1983,13 +2000,21 @@ cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const 
     T.cJ[3] = -tab.dE[0][1];
     T.cJ[4] = -tab.dE[0][2];
   }
+  const bool post = !(ds.skip & 64);
+  const size_t ncb = n_bcells(g);
+  double* sp = part + (size_t)K1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2;
   PDST_LAUNCH(k_jacobian<K1><<<grid, JNT, sm, st>>>(g, td, ds, L, x, rhs, out, part, T));
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (!(ds.skip & 64)) {
-    // the epilogue's side products overlap the tile pass (k_jacobian triggers at its start)
+  if (post && !(ds.skip & 128)) {
+    // tile pass -> side products (overlapping it, then waiting for it) -> epilogue
+    PDST_LAUNCH(e = launch_pdl(k_side_products, dim3((unsigned)((ncb + 3) / 4), K1), dim3(128), 0, st, g, td,
+                               (const double*)L.bmat, x, sp));
+    if (e != cudaSuccess) return e;
+  }
+  if (post) {
     const size_t n = jac_post_items(g);
     dim3 pg((unsigned)((n + 127) / 128), K1);
-    PDST_LAUNCH(e = launch_pdl(k_jac_post, pg, dim3(128), 0, st, g, td, L.bmat, x, (const double*)part, rhs, out));
+    PDST_LAUNCH(e = launch_pdl(k_jac_post, pg, dim3(128), 0, st, g, td, (const double*)part, (const double*)sp, rhs, out));
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
@@ -2022,8 +2047,8 @@ extern "C" int pdst_debug_trace(unsigned long long* out, int n) {
 cudaError_t set_tables(const Tables& t) { return cudaMemcpyToSymbol(c_tab, &t, sizeof(Tables)); }
 
 size_t jacobian_scratch(const Geom& g, int k1) {
-  // tile partials
-  return (size_t)k1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2;
+  // tile partials, then the boundary cells' side products
+  return (size_t)k1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2 + (size_t)k1 * 21 * n_bcells(g);
 }
 
 cudaError_t jacobian_apply(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* x,
