@@ -586,6 +586,96 @@ def run_solve(args):
     return 0
 
 
+def run_vcycle(args):
+    """BASELINE configs[4]'s strong-scaling measurement: the space-time multigrid
+    V-cycle (2 + 2 Vanka sweeps per level, coarsest level by FGMRES with Vanka
+    preconditioning) on a strip partition of ONE global mesh over N GPUs
+    (torchrun, NCCL halo exchanges and allreduces) or `--virtual-ranks P` ranks
+    on one GPU.  Time per V-cycle = max over ranks of the device time; value =
+    global dofs / that time (scaling "strong")."""
+    import numpy as np
+    import torch
+
+    from paper_2603_28706_b200 import problem as pb
+    from paper_2603_28706_b200.dist_mg import DistributedStmg, distributed_vcycle, global_levels
+    from paper_2603_28706_b200.partition import DistComm, LocalTransport, StripPartition, TorchDistTransport
+    from paper_2603_28706_b200.stmg import MgConfig
+    from paper_2603_28706_b200.synth import CONFIGS, make_slab_inputs
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    P = ws if ws > 1 else args.virtual_ranks
+    cfg = CONFIGS[args.config]
+    params = pb.ModelParams(cfg.p, cfg.delta, cfg.nu, cfg.nu_inf)
+    conf = pb.DiscretizationConfig(cfg.gamma1, cfg.gamma2, cfg.gamma_cip)
+    syn = make_slab_inputs(cfg)
+    ctx = pb.make_context(cfg.nx, cfg.ny, cfg.k, params, cfg.tau, config=conf, v_minus=syn.v_minus)
+    variant = pb.modified_newton(cfg.nu)
+    min_cells = max(1, cfg.nx >> (args.levels - 1))
+    mg = MgConfig(pre_smooth=2, post_smooth=2, omega=cfg.omega, surrogate=True, rep_fraction=cfg.rep_fraction,
+                  min_cells=min_cells, coarse_solver="fgmres", coarse_sweeps=2, coarse_iters=args.coarse_iters,
+                  coarse_rtol=1e-6)
+    nl = global_levels(cfg.nx, cfg.ny, min_cells)
+    part = StripPartition(cfg.nx, cfg.ny, P, levels=nl)
+    mine = [rank] if ws > 1 else list(range(P))
+    transport = (TorchDistTransport(part.layout(rank), part) if ws > 1
+                 else LocalTransport([part.layout(r) for r in range(P)]))
+    comm = DistComm() if ws > 1 else None
+    dev = torch.device("cuda", local)
+    t0 = time.time()
+    ranks = [DistributedStmg(ctx, syn.U, variant, part, r, mg, device=local) for r in mine]
+    torch.cuda.synchronize()
+    t_build = time.time() - t0
+    nd = part.layout(0).nd
+    rs = [torch.as_tensor(np.concatenate([rk.lay.to_local(syn.x[mu * nd:(mu + 1) * nd]) for mu in range(rk.k1)]),
+                          device=dev) for rk in ranks]
+    del syn
+
+    def cycle():
+        return distributed_vcycle(ranks, rs, transport, comm)
+
+    for _ in range(args.warmup):
+        cycle()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        cycle()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = float(np.median(ts))
+    if dist:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    N = (cfg.k + 1) * nd
+    if rank == 0:
+        print(json.dumps({
+            "metric": "space-time multigrid V-cycle on a strip partition (GDoF/s = global dofs / ms per V-cycle)",
+            "value": N / (ms * 1e6), "unit": "GDoF/s", "n_gpus": ws, "virtual_ranks": P if ws == 1 else None,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_vcycle": ms, "higher_is_better": True,
+            "scaling": "strong", "dtype": "f64", "data": "synthetic (synth.py seeded state)",
+            "config": {"workload": f"{cfg.name}: {cfg.nx}x{cfg.ny} Q2/P1disc, DG({cfg.k}); {nl} levels "
+                                   f"(min_cells={min_cells}), 2+2 Vanka (omega={cfg.omega}, surrogate at "
+                                   f"rep_fraction={cfg.rep_fraction}), coarsest level FGMRES({args.coarse_iters}) "
+                                   f"with 2 Vanka steps, strips aligned to the coarsest cells, "
+                                   f"{part.ghost} ghost rows per side",
+                       "n_dof": N, "parallelism": f"strips x{P}"},
+            "build_s": t_build}), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -601,6 +691,8 @@ def main():
     ap.add_argument("--restart", type=int, default=20)
     ap.add_argument("--max-krylov", type=int, default=60)
     ap.add_argument("--coarse-sweeps", type=int, default=30)
+    ap.add_argument("--vcycle", action="store_true", help="distributed V-cycle timing (configs[4] strong scaling)")
+    ap.add_argument("--coarse-iters", type=int, default=30)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -608,6 +700,8 @@ def main():
         return run_reference(args)
     if args.solve:
         return run_solve(args)
+    if args.vcycle:
+        return run_vcycle(args)
     return run_ours(args)
 
 

@@ -108,6 +108,8 @@ int pdst_cell_maps(pdst_handle* h, int64_t* cell_nodes, int64_t* patch_ids);
 
 /* multigrid: levels 0 (coarsest) .. L-1 (finest = the handle mesh) */
 int pdst_hierarchy(pdst_handle* h, int min_cells, int* num_levels);
+/* exactly `depth` levels (a partition rank's strip coarsens with the global mesh) */
+int pdst_hierarchy_depth(pdst_handle* h, int depth, int* num_levels);
 int pdst_level_sizes(pdst_handle* h, int level, int32_t* nx, int32_t* ny, int64_t* ndof);
 /* surrogate != 0: finest patches from the blended state at rep_fraction; coarse levels exact.
    On ESINGULAR, *bad_level / *bad_patch identify the first singular patch. */

@@ -64,6 +64,7 @@ SIGNATURES = {
     "pdst_multi_axpy": [P, P, P, I64, I, P, P, P, I64, I],
     "pdst_cell_maps": [P, P, P],
     "pdst_hierarchy": [P, I, C.POINTER(I)],
+    "pdst_hierarchy_depth": [P, I, C.POINTER(I)],
     "pdst_level_sizes": [P, I, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(I64)],
     "pdst_patches_build": [P, I, D, C.POINTER(I), C.POINTER(I64)],
     "pdst_patch_matrices": [P, I, P],

@@ -114,7 +114,20 @@ int pdst_cell_maps(pdst_handle* h, int64_t* cell_nodes, int64_t* patch_ids) {
   return PDST_OK;
 }
 
+static int build_hierarchy(pdst_handle* h, int min_cells, int depth, int* num_levels);
+
 int pdst_hierarchy(pdst_handle* h, int min_cells, int* num_levels) {
+  return build_hierarchy(h, min_cells, 0, num_levels);
+}
+
+// A hierarchy of exactly `depth` levels regardless of min_cells: a rank's
+// strip of a partitioned mesh coarsens as often as the global mesh does.
+int pdst_hierarchy_depth(pdst_handle* h, int depth, int* num_levels) {
+  if (depth < 1) return set_error(PDST_EINVAL, "depth must be >= 1");
+  return build_hierarchy(h, 0, depth, num_levels);
+}
+
+static int build_hierarchy(pdst_handle* h, int min_cells, int depth, int* num_levels) {
   if (!h) return set_error(PDST_EINVAL, "null handle");
   CK(cudaSetDevice(h->device));
   for (auto* l : h->levels) delete l;
@@ -131,7 +144,15 @@ int pdst_hierarchy(pdst_handle* h, int min_cells, int* num_levels) {
   while (true) {
     const Level* m = chain.back();
     const int nx = m->g.nx, ny = m->g.ny;
-    if (!(nx > min_cells && nx % 2 == 0 && ny > min_cells && ny % 2 == 0)) break;
+    if (depth > 0) {
+      if ((int)chain.size() == depth) break;
+      if (nx % 2 || ny % 2) {
+        for (auto* l : chain) delete l;
+        return set_error(PDST_EINVAL, "a %dx%d level cannot be coarsened (depth %d)", nx, ny, depth);
+      }
+    } else if (!(nx > min_cells && nx % 2 == 0 && ny > min_cells && ny % 2 == 0)) {
+      break;
+    }
     Level* c = new Level();
     const int cnx = nx / 2, cny = ny / 2;
     // coarse faces inherit the tag of the first fine face of their side (multigrid.py:174-182)

@@ -37,11 +37,21 @@ __all__ = ["StripPartition", "RankLayout", "LocalTransport", "TorchDistTransport
 CUT = 2
 
 
-def strip_bounds(ny: int, nranks: int):
-    """Cell-row ranges [a_r, b_r), as even as possible, each >= 2 rows."""
-    if ny < 2 * nranks:
-        raise ValueError(f"{ny} cell rows cannot give {nranks} strips of >= 2 rows")
-    return [(r * ny // nranks, (r + 1) * ny // nranks) for r in range(nranks)]
+def strip_bounds(ny: int, nranks: int, unit: int = 1):
+    """Cell-row ranges [a_r, b_r), as even as possible in multiples of `unit`
+    rows (the coarsest multigrid cell), each >= 2 units."""
+    if ny % unit:
+        raise ValueError(f"{ny} cell rows are not a multiple of the coarsest cell ({unit} rows)")
+    nu = ny // unit
+    if nu < 2 * nranks:
+        raise ValueError(f"{ny} cell rows cannot give {nranks} strips of >= 2 x {unit} rows")
+    return [(r * nu // nranks * unit, (r + 1) * nu // nranks * unit) for r in range(nranks)]
+
+
+def ghost_rows(levels: int) -> int:
+    """Ghost cell rows per side of the finest local mesh: 2 on every level of a
+    `levels`-level hierarchy (the strip coarsens with the global mesh)."""
+    return 2 if levels <= 1 else 2 ** levels
 
 
 @dataclass(frozen=True)
@@ -54,6 +64,16 @@ class RankLayout:
     b: int  # owned cell rows [a, b)
     c_lo: int
     c_hi: int  # local cell rows [c_lo, c_hi)
+    levels: int = 1  # multigrid levels the partition is aligned for
+    f: int = 0  # this layout's level (0 = finest)
+
+    def level(self, f: int) -> "RankLayout":
+        """The same rank's layout on multigrid level f (every index halved f times)."""
+        if not 0 <= f < self.levels or self.f != 0:
+            raise ValueError(f"level {f} of a {self.levels}-level partition")
+        s = f
+        return RankLayout(self.rank, self.nranks, self.nx >> s, self.ny >> s, self.a >> s, self.b >> s,
+                          self.c_lo >> s, self.c_hi >> s, self.levels, f)
 
     @property
     def ny_loc(self):
@@ -138,9 +158,9 @@ class RankLayout:
         out = []
         if self.rank > 0:
             lo = _layout_of(self, self.rank - 1)
-            out.append((self.rank - 1, self.vel_slice_local(2 * self.c_lo, 2 * self.a),
-                        lo.vel_slice_local(2 * self.c_lo, 2 * self.a)))
-            out.append((self.rank - 1, self.prs_slice_local(self.c_lo, self.a), lo.prs_slice_local(self.c_lo, self.a)))
+            h = max(self.c_lo, self.a - 2)  # two ghost cell rows feed every owned output
+            out.append((self.rank - 1, self.vel_slice_local(2 * h, 2 * self.a), lo.vel_slice_local(2 * h, 2 * self.a)))
+            out.append((self.rank - 1, self.prs_slice_local(h, self.a), lo.prs_slice_local(h, self.a)))
         if not self.last:
             hi = _layout_of(self, self.rank + 1)
             top = min(2 * self.b + 3, 2 * self.c_hi + 1)
@@ -165,17 +185,28 @@ class RankLayout:
 
 
 class StripPartition:
-    def __init__(self, nx: int, ny: int, nranks: int):
-        self.nx, self.ny, self.nranks = nx, ny, nranks
-        self.bounds = strip_bounds(ny, nranks)
+    """Cell-row strips of an nx x ny mesh.  levels > 1 aligns the strips with the
+    coarsest cells of a `levels`-level hierarchy and deepens the ghost region to
+    2^levels rows, so each rank's local mesh coarsens into the global coarse
+    mesh's rows with two ghost rows left on the coarsest level."""
+
+    def __init__(self, nx: int, ny: int, nranks: int, levels: int = 1):
+        self.nx, self.ny, self.nranks, self.levels = nx, ny, nranks, levels
+        self.unit = 2 ** (levels - 1)
+        if nx % self.unit:
+            raise ValueError(f"nx={nx} cannot be coarsened {levels - 1} times")
+        self.bounds = strip_bounds(ny, nranks, self.unit)
+        self.ghost = ghost_rows(levels)
 
     def layout(self, rank: int) -> RankLayout:
         a, b = self.bounds[rank]
-        return RankLayout(rank, self.nranks, self.nx, self.ny, a, b, max(0, a - 2), min(self.ny, b + 2))
+        gh = self.ghost
+        return RankLayout(rank, self.nranks, self.nx, self.ny, a, b, max(0, a - gh), min(self.ny, b + gh), self.levels)
 
 
 def _layout_of(lay: RankLayout, rank: int) -> RankLayout:
-    return StripPartition(lay.nx, lay.ny, lay.nranks).layout(rank)
+    fine = StripPartition(lay.nx << lay.f, lay.ny << lay.f, lay.nranks, lay.levels).layout(rank)
+    return fine.level(lay.f) if lay.f else fine
 
 
 # ---------------------------------------------------------------------------
@@ -189,11 +220,13 @@ class LocalTransport:
     def __init__(self, layouts):
         self.layouts = layouts
 
-    def exchange(self, vectors, plan_name: str, k1: int, add: bool = False):
-        """vectors[r]: rank r's local slab vector (k1 blocks of nd_loc)."""
-        for r, lay in enumerate(self.layouts):
+    def exchange(self, vectors, plan_name: str, k1: int, add: bool = False, level: int = 0):
+        """vectors[r]: rank r's local slab vector (k1 blocks of nd_loc) on
+        multigrid level `level` of the partition."""
+        lays = [l.level(level) for l in self.layouts] if level else self.layouts
+        for r, lay in enumerate(lays):
             for peer, mine, theirs in getattr(lay, plan_name)():
-                nd, ndp = lay.nd_loc, self.layouts[peer].nd_loc
+                nd, ndp = lay.nd_loc, lays[peer].nd_loc
                 for mu in range(k1):
                     dst = vectors[r][mu * nd + mine.start: mu * nd + mine.stop]
                     src = vectors[peer][mu * ndp + theirs.start: mu * ndp + theirs.stop]
@@ -217,12 +250,12 @@ class TorchDistTransport:
         self.lay = layout
         self.part = part
 
-    def exchange(self, vec, plan_name: str, k1: int, add: bool = False):
+    def exchange(self, vec, plan_name: str, k1: int, add: bool = False, level: int = 0):
         import torch
 
         if isinstance(vec, (list, tuple)):  # the distributed_* helpers pass one vector per local rank
             (vec,) = vec
-        lay = self.lay
+        lay = self.lay.level(level) if level else self.lay
         # gloo moves host tensors only: stage device slices through the host
         xdev = vec.device if self.dist.get_backend() == "gloo" else None
         bdev = torch.device("cpu") if xdev is not None and xdev.type == "cuda" else vec.device
@@ -236,6 +269,7 @@ class TorchDistTransport:
             if peer < 0 or peer >= lay.nranks:
                 continue
             pl = self.part.layout(peer)
+            pl = pl.level(level) if level else pl
             for src_rank, _, theirs in getattr(pl, plan_name)():
                 if src_rank != lay.rank:
                     continue

@@ -150,3 +150,97 @@ def test_owned_masks_partition_unity(nx, ny, P, k1):
             g[:] = 0.0
         assert m.sum() == k1 * (len(lay.owned_node_rows) * lay.nnx * 2 + 3 * nx * (lay.b - lay.a))
     assert np.array_equal(tot, np.ones_like(tot))
+
+
+@pytest.mark.parametrize("nx,ny,P,levels", [(16, 32, 2, 3), (32, 32, 4, 3), (16, 48, 3, 3), (8, 64, 2, 4)])
+def test_multilevel_layouts(nx, ny, P, levels):
+    """Strips aligned with the coarsest cells: on every level the owned node rows
+    partition the level's node rows, every local mesh keeps >= 2 ghost rows
+    towards each neighbour (exactly 2 on the coarsest level), level f+1 is level
+    f halved, and every halo / defect / increment slice lies in the peer's owned
+    rows (bit-exact index maps: the distributed V-cycle's exchange plans)."""
+    from paper_2603_28706_b200.partition import StripPartition, ghost_rows
+
+    part = StripPartition(nx, ny, P, levels=levels)
+    assert part.ghost == ghost_rows(levels) == 2 ** levels
+    for f in range(levels):
+        lays = [part.layout(r).level(f) for r in range(P)]
+        nyf = ny >> f
+        covered = np.zeros(2 * nyf + 1, int)
+        for lay in lays:
+            assert lay.ny == nyf and lay.nx == nx >> f and lay.f == f
+            covered[list(lay.owned_node_rows)] += 1
+            if lay.rank > 0:
+                assert lay.a - lay.c_lo >= 2
+            if not lay.last:
+                assert lay.c_hi - lay.b >= 2
+            if f == levels - 1:
+                assert lay.rank == 0 or lay.a - lay.c_lo == 2
+            if f + 1 < levels:
+                nxt = part.layout(lay.rank).level(f + 1)
+                assert (nxt.a, nxt.b, nxt.c_lo, nxt.c_hi) == (lay.a // 2, lay.b // 2, lay.c_lo // 2, lay.c_hi // 2)
+                assert lay.a % 2 == 0 and lay.c_lo % 2 == 0
+            for plan in ("halo_recv", "defect_recv", "inc_recv"):
+                for peer, mine, theirs in getattr(lay, plan)():
+                    pl = lays[peer]
+                    own = pl.owned_node_rows
+                    # the peer's slice, in global node rows / cell rows
+                    if theirs.start < pl.mv_loc:
+                        y0 = theirs.start // (2 * pl.nnx) + 2 * pl.c_lo
+                        y1 = theirs.stop // (2 * pl.nnx) + 2 * pl.c_lo
+                        if plan == "inc_recv":  # the peer's contribution to my first owned row
+                            assert (y0, y1) == (2 * lay.a, 2 * lay.a + 1) and y0 < 2 * pl.c_hi + 1
+                        else:
+                            assert own.start <= y0 and y1 <= own.stop, (f, plan, lay.rank, peer)
+                        assert mine.stop - mine.start == theirs.stop - theirs.start
+                    else:
+                        j0 = (theirs.start - pl.mv_loc) // (3 * pl.nx) + pl.c_lo
+                        j1 = (theirs.stop - pl.mv_loc) // (3 * pl.nx) + pl.c_lo
+                        assert pl.a <= j0 and j1 <= pl.b
+        assert np.array_equal(covered, np.ones_like(covered))
+
+
+def test_multilevel_alignment_validation():
+    from paper_2603_28706_b200.partition import StripPartition
+
+    with pytest.raises(ValueError):
+        StripPartition(16, 30, 2, levels=3)  # 30 rows are not a multiple of 4
+    with pytest.raises(ValueError):
+        StripPartition(16, 16, 3, levels=3)  # 4 coarse rows cannot give 3 strips of >= 2
+    with pytest.raises(ValueError):
+        StripPartition(16, 32, 2, levels=3).layout(0).level(3)
+
+
+def test_gloo_world2_coarse_level_exchange():
+    """The TorchDistTransport plans on a coarse level, two processes over gloo:
+    the same result as the in-process LocalTransport."""
+    import torch.multiprocessing as mp
+
+    mp.spawn(_coarse_worker, args=(2,), nprocs=2, join=True)
+
+
+def _coarse_worker(rank, world):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_28706_b200.partition import LocalTransport, StripPartition, TorchDistTransport
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = "29533"
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        part = StripPartition(8, 32, world, levels=3)
+        k1, f = 2, 1
+        lays = [part.layout(r).level(f) for r in range(world)]
+        gen = torch.Generator().manual_seed(5)
+        vecs = [torch.randn(k1 * l.nd_loc, generator=gen, dtype=torch.float64) for l in lays]
+        for plan, add in (("halo_recv", False), ("defect_recv", False), ("inc_recv", True)):
+            ref = [v.clone() for v in vecs]
+            LocalTransport([part.layout(r) for r in range(world)]).exchange(ref, plan, k1, add=add, level=f)
+            mine = vecs[rank].clone()
+            TorchDistTransport(part.layout(rank), part).exchange(mine, plan, k1, add=add, level=f)
+            assert torch.equal(mine, ref[rank]), plan
+    finally:
+        dist.destroy_process_group()
