@@ -1198,6 +1198,7 @@ __device__ void tile_partials(const Geom& g, const double* part, int mu, int X, 
 __global__ void __launch_bounds__(128, 16) k_jac_post(Geom g, TimeData td, const double* __restrict__ part,
                                                   const double* __restrict__ sp, const double* __restrict__ rhs,
                                                   double* __restrict__ out) {
+  pdl_trigger();  // a PDL-launched consumer (the Vanka GEMV) may start its own prologue
   const int mu = blockIdx.y;
   const StripIdx si(g);
   const size_t ns = si.count(g);
@@ -1296,9 +1297,13 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
   const double* cbase = L.apc + tile * K1 * APC_SLOTS * JNT + threadIdx.x;
 
   TR(0);
-  pdl_trigger();  // k_side_products runs under this grid; k_jac_post waits for both
-  if (valid)
+  if (valid)  // the coefficient stream does not depend on the predecessor
     for (int h = 0; h < PDST_PF_AHEAD; ++h) apc_prefetch_l2(cbase, h);
+  // launched with PDL: x (and the scratch the predecessor's epilogue may still
+  // read) only after the predecessor has completed; then k_side_products may
+  // start under this grid (k_jac_post waits for both)
+  pdl_wait();
+  pdl_trigger();
   for (int nu = 0; nu < K1; ++nu) stage_jac_async(g, x + (size_t)nu * g.nd, nu * 2 * JPLANE, X0, Y0);
   cp_async_wait_all();  // (commits the staging copies and waits for every group)
   __syncthreads();
@@ -2003,8 +2008,8 @@ cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const 
   const bool post = !(ds.skip & 64);
   const size_t ncb = n_bcells(g);
   double* sp = part + (size_t)K1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2;
-  PDST_LAUNCH(k_jacobian<K1><<<grid, JNT, sm, st>>>(g, td, ds, L, x, rhs, out, part, T));
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  PDST_LAUNCH(e = launch_pdl(k_jacobian<K1>, grid, dim3(JNT), sm, st, g, td, ds, L, x, rhs, out, part, T));
+  if (e != cudaSuccess) return e;
   if (post && !(ds.skip & 128)) {
     // tile pass -> side products (overlapping it, then waiting for it) -> epilogue
     PDST_LAUNCH(e = launch_pdl(k_side_products, dim3((unsigned)((ncb + 3) / 4), K1), dim3(128), 0, st, g, td,

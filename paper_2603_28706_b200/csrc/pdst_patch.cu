@@ -270,6 +270,7 @@ __global__ void __launch_bounds__(256) k_vanka_gemv(Geom g, const double* __rest
 __global__ void __launch_bounds__(256) k_vanka_scatter(Geom g, int k1, const double* __restrict__ upd, double omega,
                                                        double* __restrict__ d, int row_lo, int row_hi,
                                                        int inc_only) {
+  pdl_wait();  // PDL-launched behind the GEMV that writes upd
   const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int mu = blockIdx.y, dd = blockIdx.z;
   if (c >= (size_t)g.ncells) return;
@@ -388,8 +389,10 @@ cudaError_t vanka_scatter(const Geom& g, int k1, const double* upd, double omega
                           int row_lo, int row_hi, bool inc_only) {
   if (row_hi < 0) row_hi = g.ny;
   dim3 grid((unsigned)((g.ncells + 255) / 256), k1, 2);
-  PDST_LAUNCH(k_vanka_scatter<<<grid, 256, 0, st>>>(g, k1, upd, omega, d, row_lo, row_hi, inc_only ? 1 : 0));
-  return cudaGetLastError();
+  cudaError_t e;
+  PDST_LAUNCH(e = launch_pdl(k_vanka_scatter, grid, dim3(256), 0, st, g, k1, upd, omega, d, row_lo, row_hi,
+                             inc_only ? 1 : 0));
+  return e;
 }
 
 }  // namespace pdst

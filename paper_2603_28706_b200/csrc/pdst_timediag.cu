@@ -420,6 +420,7 @@ __global__ void __launch_bounds__(tma_pb<NB>() * 21, TMA_CTAS_PER_SM) k_vanka_ge
       gs[buf][p][b][r] = make_double2(gr, gi2);
     }
   };
+  pdl_trigger();
   if (threadIdx.x == 0) {
     for (int st = 0; st < TMA_STAGES; ++st) mbar_init(&full[st], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -428,6 +429,9 @@ __global__ void __launch_bounds__(tma_pb<NB>() * 21, TMA_CTAS_PER_SM) k_vanka_ge
       if (gi < ngroups) issue(gi, st);
     }
   }
+  // launched with PDL: the inverse stream above does not depend on the
+  // defect; everything below does (and upd may still be read by a predecessor)
+  pdl_wait();
   {
     double f[K1] = {};
     load_defect(blockIdx.x, f);
@@ -503,8 +507,10 @@ cudaError_t launch_gemv_tma(const Geom& g, const TimeDiag& td, const double2* bi
   constexpr int PB = tma_pb<NB>();
   const int ngroups = (g.ncells + PB - 1) / PB;
   const int grid = std::min(ngroups, TMA_CTAS_PER_SM * nsm);
-  PDST_LAUNCH(k_vanka_gemv_diag_tma<K1, NB><<<grid, PB * 21, sm, st>>>(g, td, binvT, defect, upd, ngroups));
-  return cudaGetLastError();
+  cudaError_t e;
+  PDST_LAUNCH(e = launch_pdl(k_vanka_gemv_diag_tma<K1, NB>, dim3(grid), dim3(PB * 21), sm, st, g, td, binvT, defect,
+                             upd, ngroups));
+  return e;
 }
 
 }  // namespace
