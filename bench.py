@@ -407,7 +407,7 @@ def run_ours(args):
     ach = b_gemv / t_gemv / 1e9
     traffic = traffic_apply = None
     tp = os.path.join(ROOT, "profiles", "traffic_r01.json")
-    if os.path.exists(tp):  # dram bytes per launch from one `ncu --set full` capture (scripts/ncu_traffic.py)
+    if os.path.exists(tp) and args.config == "cfg2":  # dram bytes per launch, one ncu capture at cfg2 (scripts/ncu_traffic.py)
         try:
             tr = json.load(open(tp))
             traffic, traffic_apply = tr.get("vanka_gemv"), tr.get("jacobian_apply")

@@ -16,6 +16,8 @@
  *   pdst_cell_maps         Discretization.cell_nodes / patch ids    femspace.py:127-140, forms.py:192-196,
  *                                                                   solver/multigrid.py:273-275
  *   pdst_hierarchy         MgGeometry.from_fine                     solver/multigrid.py:164-191
+ *   pdst_hierarchy_depth   MgGeometry.from_fine on a partition      solver/multigrid.py:164-191 (the
+ *                          rank's strip coarsens with the global mesh; no reference counterpart)
  *   pdst_patches_build     StmgPreconditioner patch setup           solver/multigrid.py:261-299, 475-488
  *   pdst_patch_matrices    PatchSet.matrices (read back)            solver/multigrid.py:198-209
  *   pdst_vanka             vanka_smooth                             solver/multigrid.py:327-340
