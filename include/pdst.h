@@ -55,6 +55,14 @@ extern "C" {
 
 #define PDST_HOST 0
 #define PDST_DEVICE 1
+/* PDST_HOST_ASYNC (pdst_jacobian_apply, pdst_jacobian_defect, pdst_vanka only):
+ * host pointers to page-locked memory; the H2D copies run on a copy-in stream,
+ * the kernels on the handle's stream once their inputs have landed, the D2H
+ * copies on a copy-out stream, and the call returns at once, so consecutive
+ * calls overlap their transfers with each other's kernels.  The caller must
+ * not touch the buffers of a call before pdst_sync(h).  Unpinned memory is
+ * rejected (PDST_EINVAL). */
+#define PDST_HOST_ASYNC 2
 
 /* linearization kinds (constitutive.py:133-160) */
 #define PDST_PICARD 0
@@ -91,6 +99,8 @@ int pdst_create(const pdst_mesh* mesh, const pdst_time* time, const pdst_disc* d
                 double tau, int device, void* stream, pdst_handle** out);
 int pdst_destroy(pdst_handle* h);
 int pdst_set_stream(pdst_handle* h, void* stream);
+/* wait for every call of the handle (kernels and PDST_HOST_ASYNC copies) */
+int pdst_sync(pdst_handle* h);
 int pdst_sizes(const pdst_handle* h, int64_t* mv, int64_t* mp, int64_t* nd, int64_t* ndof);
 
 int pdst_set_lifting(pdst_handle* h, const double* g_hat, int where); /* g_hat: Mv or NULL */

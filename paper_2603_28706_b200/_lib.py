@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PDST_LIB") or os.path.join(HERE, "libpdst.so")  # PDST_LIB: experiment builds
 
 OK, EINVAL, EDOMAIN, ESINGULAR, ECUDA, ESTATE, ENOTSUP = range(7)
-HOST, DEVICE = 0, 1
+HOST, DEVICE, HOST_ASYNC = 0, 1, 2
 KIND = {"pic": 0, "exn": 1, "modn": 2}
 
 
@@ -65,6 +65,7 @@ SIGNATURES = {
     "pdst_cell_maps": [P, P, P],
     "pdst_hierarchy": [P, I, C.POINTER(I)],
     "pdst_hierarchy_depth": [P, I, C.POINTER(I)],
+    "pdst_sync": [P],
     "pdst_level_sizes": [P, I, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(I64)],
     "pdst_patches_build": [P, I, D, C.POINTER(I), C.POINTER(I64)],
     "pdst_patch_matrices": [P, I, P],

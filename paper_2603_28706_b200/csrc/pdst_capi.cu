@@ -123,6 +123,106 @@ int pdst::finish_out(pdst_handle* h, double* host, const double* dev, size_t n, 
   return PDST_OK;
 }
 
+static int ensure_async(pdst_handle* h, pdst::AsyncSlot& s) {
+  if (!h->copy_in) {
+    CK(cudaStreamCreateWithFlags(&h->copy_in, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h->copy_out, cudaStreamNonBlocking));
+  }
+  if (!s.in_done) {
+    CK(cudaEventCreateWithFlags(&s.in_done, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&s.use_done, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&s.out_done, cudaEventDisableTiming));
+  }
+  return PDST_OK;
+}
+
+static bool pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+const double* pdst::async_in(pdst_handle* h, AsyncSlot& s, const double* p, size_t n, int* err) {
+  if (!p) return nullptr;
+  if ((*err = ensure_async(h, s))) return nullptr;
+  if (!pinned(p)) {
+    *err = fail(PDST_EINVAL, "PDST_HOST_ASYNC needs page-locked host memory");
+    return nullptr;
+  }
+  double* d = s.buf.ensure(n);
+  if (!d) {
+    *err = fail(PDST_ECUDA, "out of device memory (%zu doubles)", n);
+    return nullptr;
+  }
+  cudaError_t e = cudaSuccess;
+  // the slot's previous kernels and D2H must be done with it; a D2H into p must have landed
+  if (s.used) e = cudaStreamWaitEvent(h->copy_in, s.use_done, 0);
+  if (e == cudaSuccess && s.outed) e = cudaStreamWaitEvent(h->copy_in, s.out_done, 0);
+  for (auto& po : h->pending_out)
+    if (e == cudaSuccess && po.first == p) e = cudaStreamWaitEvent(h->copy_in, po.second, 0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d, p, n * sizeof(double), cudaMemcpyHostToDevice, h->copy_in);
+  if (e == cudaSuccess) e = cudaEventRecord(s.in_done, h->copy_in);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(h->stream, s.in_done, 0);
+  if (e != cudaSuccess) {
+    *err = cuda_fail(e, "async H2D");
+    return nullptr;
+  }
+  return d;
+}
+
+double* pdst::async_out_ptr(pdst_handle* h, AsyncSlot& s, size_t n, int* err) {
+  if ((*err = ensure_async(h, s))) return nullptr;
+  double* d = s.buf.ensure(n);
+  if (!d) {
+    *err = fail(PDST_ECUDA, "out of device memory (%zu doubles)", n);
+    return nullptr;
+  }
+  if (s.outed) {  // its previous D2H must have read it before the kernels overwrite it
+    cudaError_t e = cudaStreamWaitEvent(h->stream, s.out_done, 0);
+    if (e != cudaSuccess) {
+      *err = cuda_fail(e, "async order");
+      return nullptr;
+    }
+  }
+  return d;
+}
+
+int pdst::async_used(pdst_handle* h, AsyncSlot& s) {
+  CK(cudaEventRecord(s.use_done, h->stream));
+  s.used = true;
+  return PDST_OK;
+}
+
+int pdst::async_out(pdst_handle* h, AsyncSlot& s, double* p, size_t n) {
+  if (!pinned(p)) return fail(PDST_EINVAL, "PDST_HOST_ASYNC needs page-locked host memory");
+  if (int e = async_used(h, s)) return e;
+  CK(cudaStreamWaitEvent(h->copy_out, s.use_done, 0));
+  CK(cudaMemcpyAsync(p, s.buf.ptr, n * sizeof(double), cudaMemcpyDeviceToHost, h->copy_out));
+  CK(cudaEventRecord(s.out_done, h->copy_out));
+  s.outed = true;
+  bool found = false;
+  for (auto& po : h->pending_out)
+    if (po.first == p) {
+      po.second = s.out_done;
+      found = true;
+    }
+  if (!found) h->pending_out.push_back({p, s.out_done});
+  return PDST_OK;
+}
+
+int pdst_sync(pdst_handle* h) {
+  if (!h) return fail(PDST_EINVAL, "null handle");
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamSynchronize(h->stream));
+  if (h->copy_in) CK(cudaStreamSynchronize(h->copy_in));
+  if (h->copy_out) CK(cudaStreamSynchronize(h->copy_out));
+  h->pending_out.clear();
+  return PDST_OK;
+}
+
 int pdst::check_where(int where) {
   if (where != PDST_HOST && where != PDST_DEVICE) return fail(PDST_EINVAL, "where must be PDST_HOST or PDST_DEVICE");
   return PDST_OK;
@@ -300,6 +400,25 @@ int pdst_linearize(pdst_handle* h, const double* U, int kind, double sigma_max, 
 
 static int jac_common(pdst_handle* h, const double* x, const double* r, double* y, int where) {
   if (!h || !x || !y) return fail(PDST_EINVAL, "null argument");
+  if (where == PDST_HOST_ASYNC) {
+    if (!h->linearized) return fail(PDST_ESTATE, "jacobian used before pdst_linearize");
+    CK(cudaSetDevice(h->device));
+    const size_t n = (size_t)h->td.k1 * h->g.nd;
+    int err = PDST_OK;
+    const double* xd = async_in(h, h->as_x, x, n, &err);
+    if (err) return err;
+    const double* rd = async_in(h, h->as_r, r, n, &err);
+    if (err) return err;
+    double* yd = async_out_ptr(h, h->as_y, n, &err);
+    if (err) return err;
+    double* part = h->jpart.ensure_zeroed(jacobian_scratch(h->g, h->td.k1));
+    if (!part) return fail(PDST_ECUDA, "out of device memory");
+    CK(PDST_TIMED(h, PK_JACOBIAN, jacobian_apply(h->g, h->td, h->ds, lin_of(h), xd, rd, yd, part, h->stream)));
+    if (int e = async_used(h, h->as_x)) return e;
+    if (r)
+      if (int e = async_used(h, h->as_r)) return e;
+    return async_out(h, h->as_y, y, n);
+  }
   if (int e = check_where(where)) return e;
   if (!h->linearized) return fail(PDST_ESTATE, "jacobian used before pdst_linearize");
   CK(cudaSetDevice(h->device));

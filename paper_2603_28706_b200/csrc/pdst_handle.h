@@ -103,6 +103,23 @@ struct Profiler {
 
 }  // namespace pdst
 
+namespace pdst {
+// Device staging buffer of one PDST_HOST_ASYNC argument with the events that
+// order it: in_done (H2D finished, on the copy-in stream), use_done (the last
+// kernel reading / writing it finished, on the compute stream), out_done (its
+// D2H finished, on the copy-out stream).
+struct AsyncSlot {
+  DeviceBuffer buf;
+  cudaEvent_t in_done = nullptr, use_done = nullptr, out_done = nullptr;
+  bool used = false, outed = false;
+  ~AsyncSlot() {
+    if (in_done) cudaEventDestroy(in_done);
+    if (use_done) cudaEventDestroy(use_done);
+    if (out_done) cudaEventDestroy(out_done);
+  }
+};
+}  // namespace pdst
+
 struct pdst_handle {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -138,6 +155,12 @@ struct pdst_handle {
 
   pdst::Profiler prof;
 
+  // PDST_HOST_ASYNC: copy streams, one slot per (entry point, argument), and
+  // the host buffers with a D2H in flight (an H2D from one waits for it)
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  pdst::AsyncSlot as_x, as_r, as_y, as_d, as_vr;
+  std::vector<std::pair<const void*, cudaEvent_t>> pending_out;
+
   // multigrid
   std::vector<pdst::Level*> levels;  // 0 = coarsest
   int min_cells = 0;
@@ -155,6 +178,8 @@ struct pdst_handle {
   bool patches_valid = false;
 
   ~pdst_handle() {
+    if (copy_in) cudaStreamDestroy(copy_in);
+    if (copy_out) cudaStreamDestroy(copy_out);
     for (auto* l : levels) delete l;
     if (dirichlet) cudaFree(dirichlet);
   }
@@ -168,6 +193,14 @@ const double* stage_in(pdst_handle* h, DeviceBuffer& buf, const double* p, size_
 double* out_ptr(DeviceBuffer& buf, double* p, size_t n, int where);
 int finish_out(pdst_handle* h, double* host, const double* dev, size_t n, int where);
 int check_where(int where);
+// PDST_HOST_ASYNC staging (page-locked host buffers; see pdst.h): H2D of p into
+// the slot on the copy-in stream, ordered before the next compute-stream work;
+// async_used after the kernels that touched the slot; async_out D2H of the slot
+// into p on the copy-out stream after them.  The call returns at once.
+const double* async_in(pdst_handle* h, AsyncSlot& s, const double* p, size_t n, int* err);
+double* async_out_ptr(pdst_handle* h, AsyncSlot& s, size_t n, int* err);
+int async_used(pdst_handle* h, AsyncSlot& s);
+int async_out(pdst_handle* h, AsyncSlot& s, double* p, size_t n);
 
 // Kernel classes for pdst_profile_read.
 enum { PK_JACOBIAN = 0, PK_VANKA_GEMV = 1, PK_VANKA_SCATTER = 2, PK_RESIDUAL = 3, PK_TRANSFER = 4, PK_LEVEL = 5 };

@@ -440,6 +440,23 @@ static int vanka_level(pdst_handle* h, int l, double* d, const double* r, int st
 
 int pdst_vanka(pdst_handle* h, int level, double* d, const double* r, int steps, double omega, int where) {
   if (!h || !d || !r) return set_error(PDST_EINVAL, "null argument");
+  if (where == PDST_HOST_ASYNC) {
+    if (int e = check_level(h, level)) return e;
+    if (!h->patches_valid) return set_error(PDST_ESTATE, "vanka before pdst_patches_build");
+    if (steps < 0) return set_error(PDST_EINVAL, "steps must be >= 0");
+    CK(cudaSetDevice(h->device));
+    const size_t n = (size_t)h->td.k1 * h->levels[level]->g.nd;
+    int err = PDST_OK;
+    // r first: it does not wait for anything, while d (in and out) waits for
+    // the D2H of the previous call's d, so r's copy overlaps that round trip
+    const double* rd = async_in(h, h->as_vr, r, n, &err);
+    if (err) return err;
+    double* dd = const_cast<double*>(async_in(h, h->as_d, d, n, &err));
+    if (err) return err;
+    if (int e = vanka_level(h, level, dd, rd, steps, omega)) return e;
+    if (int e = async_used(h, h->as_vr)) return e;
+    return async_out(h, h->as_d, d, n);
+  }
   if (int e = check_where(where)) return e;
   if (int e = check_level(h, level)) return e;
   if (!h->patches_valid) return set_error(PDST_ESTATE, "vanka before pdst_patches_build");

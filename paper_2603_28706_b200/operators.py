@@ -126,7 +126,10 @@ class SlabDevice:
             pass
 
     # -- argument handling ---------------------------------------------------
-    def where(self, *arrays):
+    def where(self, *arrays, asynchronous=False):
+        """PDST_DEVICE for torch CUDA tensors (torch's current stream), else
+        PDST_HOST (copied, synchronous) or, with asynchronous=True,
+        PDST_HOST_ASYNC (page-locked numpy buffers; call sync() before using them)."""
         dev = [a for a in arrays if _is_torch(a)]
         if dev:
             if len(dev) != len([a for a in arrays if a is not None]):
@@ -134,7 +137,11 @@ class SlabDevice:
             L.check(L.lib().pdst_set_stream(self.h, _torch_stream(dev[0].device)))
             return L.DEVICE
         L.check(L.lib().pdst_set_stream(self.h, None))
-        return L.HOST
+        return L.HOST_ASYNC if asynchronous else L.HOST
+
+    def sync(self):
+        """Wait for every call of this handle, incl. asynchronous host copies."""
+        L.check(L.lib().pdst_sync(self.h), "pdst_sync")
 
     @staticmethod
     def empty_like(a, shape=None):
@@ -166,10 +173,15 @@ class SlabJacobian:
     def shape(self):
         return (self.dev.ndof, self.dev.ndof)
 
-    def matvec(self, x, out=None):
+    def matvec(self, x, out=None, asynchronous=False):
+        """y = J x.  asynchronous=True (host arrays in page-locked memory, `out`
+        given): returns at once; the copies overlap other calls' kernels and
+        transfers; `self.dev.sync()` before reading `out` or reusing `x`."""
         xc = _f64(x)
+        if asynchronous and (out is None or _is_torch(xc)):
+            raise TypeError("asynchronous matvec needs page-locked host x and out")
         y = self.dev.empty_like(xc) if out is None else out
-        w = self.dev.where(xc, y)
+        w = self.dev.where(xc, y, asynchronous=asynchronous)
         L.check(L.lib().pdst_jacobian_apply(self.dev.h, L.vptr(xc), L.vptr(y), w), "pdst_jacobian_apply")
         return y
 

@@ -68,10 +68,14 @@ class VankaLevel:
         L.check(L.lib().pdst_cell_maps(self.dev.h, L.vptr(cn), L.vptr(ids)), "pdst_cell_maps")
         return ids
 
-    def smooth(self, d, r, steps, omega, inplace=False):
+    def smooth(self, d, r, steps, omega, inplace=False, asynchronous=False):
         """d <- d + omega sum_K R_K' A_K^-1 R_K (r - A d), `steps` times.
         Returns a new array unless inplace (a device tensor, or a C-contiguous
-        writable float64 host array -- e.g. pinned -- updated through the C ABI)."""
+        writable float64 host array -- e.g. pinned -- updated through the C ABI).
+        asynchronous=True (inplace, page-locked host d and r): returns at once,
+        `self.dev.sync()` before reading d or reusing r."""
+        if asynchronous and not inplace:
+            raise TypeError("asynchronous smoothing is in place")
         rc_ = _f64(r)
         if _is_torch(d):
             out = d if inplace else d.clone()
@@ -81,7 +85,7 @@ class VankaLevel:
             out = d
         else:
             out = np.array(d, dtype=np.float64, copy=True)
-        w = self.dev.where(out, rc_)
+        w = self.dev.where(out, rc_, asynchronous=asynchronous)
         L.check(L.lib().pdst_vanka(self.dev.h, self.index, L.vptr(out), L.vptr(rc_), int(steps), float(omega), w),
                 "pdst_vanka")
         return out

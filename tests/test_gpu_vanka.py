@@ -78,3 +78,58 @@ def test_singular_patch_reported():
     with pytest.raises(SingularPatchError) as ei:
         VankaLevel(ctx, U, pb.picard())
     assert ei.value.patch == 0
+
+
+def test_async_host_calls_match_sync():
+    """PDST_HOST_ASYNC (page-locked numpy buffers, copies on their own streams,
+    calls return at once): a pipelined sequence of applies and in-place Vanka
+    sweeps on the same host buffers gives bitwise the synchronous results, and
+    unpinned memory is rejected."""
+    import torch
+
+    from paper_2603_28706_b200 import problem as pb
+    from paper_2603_28706_b200.operators import SlabJacobian
+    from paper_2603_28706_b200.smoother import VankaLevel
+    from paper_2603_28706_b200.synth import CONFIGS, make_slab_inputs
+
+    cfg = CONFIGS["cfg1"]
+    params = pb.ModelParams(cfg.p, cfg.delta, cfg.nu, cfg.nu_inf)
+    conf = pb.DiscretizationConfig(cfg.gamma1, cfg.gamma2, cfg.gamma_cip)
+    syn = make_slab_inputs(cfg)
+    ctx = pb.make_context(cfg.nx, cfg.ny, cfg.k, params, cfg.tau, config=conf, v_minus=syn.v_minus)
+    var = pb.modified_newton(cfg.nu)
+    jac = SlabJacobian(ctx, syn.U, var)
+    lvl = VankaLevel(ctx, syn.U, var, surrogate=True, rep_fraction=cfg.rep_fraction, jac=jac)
+
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+        t.numpy()[...] = a
+        return t.numpy()
+
+    xh, rh, dh, yh = pinned(syn.x), pinned(syn.x), pinned(syn.d0), pinned(np.zeros_like(syn.x))
+    ys, d = [], syn.d0.copy()
+    for i in range(3):
+        ys.append(jac.matvec(syn.x * (i + 1)))
+        d = lvl.smooth(d, syn.x, 1, cfg.omega)
+    outs = []
+    for i in range(3):
+        xh[...] = syn.x * (i + 1)
+        jac.matvec(xh, out=yh, asynchronous=True)
+        lvl.smooth(dh, rh, 1, cfg.omega, inplace=True, asynchronous=True)
+        jac.dev.sync()
+        outs.append(yh.copy())
+    for a, b in zip(outs, ys):
+        assert np.array_equal(a, b)
+    assert np.array_equal(dh, d)
+    # back to back without syncs in between: the d round trip stays ordered
+    d2 = d.copy()
+    for _ in range(4):
+        d2 = lvl.smooth(d2, syn.x, 1, cfg.omega)
+    for _ in range(4):
+        jac.matvec(xh, out=yh, asynchronous=True)
+        lvl.smooth(dh, rh, 1, cfg.omega, inplace=True, asynchronous=True)
+    jac.dev.sync()
+    assert np.array_equal(dh, d2)
+    assert np.array_equal(yh, ys[2])
+    with pytest.raises(ValueError):
+        jac.matvec(syn.x.copy(), out=np.zeros_like(syn.x), asynchronous=True)
