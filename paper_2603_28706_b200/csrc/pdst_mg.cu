@@ -211,7 +211,7 @@ static int invert_level_patches(pdst_handle* h, int l, int* badi, int* bad_level
   const int init = INT_MAX;
   CK(cudaMemcpyAsync(badi, &init, sizeof(int), cudaMemcpyHostToDevice, h->stream));
   if (lv->diag) {
-    CK(patch_invert_diag(lv->g, lv->tdiag, lv->spatial.ptr, reinterpret_cast<double2*>(lv->binv.ptr), badi,
+    CK(patch_invert_diag(lv->g, lv->tdiag, lv->spatial.ptr, lv->binv.ptr, badi,
                          h->stream));
   } else {
     double* invs = lv->invs.ensure(nc * D * D);
@@ -313,7 +313,7 @@ int pdst_patches_build(pdst_handle* h, int surrogate, double rep_fraction, int* 
   pa.spatial = nullptr;
   if (fl->diag) {
     pa.spatial = fl->spatial.ensure(nc * 441);
-    if (!pa.spatial || !fl->binv.ensure(nc * 441 * 2 * fl->tdiag.nblk))
+    if (!pa.spatial || !fl->binv.ensure(nc * fl->tdiag.pstride))
       return set_error(PDST_ECUDA, "out of device memory (diagonalized patches)");
   }
   CK(patch_assemble(pa, h->stream));
@@ -399,7 +399,7 @@ int pdst_patch_info(pdst_handle* h, int level, int32_t* D, int32_t* diag_blocks,
   if (D) *D = l->D;
   if (diag_blocks) *diag_blocks = l->diag ? l->tdiag.nblk : 0;
   if (bytes_per_patch)
-    *bytes_per_patch = l->diag ? (int64_t)l->tdiag.nblk * 441 * 16 : (int64_t)l->D * l->D * 8;
+    *bytes_per_patch = l->diag ? (int64_t)l->tdiag.pstride * 8 : (int64_t)l->D * l->D * 8;
   return PDST_OK;
 }
 
@@ -429,7 +429,7 @@ static int vanka_level(pdst_handle* h, int l, double* d, const double* r, int st
   for (int s = 0; s < steps; ++s) {
     if (int e = level_defect(h, l, d, r, defect)) return e;
     if (lv->diag)
-      CK(PDST_TIMED(h, PK_VANKA_GEMV, vanka_gemv_diag(g, lv->tdiag, reinterpret_cast<const double2*>(lv->binv.ptr),
+      CK(PDST_TIMED(h, PK_VANKA_GEMV, vanka_gemv_diag(g, lv->tdiag, lv->binv.ptr,
                                                        defect, upd, h->stream)));
     else
       CK(PDST_TIMED(h, PK_VANKA_GEMV, vanka_gemv(g, k1, lv->invs.ptr, defect, upd, h->stream)));
@@ -492,7 +492,7 @@ int pdst_vanka_increment(pdst_handle* h, int level, const double* defect, double
   double* upd = h->upd.ensure((size_t)h->g.ncells * 21 * k1);
   if (!od || !upd) return set_error(PDST_ECUDA, "out of device memory");
   if (lv->diag)
-    CK(PDST_TIMED(h, PK_VANKA_GEMV, vanka_gemv_diag(g, lv->tdiag, reinterpret_cast<const double2*>(lv->binv.ptr), dd,
+    CK(PDST_TIMED(h, PK_VANKA_GEMV, vanka_gemv_diag(g, lv->tdiag, lv->binv.ptr, dd,
                                                      upd, h->stream)));
   else
     CK(PDST_TIMED(h, PK_VANKA_GEMV, vanka_gemv(g, k1, lv->invs.ptr, dd, upd, h->stream)));

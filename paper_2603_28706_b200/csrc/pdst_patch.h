@@ -30,15 +30,20 @@ struct TimeDiag {
   double V_re[MAXK1 * MAXK1], V_im[MAXK1 * MAXK1];        // V[mu][b] for stored blocks b (column b)
   double Vi_re[MAXK1 * MAXK1], Vi_im[MAXK1 * MAXK1];      // Vinv[b][mu] rows for stored blocks
   double itw[MAXK1];           // 1 / (tau w_mu)
+  // per-patch storage: block b at boff[b] doubles into the patch, a conjugate
+  // pair's complex inverse as 441 double2, a real eigenvalue's (real) inverse
+  // as 441 doubles padded to 442 (16-byte multiple for the bulk copies)
+  int boff[MAXK1];
+  int pstride;                 // doubles per patch
 };
 
 // Host: diagonalize S = diag(tau w)^-1 K_t (k1 <= 4). Returns false when S is
 // defective / ill-conditioned (the caller keeps the full real inverses).
 bool time_diagonalize(int k1, const double* K_t, const double* tau_w, TimeDiag& out);
 
-cudaError_t patch_invert_diag(const Geom& g, const TimeDiag& td, const double* spatial, double2* binvT, int* bad,
+cudaError_t patch_invert_diag(const Geom& g, const TimeDiag& td, const double* spatial, double* binvT, int* bad,
                               cudaStream_t st);
-cudaError_t vanka_gemv_diag(const Geom& g, const TimeDiag& td, const double2* binvT, const double* defect,
+cudaError_t vanka_gemv_diag(const Geom& g, const TimeDiag& td, const double* binvT, const double* defect,
                             double* upd, cudaStream_t st);
 
 cudaError_t patch_assemble(const PatchArgs& a, cudaStream_t st);

@@ -8,9 +8,9 @@
 //   A_K^-1 = (V (x) I) blockdiag_i[(lam_i Mhat + Jhat)^-1] (V^-1 W^-1 (x) I).
 // The Radau eigenvalues of S come in complex-conjugate pairs (plus one real
 // eigenvalue for odd k+1), so each patch stores one complex 21x21 inverse per
-// pair: 882 doubles instead of 42^2 = 1764 for DG(1), 1764 (incl. the real
-// block stored as complex) instead of 63^2 = 3969 for DG(2).  The Vanka sweep
-// then streams half / less than half the bytes.  Mathematically identical to
+// pair and one real 21x21 inverse per real eigenvalue: 882 doubles instead of
+// 42^2 = 1764 for DG(1), 882 + 442 (one pad) instead of 63^2 = 3969 for DG(2),
+// 442 instead of 441 for DG(0).  The Vanka sweep streams those bytes.  Mathematically identical to
 // np.linalg.inv(A_K) @ e (multigrid.py:290-291, 338); rounding differs.
 #include <cuda_runtime.h>
 
@@ -209,9 +209,12 @@ bool time_diagonalize(int k1, const double* K_t, const double* tau_w, TimeDiag& 
     }
   if (!(res <= 1e-12 * snorm * vn) || !(vn * vin < 1e6)) return false;
   out.nblk = nk;
+  int off = 0;
   for (int s = 0; s < nk; ++s) {
     const int b = keep[s];
     out.pair[s] = partner[b] >= 0 ? 1 : 0;
+    out.boff[s] = off;
+    off += out.pair[s] ? 882 : 442;
     out.lam_re[s] = lam[b].real();
     out.lam_im[s] = lam[b].imag();
     for (int mu = 0; mu < k1; ++mu) {
@@ -221,6 +224,7 @@ bool time_diagonalize(int k1, const double* K_t, const double* tau_w, TimeDiag& 
       out.Vi_im[s * MAXK1 + mu] = Vi[b * k1 + mu].imag();
     }
   }
+  out.pstride = off;
   return true;
 }
 
@@ -242,7 +246,7 @@ __device__ __forceinline__ double cabs1(double2 z) { return fabs(z.x) + fabs(z.y
 // complex) in shared memory, Gauss-Jordan with partial pivoting (izamax /
 // dcabs1 pivot choice as zgetrf), output transposed binvT[K][b][j][r].
 __global__ void __launch_bounds__(128) k_invert_diag(Geom g, TimeDiag td, const double* __restrict__ spatial,
-                                                     double2* __restrict__ binvT, int* __restrict__ bad) {
+                                                     double* __restrict__ binvT, int* __restrict__ bad) {
   constexpr int N = 21, LD = 22, WPB = 4;
   __shared__ double2 sm[WPB][N * LD];
   __shared__ double2 colb[WPB][N];
@@ -326,10 +330,19 @@ __global__ void __launch_bounds__(128) k_invert_diag(Geom g, TimeDiag td, const 
     }
     __syncwarp();
   }
-  double2* dst = binvT + ((size_t)K * td.nblk + b) * N * N;
-  for (int idx = lane; idx < N * N; idx += 32) {
-    const int j = idx / N, r = idx - j * N;
-    dst[idx] = A[r * LD + j];
+  double* base = binvT + (size_t)K * td.pstride + td.boff[b];
+  if (td.pair[b]) {
+    double2* dst = reinterpret_cast<double2*>(base);
+    for (int idx = lane; idx < N * N; idx += 32) {
+      const int j = idx / N, r = idx - j * N;
+      dst[idx] = A[r * LD + j];
+    }
+  } else {  // real eigenvalue: the inverse is real (every imaginary part is an exact 0)
+    for (int idx = lane; idx < N * N; idx += 32) {
+      const int j = idx / N, r = idx - j * N;
+      base[idx] = A[r * LD + j].x;
+    }
+    if (lane == 0) base[N * N] = 0.0;  // pad
   }
 }
 
@@ -373,32 +386,34 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                : "memory");
 }
 
+// Pipeline shape per stored block count: PB patches per group, STAGES groups
+// in flight per CTA, 2 CTAs per SM; threads (patch p, block b, row r).
 template <int NB>
-__host__ __device__ constexpr int tma_pb() { return NB == 1 ? 4 : NB == 2 ? 2 : 1; }
-constexpr int TMA_STAGES = 3;
+__host__ __device__ constexpr int tma_pb() { return NB == 1 ? 4 : NB == 2 ? 4 : 2; }
+template <int NB>
+__host__ __device__ constexpr int tma_stages() { return NB == 1 ? 3 : 2; }
 constexpr int TMA_CTAS_PER_SM = 2;
 template <int NB>
-__host__ __device__ constexpr unsigned tma_patch_bytes() { return (unsigned)NB * 441u * 16u; }
-template <int NB>
-__host__ __device__ constexpr size_t tma_smem() { return (size_t)TMA_STAGES * tma_pb<NB>() * tma_patch_bytes<NB>(); }
+__host__ __device__ constexpr size_t tma_smem_max() { return (size_t)tma_stages<NB>() * tma_pb<NB>() * NB * 882 * 8; }
 
 template <int K1, int NB>
-__global__ void __launch_bounds__(tma_pb<NB>() * 21, TMA_CTAS_PER_SM) k_vanka_gemv_diag_tma(Geom g, TimeDiag td,
-                                                                           const double2* __restrict__ binvT,
+__global__ void __launch_bounds__(tma_pb<NB>() * NB * 21, TMA_CTAS_PER_SM) k_vanka_gemv_diag_tma(Geom g, TimeDiag td,
+                                                                           const double* __restrict__ binvT,
                                                                            const double* __restrict__ defect,
                                                                            double* __restrict__ upd, int ngroups) {
-  constexpr int PB = tma_pb<NB>();
-  constexpr unsigned PBYTES = tma_patch_bytes<NB>();
+  constexpr int PB = tma_pb<NB>(), STAGES = tma_stages<NB>();
+  const unsigned PBYTES = (unsigned)td.pstride * 8u;
   extern __shared__ __align__(128) unsigned char tma_ring[];
-  __shared__ double2 gs[2][PB][NB][21];  // eigen-transformed defects, double buffered
-  __shared__ __align__(8) uint64_t full[TMA_STAGES];
-  const int p = threadIdx.x / 21, r = threadIdx.x % 21;
-  auto stage_ptr = [&](int st) { return reinterpret_cast<double2*>(tma_ring + (size_t)st * PB * PBYTES); };
+  __shared__ double2 gs[2][PB][NB][21];               // eigen-transformed defects, double buffered
+  __shared__ double2 hs[NB > 1 ? 2 : 1][PB][NB][21];  // per-block products (NB > 1), double buffered
+  __shared__ __align__(8) uint64_t full[STAGES];
+  const int p = threadIdx.x / (21 * NB), b = (threadIdx.x / 21) % NB, r = threadIdx.x % 21;
+  auto stage_ptr = [&](int st) { return reinterpret_cast<double*>(tma_ring + (size_t)st * PB * PBYTES); };
   auto issue = [&](int gi, int st) {  // one thread: arm the stage's barrier and start its copies
     const int K0 = gi * PB, cnt = min(PB, g.ncells - K0);
     mbar_expect_tx(&full[st], (unsigned)cnt * PBYTES);
     for (int q = 0; q < cnt; ++q)
-      bulk_g2s(stage_ptr(st) + (size_t)q * NB * 441, binvT + (size_t)(K0 + q) * NB * 441, PBYTES, &full[st]);
+      bulk_g2s(stage_ptr(st) + (size_t)q * td.pstride, binvT + (size_t)(K0 + q) * td.pstride, PBYTES, &full[st]);
   };
   // defect of this thread's (patch, row) in group gi (the loads, issued early)
   auto load_defect = [&](int gi, double f[K1]) {
@@ -408,23 +423,30 @@ __global__ void __launch_bounds__(tma_pb<NB>() * 21, TMA_CTAS_PER_SM) k_vanka_ge
       for (int mu = 0; mu < K1; ++mu) f[mu] = __ldg(defect + patch_dof_d(g, K, 21 * mu + r));
     }
   };
-  auto transform = [&](const double f[K1], int buf) {
+  auto transform = [&](const double f[K1], int buf) {  // this thread's block b
+    double gr = 0.0, gi2 = 0.0;
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      double gr = 0.0, gi2 = 0.0;
-#pragma unroll
-      for (int mu = 0; mu < K1; ++mu) {
-        gr = fma(td.Vi_re[b * MAXK1 + mu], f[mu] * td.itw[mu], gr);
-        gi2 = fma(td.Vi_im[b * MAXK1 + mu], f[mu] * td.itw[mu], gi2);
-      }
-      gs[buf][p][b][r] = make_double2(gr, gi2);
+    for (int mu = 0; mu < K1; ++mu) {
+      gr = fma(td.Vi_re[b * MAXK1 + mu], f[mu] * td.itw[mu], gr);
+      gi2 = fma(td.Vi_im[b * MAXK1 + mu], f[mu] * td.itw[mu], gi2);
     }
+    gs[buf][p][b][r] = make_double2(gr, gi2);
+  };
+  // the mu output of (patch, row) from all blocks' products, blocks in order
+  auto emit = [&](int K, const double* hr, const double* hi, int mu) {
+    double sacc = 0.0;
+#pragma unroll
+    for (int bb = 0; bb < NB; ++bb) {
+      const double re = td.V_re[mu * MAXK1 + bb] * hr[bb] - td.V_im[mu * MAXK1 + bb] * hi[bb];
+      sacc += td.pair[bb] ? 2.0 * re : re;
+    }
+    upd[(size_t)(21 * mu + r) * g.ncells + K] = sacc;
   };
   pdl_trigger();
   if (threadIdx.x == 0) {
-    for (int st = 0; st < TMA_STAGES; ++st) mbar_init(&full[st], 1);
+    for (int st = 0; st < STAGES; ++st) mbar_init(&full[st], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    for (int st = 0; st < TMA_STAGES; ++st) {
+    for (int st = 0; st < STAGES; ++st) {
       const int gi = blockIdx.x + st * gridDim.x;
       if (gi < ngroups) issue(gi, st);
     }
@@ -440,18 +462,17 @@ __global__ void __launch_bounds__(tma_pb<NB>() * 21, TMA_CTAS_PER_SM) k_vanka_ge
   __syncthreads();
   int it = 0;
   for (int gi = blockIdx.x; gi < ngroups; gi += gridDim.x, ++it) {
-    const int st = it % TMA_STAGES, buf = it & 1;
-    const unsigned parity = (unsigned)(it / TMA_STAGES) & 1u;
+    const int st = it % STAGES, buf = it & 1;
+    const unsigned parity = (unsigned)(it / STAGES) & 1u;
     const int K = gi * PB + p;
     double fn[K1] = {};
     load_defect(gi + gridDim.x, fn);  // next group's defect, consumed after this group's product
     mbar_wait(&full[st], parity);
     if (K < g.ncells) {
-      const double2* blk = stage_ptr(st) + (size_t)p * NB * 441;
-      double hr[NB], hi[NB];
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const double2* col = blk + (size_t)b * 441 + r;
+      const double* blk = stage_ptr(st) + (size_t)p * td.pstride + td.boff[b];
+      double hr, hi;
+      if (td.pair[b]) {
+        const double2* col = reinterpret_cast<const double2*>(blk) + r;
         double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
 #pragma unroll 7
         for (int j = 0; j < 21; ++j) {
@@ -462,25 +483,39 @@ __global__ void __launch_bounds__(tma_pb<NB>() * 21, TMA_CTAS_PER_SM) k_vanka_ge
           ai = fma(m.x, v.y, ai);
           bi = fma(m.y, v.x, bi);
         }
-        hr[b] = ar - br;
-        hi[b] = ai + bi;
+        hr = ar - br;
+        hi = ai + bi;
+      } else {  // real block, real transformed defect: half the bytes, same sums
+        const double* col = blk + r;
+        double ar = 0.0;
+#pragma unroll 7
+        for (int j = 0; j < 21; ++j) ar = fma(col[21 * j], gs[buf][p][b][j].x, ar);
+        hr = ar;
+        hi = 0.0;
       }
-      double* o = upd + K;
+      if constexpr (NB == 1) {
 #pragma unroll
-      for (int mu = 0; mu < K1; ++mu) {
-        double sacc = 0.0;
-#pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          const double re = td.V_re[mu * MAXK1 + b] * hr[b] - td.V_im[mu * MAXK1 + b] * hi[b];
-          sacc += td.pair[b] ? 2.0 * re : re;
-        }
-        o[(size_t)(21 * mu + r) * g.ncells] = sacc;
+        for (int mu = 0; mu < K1; ++mu) emit(K, &hr, &hi, mu);
+      } else {
+        hs[buf][p][b][r] = make_double2(hr, hi);
       }
     }
     transform(fn, buf ^ 1);
-    __syncthreads();  // stage st is free, gs[buf ^ 1] is complete
+    __syncthreads();  // stage st is free, gs[buf ^ 1] and hs[buf] are complete
+    if constexpr (NB > 1) {
+      if (K < g.ncells) {
+        double hrs[NB], his[NB];
+#pragma unroll
+        for (int bb = 0; bb < NB; ++bb) {
+          const double2 h2 = hs[buf][p][bb][r];
+          hrs[bb] = h2.x;
+          his[bb] = h2.y;
+        }
+        for (int mu = b; mu < K1; mu += NB) emit(K, hrs, his, mu);
+      }
+    }
     if (threadIdx.x == 0) {
-      const int gn = gi + TMA_STAGES * gridDim.x;
+      const int gn = gi + STAGES * gridDim.x;
       if (gn < ngroups) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads before the async writes
         issue(gn, st);
@@ -490,14 +525,14 @@ __global__ void __launch_bounds__(tma_pb<NB>() * 21, TMA_CTAS_PER_SM) k_vanka_ge
 }
 
 template <int K1, int NB>
-cudaError_t launch_gemv_tma(const Geom& g, const TimeDiag& td, const double2* binvT, const double* defect,
+cudaError_t launch_gemv_tma(const Geom& g, const TimeDiag& td, const double* binvT, const double* defect,
                             double* upd, cudaStream_t st) {
   static int nsm = 0;
   static bool configured = false;
-  const size_t sm = tma_smem<NB>();
+  const size_t smax = tma_smem_max<NB>();
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(k_vanka_gemv_diag_tma<K1, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sm);
+                                         (int)smax);
     if (e != cudaSuccess) return e;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -505,24 +540,25 @@ cudaError_t launch_gemv_tma(const Geom& g, const TimeDiag& td, const double2* bi
     configured = true;
   }
   constexpr int PB = tma_pb<NB>();
+  const size_t sm = (size_t)tma_stages<NB>() * PB * td.pstride * sizeof(double);
   const int ngroups = (g.ncells + PB - 1) / PB;
   const int grid = std::min(ngroups, TMA_CTAS_PER_SM * nsm);
   cudaError_t e;
-  PDST_LAUNCH(e = launch_pdl(k_vanka_gemv_diag_tma<K1, NB>, dim3(grid), dim3(PB * 21), sm, st, g, td, binvT, defect,
+  PDST_LAUNCH(e = launch_pdl(k_vanka_gemv_diag_tma<K1, NB>, dim3(grid), dim3(PB * NB * 21), sm, st, g, td, binvT, defect,
                              upd, ngroups));
   return e;
 }
 
 }  // namespace
 
-cudaError_t patch_invert_diag(const Geom& g, const TimeDiag& td, const double* spatial, double2* binvT, int* bad,
+cudaError_t patch_invert_diag(const Geom& g, const TimeDiag& td, const double* spatial, double* binvT, int* bad,
                               cudaStream_t st) {
   const int tasks = g.ncells * td.nblk;
   PDST_LAUNCH(k_invert_diag<<<(tasks + 3) / 4, 128, 0, st>>>(g, td, spatial, binvT, bad));
   return cudaGetLastError();
 }
 
-cudaError_t vanka_gemv_diag(const Geom& g, const TimeDiag& td, const double2* binvT, const double* defect,
+cudaError_t vanka_gemv_diag(const Geom& g, const TimeDiag& td, const double* binvT, const double* defect,
                             double* upd, cudaStream_t st) {
   switch (td.k1 * 10 + td.nblk) {
     case 11: return launch_gemv_tma<1, 1>(g, td, binvT, defect, upd, st);
