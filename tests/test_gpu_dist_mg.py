@@ -113,3 +113,41 @@ def test_distributed_fgmres_with_vcycle():
     assert res.iterations == ref.iterations
     x = _gather(ranks, res.x, syn.x.size)
     assert_close(x, ref.x.cpu().numpy(), 1e-8, "distributed FGMRES + V-cycle")
+
+
+def test_two_process_vcycle_and_fgmres(tmp_path):
+    """The same cycle and FGMRES as two processes (TorchDistTransport, DistComm
+    over gloo staged through the host) against the single domain."""
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    import torch
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, here)
+    from dist_mg_worker import problem
+
+    from paper_2603_28706_b200.krylov import KrylovConfig, fgmres
+    from paper_2603_28706_b200.operators import MassNorm, SlabJacobian
+    from paper_2603_28706_b200.stmg import StmgPreconditioner
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = str(s.getsockname()[1])
+    s.close()
+    outs = [str(tmp_path / f"r{r}.npz") for r in range(2)]
+    procs = [subprocess.Popen([sys.executable, os.path.join(here, "dist_mg_worker.py"), str(r), "2", port, outs[r]])
+             for r in range(2)]
+    assert [p.wait(timeout=600) for p in procs] == [0, 0]
+    parts = [np.load(o) for o in outs]
+    cfg, ctx, syn, var, mg = problem()
+    jac = SlabJacobian(ctx, syn.U, var)
+    pre = StmgPreconditioner(ctx, syn.U, var, mg, jac=jac)
+    z_ref = pre.apply(syn.x)
+    assert_close(parts[0]["z"] + parts[1]["z"], z_ref, TOL, "two-process V-cycle")
+    ref = fgmres(jac.matvec, torch.as_tensor(syn.x, device="cuda"), 1e-8, KrylovConfig(restart=20, max_iters=20),
+                 precond=lambda v, out=None: pre.apply(v, out=out), mass=MassNorm(ctx, dev=jac.dev))
+    assert int(parts[0]["iters"]) == int(parts[1]["iters"]) == ref.iterations
+    assert_close(parts[0]["x"] + parts[1]["x"], ref.x.cpu().numpy(), 1e-8, "two-process FGMRES + V-cycle")
