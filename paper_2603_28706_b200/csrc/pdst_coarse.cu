@@ -178,13 +178,13 @@ __device__ __forceinline__ double face_entry(const LevelOp& op, int mu, int axis
   }
   const double* F = axis == 0 ? op.fv + ((size_t)mu * (op.g.nx - 1) * op.g.ny + (size_t)fj * (op.g.nx - 1) + fi) * 324
                               : op.fh + ((size_t)mu * op.g.nx * (op.g.ny - 1) + (size_t)fj * op.g.nx + fi) * 324;
-  return F[((sA * 2 + sB) * 9 + a) * 9 + b];
+  return F[((sA * 2 + sB) * 9 + b) * 9 + a];  // column-major 9x9 node blocks
 }
 
 __device__ __forceinline__ double cell_entry(const LevelOp& op, int mu, int c, int i, int j) {
-  // finest level: column-major ET[c][j][i]; coarse levels: row-major ecell[c][i][j]
+  // column-major on every level (ET[c][j][i]): a thread per row reads coalesced columns
   const size_t base = ((size_t)mu * op.g.ncells + c) * 441;
-  return op.fine ? op.ecell[base + (size_t)j * 21 + i] : op.ecell[base + (size_t)i * 21 + j];
+  return op.ecell[base + (size_t)j * 21 + i];
 }
 
 // Galerkin coarse cell block: one CTA (448 threads) per (coarse cell, mu).
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(448) k_galerkin_cells(LevelOp f, Geom gc, doub
         __syncthreads();
       }
   }
-  if (t < 441) ecell_c[((size_t)mu * gc.ncells + C) * 441 + t] = acc;
+  if (t < 441) ecell_c[((size_t)mu * gc.ncells + C) * 441 + (size_t)j * 21 + i] = acc;  // column-major
 }
 
 // Galerkin coarse face blocks from the two fine faces lying on the coarse face.
@@ -294,109 +294,126 @@ __global__ void __launch_bounds__(324) k_galerkin_faces(LevelOp f, Geom gc, doub
   }
   if (t < 324) {
     double* dst = axis == 0 ? fv_c + ((size_t)mu * nface + fc) * 324 : fh_c + ((size_t)mu * nface + fc) * 324;
-    dst[t] = acc;
+    dst[((sA * 2 + sB) * 9 + b) * 9 + a] = acc;  // column-major node blocks
   }
 }
 
-// Coarse level apply (node gather, deterministic):
-// y_mu = tau w_mu J_mu x_mu + sum_nu K_t[mu,nu] M x_nu (multigrid.py:234-248);
-// rhs != null gives y = rhs - A x.
-__global__ void k_level_apply(LevelOp op, TimeData td, const double* __restrict__ x, const double* __restrict__ rhs,
-                              double* __restrict__ y) {
+// Coarse level apply (multigrid.py:234-248), two PDL-chained kernels:
+// y_mu = tau w_mu J_mu x_mu + sum_nu K_t[mu,nu] M x_nu; rhs != null gives
+// y = rhs - A x.
+//  1. k_level_products: per cell c and local row i, the cell's whole share
+//        cp[mu][c][i] = sum_j E_c[i][j] x_c[j]
+//                     + sum over c's faces f (right, top, left, bottom) of
+//                       sum_sB,b F_f[s(c)][sB][a][b] x_sB[b][d]   (i = 2a + d < 18)
+//     one thread per row; the column-major element / face blocks make each
+//     warp-wide column load one contiguous segment; every block entry is read
+//     once (a face block's two row halves by its two cells); x_c staged in
+//     shared memory.
+//     The share is tau w_mu (that) + the cell's temporal mass share
+//     hx hy (M1 (x) M1)(K_t x) (the assembled Q2 mass is the sum of them).
+//  2. k_level_gather: every dof sums the <= 4 cell shares containing it in a
+//     fixed order and finishes (deterministic).
+constexpr int LP_CELLS = 12;  // cells per CTA (12 x 21 = 252 threads)
+constexpr int LP_NT = 252;
+
+__global__ void __launch_bounds__(LP_NT, 4) k_level_products(LevelOp op, TimeData td, const double* __restrict__ x,
+                                                             double* __restrict__ cp) {
+  pdl_trigger();  // the gather may launch; it waits for this grid
+  const Geom& g = op.g;
+  const int mu = blockIdx.y;
+  const double* xm = x + (size_t)mu * g.nd;
+  __shared__ double xs[LP_CELLS][21];
+  __shared__ double xt[LP_CELLS][18];  // sum_nu K_t[mu,nu] x_nu at the cell's velocity dofs
+  const int t = threadIdx.x;
+  const int p = t / 21, i = t % 21;
+  const int c = blockIdx.x * LP_CELLS + p;
+  const bool ok = p < LP_CELLS && c < g.ncells;
+  const int cx = ok ? c % g.nx : 0, cy = ok ? c / g.nx : 0;
+  auto xnode = [&](int cell_x, int cell_y, int b, int d) {
+    return xm[2 * ((size_t)(2 * cell_y + b / 3) * g.nnx + 2 * cell_x + b % 3) + d];
+  };
+  if (ok) {
+    xs[p][i] = i < 18 ? xnode(cx, cy, i >> 1, i & 1) : xm[g.mv + 3 * (size_t)c + i - 18];
+    if (i < 18) {
+      const int b = i >> 1;
+      const size_t o = 2 * ((size_t)(2 * cy + b / 3) * g.nnx + 2 * cx + b % 3) + (i & 1);
+      double v = 0.0;
+      for (int nu = 0; nu < td.k1; ++nu) v = fma(td.K_t[mu * td.k1 + nu], x[(size_t)nu * g.nd + o], v);
+      xt[p][i] = v;
+    }
+  }
+  __syncthreads();
+  if (!ok) return;
+  const double* E = op.ecell + ((size_t)mu * g.ncells + c) * 441 + i;  // column j at E[21 j]
+  double s = 0.0;
+#pragma unroll 7
+  for (int j = 0; j < 21; ++j) s = fma(__ldg(E + 21 * j), xs[p][j], s);
+  if (i < 18) {
+    const int a = i >> 1, d = i & 1;
+    // faces of c: right (c = left cell of a vertical face), top, left, bottom
+#pragma unroll 1
+    for (int k = 0; k < 4; ++k) {
+      const int axis = k & 1;
+      const bool own_first = k < 2;  // c is the left / lower cell
+      const int fi = axis == 0 ? (own_first ? cx : cx - 1) : cx;
+      const int fj = axis == 0 ? cy : (own_first ? cy : cy - 1);
+      const int nfx = axis == 0 ? g.nx - 1 : g.nx, nfy = axis == 0 ? g.ny : g.ny - 1;
+      if (fi < 0 || fj < 0 || fi >= nfx || fj >= nfy) continue;
+      const int sA = own_first ? 0 : 1;
+      const int ox = axis == 0 ? (own_first ? 1 : -1) : 0, oy = axis == 1 ? (own_first ? 1 : -1) : 0;
+      const size_t f = (size_t)fj * nfx + fi;
+      const size_t nf = (size_t)nfx * nfy;
+      const double* F = (axis == 0 ? op.fv : op.fh) + ((size_t)mu * nf + f) * 324 + (size_t)sA * 162 + a;
+#pragma unroll
+      for (int sB = 0; sB < 2; ++sB) {
+        const bool own = (sB == sA);
+        const int bxc = own ? cx : cx + ox, byc = own ? cy : cy + oy;
+#pragma unroll
+        for (int b = 0; b < 9; ++b) {
+          const double xv = own ? xs[p][2 * b + d] : xnode(bxc, byc, b, d);
+          s = fma(__ldg(F + sB * 81 + b * 9), xv, s);  // F[sA][sB][b][a], column-major node block
+        }
+      }
+    }
+  }
+  double out = td.tau_w[mu] * s;
+  if (i < 18) {  // + the cell's temporal mass share hx hy (M1 (x) M1) (K_t x)
+    const int a = i >> 1, d = i & 1, ay = a / 3, ax = a % 3;
+    double m = 0.0;
+#pragma unroll
+    for (int b = 0; b < 9; ++b) m = fma(c_tab.M1[ay][b / 3] * c_tab.M1[ax][b % 3], xt[p][2 * b + d], m);
+    out = fma(g.hx * g.hy, m, out);
+  }
+  cp[((size_t)mu * g.ncells + c) * 21 + i] = out;
+}
+
+__global__ void k_level_gather(LevelOp op, const double* __restrict__ cp, const double* __restrict__ rhs,
+                               double* __restrict__ y) {
   const Geom& g = op.g;
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int mu = blockIdx.y;
   const size_t nn = (size_t)g.nnx * g.nny;
-  const double* xm = x + (size_t)mu * g.nd;
-  double out0 = 0.0, out1 = 0.0;
-  size_t o0;
+  pdl_wait();
   if (t < nn) {
     const int X = (int)(t % g.nnx), Y = (int)(t / g.nnx);
-    o0 = (size_t)mu * g.nd + 2 * t;
+    const size_t o0 = (size_t)mu * g.nd + 2 * t;
     double j0 = 0.0, j1 = 0.0;
     for (int cy = max(0, (Y - 1) / 2); cy <= min(g.ny - 1, Y / 2); ++cy)
       for (int cx = max(0, (X - 1) / 2); cx <= min(g.nx - 1, X / 2); ++cx) {
         const int c = cy * g.nx + cx;
         const int a = 3 * (Y - 2 * cy) + (X - 2 * cx);
-        for (int jj = 0; jj < 21; ++jj) {
-          double xv;
-          if (jj < 18) {
-            const int bb = jj >> 1;
-            xv = xm[2 * ((size_t)(2 * cy + bb / 3) * g.nnx + 2 * cx + bb % 3) + (jj & 1)];
-          } else {
-            xv = xm[g.mv + 3 * (size_t)c + jj - 18];
-          }
-          j0 = fma(cell_entry(op, mu, c, 2 * a, jj), xv, j0);
-          j1 = fma(cell_entry(op, mu, c, 2 * a + 1, jj), xv, j1);
-        }
+        const double* q = cp + ((size_t)mu * g.ncells + c) * 21 + 2 * a;
+        j0 += q[0];
+        j1 += q[1];
       }
-    // faces whose two cells contain the node
-    for (int axis = 0; axis < 2; ++axis) {
-      const int nfx = axis == 0 ? g.nx - 1 : g.nx, nfy = axis == 0 ? g.ny : g.ny - 1;
-      const int xr = axis == 0 ? 4 : 2, yr = axis == 0 ? 2 : 4;  // node extent of L u R
-      for (int fj = max(0, (Y - yr + 1) / 2); fj <= min(nfy - 1, Y / 2); ++fj)
-        for (int fi = max(0, (X - xr + 1) / 2); fi <= min(nfx - 1, X / 2); ++fi) {
-          const int cl = fj * g.nx + fi;
-          const int cr = axis == 0 ? cl + 1 : cl + g.nx;
-          for (int sA = 0; sA < 2; ++sA) {
-            const int cA = sA == 0 ? cl : cr;
-            const int ax = X - 2 * (cA % g.nx), ay = Y - 2 * (cA / g.nx);
-            if (ax < 0 || ax > 2 || ay < 0 || ay > 2) continue;
-            const int a = 3 * ay + ax;
-            for (int sB = 0; sB < 2; ++sB) {
-              const int cB = sB == 0 ? cl : cr;
-              const int bxo = 2 * (cB % g.nx), byo = 2 * (cB / g.nx);
-              for (int bb = 0; bb < 9; ++bb) {
-                const double fvv = face_entry(op, mu, axis, fi, fj, sA, a, sB, bb);
-                const size_t nb = (size_t)(byo + bb / 3) * g.nnx + bxo + bb % 3;
-                j0 = fma(fvv, xm[2 * nb], j0);
-                j1 = fma(fvv, xm[2 * nb + 1], j1);
-              }
-            }
-          }
-        }
-    }
-    // temporal mass coupling on the coarse Q2 mass
-    double m0 = 0.0, m1 = 0.0;
-    for (int Yp = max(0, Y - 2); Yp <= min(g.nny - 1, Y + 2); ++Yp) {
-      const double my = m1g(Y, Yp, g.ny);
-      if (my == 0.0) continue;
-      for (int Xp = max(0, X - 2); Xp <= min(g.nnx - 1, X + 2); ++Xp) {
-        const double mx = m1g(X, Xp, g.nx);
-        if (mx == 0.0) continue;
-        const size_t nb = (size_t)Yp * g.nnx + Xp;
-        double x0 = 0.0, x1 = 0.0;
-        for (int nu = 0; nu < td.k1; ++nu) {
-          x0 = fma(td.K_t[mu * td.k1 + nu], x[(size_t)nu * g.nd + 2 * nb], x0);
-          x1 = fma(td.K_t[mu * td.k1 + nu], x[(size_t)nu * g.nd + 2 * nb + 1], x1);
-        }
-        m0 = fma(my * mx, x0, m0);
-        m1 = fma(my * mx, x1, m1);
-      }
-    }
-    const double h = g.hx * g.hy;
-    out0 = td.tau_w[mu] * j0 + h * m0;
-    out1 = td.tau_w[mu] * j1 + h * m1;
-    y[o0] = rhs ? rhs[o0] - out0 : out0;
-    y[o0 + 1] = rhs ? rhs[o0 + 1] - out1 : out1;
+    y[o0] = rhs ? rhs[o0] - j0 : j0;
+    y[o0 + 1] = rhs ? rhs[o0 + 1] - j1 : j1;
   } else if (t < nn + (size_t)g.ncells) {
-    const int c = (int)(t - nn);
-    const int cx = c % g.nx, cy = c / g.nx;
+    const size_t c = t - nn;
+    const double* q = cp + ((size_t)mu * g.ncells + c) * 21 + 18;
     for (int r = 0; r < 3; ++r) {
-      double s = 0.0;
-      for (int jj = 0; jj < 21; ++jj) {
-        double xv;
-        if (jj < 18) {
-          const int bb = jj >> 1;
-          xv = xm[2 * ((size_t)(2 * cy + bb / 3) * g.nnx + 2 * cx + bb % 3) + (jj & 1)];
-        } else {
-          xv = xm[g.mv + 3 * (size_t)c + jj - 18];
-        }
-        s = fma(cell_entry(op, mu, c, 18 + r, jj), xv, s);
-      }
-      const size_t o = (size_t)mu * g.nd + g.mv + 3 * (size_t)c + r;
-      const double v = td.tau_w[mu] * s;
-      y[o] = rhs ? rhs[o] - v : v;
+      const size_t o = (size_t)mu * g.nd + g.mv + 3 * c + r;
+      y[o] = rhs ? rhs[o] - q[r] : q[r];
     }
   }
 }
@@ -693,11 +710,20 @@ cudaError_t galerkin(const LevelOp& fine, const Geom& gc, int k1, double* ecell_
   return cudaGetLastError();
 }
 
+size_t level_apply_scratch(const Geom& g, int k1) { return (size_t)k1 * 21 * (size_t)g.ncells; }
+
 cudaError_t level_apply(const LevelOp& op, const TimeData& td, const double* x, const double* rhs, double* y,
-                        cudaStream_t st) {
-  const size_t n = (size_t)op.g.nnx * op.g.nny + op.g.ncells;
-  PDST_LAUNCH(k_level_apply<<<dim3((unsigned)((n + 127) / 128), td.k1), 128, 0, st>>>(op, td, x, rhs, y));
-  return cudaGetLastError();
+                        double* scratch, cudaStream_t st) {
+  if (!scratch) return cudaErrorMemoryAllocation;
+  const Geom& g = op.g;
+  const int ncb = (g.ncells + LP_CELLS - 1) / LP_CELLS;
+  PDST_LAUNCH(k_level_products<<<dim3((unsigned)ncb, td.k1), LP_NT, 0, st>>>(op, td, x, scratch));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const size_t n = (size_t)g.nnx * g.nny + g.ncells;
+  PDST_LAUNCH(e = launch_pdl(k_level_gather, dim3((unsigned)((n + 127) / 128), td.k1), dim3(128), 0, st, op,
+                             (const double*)scratch, rhs, y));
+  return e;
 }
 
 cudaError_t patch_assemble_level(const LevelOp& op, const TimeData& td, double* mats, cudaStream_t st) {

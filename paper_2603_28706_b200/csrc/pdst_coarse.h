@@ -24,8 +24,11 @@ cudaError_t prolong(const Geom& gc, const Geom& gf, int k1, const double* ec, do
 cudaError_t restrict_(const Geom& gc, const Geom& gf, int k1, const double* rf, double* rc, cudaStream_t st);
 cudaError_t galerkin(const LevelOp& fine, const Geom& gc, int k1, double* ecell_c, double* fv_c, double* fh_c,
                      cudaStream_t st);
+// y = A x (rhs == null) or rhs - A x on a coarse level; scratch holds
+// level_apply_scratch() doubles (the element products).
+size_t level_apply_scratch(const Geom& g, int k1);
 cudaError_t level_apply(const LevelOp& op, const TimeData& td, const double* x, const double* rhs, double* y,
-                        cudaStream_t st);
+                        double* scratch, cudaStream_t st);
 cudaError_t patch_assemble_level(const LevelOp& op, const TimeData& td, double* mats, cudaStream_t st);
 // Dense coarsest slab matrix, optional pressure pinning, in-place inverse.
 // scratch: >= 1 double; piv: >= n ints; bad: 1 int (set to 1 when singular).

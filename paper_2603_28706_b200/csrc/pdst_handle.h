@@ -152,6 +152,7 @@ struct pdst_handle {
   // surrogate (representative-state) linearization and patch scratch
   pdst::DeviceBuffer state_rep, eta_rep, gam_rep, etaf_rep, gamf_rep;
   pdst::DeviceBuffer ET, upd, defect, ibuf;
+  pdst::DeviceBuffer lvs;  // coarse level apply: element products (level_apply_scratch)
 
   pdst::Profiler prof;
 

@@ -186,6 +186,11 @@ int pdst_level_sizes(pdst_handle* h, int level, int32_t* nx, int32_t* ny, int64_
   return PDST_OK;
 }
 
+// Scratch of a coarse level apply (grown to the largest level used).
+static double* level_scratch(pdst_handle* h, int l) {
+  return h->lvs.ensure(level_apply_scratch(h->levels[l]->g, h->td.k1));
+}
+
 // Level operator descriptor of level l (element form).
 static LevelOp level_op(pdst_handle* h, int l) {
   Level* lv = h->levels[l];
@@ -412,7 +417,7 @@ static int level_defect(pdst_handle* h, int l, const double* x, const double* r,
     CK(PDST_TIMED(h, PK_JACOBIAN,
                   jacobian_apply(h->g, h->td, h->ds, lin_of(h), x, r, y, part, h->stream)));
   } else {
-    CK(PDST_TIMED(h, PK_LEVEL, level_apply(level_op(h, l), h->td, x, r, y, h->stream)));
+    CK(PDST_TIMED(h, PK_LEVEL, level_apply(level_op(h, l), h->td, x, r, y, level_scratch(h, l), h->stream)));
   }
   return PDST_OK;
 }
@@ -514,7 +519,7 @@ int pdst_level_apply(pdst_handle* h, int level, const double* x, double* y, int 
   if (err) return err;
   double* yd = out_ptr(h->scratch_b, y, n, where);
   if (!yd) return set_error(PDST_ECUDA, "out of device memory");
-  CK(PDST_TIMED(h, PK_LEVEL, level_apply(level_op(h, level), h->td, xd, nullptr, yd, h->stream)));
+  CK(PDST_TIMED(h, PK_LEVEL, level_apply(level_op(h, level), h->td, xd, nullptr, yd, level_scratch(h, level), h->stream)));
   return finish_out(h, y, yd, n, where);
 }
 
@@ -591,7 +596,7 @@ static int coarse_fgmres(pdst_handle* h, const double* b, double* z) {
     double* Zj = Z + (size_t)j * n;
     CK(cudaMemsetAsync(Zj, 0, n * sizeof(double), h->stream));
     if (int e = vanka_level(h, 0, Zj, Vj, h->coarse_sweeps, h->coarse_omega)) return e;
-    CK(PDST_TIMED(h, PK_LEVEL, level_apply(level_op(h, 0), h->td, Zj, nullptr, w, h->stream)));
+    CK(PDST_TIMED(h, PK_LEVEL, level_apply(level_op(h, 0), h->td, Zj, nullptr, w, level_scratch(h, 0), h->stream)));
     for (int pass = 0; pass < 2; ++pass) {  // CGS2
       CK(multidot(V, (int64_t)n, j + 1, w, (int64_t)n, part, dvec, h->stream));
       CK(multi_axpy(V, nullptr, (int64_t)n, j + 1, dvec, w, nullptr, (int64_t)n, h->stream));
