@@ -159,7 +159,7 @@ def run_distributed(args):
     from paper_2603_28706_b200 import _lib as L
     from paper_2603_28706_b200 import problem as pb
     from paper_2603_28706_b200.partition import (DistributedSlab, LocalTransport, StripPartition,
-                                                 TorchDistTransport, distributed_apply, distributed_vanka_step)
+                                                 TorchDistTransport, distributed_apply_and_vanka_step)
     from paper_2603_28706_b200.synth import CONFIGS, make_slab_inputs
 
     ws, rank, local = dist_env()
@@ -199,8 +199,7 @@ def run_distributed(args):
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
 
     def step():
-        distributed_apply(ranks, xs, transport)
-        distributed_vanka_step(ranks, ds, rs, cfg.omega, transport)
+        distributed_apply_and_vanka_step(ranks, xs, ds, rs, cfg.omega, transport)
 
     for _ in range(args.warmup):
         step()
@@ -248,8 +247,7 @@ def run_distributed(args):
             r.copy_(h, non_blocking=True)
         for h, d in zip(hd, ds):
             d.copy_(h, non_blocking=True)
-        ys = distributed_apply(ranks, xs, transport)
-        distributed_vanka_step(ranks, ds, rs, cfg.omega, transport)
+        ys = distributed_apply_and_vanka_step(ranks, xs, ds, rs, cfg.omega, transport)
         for h, y in zip(hy, ys):
             h.copy_(y, non_blocking=True)
         for h, d in zip(hd, ds):
@@ -277,8 +275,8 @@ def run_distributed(args):
         "config": {"workload": f"{base.name} strips: {cfg.nx}x{cfg.ny} global mesh on [0,1]x[0,{P}], "
                                f"{base.ny} cell rows per rank + 2 ghost rows per side, DG({cfg.k}), modN, surrogate "
                                f"patches, omega={cfg.omega}",
-                   "n_dof": N, "step": "distributed Jacobian apply + Vanka step (x halo, defect row, increment "
-                                       "reverse-add exchanges)",
+                   "n_dof": N, "step": "distributed Jacobian apply + Vanka step (x and d halos in one grouped exchange, "
+                                       "defect row, increment reverse-add)",
                    "l2": "flushed between timed steps (256 MiB write, outside events)",
                    "parallelism": (f"strip partition x{ws} over NCCL send/recv" if ws > 1 else
                                    f"{P} virtual ranks on one GPU (LocalTransport)")},

@@ -32,7 +32,7 @@ from dataclasses import dataclass
 import numpy as np
 
 __all__ = ["StripPartition", "RankLayout", "LocalTransport", "TorchDistTransport", "DistributedSlab", "DistComm",
-           "distributed_fgmres"]
+           "distributed_fgmres", "distributed_apply_and_vanka_step"]
 
 CUT = 2
 
@@ -235,6 +235,15 @@ class LocalTransport:
                     else:
                         dst[...] = src
 
+    def exchange_many(self, items, k1: int, level: int = 0):
+        """Several independent exchanges [(vectors, plan_name, add), ...]."""
+        _exchange_many_sequential(self, items, k1, level)
+
+
+def _exchange_many_sequential(transport, items, k1, level=0):
+    for vectors, plan_name, add in items:
+        transport.exchange(vectors, plan_name, k1, add=add, level=level)
+
 
 class TorchDistTransport:
     """One rank per process over torch.distributed point-to-point messages.
@@ -250,7 +259,8 @@ class TorchDistTransport:
         self.lay = layout
         self.part = part
 
-    def exchange(self, vec, plan_name: str, k1: int, add: bool = False, level: int = 0):
+    def _ops(self, vec, plan_name, k1, level):
+        """(P2P ops, received-buffer placements) of one exchange of `vec`."""
         import torch
 
         if isinstance(vec, (list, tuple)):  # the distributed_* helpers pass one vector per local rank
@@ -262,7 +272,7 @@ class TorchDistTransport:
         ops, recv_bufs = [], []
         for peer, mine, _ in getattr(lay, plan_name)():
             buf = torch.empty((k1, mine.stop - mine.start), dtype=vec.dtype, device=bdev)
-            recv_bufs.append((mine, buf))
+            recv_bufs.append((vec, lay, mine, buf))
             ops.append(self.dist.P2POp(self.dist.irecv, buf, peer))
         # what my neighbours receive from me
         for peer in (lay.rank - 1, lay.rank + 1):
@@ -275,16 +285,34 @@ class TorchDistTransport:
                     continue
                 v2 = vec.view(k1, lay.nd_loc)
                 ops.append(self.dist.P2POp(self.dist.isend, v2[:, theirs].contiguous().to(bdev), peer))
-        if ops:
-            for req in self.dist.batch_isend_irecv(ops):
-                req.wait()
-        v2 = vec.view(k1, lay.nd_loc)
-        for mine, buf in recv_bufs:
+        return ops, recv_bufs
+
+    @staticmethod
+    def _place(recv_bufs, k1, add):
+        for vec, lay, mine, buf in recv_bufs:
+            v2 = vec.view(k1, lay.nd_loc)
             buf = buf.to(vec.device)
             if add:
                 v2[:, mine] += buf
             else:
                 v2[:, mine] = buf
+
+    def exchange(self, vec, plan_name: str, k1: int, add: bool = False, level: int = 0):
+        self.exchange_many([(vec, plan_name, add)], k1, level)
+
+    def exchange_many(self, items, k1: int, level: int = 0):
+        """Several independent exchanges [(vec, plan_name, add), ...] in ONE
+        grouped send/recv (one NCCL launch and latency instead of one each)."""
+        ops, placements = [], []
+        for vec, plan_name, add in items:
+            o, r = self._ops(vec, plan_name, k1, level)
+            ops += o
+            placements.append((r, add))
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+        for r, add in placements:
+            self._place(r, k1, add)
 
 
 # ---------------------------------------------------------------------------
@@ -372,6 +400,26 @@ def distributed_vanka_step(ranks, ds, rs, omega, transport):
     for d, inc in zip(ds, incs):
         d += inc
     return ds
+
+
+def distributed_apply_and_vanka_step(ranks, xs, ds, rs, omega, transport):
+    """y = J x and one Vanka step on d (rhs r) on every rank, the two
+    independent x / d halos in one grouped exchange.  Returns the ys; ds
+    updated in place.  Same results as distributed_apply then
+    distributed_vanka_step."""
+    k1 = ranks[0].k1
+    transport.exchange_many([(xs, "halo_recv", False), (ds, "halo_recv", False)], k1)
+    ys = [rk.jac.matvec(x) for rk, x in zip(ranks, xs)]
+    defects = [rk.jac.defect(d, r) for rk, d, r in zip(ranks, ds, rs)]
+    transport.exchange(defects, "defect_recv", k1)
+    incs = []
+    for rk, df in zip(ranks, defects):
+        lay = rk.lay
+        incs.append(rk.level.increment(df, lay.a - lay.c_lo, lay.b - lay.c_lo, omega))
+    transport.exchange(incs, "inc_recv", k1, add=True)
+    for d, inc in zip(ds, incs):
+        d += inc
+    return ys
 
 
 # ---------------------------------------------------------------------------

@@ -92,3 +92,30 @@ def test_distributed_vanka_step(nx, ny, k, P, surrogate):
     assert_close(_gather(ranks, ds, ref1.size), ref1, TOL, "distributed vanka 1 step")
     distributed_vanka_step(ranks, ds, rs, 0.7, tr)
     assert_close(_gather(ranks, ds, ref2.size), ref2, TOL, "distributed vanka 2 steps")
+
+
+@pytest.mark.parametrize("nx,ny,k,P", [(12, 9, 1, 2), (18, 16, 1, 4)])
+def test_fused_apply_and_vanka_step(nx, ny, k, P):
+    """The bench's distributed step with the x / d halos grouped equals the
+    separate distributed apply and Vanka step bitwise."""
+    import torch
+
+    from test_gpu_operator import _sized_case
+
+    from paper_2603_28706_b200.partition import (distributed_apply, distributed_apply_and_vanka_step,
+                                                 distributed_vanka_step)
+
+    case, fx, syn = _sized_case(nx, ny, k, "modn")
+    ctx = product_ctx(case, fx)
+    ranks, tr = _ranks(ctx, syn.U, product_variant(case), P, build_patches=True)
+    xs = [torch.as_tensor(x, device="cuda") for x in _scatter_with_garbage(ranks, syn.x, 3)]
+    ds = [torch.as_tensor(x, device="cuda") for x in _scatter_with_garbage(ranks, syn.d0, 4)]
+    rs = [torch.as_tensor(rk.local(syn.x), device="cuda") for rk in ranks]
+    xs2, ds2 = [x.clone() for x in xs], [d.clone() for d in ds]
+    ys = distributed_apply(ranks, xs, tr)
+    distributed_vanka_step(ranks, ds, rs, 0.7, tr)
+    ys2 = distributed_apply_and_vanka_step(ranks, xs2, ds2, rs, 0.7, tr)
+    for a, b in zip(ys, ys2):
+        assert torch.equal(a, b)
+    for a, b in zip(ds, ds2):
+        assert torch.equal(a, b)

@@ -216,10 +216,15 @@ def test_gloo_world2_coarse_level_exchange():
     the same result as the in-process LocalTransport."""
     import torch.multiprocessing as mp
 
-    mp.spawn(_coarse_worker, args=(2,), nprocs=2, join=True)
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    mp.spawn(_coarse_worker, args=(2, port), nprocs=2, join=True)
 
 
-def _coarse_worker(rank, world):
+def _coarse_worker(rank, world, port):
     import os
 
     import torch
@@ -228,7 +233,7 @@ def _coarse_worker(rank, world):
     from paper_2603_28706_b200.partition import LocalTransport, StripPartition, TorchDistTransport
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = "29533"
+    os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         part = StripPartition(8, 32, world, levels=3)
@@ -242,5 +247,16 @@ def _coarse_worker(rank, world):
             mine = vecs[rank].clone()
             TorchDistTransport(part.layout(rank), part).exchange(mine, plan, k1, add=add, level=f)
             assert torch.equal(mine, ref[rank]), plan
+        # two independent exchanges in one grouped send/recv (finest level)
+        lays0 = [part.layout(r) for r in range(world)]
+        a = [torch.randn(k1 * l.nd_loc, generator=gen, dtype=torch.float64) for l in lays0]
+        b = [torch.randn(k1 * l.nd_loc, generator=gen, dtype=torch.float64) for l in lays0]
+        ra, rb = [v.clone() for v in a], [v.clone() for v in b]
+        lt = LocalTransport(lays0)
+        lt.exchange(ra, "halo_recv", k1)
+        lt.exchange(rb, "inc_recv", k1, add=True)
+        ma, mb = a[rank].clone(), b[rank].clone()
+        TorchDistTransport(part.layout(rank), part).exchange_many([(ma, "halo_recv", False), (mb, "inc_recv", True)], k1)
+        assert torch.equal(ma, ra[rank]) and torch.equal(mb, rb[rank])
     finally:
         dist.destroy_process_group()
