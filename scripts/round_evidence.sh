@@ -13,5 +13,7 @@ for c in cfg3 cfg5; do
   timeout 900 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${c}_$TAG.log 2>&1
 done
 timeout 900 python bench.py --vcycle --config cfg5 --steps 5 --warmup 3 > gpurun_out/vcycle_cfg5_$TAG.log 2>&1
+timeout 900 python bench.py --solve --config cfg5 > gpurun_out/solve_cfg5_$TAG.log 2>&1
+python scripts/prof_vcycle.py cfg5 5 > gpurun_out/prof_vcycle_cfg5_$TAG.log 2>&1
 timeout 300 python bench.py --vcycle --config cfg2 --steps 5 --warmup 3 --virtual-ranks 2 > gpurun_out/vcycle_cfg2_p2_$TAG.log 2>&1
 tail -c 400 gpurun_out/bench_$TAG.log
