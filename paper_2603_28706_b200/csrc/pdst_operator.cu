@@ -82,6 +82,9 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool v
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(sz) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p)); }
 
 // Stage one slab block's velocity into two shared planes (zero outside the domain).
@@ -1304,8 +1307,13 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
   // start under this grid (k_jac_post waits for both)
   pdl_wait();
   pdl_trigger();
-  for (int nu = 0; nu < K1; ++nu) stage_jac_async(g, x + (size_t)nu * g.nd, nu * 2 * JPLANE, X0, Y0);
-  cp_async_wait_all();  // (commits the staging copies and waits for every group)
+  // node 0's plane in its own group: its volume and CIP (which read only that
+  // plane) start while the other planes land; the temporal mass waits for all
+  stage_jac_async(g, x, 0, X0, Y0);
+  cp_async_commit();
+  for (int nu = 1; nu < K1; ++nu) stage_jac_async(g, x + (size_t)nu * g.nd, nu * 2 * JPLANE, X0, Y0);
+  cp_async_commit();
+  cp_async_wait_group<1>();
   __syncthreads();
   TR(1);
   for (int mu = 0; mu < K1; ++mu) {
@@ -1315,13 +1323,22 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
     const JAcc acc{slot};
     const PlaneS XM{mu * 2 * JPLANE};
     double rv[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};  // rhs of the own 2x2 nodes (defect mode)
+    double accp[3] = {0.0, 0.0, 0.0};
+    double rp[3] = {0, 0, 0};
+    // CIP, temporal mass and boundary sides accumulate in registers (the
+    // volume's registers are free by then) and reach the slot in one pass
+    double ra[3][3][2];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) ra[a][b][0] = ra[a][b][1] = 0.0;
+    const RegAcc racc{ra};
     if (valid) {
       double P[3];
       const double* xp = x + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
       P[0] = __ldg(xp);
       P[1] = __ldg(xp + 1);
       P[2] = __ldg(xp + 2);
-      double accp[3] = {0.0, 0.0, 0.0};
       // tau w_mu J_mu x_mu: volume, boundary sides, CIP faces (weights carry tau w_mu)
       if (!(ds.skip & 1))
         jac_volume_cached(T, ds, cp, XM, r0, c0, P, slot, accp, g.hx * g.hy * tw);
@@ -1331,7 +1348,6 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
       TR(2 + 5 * mu);
       // defect mode: the right-hand side of this cell's own nodes (lower-left
       // 2x2) and pressures, loaded now for the assembly
-      double rp[3] = {0, 0, 0};
       if (rhs) {
 #pragma unroll
         for (int n = 0; n < 4; ++n) {
@@ -1342,14 +1358,6 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
 #pragma unroll
         for (int j = 0; j < 3; ++j) rp[j] = __ldg(rhs + (size_t)mu * g.nd + g.mv + 3 * (size_t)c + j);
       }
-      // CIP, temporal mass and boundary sides accumulate in registers (the
-      // volume's registers are free now) and reach the slot in one pass
-      double ra[3][3][2];
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int b = 0; b < 3; ++b) ra[a][b][0] = ra[a][b][1] = 0.0;
-      const RegAcc racc{ra};
       if (cip && !(ds.skip & 2)) {
         // face matrices: own right / top, the left / bottom neighbours' right / top
         double W[4][6];
@@ -1367,6 +1375,12 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
       if (mu + 1 < K1)  // the next node's first half-columns towards L2
         for (int h = 0; h < PDST_PF_AHEAD; ++h) apc_prefetch_l2(cp + APC_SLOTS * JNT, h);
       TR(3 + 5 * mu);
+    }
+    if (K1 > 1 && mu == 0) {  // the other nodes' planes (staging group 2) for the temporal mass
+      cp_async_wait_group<0>();
+      __syncthreads();
+    }
+    if (valid) {
       // + M_K sum_nu K_t[mu,nu] x_nu (slab.py:199-200)
       if (!(ds.skip & 8)) {
         const double* Krow = td.K_t + mu * K1;
