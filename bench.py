@@ -538,6 +538,8 @@ def run_solve(args):
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
+    if ws > 1 or args.virtual_ranks > 1:
+        return run_solve_distributed(args)
     cfg = CONFIGS[args.config]
     params = pb.ModelParams(cfg.p, cfg.delta, cfg.nu, cfg.nu_inf)
     conf = pb.DiscretizationConfig(cfg.gamma1, cfg.gamma2, cfg.gamma_cip)
@@ -604,6 +606,84 @@ def run_solve(args):
         "preconditioner_build_s": vc["build_s"], "newton_iteration_wall_s": wall,
     }
     print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_solve_distributed(args):
+    """configs[4] on a strip partition: one modified-Newton iteration of the
+    slab system (distributed residual and M-norms, FGMRES preconditioned by the
+    distributed V-cycle, coarsest level by FGMRES(coarse_iters) with 2 Vanka
+    steps) over N GPUs (torchrun, NCCL) or --virtual-ranks P on one GPU."""
+    import numpy as np
+    import torch
+
+    from paper_2603_28706_b200 import problem as pb
+    from paper_2603_28706_b200.dist_mg import distributed_nonlinear_solve, global_levels
+    from paper_2603_28706_b200.errors import SlabSolveError
+    from paper_2603_28706_b200.krylov import KrylovConfig
+    from paper_2603_28706_b200.newton import NewtonConfig
+    from paper_2603_28706_b200.partition import DistComm, LocalTransport, StripPartition, TorchDistTransport
+    from paper_2603_28706_b200.stmg import MgConfig
+    from paper_2603_28706_b200.synth import CONFIGS, make_slab_inputs
+
+    ws, rank, local = dist_env()
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    P = ws if ws > 1 else args.virtual_ranks
+    cfg = CONFIGS[args.config]
+    params = pb.ModelParams(cfg.p, cfg.delta, cfg.nu, cfg.nu_inf)
+    conf = pb.DiscretizationConfig(cfg.gamma1, cfg.gamma2, cfg.gamma_cip)
+    syn = make_slab_inputs(cfg)
+    ctx = pb.make_context(cfg.nx, cfg.ny, cfg.k, params, cfg.tau, config=conf, v_minus=syn.v_minus)
+    variant = pb.modified_newton(cfg.nu)
+    min_cells = max(1, cfg.nx >> (args.levels - 1))
+    mg = MgConfig(pre_smooth=2, post_smooth=2, omega=cfg.omega, surrogate=True, rep_fraction=cfg.rep_fraction,
+                  min_cells=min_cells, coarse_solver="fgmres", coarse_sweeps=2, coarse_iters=args.coarse_iters,
+                  coarse_rtol=1e-6)
+    part = StripPartition(cfg.nx, cfg.ny, P, levels=global_levels(cfg.nx, cfg.ny, min_cells))
+    mine = [rank] if ws > 1 else list(range(P))
+    transport = (TorchDistTransport(part.layout(rank), part) if ws > 1
+                 else LocalTransport([part.layout(r) for r in range(P)]))
+    comm = DistComm() if ws > 1 else None
+    newton = NewtonConfig(variant=variant, max_nonlinear=1)
+    krylov = KrylovConfig(restart=args.restart, max_iters=args.max_krylov)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.time()
+    status, msg = "converged", ""
+    try:
+        _, stats = distributed_nonlinear_solve(ctx, syn.U, newton, krylov, mg, part, mine, transport, comm, local)
+    except SlabSolveError as e:
+        stats, status, msg = e.diagnostics, e.kind, str(e)
+    torch.cuda.synchronize()
+    wall = time.time() - t0
+    if dist:
+        t = torch.tensor([wall], device=torch.device("cuda", local))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        wall = float(t.item())
+    st = stats.steps[0] if stats is not None and stats.steps else None
+    if rank == 0:
+        print(json.dumps({
+            "metric": "modified-Newton iteration on a strip partition: FGMRES + distributed space-time multigrid "
+                      "(Krylov iterations, wall time)", "impl": "ours", "n_gpus": ws,
+            "virtual_ranks": P if ws == 1 else None, "dtype": "f64", "data": "synthetic (synth.py seeded state)",
+            "scaling": "strong",
+            "config": {"workload": f"{cfg.name}: {cfg.nx}x{cfg.ny} Q2/P1disc, DG({cfg.k}); {part.levels} levels, "
+                                   f"2+2 Vanka, coarsest FGMRES({args.coarse_iters}) + 2 Vanka steps, "
+                                   f"FGMRES(restart={args.restart}, budget {args.max_krylov})",
+                       "n_dof": (cfg.k + 1) * part.layout(0).nd, "parallelism": f"strips x{P}"},
+            "newton_status": status, "newton_message": msg,
+            "initial_residual": stats.initial_res if stats is not None else None,
+            # a stalled FGMRES has spent its whole budget (krylov.py:118-139)
+            "krylov_iterations": st.n_l if st else (args.max_krylov if status == "krylov" else None),
+            "residual_after": st.res_after if st else None,
+            "newton_iteration_wall_s": wall}), flush=True)
+    if dist:
+        dist.destroy_process_group()
     return 0
 
 

@@ -41,7 +41,8 @@ import numpy as np
 from . import _lib as L
 from .partition import CUT, StripPartition, local_context, owned_mask
 
-__all__ = ["global_levels", "DistributedStmg", "distributed_vcycle", "LocalComm"]
+__all__ = ["global_levels", "DistributedStmg", "distributed_vcycle", "LocalComm", "distributed_fgmres_mg",
+           "distributed_nonlinear_solve"]
 
 _VANKA = 1  # pdst_set_coarse_solver kind without a dense setup (the local coarsest level is never solved alone)
 
@@ -338,7 +339,7 @@ class _NoComm:
         return t
 
 
-def distributed_fgmres_mg(ranks, transport, rhs, tol, config=None, comm=None, x0=None):
+def distributed_fgmres_mg(ranks, transport, rhs, tol, config=None, comm=None, x0=None, op_jacs=None):
     """FGMRES in the M-inner product (krylov.fgmres) on the strip partition,
     right-preconditioned by `distributed_vcycle`.
 
@@ -347,7 +348,9 @@ def distributed_fgmres_mg(ranks, transport, rhs, tol, config=None, comm=None, x0
     `partition.DistComm`).  The ranks' local vectors (ghost entries zero) are
     stacked into one Krylov vector, so every inner product is the owned-entry
     sum — plus one allreduce per Gram-Schmidt pass across processes.  Returns
-    the FgmresResult with x as the list of local vectors (ghosts zero)."""
+    the FgmresResult with x as the list of local vectors (ghosts zero).
+    op_jacs: the operator's SlabJacobians (default: the ranks' own, i.e. the
+    preconditioner's linearization)."""
     import dataclasses
 
     import torch
@@ -371,8 +374,10 @@ def distributed_fgmres_mg(ranks, transport, rhs, tol, config=None, comm=None, x0
         transport.exchange(parts, "halo_recv", k1)
         return parts
 
+    jacs = op_jacs if op_jacs is not None else [rk.jac for rk in ranks]
+
     def op(v, out=None):
-        y = torch.cat([rk.jac.matvec(p) for rk, p in zip(ranks, halo_copy(v))]) * mask
+        y = torch.cat([jac.matvec(p) for jac, p in zip(jacs, halo_copy(v))]) * mask
         if out is not None:
             out.copy_(y)
             return out
@@ -398,3 +403,140 @@ def distributed_fgmres_mg(ranks, transport, rhs, tol, config=None, comm=None, x0
     x0c = None if x0 is None else torch.cat([torch.as_tensor(x, device=device).reshape(-1) for x in x0]) * mask
     res = fgmres(op, b, tol, config, precond=precond, mass=_Mass(), x0=x0c, comm=comm or _NoComm())
     return dataclasses.replace(res, x=split(res.x))
+
+
+# ---------------------------------------------------------------------------
+# One slab's modified-Newton solve on a strip partition (newton.py:168-284)
+# ---------------------------------------------------------------------------
+
+
+def distributed_nonlinear_solve(ctx, U0, newton, krylov, mg, part: StripPartition, rank_ids, transport, comm=None,
+                                device=0):
+    """`newton.nonlinear_solve_slab` with FGMRES preconditioned by the
+    distributed V-cycle, on the strips `rank_ids` of `part` held by this
+    process (all of them with LocalTransport, one with TorchDistTransport and
+    a `partition.DistComm`).  Same control flow: Eisenstat-Walker forcing,
+    Armijo backtracking, the rebuild policy, the same failure kinds.  The
+    state lives as local (ghosted) slabs whose 2^L ghost rows are refreshed
+    from the neighbours after every update (`deep_halo_recv`), so each rank's
+    residual, linearization and hierarchy see the global state.  Norms are
+    M-norms of the owned entries summed over the ranks.  Returns (list of the
+    local states, SlabStats)."""
+    import torch
+
+    from .errors import SlabSolveError
+    from .newton import PIC, NewtonStepStats, SlabStats, _forcing, rebuild_policy
+    from .operators import MassNorm, SlabDevice, SlabJacobian, slab_residual
+    from .problem import dirichlet_flags
+
+    k1 = ctx.basis.k + 1
+    dev = torch.device("cuda", device)
+    lays = [part.layout(r) for r in rank_ids]
+    lctxs = [local_context(ctx, lay) for lay in lays]
+    masks = [owned_mask(lay, k1, dev) for lay in lays]
+    U0 = np.asarray(U0, dtype=np.float64)
+    Us = [torch.as_tensor(np.stack([lay.to_local(U0[mu]) for mu in range(k1)]), device=dev) for lay in lays]
+    sds = [SlabDevice(lc, device) for lc in lctxs]
+    jds = [SlabDevice(lc, device) for lc in lctxs]
+    masses = [MassNorm(lc, dev=sd) for lc, sd in zip(lctxs, sds)]
+    vcomm = LocalComm() if comm is None else _DistCommList(comm)
+    is_picard = newton.variant.kind == PIC
+
+    def refresh(U_list):
+        transport.exchange([u.view(-1) for u in U_list], "deep_halo_recv", k1)
+
+    def residual(U_list):
+        refresh(U_list)
+        return [slab_residual(lc, u, dev=sd).reshape(-1) * m for lc, u, sd, m in zip(lctxs, U_list, sds, masks)]
+
+    def mnorm(R_list):
+        tmp = [r.clone() for r in R_list]
+        transport.exchange(tmp, "halo_recv", k1)
+        vals = []
+        for ms, t, r, m in zip(masses, tmp, R_list, masks):
+            mr = torch.empty_like(t)
+            ms.apply_into(t, mr)
+            vals.append((r * (mr * m)).sum().reshape(1))
+        vcomm.allreduce_list(vals)
+        return float(np.sqrt(max(float(vals[0].item()), 0.0)))
+
+    R = residual(Us)
+    rnorm = mnorm(R)
+    stats = SlabStats(initial_res=rnorm)
+    r0 = rnorm
+    pre = None
+    eta_prev = newton.forcing_eta0
+    rnorm_prev = rnorm
+    prev_n_l = 0
+
+    def finish():
+        if bool((dirichlet_flags(ctx.disc.mesh) == 1).all()):  # zero mean of the constant pressure mode
+            sums = []
+            for lay, u in zip(lays, Us):
+                pl = lay.prs_slice_local(lay.a, lay.b)
+                sums.append(u[:, pl.start:pl.stop:3].sum(dim=1))
+            vcomm.allreduce_list(sums)
+            n = ctx.disc.mesh.nx * ctx.disc.mesh.ny
+            out = []
+            for lay, u, sm in zip(lays, Us, sums):
+                v = u.clone()
+                v[:, lay.mv_loc::3] -= (sm / n).view(k1, 1)
+                out.append(v)
+            return out
+        return Us
+
+    for m in range(newton.max_nonlinear):
+        if rnorm <= newton.abs_tol or rnorm <= newton.rel_tol * r0:
+            stats.converged = True
+            stats.final_res = rnorm
+            return finish(), stats
+        jacs = [SlabJacobian(lc, u, newton.variant, dev=jd) for lc, u, jd in zip(lctxs, Us, jds)]
+        ratio = rnorm / rnorm_prev if m > 0 else 0.0
+        last_n_l = stats.steps[-1].n_l if stats.steps else 0
+        rebuilt = False
+        if pre is None or rebuild_policy(ratio, last_n_l, prev_n_l, mg.rebuild_rho, mg.rebuild_factor):
+            pre = [DistributedStmg(ctx, u, newton.variant, part, r, mg, device=device, U_is_local=True)
+                   for r, u in zip(rank_ids, Us)]
+            rebuilt = True
+        prev_n_l = stats.steps[-1].n_l if stats.steps else 0
+        eta = newton.picard_fixed_tol if is_picard else _forcing(newton, m, rnorm, rnorm_prev, eta_prev)
+        result = distributed_fgmres_mg(pre, transport, R, eta, krylov, comm=comm, op_jacs=jacs)
+        if not result.converged:
+            stats.failure = "krylov"
+            stats.final_res = rnorm
+            raise SlabSolveError("krylov", f"FGMRES stalled at |r|={result.residual_norm:.3e} "
+                                           f"(target {result.target:.3e})", stats)
+        dUs = [x.reshape(u.shape) for x, u in zip(result.x, Us)]
+        phi = 0.5 * rnorm**2
+        lam = 1.0
+        if is_picard:
+            Us = [u + du for u, du in zip(Us, dUs)]
+            R_new = residual(Us)
+            rnorm_new = mnorm(R_new)
+        else:
+            while True:
+                U_try = [u + lam * du for u, du in zip(Us, dUs)]
+                R_new = residual(U_try)
+                rnorm_new = mnorm(R_new)
+                if 0.5 * rnorm_new**2 <= (1.0 - newton.armijo_c1 * lam) * phi:
+                    Us = U_try
+                    break
+                lam *= newton.armijo_backtrack
+                if lam < newton.armijo_lambda_min:
+                    stats.failure = "line_search"
+                    stats.final_res = rnorm
+                    raise SlabSolveError("line_search",
+                                         f"no sufficient decrease above lambda={lam:.2e} at |R|={rnorm:.3e}", stats)
+        stats.steps.append(NewtonStepStats(n_l=result.iterations, lam=lam, eta=eta, res_before=rnorm,
+                                           res_after=rnorm_new, lin_res=result.residual_norm, rebuilt=rebuilt))
+        rnorm_prev = rnorm
+        rnorm = rnorm_new
+        eta_prev = eta
+        R = R_new
+    if rnorm <= newton.abs_tol or rnorm <= newton.rel_tol * r0:
+        stats.converged = True
+        stats.final_res = rnorm
+        return finish(), stats
+    stats.failure = "max_iterations"
+    stats.final_res = rnorm
+    raise SlabSolveError("max_iterations", f"|R|={rnorm:.3e} after {newton.max_nonlinear} iterations", stats)

@@ -167,6 +167,27 @@ class RankLayout:
             out.append((self.rank + 1, self.vel_slice_local(2 * self.b, top), hi.vel_slice_local(2 * self.b, top)))
         return out
 
+    def deep_halo_recv(self):
+        """Every ghost row of the local mesh (state / linearization halo of a
+        multigrid partition, 2^L rows deep) from the two neighbours, which own
+        them when the strips are at least that thick (checked)."""
+        out = []
+        if self.rank > 0:
+            lo = _layout_of(self, self.rank - 1)
+            if self.c_lo < lo.a:
+                raise ValueError(f"rank {self.rank}: ghost rows from {self.c_lo} reach past rank {self.rank - 1}")
+            out.append((self.rank - 1, self.vel_slice_local(2 * self.c_lo, 2 * self.a),
+                        lo.vel_slice_local(2 * self.c_lo, 2 * self.a)))
+            out.append((self.rank - 1, self.prs_slice_local(self.c_lo, self.a), lo.prs_slice_local(self.c_lo, self.a)))
+        if not self.last:
+            hi = _layout_of(self, self.rank + 1)
+            if not (self.c_hi < hi.b or hi.last):
+                raise ValueError(f"rank {self.rank}: ghost rows up to {self.c_hi} reach past rank {self.rank + 1}")
+            out.append((self.rank + 1, self.vel_slice_local(2 * self.b, 2 * self.c_hi + 1),
+                        hi.vel_slice_local(2 * self.b, 2 * self.c_hi + 1)))
+            out.append((self.rank + 1, self.prs_slice_local(self.b, self.c_hi), hi.prs_slice_local(self.b, self.c_hi)))
+        return out
+
     def defect_recv(self):
         """The defect of node row 2b (owned by rank+1)."""
         if self.last:

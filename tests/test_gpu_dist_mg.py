@@ -151,3 +151,56 @@ def test_two_process_vcycle_and_fgmres(tmp_path):
                  precond=lambda v, out=None: pre.apply(v, out=out), mass=MassNorm(ctx, dev=jac.dev))
     assert int(parts[0]["iters"]) == int(parts[1]["iters"]) == ref.iterations
     assert_close(parts[0]["x"] + parts[1]["x"], ref.x.cpu().numpy(), 1e-8, "two-process FGMRES + V-cycle")
+
+
+@pytest.mark.parametrize("P,max_nl", [(2, 3), (4, 2)])
+def test_distributed_newton_matches_single_domain(P, max_nl):
+    """A slab's modified-Newton solve on P strips (distributed residual, M-norms,
+    deep state halos, FGMRES + distributed V-cycle, Armijo line search) takes the
+    single-domain solve's steps: same Krylov iteration counts, step lengths,
+    failure kind, residual history to 1e-7."""
+    import sys
+
+    import os
+
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from dist_mg_worker import problem
+
+    from paper_2603_28706_b200.dist_mg import distributed_nonlinear_solve, global_levels
+    from paper_2603_28706_b200.errors import SlabSolveError
+    from paper_2603_28706_b200.krylov import KrylovConfig
+    from paper_2603_28706_b200.newton import NewtonConfig, StmgFactory, nonlinear_solve_slab
+    from paper_2603_28706_b200.partition import LocalTransport, StripPartition
+
+    cfg, ctx, syn, var, mg = problem()
+    if P == 4:  # strips of 8 rows: the 2^L = 8 ghost rows still come from direct neighbours
+        import dataclasses
+
+        mg = dataclasses.replace(mg, min_cells=8)
+    newton = NewtonConfig(variant=var, max_nonlinear=max_nl)
+    krylov = KrylovConfig(restart=20, max_iters=40)
+
+    def run(fn):
+        try:
+            out, st = fn()
+            return out, st, None
+        except SlabSolveError as e:
+            return None, e.diagnostics, e.kind
+
+    U_ref, st_ref, kind_ref = run(lambda: nonlinear_solve_slab(ctx, syn.U, newton, krylov, StmgFactory(mg)))
+    part = StripPartition(cfg.nx, cfg.ny, P, levels=global_levels(cfg.nx, cfg.ny, mg.min_cells))
+    tr = LocalTransport([part.layout(r) for r in range(P)])
+    Us, st, kind = run(lambda: distributed_nonlinear_solve(ctx, syn.U, newton, krylov, mg, part, list(range(P)), tr))
+    assert kind == kind_ref
+    assert len(st.steps) == len(st_ref.steps) >= 1
+    assert abs(st.initial_res - st_ref.initial_res) <= 1e-10 * st_ref.initial_res
+    for a, b in zip(st.steps, st_ref.steps):
+        assert a.n_l == b.n_l and a.lam == b.lam and a.rebuilt == b.rebuilt
+        assert abs(a.res_after - b.res_after) <= 1e-7 * b.res_before
+    if U_ref is not None:
+        lays = [part.layout(r) for r in range(P)]
+        g = np.full(U_ref.shape, np.nan)
+        for lay, u in zip(lays, Us):
+            for mu in range(U_ref.shape[0]):
+                lay.owned_into_global(u[mu].cpu().numpy(), g[mu])
+        assert_close(g.reshape(-1), np.asarray(U_ref).reshape(-1), 1e-9, "distributed Newton state")
