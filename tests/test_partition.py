@@ -260,3 +260,38 @@ def _coarse_worker(rank, world, port):
         assert torch.equal(ma, ra[rank]) and torch.equal(mb, rb[rank])
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nx,ny,P,levels", [(16, 32, 2, 3), (16, 48, 3, 3), (8, 64, 4, 3)])
+def test_deep_halo_plan(nx, ny, P, levels):
+    """The state halo of a multigrid partition: every ghost row of every local
+    mesh comes from the neighbour that owns it, and together with the owned
+    rows the local slab is exactly the global slab restricted to the local mesh."""
+    from paper_2603_28706_b200.partition import LocalTransport, StripPartition
+
+    part = StripPartition(nx, ny, P, levels=levels)
+    lays = [part.layout(r) for r in range(P)]
+    rng = np.random.default_rng(1)
+    k1 = 2
+    xg = rng.standard_normal(k1 * lays[0].nd)
+    nd = lays[0].nd
+    vecs = []
+    for lay in lays:  # owned entries right, ghosts garbage
+        own = np.zeros(nd)
+        lay.owned_into_global(np.ones(lay.nd_loc), own)
+        v = np.concatenate([np.where(lay.to_local(own) > 0, lay.to_local(xg[mu * nd:(mu + 1) * nd]), 1e9)
+                            for mu in range(k1)])
+        vecs.append(v)
+    LocalTransport(lays).exchange(vecs, "deep_halo_recv", k1)
+    for lay, v in zip(lays, vecs):
+        ref = np.concatenate([lay.to_local(xg[mu * nd:(mu + 1) * nd]) for mu in range(k1)])
+        assert np.array_equal(v, ref)
+
+
+def test_deep_halo_needs_thick_strips():
+    from paper_2603_28706_b200.partition import StripPartition
+
+    part = StripPartition(16, 32, 4, levels=3)  # strips of 8 rows, 8 ghost rows: the top one reaches 2 ranks up
+    with pytest.raises(ValueError):
+        for r in range(4):
+            part.layout(r).deep_halo_recv()
