@@ -8,7 +8,9 @@ DG(1), cfg3 1024^2 DG(2)), where the CPU oracle cannot follow:
 * exact-Newton Jacobian == finite difference of the residual with the
   lagged CIP / inflow weights frozen (slab.py:144-159 `advect`), relative
   error O(eps);
-* the 2-rank strip partition reproduces the single-domain apply (1e-13).
+* the 2-rank strip partition reproduces the single-domain apply (1e-13);
+* cfg3's three linearizations: modified Newton with an unbounded sigma_max is
+  exact Newton bitwise, the three differ, exact Newton = d(residual).
 """
 
 import numpy as np
@@ -106,4 +108,41 @@ def test_cfg2_exact_newton_is_residual_derivative():
         fd = ((Rp - Rm) / (2 * eps)).reshape(-1)
         # R = -tau w F + ..., the Jacobian of the slab system is -dR/dU (newton.py solves J dU = R)
         errs.append(min(_rel(-fd, JdU), _rel(fd, JdU)))
+    assert min(errs) <= 1e-6, errs
+
+
+def test_cfg3_three_linearizations():
+    """BASELINE configs[2]: the apply in all three linearizations at full size
+    (1024^2, DG(2), 34.6 M dofs), compared: modified Newton with an unbounded
+    sigma_max IS exact Newton (the clip factor is exactly 1: bitwise), the
+    three differ from each other, each is linear, and exact Newton is the
+    derivative of the residual (central differences, lagged weights frozen)."""
+    import torch
+
+    from paper_2603_28706_b200 import problem as pb
+    from paper_2603_28706_b200.operators import SlabDevice, SlabJacobian, slab_residual
+
+    cfg, ctx, _, syn, dev = _setup("cfg3")
+    U = torch.as_tensor(syn.U, device=dev)
+    x = torch.as_tensor(syn.x, device=dev)
+    y = torch.as_tensor(syn.d0, device=dev)
+    sd = SlabDevice(ctx)
+    out = {}
+    for name, var in (("pic", pb.picard()), ("exn", pb.exact_newton()), ("modn", pb.modified_newton(cfg.nu)),
+                      ("modn_inf", pb.modified_newton(1e300))):
+        jac = SlabJacobian(ctx, U, var, dev=sd)
+        Jx, Jy = jac.matvec(x), jac.matvec(y)
+        assert torch.isfinite(Jx).all()
+        assert _rel(jac.matvec(2.0 * x - 0.5 * y), 2.0 * Jx - 0.5 * Jy) <= 1e-13
+        out[name] = Jx
+    assert torch.equal(out["modn_inf"], out["exn"])
+    for a, b in (("pic", "exn"), ("pic", "modn"), ("modn", "exn")):
+        assert _rel(out[a], out[b]) > 1e-8, (a, b)
+    dU = x.reshape(U.shape)
+    errs = []
+    for eps in (1e-6, 1e-7):
+        Rp = slab_residual(ctx, U + eps * dU, advect=U, dev=sd)
+        Rm = slab_residual(ctx, U - eps * dU, advect=U, dev=sd)
+        fd = ((Rp - Rm) / (2 * eps)).reshape(-1)
+        errs.append(min(_rel(-fd, out["exn"]), _rel(fd, out["exn"])))
     assert min(errs) <= 1e-6, errs
