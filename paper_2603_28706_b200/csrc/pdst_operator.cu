@@ -861,13 +861,14 @@ constexpr int APC_SLOTS = APC_VOL + 12;
 
 // L2 prefetch of half h (0..7: Gauss column h/2, points 2(h%2), 2(h%2)+1) of
 // a node's cache block; h == 8 is the CIP block.
-__device__ __forceinline__ void apc_prefetch_l2(const double* __restrict__ cp, int h) {
+__device__ __forceinline__ void apc_prefetch_l2(const double* __restrict__ cp, int h, bool hasg = true) {
   if (h < 8) {
     const int qx = h >> 1, qy0 = (h & 1) * 2;
 #pragma unroll
     for (int j = 0; j < 2; ++j)
 #pragma unroll
-      for (int k = 0; k < 6; ++k) prefetch_l2(cp + (qx * 24 + k * 4 + qy0 + j) * JNT);
+      for (int k = 0; k < 6; ++k)
+        if (hasg || k == 0 || k > 3) prefetch_l2(cp + (qx * 24 + k * 4 + qy0 + j) * JNT);
   } else if (h == 8) {
 #pragma unroll
     for (int i = 0; i < 12; ++i) prefetch_l2(cp + (APC_VOL + i) * JNT);
@@ -888,7 +889,7 @@ struct JTabs {
 
 // Volume terms (forms.py:589-603) from the apply cache; the first writer of
 // the cell's slot.
-template <class XA>
+template <bool HG, class XA>
 __device__ __forceinline__ void jac_volume_cached(const JTabs& T, const Disc& ds, const double* __restrict__ cp,
                                                   const XA& XM, int r0, int c0, const double P[3], double* slot,
                                                   double accp[3], double WT) {
@@ -915,8 +916,9 @@ __device__ __forceinline__ void jac_volume_cached(const JTabs& T, const Disc& ds
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
-        for (int k = 0; k < 6; ++k) cv[j][k] = __ldg(cp + (qx * 24 + k * 4 + 2 * hh + j) * JNT);
-      apc_prefetch_l2(cp, h + PDST_PF_AHEAD);
+        for (int k = 0; k < 6; ++k)  // Picard: the a~ slots are zeros, not read
+          cv[j][k] = (k >= 1 && k <= 3 && !HG) ? 0.0 : __ldg(cp + (qx * 24 + k * 4 + 2 * hh + j) * JNT);
+      apc_prefetch_l2(cp, h + PDST_PF_AHEAD, HG);
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int qy = 2 * hh + j;
@@ -1272,7 +1274,7 @@ __host__ __device__ inline size_t jac_post_items(const Geom& g) {
 // its contribution comes from the apply cache, streamed once per apply — so
 // the CTA holds only the direction planes of all Radau nodes and one set of
 // per-cell node slots.
-template <int K1>
+template <int K1, bool HG>
 __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, TimeData td, Disc ds, Lin L,
                                                   const double* __restrict__ x, const double* __restrict__ rhs,
                                                   double* __restrict__ out, double* __restrict__ part,
@@ -1300,8 +1302,9 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
   const double* cbase = L.apc + tile * K1 * APC_SLOTS * JNT + threadIdx.x;
 
   TR(0);
+  // HG == false (Picard, or no viscous term): the a~ slots are zeros and never read
   if (valid)  // the coefficient stream does not depend on the predecessor
-    for (int h = 0; h < PDST_PF_AHEAD; ++h) apc_prefetch_l2(cbase, h);
+    for (int h = 0; h < PDST_PF_AHEAD; ++h) apc_prefetch_l2(cbase, h, HG);
   // launched with PDL: x (and the scratch the predecessor's epilogue may still
   // read) only after the predecessor has completed; then k_side_products may
   // start under this grid (k_jac_post waits for both)
@@ -1341,7 +1344,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
       P[2] = __ldg(xp + 2);
       // tau w_mu J_mu x_mu: volume, boundary sides, CIP faces (weights carry tau w_mu)
       if (!(ds.skip & 1))
-        jac_volume_cached(T, ds, cp, XM, r0, c0, P, slot, accp, g.hx * g.hy * tw);
+        jac_volume_cached<HG>(T, ds, cp, XM, r0, c0, P, slot, accp, g.hx * g.hy * tw);
       else
 #pragma unroll
         for (int k = 0; k < 18; ++k) slot[k * JNT] = 0.0;
@@ -1373,7 +1376,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
         cip_all_w(T, g, XM, ci, cj, r0, c0, W, racc);
       }
       if (mu + 1 < K1)  // the next node's first half-columns towards L2
-        for (int h = 0; h < PDST_PF_AHEAD; ++h) apc_prefetch_l2(cp + APC_SLOTS * JNT, h);
+        for (int h = 0; h < PDST_PF_AHEAD; ++h) apc_prefetch_l2(cp + APC_SLOTS * JNT, h, HG);
       TR(3 + 5 * mu);
     }
     if (K1 > 1 && mu == 0) {  // the other nodes' planes (staging group 2) for the temporal mass
@@ -1993,7 +1996,9 @@ cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const 
   static bool configured = false;
   const size_t sm = jac_smem<K1>();
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_jacobian<K1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = cudaFuncSetAttribute(k_jacobian<K1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_jacobian<K1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -2022,7 +2027,10 @@ cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const 
   const bool post = !(ds.skip & 64);
   const size_t ncb = n_bcells(g);
   double* sp = part + (size_t)K1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2;
-  PDST_LAUNCH(e = launch_pdl(k_jacobian<K1>, grid, dim3(JNT), sm, st, g, td, ds, L, x, rhs, out, part, T));
+  if (L.has_gamma && ds.viscous)
+    PDST_LAUNCH(e = launch_pdl(k_jacobian<K1, true>, grid, dim3(JNT), sm, st, g, td, ds, L, x, rhs, out, part, T));
+  else  // Picard (or no viscous term): the tangent's a~ slots are zeros, not streamed
+    PDST_LAUNCH(e = launch_pdl(k_jacobian<K1, false>, grid, dim3(JNT), sm, st, g, td, ds, L, x, rhs, out, part, T));
   if (e != cudaSuccess) return e;
   if (post && !(ds.skip & 128)) {
     // tile pass -> side products (overlapping it, then waiting for it) -> epilogue
