@@ -309,7 +309,7 @@ def run_ours(args):
     from paper_2603_28706_b200 import _lib as L
     from paper_2603_28706_b200 import problem as pb
     from paper_2603_28706_b200.operators import SlabJacobian
-    from paper_2603_28706_b200.smoother import VankaLevel, vanka_smooth
+    from paper_2603_28706_b200.smoother import VankaLevel
     from paper_2603_28706_b200.synth import CONFIGS, make_slab_inputs
 
     cfg = CONFIGS[args.config]

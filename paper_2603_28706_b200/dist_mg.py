@@ -39,7 +39,7 @@ import math
 import numpy as np
 
 from . import _lib as L
-from .partition import CUT, StripPartition, local_context, owned_mask
+from .partition import StripPartition, local_context, owned_mask
 
 __all__ = ["global_levels", "DistributedStmg", "distributed_vcycle", "LocalComm", "distributed_fgmres_mg",
            "distributed_nonlinear_solve"]
