@@ -16,6 +16,8 @@
 // (M = hx hy M1y (x) M1x (x) I2).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "pdst_device.cuh"
 #include "pdst_patch.h"
 
@@ -376,6 +378,8 @@ cudaError_t patch_invert(int k1, const double* mats, double* invT, int npatch, i
 }
 
 cudaError_t vanka_gemv(const Geom& g, int k1, const double* invT, const double* defect, double* upd, cudaStream_t st) {
+  cudaError_t e = cudaSuccess;
+  if (!getenv("PDST_NO_XTMA") && vanka_gemv_exact_tma(g, k1, invT, defect, upd, st, &e)) return e;
   switch (k1) {
     case 1: return launch_gemv<21>(g, invT, defect, upd, st);
     case 2: return launch_gemv<42>(g, invT, defect, upd, st);

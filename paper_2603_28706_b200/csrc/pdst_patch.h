@@ -46,6 +46,9 @@ cudaError_t patch_invert_diag(const Geom& g, const TimeDiag& td, const double* s
 cudaError_t vanka_gemv_diag(const Geom& g, const TimeDiag& td, const double* binvT, const double* defect,
                             double* upd, cudaStream_t st);
 
+bool vanka_gemv_exact_tma(const Geom& g, int k1, const double* invT, const double* defect, double* upd,
+                          cudaStream_t st, cudaError_t* err);
+
 cudaError_t patch_assemble(const PatchArgs& a, cudaStream_t st);
 cudaError_t patch_invert(int k1, const double* mats, double* invT, int npatch, int* bad, cudaStream_t st);
 cudaError_t vanka_gemv(const Geom& g, int k1, const double* invT, const double* defect, double* upd, cudaStream_t st);

@@ -549,6 +549,110 @@ cudaError_t launch_gemv_tma(const Geom& g, const TimeDiag& td, const double* bin
   return e;
 }
 
+// Exact (non-surrogate) patch inverses through the same kind of pipeline:
+// D x D column-major inverses (D even: 16-byte bulk copies) streamed by
+// thread 0 into an S-stage ring, threads (patch p, row i) form
+// sum_j invT[j][i] e_j against the gathered defect in shared memory (same
+// 4-accumulator order as k_vanka_gemv), next group's defect gathered under the
+// current product.  Coarse multigrid levels use these patches.
+template <int D>
+__host__ __device__ constexpr int xtma_pb() { return D <= 42 ? 2 : 1; }
+constexpr int XTMA_STAGES = 3;
+
+template <int D>
+__global__ void __launch_bounds__(xtma_pb<D>() * D, 2) k_vanka_gemv_exact_tma(Geom g, const double* __restrict__ invT,
+                                                                           const double* __restrict__ defect,
+                                                                           double* __restrict__ upd, int ngroups) {
+  constexpr int PB = xtma_pb<D>();
+  constexpr unsigned PBYTES = (unsigned)D * D * 8u;
+  static_assert(PBYTES % 16 == 0, "bulk copies move 16-byte multiples");
+  extern __shared__ __align__(128) unsigned char xring[];
+  __shared__ double es[2][PB][D];
+  __shared__ __align__(8) uint64_t full[XTMA_STAGES];
+  const int p = threadIdx.x / D, i = threadIdx.x % D;
+  auto stage_ptr = [&](int st) { return reinterpret_cast<double*>(xring + (size_t)st * PB * PBYTES); };
+  auto issue = [&](int gi, int st) {
+    const int K0 = gi * PB, cnt = min(PB, g.ncells - K0);
+    mbar_expect_tx(&full[st], (unsigned)cnt * PBYTES);
+    bulk_g2s(stage_ptr(st), invT + (size_t)K0 * D * D, (unsigned)cnt * PBYTES, &full[st]);
+  };
+  auto load_defect = [&](int gi) {
+    const int K = gi * PB + p;
+    return (gi < ngroups && K < g.ncells) ? __ldg(defect + patch_dof_d(g, K, i)) : 0.0;
+  };
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < XTMA_STAGES; ++st) mbar_init(&full[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    for (int st = 0; st < XTMA_STAGES; ++st) {
+      const int gi = blockIdx.x + st * gridDim.x;
+      if (gi < ngroups) issue(gi, st);
+    }
+  }
+  pdl_wait();
+  es[0][p][i] = load_defect(blockIdx.x);
+  __syncthreads();
+  int it = 0;
+  for (int gi = blockIdx.x; gi < ngroups; gi += gridDim.x, ++it) {
+    const int st = it % XTMA_STAGES, buf = it & 1;
+    const unsigned parity = (unsigned)(it / XTMA_STAGES) & 1u;
+    const int K = gi * PB + p;
+    const double en = load_defect(gi + gridDim.x);
+    mbar_wait(&full[st], parity);
+    if (K < g.ncells) {
+      const double* col = stage_ptr(st) + (size_t)p * D * D + i;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int jj = 0;
+#pragma unroll 4
+      for (; jj + 3 < D; jj += 4) {
+        s0 = fma(col[(size_t)jj * D], es[buf][p][jj], s0);
+        s1 = fma(col[(size_t)(jj + 1) * D], es[buf][p][jj + 1], s1);
+        s2 = fma(col[(size_t)(jj + 2) * D], es[buf][p][jj + 2], s2);
+        s3 = fma(col[(size_t)(jj + 3) * D], es[buf][p][jj + 3], s3);
+      }
+      for (; jj < D; ++jj) s0 = fma(col[(size_t)jj * D], es[buf][p][jj], s0);
+      upd[(size_t)i * g.ncells + K] = (s0 + s1) + (s2 + s3);  // structure of arrays [D][ncells]
+    }
+    es[buf ^ 1][p][i] = en;
+    __syncthreads();  // stage st is free, es[buf ^ 1] is complete
+    if (threadIdx.x == 0) {
+      const int gn = gi + XTMA_STAGES * gridDim.x;
+      if (gn < ngroups) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        issue(gn, st);
+      }
+    }
+  }
+}
+
+template <int D>
+cudaError_t launch_gemv_exact_tma(const Geom& g, const double* invT, const double* defect, double* upd,
+                                  cudaStream_t st) {
+  static int nsm = 0, per_sm = 1;
+  static bool configured = false;
+  constexpr int PB = xtma_pb<D>();
+  const size_t sm = (size_t)XTMA_STAGES * PB * D * D * sizeof(double);
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_vanka_gemv_exact_tma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sm);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    // persistent: exactly the CTAs that are resident at once
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vanka_gemv_exact_tma<D>, PB * D, sm);
+    if (e != cudaSuccess) return e;
+    per_sm = std::max(1, per_sm);
+    configured = true;
+  }
+  const int ngroups = (g.ncells + PB - 1) / PB;
+  const int grid = std::min(ngroups, per_sm * nsm);
+  cudaError_t e;
+  PDST_LAUNCH(e = launch_pdl(k_vanka_gemv_exact_tma<D>, dim3(grid), dim3(PB * D), sm, st, g, invT, defect, upd,
+                             ngroups));
+  return e;
+}
+
 }  // namespace
 
 cudaError_t patch_invert_diag(const Geom& g, const TimeDiag& td, const double* spatial, double* binvT, int* bad,
@@ -573,4 +677,17 @@ cudaError_t vanka_gemv_diag(const Geom& g, const TimeDiag& td, const double* bin
   }
 }
 
+}  // namespace pdst
+
+namespace pdst {
+// Exact-patch GEMV through the TMA pipeline for even D (k+1 = 2, 4); false
+// when the caller must use the row-per-thread kernel (odd D: 8-byte rows).
+bool vanka_gemv_exact_tma(const Geom& g, int k1, const double* invT, const double* defect, double* upd,
+                          cudaStream_t st, cudaError_t* err) {
+  switch (k1) {
+    case 2: *err = launch_gemv_exact_tma<42>(g, invT, defect, upd, st); return true;
+    case 4: *err = launch_gemv_exact_tma<84>(g, invT, defect, upd, st); return true;
+    default: return false;
+  }
+}
 }  // namespace pdst
