@@ -16,6 +16,7 @@
 // (M = hx hy M1y (x) M1x (x) I2).
 #include <cuda_runtime.h>
 
+#include <cstdint>
 #include <cstdlib>
 
 #include "pdst_device.cuh"
@@ -260,25 +261,26 @@ __global__ void __launch_bounds__(256) k_vanka_gemv(Geom g, const double* __rest
   upd[(size_t)i * g.ncells + K] = (s0 + s1) + (s2 + s3);  // structure of arrays [D][ncells]
 }
 
-// d += omega * sum_K R_K' upd_K, one thread per (cell, Radau node, velocity
-// component): the cell writes the nodes it owns (lower-left 2x2 of its 3x3
-// block, plus the last row / column of the mesh) summing the <= 4 patches
-// containing each node in a fixed order (down-left, down, left, self); the
-// component-0 thread also writes the cell's 3 pressure dofs.  upd is structure
-// of arrays [21 k1][ncells], so every read is coalesced; all loads are issued
-// before the first store.
+// d += omega * sum_K R_K' upd_K, one thread per (cell, Radau node): the cell
+// writes the nodes it owns (lower-left 2x2 of its 3x3 block, plus the last
+// row / column of the mesh) summing the <= 4 patches containing each node in a
+// fixed order (down-left, down, left, self), both velocity components of a
+// node as one 16-byte pair when the node plane is 16-byte aligned (VEC), and
+// the cell's 3 pressure dofs.  upd is structure of arrays [21 k1][ncells], so
+// every read is coalesced; all loads are issued before the first store.
 // Only patches of cell rows [row_lo, row_hi) contribute; inc_only writes the
 // increment instead of adding it (distributed sweeps combine increments).
-__global__ void __launch_bounds__(256) k_vanka_scatter(Geom g, int k1, const double* __restrict__ upd, double omega,
+template <bool VEC>
+__global__ void __launch_bounds__(256, 4) k_vanka_scatter(Geom g, int k1, const double* __restrict__ upd, double omega,
                                                        double* __restrict__ d, int row_lo, int row_hi,
                                                        int inc_only) {
   pdl_wait();  // PDL-launched behind the GEMV that writes upd
   const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int mu = blockIdx.y, dd = blockIdx.z;
+  const int mu = blockIdx.y;
   if (c >= (size_t)g.ncells) return;
   const int ci = (int)(c % g.nx), cj = (int)(c / g.nx);
   const size_t nc = g.ncells;
-  const double* u = upd + (size_t)21 * mu * nc + (size_t)dd * nc;  // u[2a * nc + cell] = component dd of node a
+  const double* u = upd + (size_t)21 * mu * nc;  // u[(2a + comp) * nc + cell]
   double* dm = d + (size_t)mu * g.nd;
   const bool me = cj >= row_lo && cj < row_hi;
   const bool hd = cj > 0 && cj - 1 >= row_lo && cj - 1 < row_hi;
@@ -287,55 +289,75 @@ __global__ void __launch_bounds__(256) k_vanka_scatter(Geom g, int k1, const dou
   const size_t cl = ci > 0 ? c - 1 : c, cd = cj > 0 ? c - g.nx : c, cld = (ci > 0 && cj > 0) ? c - g.nx - 1 : c;
   const double ml = (ci > 0 && me) ? 1.0 : 0.0, md = hd ? 1.0 : 0.0, mld = (hd && ci > 0) ? 1.0 : 0.0;
   const double ms = me ? 1.0 : 0.0;
-  auto U = [&](size_t cell, int a) { return __ldg(u + (size_t)(2 * a) * nc + cell); };
-  double S[9];
-#pragma unroll
-  for (int a = 0; a < 9; ++a) S[a] = U(c, a);
-  const double l2 = U(cl, 2), l5 = U(cl, 5), l8 = U(cl, 8);  // left cell: its local nodes 2, 5, 8
-  const double d6 = U(cd, 6), d7 = U(cd, 7), d8 = U(cd, 8);  // down cell: 6, 7, 8
-  const double ld8 = U(cld, 8);
-  double pv[3] = {0.0, 0.0, 0.0}, po[3] = {0.0, 0.0, 0.0};
+  auto U = [&](size_t cell, int a, int dd) { return __ldg(u + (size_t)(2 * a + dd) * nc + cell); };
+  auto node = [&](int r, int cc) { return dm + 2 * ((size_t)(2 * cj + r) * g.nnx + 2 * ci + cc); };
+  auto load2 = [&](const double* p, double* v) {
+    if (VEC) {
+      const double2 t = *reinterpret_cast<const double2*>(p);
+      v[0] = t.x, v[1] = t.y;
+    } else {
+      v[0] = p[0], v[1] = p[1];
+    }
+  };
+  auto store2 = [&](double* p, const double* o, const double* sv) {
+    const double v0 = inc_only ? omega * sv[0] : o[0] + omega * sv[0];
+    const double v1 = inc_only ? omega * sv[1] : o[1] + omega * sv[1];
+    if (VEC) {
+      *reinterpret_cast<double2*>(p) = make_double2(v0, v1);
+    } else {
+      p[0] = v0, p[1] = v1;
+    }
+  };
+  double pv[3], po[3] = {0.0, 0.0, 0.0};
   double* op = dm + g.mv + 3 * c;
-  if (dd == 0) {
+  {  // the 4 nodes every cell owns: local nodes 0, 1, 3, 4 (all loads first)
+    double s[4][2], o[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int dd = 0; dd < 2; ++dd) {
+      s[0][dd] = ((0.0 + mld * U(cld, 8, dd)) + md * U(cd, 6, dd)) + ml * U(cl, 2, dd) + ms * U(c, 0, dd);
+      s[1][dd] = (0.0 + md * U(cd, 7, dd)) + ms * U(c, 1, dd);
+      s[2][dd] = (0.0 + ml * U(cl, 5, dd)) + ms * U(c, 3, dd);
+      s[3][dd] = 0.0 + ms * U(c, 4, dd);
+    }
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
       pv[j] = __ldg(upd + (size_t)(21 * mu + 18 + j) * nc + c);
       if (!inc_only) po[j] = op[j];
     }
-  }
-  const size_t s2 = 2 * (size_t)g.nnx;
-  double* r0 = dm + 2 * ((size_t)(2 * cj) * g.nnx + 2 * ci) + dd;
-  double* r1 = r0 + s2;
-  double* r2 = r1 + s2;
-  double o[9];
-  if (!inc_only) {
-    o[0] = r0[0], o[1] = r0[2], o[3] = r1[0], o[4] = r1[2];
-    if (lastx) o[2] = r0[4], o[5] = r1[4];
-    if (lasty) {
-      o[6] = r2[0], o[7] = r2[2];
-      if (lastx) o[8] = r2[4];
+    if (!inc_only) {
+      load2(node(0, 0), o[0]);
+      load2(node(0, 1), o[1]);
+      load2(node(1, 0), o[2]);
+      load2(node(1, 1), o[3]);
     }
+    store2(node(0, 0), o[0], s[0]);
+    store2(node(0, 1), o[1], s[1]);
+    store2(node(1, 0), o[2], s[2]);
+    store2(node(1, 1), o[3], s[3]);
   }
-  auto fin = [&](double* dst, int e, int slot, double sv) { dst[e] = inc_only ? omega * sv : o[slot] + omega * sv; };
-  fin(r0, 0, 0, ((0.0 + mld * ld8) + md * d6) + ml * l2 + ms * S[0]);
-  fin(r0, 2, 1, (0.0 + md * d7) + ms * S[1]);
-  fin(r1, 0, 3, (0.0 + ml * l5) + ms * S[3]);
-  fin(r1, 2, 4, 0.0 + ms * S[4]);
-  if (lastx) {
-    fin(r0, 4, 2, (0.0 + md * d8) + ms * S[2]);
-    fin(r1, 4, 5, 0.0 + ms * S[5]);
-  }
-  if (lasty) {
-    fin(r2, 0, 6, (0.0 + ml * l8) + ms * S[6]);
-    fin(r2, 2, 7, 0.0 + ms * S[7]);
-    if (lastx) fin(r2, 4, 8, 0.0 + ms * S[8]);
-  }
-  if (dd == 0) {
+  // the mesh's last node column / row: local nodes 2, 5 / 6, 7 / 8
+  if (lastx || lasty) {
+    double s[2], o[2] = {0.0, 0.0};
+    auto one = [&](int r, int cc, int a, int na, size_t ncell, double m) {
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      const double v = me ? omega * pv[j] : 0.0;
-      op[j] = inc_only ? v : po[j] + v;
+      for (int dd = 0; dd < 2; ++dd) s[dd] = na >= 0 ? (0.0 + m * U(ncell, na, dd)) + ms * U(c, a, dd) : 0.0 + ms * U(c, a, dd);
+      if (!inc_only) load2(node(r, cc), o);
+      store2(node(r, cc), o, s);
+    };
+    if (lastx) {
+      one(0, 2, 2, 8, cd, md);  // (2,0): down, self
+      one(1, 2, 5, -1, c, 0.0);
     }
+    if (lasty) {
+      one(2, 0, 6, 8, cl, ml);  // (0,2): left, self
+      one(2, 1, 7, -1, c, 0.0);
+      if (lastx) one(2, 2, 8, -1, c, 0.0);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const double v = me ? omega * pv[j] : 0.0;
+    op[j] = inc_only ? v : po[j] + v;
   }
 }
 
@@ -392,10 +414,12 @@ cudaError_t vanka_gemv(const Geom& g, int k1, const double* invT, const double* 
 cudaError_t vanka_scatter(const Geom& g, int k1, const double* upd, double omega, double* d, cudaStream_t st,
                           int row_lo, int row_hi, bool inc_only) {
   if (row_hi < 0) row_hi = g.ny;
-  dim3 grid((unsigned)((g.ncells + 255) / 256), k1, 2);
+  dim3 grid((unsigned)((g.ncells + 255) / 256), k1);
+  // node pairs (2 node, 2 node + 1) are 16-byte aligned in every Radau plane
+  const bool vec = (g.nd % 2 == 0 || k1 == 1) && ((uintptr_t)d % 16 == 0);
   cudaError_t e;
-  PDST_LAUNCH(e = launch_pdl(k_vanka_scatter, grid, dim3(256), 0, st, g, k1, upd, omega, d, row_lo, row_hi,
-                             inc_only ? 1 : 0));
+  auto kern = vec ? k_vanka_scatter<true> : k_vanka_scatter<false>;
+  PDST_LAUNCH(e = launch_pdl(kern, grid, dim3(256), 0, st, g, k1, upd, omega, d, row_lo, row_hi, inc_only ? 1 : 0));
   return e;
 }
 
