@@ -124,10 +124,28 @@ def dptr(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_double))
 
 
-def vptr(a):
-    """void* of a contiguous numpy array or a torch tensor (None -> NULL)."""
+def vptr(a, n=None, name="array"):
+    """void* of a contiguous numpy array or a torch tensor (None -> NULL).
+
+    With ``n``: the buffer must hold exactly n contiguous float64 values (the
+    C ABI takes bare pointers, so a short or mistyped buffer would be read or
+    written out of bounds); anything else raises ValueError, as the
+    reference's numpy reshapes do on a size mismatch."""
     if a is None:
         return None
+    if n is not None:
+        if isinstance(a, np.ndarray):
+            ok = a.dtype == np.float64 and a.flags.c_contiguous
+            size = a.size
+        else:
+            import torch
+
+            ok = a.dtype == torch.float64 and a.is_contiguous()
+            size = a.numel()
+        if not ok:
+            raise ValueError(f"{name}: expected a contiguous float64 buffer")
+        if size != n:
+            raise ValueError(f"{name}: expected {n} values, got {size}")
     if isinstance(a, np.ndarray):
         return C.c_void_p(a.ctypes.data)
     return C.c_void_p(a.data_ptr())

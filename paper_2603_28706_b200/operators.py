@@ -167,7 +167,7 @@ class SlabJacobian:
         kind, sigma = variant_kind(variant)
         Uc = _f64(U)
         w = self.dev.where(Uc)
-        L.check(L.lib().pdst_linearize(self.dev.h, L.vptr(Uc), kind, sigma, w), "pdst_linearize")
+        L.check(L.lib().pdst_linearize(self.dev.h, L.vptr(Uc, self.dev.ndof, "U"), kind, sigma, w), "pdst_linearize")
 
     @property
     def shape(self):
@@ -182,7 +182,8 @@ class SlabJacobian:
             raise TypeError("asynchronous matvec needs page-locked host x and out")
         y = self.dev.empty_like(xc) if out is None else out
         w = self.dev.where(xc, y, asynchronous=asynchronous)
-        L.check(L.lib().pdst_jacobian_apply(self.dev.h, L.vptr(xc), L.vptr(y), w), "pdst_jacobian_apply")
+        n = self.dev.ndof
+        L.check(L.lib().pdst_jacobian_apply(self.dev.h, L.vptr(xc, n, "x"), L.vptr(y, n, "out"), w), "pdst_jacobian_apply")
         return y
 
     def apply(self, dU):
@@ -194,7 +195,8 @@ class SlabJacobian:
         xc, rc = _f64(x), _f64(r)
         y = self.dev.empty_like(xc) if out is None else out
         w = self.dev.where(xc, rc, y)
-        L.check(L.lib().pdst_jacobian_defect(self.dev.h, L.vptr(xc), L.vptr(rc), L.vptr(y), w), "pdst_jacobian_defect")
+        n = self.dev.ndof
+        L.check(L.lib().pdst_jacobian_defect(self.dev.h, L.vptr(xc, n, "x"), L.vptr(rc, n, "r"), L.vptr(y, n, "out"), w), "pdst_jacobian_defect")
         return y
 
     __matmul__ = matvec
@@ -231,7 +233,8 @@ def slab_residual(ctx, U, advect=None, dev: SlabDevice | None = None, device=0):
             vm = np.ascontiguousarray(vm, dtype=np.float64)
         R = dev.empty_like(Uc)
         w = dev.where(Uc, vm, fq, adv, R)
-        L.check(L.lib().pdst_residual(dev.h, L.vptr(Uc), L.vptr(vm), L.vptr(fq), L.vptr(adv), L.vptr(R), w),
+        L.check(L.lib().pdst_residual(dev.h, L.vptr(Uc, dev.ndof, "U"), L.vptr(vm, dev.mv, "v_minus"), L.vptr(fq),
+                                      L.vptr(adv, None if adv is None else dev.ndof, "advect"), L.vptr(R), w),
                 "pdst_residual")
         return R
     finally:
@@ -251,13 +254,13 @@ class MassNorm:
         flat = xc.reshape(-1)
         y = self.dev.empty_like(flat)
         w = self.dev.where(flat, y)
-        L.check(L.lib().pdst_mass_apply(self.dev.h, L.vptr(flat), L.vptr(y), w), "pdst_mass_apply")
+        L.check(L.lib().pdst_mass_apply(self.dev.h, L.vptr(flat, self.dev.ndof, "x"), L.vptr(y), w), "pdst_mass_apply")
         return y.reshape(shape)
 
     def apply_into(self, x, out):
         """out = M x for device tensors (no allocation; FGMRES basis rows)."""
         w = self.dev.where(x, out)
-        L.check(L.lib().pdst_mass_apply(self.dev.h, L.vptr(x), L.vptr(out), w), "pdst_mass_apply")
+        L.check(L.lib().pdst_mass_apply(self.dev.h, L.vptr(x, self.dev.ndof, "x"), L.vptr(out, self.dev.ndof, "out"), w), "pdst_mass_apply")
         return out
 
     def dot(self, a, b):
@@ -267,10 +270,10 @@ class MassNorm:
 
             out = torch.empty(1, dtype=torch.float64, device=ac.device)
             w = self.dev.where(ac, bc, out)
-            L.check(L.lib().pdst_mass_dot(self.dev.h, L.vptr(ac), L.vptr(bc), L.vptr(out), w), "pdst_mass_dot")
+            L.check(L.lib().pdst_mass_dot(self.dev.h, L.vptr(ac, self.dev.ndof, "a"), L.vptr(bc, self.dev.ndof, "b"), L.vptr(out), w), "pdst_mass_dot")
             return out
         out = np.zeros(1)
-        L.check(L.lib().pdst_mass_dot(self.dev.h, L.vptr(ac), L.vptr(bc), L.vptr(out), L.HOST), "pdst_mass_dot")
+        L.check(L.lib().pdst_mass_dot(self.dev.h, L.vptr(ac, self.dev.ndof, "a"), L.vptr(bc, self.dev.ndof, "b"), L.vptr(out), L.HOST), "pdst_mass_dot")
         return float(out[0])
 
     def norm(self, x):

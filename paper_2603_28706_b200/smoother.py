@@ -86,7 +86,9 @@ class VankaLevel:
         else:
             out = np.array(d, dtype=np.float64, copy=True)
         w = self.dev.where(out, rc_, asynchronous=asynchronous)
-        L.check(L.lib().pdst_vanka(self.dev.h, self.index, L.vptr(out), L.vptr(rc_), int(steps), float(omega), w),
+        n = self.dev.ndof
+        L.check(L.lib().pdst_vanka(self.dev.h, self.index, L.vptr(out, n, "d"), L.vptr(rc_, n, "r"), int(steps),
+                                   float(omega), w),
                 "pdst_vanka")
         return out
 
@@ -96,7 +98,7 @@ class VankaLevel:
         dc = _f64(defect)
         inc = self.dev.empty_like(dc)
         w = self.dev.where(dc, inc)
-        L.check(L.lib().pdst_vanka_increment(self.dev.h, self.index, L.vptr(dc), L.vptr(inc), int(row_lo),
+        L.check(L.lib().pdst_vanka_increment(self.dev.h, self.index, L.vptr(dc, self.dev.ndof, "defect"), L.vptr(inc), int(row_lo),
                                              int(row_hi), float(omega), w), "pdst_vanka_increment")
         return inc
 

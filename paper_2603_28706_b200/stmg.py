@@ -107,27 +107,31 @@ class StmgPreconditioner:
         L.check(L.lib().pdst_patch_matrices(self.dev.h, level, L.vptr(out)), "pdst_patch_matrices")
         return out
 
-    def _call(self, fn, level, x, out_len, name):
+    def _call(self, fn, level, x, in_len, out_len, name):
         xc = _f64(x).reshape(-1)
         y = self.dev.empty_like(xc, shape=(out_len,))
         w = self.dev.where(xc, y)
-        L.check(fn(self.dev.h, level, L.vptr(xc), L.vptr(y), w), name)
+        L.check(fn(self.dev.h, level, L.vptr(xc, in_len, "x"), L.vptr(y), w), name)
         return y
 
     def level_matvec(self, level, x):
-        return self._call(L.lib().pdst_level_apply, level, x, self.level_shape(level)[2], "pdst_level_apply")
+        n = self.level_shape(level)[2]
+        return self._call(L.lib().pdst_level_apply, level, x, n, n, "pdst_level_apply")
 
     def restrict(self, fine_level, r):
-        return self._call(L.lib().pdst_restrict, fine_level, r, self.level_shape(fine_level - 1)[2], "pdst_restrict")
+        return self._call(L.lib().pdst_restrict, fine_level, r, self.level_shape(fine_level)[2],
+                          self.level_shape(fine_level - 1)[2], "pdst_restrict")
 
     def prolong(self, fine_level, e):
-        return self._call(L.lib().pdst_prolong, fine_level, e, self.level_shape(fine_level)[2], "pdst_prolong")
+        return self._call(L.lib().pdst_prolong, fine_level, e, self.level_shape(fine_level - 1)[2],
+                          self.level_shape(fine_level)[2], "pdst_prolong")
 
     def vanka(self, level, d, r, steps, omega):
         rc_ = _f64(r).reshape(-1)
         out = d.clone() if _is_torch(d) else np.array(d, dtype=np.float64, copy=True).reshape(-1)
         w = self.dev.where(out, rc_)
-        L.check(L.lib().pdst_vanka(self.dev.h, level, L.vptr(out), L.vptr(rc_), int(steps), float(omega), w),
+        n = self.level_shape(level)[2]
+        L.check(L.lib().pdst_vanka(self.dev.h, level, L.vptr(out, n, "d"), L.vptr(rc_, n, "r"), int(steps), float(omega), w),
                 "pdst_vanka")
         return out
 
@@ -137,7 +141,8 @@ class StmgPreconditioner:
         rc_ = _f64(r).reshape(-1)
         z = self.dev.empty_like(rc_) if out is None else out
         w = self.dev.where(rc_, z)
-        L.check(L.lib().pdst_vcycle(self.dev.h, L.vptr(rc_), L.vptr(z), int(self.mg.pre_smooth),
+        n = self.dev.ndof
+        L.check(L.lib().pdst_vcycle(self.dev.h, L.vptr(rc_, n, "r"), L.vptr(z, n, "out"), int(self.mg.pre_smooth),
                                     int(self.mg.post_smooth), float(self.mg.omega), w), "pdst_vcycle")
         return z
 

@@ -48,3 +48,22 @@ def test_no_unresolved_library_symbols():
         return
     out = subprocess.run(["nm", "-C", "-u", _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "pdst::" not in out, [l for l in out.splitlines() if "pdst::" in l]
+
+
+def test_vptr_validates_buffers():
+    """The C ABI takes bare pointers: the host mirror checks length, dtype and
+    contiguity before handing a buffer over (ValueError, like the reference's
+    numpy reshapes on a size mismatch)."""
+    import numpy as np
+    import pytest
+    import torch
+
+    from paper_2603_28706_b200 import _lib as L
+
+    assert L.vptr(None, 5) is None
+    L.vptr(np.zeros(5), 5)
+    L.vptr(torch.zeros(5, dtype=torch.float64), 5)
+    for bad in (np.zeros(4), np.zeros(5, dtype=np.float32), np.zeros(10)[::2], torch.zeros(5),
+                torch.zeros(10, dtype=torch.float64)[::2]):
+        with pytest.raises(ValueError):
+            L.vptr(bad, 5, "x")

@@ -109,3 +109,40 @@ def test_domain_errors():
         SlabJacobian(ctx, U, pb.picard())
     with pytest.raises(ConstitutiveDomainError):
         slab_residual(ctx, U)
+
+
+def test_buffer_size_errors():
+    """Short, mistyped or strided vectors are rejected before the C ABI sees
+    their pointers (apply, defect, residual, mass, Vanka, V-cycle)."""
+    import torch
+
+    from paper_2603_28706_b200 import problem as pb
+    from paper_2603_28706_b200.operators import MassNorm, SlabJacobian, slab_residual
+    from paper_2603_28706_b200.smoother import VankaLevel
+
+    ctx = pb.make_context(4, 4, 1, pb.ModelParams(1.5, 1e-2, 1.0, 0.0), 0.01)
+    n = 2 * ctx.disc.ndof
+    U = np.zeros((2, ctx.disc.ndof))
+    jac = SlabJacobian(ctx, U, pb.modified_newton(1.0))
+    x = np.ones(n)
+    for bad in (np.ones(n - 1), np.ones(n, dtype=np.float32).astype(np.float64)[:-1]):
+        with pytest.raises(ValueError):
+            jac.matvec(bad)
+    with pytest.raises(ValueError):
+        jac.matvec(x, out=np.zeros(n, dtype=np.float32))
+    with pytest.raises(ValueError):
+        jac.matvec(x, out=np.zeros(n + 1))
+    with pytest.raises(ValueError):
+        jac.defect(x, np.ones(n - 2))
+    with pytest.raises(ValueError):
+        jac.matvec(torch.ones(2 * n, dtype=torch.float64, device="cuda")[::2])
+    with pytest.raises(ValueError):
+        slab_residual(ctx, np.zeros(n - 1))
+    with pytest.raises(ValueError):
+        MassNorm(ctx, dev=jac.dev).dot(x, np.ones(n - 1))
+    lvl = VankaLevel(ctx, U, pb.modified_newton(1.0), jac=jac)
+    with pytest.raises(ValueError):
+        lvl.smooth(x, np.ones(n - 1), 1, 0.7)
+    # the right sizes still work
+    assert np.isfinite(jac.matvec(x)).all()
+    assert np.isfinite(lvl.smooth(x, x, 1, 0.7)).all()
