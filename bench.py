@@ -400,7 +400,7 @@ def run_ours(args):
     b_apply_ours = 8.0 * (2 * N + 108 * k1 * nc + 441 * k1 * nbf)
     b_apply_ref = 8.0 * k1 * (2 * nd + 112 * nc + 56 * nbf + 4 * (2 * cfg.nx * (cfg.nx - 1)))
     # SURVEY §8d's minimal variant: state only (coefficients recomputed per apply)
-    b_apply_min = 8.0 * k1 * (2 * nd + 2 * (2 * cfg.nx + 1) * (2 * cfg.ny + 1))
+    b_apply_min = 8.0 * k1 * (2 * nd + mv)
     peak, peak_kind = _peaks()
     t_gemv = kt["vanka_gemv"][0] * 1e-3
     t_jac = kt["jacobian"][0] * 1e-3
