@@ -17,7 +17,7 @@ import numpy as np
 from . import _lib as L
 from .operators import SlabJacobian, _f64, _is_torch
 
-__all__ = ["VankaLevel", "vanka_smooth", "smoke_vanka"]
+__all__ = ["VankaLevel", "vanka_smooth"]
 
 
 class VankaLevel:
@@ -103,32 +103,13 @@ class VankaLevel:
         return inc
 
 
-def vanka_smooth(level: VankaLevel, d, r, steps: int, omega: float):
-    """Damped additive Schwarz sweeps (solver/multigrid.py:327-340)."""
-    return level.smooth(d, r, steps, omega)
-
-
-def smoke_vanka():
-    """cfg1 surrogate patches + one Vanka sweep on cuda:0 vs the CPU oracle."""
-    from oracle import pdst_oracle as orc
-
-    from . import problem as pb
-    from .synth import CONFIGS, make_slab_inputs
-
-    cfg = CONFIGS["cfg1"]
-    params = pb.ModelParams(cfg.p, cfg.delta, cfg.nu, cfg.nu_inf)
-    conf = pb.DiscretizationConfig(cfg.gamma1, cfg.gamma2, cfg.gamma_cip)
-    syn = make_slab_inputs(cfg)
-    ctx = pb.make_context(cfg.nx, cfg.ny, cfg.k, params, cfg.tau, config=conf, v_minus=syn.v_minus)
-    lvl = VankaLevel(ctx, syn.U, pb.modified_newton(cfg.nu), surrogate=True, rep_fraction=cfg.rep_fraction)
-    d = vanka_smooth(lvl, syn.d0, syn.x, 1, cfg.omega)
-
-    grid = orc.Grid(cfg.nx, cfg.ny, gamma1=cfg.gamma1, gamma2=cfg.gamma2, gamma_cip=cfg.gamma_cip)
-    slab = orc.Slab(grid, orc.Params(cfg.p, cfg.delta, cfg.nu, cfg.nu_inf), cfg.k, ctx.basis.nodes,
-                    ctx.basis.weights, ctx.tmat.K_t, ctx.tmat.m_t, cfg.tau, 0.0, syn.v_minus, None)
-    pre = orc.StmgOracle(slab, syn.U, orc.Variant("modn", cfg.nu), omega=cfg.omega, surrogate=True,
-                         rep_fraction=cfg.rep_fraction, min_cells=cfg.nx)
-    d_ref = orc.vanka(pre.levels[-1], syn.d0, syn.x, 1, cfg.omega)
-    err = np.linalg.norm(d - d_ref) / np.linalg.norm(d_ref)
-    if not err <= 1e-12:
-        raise AssertionError(f"smoke: Vanka sweep mismatch vs oracle, rel err {err:.3e}")
+def vanka_smooth(level, d, r, steps: int, omega: float):
+    """Damped additive Schwarz sweeps d <- d + omega sum_K R_K' A_K^-1 R_K (r - A d)
+    (solver/multigrid.py:327-340) on a device level: a ``VankaLevel`` or one of
+    ``StmgPreconditioner.levels`` (``stmg.MgLevel``).  Returns a new array, as
+    the reference does (multigrid.py:334)."""
+    smooth = getattr(level, "smooth", None)
+    if smooth is None:
+        raise TypeError("vanka_smooth needs a device level (VankaLevel or StmgPreconditioner.levels[i]); "
+                        f"got {type(level).__name__} whose patches live on the host")
+    return smooth(d, r, steps, omega)

@@ -23,7 +23,7 @@ jac = SlabJacobian(ctx, U, var)
 print("R finite", bool(torch.isfinite(R).all()), "|R|_M", norm.norm(R))
 for mc, cs in ((n // 4, "dense"), (n // 4, "fgmres"), (n, "fgmres")):
     try:
-        pre = StmgPreconditioner(ctx, U, var, MgConfig(min_cells=mc, rep_fraction=1.0, coarse_solver=cs))
+        pre = StmgPreconditioner(None, ctx, U, var, MgConfig(min_cells=mc, rep_fraction=1.0, coarse_solver=cs))
     except Exception as e:
         print("build failed", mc, cs, e); continue
     z = pre.apply(R.reshape(-1))

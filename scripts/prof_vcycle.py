@@ -19,7 +19,7 @@ ctx = pb.make_context(cfg.nx, cfg.ny, cfg.k, params, cfg.tau, config=conf, v_min
 mg = MgConfig(omega=cfg.omega, rep_fraction=cfg.rep_fraction, min_cells=max(1, cfg.nx >> (levels - 1)),
               coarse_solver="fgmres", coarse_sweeps=2, coarse_iters=30, coarse_rtol=1e-6)
 U = torch.as_tensor(syn.U, device="cuda")
-pre = StmgPreconditioner(ctx, U, pb.modified_newton(cfg.nu), mg)
+pre = StmgPreconditioner(None, ctx, U, pb.modified_newton(cfg.nu), mg)
 r = torch.as_tensor(syn.x, device="cuda")
 z = torch.empty_like(r)
 for _ in range(2):

@@ -71,7 +71,7 @@ def test_distributed_vcycle_matches_single_domain(nx, ny, k, P, min_cells, surro
     var = product_variant(case)
     mg = MgConfig(min_cells=min_cells, coarse_solver="fgmres", coarse_iters=12, coarse_rtol=1e-10,
                   surrogate=surrogate, rep_fraction=1.0)
-    z_ref = StmgPreconditioner(ctx, syn.U, var, mg).apply(syn.x)
+    z_ref = StmgPreconditioner(None, ctx, syn.U, var, mg).apply(syn.x)
     nl = global_levels(nx, ny, min_cells)
     assert nl >= 3
     part = StripPartition(nx, ny, P, levels=nl)
@@ -100,7 +100,7 @@ def test_distributed_fgmres_with_vcycle():
     var = product_variant(case)
     mg = MgConfig(min_cells=4, coarse_solver="fgmres", coarse_iters=12, coarse_rtol=1e-10, rep_fraction=1.0)
     jac = SlabJacobian(ctx, syn.U, var)
-    pre = StmgPreconditioner(ctx, syn.U, var, mg, jac=jac)
+    pre = StmgPreconditioner(None, ctx, syn.U, var, mg, jac=jac)
     b = torch.as_tensor(syn.x, device="cuda")
     cfg = KrylovConfig(restart=20, max_iters=20)
     ref = fgmres(jac.matvec, b, 1e-8, cfg, precond=lambda v, out=None: pre.apply(v, out=out),
@@ -144,7 +144,7 @@ def test_two_process_vcycle_and_fgmres(tmp_path):
     parts = [np.load(o) for o in outs]
     cfg, ctx, syn, var, mg = problem()
     jac = SlabJacobian(ctx, syn.U, var)
-    pre = StmgPreconditioner(ctx, syn.U, var, mg, jac=jac)
+    pre = StmgPreconditioner(None, ctx, syn.U, var, mg, jac=jac)
     z_ref = pre.apply(syn.x)
     assert_close(parts[0]["z"] + parts[1]["z"], z_ref, TOL, "two-process V-cycle")
     ref = fgmres(jac.matvec, torch.as_tensor(syn.x, device="cuda"), 1e-8, KrylovConfig(restart=20, max_iters=20),

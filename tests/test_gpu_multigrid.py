@@ -24,7 +24,7 @@ def _precond(case, fx):
     ctx = product_ctx(case, fx)
     mg = MgConfig(omega=case.cfg.omega, surrogate=case.surrogate, rep_fraction=case.cfg.rep_fraction,
                   min_cells=case.min_cells)
-    return StmgPreconditioner(ctx, fx["U"], product_variant(case), mg)
+    return StmgPreconditioner(None, ctx, fx["U"], product_variant(case), mg)
 
 
 @pytest.mark.parametrize("case", PATCH_CASES, ids=lambda c: c.name)
@@ -67,7 +67,7 @@ def test_transfers_vs_oracle(nc, k):
     fx = dict(nodes=b.nodes, weights=b.weights, K_t=tm.K_t, m_t=tm.m_t, M_t=tm.M_t, v_minus=syn.v_minus,
               tags=np.ones(2 * (3 * cx + 3 * cy), dtype=bool)[: 2 * (2 * cx + 2 * cy)], U=syn.U)
     ctx = product_ctx(case, fx)
-    pre = StmgPreconditioner(ctx, syn.U, product_variant(case),
+    pre = StmgPreconditioner(None, ctx, syn.U, product_variant(case),
                              MgConfig(min_cells=min(cx, cy), surrogate=False))
     assert pre.num_levels == 2
     P, _, _, _ = orc.transfer(orc.Grid(cx, cy), orc.Grid(2 * cx, 2 * cy))
@@ -98,7 +98,7 @@ def test_vcycle_matches_oracle_sizes():
     ctx = product_ctx(case, fx)
     s = oracle_slab(case, fx)
     ref = orc.StmgOracle(s, syn.U, variant_of(case), omega=0.7, surrogate=True, rep_fraction=0.5, min_cells=4)
-    pre = StmgPreconditioner(ctx, syn.U, product_variant(case), MgConfig(rep_fraction=0.5, min_cells=4))
+    pre = StmgPreconditioner(None, ctx, syn.U, product_variant(case), MgConfig(rep_fraction=0.5, min_cells=4))
     assert pre.num_levels == 3 == len(ref.levels)
     for ell in range(2):
         x = np.linspace(-1, 1, pre.level_shape(ell)[2])
@@ -122,7 +122,7 @@ def test_vcycle_iterative_coarse_solve(solver, sweeps):
     if solver == "vanka":
         ref.coarse_sweeps, ref.coarse_omega = sweeps, 0.6
     mg = MgConfig(rep_fraction=0.5, min_cells=4, coarse_solver=solver, coarse_sweeps=sweeps, coarse_omega=0.6)
-    pre = StmgPreconditioner(ctx, syn.U, product_variant(case), mg)
+    pre = StmgPreconditioner(None, ctx, syn.U, product_variant(case), mg)
     assert pre.num_levels == 3
     assert_close(pre.apply(syn.x), ref.apply(syn.x.copy()), VCYCLE_TOL, f"V-cycle coarse={solver}/{sweeps}")
 
@@ -142,5 +142,5 @@ def test_vcycle_coarse_fgmres(iters, rtol):
     ref.coarse_fgmres, ref.coarse_omega = (2, iters, rtol), 0.7
     mg = MgConfig(rep_fraction=0.5, min_cells=4, coarse_solver="fgmres", coarse_sweeps=2, coarse_iters=iters,
                   coarse_rtol=rtol)
-    pre = StmgPreconditioner(ctx, syn.U, product_variant(case), mg)
+    pre = StmgPreconditioner(None, ctx, syn.U, product_variant(case), mg)
     assert_close(pre.apply(syn.x), ref.apply(syn.x.copy()), 1e-8, f"V-cycle coarse fgmres {iters}/{rtol}")

@@ -24,7 +24,7 @@ def test_fgmres_matches_reference(sc):
     ctx = solver_ctx(sc, fx)
     var = product_variant(sc.case)
     jac = SlabJacobian(ctx, fx["U0"], var)
-    pre = None if "noprec" in sc.name else StmgPreconditioner(ctx, fx["U0"], var, MgConfig(min_cells=sc.min_cells))
+    pre = None if "noprec" in sc.name else StmgPreconditioner(None, ctx, fx["U0"], var, MgConfig(min_cells=sc.min_cells))
     res = fgmres(jac.matvec, fx["rhs"], sc.tol, KrylovConfig(sc.restart, sc.max_iters),
                  precond=pre.apply if pre else None, mass=MassNorm(ctx, dev=jac.dev))
     assert res.iterations == int(fx["iterations"])

@@ -135,3 +135,50 @@ def test_async_host_calls_match_sync():
     assert np.array_equal(yh, ys[2])
     with pytest.raises(ValueError):
         jac.matvec(syn.x.copy(), out=np.zeros_like(syn.x), asynchronous=True)
+
+
+# The exact kernels bench.py times: the persistent TMA-ring patch GEMVs
+# (pdst_timediag.cu k_vanka_gemv_diag_tma / k_vanka_gemv_exact_tma).  Their
+# grids are 2 CTAs per SM, so meshes of <= 24^2 cells never give a CTA a
+# second patch group; these sizes make every CTA run >= 3.5 groups, so the
+# mbarrier ring wraps (parity flips, bulk copies re-issued after
+# fence.proxy.async) several times.  (nx, ny, k, surrogate, pb): pb = patches
+# per group of the launched instantiation (tma_pb<NB>, xtma_pb<D>).
+RING_CASES = [
+    (64, 64, 1, True, 4),    # DG(1) surrogate: one complex 21x21 block, 3-stage ring
+    (96, 96, 1, True, 4),    # 7.8 groups per CTA
+    (72, 72, 2, True, 4),    # DG(2) surrogate: NB = 2 (complex + real block), 2-stage ring
+    (64, 64, 3, True, 4),    # DG(3) surrogate: two complex blocks
+    (64, 64, 0, True, 4),    # DG(0): one real block
+    (48, 48, 1, False, 2),   # exact D = 42 (the coarse levels' kernel)
+    (32, 32, 3, False, 1),   # exact D = 84
+]
+
+
+@pytest.mark.parametrize("nx,ny,k,surrogate,pb", RING_CASES)
+def test_oracle_parity_vanka_ring_wraps(nx, ny, k, surrogate, pb):
+    import torch
+
+    from test_gpu_operator import _sized_case
+
+    from paper_2603_28706_b200.smoother import VankaLevel, vanka_smooth
+
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    groups = (nx * ny + pb - 1) // pb
+    assert groups / (2 * nsm) >= 1.7, "case too small to wrap the ring"
+    case, fx, syn = _sized_case(nx, ny, k, "modn")
+    ctx = product_ctx(case, fx)
+    s = oracle_slab(case, fx)
+    pre = orc.StmgOracle(s, syn.U, variant_of(case), surrogate=surrogate, rep_fraction=1.0, min_cells=max(nx, ny))
+    fine = pre.levels[-1]
+    lvl = VankaLevel(ctx, syn.U, product_variant(case), surrogate=surrogate, rep_fraction=1.0)
+    for steps in (1, 2):
+        assert_close(vanka_smooth(lvl, syn.d0, syn.x, steps, 0.7), orc.vanka(fine, syn.d0, syn.x, steps, 0.7), TOL,
+                     f"vanka {steps} step(s)")
+    z = np.zeros_like(syn.x)
+    assert_close(vanka_smooth(lvl, z, syn.x, 1, 0.7), orc.vanka(fine, z, syn.x, 1, 0.7), TOL, "vanka from zero")
+    # device-resident vectors take the same kernels
+    dd = torch.as_tensor(syn.d0, device="cuda")
+    rr = torch.as_tensor(syn.x, device="cuda")
+    assert_close(vanka_smooth(lvl, dd, rr, 2, 0.7).cpu().numpy(), orc.vanka(fine, syn.d0, syn.x, 2, 0.7), TOL,
+                 "vanka device 2 steps")
