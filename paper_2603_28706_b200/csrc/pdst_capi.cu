@@ -294,10 +294,6 @@ int pdst_create(const pdst_mesh* mesh, const pdst_time* time, const pdst_disc* d
   h->ds.viscous = disc->enable_viscous;
   h->ds.convection = disc->enable_convection;
   h->ds.pressure = disc->enable_pressure;
-  {
-    const char* sk = getenv("PDST_SKIP");  // profiling experiments only
-    h->ds.skip = sk ? atoi(sk) : 0;
-  }
   h->model.p = params->p;
   h->model.delta = params->delta;
   h->model.nu = params->nu;

@@ -57,6 +57,27 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 
 namespace pdst {
 
+// One-time setup of a launch site, kept PER DEVICE: the dynamic shared-memory
+// opt-in (cudaFuncSetAttribute) and the SM / occupancy figures belong to a
+// device context, so handles on several devices in one process each
+// configure their own.
+constexpr int kMaxDevices = 64;
+struct DeviceOnce {
+  bool done[kMaxDevices] = {};
+  int nsm[kMaxDevices] = {};
+  int per_sm[kMaxDevices] = {};
+};
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < kMaxDevices ? d : kMaxDevices - 1;
+}
+inline int device_sms(int dev) {
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
 constexpr int MAXK1 = 7;
 
 // 1-D Gauss(4) on [0,1] and Q2 Lagrange tables, filled from the host.
@@ -97,7 +118,6 @@ struct TimeData {
 struct Disc {
   double gamma1, gamma2, gamma_cip;
   int viscous, convection, pressure;
-  int skip;  // profiling only (PDST_SKIP): 1 volume, 2 CIP, 4 sides, 8 mass, 16 assembly, 32 boundary kernel, 64 tile fixup
 };
 
 struct Model {

@@ -1343,11 +1343,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
       P[1] = __ldg(xp + 1);
       P[2] = __ldg(xp + 2);
       // tau w_mu J_mu x_mu: volume, boundary sides, CIP faces (weights carry tau w_mu)
-      if (!(ds.skip & 1))
-        jac_volume_cached<HG>(T, ds, cp, XM, r0, c0, P, slot, accp, g.hx * g.hy * tw);
-      else
-#pragma unroll
-        for (int k = 0; k < 18; ++k) slot[k * JNT] = 0.0;
+      jac_volume_cached<HG>(T, ds, cp, XM, r0, c0, P, slot, accp, g.hx * g.hy * tw);
       TR(2 + 5 * mu);
       // defect mode: the right-hand side of this cell's own nodes (lower-left
       // 2x2) and pressures, loaded now for the assembly
@@ -1361,7 +1357,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
 #pragma unroll
         for (int j = 0; j < 3; ++j) rp[j] = __ldg(rhs + (size_t)mu * g.nd + g.mv + 3 * (size_t)c + j);
       }
-      if (cip && !(ds.skip & 2)) {
+      if (cip) {
         // face matrices: own right / top, the left / bottom neighbours' right / top
         double W[4][6];
         const double* wl = tx > 0 ? cp - 1 : L.apc + ((tile - 1) * K1 + mu) * APC_SLOTS * JNT + ty * JT + JT - 1;
@@ -1385,7 +1381,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
     }
     if (valid) {
       // + M_K sum_nu K_t[mu,nu] x_nu (slab.py:199-200)
-      if (!(ds.skip & 8)) {
+      {
         const double* Krow = td.K_t + mu * K1;
         const double m = g.hx * g.hy;
 #pragma unroll
@@ -1437,7 +1433,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
     // node assembly: each cell writes the nodes it owns (lower-left 2x2 of its
     // 3x3 block, plus the right column / top row for the tile's last cells),
     // summing the <= 4 cells that contain a node in a fixed order.
-    if (valid && !(ds.skip & 16)) {
+    if (valid) {
       const size_t base = (size_t)mu * g.nd;
       const int me = ty * JT + tx;
       const bool hl = tx > 0, hd = ty > 0;
@@ -1993,14 +1989,15 @@ size_t res_smem() {
 template <int K1>
 cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* x,
                        const double* rhs, double* out, double* part, cudaStream_t st) {
-  static bool configured = false;
+  static DeviceOnce once;
   const size_t sm = jac_smem<K1>();
-  if (!configured) {
+  const int dev = current_device();
+  if (!once.done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(k_jacobian<K1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_jacobian<K1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    configured = true;
+    once.done[dev] = true;
   }
   if (!L.bmat || !L.apc) return cudaErrorInvalidValue;  // built by pdst_linearize
   dim3 grid(jac_tiles_x(g), jac_tiles_y(g));
@@ -2024,7 +2021,6 @@ cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const 
     T.cJ[3] = -tab.dE[0][1];
     T.cJ[4] = -tab.dE[0][2];
   }
-  const bool post = !(ds.skip & 64);
   const size_t ncb = n_bcells(g);
   double* sp = part + (size_t)K1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2;
   if (L.has_gamma && ds.viscous)
@@ -2032,13 +2028,13 @@ cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const 
   else  // Picard (or no viscous term): the tangent's a~ slots are zeros, not streamed
     PDST_LAUNCH(e = launch_pdl(k_jacobian<K1, false>, grid, dim3(JNT), sm, st, g, td, ds, L, x, rhs, out, part, T));
   if (e != cudaSuccess) return e;
-  if (post && !(ds.skip & 128)) {
+  {
     // tile pass -> side products (overlapping it, then waiting for it) -> epilogue
     PDST_LAUNCH(e = launch_pdl(k_side_products, dim3((unsigned)((ncb + 3) / 4), K1), dim3(128), 0, st, g, td,
                                (const double*)L.bmat, x, sp));
     if (e != cudaSuccess) return e;
   }
-  if (post) {
+  {
     const size_t n = jac_post_items(g);
     dim3 pg((unsigned)((n + 127) / 128), K1);
     PDST_LAUNCH(e = launch_pdl(k_jac_post, pg, dim3(128), 0, st, g, td, (const double*)part, (const double*)sp, rhs, out));
@@ -2051,12 +2047,13 @@ template <int K1>
 cudaError_t launch_res(const Geom& g, const TimeData& td, const Disc& ds, const Model& m, const Lin& L,
                        const double* U, const double* advect, const double* vminus, const double* fqp,
                        const double* ghat, double* out, cudaStream_t st) {
-  static bool configured = false;
+  static DeviceOnce once;
   const size_t sm = res_smem<K1>();
-  if (!configured) {
+  const int dev = current_device();
+  if (!once.done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(k_residual<K1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    configured = true;
+    once.done[dev] = true;
   }
   dim3 grid((g.nx + TX - 1) / TX, (g.ny + TY - 1) / TY);
   PDST_LAUNCH(k_residual<K1><<<grid, NT, sm, st>>>(g, td, ds, m, L, U, advect, vminus, fqp, ghat, out));

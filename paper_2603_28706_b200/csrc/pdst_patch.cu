@@ -365,11 +365,12 @@ template <int D>
 cudaError_t launch_invert(const double* mats, double* invT, int np, int* bad, cudaStream_t st) {
   constexpr int WPB = inv_wpb<D>();
   const size_t smem = (size_t)WPB * (D * (D + 1) + D) * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
+  static DeviceOnce once;
+  const int dev = current_device();
+  if (!once.done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(k_invert<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    once.done[dev] = true;
   }
   PDST_LAUNCH(k_invert<D><<<(np + WPB - 1) / WPB, 32 * WPB, smem, st>>>(mats, invT, np, bad));
   return cudaGetLastError();

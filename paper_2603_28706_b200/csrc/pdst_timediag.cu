@@ -527,18 +527,17 @@ __global__ void __launch_bounds__(tma_pb<NB>() * NB * 21, TMA_CTAS_PER_SM) k_van
 template <int K1, int NB>
 cudaError_t launch_gemv_tma(const Geom& g, const TimeDiag& td, const double* binvT, const double* defect,
                             double* upd, cudaStream_t st) {
-  static int nsm = 0;
-  static bool configured = false;
+  static DeviceOnce once;
   const size_t smax = tma_smem_max<NB>();
-  if (!configured) {
+  const int dev = current_device();
+  if (!once.done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(k_vanka_gemv_diag_tma<K1, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smax);
     if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    configured = true;
+    once.nsm[dev] = device_sms(dev);
+    once.done[dev] = true;
   }
+  const int nsm = once.nsm[dev];
   constexpr int PB = tma_pb<NB>();
   const size_t sm = (size_t)tma_stages<NB>() * PB * td.pstride * sizeof(double);
   const int ngroups = (g.ncells + PB - 1) / PB;
@@ -628,23 +627,23 @@ __global__ void __launch_bounds__(xtma_pb<D>() * D, 2) k_vanka_gemv_exact_tma(Ge
 template <int D>
 cudaError_t launch_gemv_exact_tma(const Geom& g, const double* invT, const double* defect, double* upd,
                                   cudaStream_t st) {
-  static int nsm = 0, per_sm = 1;
-  static bool configured = false;
+  static DeviceOnce once;
   constexpr int PB = xtma_pb<D>();
   const size_t sm = (size_t)XTMA_STAGES * PB * D * D * sizeof(double);
-  if (!configured) {
+  const int dev = current_device();
+  if (!once.done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(k_vanka_gemv_exact_tma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)sm);
     if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    once.nsm[dev] = device_sms(dev);
     // persistent: exactly the CTAs that are resident at once
+    int per_sm = 1;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vanka_gemv_exact_tma<D>, PB * D, sm);
     if (e != cudaSuccess) return e;
-    per_sm = std::max(1, per_sm);
-    configured = true;
+    once.per_sm[dev] = std::max(1, per_sm);
+    once.done[dev] = true;
   }
+  const int nsm = once.nsm[dev], per_sm = once.per_sm[dev];
   const int ngroups = (g.ncells + PB - 1) / PB;
   const int grid = std::min(ngroups, per_sm * nsm);
   cudaError_t e;

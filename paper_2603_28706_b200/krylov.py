@@ -4,13 +4,15 @@ Drop-in counterpart of ``pdflow.solver.krylov`` (krylov.py:17-139): same
 ``KrylovConfig`` / ``FgmresResult`` / ``fgmres(op, rhs, tol, config, precond,
 mass, x0)`` signature, restart / budget / breakdown / Givens / lstsq logic and
 iteration count semantics.  The Krylov basis ``V``, its mass image ``MV`` and
-the flexible directions ``Z`` live in device memory as (m+1, n) blocks; the
-orthogonalization is classical Gram-Schmidt applied twice (CGS2), each pass
-one batched multi-dot and one fused block update in libpdst
-(``pdst_multidot`` / ``pdst_multi_axpy``), instead of the reference's modified
-Gram-Schmidt with one re-orthogonalization (krylov.py:100-108).  The small
-Hessenberg least-squares problem stays on the host, exactly as the reference
-does it (numpy Givens rotations and ``lstsq``).
+the flexible directions ``Z`` live in device memory as (m+1, n) blocks.  The
+orthogonalization is the reference's modified Gram-Schmidt with one
+re-orthogonalization pass (krylov.py:100-108) in block form: per pass one
+batched multi-dot ``c = MV' w`` (``pdst_multidot``), the MGS recurrence
+``h_i = c_i - sum_{l<i} <MV_i, V_l> h_l`` on the host from the Gram rows of
+the basis, and one fused update of ``w`` and ``M w`` (``pdst_multi_axpy``) --
+algebraically MGS for any basis.  The small Hessenberg
+least-squares problem stays on the host, exactly as the reference does it
+(numpy Givens rotations and ``lstsq``).
 
 Vectors may be torch device tensors (the fast path) or numpy arrays (copied
 to the device once; the result is returned as numpy).

@@ -1,9 +1,11 @@
-"""GPU FGMRES (M-inner product, CGS2 on device) and Newton driver against
+"""GPU FGMRES (M-inner product, block modified Gram-Schmidt on device) and Newton driver against
 the reference's own solver runs (tests/golden/make_golden_solver.py).
 
 Tolerances: iteration counts, step lengths and failure kinds exact; norms
 and solutions relative 1e-6 (Krylov iterates accumulate rounding over up to
-80 Arnoldi steps; the device orthogonalization is CGS2 instead of MGS2)."""
+80 Arnoldi steps; the device orthogonalization is MGS in block form -- a
+multi-dot plus the host-side MGS recurrence -- so its rounding differs from
+the reference's vector-by-vector MGS)."""
 
 import numpy as np
 import pytest
