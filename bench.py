@@ -171,7 +171,8 @@ def run_distributed(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     P = ws if ws > 1 else args.virtual_ranks
     base = CONFIGS[args.config]
-    cfg = dataclasses.replace(base, ny=base.ny * P, extents=(0.0, 0.0, 1.0, float(P)))
+    # weak scaling (default): cfg's rows per rank; --strong: cfg's mesh in P strips
+    cfg = base if args.strong else dataclasses.replace(base, ny=base.ny * P, extents=(0.0, 0.0, 1.0, float(P)))
     params = pb.ModelParams(cfg.p, cfg.delta, cfg.nu, cfg.nu_inf)
     conf = pb.DiscretizationConfig(cfg.gamma1, cfg.gamma2, cfg.gamma_cip)
     syn = make_slab_inputs(cfg)
@@ -270,11 +271,12 @@ def run_distributed(args):
     nloc = sum(x.numel() for x in xs)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
+        "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded 16-mode modal state + 1e-3 noise, SURVEY.md §8d; no dataset)",
-        "config": {"workload": f"{base.name} strips: {cfg.nx}x{cfg.ny} global mesh on [0,1]x[0,{P}], "
-                               f"{base.ny} cell rows per rank + 2 ghost rows per side, DG({cfg.k}), modN, surrogate "
-                               f"patches, omega={cfg.omega}",
+        "config": {"workload": f"{base.name} strips: {cfg.nx}x{cfg.ny} global mesh on [0,1]x[0,{cfg.extents[3]:g}], "
+                               f"{cfg.ny // P} cell rows per rank + 2 ghost rows per side, DG({cfg.k}), modN, "
+                               f"surrogate patches, omega={cfg.omega}",
                    "n_dof": N, "step": "distributed Jacobian apply + Vanka step (x and d halos in one grouped exchange, "
                                        "defect row, increment reverse-add)",
                    "l2": "flushed between timed steps (256 MiB write, outside events)",
@@ -781,6 +783,27 @@ def run_vcycle(args):
     return 0
 
 
+def relaunch(n):
+    """`bench.py --gpus N` outside torchrun: start N ranks (one per GPU) under
+    torch.distributed.run on 127.0.0.1 and return their exit status; fails
+    loudly when fewer than N GPUs are visible."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < n:
+        sys.stderr.write(f"bench.py: --gpus {n} requested but only {have} CUDA device(s) are visible\n")
+        return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(n), "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, cwd=ROOT).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -798,9 +821,17 @@ def main():
     ap.add_argument("--coarse-sweeps", type=int, default=30)
     ap.add_argument("--vcycle", action="store_true", help="distributed V-cycle timing (configs[4] strong scaling)")
     ap.add_argument("--coarse-iters", type=int, default=30)
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: the config's mesh split into N strips (default: weak, cfg rows per rank)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    ws = int(os.environ.get("WORLD_SIZE", "0") or 0)
+    if ws == 0 and args.gpus > 1:
+        return relaunch(args.gpus)
+    if ws and ws != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}\n")
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     if args.solve:
