@@ -408,8 +408,11 @@ def run_ours(args):
     t_jac = kt["jacobian"][0] * 1e-3
     ach = b_gemv / t_gemv / 1e9
     traffic = traffic_apply = None
-    tp = os.path.join(ROOT, "profiles", "traffic_r01.json")
-    if os.path.exists(tp) and args.config == "cfg2":  # dram bytes per launch, one ncu capture at cfg2 (scripts/ncu_traffic.py)
+    import glob
+
+    tps = sorted(glob.glob(os.path.join(ROOT, "profiles", "traffic_r*.json")))  # the latest round's capture
+    tp = tps[-1] if tps else ""
+    if tp and args.config == "cfg2":  # dram bytes per launch, one ncu capture at cfg2 (scripts/ncu_traffic.py)
         try:
             tr = json.load(open(tp))
             traffic, traffic_apply = tr.get("vanka_gemv"), tr.get("jacobian_apply")
@@ -473,6 +476,12 @@ def run_ours(args):
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_single(args.cpu_steps)
+    extra = measure_residual_and_build(cfg, ctx, syn, jac, lvl, dev, flush, peak)
+    others = {}
+    if ws == 1 and not args.no_secondary:
+        for name in args.secondary.split(","):
+            if name and name != args.config:
+                others[name] = measure_config_kernels(name, peak)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -509,6 +518,7 @@ def run_ours(args):
                                "minimal_state_equiv_gbs": b_apply_min / t_jac / 1e9},
             "vanka_gemv": {"ms": kt["vanka_gemv"][0]},
             "vanka_scatter": {"ms": kt["vanka_scatter"][0]},
+            **extra,
         },
         "apply_gdofs": N / t_jac / 1e9,
         "sweep_gdofs": N / (t_jac + t_gemv + kt["vanka_scatter"][0] * 1e-3) / 1e9,
@@ -516,6 +526,8 @@ def run_ours(args):
         "clocks": clk,
         "e2e": e2e,
     }
+    if others:
+        line["other_configs"] = others
     if cpu is not None:
         line["cpu_baseline"] = cpu
     if rank == 0:
@@ -523,6 +535,131 @@ def run_ours(args):
     if ws > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def measure_residual_and_build(cfg, ctx, syn, jac, lvl, dev, flush, peak, reps=10):
+    """Device time of the slab residual (pdst_residual, device pointers, L2
+    flushed) with its HBM roofline, and of the preconditioner build
+    (pdst_patches_build: surrogate linearization, patch assembly and the
+    temporally diagonalized factorization) against the measured FP64 peak.
+    Algorithmic traffic of the residual: U and R (k+1) nd each plus v_minus
+    (Mv); algorithmic flops of the build: SURVEY §8(d)'s 2 D^3 per patch."""
+    import torch
+
+    from paper_2603_28706_b200 import _lib as L
+
+    N = syn.x.size
+    U = torch.as_tensor(syn.U, device=dev).reshape(-1)
+    vm = torch.as_tensor(syn.v_minus, device=dev)
+    R = torch.empty_like(U)
+    w = jac.dev.where(U, vm, R)
+
+    def res():
+        L.check(L.lib().pdst_residual(jac.dev.h, L.vptr(U), L.vptr(vm), None, None, L.vptr(R), w), "pdst_residual")
+
+    for _ in range(2):
+        res()
+    ts = []
+    for i in range(reps):
+        flush.fill_(float(i))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        res()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    t_res = sum(ts) / len(ts) * 1e-3
+    b_res = 8.0 * (2 * N + ctx.disc.n_velocity)
+    # preconditioner build: rebuild the same patches (one synchronous call)
+    tb = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        lvl2 = type(lvl)(ctx, None, None, surrogate=True, rep_fraction=cfg.rep_fraction, jac=jac)
+        torch.cuda.synchronize()
+        tb.append(time.perf_counter() - t0)
+        del lvl2
+    t_build = min(tb)
+    nc, D = cfg.nx * cfg.ny, 21 * (cfg.k + 1)
+    flop = 2.0 * nc * D ** 3
+    tf = L.C.c_double()
+    L.check(L.lib().pdst_fp64_peak(torch.cuda.current_device(), L.C.byref(tf)), "pdst_fp64_peak")
+    return {
+        "residual": {"ms": t_res * 1e3, "gdofs": N / t_res / 1e9, "algorithmic_bytes": b_res,
+                     "gbs": b_res / t_res / 1e9, "frac_hbm": b_res / t_res / 1e9 / peak,
+                     "note": "pdst_residual on device pointers, L2 flushed; algorithmic bytes 8 [2 (k+1) nd + Mv] "
+                             "(state in, residual out, v_minus); FP64/latency-bound (one pow per volume point)"},
+        "patch_build": {"ms": t_build * 1e3, "algorithmic_flop": flop, "tflops": flop / t_build / 1e12,
+                        "fp64_peak_tflops": tf.value, "frac_fp64": flop / t_build / 1e12 / tf.value,
+                        "note": "pdst_patches_build wall time (surrogate linearization, element and patch assembly, "
+                                "temporally diagonalized inverses) against SURVEY 8(d)'s 2 D^3 flop per patch; "
+                                "fp64 peak measured in-run (pdst_fp64_peak, DFMA chains)"},
+    }
+
+
+def measure_config_kernels(name, peak, steps=5):
+    """Apply and Vanka-GEMV rooflines of another BASELINE config in the same
+    run (libpdst's per-launch CUDA events over `steps` apply + sweep steps,
+    L2 flushed between steps): the secondary lines of the bench output."""
+    import torch
+
+    from paper_2603_28706_b200 import _lib as L
+    from paper_2603_28706_b200 import problem as pb
+    from paper_2603_28706_b200.operators import SlabJacobian
+    from paper_2603_28706_b200.smoother import VankaLevel
+    from paper_2603_28706_b200.synth import CONFIGS, make_slab_inputs
+
+    cfg = CONFIGS[name]
+    params = pb.ModelParams(cfg.p, cfg.delta, cfg.nu, cfg.nu_inf)
+    conf = pb.DiscretizationConfig(cfg.gamma1, cfg.gamma2, cfg.gamma_cip)
+    syn = make_slab_inputs(cfg)
+    ctx = pb.make_context(cfg.nx, cfg.ny, cfg.k, params, cfg.tau, config=conf, v_minus=syn.v_minus)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    U = torch.as_tensor(syn.U, device=dev)
+    x = torch.as_tensor(syn.x, device=dev)
+    d = torch.as_tensor(syn.d0, device=dev)
+    y = torch.empty_like(x)
+    del syn
+    jac = SlabJacobian(ctx, U, pb.modified_newton(cfg.nu))
+    lvl = VankaLevel(ctx, U, pb.modified_newton(cfg.nu), surrogate=True, rep_fraction=cfg.rep_fraction, jac=jac)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+    for _ in range(2):
+        jac.matvec(x, out=y)
+        lvl.smooth(d, x, 1, cfg.omega, inplace=True)
+    torch.cuda.synchronize()
+    h = jac.dev.h
+    L.lib().pdst_profile(h, 1)
+    for i in range(steps):
+        flush.fill_(float(i))
+        jac.matvec(x, out=y)
+        lvl.smooth(d, x, 1, cfg.omega, inplace=True)
+    torch.cuda.synchronize()
+    kt = {}
+    for kid, kn in ((0, "jacobian"), (1, "vanka_gemv"), (2, "vanka_scatter")):
+        ms, cnt = L.C.c_double(), L.C.c_int64()
+        L.lib().pdst_profile_read(h, kid, L.C.byref(ms), L.C.byref(cnt))
+        kt[kn] = ms.value / max(cnt.value, 1)
+    L.lib().pdst_profile(h, 0)
+    N = x.numel()
+    nc, k1 = cfg.nx * cfg.ny, cfg.k + 1
+    nd, nbf = ctx.disc.ndof, 2 * (cfg.nx + cfg.ny)
+    b_apply_ref = 8.0 * k1 * (2 * nd + 112 * nc + 56 * nbf + 4 * (2 * cfg.nx * (cfg.nx - 1)))
+    _, nblk, bpp = lvl.patch_info()
+    b_gemv = float(nc * bpp) + 8.0 * (N + nc * 21 * k1)
+    t_j, t_g = kt["jacobian"] * 1e-3, kt["vanka_gemv"] * 1e-3
+    t_step = t_j + t_j + t_g + kt["vanka_scatter"] * 1e-3  # apply + (defect apply, GEMV, scatter)
+    out = {"workload": f"{name}: {cfg.nx}x{cfg.ny} Q2/P1disc, DG({cfg.k}), p={cfg.p}, delta={cfg.delta}, "
+                       f"nu_inf={cfg.nu_inf}, modN, surrogate patches", "n_dof": N,
+           "apply": {"ms": kt["jacobian"], "gdofs": N / t_j / 1e9, "algorithmic_bytes": b_apply_ref,
+                     "achieved_gbs": b_apply_ref / t_j / 1e9, "frac": b_apply_ref / t_j / 1e9 / peak},
+           "vanka_gemv": {"ms": kt["vanka_gemv"], "algorithmic_bytes": b_gemv, "achieved_gbs": b_gemv / t_g / 1e9,
+                          "frac": b_gemv / t_g / 1e9 / peak},
+           "vanka_scatter_ms": kt["vanka_scatter"],
+           "step_gdofs_from_kernels": N / t_step / 1e9,
+           "note": "same run as the headline line; libpdst per-launch CUDA events, L2 flushed between steps"}
+    del jac, lvl, U, x, d, y, flush
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_solve(args):
@@ -821,6 +958,9 @@ def main():
     ap.add_argument("--coarse-sweeps", type=int, default=30)
     ap.add_argument("--vcycle", action="store_true", help="distributed V-cycle timing (configs[4] strong scaling)")
     ap.add_argument("--coarse-iters", type=int, default=30)
+    ap.add_argument("--secondary", default="cfg5",
+                    help="comma-separated configs whose apply / GEMV rooflines are measured after the headline step")
+    ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: the config's mesh split into N strips (default: weak, cfg rows per rank)")
     args = ap.parse_args()

@@ -188,6 +188,11 @@ int pdst_multi_axpy(pdst_handle* h, const double* A, const double* B, int64_t ld
 int pdst_profile(pdst_handle* h, int enable);
 int pdst_profile_read(pdst_handle* h, int kernel, double* total_ms, int64_t* launches);
 
+/* Measured FP64 (DFMA) throughput of `device` in TFLOP/s: the roofline
+   denominator of the FP64-bound kernels (patch factorization, residual); no
+   reference counterpart -- benchmark bookkeeping. */
+int pdst_fp64_peak(int device, double* tflops);
+
 const char* pdst_last_error(void);
 const char* pdst_version(void);
 /* Number of kernels libpdst has launched in this process (all handles); no

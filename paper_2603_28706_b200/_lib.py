@@ -81,6 +81,7 @@ SIGNATURES = {
     "pdst_error_norms": [P, P, D, D, I, I, P, I],
     "pdst_profile": [P, I],
     "pdst_profile_read": [P, I, C.POINTER(D), C.POINTER(I64)],
+    "pdst_fp64_peak": [I, C.POINTER(D)],
     "pdst_last_error": [],
     "pdst_version": [],
     "pdst_launch_count": [],

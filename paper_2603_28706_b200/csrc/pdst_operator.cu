@@ -410,9 +410,9 @@ __device__ __noinline__ void jac_boundary_side(const Geom& g, const Disc& ds, co
 // Residual boundary-side terms (forms.py:474-507) plus, when a lifting is
 // present, the Nitsche vector B_gamma(g_hat, .) of forms.py:374-412.
 template <class ACC>
-__device__ __noinline__ void res_boundary_side(const Geom& g, const Disc& ds, const Model& m, const Lin& L, int side, int bf,
+__device__ __forceinline__ void res_boundary_side(const Geom& g, const Disc& ds, const Model& m, const Lin& L, int side, int bf,
                                   const Plane2& S, const Plane2& A, int r0, int c0, const double PI[3],
-                                  const double* ghat_nodes /*9x2 or null*/, const ACC& acc, double accp[3]) {
+                                  const double* ghat_nodes /*9x2*/, bool has_ghat, const ACC& acc, double accp[3]) {
   int axis, e;
   double n0, n1;
   side_info(side, axis, e, n0, n1);
@@ -427,7 +427,7 @@ __device__ __noinline__ void res_boundary_side(const Geom& g, const Disc& ds, co
   line_sums(A, r0, c0, axis, c_tab.E[e], LA.E);
   line_sums(A, r0, c0, axis, c_tab.dE[e], LA.D);
   double GE[3][2] = {{0, 0}, {0, 0}, {0, 0}};
-  if (ghat_nodes) {
+  if (has_ghat) {
 #pragma unroll
     for (int t = 0; t < 3; ++t)
 #pragma unroll
@@ -489,7 +489,7 @@ __device__ __noinline__ void res_boundary_side(const Geom& g, const Disc& ds, co
         accp[1] -= wq * vn * (xh - 0.5);
         accp[2] -= wq * vn * (yh - 0.5);
       }
-      if (ghat_nodes) {
+      if (has_ghat) {
         double gv[2];
 #pragma unroll
         for (int d = 0; d < 2; ++d) {
@@ -1546,11 +1546,17 @@ __global__ void __launch_bounds__(NT) k_residual(Geom g, TimeData td, Disc ds, M
   const int r0 = 2 + 2 * ty, c0 = 2 + 2 * tx;
   const double W = g.hx * g.hy;
 
-  for (int mu = 0; mu < K1; ++mu) {
+  // small meshes: one Radau node per CTA (grid.z = k+1), so the register-heavy
+  // residual (1 CTA per SM) fills the waves more evenly; large ones loop over
+  // the nodes with the state staged once
+  const int mu_lo = gridDim.z > 1 ? (int)blockIdx.z : 0, mu_hi = gridDim.z > 1 ? (int)blockIdx.z + 1 : K1;
+  for (int mu = mu_lo; mu < mu_hi; ++mu) {
     if (advect) stage_velocity(g, advect + (size_t)mu * g.nd, as, as + PLANE, X0, Y0);
     __syncthreads();
-    const Plane2& SP = UP[mu];
-    const Plane2& AW = advect ? AP : UP[mu];
+    // the node's planes by offset (indexing the plane array with the runtime mu
+    // would place it in local memory)
+    const Plane2 SP{us + mu * 2 * PLANE, us + mu * 2 * PLANE + PLANE};
+    const Plane2 AW = advect ? AP : SP;
     double acc[3][3][2];
 #pragma unroll
     for (int a = 0; a < 3; ++a)
@@ -1627,29 +1633,48 @@ __global__ void __launch_bounds__(NT) k_residual(Geom g, TimeData td, Disc ds, M
             for (int d = 0; d < 2; ++d)
               acc[jy][ix][d] += (c_tab.G[qx][ix] * g.ihx) * Pa[jy][d] + c_tab.B[qx][ix] * Qa[jy][d];
       }
-      if (ci == 0 || cj == 0 || ci == g.nx - 1 || cj == g.ny - 1) {
-        double gn[18];
-        const double* gp = nullptr;
-        if (ghat) {
-#pragma unroll
-          for (int a = 0; a < 9; ++a) {
-            const size_t node = (size_t)(2 * cj + a / 3) * g.nnx + 2 * ci + a % 3;
-            gn[2 * a] = ghat[2 * node];
-            gn[2 * a + 1] = ghat[2 * node + 1];
-          }
-          gp = gn;
-        }
-        if (cj == 0) res_boundary_side(g, ds, m, L, 0, side_offset(g, 0) + ci, SP, AW, r0, c0, PI, gp, RegAcc{acc}, accp);
-        if (ci == g.nx - 1)
-          res_boundary_side(g, ds, m, L, 1, side_offset(g, 1) + cj, SP, AW, r0, c0, PI, gp, RegAcc{acc}, accp);
-        if (cj == g.ny - 1)
-          res_boundary_side(g, ds, m, L, 2, side_offset(g, 2) + ci, SP, AW, r0, c0, PI, gp, RegAcc{acc}, accp);
-        if (ci == 0) res_boundary_side(g, ds, m, L, 3, side_offset(g, 3) + cj, SP, AW, r0, c0, PI, gp, RegAcc{acc}, accp);
-      }
       if (cip) cip_own(g, ds, SP, AW, ci, cj, tx, ty, r0, c0, -1.0, fR, fT, RegAcc{acc});
+    }
+    // the cell's sums to its shared slot; the boundary sides (a noinline
+    // call) add into the slot, so the register accumulators never need an
+    // address (no local-memory copy of acc)
+    double* slot = sacc + threadIdx.x;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        slot[(2 * (3 * a + b)) * NT] = acc[a][b][0];
+        slot[(2 * (3 * a + b) + 1) * NT] = acc[a][b][1];
+      }
+    if (valid && (ci == 0 || cj == 0 || ci == g.nx - 1 || cj == g.ny - 1)) {
+      double PI[3];
+      const double* pp = U + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
+      PI[0] = __ldg(pp);
+      PI[1] = __ldg(pp + 1);
+      PI[2] = __ldg(pp + 2);
+      double gn[18];
+#pragma unroll
+      for (int a = 0; a < 9; ++a) {
+        const size_t node = (size_t)(2 * cj + a / 3) * g.nnx + 2 * ci + a % 3;
+        gn[2 * a] = ghat ? ghat[2 * node] : 0.0;
+        gn[2 * a + 1] = ghat ? ghat[2 * node + 1] : 0.0;
+      }
+      const bool gp = ghat != nullptr;
+      const SmemAccN<NT> sa{slot};
+      if (cj == 0) res_boundary_side(g, ds, m, L, 0, side_offset(g, 0) + ci, SP, AW, r0, c0, PI, gn, gp, sa, accp);
+      if (ci == g.nx - 1) res_boundary_side(g, ds, m, L, 1, side_offset(g, 1) + cj, SP, AW, r0, c0, PI, gn, gp, sa, accp);
+      if (cj == g.ny - 1) res_boundary_side(g, ds, m, L, 2, side_offset(g, 2) + ci, SP, AW, r0, c0, PI, gn, gp, sa, accp);
+      if (ci == 0) res_boundary_side(g, ds, m, L, 3, side_offset(g, 3) + cj, SP, AW, r0, c0, PI, gn, gp, sa, accp);
     }
     __syncthreads();
     if (valid) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          acc[a][b][0] = slot[(2 * (3 * a + b)) * NT];
+          acc[a][b][1] = slot[(2 * (3 * a + b) + 1) * NT];
+        }
       if (cip) cip_received(g, ci, cj, tx, ty, -1.0, fR, fT, RegAcc{acc});
       const double tw = td.tau_w[mu];
 #pragma unroll
@@ -1665,14 +1690,14 @@ __global__ void __launch_bounds__(NT) k_residual(Geom g, TimeData td, Disc ds, M
 #pragma unroll
         for (int j = 0; j < 3; ++j) out[o + j] = tw * accp[j];
       }
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          slot[(2 * (3 * a + b)) * NT] = acc[a][b][0];
+          slot[(2 * (3 * a + b) + 1) * NT] = acc[a][b][1];
+        }
     }
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        sacc[(2 * (3 * a + b)) * NT + threadIdx.x] = acc[a][b][0];
-        sacc[(2 * (3 * a + b) + 1) * NT + threadIdx.x] = acc[a][b][1];
-      }
     __syncthreads();
     assemble_and_store(g, sacc, i0, j0, mu, nullptr, out);
     __syncthreads();
@@ -2053,9 +2078,11 @@ cudaError_t launch_res(const Geom& g, const TimeData& td, const Disc& ds, const 
   if (!once.done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(k_residual<K1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
+    once.nsm[dev] = device_sms(dev);
     once.done[dev] = true;
   }
-  dim3 grid((g.nx + TX - 1) / TX, (g.ny + TY - 1) / TY);
+  const unsigned tiles = (unsigned)(((g.nx + TX - 1) / TX) * ((g.ny + TY - 1) / TY));
+  dim3 grid((g.nx + TX - 1) / TX, (g.ny + TY - 1) / TY, tiles < 8u * (unsigned)once.nsm[dev] ? K1 : 1);
   PDST_LAUNCH(k_residual<K1><<<grid, NT, sm, st>>>(g, td, ds, m, L, U, advect, vminus, fqp, ghat, out));
   return cudaGetLastError();
 }

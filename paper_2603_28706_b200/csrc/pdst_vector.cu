@@ -7,6 +7,8 @@
 // fixed two-level tree (deterministic).
 #include "pdst_device.cuh"
 #include "pdst_internal.h"
+#include "pdst_handle.h"
+#include "../../include/pdst.h"
 
 namespace pdst {
 namespace {
@@ -185,3 +187,50 @@ cudaError_t blend_velocity(const Geom& g, int k1, const double* coef, const doub
 }
 
 }  // namespace pdst
+
+// ---------------------------------------------------------------------------
+// FP64 peak of the device (the roofline denominator of the FP64-bound kernels:
+// patch factorization, residual): independent DFMA chains, CUDA-event timed.
+// ---------------------------------------------------------------------------
+namespace pdst {
+namespace {
+__global__ void k_dfma_peak(double* out, int iters, double s) {
+  double a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = fma(a[i], s, 1e-9);
+  }
+  double r = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r += a[i];
+  if (r == 12345.678) out[threadIdx.x] = r;  // never true: keeps the chains live
+}
+}  // namespace
+}  // namespace pdst
+
+extern "C" int pdst_fp64_peak(int device, double* tflops) {
+  if (!tflops) return pdst::set_error(PDST_EINVAL, "null argument");
+  if (cudaSetDevice(device) != cudaSuccess) return pdst::set_error(PDST_ECUDA, "cudaSetDevice(%d) failed", device);
+  const int sms = pdst::device_sms(device);
+  double* out = nullptr;
+  if (cudaMalloc(&out, 1 << 16) != cudaSuccess) return pdst::set_error(PDST_ECUDA, "out of device memory");
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int blocks = sms * 8, threads = 256, iters = 20000;
+  pdst::k_dfma_peak<<<blocks, threads>>>(out, 100, 0.999);  // warm-up
+  cudaEventRecord(a);
+  pdst::k_dfma_peak<<<blocks, threads>>>(out, iters, 0.999);
+  cudaEventRecord(b);
+  cudaError_t e = cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  if (e != cudaSuccess) return pdst::set_error(PDST_ECUDA, "%s", cudaGetErrorString(e));
+  *tflops = 2.0 * 8 * iters * (double)blocks * threads / (ms * 1e-3) / 1e12;
+  return PDST_OK;
+}

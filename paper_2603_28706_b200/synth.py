@@ -106,12 +106,17 @@ def make_slab_inputs(cfg: SynthConfig | str, nodes: np.ndarray | None = None, se
 
     amp = rng.uniform(-1.0, 1.0, size=(cfg.modes, 2))
     wav = rng.integers(1, 5, size=(cfg.modes, 2))
-    X, Y = q2_node_coords(nx, ny, cfg.extents)
-    v = np.zeros((nnodes, 2))
+    # the node grid is a tensor product, so each mode is an outer product of
+    # 1-D factors: elementwise the same operations (and bits) as evaluating
+    # amp * sin(pi k X) * cos(pi l Y) on the full (2ny+1) x (2nx+1) grid
+    x0, y0, x1, y1 = cfg.extents
+    xs = x0 + 0.5 * ((x1 - x0) / nx) * np.arange(2 * nx + 1)
+    ys = y0 + 0.5 * ((y1 - y0) / ny) * np.arange(2 * ny + 1)
+    v = np.zeros((2 * ny + 1, 2 * nx + 1, 2))
     for m in range(cfg.modes):
         km, lm = wav[m]
-        v[:, 0] += amp[m, 0] * np.sin(np.pi * km * X) * np.cos(np.pi * lm * Y)
-        v[:, 1] += amp[m, 1] * np.cos(np.pi * km * X) * np.sin(np.pi * lm * Y)
+        v[:, :, 0] += (amp[m, 0] * np.sin(np.pi * km * xs))[None, :] * np.cos(np.pi * lm * ys)[:, None]
+        v[:, :, 1] += (amp[m, 1] * np.cos(np.pi * km * xs))[None, :] * np.sin(np.pi * lm * ys)[:, None]
     vflat = v.reshape(-1)
 
     U = np.empty((k1, nd))
