@@ -303,12 +303,12 @@ int pdst_patches_build(pdst_handle* h, int surrogate, double rep_fraction, int* 
   }
   // Surrogate patches share one spatial block across the Radau nodes: keep it
   // and invert the temporally diagonalized blocks instead of A_K itself.
-  const char* nd_env = getenv("PDST_NO_TIMEDIAG");
-  fl->diag = surrogate && !(nd_env && nd_env[0] == '1') && time_diagonalize(k1, h->td.K_t, h->td.tau_w, fl->tdiag);
+  fl->diag = surrogate && time_diagonalize(k1, h->td.K_t, h->td.tau_w, fl->tdiag);
   // the full D x D patch matrices are inverted on the exact path; on the
-  // diagonalized path they are kept only for read-back at moderate sizes
+  // diagonalized path nothing needs them (pdst_patch_matrices re-assembles
+  // them on request from the retained surrogate element data)
   double* mats = nullptr;
-  if (!fl->diag || nc * D * D <= kKeepMats) {
+  if (!fl->diag) {
     mats = fl->mats.ensure(nc * D * D);
     if (!mats) return set_error(PDST_ECUDA, "out of device memory (patches)");
   } else {
@@ -388,9 +388,28 @@ int pdst_patch_matrices(pdst_handle* h, int level, double* mats) {
   if (int e = check_level(h, level)) return e;
   Level* l = h->levels[level];
   if (!l->D) return set_error(PDST_ESTATE, "patches not built");
-  if (!l->mats.ptr) return set_error(PDST_ESTATE, "patch matrices of level %d are not retained at this size", level);
   CK(cudaSetDevice(h->device));
   const size_t n = (size_t)l->g.ncells * l->D * l->D;
+  if (!l->mats.ptr && l->diag && level == (int)h->levels.size() - 1 && h->ET.ptr) {
+    // diagonalized surrogate patches: assemble the D x D matrices on request
+    // from the retained surrogate element matrices (the same kernel and
+    // arithmetic as the exact path's assembly)
+    DeviceBuffer tmp;
+    PatchArgs pa{};
+    pa.g = h->g;
+    pa.td = h->td;
+    pa.ds = h->ds;
+    pa.nslot = 1;
+    pa.ET = h->ET.ptr;
+    pa.state = h->td.k1 > 1 ? h->state_rep.ptr : h->state.ptr;
+    pa.mats = tmp.ensure(n);
+    if (!pa.mats) return set_error(PDST_ECUDA, "out of device memory (patch read-back)");
+    CK(patch_assemble(pa, h->stream));
+    CK(cudaMemcpyAsync(mats, pa.mats, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return PDST_OK;
+  }
+  if (!l->mats.ptr) return set_error(PDST_ESTATE, "patch matrices of level %d are not retained at this size", level);
   CK(cudaMemcpyAsync(mats, l->mats.ptr, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   return PDST_OK;

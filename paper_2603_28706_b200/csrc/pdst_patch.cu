@@ -50,8 +50,52 @@ __device__ __forceinline__ double jump_factor(int Xn, int f) {
   return v;
 }
 
-// Spatial block entry (R_K J R_K')_{ij} of element slot s.
-__device__ double spatial_entry(const PatchArgs& a, int s, int K, int i, int j) {
+// CIP face weights of the faces that can couple two nodes of patch K, one
+// table per slot, computed once per patch (CTA) instead of once per entry:
+//   vertical faces (normal +x) between cells (fi, fj) and (fi+1, fj), fi =
+//   ki-2..ki+1, fj = kj-1..kj+1:  cwv[s][fi - ki + 2][fj - kj + 1][q]
+//   horizontal faces (normal +y) between (fi, fj) and (fi, fj+1), fj =
+//   kj-2..kj+1, fi = ki-1..ki+1:  cwh[s][fj - kj + 2][fi - ki + 1][q]
+// with the value (w_q h) |v_L . n| of the lagged left / lower trace at face
+// point q (0 for faces outside the mesh; never read for them).
+constexpr int CW_FACE = 4 * 3 * 4;  // 48 values per orientation and slot
+
+__device__ void cip_weights(const PatchArgs& a, int K, double* cwv, double* cwh) {
+  const Geom& g = a.g;
+  const int ki = K % g.nx, kj = K / g.nx;
+  for (int idx = threadIdx.x; idx < a.nslot * 2 * CW_FACE; idx += blockDim.x) {
+    const int s = idx / (2 * CW_FACE), r = idx % (2 * CW_FACE), hor = r / CW_FACE, u = r % CW_FACE;
+    const int o1 = u / 12, o2 = (u / 4) % 3, q = u % 4;
+    const double* v = a.state + (size_t)s * g.mv;
+    double val = 0.0;
+    if (!hor) {
+      const int fi = ki - 2 + o1, fj = kj - 1 + o2;
+      if (fi >= 0 && fi <= g.nx - 2 && fj >= 0 && fj <= g.ny - 1) {
+        const double h = g.hy;
+        double tr = 0.0;
+        for (int t = 0; t < 3; ++t)
+          tr = fma(c_tab.B[q][t], v[2 * ((size_t)(2 * fj + t) * g.nnx + 2 * fi + 2)], tr);
+        val = (c_tab.w[q] * h) * fabs(tr);
+      }
+      cwv[s * CW_FACE + u] = val;
+    } else {
+      const int fj = kj - 2 + o1, fi = ki - 1 + o2;
+      if (fi >= 0 && fi <= g.nx - 1 && fj >= 0 && fj <= g.ny - 2) {
+        const double h = g.hx;
+        double tr = 0.0;
+        for (int t = 0; t < 3; ++t)
+          tr = fma(c_tab.B[q][t], v[2 * ((size_t)(2 * fj + 2) * g.nnx + 2 * fi + t) + 1], tr);
+        val = (c_tab.w[q] * h) * fabs(tr);
+      }
+      cwh[s * CW_FACE + u] = val;
+    }
+  }
+}
+
+// Spatial block entry (R_K J R_K')_{ij} of element slot s (cwv / cwh: the
+// patch's face weights, cip_weights).
+__device__ double spatial_entry(const PatchArgs& a, int s, int K, int i, int j, const double* cwv,
+                                const double* cwh) {
   const Geom& g = a.g;
   const int ki = K % g.nx, kj = K / g.nx;
   const double* ET = a.ET + (size_t)s * g.ncells * 441;
@@ -69,7 +113,6 @@ __device__ double spatial_entry(const PatchArgs& a, int s, int K, int i, int j) 
       val += ET[((size_t)c * 21 + 2 * bl + e) * 21 + 2 * al + d];
     }
   if (d != e || !(a.ds.convection && a.ds.gamma_cip > 0.0)) return val;
-  const double* v = a.state + (size_t)s * g.mv;
   // vertical faces (normal +x) between (fi, fj) and (fi+1, fj)
   {
     const double h = g.hy, coef = a.ds.gamma_cip * h * h / (g.hx * g.hx);
@@ -78,13 +121,9 @@ __device__ double spatial_entry(const PatchArgs& a, int s, int K, int i, int j) 
         const double ja = jump_factor(XA, fi), jb2 = jump_factor(XB, fi);
         if (ja == 0.0 || jb2 == 0.0) continue;
         const int ta = YA - 2 * fj, tb = YB - 2 * fj;
+        const double* cw = cwv + s * CW_FACE + ((fi - ki + 2) * 3 + (fj - kj + 1)) * 4;
         double sum = 0.0;
-        for (int q = 0; q < 4; ++q) {
-          double tr = 0.0;
-          for (int t = 0; t < 3; ++t)
-            tr = fma(c_tab.B[q][t], v[2 * ((size_t)(2 * fj + t) * g.nnx + 2 * fi + 2)], tr);
-          sum += (c_tab.w[q] * h) * fabs(tr) * (ja * c_tab.B[q][ta]) * (jb2 * c_tab.B[q][tb]);
-        }
+        for (int q = 0; q < 4; ++q) sum += cw[q] * (ja * c_tab.B[q][ta]) * (jb2 * c_tab.B[q][tb]);
         val += coef * sum;
       }
   }
@@ -96,13 +135,9 @@ __device__ double spatial_entry(const PatchArgs& a, int s, int K, int i, int j) 
         const double ja = jump_factor(YA, fj), jb2 = jump_factor(YB, fj);
         if (ja == 0.0 || jb2 == 0.0) continue;
         const int ta = XA - 2 * fi, tb = XB - 2 * fi;
+        const double* cw = cwh + s * CW_FACE + ((fj - kj + 2) * 3 + (fi - ki + 1)) * 4;
         double sum = 0.0;
-        for (int q = 0; q < 4; ++q) {
-          double tr = 0.0;
-          for (int t = 0; t < 3; ++t)
-            tr = fma(c_tab.B[q][t], v[2 * ((size_t)(2 * fj + 2) * g.nnx + 2 * fi + t) + 1], tr);
-          sum += (c_tab.w[q] * h) * fabs(tr) * (ja * c_tab.B[q][ta]) * (jb2 * c_tab.B[q][tb]);
-        }
+        for (int q = 0; q < 4; ++q) sum += cw[q] * (ja * c_tab.B[q][ta]) * (jb2 * c_tab.B[q][tb]);
         val += coef * sum;
       }
   }
@@ -112,6 +147,9 @@ __device__ double spatial_entry(const PatchArgs& a, int s, int K, int i, int j) 
 __global__ void __launch_bounds__(448) k_patch_fine(PatchArgs a) {
   const int K = blockIdx.x;
   const int t = threadIdx.x;
+  __shared__ double cwv[MAXK1 * CW_FACE], cwh[MAXK1 * CW_FACE];
+  if (a.ds.convection && a.ds.gamma_cip > 0.0) cip_weights(a, K, cwv, cwh);
+  __syncthreads();
   if (t >= 441) return;
   const Geom& g = a.g;
   const int i = t / 21, j = t % 21;
@@ -123,7 +161,7 @@ __global__ void __launch_bounds__(448) k_patch_fine(PatchArgs a) {
     M = g.hx * g.hy * (m1g(2 * kj + ia / 3, 2 * kj + jb / 3, g.ny) * m1g(2 * ki + ia % 3, 2 * ki + jb % 3, g.nx));
   }
   double Js[MAXK1];
-  for (int s = 0; s < a.nslot; ++s) Js[s] = spatial_entry(a, s, K, i, j);
+  for (int s = 0; s < a.nslot; ++s) Js[s] = spatial_entry(a, s, K, i, j, cwv, cwh);
   if (a.spatial) a.spatial[(size_t)K * 441 + t] = Js[0];
   if (!a.mats) return;  // diagonalized path at scale: the spatial block is all the inverse needs
   double* A = a.mats + (size_t)K * D * D;
@@ -402,7 +440,7 @@ cudaError_t patch_invert(int k1, const double* mats, double* invT, int npatch, i
 
 cudaError_t vanka_gemv(const Geom& g, int k1, const double* invT, const double* defect, double* upd, cudaStream_t st) {
   cudaError_t e = cudaSuccess;
-  if (!getenv("PDST_NO_XTMA") && vanka_gemv_exact_tma(g, k1, invT, defect, upd, st, &e)) return e;
+  if (vanka_gemv_exact_tma(g, k1, invT, defect, upd, st, &e)) return e;
   switch (k1) {
     case 1: return launch_gemv<21>(g, invT, defect, upd, st);
     case 2: return launch_gemv<42>(g, invT, defect, upd, st);

@@ -243,41 +243,48 @@ __device__ __forceinline__ double m1g_d(int X, int Xp, int n) {
 __device__ __forceinline__ double cabs1(double2 z) { return fabs(z.x) + fabs(z.y); }
 
 // One warp per (patch, stored eigen-block): C = lam Mhat + Jhat (21x21
-// complex) in shared memory, Gauss-Jordan with partial pivoting (izamax /
-// dcabs1 pivot choice as zgetrf), output transposed binvT[K][b][j][r].
+// complex), lane r < 21 holding row r in REGISTERS, Gauss-Jordan by exchange
+// steps with partial pivoting (the pivot row is chosen among the rows not yet
+// used by the largest |Re| + |Im| as izamax / dcabs1 in zgetrf, ties to the
+// lower row) and no physical row swaps: the pivot lane scales its row and
+// broadcasts it through shared memory, the other lanes eliminate.  The same
+// operations as the in-place Gauss-Jordan with row swaps, so the same
+// rounding; after all steps lane p_k holds row k of the inverse with its
+// column k' standing for column p_k' (tableau exchange), undone on the store.
+// Output transposed: binvT[K][b][col][row].
 __global__ void __launch_bounds__(128) k_invert_diag(Geom g, TimeDiag td, const double* __restrict__ spatial,
                                                      double* __restrict__ binvT, int* __restrict__ bad) {
-  constexpr int N = 21, LD = 22, WPB = 4;
-  __shared__ double2 sm[WPB][N * LD];
-  __shared__ double2 colb[WPB][N];
-  __shared__ int perm[WPB][N];
+  constexpr int N = 21, WPB = 4;
+  __shared__ double2 prow[WPB][N];  // the current pivot row
+  __shared__ int piv[WPB][N];       // piv[k] = lane that pivoted column k
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int task = blockIdx.x * WPB + warp;
   if (task >= g.ncells * td.nblk) return;
   const int K = task / td.nblk, b = task % td.nblk;
   const int ki = K % g.nx, kj = K / g.nx;
-  double2* A = sm[warp];
   const double lr = td.lam_re[b], li = td.lam_im[b];
-  for (int idx = lane; idx < N * N; idx += 32) {
-    const int i = idx / N, j = idx % N;
-    double m = 0.0;
-    if (i < 18 && j < 18 && (i & 1) == (j & 1)) {
-      const int ia = i >> 1, jb = j >> 1;
-      m = g.hx * g.hy * (m1g_d(2 * kj + ia / 3, 2 * kj + jb / 3, g.ny) * m1g_d(2 * ki + ia % 3, 2 * ki + jb % 3, g.nx));
+  const bool row = lane < N;
+  double2 R[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    double m = 0.0, jv = 0.0;
+    if (row) {
+      if (lane < 18 && j < 18 && (lane & 1) == (j & 1)) {
+        const int ia = lane >> 1, jb = j >> 1;
+        m = g.hx * g.hy * (m1g_d(2 * kj + ia / 3, 2 * kj + jb / 3, g.ny) * m1g_d(2 * ki + ia % 3, 2 * ki + jb % 3, g.nx));
+      }
+      jv = spatial[(size_t)K * 441 + lane * N + j];
     }
-    const double jv = spatial[(size_t)K * 441 + idx];
-    A[i * LD + j] = make_double2(fma(lr, m, jv), li * m);
+    R[j] = make_double2(fma(lr, m, jv), li * m);
   }
-  __syncwarp();
+  bool used = !row;
+  int mycol = -1;
   bool singular = false;
+#pragma unroll
   for (int k = 0; k < N; ++k) {
-    double best = -1.0;
-    int bi = N;
-    const int i = k + lane;
-    if (i < N) {
-      best = cabs1(A[i * LD + k]);
-      bi = i;
-    }
+    double best = used ? -1.0 : cabs1(R[k]);
+    int bi = used ? 32 : lane;
+#pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       const double ov = __shfl_xor_sync(0xffffffffu, best, off);
       const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
@@ -290,30 +297,29 @@ __global__ void __launch_bounds__(128) k_invert_diag(Geom g, TimeDiag td, const 
       singular = true;
       break;
     }
-    if (lane == 0) perm[warp][k] = bi;
-    if (bi != k && lane < N) {
-      const double2 t = A[k * LD + lane];
-      A[k * LD + lane] = A[bi * LD + lane];
-      A[bi * LD + lane] = t;
+    if (lane == bi) {  // the pivot row: R[k] <- 1 / R[k], R[j] <- R[j] / R[k]
+      const double2 p = R[k];
+      const double den = p.x * p.x + p.y * p.y;
+      const double2 pinv = make_double2(p.x / den, -p.y / den);
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        const double2 a = (j == k) ? make_double2(1.0, 0.0) : R[j];
+        R[j] = make_double2(a.x * pinv.x - a.y * pinv.y, a.x * pinv.y + a.y * pinv.x);
+        prow[warp][j] = R[j];
+      }
+      piv[warp][k] = lane;
+      used = true;
+      mycol = k;
     }
     __syncwarp();
-    const double2 p = A[k * LD + k];
-    const double den = p.x * p.x + p.y * p.y;
-    const double2 pinv = make_double2(p.x / den, -p.y / den);
-    __syncwarp();
-    if (lane < N) {
-      const double2 a = (lane == k) ? make_double2(1.0, 0.0) : A[k * LD + lane];
-      A[k * LD + lane] = make_double2(a.x * pinv.x - a.y * pinv.y, a.x * pinv.y + a.y * pinv.x);
-      colb[warp][lane] = A[lane * LD + k];
-    }
-    __syncwarp();
-    for (int idx = lane; idx < N * N; idx += 32) {
-      const int r = idx / N, j = idx - r * N;
-      if (r == k) continue;
-      const double2 f = colb[warp][r];
-      const double2 base = (j == k) ? make_double2(0.0, 0.0) : A[r * LD + j];
-      const double2 a = A[k * LD + j];
-      A[r * LD + j] = make_double2(base.x - (f.x * a.x - f.y * a.y), base.y - (f.x * a.y + f.y * a.x));
+    if (row && lane != bi) {  // eliminate column k: R[j] -= f P[j], R[k] = -f P[k]
+      const double2 f = R[k];
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        const double2 base = (j == k) ? make_double2(0.0, 0.0) : R[j];
+        const double2 a = prow[warp][j];
+        R[j] = make_double2(base.x - (f.x * a.x - f.y * a.y), base.y - (f.x * a.y + f.y * a.x));
+      }
     }
     __syncwarp();
   }
@@ -321,28 +327,18 @@ __global__ void __launch_bounds__(128) k_invert_diag(Geom g, TimeDiag td, const 
     if (lane == 0) atomicMin(bad, K);
     return;
   }
-  for (int k = N - 1; k >= 0; --k) {
-    const int p = perm[warp][k];
-    if (p != k && lane < N) {
-      const double2 t = A[lane * LD + k];
-      A[lane * LD + k] = A[lane * LD + p];
-      A[lane * LD + p] = t;
-    }
-    __syncwarp();
-  }
+  // lane p_k holds row k = mycol of the inverse; its entry j is column piv[j]
   double* base = binvT + (size_t)K * td.pstride + td.boff[b];
-  if (td.pair[b]) {
-    double2* dst = reinterpret_cast<double2*>(base);
-    for (int idx = lane; idx < N * N; idx += 32) {
-      const int j = idx / N, r = idx - j * N;
-      dst[idx] = A[r * LD + j];
+  if (row) {
+    if (td.pair[b]) {
+      double2* dst = reinterpret_cast<double2*>(base);
+#pragma unroll
+      for (int j = 0; j < N; ++j) dst[piv[warp][j] * N + mycol] = R[j];
+    } else {  // real eigenvalue: the inverse is real (every imaginary part is an exact 0)
+#pragma unroll
+      for (int j = 0; j < N; ++j) base[piv[warp][j] * N + mycol] = R[j].x;
+      if (lane == 0) base[N * N] = 0.0;  // pad
     }
-  } else {  // real eigenvalue: the inverse is real (every imaginary part is an exact 0)
-    for (int idx = lane; idx < N * N; idx += 32) {
-      const int j = idx / N, r = idx - j * N;
-      base[idx] = A[r * LD + j].x;
-    }
-    if (lane == 0) base[N * N] = 0.0;  // pad
   }
 }
 
