@@ -153,6 +153,14 @@ int pdst_manufactured_forcing(pdst_handle* h, double t_start, double* fqp, int w
 int pdst_error_norms(pdst_handle* h, const double* U, double t0, double t1, int spatial_points, int temporal_points,
                      double* sq2, int where);
 
+/* Coarse operators of the hierarchy (MgConfig.coarse_mode,
+   solver/multigrid.py:302-324, 406-431): 0 "galerkin" (default, P' J P in
+   element form), 1 "rediscretize" (every coarse level re-linearized on its
+   own mesh at the state injected from the next finer level -- pressure zero,
+   g_hat injected alike -- with the coarse mesh's own mass and exact patches).
+   Takes effect at the next pdst_patches_build. */
+int pdst_set_coarse_mode(pdst_handle* h, int mode);
+
 /* Coarsest-level solve of the V-cycle (takes effect at the next
  * pdst_patches_build).  kind:
  *   PDST_COARSE_DENSE   the reference's dense LU of the pinned slab system

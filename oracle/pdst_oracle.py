@@ -37,7 +37,7 @@ Reference citations (file:line in /root/reference/pkg/src/pdflow):
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 import scipy.linalg as sla
@@ -920,7 +920,7 @@ def hierarchy(g: Grid, min_cells: int):
 
 class StmgOracle:
     def __init__(self, slab: Slab, U, variant: Variant, omega=0.7, pre=2, post=2, surrogate=True,
-                 rep_fraction=0.5, min_cells=4):
+                 rep_fraction=0.5, min_cells=4, coarse_mode="galerkin"):
         self.slab = slab
         self.omega, self.pre, self.post = omega, pre, post
         grids = hierarchy(slab.grid, min_cells)
@@ -932,10 +932,24 @@ class StmgOracle:
         L = len(grids)
         levels = [None] * L
         levels[-1] = LevelOp(grids[-1], j_fine, grids[-1].mass_v(), slab.K_t, slab.tau_w, jac.matvec)
+        # rediscretize (multigrid.py:302-324, 406-431): node states injected level
+        # by level (pressure 0, unused by the Jacobian), g_hat injected alike
+        states = [np.asarray(U[mu][:slab.grid.mv], float) for mu in range(slab.k1)]
+        ghat = slab.grid.g_hat
         for ell in range(L - 2, -1, -1):
-            P, P_v, _, _ = self.transfers[ell]
-            blocks = [(P.T @ jb @ P).tocsr() for jb in levels[ell + 1].j_nodes]
-            mass_c = (P_v.T @ levels[ell + 1].mass_v @ P_v).tocsr()
+            P, P_v, _, inject_v = self.transfers[ell]
+            if coarse_mode == "galerkin":
+                blocks = [(P.T @ jb @ P).tocsr() for jb in levels[ell + 1].j_nodes]
+                mass_c = (P_v.T @ levels[ell + 1].mass_v @ P_v).tocsr()
+            elif coarse_mode == "rediscretize":
+                states = [st[inject_v] for st in states]
+                if ghat is not None:
+                    ghat = np.asarray(ghat)[inject_v]
+                    grids[ell] = replace(grids[ell], g_hat=ghat)
+                blocks = [spatial_jacobian_matrix(linearize(grids[ell], slab.params, variant, st)) for st in states]
+                mass_c = grids[ell].mass_v()
+            else:
+                raise ValueError(coarse_mode)
             levels[ell] = LevelOp(grids[ell], blocks, mass_c, slab.K_t, slab.tau_w)
             levels[ell].matvec = sparse_matvec(levels[ell])
         for ell, lv in enumerate(levels):

@@ -77,6 +77,7 @@ SIGNATURES = {
     "pdst_prolong": [P, I, P, P, I],
     "pdst_vcycle": [P, P, P, I, I, D, I],
     "pdst_set_coarse_solver": [P, I, I, D, I, D],
+    "pdst_set_coarse_mode": [P, I],
     "pdst_manufactured_forcing": [P, D, P, I],
     "pdst_error_norms": [P, P, D, D, I, I, P, I],
     "pdst_profile": [P, I],

@@ -283,6 +283,7 @@ int pdst_create(const pdst_mesh* mesh, const pdst_time* time, const pdst_disc* d
   h->td.k1 = k1;
   h->tau = tau;
   h->nodes.assign(time->nodes, time->nodes + k1);
+  h->weights.assign(time->weights, time->weights + k1);
   for (int i = 0; i < k1; ++i) {
     h->td.tau_w[i] = tau * time->weights[i];  // ctx.tau * ctx.basis.weights (slab.py:171)
     h->td.m_t[i] = time->m_t[i];

@@ -767,4 +767,29 @@ cudaError_t axpy(size_t n, double a, const double* x, double* y, cudaStream_t st
   return cudaGetLastError();
 }
 
+namespace {
+__global__ void k_inject(Geom gc, Geom gf, const double* __restrict__ vf, size_t sf, double* __restrict__ vc,
+                         size_t sc, int zero_pressure) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int mu = blockIdx.y;
+  const size_t nn = (size_t)gc.nnx * gc.nny;
+  if (t < nn) {
+    const int i = (int)(t % gc.nnx), j = (int)(t / gc.nnx);
+    const size_t f = 2 * ((size_t)(2 * j) * gf.nnx + 2 * i);
+    vc[mu * sc + 2 * t] = vf[mu * sf + f];
+    vc[mu * sc + 2 * t + 1] = vf[mu * sf + f + 1];
+  } else if (zero_pressure && t < nn + 3 * (size_t)gc.ncells) {
+    vc[mu * sc + gc.mv + (t - nn)] = 0.0;
+  }
+}
+}  // namespace
+
+cudaError_t inject_velocity(const Geom& gc, const Geom& gf, int k1, const double* vf, size_t sf, double* vc,
+                            size_t sc, bool zero_pressure, cudaStream_t st) {
+  const size_t n = (size_t)gc.nnx * gc.nny + (zero_pressure ? 3 * (size_t)gc.ncells : 0);
+  PDST_LAUNCH(k_inject<<<dim3((unsigned)((n + 255) / 256), k1), 256, 0, st>>>(gc, gf, vf, sf, vc, sc,
+                                                                              zero_pressure ? 1 : 0));
+  return cudaGetLastError();
+}
+
 }  // namespace pdst

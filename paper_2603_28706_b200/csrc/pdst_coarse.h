@@ -37,5 +37,11 @@ cudaError_t dense_build(const LevelOp& op, const TimeData& td, bool pin, double*
 cudaError_t dense_solve(const double* Ainv, int n, const double* b, double* y, cudaStream_t st);
 cudaError_t project_pressure(const Geom& g, int k1, double* z, cudaStream_t st);
 cudaError_t axpy(size_t n, double a, const double* x, double* y, cudaStream_t st);
+// Node injection (multigrid.py:146-153 inject_v, used by coarse_mode
+// "rediscretize", :406-418): coarse node (i, j) <- fine node (2i, 2j), both
+// components, per block mu; blocks of stride sf (fine) / sc (coarse) doubles.
+// With zero_pressure the coarse blocks' pressure dofs are set to 0.
+cudaError_t inject_velocity(const Geom& gc, const Geom& gf, int k1, const double* vf, size_t sf, double* vc,
+                            size_t sc, bool zero_pressure, cudaStream_t st);
 
 }  // namespace pdst

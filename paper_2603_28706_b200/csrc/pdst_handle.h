@@ -9,7 +9,12 @@
 #include "pdst_internal.h"
 #include "pdst_patch.h"
 
+struct pdst_handle;
+
 namespace pdst {
+
+// Destroys a rediscretized level's handle (pdst_mg.cu).
+void destroy_child(pdst_handle* c);
 
 struct DeviceBuffer {
   double* ptr = nullptr;
@@ -54,7 +59,13 @@ struct Level {
   // coarsest-level FGMRES: basis V [(m+1) n], preconditioned directions Z [m n],
   // work vector, reduction scratch
   DeviceBuffer kv, kz, kw, ks;
+  // coarse_mode "rediscretize" (multigrid.py:302-324, 406-431): the level's
+  // operator is the matrix-free Jacobian of its own mesh, linearized at the
+  // injected state, held by a child handle (which also owns the level's exact
+  // patches and, on the coarsest level, its coarse solve)
+  pdst_handle* child = nullptr;
   ~Level() {
+    if (child) destroy_child(child);
     if (dirichlet) cudaFree(dirichlet);
   }
 };
@@ -132,6 +143,7 @@ struct pdst_handle {
   pdst::Model model{};
   double tau = 0.0;
   std::vector<double> nodes;
+  std::vector<double> weights;  // Radau weights as given (tau_w = tau * weights)
 
   // linearization caches
   pdst::DeviceBuffer state;  // (k1, Mv)
@@ -169,6 +181,7 @@ struct pdst_handle {
   // LU, <= 16384 dofs), 1 `coarse_sweeps` Vanka steps from zero with
   // `coarse_omega`, 2 dense up to 4096 dofs else FGMRES, 3 FGMRES
   // right-preconditioned by `coarse_sweeps` Vanka steps
+  int coarse_mode = 0;  // 0 galerkin, 1 rediscretize (pdst_set_coarse_mode)
   int coarse_kind = 0;
   int coarse_sweeps = 30;
   double coarse_omega = 0.7;

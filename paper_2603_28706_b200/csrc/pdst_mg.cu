@@ -75,6 +75,18 @@ std::vector<double> lagrange_at(const std::vector<double>& nodes, double that) {
   return out;
 }
 
+}  // namespace
+
+namespace pdst {
+void destroy_child(pdst_handle* c) { pdst_destroy(c); }
+}  // namespace pdst
+
+extern "C" {
+static int build_rediscretized(pdst_handle* h, int* bad_level, int64_t* bad_patch);
+}
+
+namespace {
+
 Level* finest(pdst_handle* h) {
   if (h->levels.empty()) {
     Level* l = new Level();
@@ -255,7 +267,8 @@ int pdst_patches_build(pdst_handle* h, int surrogate, double rep_fraction, int* 
   int* badi = reinterpret_cast<int*>(bad);
 
   // exact per-node element matrices of the finest level (Galerkin input and exact patches)
-  const bool need_exact = multilevel || !surrogate || single_solve;
+  const bool redisc = multilevel && h->coarse_mode == 1;
+  const bool need_exact = (multilevel && !redisc) || !surrogate || single_solve;
   if (need_exact) {
     double* ET = fl->ecell.ensure((size_t)k1 * nc * 441);
     if (!ET) return set_error(PDST_ECUDA, "out of device memory (element matrices)");
@@ -325,7 +338,10 @@ int pdst_patches_build(pdst_handle* h, int surrogate, double rep_fraction, int* 
   if (int e = invert_level_patches(h, L - 1, badi, bad_level, bad_patch)) return e;
 
   // ---- coarse levels: Galerkin operators, exact patches (multigrid.py:435-488) ----
-  for (int l = L - 2; l >= 0; --l) {
+  if (redisc) {
+    if (int e = build_rediscretized(h, bad_level, bad_patch)) return e;
+  }
+  for (int l = redisc ? -1 : L - 2; l >= 0; --l) {
     Level* lv = h->levels[l];
     const Geom& gc = lv->g;
     double* ec = lv->ecell.ensure((size_t)k1 * gc.ncells * 441);
@@ -353,6 +369,10 @@ int pdst_patches_build(pdst_handle* h, int surrogate, double rep_fraction, int* 
   }
 
   // ---- coarsest-level solve (multigrid.py:494-520) ----
+  if (redisc) {  // held by the coarsest level's child handle
+    h->coarse_valid = true;
+    return PDST_OK;
+  }
   if (multilevel || single_solve) {
     Level* c0 = h->levels[0];
     const int n = k1 * c0->g.nd;
@@ -388,6 +408,7 @@ int pdst_patch_matrices(pdst_handle* h, int level, double* mats) {
   if (int e = check_level(h, level)) return e;
   Level* l = h->levels[level];
   if (!l->D) return set_error(PDST_ESTATE, "patches not built");
+  if (l->child) return pdst_patch_matrices(l->child, 0, mats);
   CK(cudaSetDevice(h->device));
   const size_t n = (size_t)l->g.ncells * l->D * l->D;
   if (!l->mats.ptr && l->diag && level == (int)h->levels.size() - 1 && h->ET.ptr) {
@@ -420,6 +441,7 @@ int pdst_patch_info(pdst_handle* h, int level, int32_t* D, int32_t* diag_blocks,
   if (int e = check_level(h, level)) return e;
   Level* l = h->levels[level];
   if (!l->D) return set_error(PDST_ESTATE, "patches not built");
+  if (l->child) return pdst_patch_info(l->child, 0, D, diag_blocks, bytes_per_patch);
   if (D) *D = l->D;
   if (diag_blocks) *diag_blocks = l->diag ? l->tdiag.nblk : 0;
   if (bytes_per_patch)
@@ -427,9 +449,89 @@ int pdst_patch_info(pdst_handle* h, int level, int32_t* D, int32_t* diag_blocks,
   return PDST_OK;
 }
 
+// coarse_mode "rediscretize" (multigrid.py:302-324, 406-431): a child handle
+// per coarse level, created on the level's mesh (inherited side tags) with the
+// slab's time basis, discretization and model, linearized with the same
+// tangent at the velocity injected from the next finer level (pressure 0) and
+// the injected lifting; its exact patches are the level's patches, its mass
+// the level's mass (the coarse mesh's own, multigrid.py:431), and the
+// coarsest child solves the coarsest level (dense or iterative, as the
+// parent is configured).
+static int build_rediscretized(pdst_handle* h, int* bad_level, int64_t* bad_patch) {
+  const int L = (int)h->levels.size();
+  const int k1 = h->td.k1;
+  const double* vf = h->state.ptr;  // (k1, Mv) velocity of the finer level
+  size_t sf = h->g.mv;
+  Geom gf = h->g;
+  const double* ghf = h->has_ghat ? h->ghat.ptr : nullptr;
+  std::vector<double> Kt((size_t)k1 * k1), mt(k1);
+  for (int i = 0; i < k1; ++i) {
+    mt[i] = h->td.m_t[i];
+    for (int j = 0; j < k1; ++j) Kt[(size_t)i * k1 + j] = h->td.K_t[i * k1 + j];
+  }
+  for (int l = L - 2; l >= 0; --l) {
+    Level* lv = h->levels[l];
+    if (lv->child) {
+      destroy_child(lv->child);
+      lv->child = nullptr;
+    }
+    const Geom gc = lv->g;
+    pdst_mesh m{gc.nx, gc.ny, h->extents[0], h->extents[1], h->extents[2], h->extents[3], lv->dirichlet_host.data()};
+    pdst_time t{k1 - 1, h->nodes.data(), h->weights.data(), Kt.data(), mt.data()};
+    pdst_disc d{h->ds.gamma1, h->ds.gamma2, h->ds.gamma_cip, h->ds.viscous, h->ds.convection, h->ds.pressure};
+    pdst_params pp{h->model.p, h->model.delta, h->model.nu, h->model.nu_inf};
+    pdst_handle* c = nullptr;
+    if (int e = pdst_create(&m, &t, &d, &pp, h->tau, h->device, h->stream, &c)) return e;
+    lv->child = c;
+    double* uc = c->scratch_c.ensure((size_t)k1 * gc.nd);
+    if (!uc) return set_error(PDST_ECUDA, "out of device memory (rediscretized level)");
+    CK(inject_velocity(gc, gf, k1, vf, sf, uc, gc.nd, true, h->stream));
+    if (ghf) {
+      double* gh = c->scratch_f.ensure(gc.mv);
+      if (!gh) return set_error(PDST_ECUDA, "out of device memory (rediscretized level)");
+      CK(inject_velocity(gc, gf, 1, ghf, gf.mv, gh, gc.mv, false, h->stream));
+      if (int e = pdst_set_lifting(c, gh, PDST_DEVICE)) return e;
+    }
+    if (int e = pdst_linearize(c, uc, h->model.kind, h->model.sigma_max, PDST_DEVICE)) return e;
+    if (l == 0) {  // the coarsest level: a one-level hierarchy whose V-cycle is the coarse solve
+      int nl = 0;
+      if (int e = pdst_hierarchy(c, INT_MAX, &nl)) return e;
+      if (int e = pdst_set_coarse_solver(c, h->coarse_kind, h->coarse_sweeps, h->coarse_omega, h->coarse_iters,
+                                         h->coarse_rtol))
+        return e;
+    }
+    int bl = -1;
+    int64_t bp = -1;
+    if (int e = pdst_patches_build(c, 0, 0.5, &bl, &bp)) {
+      if (e == PDST_ESINGULAR) {
+        if (bad_level) *bad_level = l;
+        if (bad_patch) *bad_patch = bp;
+        return set_error(PDST_ESINGULAR, "singular patch matrix (level %d, patch %lld)", l, (long long)bp);
+      }
+      return e;
+    }
+    lv->D = 21 * k1;
+    const size_t n = (size_t)k1 * gc.nd;
+    if (!lv->w0.ensure(n) || !lv->w1.ensure(n) || !lv->w2.ensure(n) || !lv->w3.ensure(n))
+      return set_error(PDST_ECUDA, "out of device memory (level vectors)");
+    vf = c->state.ptr;
+    sf = gc.mv;
+    gf = gc;
+    ghf = c->has_ghat ? c->ghat.ptr : nullptr;
+  }
+  return PDST_OK;
+}
+
 // y = r - A_l x on level l (device pointers).
 static int level_defect(pdst_handle* h, int l, const double* x, const double* r, double* y) {
   const int L = (int)h->levels.size();
+  if (pdst_handle* c = h->levels[l]->child) {  // rediscretized level: its own matrix-free Jacobian
+    c->stream = h->stream;
+    double* part = c->jpart.ensure_zeroed(jacobian_scratch(c->g, c->td.k1));
+    if (!part) return set_error(PDST_ECUDA, "out of device memory");
+    CK(PDST_TIMED(h, PK_LEVEL, jacobian_apply(c->g, c->td, c->ds, lin_of(c), x, r, y, part, h->stream)));
+    return PDST_OK;
+  }
   if (l == L - 1) {
     double* part = h->jpart.ensure_zeroed(jacobian_scratch(h->g, h->td.k1));
     if (!part) return set_error(PDST_ECUDA, "out of device memory");
@@ -444,6 +546,10 @@ static int level_defect(pdst_handle* h, int l, const double* x, const double* r,
 // `steps` Vanka steps on level l, d updated in place (device pointers).
 static int vanka_level(pdst_handle* h, int l, double* d, const double* r, int steps, double omega) {
   Level* lv = h->levels[l];
+  if (lv->child) {  // rediscretized level: the child's exact patches
+    lv->child->stream = h->stream;
+    return vanka_level(lv->child, 0, d, r, steps, omega);
+  }
   const Geom& g = lv->g;
   const int k1 = h->td.k1;
   const size_t n = (size_t)k1 * g.nd;
@@ -530,6 +636,10 @@ int pdst_level_apply(pdst_handle* h, int level, const double* x, double* y, int 
   if (int e = check_level(h, level)) return e;
   if (level == (int)h->levels.size() - 1) return pdst_jacobian_apply(h, x, y, where);
   if (!h->patches_valid) return set_error(PDST_ESTATE, "coarse operators are built by pdst_patches_build");
+  if (pdst_handle* c = h->levels[level]->child) {
+    c->stream = h->stream;
+    return pdst_jacobian_apply(c, x, y, where);
+  }
   if (int e = check_where(where)) return e;
   CK(cudaSetDevice(h->device));
   const size_t n = (size_t)h->td.k1 * h->levels[level]->g.nd;
@@ -615,7 +725,8 @@ static int coarse_fgmres(pdst_handle* h, const double* b, double* z) {
     double* Zj = Z + (size_t)j * n;
     CK(cudaMemsetAsync(Zj, 0, n * sizeof(double), h->stream));
     if (int e = vanka_level(h, 0, Zj, Vj, h->coarse_sweeps, h->coarse_omega)) return e;
-    CK(PDST_TIMED(h, PK_LEVEL, level_apply(level_op(h, 0), h->td, Zj, nullptr, w, level_scratch(h, 0), h->stream)));
+    // w = A_0 z_j (the matrix-free Jacobian when level 0 is the handle's own mesh)
+    if (int e = level_defect(h, 0, Zj, nullptr, w)) return e;
     for (int pass = 0; pass < 2; ++pass) {  // CGS2
       CK(multidot(V, (int64_t)n, j + 1, w, (int64_t)n, part, dvec, h->stream));
       CK(multi_axpy(V, nullptr, (int64_t)n, j + 1, dvec, w, nullptr, (int64_t)n, h->stream));
@@ -665,6 +776,10 @@ static int vcycle_level(pdst_handle* h, int l, const double* b, double* z, int p
   Level* lv = h->levels[l];
   const int k1 = h->td.k1;
   const size_t n = (size_t)k1 * lv->g.nd;
+  if (l == 0 && lv->child) {  // rediscretized coarsest level: the child's coarse solve
+    lv->child->stream = h->stream;
+    return vcycle_level(lv->child, 0, b, z, pre, post, omega);
+  }
   if (l == 0) {
     if (h->coarse_iterative) {
       if (h->coarse_kind == PDST_COARSE_VANKA) {  // Vanka steps from zero on the coarsest level
@@ -688,6 +803,15 @@ static int vcycle_level(pdst_handle* h, int l, const double* b, double* z, int p
   CK(PDST_TIMED(h, PK_TRANSFER, prolong(gc, lv->g, k1, lc->w2.ptr, r, h->stream)));
   CK(axpy(n, 1.0, r, z, h->stream));
   if (int e = vanka_level(h, l, z, b, post, omega)) return e;
+  return PDST_OK;
+}
+
+int pdst_set_coarse_mode(pdst_handle* h, int mode) {
+  if (!h) return set_error(PDST_EINVAL, "null handle");
+  if (mode != 0 && mode != 1) return set_error(PDST_EINVAL, "unknown coarse mode %d (0 galerkin, 1 rediscretize)", mode);
+  h->coarse_mode = mode;
+  h->patches_valid = false;
+  h->coarse_valid = false;
   return PDST_OK;
 }
 

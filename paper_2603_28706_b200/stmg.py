@@ -66,8 +66,6 @@ class MgConfig:
             raise ValueError("coarse_omega must lie in (0, 1]")
         if self.coarse_mode not in ("galerkin", "rediscretize"):
             raise ValueError(f"unknown coarse mode {self.coarse_mode!r}")
-        if self.coarse_mode == "rediscretize":
-            raise NotImplementedError("coarse_mode='rediscretize' is not ported (galerkin is the default)")
 
 
 def _mg_get(mg, name, default):
@@ -216,8 +214,6 @@ class StmgPreconditioner:
         coarse_mode = _mg_get(mg, "coarse_mode", "galerkin")
         if coarse_mode not in ("galerkin", "rediscretize"):
             raise ValueError(f"unknown coarse mode {coarse_mode!r}")
-        if coarse_mode == "rediscretize":
-            raise NotImplementedError("coarse_mode='rediscretize' is not ported (galerkin is the default)")
         coarse_solver = _mg_get(mg, "coarse_solver", "dense")
         if coarse_solver not in _COARSE:
             raise ValueError(f"unknown coarse solver {coarse_solver!r}")
@@ -244,6 +240,10 @@ class StmgPreconditioner:
         L.check(L.lib().pdst_set_coarse_solver(self.dev.h, _COARSE[coarse_solver], sw, cw,
                                                int(_mg_get(mg, "coarse_iters", 30)),
                                                float(_mg_get(mg, "coarse_rtol", 1.0e-6))), "pdst_set_coarse_solver")
+        # coarse operators: Galerkin P' J P, or each coarse level re-linearized on
+        # its own mesh at the injected state (multigrid.py:302-324, 406-431)
+        L.check(L.lib().pdst_set_coarse_mode(self.dev.h, 1 if coarse_mode == "rediscretize" else 0),
+                "pdst_set_coarse_mode")
         self.omega = omega
         self.pre_smooth = int(_mg_get(mg, "pre_smooth", 2))
         self.post_smooth = int(_mg_get(mg, "post_smooth", 2))

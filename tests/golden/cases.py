@@ -42,6 +42,7 @@ class Case:
     patches: bool = False  # also build STMG patches / Vanka / V-cycle
     surrogate: bool = True
     min_cells: int = 4
+    coarse_mode: str = "galerkin"  # MgConfig.coarse_mode (multigrid.py:302-324)
 
 
 def _cfg(name, nx, ny, k, p=1.5, delta=1e-2, nu=1.0, nu_inf=1e-3, modes=4, seed=1, **kw):
@@ -73,6 +74,12 @@ CASES = [
          neumann_sides=("bottom",), ghat=True),
     Case("p8_k1_exn_rect", _cfg("p8_k1_exn_rect", 8, 4, 1, seed=25, extents=(0.0, 0.0, 2.0, 1.0)), variant="exn",
          patches=True, min_cells=2),
+    # coarse_mode="rediscretize": coarse levels re-linearized at the injected state
+    Case("p6_k1_modn_redisc", _cfg("p6_k1_modn_redisc", 6, 6, 1, seed=26), patches=True, coarse_mode="rediscretize"),
+    Case("p8_ghat_redisc", _cfg("p8_ghat_redisc", 8, 8, 1, seed=27), variant="exn", patches=True, min_cells=2,
+         neumann_sides=("bottom",), ghat=True, coarse_mode="rediscretize"),
+    Case("p8_k2_pic_redisc", _cfg("p8_k2_pic_redisc", 8, 8, 2, seed=28, p=1.3, delta=1e-3), variant="pic",
+         patches=True, min_cells=2, surrogate=False, coarse_mode="rediscretize"),
 ]
 
 CASE_BY_NAME = {c.name: c for c in CASES}

@@ -95,7 +95,7 @@ def gen_case(case):
     out["mass_v_diag"] = ctx.disc.mass_v.diagonal()
     if case.patches:
         mg = MgConfig(rep_fraction=cfg.rep_fraction, surrogate=case.surrogate, min_cells=case.min_cells,
-                      omega=cfg.omega)
+                      omega=cfg.omega, coarse_mode=case.coarse_mode)
         geom = MgGeometry.from_fine(ctx.disc, min_cells=mg.min_cells)
         pre = StmgPreconditioner(geom, ctx, syn.U, variant, mg)
         fine = pre.levels[-1]

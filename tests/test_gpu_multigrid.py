@@ -23,7 +23,7 @@ def _precond(case, fx):
 
     ctx = product_ctx(case, fx)
     mg = MgConfig(omega=case.cfg.omega, surrogate=case.surrogate, rep_fraction=case.cfg.rep_fraction,
-                  min_cells=case.min_cells)
+                  min_cells=case.min_cells, coarse_mode=case.coarse_mode)
     return StmgPreconditioner(None, ctx, fx["U"], product_variant(case), mg)
 
 
@@ -88,8 +88,10 @@ def test_transfers_vs_oracle(nc, k):
         assert np.array_equal(out, Pd[:, col])
 
 
-def test_vcycle_matches_oracle_sizes():
-    """V-cycle on a 3-level hierarchy (16x16 -> 8 -> 4), k = 1, surrogate patches."""
+@pytest.mark.parametrize("coarse_mode", ["galerkin", "rediscretize"])
+def test_vcycle_matches_oracle_sizes(coarse_mode):
+    """V-cycle on a 3-level hierarchy (16x16 -> 8 -> 4), k = 1, surrogate
+    patches; Galerkin or rediscretized coarse operators (multigrid.py:302-324)."""
     from test_gpu_operator import _sized_case
 
     from paper_2603_28706_b200.stmg import MgConfig, StmgPreconditioner
@@ -97,13 +99,36 @@ def test_vcycle_matches_oracle_sizes():
     case, fx, syn = _sized_case(16, 16, 1, "modn")
     ctx = product_ctx(case, fx)
     s = oracle_slab(case, fx)
-    ref = orc.StmgOracle(s, syn.U, variant_of(case), omega=0.7, surrogate=True, rep_fraction=0.5, min_cells=4)
-    pre = StmgPreconditioner(None, ctx, syn.U, product_variant(case), MgConfig(rep_fraction=0.5, min_cells=4))
+    ref = orc.StmgOracle(s, syn.U, variant_of(case), omega=0.7, surrogate=True, rep_fraction=0.5, min_cells=4,
+                         coarse_mode=coarse_mode)
+    pre = StmgPreconditioner(None, ctx, syn.U, product_variant(case),
+                             MgConfig(rep_fraction=0.5, min_cells=4, coarse_mode=coarse_mode))
     assert pre.num_levels == 3 == len(ref.levels)
     for ell in range(2):
         x = np.linspace(-1, 1, pre.level_shape(ell)[2])
-        assert_close(pre.level_matvec(ell, x), ref.levels[ell].matvec(x), TOL, f"Galerkin L{ell}")
+        assert_close(pre.level_matvec(ell, x), ref.levels[ell].matvec(x), TOL, f"{coarse_mode} L{ell}")
+        assert_close(pre.vanka(ell, 0 * x, x, 2, 0.7), orc.vanka(ref.levels[ell], 0 * x, x, 2, 0.7), TOL,
+                     f"{coarse_mode} vanka L{ell}")
     assert_close(pre.apply(syn.x), ref.apply(syn.x.copy()), VCYCLE_TOL, "V-cycle")
+
+
+def test_rediscretize_fgmres_coarse_solve():
+    """Rediscretized hierarchy whose coarsest level is solved by the coarse
+    FGMRES (the child handle takes the parent's coarse-solver settings)."""
+    from test_gpu_operator import _sized_case
+
+    from paper_2603_28706_b200.stmg import MgConfig, StmgPreconditioner
+
+    case, fx, syn = _sized_case(16, 16, 1, "exn")
+    ctx = product_ctx(case, fx)
+    s = oracle_slab(case, fx)
+    ref = orc.StmgOracle(s, syn.U, variant_of(case), omega=0.7, surrogate=True, rep_fraction=0.5, min_cells=4,
+                         coarse_mode="rediscretize")
+    ref.coarse_fgmres = (2, 20, 1e-10)
+    mg = MgConfig(rep_fraction=0.5, min_cells=4, coarse_mode="rediscretize", coarse_solver="fgmres", coarse_sweeps=2,
+                  coarse_iters=20, coarse_rtol=1e-10)
+    pre = StmgPreconditioner(None, ctx, syn.U, product_variant(case), mg)
+    assert_close(pre.apply(syn.x), ref.apply(syn.x.copy()), 1e-8, "V-cycle with coarse FGMRES")
 
 
 @pytest.mark.parametrize("solver,sweeps", [("vanka", 0), ("vanka", 12), ("auto", 12)])

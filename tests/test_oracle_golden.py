@@ -34,7 +34,7 @@ def test_patches_vanka_vcycle(case):
     fx = load(case.name)
     s = oracle_slab(case, fx)
     pre = orc.StmgOracle(s, fx["U"], variant_of(case), omega=case.cfg.omega, surrogate=case.surrogate,
-                         rep_fraction=case.cfg.rep_fraction, min_cells=case.min_cells)
+                         rep_fraction=case.cfg.rep_fraction, min_cells=case.min_cells, coarse_mode=case.coarse_mode)
     fine = pre.levels[-1]
     assert [g.nx for g in pre.grids] == list(fx["levels_nx"])
     assert np.array_equal(fine.ids, fx["patch_ids"])
