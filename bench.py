@@ -191,6 +191,9 @@ def run_distributed(args):
              for r in mine]
     for rk in ranks:
         rk.build_patches()
+        rk.strip_setup()  # the data plane inside libpdst (pdst_strip_step / pdst_strips_step_local)
+        if ws > 1:
+            rk.attach_nccl()  # torch.distributed's NCCL communicator, used by libpdst's exchanges
     torch.cuda.synchronize()
     t_setup = time.time() - t_setup
     xs = [torch.as_tensor(rk.local(syn.x), device=dev) for rk in ranks]
@@ -277,11 +280,13 @@ def run_distributed(args):
         "config": {"workload": f"{base.name} strips: {cfg.nx}x{cfg.ny} global mesh on [0,1]x[0,{cfg.extents[3]:g}], "
                                f"{cfg.ny // P} cell rows per rank + 2 ghost rows per side, DG({cfg.k}), modN, "
                                f"surrogate patches, omega={cfg.omega}",
-                   "n_dof": N, "step": "distributed Jacobian apply + Vanka step (x and d halos in one grouped exchange, "
-                                       "defect row, increment reverse-add)",
+                   "n_dof": N, "step": "distributed Jacobian apply + Vanka step inside libpdst (pdst_strip_step: "
+                                       "x / d halos, defect row and increment reverse-add as pack -> NCCL "
+                                       "send/recv (or in-process copy) -> unpack kernels, fused owned-row Vanka "
+                                       "update; one stream, no host synchronization)",
                    "l2": "flushed between timed steps (256 MiB write, outside events)",
-                   "parallelism": (f"strip partition x{ws} over NCCL send/recv" if ws > 1 else
-                                   f"{P} virtual ranks on one GPU (LocalTransport)")},
+                   "parallelism": (f"strip partition x{ws} over NCCL send/recv (libpdst, torch's communicator)"
+                                   if ws > 1 else f"{P} virtual ranks on one GPU (pdst_strips_step_local)")},
         "gpu_launches": n_launches,
         "setup_s": t_setup,
         "clocks": clk,

@@ -52,6 +52,7 @@ extern "C" {
 #define PDST_ECUDA 4     /* CUDA runtime failure */
 #define PDST_ESTATE 5    /* call order (e.g. apply before linearize) */
 #define PDST_ENOTSUP 6   /* unsupported size (k > 3 for the kernels) */
+#define PDST_ENCCL 7     /* NCCL failure in a strip exchange */
 
 #define PDST_HOST 0
 #define PDST_DEVICE 1
@@ -195,6 +196,34 @@ int pdst_multi_axpy(pdst_handle* h, const double* A, const double* B, int64_t ld
 
 int pdst_profile(pdst_handle* h, int enable);
 int pdst_profile_read(pdst_handle* h, int kernel, double* total_ms, int64_t* launches);
+
+/* ---- strip partition: the distributed data plane -------
+   The handle's mesh is rank `rank`'s local strip of an nx x ny_global mesh:
+   global cell rows [c_lo, c_hi), owned [a, b) (paper_2603_28706_b200.partition
+   RankLayout; two ghost cell rows towards every neighbour).  lower_c_hi /
+   upper_c_lo: the neighbours' local row ranges (what they receive). */
+int pdst_strip(pdst_handle* h, int rank, int nranks, int ny_global, int a, int b, int c_lo, int c_hi, int lower_c_hi,
+               int upper_c_lo);
+/* The ranks' NCCL communicator (ncclComm_t, rank order = partition order),
+   e.g. torch.distributed's ProcessGroupNCCL._comm_ptr(); NULL detaches.
+   Exchanges are ncclSend / ncclRecv groups on the handle's stream, resolved
+   in the process's loaded libnccl.so.2 (SURVEY §8b "nccl_comm"). */
+int pdst_strip_comm(pdst_handle* h, void* nccl_comm);
+/* Refresh the ghost rows of the local (device) vector x from the neighbours
+   (halo pack kernel -> NCCL group -> unpack kernel). */
+int pdst_strip_halo(pdst_handle* h, double* x);
+/* This rank's distributed Jacobian apply + one Vanka step, device pointers,
+   everything enqueued on the handle's stream (no host synchronization):
+   x and d halos, y = J x, e = r - J d, the defect row from the upper rank,
+   the patch GEMV, d += omega sum over the OWNED patches (one fused scatter;
+   node row 2b's increment goes to the upper rank), the lower rank's
+   increment added to row 2a.  x's and d's ghost rows are overwritten. */
+int pdst_strip_step(pdst_handle* h, const double* x, double* y, double* d, const double* r, double omega);
+/* The same step for all ranks of a partition held in one process on one
+   device (virtual ranks, partition order; the neighbours' packed buffers
+   are read directly): the parity and overhead check of the data plane. */
+int pdst_strips_step_local(pdst_handle* const* hs, int nranks, double* const* xs, double* const* ys,
+                           double* const* ds, const double* const* rs, double omega);
 
 /* Measured FP64 (DFMA) throughput of `device` in TFLOP/s: the roofline
    denominator of the FP64-bound kernels (patch factorization, residual); no

@@ -16,7 +16,7 @@ from .errors import ConstitutiveDomainError, PdstCudaError, SingularPatchError
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PDST_LIB") or os.path.join(HERE, "libpdst.so")  # PDST_LIB: experiment builds
 
-OK, EINVAL, EDOMAIN, ESINGULAR, ECUDA, ESTATE, ENOTSUP = range(7)
+OK, EINVAL, EDOMAIN, ESINGULAR, ECUDA, ESTATE, ENOTSUP, ENCCL = range(8)
 HOST, DEVICE, HOST_ASYNC = 0, 1, 2
 KIND = {"pic": 0, "exn": 1, "modn": 2}
 
@@ -83,6 +83,11 @@ SIGNATURES = {
     "pdst_profile": [P, I],
     "pdst_profile_read": [P, I, C.POINTER(D), C.POINTER(I64)],
     "pdst_fp64_peak": [I, C.POINTER(D)],
+    "pdst_strip": [P, I, I, I, I, I, I, I, I, I],
+    "pdst_strip_comm": [P, P],
+    "pdst_strip_halo": [P, P],
+    "pdst_strip_step": [P, P, P, P, P, D],
+    "pdst_strips_step_local": [P, I, P, P, P, P, D],
     "pdst_last_error": [],
     "pdst_version": [],
     "pdst_launch_count": [],

@@ -9,7 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpdst.so")
-SOURCES = ["pdst_operator.cu", "pdst_vector.cu", "pdst_krylov.cu", "pdst_patch.cu", "pdst_timediag.cu", "pdst_coarse.cu", "pdst_mg.cu", "pdst_manufactured.cu", "pdst_capi.cu"]
+SOURCES = ["pdst_operator.cu", "pdst_vector.cu", "pdst_krylov.cu", "pdst_patch.cu", "pdst_timediag.cu", "pdst_coarse.cu", "pdst_mg.cu", "pdst_manufactured.cu", "pdst_strip.cu", "pdst_capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -53,7 +53,7 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
-    cmd = [NVCC, *FLAGS, "-shared", "-o", LIB + ".tmp", *sources(), "-lcudart"]
+    cmd = [NVCC, *FLAGS, "-shared", "-o", LIB + ".tmp", *sources(), "-lcudart", "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build_ptxas.log")
     with open(log, "w") as f:

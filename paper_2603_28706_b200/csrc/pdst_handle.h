@@ -174,6 +174,17 @@ struct pdst_handle {
   pdst::AsyncSlot as_x, as_r, as_y, as_d, as_vr;
   std::vector<std::pair<const void*, cudaEvent_t>> pending_out;
 
+  // strip partition (pdst_strip.cu): this handle's mesh is rank `rank`'s
+  // local strip, global cell rows [c_lo, c_hi), owned [a, b); the neighbours'
+  // local row ranges define what they receive; nccl = the communicator of
+  // the ranks (or null for virtual ranks of one process)
+  struct StripInfo {
+    bool on = false;
+    int rank = 0, nranks = 1, ny = 0, a = 0, b = 0, c_lo = 0, c_hi = 0, lower_c_hi = 0, upper_c_lo = 0;
+    void* nccl = nullptr;
+    pdst::DeviceBuffer buf[4];  // send to lower / upper, receive from lower / upper
+  } strip;
+
   // multigrid
   std::vector<pdst::Level*> levels;  // 0 = coarsest
   int min_cells = 0;

@@ -308,10 +308,13 @@ __global__ void __launch_bounds__(256) k_vanka_gemv(Geom g, const double* __rest
 // every read is coalesced; all loads are issued before the first store.
 // Only patches of cell rows [row_lo, row_hi) contribute; inc_only writes the
 // increment instead of adding it (distributed sweeps combine increments).
+// inc_row (optional): omega * (sum of the contributing patches) of node row
+// inc_Y is also written there, [mu][2 nnx] (the increment a strip partition's
+// upper neighbour adds to its own row, csrc/pdst_strip.cu).
 template <bool VEC>
 __global__ void __launch_bounds__(256, 4) k_vanka_scatter(Geom g, int k1, const double* __restrict__ upd, double omega,
                                                        double* __restrict__ d, int row_lo, int row_hi,
-                                                       int inc_only) {
+                                                       int inc_only, double* __restrict__ inc_row, int inc_Y) {
   pdl_wait();  // PDL-launched behind the GEMV that writes upd
   const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int mu = blockIdx.y;
@@ -340,6 +343,14 @@ __global__ void __launch_bounds__(256, 4) k_vanka_scatter(Geom g, int k1, const 
   auto store2 = [&](double* p, const double* o, const double* sv) {
     const double v0 = inc_only ? omega * sv[0] : o[0] + omega * sv[0];
     const double v1 = inc_only ? omega * sv[1] : o[1] + omega * sv[1];
+    if (inc_row) {
+      const size_t node = (size_t)(p - dm) / 2;  // node index in the Radau plane
+      if ((int)(node / g.nnx) == inc_Y) {
+        double* q = inc_row + (size_t)mu * 2 * g.nnx + 2 * (node % g.nnx);
+        q[0] = omega * sv[0];
+        q[1] = omega * sv[1];
+      }
+    }
     if (VEC) {
       *reinterpret_cast<double2*>(p) = make_double2(v0, v1);
     } else {
@@ -451,14 +462,15 @@ cudaError_t vanka_gemv(const Geom& g, int k1, const double* invT, const double* 
 }
 
 cudaError_t vanka_scatter(const Geom& g, int k1, const double* upd, double omega, double* d, cudaStream_t st,
-                          int row_lo, int row_hi, bool inc_only) {
+                          int row_lo, int row_hi, bool inc_only, double* inc_row, int inc_Y) {
   if (row_hi < 0) row_hi = g.ny;
   dim3 grid((unsigned)((g.ncells + 255) / 256), k1);
   // node pairs (2 node, 2 node + 1) are 16-byte aligned in every Radau plane
   const bool vec = (g.nd % 2 == 0 || k1 == 1) && ((uintptr_t)d % 16 == 0);
   cudaError_t e;
   auto kern = vec ? k_vanka_scatter<true> : k_vanka_scatter<false>;
-  PDST_LAUNCH(e = launch_pdl(kern, grid, dim3(256), 0, st, g, k1, upd, omega, d, row_lo, row_hi, inc_only ? 1 : 0));
+  PDST_LAUNCH(e = launch_pdl(kern, grid, dim3(256), 0, st, g, k1, upd, omega, d, row_lo, row_hi, inc_only ? 1 : 0,
+                             inc_row, inc_Y));
   return e;
 }
 

@@ -53,6 +53,7 @@ cudaError_t patch_assemble(const PatchArgs& a, cudaStream_t st);
 cudaError_t patch_invert(int k1, const double* mats, double* invT, int npatch, int* bad, cudaStream_t st);
 cudaError_t vanka_gemv(const Geom& g, int k1, const double* invT, const double* defect, double* upd, cudaStream_t st);
 cudaError_t vanka_scatter(const Geom& g, int k1, const double* upd, double omega, double* d, cudaStream_t st,
-                          int row_lo = 0, int row_hi = -1, bool inc_only = false);
+                          int row_lo = 0, int row_hi = -1, bool inc_only = false, double* inc_row = nullptr,
+                          int inc_Y = -1);
 
 }  // namespace pdst

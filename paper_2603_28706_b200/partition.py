@@ -382,6 +382,36 @@ class DistributedSlab:
         self.jac = SlabJacobian(self.ctx, Ul, variant, device=device)
         self.level = None
         self.surrogate, self.rep_fraction = surrogate, rep_fraction
+        self.strip = self.nccl = False  # libpdst data plane (strip_setup / attach_nccl)
+
+    def strip_setup(self):
+        """Register this rank's strip with its libpdst handle (pdst_strip):
+        the in-library data plane (halo pack / unpack kernels, fused owned-row
+        Vanka update, NCCL exchanges) of pdst_strip_step."""
+        from . import _lib as L
+
+        lay = self.lay
+        lower_c_hi = _layout_of(lay, lay.rank - 1).c_hi if lay.rank > 0 else 0
+        upper_c_lo = _layout_of(lay, lay.rank + 1).c_lo if not lay.last else lay.ny
+        L.check(L.lib().pdst_strip(self.jac.dev.h, lay.rank, lay.nranks, lay.ny, lay.a, lay.b, lay.c_lo, lay.c_hi,
+                                   lower_c_hi, upper_c_lo), "pdst_strip")
+        self.strip = True
+
+    def attach_nccl(self, group=None):
+        """Hand torch.distributed's NCCL communicator (ProcessGroupNCCL's
+        ncclComm_t, rank order = partition order) to libpdst (pdst_strip_comm)."""
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib as L
+
+        pg = group or dist.group.WORLD
+        backend = pg._get_backend(torch.device("cuda", self.jac.dev.device))
+        ptr = backend._comm_ptr()
+        if not ptr:
+            raise RuntimeError("the NCCL communicator is not initialized (init_process_group(device_id=...))")
+        L.check(L.lib().pdst_strip_comm(self.jac.dev.h, L.C.c_void_p(ptr)), "pdst_strip_comm")
+        self.nccl = True
 
     def build_patches(self):
         from .smoother import VankaLevel
@@ -423,11 +453,55 @@ def distributed_vanka_step(ranks, ds, rs, omega, transport):
     return ds
 
 
+def strip_step(ranks, xs, ds, rs, omega, ys=None):
+    """The distributed apply + Vanka step inside libpdst (pdst_strip.cu):
+    every exchange a pack kernel, a transfer and an unpack kernel, the Vanka
+    update one fused scatter over the owned patches, all on one stream with
+    no host synchronization.  ranks: all ranks of the partition in this
+    process (virtual ranks on one device, pdst_strips_step_local) or this
+    process's one rank with an attached NCCL communicator (pdst_strip_step).
+    Returns the ys; ds updated in place."""
+    import torch
+
+    from . import _lib as L
+
+    ys = ys if ys is not None else [torch.empty_like(x) for x in xs]
+    h0 = ranks[0].jac.dev
+    h0.where(xs[0])  # torch's current stream for the whole step
+    if len(ranks) == 1 and ranks[0].lay.nranks > 1:
+        L.check(L.lib().pdst_strip_step(h0.h, L.vptr(xs[0]), L.vptr(ys[0]), L.vptr(ds[0]), L.vptr(rs[0]),
+                                        float(omega)), "pdst_strip_step")
+        return ys
+    n = len(ranks)
+    P = L.C.c_void_p * n
+    hs = P(*[rk.jac.dev.h.value for rk in ranks])
+    arr = lambda vs: P(*[v.data_ptr() for v in vs])  # noqa: E731
+    L.check(L.lib().pdst_strips_step_local(L.C.cast(hs, L.C.c_void_p), n, L.C.cast(arr(xs), L.C.c_void_p),
+                                           L.C.cast(arr(ys), L.C.c_void_p), L.C.cast(arr(ds), L.C.c_void_p),
+                                           L.C.cast(arr(rs), L.C.c_void_p), float(omega)), "pdst_strips_step_local")
+    return ys
+
+
+def _strip_ready(ranks, transport):
+    """The libpdst data plane applies: every rank registered as a strip, and
+    either all ranks in this process (LocalTransport) or one rank with its
+    NCCL communicator attached."""
+    if not all(getattr(rk, "strip", False) for rk in ranks):
+        return False
+    if isinstance(transport, LocalTransport):
+        return True
+    return len(ranks) == 1 and getattr(ranks[0], "nccl", False)
+
+
 def distributed_apply_and_vanka_step(ranks, xs, ds, rs, omega, transport):
     """y = J x and one Vanka step on d (rhs r) on every rank, the two
     independent x / d halos in one grouped exchange.  Returns the ys; ds
     updated in place.  Same results as distributed_apply then
-    distributed_vanka_step."""
+    distributed_vanka_step.  With the ranks registered as strips
+    (DistributedSlab.strip_setup, and attach_nccl across processes) the
+    whole step runs inside libpdst (strip_step)."""
+    if _strip_ready(ranks, transport) and all(hasattr(x, "data_ptr") for x in xs):
+        return strip_step(ranks, xs, ds, rs, omega)
     k1 = ranks[0].k1
     transport.exchange_many([(xs, "halo_recv", False), (ds, "halo_recv", False)], k1)
     ys = [rk.jac.matvec(x) for rk, x in zip(ranks, xs)]

@@ -119,3 +119,40 @@ def test_fused_apply_and_vanka_step(nx, ny, k, P):
         assert torch.equal(a, b)
     for a, b in zip(ds, ds2):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("nx,ny,k,P,surrogate", [(12, 9, 1, 2, True), (20, 14, 2, 3, False), (18, 16, 1, 4, True),
+                                                 (17, 24, 0, 4, True), (33, 40, 3, 5, True)])
+def test_libpdst_strip_step(nx, ny, k, P, surrogate):
+    """The data plane inside libpdst (pdst_strips_step_local: halo pack /
+    unpack kernels, owned-row fused Vanka update with the increment row sent
+    up, reverse-add): owned entries of y = J x and of 1 / 2 Vanka steps equal
+    the single domain (1e-13), ghost entries garbage on input."""
+    import torch
+
+    from test_gpu_operator import _sized_case
+
+    from paper_2603_28706_b200.operators import SlabJacobian
+    from paper_2603_28706_b200.partition import strip_step
+    from paper_2603_28706_b200.smoother import VankaLevel, vanka_smooth
+
+    case, fx, syn = _sized_case(nx, ny, k, "exn")
+    ctx = product_ctx(case, fx)
+    var = product_variant(case)
+    jac = SlabJacobian(ctx, syn.U, var)
+    lvl = VankaLevel(ctx, syn.U, var, surrogate=surrogate, rep_fraction=0.5, jac=jac)
+    y_ref = jac.matvec(syn.x)
+    ref1 = vanka_smooth(lvl, syn.d0, syn.x, 1, 0.7)
+    ref2 = vanka_smooth(lvl, syn.d0, syn.x, 2, 0.7)
+    ranks, tr = _ranks(ctx, syn.U, var, P, build_patches=True, surrogate=surrogate)
+    for rk in ranks:
+        rk.strip_setup()
+    xs = [torch.as_tensor(x, device="cuda") for x in _scatter_with_garbage(ranks, syn.x, 5)]
+    ds = [torch.as_tensor(x, device="cuda") for x in _scatter_with_garbage(ranks, syn.d0, 6)]
+    rs = [torch.as_tensor(x, device="cuda") for x in _scatter_with_garbage(ranks, syn.x, 7)]
+    ys = strip_step(ranks, xs, ds, rs, 0.7)
+    n = y_ref.size
+    assert_close(_gather(ranks, [y.cpu().numpy() for y in ys], n), y_ref, TOL, "strip apply")
+    assert_close(_gather(ranks, [d.cpu().numpy() for d in ds], n), ref1, TOL, "strip vanka 1 step")
+    strip_step(ranks, xs, ds, rs, 0.7)
+    assert_close(_gather(ranks, [d.cpu().numpy() for d in ds], n), ref2, TOL, "strip vanka 2 steps")
