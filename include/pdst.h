@@ -90,6 +90,14 @@ typedef struct {
 typedef struct {
   double gamma1, gamma2, gamma_cip;
   int32_t enable_viscous, enable_convection, enable_pressure;
+  /* 0: Q2/P1disc, the reference's pair (3 pressure dofs per cell);
+     1: Taylor-Hood Q2/Q1 (continuous bilinear pressure on the (nx+1)(ny+1)
+     vertices, row-major (y, x), after the velocity block; BASELINE north_star
+     (1), no reference counterpart -- SURVEY §9.1).  Taylor-Hood handles
+     support the Jacobian apply, the residual and the mass products; the
+     patch / multigrid / strip / manufactured entry points return
+     PDST_ENOTSUP for them. */
+  int32_t pressure_space;
 } pdst_disc;
 
 typedef struct {

@@ -33,7 +33,8 @@ class Time(C.Structure):
 
 class Disc(C.Structure):
     _fields_ = [("gamma1", C.c_double), ("gamma2", C.c_double), ("gamma_cip", C.c_double),
-                ("enable_viscous", C.c_int32), ("enable_convection", C.c_int32), ("enable_pressure", C.c_int32)]
+                ("enable_viscous", C.c_int32), ("enable_convection", C.c_int32), ("enable_pressure", C.c_int32),
+                ("pressure_space", C.c_int32)]
 
 
 class Params(C.Structure):

@@ -9,7 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpdst.so")
-SOURCES = ["pdst_operator.cu", "pdst_vector.cu", "pdst_krylov.cu", "pdst_patch.cu", "pdst_timediag.cu", "pdst_coarse.cu", "pdst_mg.cu", "pdst_manufactured.cu", "pdst_strip.cu", "pdst_capi.cu"]
+SOURCES = ["pdst_operator.cu", "pdst_vector.cu", "pdst_krylov.cu", "pdst_patch.cu", "pdst_timediag.cu", "pdst_coarse.cu", "pdst_mg.cu", "pdst_manufactured.cu", "pdst_strip.cu", "pdst_th.cu", "pdst_capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -75,7 +75,7 @@ void DeviceBuffer::release() {
   cap = 0;
 }
 
-Geom make_geom(int nx, int ny, double x0, double y0, double x1, double y1, const uint8_t* dirichlet_dev) {
+Geom make_geom(int nx, int ny, double x0, double y0, double x1, double y1, const uint8_t* dirichlet_dev, int th) {
   Geom g{};
   g.nx = nx;
   g.ny = ny;
@@ -83,7 +83,8 @@ Geom make_geom(int nx, int ny, double x0, double y0, double x1, double y1, const
   g.nny = 2 * ny + 1;
   g.ncells = nx * ny;
   g.mv = 2 * g.nnx * g.nny;
-  g.nd = g.mv + 3 * g.ncells;
+  g.th = th;
+  g.nd = g.mv + (th ? (nx + 1) * (ny + 1) : 3 * g.ncells);
   g.nbf = 2 * (nx + ny);
   g.hx = (x1 - x0) / nx;
   g.hy = (y1 - y0) / ny;
@@ -250,6 +251,8 @@ int pdst_create(const pdst_mesh* mesh, const pdst_time* time, const pdst_disc* d
   if (disc->gamma1 <= 0.0 || disc->gamma2 <= 0.0)
     return fail(PDST_EINVAL, "Nitsche penalties gamma1, gamma2 must be positive");
   if (disc->gamma_cip < 0.0) return fail(PDST_EINVAL, "gamma_cip must be >= 0");
+  if (disc->pressure_space != 0 && disc->pressure_space != 1)
+    return fail(PDST_EINVAL, "pressure_space must be 0 (P1disc) or 1 (Taylor-Hood Q1)");
   if (!(params->p > 1.0 && params->p <= 2.0)) return fail(PDST_EDOMAIN, "exponent p must lie in (1, 2]");
   if (params->delta < 0.0) return fail(PDST_EDOMAIN, "delta must be >= 0");
   if (params->nu <= 0.0) return fail(PDST_EDOMAIN, "nu must be > 0");
@@ -278,7 +281,7 @@ int pdst_create(const pdst_mesh* mesh, const pdst_time* time, const pdst_disc* d
   h->extents[1] = mesh->y0;
   h->extents[2] = mesh->x1;
   h->extents[3] = mesh->y1;
-  h->g = make_geom(mesh->nx, mesh->ny, mesh->x0, mesh->y0, mesh->x1, mesh->y1, h->dirichlet);
+  h->g = make_geom(mesh->nx, mesh->ny, mesh->x0, mesh->y0, mesh->x1, mesh->y1, h->dirichlet, disc->pressure_space);
   const int k1 = time->k + 1;
   h->td.k1 = k1;
   h->tau = tau;
@@ -295,6 +298,10 @@ int pdst_create(const pdst_mesh* mesh, const pdst_time* time, const pdst_disc* d
   h->ds.viscous = disc->enable_viscous;
   h->ds.convection = disc->enable_convection;
   h->ds.pressure = disc->enable_pressure;
+  if (h->g.th) {  // Taylor-Hood: the velocity kernels run without pressure terms, pdst_th.cu adds them
+    h->th_pressure = disc->enable_pressure != 0;
+    h->ds.pressure = 0;
+  }
   h->model.p = params->p;
   h->model.delta = params->delta;
   h->model.nu = params->nu;
@@ -395,8 +402,18 @@ int pdst_linearize(pdst_handle* h, const double* U, int kind, double sigma_max, 
   return PDST_OK;
 }
 
+// Taylor-Hood: add the pressure coupling to the velocity apply (pdst_th.cu)
+static int th_add(pdst_handle* h, const double* x, double* y) {
+  double* cb = h->th_cells.ensure(th_scratch(h->g, h->td.k1));
+  if (!cb) return fail(PDST_ECUDA, "out of device memory");
+  CK(th_apply(h->g, h->td, h->th_pressure, x, y, cb, h->stream));
+  return PDST_OK;
+}
+
 static int jac_common(pdst_handle* h, const double* x, const double* r, double* y, int where) {
   if (!h || !x || !y) return fail(PDST_EINVAL, "null argument");
+  if (h->g.th && r) return fail(PDST_ENOTSUP, "defect form (the Vanka sweep) is P1disc-only; Taylor-Hood handles "
+                                              "support the apply, the residual and the mass products");
   if (where == PDST_HOST_ASYNC) {
     if (!h->linearized) return fail(PDST_ESTATE, "jacobian used before pdst_linearize");
     CK(cudaSetDevice(h->device));
@@ -411,6 +428,8 @@ static int jac_common(pdst_handle* h, const double* x, const double* r, double* 
     double* part = h->jpart.ensure_zeroed(jacobian_scratch(h->g, h->td.k1));
     if (!part) return fail(PDST_ECUDA, "out of device memory");
     CK(PDST_TIMED(h, PK_JACOBIAN, jacobian_apply(h->g, h->td, h->ds, lin_of(h), xd, rd, yd, part, h->stream)));
+    if (h->g.th)
+      if (int e = th_add(h, xd, yd)) return e;
     if (int e = async_used(h, h->as_x)) return e;
     if (r)
       if (int e = async_used(h, h->as_r)) return e;
@@ -431,6 +450,8 @@ static int jac_common(pdst_handle* h, const double* x, const double* r, double* 
   if (!part) return fail(PDST_ECUDA, "out of device memory");
   CK(PDST_TIMED(h, PK_JACOBIAN,
                 jacobian_apply(h->g, h->td, h->ds, lin_of(h), xd, rd, yd, part, h->stream)));
+  if (h->g.th)
+    if (int e = th_add(h, xd, yd)) return e;
   return finish_out(h, y, yd, n, where);
 }
 
@@ -467,6 +488,11 @@ int pdst_residual(pdst_handle* h, const double* U, const double* v_minus, const 
   CK(PDST_TIMED(h, PK_RESIDUAL,
                 slab_residual(g, h->td, h->ds, h->model, L, Ud, ad, vm, fq, h->has_ghat ? h->ghat.ptr : nullptr, Rd,
                               h->stream)));
+  if (g.th) {  // Taylor-Hood pressure terms (pdst_th.cu)
+    double* cb = h->th_cells.ensure(th_scratch(g, k1));
+    if (!cb) return fail(PDST_ECUDA, "out of device memory");
+    CK(th_residual(g, h->td, h->th_pressure, Ud, h->has_ghat ? h->ghat.ptr : nullptr, Rd, cb, h->stream));
+  }
   return finish_out(h, R, Rd, n, where);
 }
 
@@ -481,6 +507,7 @@ int pdst_mass_apply(pdst_handle* h, const double* x, double* y, int where) {
   double* yd = out_ptr(h->scratch_b, y, n, where);
   if (!yd) return fail(PDST_ECUDA, "out of device memory");
   CK(mass_apply(h->g, h->td, xd, yd, h->stream));
+  if (h->g.th) CK(th_pressure_mass(h->g, h->td, xd, yd, h->stream));
   return finish_out(h, y, yd, n, where);
 }
 
@@ -498,10 +525,17 @@ static int dot_common(pdst_handle* h, const double* a, const double* b, int64_t 
   double* part = h->partials.ensure(reduce_partials() + 1);
   if (!part) return fail(PDST_ECUDA, "out of device memory");
   double* res = where == PDST_DEVICE ? out : part + reduce_partials();
-  if (mass)
+  if (mass && h->g.th) {  // Taylor-Hood: <a, M b> with the consistent Q1 pressure mass
+    double* mb = h->scratch_d.ensure(n);
+    if (!mb) return fail(PDST_ECUDA, "out of device memory");
+    CK(mass_apply(h->g, h->td, bd, mb, h->stream));
+    CK(th_pressure_mass(h->g, h->td, bd, mb, h->stream));
+    CK(dot(ad, mb, n, part, res, h->stream));
+  } else if (mass) {
     CK(mass_dot(h->g, h->td, ad, bd, part, res, h->stream));
-  else
+  } else {
     CK(dot(ad, bd, n, part, res, h->stream));
+  }
   return finish_out(h, out, res, 1, where);
 }
 

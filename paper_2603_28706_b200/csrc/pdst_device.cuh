@@ -106,6 +106,8 @@ struct Geom {
   double hx, hy;
   double ihx, ihy;           // 1/hx, 1/hy (the reference's grad_scale, femspace.py:142-143)
   const uint8_t* dirichlet;  // nbf tags (device): 0 Neumann, 1 Dirichlet, 2 cut
+  int th;                    // pressure space: 0 the reference's P1disc (3 per cell), 1 Taylor-Hood Q1
+                             // ((nx+1)(ny+1) vertex values after the velocity block, pdst_th.cu)
 };
 
 struct TimeData {

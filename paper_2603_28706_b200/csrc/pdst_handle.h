@@ -29,7 +29,7 @@ struct DeviceBuffer {
   void release();
 };
 
-Geom make_geom(int nx, int ny, double x0, double y0, double x1, double y1, const uint8_t* dirichlet_dev);
+Geom make_geom(int nx, int ny, double x0, double y0, double x1, double y1, const uint8_t* dirichlet_dev, int th = 0);
 
 // One multigrid level.  Level L-1 is the handle's own (finest) mesh whose
 // operator is matrix free; coarser levels carry Galerkin element operators.
@@ -140,6 +140,8 @@ struct pdst_handle {
   double extents[4] = {0, 0, 1, 1};
   pdst::TimeData td{};
   pdst::Disc ds{};
+  bool th_pressure = false;      // Taylor-Hood handle: pressure coupling enabled (pdst_th.cu)
+  pdst::DeviceBuffer th_cells;   // Taylor-Hood per-cell contributions
   pdst::Model model{};
   double tau = 0.0;
   std::vector<double> nodes;

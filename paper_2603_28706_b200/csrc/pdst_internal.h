@@ -50,6 +50,14 @@ cudaError_t mass_dot(const Geom& g, const TimeData& td, const double* a, const d
                      double* result, cudaStream_t st);
 cudaError_t dot(const double* a, const double* b, size_t n, double* partials, double* result, cudaStream_t st);
 
+// Taylor-Hood Q2/Q1 pressure coupling (pdst_th.cu); cb holds th_scratch() doubles.
+size_t th_scratch(const Geom& g, int k1);
+cudaError_t th_apply(const Geom& g, const TimeData& td, bool on, const double* x, double* y, double* cb,
+                     cudaStream_t st);
+cudaError_t th_residual(const Geom& g, const TimeData& td, bool on, const double* U, const double* ghat, double* R,
+                        double* cb, cudaStream_t st);
+cudaError_t th_pressure_mass(const Geom& g, const TimeData& td, const double* x, double* y, cudaStream_t st);
+
 // Strip the velocity components of a slab state into a dense (k1, Mv) copy.
 cudaError_t copy_velocity_blocks(const Geom& g, int k1, const double* U, double* V, cudaStream_t st);
 // V = sum_mu c[mu] U_mu (velocity part of blocks of length `stride`)

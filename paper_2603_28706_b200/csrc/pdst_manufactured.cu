@@ -237,6 +237,7 @@ using namespace pdst;
 extern "C" {
 
 int pdst_manufactured_forcing(pdst_handle* h, double t_start, double* fqp, int where) {
+  if (h && h->g.th) return set_error(PDST_ENOTSUP, "the manufactured forcing is Q2/P1disc-only (Taylor-Hood handles: apply, residual, mass)");
   if (!h || !fqp) return set_error(PDST_EINVAL, "null argument");
   if (int e = check_where(where)) return e;
   if (cudaSetDevice(h->device) != cudaSuccess) return set_error(PDST_ECUDA, "cudaSetDevice failed");
@@ -256,6 +257,7 @@ int pdst_manufactured_forcing(pdst_handle* h, double t_start, double* fqp, int w
 
 int pdst_error_norms(pdst_handle* h, const double* U, double t0, double t1, int spatial_points, int temporal_points,
                      double* sq2, int where) {
+  if (h && h->g.th) return set_error(PDST_ENOTSUP, "the error norms is Q2/P1disc-only (Taylor-Hood handles: apply, residual, mass)");
   if (!h || !U || !sq2) return set_error(PDST_EINVAL, "null argument");
   if (int e = check_where(where)) return e;
   if (spatial_points < 1 || spatial_points > MFQ || temporal_points < 1 || temporal_points > MFQ)

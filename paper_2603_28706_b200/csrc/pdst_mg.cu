@@ -109,6 +109,7 @@ int check_level(pdst_handle* h, int level) {
 extern "C" {
 
 int pdst_cell_maps(pdst_handle* h, int64_t* cell_nodes, int64_t* patch_ids) {
+  if (h && h->g.th) return set_error(PDST_ENOTSUP, "pdst_cell_maps is Q2/P1disc-only (Taylor-Hood handles: apply, residual, mass)");
   if (!h || !cell_nodes || !patch_ids) return set_error(PDST_EINVAL, "null argument");
   CK(cudaSetDevice(h->device));
   const Geom& g = h->g;
@@ -129,12 +130,14 @@ int pdst_cell_maps(pdst_handle* h, int64_t* cell_nodes, int64_t* patch_ids) {
 static int build_hierarchy(pdst_handle* h, int min_cells, int depth, int* num_levels);
 
 int pdst_hierarchy(pdst_handle* h, int min_cells, int* num_levels) {
+  if (h && h->g.th) return set_error(PDST_ENOTSUP, "the multigrid hierarchy is Q2/P1disc-only (Taylor-Hood handles: apply, residual, mass)");
   return build_hierarchy(h, min_cells, 0, num_levels);
 }
 
 // A hierarchy of exactly `depth` levels regardless of min_cells: a rank's
 // strip of a partitioned mesh coarsens as often as the global mesh does.
 int pdst_hierarchy_depth(pdst_handle* h, int depth, int* num_levels) {
+  if (h && h->g.th) return set_error(PDST_ENOTSUP, "the multigrid hierarchy is Q2/P1disc-only (Taylor-Hood handles: apply, residual, mass)");
   if (depth < 1) return set_error(PDST_EINVAL, "depth must be >= 1");
   return build_hierarchy(h, 0, depth, num_levels);
 }
@@ -248,6 +251,7 @@ static int invert_level_patches(pdst_handle* h, int l, int* badi, int* bad_level
 }
 
 int pdst_patches_build(pdst_handle* h, int surrogate, double rep_fraction, int* bad_level, int64_t* bad_patch) {
+  if (h && h->g.th) return set_error(PDST_ENOTSUP, "the Vanka patches is Q2/P1disc-only (Taylor-Hood handles: apply, residual, mass)");
   if (!h) return set_error(PDST_EINVAL, "null handle");
   if (!h->linearized) return set_error(PDST_ESTATE, "patches built before pdst_linearize");
   CK(cudaSetDevice(h->device));
@@ -569,6 +573,7 @@ static int vanka_level(pdst_handle* h, int l, double* d, const double* r, int st
 }
 
 int pdst_vanka(pdst_handle* h, int level, double* d, const double* r, int steps, double omega, int where) {
+  if (h && h->g.th) return set_error(PDST_ENOTSUP, "the Vanka sweep is Q2/P1disc-only (Taylor-Hood handles: apply, residual, mass)");
   if (!h || !d || !r) return set_error(PDST_EINVAL, "null argument");
   if (where == PDST_HOST_ASYNC) {
     if (int e = check_level(h, level)) return e;
@@ -605,6 +610,7 @@ int pdst_vanka(pdst_handle* h, int level, double* d, const double* r, int steps,
 
 int pdst_vanka_increment(pdst_handle* h, int level, const double* defect, double* inc, int row_lo, int row_hi,
                          double omega, int where) {
+  if (h && h->g.th) return set_error(PDST_ENOTSUP, "the Vanka sweep is Q2/P1disc-only (Taylor-Hood handles: apply, residual, mass)");
   if (!h || !defect || !inc) return set_error(PDST_EINVAL, "null argument");
   if (int e = check_where(where)) return e;
   if (int e = check_level(h, level)) return e;
@@ -832,6 +838,7 @@ int pdst_set_coarse_solver(pdst_handle* h, int kind, int sweeps, double omega, i
 }
 
 int pdst_vcycle(pdst_handle* h, const double* r, double* z, int pre, int post, double omega, int where) {
+  if (h && h->g.th) return set_error(PDST_ENOTSUP, "the V-cycle is Q2/P1disc-only (Taylor-Hood handles: apply, residual, mass)");
   if (!h || !r || !z) return set_error(PDST_EINVAL, "null argument");
   if (int e = check_where(where)) return e;
   if (!h->patches_valid || !h->coarse_valid)

@@ -1126,7 +1126,7 @@ __global__ void __launch_bounds__(128, 8) k_side_products(Geom g, TimeData td, c
     if (lane < 18) {
       const int n = lane >> 1;
       xj = __ldg(xm + 2 * ((size_t)(2 * cj + n / 3) * g.nnx + 2 * ci + n % 3) + (lane & 1));
-    } else if (lane < 21) {
+    } else if (lane < 21 && !g.th) {  // (Taylor-Hood: no P1disc pressure; pdst_th.cu)
       xj = __ldg(xm + g.mv + 3 * ((size_t)cj * g.nx + ci) + (lane - 18));
     }
     const int r = lane < 21 ? lane : 20;
@@ -1253,7 +1253,7 @@ __global__ void __launch_bounds__(128, 16) k_jac_post(Geom g, TimeData td, const
     return;
   }
   t -= nv + nh;
-  if (t < ncb) {
+  if (t < ncb && !g.th) {
     int ci, cj;
     bcell_of(g, t, ci, cj);
     const size_t o = base + g.mv + 3 * ((size_t)cj * g.nx + ci);
@@ -1337,11 +1337,13 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
       for (int b = 0; b < 3; ++b) ra[a][b][0] = ra[a][b][1] = 0.0;
     const RegAcc racc{ra};
     if (valid) {
-      double P[3];
-      const double* xp = x + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
-      P[0] = __ldg(xp);
-      P[1] = __ldg(xp + 1);
-      P[2] = __ldg(xp + 2);
+      double P[3] = {0.0, 0.0, 0.0};
+      if (!g.th) {  // Taylor-Hood: the pressure coupling is pdst_th.cu's
+        const double* xp = x + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
+        P[0] = __ldg(xp);
+        P[1] = __ldg(xp + 1);
+        P[2] = __ldg(xp + 2);
+      }
       // tau w_mu J_mu x_mu: volume, boundary sides, CIP faces (weights carry tau w_mu)
       jac_volume_cached<HG>(T, ds, cp, XM, r0, c0, P, slot, accp, g.hx * g.hy * tw);
       TR(2 + 5 * mu);
@@ -1354,8 +1356,9 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
           rv[n][0] = __ldg(rhs + o);
           rv[n][1] = __ldg(rhs + o + 1);
         }
+        if (!g.th)
 #pragma unroll
-        for (int j = 0; j < 3; ++j) rp[j] = __ldg(rhs + (size_t)mu * g.nd + g.mv + 3 * (size_t)c + j);
+          for (int j = 0; j < 3; ++j) rp[j] = __ldg(rhs + (size_t)mu * g.nd + g.mv + 3 * (size_t)c + j);
       }
       if (cip) {
         // face matrices: own right / top, the left / bottom neighbours' right / top
@@ -1424,8 +1427,9 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
 #pragma unroll
       // boundary cells: raw sum, finished (side terms, rhs) by k_jac_post
       const bool bcell = ci == 0 || cj == 0 || ci == g.nx - 1 || cj == g.ny - 1;
+      if (!g.th)
 #pragma unroll
-      for (int j = 0; j < 3; ++j) out[o + j] = (rhs && !bcell) ? rp[j] - accp[j] : accp[j];
+        for (int j = 0; j < 3; ++j) out[o + j] = (rhs && !bcell) ? rp[j] - accp[j] : accp[j];
     }
     TR(4 + 5 * mu);
     __syncthreads();
@@ -1564,11 +1568,13 @@ __global__ void __launch_bounds__(NT) k_residual(Geom g, TimeData td, Disc ds, M
       for (int b = 0; b < 3; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
     double accp[3] = {0.0, 0.0, 0.0};
     if (valid) {
-      double PI[3];
-      const double* pp = U + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
-      PI[0] = __ldg(pp);
-      PI[1] = __ldg(pp + 1);
-      PI[2] = __ldg(pp + 2);
+      double PI[3] = {0.0, 0.0, 0.0};
+      if (!g.th) {  // Taylor-Hood: the pressure terms are pdst_th.cu's
+        const double* pp = U + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
+        PI[0] = __ldg(pp);
+        PI[1] = __ldg(pp + 1);
+        PI[2] = __ldg(pp + 2);
+      }
 #pragma unroll 1
       for (int qx = 0; qx < 4; ++qx) {
         double sB[3][2], sG[3][2];
@@ -1647,11 +1653,13 @@ __global__ void __launch_bounds__(NT) k_residual(Geom g, TimeData td, Disc ds, M
         slot[(2 * (3 * a + b) + 1) * NT] = acc[a][b][1];
       }
     if (valid && (ci == 0 || cj == 0 || ci == g.nx - 1 || cj == g.ny - 1)) {
-      double PI[3];
-      const double* pp = U + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
-      PI[0] = __ldg(pp);
-      PI[1] = __ldg(pp + 1);
-      PI[2] = __ldg(pp + 2);
+      double PI[3] = {0.0, 0.0, 0.0};
+      if (!g.th) {  // Taylor-Hood: the pressure terms are pdst_th.cu's
+        const double* pp = U + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
+        PI[0] = __ldg(pp);
+        PI[1] = __ldg(pp + 1);
+        PI[2] = __ldg(pp + 2);
+      }
       double gn[18];
 #pragma unroll
       for (int a = 0; a < 9; ++a) {
@@ -1685,7 +1693,7 @@ __global__ void __launch_bounds__(NT) k_residual(Geom g, TimeData td, Disc ds, M
           acc[a][b][1] *= tw;
         }
       add_mass<K1>(UP, &VM, td.m_t[mu], td.K_t + mu * K1, r0, c0, -W, RegAcc{acc});
-      if (owned) {
+      if (owned && !g.th) {
         const size_t o = (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
 #pragma unroll
         for (int j = 0; j < 3; ++j) out[o + j] = tw * accp[j];

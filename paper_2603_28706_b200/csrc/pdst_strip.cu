@@ -329,6 +329,7 @@ extern "C" {
 
 int pdst_strip(pdst_handle* h, int rank, int nranks, int ny_global, int a, int b, int c_lo, int c_hi, int lower_c_hi,
                int upper_c_lo) {
+  if (h && h->g.th) return set_error(PDST_ENOTSUP, "the strip partition is Q2/P1disc-only (Taylor-Hood handles: apply, residual, mass)");
   if (!h) return set_error(PDST_EINVAL, "null handle");
   if (nranks < 1 || rank < 0 || rank >= nranks) return set_error(PDST_EINVAL, "bad rank %d of %d", rank, nranks);
   if (!(0 <= c_lo && c_lo <= a && a < b && b <= c_hi && c_hi <= ny_global))

@@ -53,7 +53,7 @@ __global__ void k_mass_apply(Geom g, TimeData td, const double* __restrict__ x, 
     const double h = g.hx * g.hy;
     ym[2 * tid] = tw * (h * s0);
     ym[2 * tid + 1] = tw * (h * s1);
-  } else if (tid < nn + (size_t)g.ncells) {
+  } else if (tid < nn + (size_t)g.ncells && !g.th) {  // Taylor-Hood pressure mass: pdst_th.cu
     const size_t c = tid - nn;
     const double h = g.hx * g.hy;
     const size_t o = g.mv + 3 * c;
@@ -105,7 +105,7 @@ __global__ void k_mass_dot_partial(Geom g, TimeData td, const double* __restrict
         }
     }
     const size_t o = g.mv + 3 * (size_t)c;
-    const double pp = am[o] * bm[o] + (1.0 / 12.0) * (am[o + 1] * bm[o + 1] + am[o + 2] * bm[o + 2]);
+    const double pp = g.th ? 0.0 : am[o] * bm[o] + (1.0 / 12.0) * (am[o + 1] * bm[o + 1] + am[o + 2] * bm[o + 2]);
     acc += td.tau_w[mu] * h * (cell + pp);
   }
   const double s = block_sum(acc, sh);

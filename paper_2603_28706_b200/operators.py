@@ -96,7 +96,7 @@ class SlabDevice:
         t = L.Time(k, L.dptr(self._nodes), L.dptr(self._weights), L.dptr(self._K), L.dptr(self._m))
         cfg = ctx.config
         d = L.Disc(cfg.gamma1, cfg.gamma2, cfg.gamma_cip, int(cfg.enable_viscous), int(cfg.enable_convection),
-                   int(cfg.enable_pressure))
+                   int(cfg.enable_pressure), 1 if getattr(disc, "pressure", "p1disc") == "q1" else 0)
         pr = ctx.params
         p = L.Params(pr.p, pr.delta, pr.nu, pr.nu_inf)
         h = C.c_void_p()

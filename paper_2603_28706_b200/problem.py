@@ -121,11 +121,22 @@ def dirichlet_flags(mesh) -> np.ndarray:
     return np.array([str(t) == DIRICHLET for t in tags], dtype=np.uint8)
 
 
+PRESSURE_SPACES = ("p1disc", "q1")
+
+
 @dataclass
 class Discretization:
-    """Q2/P1disc sizes of a mesh (femspace.py:109-160)."""
+    """Q2 velocity with the reference's P1disc pressure (femspace.py:109-160),
+    or -- pressure="q1" -- the Taylor-Hood pair Q2/Q1 (continuous bilinear
+    pressure on the (nx+1)(ny+1) vertices, row-major (y, x); BASELINE
+    north_star (1), no reference counterpart)."""
 
     mesh: QuadMesh
+    pressure: str = "p1disc"
+
+    def __post_init__(self):
+        if self.pressure not in PRESSURE_SPACES:
+            raise ValueError(f"unknown pressure space {self.pressure!r} (one of {PRESSURE_SPACES})")
 
     @property
     def n_velocity(self):
@@ -133,6 +144,8 @@ class Discretization:
 
     @property
     def n_pressure(self):
+        if self.pressure == "q1":
+            return (self.mesh.nx + 1) * (self.mesh.ny + 1)
         return 3 * self.mesh.ncells
 
     @property
@@ -198,10 +211,12 @@ class SlabContext:
 
 
 def make_context(nx, ny, k, params: ModelParams, tau, *, extents=(0.0, 0.0, 1.0, 1.0), neumann_sides=(),
-                 config: DiscretizationConfig | None = None, f=None, t_start=0.0, v_minus=None) -> SlabContext:
-    """Convenience constructor for a slab context on a uniform mesh."""
+                 config: DiscretizationConfig | None = None, f=None, t_start=0.0, v_minus=None,
+                 pressure: str = "p1disc") -> SlabContext:
+    """Convenience constructor for a slab context on a uniform mesh
+    (pressure="q1": the Taylor-Hood pair)."""
     mesh = tag_sides(QuadMesh(nx, ny, *extents), neumann_sides)
-    disc = Discretization(mesh)
+    disc = Discretization(mesh, pressure)
     basis = gauss_radau(k)
     tmat = temporal_matrices(basis)
     if v_minus is None:

@@ -12,6 +12,6 @@ mkdir -p "$ROOT/exp"
 cd "$TMP/pkg/csrc"
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -rdc=true -Xcompiler -fPIC -Xptxas -v -shared \
   -o "$ROOT/exp/libpdst_$NAME.so" pdst_operator.cu pdst_vector.cu pdst_krylov.cu pdst_patch.cu pdst_timediag.cu pdst_coarse.cu \
-  pdst_mg.cu pdst_manufactured.cu pdst_strip.cu pdst_capi.cu -lcudart -ldl > "$ROOT/exp/build_$NAME.log" 2>&1 || { tail -5 "$ROOT/exp/build_$NAME.log"; exit 1; }
+  pdst_mg.cu pdst_manufactured.cu pdst_strip.cu pdst_th.cu pdst_capi.cu -lcudart -ldl > "$ROOT/exp/build_$NAME.log" 2>&1 || { tail -5 "$ROOT/exp/build_$NAME.log"; exit 1; }
 grep -A2 "k_jacobianILi2" "$ROOT/exp/build_$NAME.log" | grep -E "spill|registers" || true
 rm -rf "$TMP"

@@ -29,16 +29,22 @@ def main():
     rk = DistributedSlab(ctx, syn.U, var, part, rank, tr, device=local, surrogate=True, rep_fraction=cfg.rep_fraction)
     rk.build_patches()
     dev = torch.device("cuda", local)
-    x = torch.as_tensor(rk.local(syn.x), device=dev)
-    r = x.clone()
-    d = torch.as_tensor(rk.local(syn.d0), device=dev)
-    (y,) = distributed_apply_and_vanka_step([rk], [x], [d], [r], cfg.omega, tr)
-    distributed_apply_and_vanka_step([rk], [x], [d], [r], cfg.omega, tr)  # a second step on the updated d
-    torch.cuda.synchronize()
-    yg, dg = np.zeros(syn.x.size), np.zeros(syn.x.size)
-    rk.owned_into(y.cpu().numpy(), yg)
-    rk.owned_into(d.cpu().numpy(), dg)
-    np.savez(f"{sys.argv[1]}{rank}.npz", y=yg, d=dg, device=torch.cuda.current_device())
+    out = {"device": torch.cuda.current_device()}
+    for tag in ("py", "lib"):  # torch.distributed exchanges, then libpdst's NCCL data plane
+        if tag == "lib":
+            rk.strip_setup()
+            rk.attach_nccl()
+        x = torch.as_tensor(rk.local(syn.x), device=dev)
+        r = x.clone()
+        d = torch.as_tensor(rk.local(syn.d0), device=dev)
+        (y,) = distributed_apply_and_vanka_step([rk], [x], [d], [r], cfg.omega, tr)
+        distributed_apply_and_vanka_step([rk], [x], [d], [r], cfg.omega, tr)  # a second step on the updated d
+        torch.cuda.synchronize()
+        yg, dg = np.zeros(syn.x.size), np.zeros(syn.x.size)
+        rk.owned_into(y.cpu().numpy(), yg)
+        rk.owned_into(d.cpu().numpy(), dg)
+        out[f"y_{tag}"], out[f"d_{tag}"] = yg, dg
+    np.savez(f"{sys.argv[1]}{rank}.npz", **out)
     dist.barrier()
     dist.destroy_process_group()
 

@@ -57,8 +57,11 @@ def test_nccl_two_ranks_match_single_domain(tmp_path):
     assert res.returncode == 0, res.stderr[-3000:]
     parts = [np.load(f"{prefix}{r}.npz") for r in range(2)]
     assert int(parts[0]["device"]) != int(parts[1]["device"])
-    y = parts[0]["y"] + parts[1]["y"]  # owned dofs are disjoint
-    d = parts[0]["d"] + parts[1]["d"]
+    cases = []
+    for tag in ("py", "lib"):  # torch.distributed exchanges; libpdst's NCCL data plane (pdst_strip_step)
+        y = parts[0][f"y_{tag}"] + parts[1][f"y_{tag}"]  # owned dofs are disjoint
+        d = parts[0][f"d_{tag}"] + parts[1][f"d_{tag}"]
+        cases.append((tag, y, d))
     cfg, ctx, syn, var = problem()
     U = torch.as_tensor(syn.U, device="cuda")
     jac = SlabJacobian(ctx, U, var)
@@ -66,9 +69,10 @@ def test_nccl_two_ranks_match_single_domain(tmp_path):
     x = torch.as_tensor(syn.x, device="cuda")
     y_ref = jac.matvec(x).cpu().numpy()
     d_ref = lvl.smooth(torch.as_tensor(syn.d0, device="cuda"), x, 2, cfg.omega).cpu().numpy()
-    for a, b, what in ((y, y_ref, "apply"), (d, d_ref, "2 Vanka steps")):
-        e = np.linalg.norm(a - b) / np.linalg.norm(b)
-        assert e <= 1e-13, f"{what}: rel err {e:.3e}"
+    for tag, y, d in cases:
+        for a, b, what in ((y, y_ref, "apply"), (d, d_ref, "2 Vanka steps")):
+            e = np.linalg.norm(a - b) / np.linalg.norm(b)
+            assert e <= 1e-13, f"{tag} {what}: rel err {e:.3e}"
 
 
 @needs2
