@@ -54,7 +54,7 @@ struct Plane2 {
 // A staged plane pair addressed by its offset in the kernel's dynamic shared
 // memory: the accesses stay LDS (a pointer array can be demoted to local
 // memory and turn them into generic loads).
-extern __shared__ double g_dsmem[];
+extern __shared__ __align__(16) double g_dsmem[];
 
 // Accumulators for the cell's 9-node velocity contributions: registers (the
 // element-matrix kernel, the volume phase) or the thread's shared-memory slot
@@ -81,10 +81,23 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool v
   const int sz = valid ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(sz) : "memory");
 }
+// 16-byte variant (both components of a node); source and destination 16-byte aligned.
+__device__ __forceinline__ void cp_async16(void* dst, const double* src, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(src), "r"(sz) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+// Streaming 8-byte load of read-once data (the apply's coefficient cache): not
+// allocated in L1, which holds the staged-plane misses and the few spill slots.
+__device__ __forceinline__ double ldg_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p)); }
 
 // Stage one slab block's velocity into two shared planes (zero outside the domain).
@@ -801,24 +814,41 @@ constexpr int JPLANE = JNC * JRS;
 __host__ __device__ constexpr int jpidx(int r, int c) { return r * JRS + (c & 1) * JNC2 + (c >> 1); }
 using JAcc = SmemAccN<JNT>;
 
-// A staged plane pair addressed by its offset in the kernel's dynamic shared
-// memory: the accesses stay LDS (a pointer array can be demoted to local
-// memory and turn them into generic loads).
+// A staged direction plane addressed by its offset in the kernel's dynamic
+// shared memory (the accesses stay LDS; a pointer array can be demoted to
+// local memory and turn them into generic loads).  A node holds both velocity
+// components as one double2, even / odd node columns split per row, so the
+// threads of consecutive cells read consecutive 16-byte words: one
+// conflict-free LDS.128 per node instead of two LDS.64.
 struct PlaneS {
-  int o;  // component 0 at o, component 1 at o + JPLANE
-  __device__ double at(int d, int r, int c) const { return g_dsmem[o + d * JPLANE + jpidx(r, c)]; }
+  int o;  // offset of the plane in doubles (a multiple of 2)
+  __device__ __forceinline__ double2 at2(int r, int c) const {
+    return reinterpret_cast<const double2*>(g_dsmem + o)[jpidx(r, c)];
+  }
+  __device__ __forceinline__ double at(int d, int r, int c) const {
+    const double2 v = at2(r, c);
+    return d == 0 ? v.x : v.y;
+  }
 };
 
 // Issue the asynchronous staging of one velocity block into the apply's plane
-// pair at offset o (zero outside the domain).
+// at offset o (zero outside the domain): one 16-byte copy per node when the
+// block is 16-byte aligned (even nd, or node 0), else two 8-byte copies.
 __device__ __forceinline__ void stage_jac_async(const Geom& g, const double* __restrict__ v, int o, int X0, int Y0) {
+  const bool al16 = (reinterpret_cast<size_t>(v) & 15) == 0;
+  double2* pl = reinterpret_cast<double2*>(g_dsmem + o);
   for (int idx = threadIdx.x; idx < JNC * JNC; idx += JNT) {
     const int r = idx / JNC, c = idx - r * JNC;
     const int X = X0 + c, Y = Y0 + r;
     const bool in = X >= 0 && X < g.nnx && Y >= 0 && Y < g.nny;
     const double* src = in ? v + 2 * ((size_t)Y * g.nnx + X) : v;
-    cp_async8(g_dsmem + o + jpidx(r, c), src, in);
-    cp_async8(g_dsmem + o + JPLANE + jpidx(r, c), in ? src + 1 : v, in);
+    double2* dst = pl + jpidx(r, c);
+    if (al16) {
+      cp_async16(dst, src, in);
+    } else {
+      cp_async8(&dst->x, src, in);
+      cp_async8(&dst->y, in ? src + 1 : v, in);
+    }
   }
 }
 
@@ -885,30 +915,30 @@ struct JTabs {
   double xh[4];      // s_q - 1/2
   double cJ[5];      // normal-derivative jump across a face from the 5 node
                      // lines of the two cells: L'(1) on the left, -L'(0) on the right
+  // 1-D Gauss sums of the pressure coupling (P1disc x Q2 is separable):
+  double pAx[3], pAy[3];  // sum_q w_q L_i'(s_q) / h
+  double pBx[3], pBy[3];  // sum_q w_q (s_q - 1/2) L_i'(s_q) / h
+  double pM0[3];          // sum_q w_q L_i(s_q)
+  double pM1[3];          // sum_q w_q (s_q - 1/2) L_i(s_q)
 };
 
-// Volume terms (forms.py:589-603) from the apply cache; the first writer of
-// the cell's slot.
+// Volume terms (forms.py:589-603) from the apply cache, without the pressure
+// coupling (pressure_coupling below); the first writer of the cell's slot.
 template <bool HG, class XA>
 __device__ __forceinline__ void jac_volume_cached(const JTabs& T, const Disc& ds, const double* __restrict__ cp,
-                                                  const XA& XM, int r0, int c0, const double P[3], double* slot,
-                                                  double accp[3], double WT) {
+                                                  const XA& XM, int r0, int c0, double* slot) {
 #pragma unroll 1
   for (int qx = 0; qx < 4; ++qx) {
     double xB[3][2], xG[3][2];
 #pragma unroll
-    for (int jy = 0; jy < 3; ++jy)
-#pragma unroll
-      for (int d = 0; d < 2; ++d) {
-        const double f0 = XM.at(d, r0 + jy, c0), f1 = XM.at(d, r0 + jy, c0 + 1), f2 = XM.at(d, r0 + jy, c0 + 2);
-        xB[jy][d] = T.B[qx][0] * f0 + T.B[qx][1] * f1 + T.B[qx][2] * f2;
-        xG[jy][d] = T.Gx[qx][0] * f0 + T.Gx[qx][1] * f1 + T.Gx[qx][2] * f2;
-      }
+    for (int jy = 0; jy < 3; ++jy) {
+      const double2 f0 = XM.at2(r0 + jy, c0), f1 = XM.at2(r0 + jy, c0 + 1), f2 = XM.at2(r0 + jy, c0 + 2);
+      xB[jy][0] = T.B[qx][0] * f0.x + T.B[qx][1] * f1.x + T.B[qx][2] * f2.x;
+      xB[jy][1] = T.B[qx][0] * f0.y + T.B[qx][1] * f1.y + T.B[qx][2] * f2.y;
+      xG[jy][0] = T.Gx[qx][0] * f0.x + T.Gx[qx][1] * f1.x + T.Gx[qx][2] * f2.x;
+      xG[jy][1] = T.Gx[qx][0] * f0.y + T.Gx[qx][1] * f1.y + T.Gx[qx][2] * f2.y;
+    }
     double Pa[3][2] = {{0, 0}, {0, 0}, {0, 0}}, Qa[3][2] = {{0, 0}, {0, 0}, {0, 0}};
-    const double wxT = T.w[qx] * WT;
-    // pressure along the column: dp(qy) = w_qy pA + wyh_qy pB
-    const double pA = wxT * (P[0] + P[1] * T.xh[qx]), pB = wxT * P[2];
-    double dv0 = 0.0, dv1 = 0.0;
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
       const int h = 2 * qx + hh;
@@ -917,7 +947,7 @@ __device__ __forceinline__ void jac_volume_cached(const JTabs& T, const Disc& ds
       for (int j = 0; j < 2; ++j)
 #pragma unroll
         for (int k = 0; k < 6; ++k)  // Picard: the a~ slots are zeros, not read
-          cv[j][k] = (k >= 1 && k <= 3 && !HG) ? 0.0 : __ldg(cp + (qx * 24 + k * 4 + 2 * hh + j) * JNT);
+          cv[j][k] = (k >= 1 && k <= 3 && !HG) ? 0.0 : ldg_stream(cp + (qx * 24 + k * 4 + 2 * hh + j) * JNT);
       apc_prefetch_l2(cp, h + PDST_PF_AHEAD, HG);
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
@@ -940,14 +970,6 @@ __device__ __forceinline__ void jac_volume_cached(const JTabs& T, const Disc& ds
         F00 -= 2.0 * u[0] * cv0;
         F11 -= 2.0 * u[1] * cv1;
         F01 -= u[1] * cv0 + u[0] * cv1;
-        if (ds.pressure) {
-          const double dp = T.w[qy] * pA + T.wyh[qy] * pB;
-          F00 -= dp;
-          F11 -= dp;
-          const double div = ux[0] + uy[1];
-          dv0 = fma(T.w[qy], div, dv0);
-          dv1 = fma(T.wyh[qy], div, dv1);
-        }
 #pragma unroll
         for (int jy = 0; jy < 3; ++jy) {
           Pa[jy][0] = fma(F00, T.B[qy][jy], Pa[jy][0]);
@@ -957,9 +979,6 @@ __device__ __forceinline__ void jac_volume_cached(const JTabs& T, const Disc& ds
         }
       }
     }
-    accp[0] -= wxT * dv0;
-    accp[1] -= (wxT * T.xh[qx]) * dv0;
-    accp[2] -= wxT * dv1;
     // the column's test-function sums go straight to the cell's slot (the
     // first column stores): keeps the loop at 128 registers
 #pragma unroll
@@ -983,14 +1002,17 @@ __device__ __forceinline__ void cip_face_w(const JTabs& T, int axis, const FA& F
                                            double RD[3][2]) {
   double J[3][2];
 #pragma unroll
-  for (int t = 0; t < 3; ++t)
+  for (int t = 0; t < 3; ++t) {
+    double v0 = 0.0, v1 = 0.0;
 #pragma unroll
-    for (int d = 0; d < 2; ++d) {
-      double v = 0.0;
-#pragma unroll
-      for (int m = 0; m < 5; ++m) v = fma(T.cJ[m], axis == 0 ? F.at(d, rL + t, cL + m) : F.at(d, rL + m, cL + t), v);
-      J[t][d] = v;
+    for (int m = 0; m < 5; ++m) {
+      const double2 f = axis == 0 ? F.at2(rL + t, cL + m) : F.at2(rL + m, cL + t);
+      v0 = fma(T.cJ[m], f.x, v0);
+      v1 = fma(T.cJ[m], f.y, v1);
     }
+    J[t][0] = v0;
+    J[t][1] = v1;
+  }
 #pragma unroll
   for (int d = 0; d < 2; ++d) {
     RD[0][d] = W[0] * J[0][d] + W[1] * J[1][d] + W[2] * J[2][d];
@@ -1325,9 +1347,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
     double* slot = sacc + threadIdx.x;
     const JAcc acc{slot};
     const PlaneS XM{mu * 2 * JPLANE};
-    double rv[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};  // rhs of the own 2x2 nodes (defect mode)
     double accp[3] = {0.0, 0.0, 0.0};
-    double rp[3] = {0, 0, 0};
     // CIP, temporal mass and boundary sides accumulate in registers (the
     // volume's registers are free by then) and reach the slot in one pass
     double ra[3][3][2];
@@ -1337,16 +1357,25 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
       for (int b = 0; b < 3; ++b) ra[a][b][0] = ra[a][b][1] = 0.0;
     const RegAcc racc{ra};
     if (valid) {
-      double P[3] = {0.0, 0.0, 0.0};
-      if (!g.th) {  // Taylor-Hood: the pressure coupling is pdst_th.cu's
-        const double* xp = x + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
-        P[0] = __ldg(xp);
-        P[1] = __ldg(xp + 1);
-        P[2] = __ldg(xp + 2);
-      }
       // tau w_mu J_mu x_mu: volume, boundary sides, CIP faces (weights carry tau w_mu)
-      jac_volume_cached<HG>(T, ds, cp, XM, r0, c0, P, slot, accp, g.hx * g.hy * tw);
+      jac_volume_cached<HG>(T, ds, cp, XM, r0, c0, slot);
       TR(2 + 5 * mu);
+    }
+    // The cell's indices are recomputed from the (laundered) thread and block
+    // ids here, so that nothing but the stream pointer, the slot and the staged
+    // origin stays live across the volume phase (ptxas spilled the tile-edge
+    // flags to local memory otherwise and the assembly stalled on the reload).
+    int tid_ = threadIdx.x, bx_ = blockIdx.x, by_ = blockIdx.y;
+    asm volatile("" : "+r"(tid_), "+r"(bx_), "+r"(by_));
+    const int tx = tid_ % JT, ty = tid_ / JT;
+    const int i0 = bx_ * JT, j0 = by_ * JT;
+    const int ci = i0 + tx, cj = j0 + ty;
+    const int c = cj * g.nx + ci;
+    const size_t tile = (size_t)by_ * jac_tiles_x(g) + bx_;
+    const bool lastx = tx == min(JT, g.nx - i0) - 1, lasty = ty == min(JT, g.ny - j0) - 1;
+    double rv[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};  // rhs of the own 2x2 nodes (defect mode)
+    double rp[3] = {0, 0, 0};
+    if (valid) {
       // defect mode: the right-hand side of this cell's own nodes (lower-left
       // 2x2) and pressures, loaded now for the assembly
       if (rhs) {
@@ -1391,16 +1420,17 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
         for (int jj = 0; jj < 3; ++jj) {  // source row jy'
           double xt[3][2];
 #pragma unroll
-          for (int i = 0; i < 3; ++i)
+          for (int i = 0; i < 3; ++i) {
+            double v0 = 0.0, v1 = 0.0;
 #pragma unroll
-            for (int d = 0; d < 2; ++d) {
-              double v = 0.0;
-#pragma unroll
-              for (int nu = 0; nu < K1; ++nu) {
-                v = fma(Krow[nu], XP[nu].at(d, r0 + jj, c0 + i), v);
-              }
-              xt[i][d] = v;
+            for (int nu = 0; nu < K1; ++nu) {
+              const double2 f = XP[nu].at2(r0 + jj, c0 + i);
+              v0 = fma(Krow[nu], f.x, v0);
+              v1 = fma(Krow[nu], f.y, v1);
             }
+            xt[i][0] = v0;
+            xt[i][1] = v1;
+          }
           double T1[3][2];
 #pragma unroll
           for (int i = 0; i < 3; ++i)
@@ -1417,6 +1447,41 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
           }
         }
       }
+      // Pressure coupling (forms.py:589-603, the -p div w and -q div u terms):
+      // P1disc x Q2 on a rectangle is separable, so the 16-point sums collapse
+      // to 1-D Gauss sums (JTabs pA/pB/pM) and stay out of the volume loop.
+      if (ds.pressure && !g.th) {  // Taylor-Hood: the pressure coupling is pdst_th.cu's
+        const double WT = g.hx * g.hy * tw;
+        const double* xp = x + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
+        const double P0 = WT * __ldg(xp), P1 = WT * __ldg(xp + 1), P2 = WT * __ldg(xp + 2);
+        // -q div u: rows of x_mu against the 1-D sums
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll
+        for (int jy = 0; jy < 3; ++jy) {
+          const double2 f0 = XM.at2(r0 + jy, c0), f1 = XM.at2(r0 + jy, c0 + 1), f2 = XM.at2(r0 + jy, c0 + 2);
+          const double sA = T.pAx[0] * f0.x + T.pAx[1] * f1.x + T.pAx[2] * f2.x;   // sum_i A_i x0
+          const double sB = T.pBx[0] * f0.x + T.pBx[1] * f1.x + T.pBx[2] * f2.x;   // sum_i Bx_i x0
+          const double s0 = T.pM0[0] * f0.y + T.pM0[1] * f1.y + T.pM0[2] * f2.y;   // sum_i M0_i x1
+          const double s1 = T.pM1[0] * f0.y + T.pM1[1] * f1.y + T.pM1[2] * f2.y;   // sum_i M1_i x1
+          a0 += T.pM0[jy] * sA + T.pAy[jy] * s0;
+          a1 += T.pM0[jy] * sB + T.pAy[jy] * s1;
+          a2 += T.pM1[jy] * sA + T.pBy[jy] * s0;
+        }
+        accp[0] = -WT * a0;
+        accp[1] = -WT * a1;
+        accp[2] = -WT * a2;
+        // -p div w
+#pragma unroll
+        for (int jy = 0; jy < 3; ++jy) {
+          const double dy = P0 * T.pAy[jy] + P2 * T.pBy[jy], ey = P1 * T.pAy[jy];
+#pragma unroll
+          for (int ix = 0; ix < 3; ++ix) {
+            const double cA = P0 * T.pAx[ix] + P1 * T.pBx[ix], cB = P2 * T.pAx[ix];
+            ra[jy][ix][0] -= cA * T.pM0[jy] + cB * T.pM1[jy];
+            ra[jy][ix][1] -= T.pM0[ix] * dy + T.pM1[ix] * ey;
+          }
+        }
+      }
 #pragma unroll
       for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -1424,7 +1489,6 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
 #pragma unroll
           for (int d = 0; d < 2; ++d) acc.add(a, b, d, ra[a][b][d]);
       const size_t o = (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
-#pragma unroll
       // boundary cells: raw sum, finished (side terms, rhs) by k_jac_post
       const bool bcell = ci == 0 || cj == 0 || ci == g.nx - 1 || cj == g.ny - 1;
       if (!g.th)
@@ -2047,6 +2111,21 @@ cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const 
       T.w[q] = tab.w[q];
       T.xh[q] = tab.s[q] - 0.5;
       T.wyh[q] = tab.w[q] * (tab.s[q] - 0.5);
+    }
+    for (int i = 0; i < 3; ++i) {
+      double a = 0.0, b = 0.0, m0 = 0.0, m1 = 0.0;
+      for (int q = 0; q < 4; ++q) {
+        a += tab.w[q] * tab.G[q][i];
+        b += tab.w[q] * (tab.s[q] - 0.5) * tab.G[q][i];
+        m0 += tab.w[q] * tab.B[q][i];
+        m1 += tab.w[q] * (tab.s[q] - 0.5) * tab.B[q][i];
+      }
+      T.pAx[i] = a * g.ihx;
+      T.pAy[i] = a * g.ihy;
+      T.pBx[i] = b * g.ihx;
+      T.pBy[i] = b * g.ihy;
+      T.pM0[i] = m0;
+      T.pM1[i] = m1;
     }
     T.cJ[0] = tab.dE[1][0];
     T.cJ[1] = tab.dE[1][1];

@@ -32,3 +32,15 @@ for i, nm in enumerate(names):
     print(f"{i:2d} {nm:18s} {c.min():7.1f} {np.median(c):7.1f} {c.max():7.1f}")
 d = (t[:, len(names) - 1] - t[:, 0]) / 1e3
 print("CTA duration min/median/max", d.min(), np.median(d), d.max())
+
+# per-role / per-SM-load breakdown (role = (tile // 148) & 1; SM id in column 15)
+sm = buf[:n, 15].astype(np.int64)
+cnt = np.bincount(sm, minlength=160)
+load = cnt[sm]
+role = (np.arange(n) // 148) & 1
+same = sum(1 for s_ in np.unique(sm) if cnt[s_] == 2 and len(set(role[sm == s_])) == 1)
+print("SMs used", (cnt > 0).sum(), "with 2 CTAs", (cnt == 2).sum(), "of which same-role pairs", same, "max CTAs/SM", cnt.max())
+for key, sel in (("role0", role == 0), ("role1", role == 1), ("lone", load == 1), ("paired", load == 2)):
+    if sel.sum() == 0: continue
+    c = (t[sel][:, :len(names)] - t0) / 1e3
+    print(key, sel.sum(), " ".join(f"{np.median(c[:, i]):6.1f}" for i in range(len(names))))
