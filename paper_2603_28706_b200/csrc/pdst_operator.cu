@@ -794,9 +794,37 @@ __device__ unsigned long long g_trace[8192][16];
       g_trace[blockIdx.y * gridDim.x + blockIdx.x][i] = t_;                                            \
     }                                                                                                  \
   } while (0)
+// kernel-level marks: even slots keep the minimum, odd slots the maximum
+__device__ unsigned long long g_ktrace[8] = {~0ull, 0ull, ~0ull, 0ull, ~0ull, 0ull, ~0ull, 0ull};
+#define KTR(i)                                                     \
+  do {                                                             \
+    if (threadIdx.x == 0) {                                        \
+      unsigned long long t_;                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));       \
+      if ((i) & 1)                                                 \
+        atomicMax(&g_ktrace[i], t_);                               \
+      else                                                         \
+        atomicMin(&g_ktrace[i], t_);                               \
+    }                                                              \
+  } while (0)
+#define KTRT(i)                                                  \
+  do {                                                           \
+    unsigned long long t_;                                       \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));       \
+    if ((i) & 1)                                                 \
+      atomicMax(&g_ktrace[i], t_);                               \
+    else                                                         \
+      atomicMin(&g_ktrace[i], t_);                               \
+  } while (0)
 #else
 #define TR(i) \
   do {        \
+  } while (0)
+#define KTRT(i) \
+  do {          \
+  } while (0)
+#define KTR(i) \
+  do {         \
   } while (0)
 #endif
 #ifndef PDST_JT
@@ -905,6 +933,32 @@ __device__ __forceinline__ void apc_prefetch_l2(const double* __restrict__ cp, i
   }
 }
 
+// Completion counters of the tile pass, one per Radau node: a tile adds 1
+// once all its stores of that node (interior sums, tile-line partials, raw
+// strip sums) are done — after a CTA barrier, by one thread, behind a
+// device-scope fence — and the epilogue (k_jac_post) of that node polls the
+// counter instead of waiting for the whole grid, so node mu's epilogue runs
+// under the tile pass of node mu + 1.  The counters only grow: apply number e
+// of a handle waits for e * tiles.  No deadlock: the epilogue is launched
+// (PDL) only after every tile CTA has started.
+__device__ __forceinline__ void tile_signal(unsigned long long* sig) {
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(sig, 1ull);
+  }
+}
+__device__ __forceinline__ void tile_wait(const unsigned long long* sig, unsigned long long target) {
+  if (threadIdx.x == 0) {
+    unsigned long long v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(sig) : "memory");
+      if (v >= target) break;
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
 // 1-D tables of the apply with the mesh scales folded in (kernel parameter).
 struct JTabs {
   double B[4][3];    // L_i(s_q)
@@ -923,10 +977,13 @@ struct JTabs {
 };
 
 // Volume terms (forms.py:589-603) from the apply cache, without the pressure
-// coupling (pressure_coupling below); the first writer of the cell's slot.
+// coupling (evaluated with the temporal mass); the first writer of the cell's
+// slot.  Called by every thread of the CTA (cells outside the mesh stream
+// zeros into their own slot) because of the barrier inside.
 template <bool HG, class XA>
 __device__ __forceinline__ void jac_volume_cached(const JTabs& T, const Disc& ds, const double* __restrict__ cp,
-                                                  const XA& XM, int r0, int c0, double* slot) {
+                                                  const XA& XM, int r0, int c0, double* slot, bool sync_first,
+                                                  unsigned long long* sig) {
 #pragma unroll 1
   for (int qx = 0; qx < 4; ++qx) {
     double xB[3][2], xG[3][2];
@@ -980,7 +1037,13 @@ __device__ __forceinline__ void jac_volume_cached(const JTabs& T, const Disc& ds
       }
     }
     // the column's test-function sums go straight to the cell's slot (the
-    // first column stores): keeps the loop at 128 registers
+    // first column stores): keeps the loop at 128 registers.  The slots still
+    // hold the previous Radau node's sums until every thread has assembled
+    // its nodes: that barrier sits here, behind the first column's arithmetic.
+    if (qx == 0 && sync_first) {
+      __syncthreads();
+      tile_signal(sig);  // the previous node's sums of this tile are all stored
+    }
 #pragma unroll
     for (int jy = 0; jy < 3; ++jy)
 #pragma unroll
@@ -1132,10 +1195,12 @@ __device__ inline int bcell_index(const Geom& g, int ci, int cj) {
 // (k_boundary_matrices, face-contiguous [mu][bf][21][21]).  One warp per
 // boundary cell, lane r < 21 computes row r; x_loc is loaded once and
 // broadcast by shuffles.  Depends only on x: launched with PDL behind the tile
-// pass, its short-lived CTAs run on the SMs the tile pass leaves half empty;
-// the grid completes after the tile pass, so k_jac_post (launched behind this grid) sees both.
+// pass (whose CTAs trigger it after their own wait, so x is complete), its
+// short-lived CTAs run on the SMs the tile pass leaves half empty and count
+// themselves done in `sdone` (tile_signal) for the epilogue.
 __global__ void __launch_bounds__(128, 8) k_side_products(Geom g, TimeData td, const double* __restrict__ bmat,
-                                                       const double* __restrict__ x, double* __restrict__ sp) {
+                                                       const double* __restrict__ x, double* __restrict__ sp,
+                                                       unsigned long long* __restrict__ sdone) {
   pdl_trigger();
   const int mu = blockIdx.y, lane = threadIdx.x & 31;
   const size_t ncb = n_bcells(g);
@@ -1166,9 +1231,9 @@ __global__ void __launch_bounds__(128, 8) k_side_products(Geom g, TimeData td, c
     }
     if (lane < 21) sp[((size_t)mu * 21 + lane) * ncb + cb] = acc;
   }
-  // one CTA waits for the tile pass, so this grid completes after it (the
-  // others retire at once and free their SM slots for more of this grid)
-  if (blockIdx.x == 0 && blockIdx.y == 0) pdl_wait();
+  __syncthreads();
+  tile_signal(sdone);
+  KTR(3);
 }
 
 // Side terms at velocity node (X, Y): sum of the side products of the
@@ -1214,17 +1279,23 @@ __device__ void tile_partials(const Geom& g, const double* part, int mu, int X, 
     for (int a = 0; a < nbx; ++a) {
       const int lx = X - 2 * JT * bxs[a], ly = Y - 2 * JT * bys[b];
       const double* pp = part + (((size_t)mu * ntiles + (size_t)bys[b] * ntx + bxs[a]) * JPER + perim(lx, ly)) * 2;
-      s[0] += pp[0];
-      s[1] += pp[1];
+      s[0] += __ldcg(pp);  // written by CTAs still running: not through L1
+      s[1] += __ldcg(pp + 1);
     }
 }
 
 // Work items per Radau node: strip nodes, then tile-line nodes off the
-// strips, then boundary cells (pressure).  Launched with PDL behind the tile
-// pass; every item only waits and sums.
+// strips, then boundary cells (pressure).  Launched with PDL behind the side
+// products but WITHOUT a grid-dependency wait (which would also wait for the
+// tile pass, the side products' own predecessor): the side products and the
+// tile pass's sums of node mu are awaited through their completion counters
+// (tile_wait), so node mu's items run while the tile pass works on the later
+// nodes.  Every item only sums.
 __global__ void __launch_bounds__(128, 16) k_jac_post(Geom g, TimeData td, const double* __restrict__ part,
                                                   const double* __restrict__ sp, const double* __restrict__ rhs,
-                                                  double* __restrict__ out) {
+                                                  double* __restrict__ out,
+                                                  const unsigned long long* __restrict__ done,
+                                                  unsigned long long target, unsigned long long starget) {
   pdl_trigger();  // a PDL-launched consumer (the Vanka GEMV) may start its own prologue
   const int mu = blockIdx.y;
   const StripIdx si(g);
@@ -1234,23 +1305,26 @@ __global__ void __launch_bounds__(128, 16) k_jac_post(Geom g, TimeData td, const
   const size_t ncb = n_bcells(g);
   size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t base = (size_t)mu * g.nd;
+  tile_wait(done + 4, starget);  // the side products (all threads pass a barrier)
+  tile_wait(done + mu, target);  // the tile pass's node mu
+  KTRT(6);
   if (t < ns) {
     int X, Y;
     si.node(g, t, X, Y);
     const size_t o = base + 2 * ((size_t)Y * g.nnx + X);
-    pdl_wait();
     double b[2], s[2];
     strip_sides(g, sp, mu, X, Y, b);
     if (on_tile_line(g, X, Y)) {
       tile_partials(g, part, mu, X, Y, s);
     } else {
-      s[0] = out[o];
-      s[1] = out[o + 1];
+      s[0] = __ldcg(out + o);
+      s[1] = __ldcg(out + o + 1);
     }
     s[0] += b[0];
     s[1] += b[1];
     out[o] = rhs ? rhs[o] - s[0] : s[0];
     out[o + 1] = rhs ? rhs[o + 1] - s[1] : s[1];
+    KTRT(7);
     return;
   }
   t -= ns;
@@ -1266,12 +1340,12 @@ __global__ void __launch_bounds__(128, 16) k_jac_post(Geom g, TimeData td, const
       if (X % (2 * JT) == 0 && X > 0 && X / (2 * JT) < ntx) return;  // on a vertical line
     }
     if (in_strip(g, X, Y)) return;
-    pdl_wait();
     double s[2];
     tile_partials(g, part, mu, X, Y, s);
     const size_t o = base + 2 * ((size_t)Y * g.nnx + X);
     out[o] = rhs ? rhs[o] - s[0] : s[0];
     out[o + 1] = rhs ? rhs[o + 1] - s[1] : s[1];
+    KTRT(7);
     return;
   }
   t -= nv + nh;
@@ -1279,11 +1353,11 @@ __global__ void __launch_bounds__(128, 16) k_jac_post(Geom g, TimeData td, const
     int ci, cj;
     bcell_of(g, t, ci, cj);
     const size_t o = base + g.mv + 3 * ((size_t)cj * g.nx + ci);
-    pdl_wait();
     for (int r = 0; r < 3; ++r) {
-      const double s = out[o + r] + sp[((size_t)mu * 21 + 18 + r) * ncb + t];
+      const double s = __ldcg(out + o + r) + sp[((size_t)mu * 21 + 18 + r) * ncb + t];
       out[o + r] = rhs ? rhs[o + r] - s : s;
     }
+    KTRT(7);
   }
 }
 
@@ -1300,8 +1374,9 @@ template <int K1, bool HG>
 __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, TimeData td, Disc ds, Lin L,
                                                   const double* __restrict__ x, const double* __restrict__ rhs,
                                                   double* __restrict__ out, double* __restrict__ part,
-                                                  const JTabs T) {
+                                                  unsigned long long* __restrict__ done, const JTabs T) {
   double* sacc = g_dsmem + (size_t)K1 * 2 * JPLANE;  // [18][JNT] per-cell node contributions
+  double* spres = sacc + 18 * JNT;                    // [K1][3][JNT] the cells' pressure dofs
   // [K1][2][JPLANE] direction x_nu, all Radau nodes (one-cell ring), in front
   const int bx = blockIdx.x, by = blockIdx.y;
   const int i0 = bx * JT, j0 = by * JT;
@@ -1324,6 +1399,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
   const double* cbase = L.apc + tile * K1 * APC_SLOTS * JNT + threadIdx.x;
 
   TR(0);
+  KTR(0);
   // HG == false (Picard, or no viscous term): the a~ slots are zeros and never read
   if (valid)  // the coefficient stream does not depend on the predecessor
     for (int h = 0; h < PDST_PF_AHEAD; ++h) apc_prefetch_l2(cbase, h, HG);
@@ -1337,6 +1413,13 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
   stage_jac_async(g, x, 0, X0, Y0);
   cp_async_commit();
   for (int nu = 1; nu < K1; ++nu) stage_jac_async(g, x + (size_t)nu * g.nd, nu * 2 * JPLANE, X0, Y0);
+  // the cell's pressure dofs of every node (read by the own thread with the temporal mass)
+  if (valid && ds.pressure && !g.th)
+#pragma unroll
+    for (int nu = 0; nu < K1; ++nu)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        cp_async8(spres + (size_t)(nu * 3 + j) * JNT + threadIdx.x, x + (size_t)nu * g.nd + g.mv + 3 * (size_t)c + j, true);
   cp_async_commit();
   cp_async_wait_group<1>();
   __syncthreads();
@@ -1356,11 +1439,9 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
 #pragma unroll
       for (int b = 0; b < 3; ++b) ra[a][b][0] = ra[a][b][1] = 0.0;
     const RegAcc racc{ra};
-    if (valid) {
-      // tau w_mu J_mu x_mu: volume, boundary sides, CIP faces (weights carry tau w_mu)
-      jac_volume_cached<HG>(T, ds, cp, XM, r0, c0, slot);
-      TR(2 + 5 * mu);
-    }
+    // tau w_mu J_mu x_mu: volume, boundary sides, CIP faces (weights carry tau w_mu)
+    if (K1 > 1 || valid) jac_volume_cached<HG>(T, ds, cp, XM, r0, c0, slot, K1 > 1 && mu > 0, done + (mu > 0 ? mu - 1 : 0));
+    TR(2 + 5 * mu);
     // The cell's indices are recomputed from the (laundered) thread and block
     // ids here, so that nothing but the stream pointer, the slot and the staged
     // origin stays live across the volume phase (ptxas spilled the tile-edge
@@ -1452,8 +1533,8 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
       // to 1-D Gauss sums (JTabs pA/pB/pM) and stay out of the volume loop.
       if (ds.pressure && !g.th) {  // Taylor-Hood: the pressure coupling is pdst_th.cu's
         const double WT = g.hx * g.hy * tw;
-        const double* xp = x + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
-        const double P0 = WT * __ldg(xp), P1 = WT * __ldg(xp + 1), P2 = WT * __ldg(xp + 2);
+        const double* pp = spres + (size_t)mu * 3 * JNT + threadIdx.x;  // staged with the planes
+        const double P0 = WT * pp[0], P1 = WT * pp[JNT], P2 = WT * pp[2 * JNT];
         // -q div u: rows of x_mu against the 1-D sums
         double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll
@@ -1573,9 +1654,11 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
         if (lastx) emit(lx + 2, ly + 2, 0.0 + at(sm_, 8, 0), 0.0 + at(sm_, 8, 1), -1);
       }
     }
-    __syncthreads();  // the slots are rewritten by the next node's volume pass
-    TR(6 + 5 * mu);
+    TR(6 + 5 * mu);  // (the barrier before the slots are rewritten is inside the next volume pass)
   }
+  __syncthreads();
+  tile_signal(done + K1 - 1);
+  KTR(1);
 }
 
 // ---------------------------------------------------------------------------
@@ -2076,7 +2159,7 @@ __global__ void __launch_bounds__(128) k_boundary_matrices(Geom g, Disc ds, Lin 
 
 template <int K1>
 size_t jac_smem() {
-  return ((size_t)2 * K1 * JPLANE + (size_t)JNT * 18) * sizeof(double);
+  return ((size_t)2 * K1 * JPLANE + (size_t)JNT * (18 + 3 * K1)) * sizeof(double);
 }
 template <int K1>
 size_t res_smem() {
@@ -2085,7 +2168,7 @@ size_t res_smem() {
 
 template <int K1>
 cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* x,
-                       const double* rhs, double* out, double* part, cudaStream_t st) {
+                       const double* rhs, double* out, double* part, unsigned long long* epoch, cudaStream_t st) {
   static DeviceOnce once;
   const size_t sm = jac_smem<K1>();
   const int dev = current_device();
@@ -2134,22 +2217,28 @@ cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const 
     T.cJ[4] = -tab.dE[0][2];
   }
   const size_t ncb = n_bcells(g);
-  double* sp = part + (size_t)K1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2;
+  const size_t ntiles = (size_t)jac_tiles_x(g) * jac_tiles_y(g);
+  double* sp = part + (size_t)K1 * ntiles * JPER * 2;
+  // completion counters behind the side products (zero in a fresh scratch)
+  unsigned long long* done = reinterpret_cast<unsigned long long*>(sp + (size_t)K1 * 21 * ncb);
+  const dim3 sgrid((unsigned)((ncb + 3) / 4), K1);
+  const unsigned long long target = ++(*epoch) * (unsigned long long)ntiles;
+  const unsigned long long starget = *epoch * (unsigned long long)(sgrid.x * sgrid.y);
   if (L.has_gamma && ds.viscous)
-    PDST_LAUNCH(e = launch_pdl(k_jacobian<K1, true>, grid, dim3(JNT), sm, st, g, td, ds, L, x, rhs, out, part, T));
+    PDST_LAUNCH(e = launch_pdl(k_jacobian<K1, true>, grid, dim3(JNT), sm, st, g, td, ds, L, x, rhs, out, part, done, T));
   else  // Picard (or no viscous term): the tangent's a~ slots are zeros, not streamed
-    PDST_LAUNCH(e = launch_pdl(k_jacobian<K1, false>, grid, dim3(JNT), sm, st, g, td, ds, L, x, rhs, out, part, T));
+    PDST_LAUNCH(e = launch_pdl(k_jacobian<K1, false>, grid, dim3(JNT), sm, st, g, td, ds, L, x, rhs, out, part, done, T));
   if (e != cudaSuccess) return e;
   {
     // tile pass -> side products (overlapping it, then waiting for it) -> epilogue
-    PDST_LAUNCH(e = launch_pdl(k_side_products, dim3((unsigned)((ncb + 3) / 4), K1), dim3(128), 0, st, g, td,
-                               (const double*)L.bmat, x, sp));
+    PDST_LAUNCH(e = launch_pdl(k_side_products, sgrid, dim3(128), 0, st, g, td, (const double*)L.bmat, x, sp, done + 4));
     if (e != cudaSuccess) return e;
   }
   {
     const size_t n = jac_post_items(g);
     dim3 pg((unsigned)((n + 127) / 128), K1);
-    PDST_LAUNCH(e = launch_pdl(k_jac_post, pg, dim3(128), 0, st, g, td, (const double*)part, (const double*)sp, rhs, out));
+    PDST_LAUNCH(e = launch_pdl(k_jac_post, pg, dim3(128), 0, st, g, td, (const double*)part, (const double*)sp, rhs, out,
+                               (const unsigned long long*)done, target, starget));
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
@@ -2178,24 +2267,31 @@ cudaError_t launch_res(const Geom& g, const TimeData& td, const Disc& ds, const 
 
 #ifdef PDST_TRACE
 extern "C" int pdst_debug_trace(unsigned long long* out, int n) {
-  return (int)cudaMemcpyFromSymbol(out, g_trace, (size_t)n * 16 * sizeof(unsigned long long));
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_trace, (size_t)n * 16 * sizeof(unsigned long long));
+  if (e == cudaSuccess && n >= 8192) {  // the kernel marks ride in the last row, then reset
+    e = cudaMemcpyFromSymbol(out + (size_t)8191 * 16, g_ktrace, sizeof(g_ktrace));
+    const unsigned long long init[8] = {~0ull, 0ull, ~0ull, 0ull, ~0ull, 0ull, ~0ull, 0ull};
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_ktrace, init, sizeof(init));
+  }
+  return (int)e;
 }
 #endif
 
 cudaError_t set_tables(const Tables& t) { return cudaMemcpyToSymbol(c_tab, &t, sizeof(Tables)); }
 
 size_t jacobian_scratch(const Geom& g, int k1) {
-  // tile partials, then the boundary cells' side products
-  return (size_t)k1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2 + (size_t)k1 * 21 * n_bcells(g);
+  // tile partials, then the boundary cells' side products, then the completion counters (4 nodes, side products)
+  return (size_t)k1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2 + (size_t)k1 * 21 * n_bcells(g) + 8;
 }
 
 cudaError_t jacobian_apply(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* x,
-                           const double* rhs, double* out, double* part, cudaStream_t st) {
+                           const double* rhs, double* out, double* part, unsigned long long* epoch,
+                           cudaStream_t st) {
   switch (td.k1) {
-    case 1: return launch_jac<1>(g, td, ds, L, x, rhs, out, part, st);
-    case 2: return launch_jac<2>(g, td, ds, L, x, rhs, out, part, st);
-    case 3: return launch_jac<3>(g, td, ds, L, x, rhs, out, part, st);
-    case 4: return launch_jac<4>(g, td, ds, L, x, rhs, out, part, st);
+    case 1: return launch_jac<1>(g, td, ds, L, x, rhs, out, part, epoch, st);
+    case 2: return launch_jac<2>(g, td, ds, L, x, rhs, out, part, epoch, st);
+    case 3: return launch_jac<3>(g, td, ds, L, x, rhs, out, part, epoch, st);
+    case 4: return launch_jac<4>(g, td, ds, L, x, rhs, out, part, epoch, st);
     default: return cudaErrorNotSupported;
   }
 }

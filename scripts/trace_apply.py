@@ -16,6 +16,10 @@ jac = SlabJacobian(ctx, U, pb.modified_newton(cfg.nu))
 y = torch.empty_like(x)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for _ in range(5): jac.matvec(x, out=y)
+lib = _lib.lib()
+_b0 = np.zeros((8192, 16), dtype=np.uint64)
+torch.cuda.synchronize()
+lib.pdst_debug_trace(_b0.ctypes.data_as(ctypes.c_void_p), 8192)
 flush.fill_(1)
 jac.matvec(x, out=y)
 torch.cuda.synchronize()
@@ -33,6 +37,11 @@ for i, nm in enumerate(names):
 d = (t[:, len(names) - 1] - t[:, 0]) / 1e3
 print("CTA duration min/median/max", d.min(), np.median(d), d.max())
 
+kt = buf[8191, :8].astype(np.float64)
+if kt[1] > 0:
+    k0 = kt[0]
+    print("kernel marks (us from the first tile CTA start): tile pass end %.1f | side products end %.1f, waiting CTA released %.1f | post released (first thread) %.1f, post end %.1f"
+          % ((kt[1] - k0) / 1e3, (kt[3] - k0) / 1e3, (kt[5] - k0) / 1e3, (kt[6] - k0) / 1e3, (kt[7] - k0) / 1e3))
 # per-role / per-SM-load breakdown (role = (tile // 148) & 1; SM id in column 15)
 sm = buf[:n, 15].astype(np.int64)
 cnt = np.bincount(sm, minlength=160)
