@@ -808,7 +808,7 @@ __device__ unsigned long long g_ktrace[8] = {~0ull, 0ull, ~0ull, 0ull, ~0ull, 0u
     }                                                              \
   } while (0)
 #define KTRT(i)                                                  \
-  do {                                                           \
+  if ((threadIdx.x & 31) == 0) do {                              \
     unsigned long long t_;                                       \
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));       \
     if ((i) & 1)                                                 \
@@ -1248,8 +1248,8 @@ __device__ void strip_sides(const Geom& g, const double* __restrict__ sp, int mu
       const int cb = bcell_index(g, ci, cj);
       if (cb < 0) continue;
       const int a = 3 * (Y - 2 * cj) + (X - 2 * ci);
-      b[0] += sp[((size_t)mu * 21 + 2 * a) * ncb + cb];
-      b[1] += sp[((size_t)mu * 21 + 2 * a + 1) * ncb + cb];
+      b[0] += __ldcg(sp + ((size_t)mu * 21 + 2 * a) * ncb + cb);
+      b[1] += __ldcg(sp + ((size_t)mu * 21 + 2 * a + 1) * ncb + cb);
     }
 }
 
@@ -1291,30 +1291,70 @@ __device__ void tile_partials(const Geom& g, const double* part, int mu, int X, 
 // tile pass's sums of node mu are awaited through their completion counters
 // (tile_wait), so node mu's items run while the tile pass works on the later
 // nodes.  Every item only sums.
-__global__ void __launch_bounds__(128, 16) k_jac_post(Geom g, TimeData td, const double* __restrict__ part,
-                                                  const double* __restrict__ sp, const double* __restrict__ rhs,
-                                                  double* __restrict__ out,
-                                                  const unsigned long long* __restrict__ done,
-                                                  unsigned long long target, unsigned long long starget) {
+__global__ void __launch_bounds__(128, 8) k_jac_post(Geom g, TimeData td, const double* __restrict__ part,
+                                                 const double* __restrict__ sp, const double* __restrict__ rhs,
+                                                 double* __restrict__ out,
+                                                 const unsigned long long* __restrict__ done,
+                                                 unsigned long long target, unsigned long long starget) {
   pdl_trigger();  // a PDL-launched consumer (the Vanka GEMV) may start its own prologue
   const int mu = blockIdx.y;
-  const StripIdx si(g);
-  const size_t ns = si.count(g);
-  const int ntx = jac_tiles_x(g), nty = jac_tiles_y(g);
-  const size_t nv = (size_t)(ntx - 1) * g.nny, nh = (size_t)(nty - 1) * g.nnx;
-  const size_t ncb = n_bcells(g);
-  size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t base = (size_t)mu * g.nd;
+  // 1. decode the item (nothing here depends on the other kernels)
+  int kind = 0;  // 1 strip node, 2 tile-line node off the strips, 3 boundary cell (pressure)
+  int X = 0, Y = 0;
+  size_t o = 0, cb = 0;
+  {
+    const StripIdx si(g);
+    const size_t ns = si.count(g);
+    const int ntx = jac_tiles_x(g), nty = jac_tiles_y(g);
+    const size_t nv = (size_t)(ntx - 1) * g.nny, nh = (size_t)(nty - 1) * g.nnx;
+    const size_t ncb = n_bcells(g);
+    size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < ns) {
+      si.node(g, t, X, Y);
+      kind = 1;
+    } else if ((t -= ns) < nv + nh) {
+      bool skip = false;
+      if (t < nv) {
+        X = 2 * JT * (int)(t / g.nny + 1);
+        Y = (int)(t % g.nny);
+      } else {
+        const size_t u = t - nv;
+        Y = 2 * JT * (int)(u / g.nnx + 1);
+        X = (int)(u % g.nnx);
+        skip = X % (2 * JT) == 0 && X > 0 && X / (2 * JT) < ntx;  // on a vertical line
+      }
+      if (!skip && !in_strip(g, X, Y)) kind = 2;
+    } else if ((t -= nv + nh) < ncb && !g.th) {
+      int ci, cj;
+      bcell_of(g, t, ci, cj);
+      cb = t;
+      o = base + g.mv + 3 * ((size_t)cj * g.nx + ci);
+      kind = 3;
+    }
+    if (kind == 1 || kind == 2) o = base + 2 * ((size_t)Y * g.nnx + X);
+  }
+  // 2. what does not depend on the tile pass: right-hand side, side products
+  double r[3] = {0.0, 0.0, 0.0}, b[3] = {0.0, 0.0, 0.0};
+  if (rhs && kind) {
+    r[0] = __ldg(rhs + o);
+    r[1] = __ldg(rhs + o + 1);
+    if (kind == 3) r[2] = __ldg(rhs + o + 2);
+  }
   tile_wait(done + 4, starget);  // the side products (all threads pass a barrier)
-  tile_wait(done + mu, target);  // the tile pass's node mu
-  KTRT(6);
-  if (t < ns) {
-    int X, Y;
-    si.node(g, t, X, Y);
-    const size_t o = base + 2 * ((size_t)Y * g.nnx + X);
-    double b[2], s[2];
+  if (kind == 1) {
     strip_sides(g, sp, mu, X, Y, b);
-    if (on_tile_line(g, X, Y)) {
+  } else if (kind == 3) {
+    const size_t ncb = n_bcells(g);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) b[j] = __ldcg(sp + ((size_t)mu * 21 + 18 + j) * ncb + cb);
+  }
+  // 3. the tile pass's sums of node mu
+  tile_wait(done + mu, target);
+  KTRT(6);
+  if (kind == 1 || kind == 2) {
+    double s[2];
+    if (kind == 2 || on_tile_line(g, X, Y)) {
       tile_partials(g, part, mu, X, Y, s);
     } else {
       s[0] = __ldcg(out + o);
@@ -1322,40 +1362,14 @@ __global__ void __launch_bounds__(128, 16) k_jac_post(Geom g, TimeData td, const
     }
     s[0] += b[0];
     s[1] += b[1];
-    out[o] = rhs ? rhs[o] - s[0] : s[0];
-    out[o + 1] = rhs ? rhs[o + 1] - s[1] : s[1];
+    out[o] = rhs ? r[0] - s[0] : s[0];
+    out[o + 1] = rhs ? r[1] - s[1] : s[1];
     KTRT(7);
-    return;
-  }
-  t -= ns;
-  if (t < nv + nh) {
-    int X, Y;
-    if (t < nv) {
-      X = 2 * JT * (int)(t / g.nny + 1);
-      Y = (int)(t % g.nny);
-    } else {
-      const size_t u = t - nv;
-      Y = 2 * JT * (int)(u / g.nnx + 1);
-      X = (int)(u % g.nnx);
-      if (X % (2 * JT) == 0 && X > 0 && X / (2 * JT) < ntx) return;  // on a vertical line
-    }
-    if (in_strip(g, X, Y)) return;
-    double s[2];
-    tile_partials(g, part, mu, X, Y, s);
-    const size_t o = base + 2 * ((size_t)Y * g.nnx + X);
-    out[o] = rhs ? rhs[o] - s[0] : s[0];
-    out[o + 1] = rhs ? rhs[o + 1] - s[1] : s[1];
-    KTRT(7);
-    return;
-  }
-  t -= nv + nh;
-  if (t < ncb && !g.th) {
-    int ci, cj;
-    bcell_of(g, t, ci, cj);
-    const size_t o = base + g.mv + 3 * ((size_t)cj * g.nx + ci);
-    for (int r = 0; r < 3; ++r) {
-      const double s = __ldcg(out + o + r) + sp[((size_t)mu * 21 + 18 + r) * ncb + t];
-      out[o + r] = rhs ? rhs[o + r] - s : s;
+  } else if (kind == 3) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const double s = __ldcg(out + o + j) + b[j];
+      out[o + j] = rhs ? r[j] - s : s;
     }
     KTRT(7);
   }

@@ -23,7 +23,6 @@ lib.pdst_debug_trace(_b0.ctypes.data_as(ctypes.c_void_p), 8192)
 flush.fill_(1)
 jac.matvec(x, out=y)
 torch.cuda.synchronize()
-lib = _lib.lib()
 n = ((cfg.nx + 15) // 16) * ((cfg.ny + 15) // 16)
 buf = np.zeros((8192, 16), dtype=np.uint64)
 lib.pdst_debug_trace(buf.ctypes.data_as(ctypes.c_void_p), 8192)
@@ -40,8 +39,8 @@ print("CTA duration min/median/max", d.min(), np.median(d), d.max())
 kt = buf[8191, :8].astype(np.float64)
 if kt[1] > 0:
     k0 = kt[0]
-    print("kernel marks (us from the first tile CTA start): tile pass end %.1f | side products end %.1f, waiting CTA released %.1f | post released (first thread) %.1f, post end %.1f"
-          % ((kt[1] - k0) / 1e3, (kt[3] - k0) / 1e3, (kt[5] - k0) / 1e3, (kt[6] - k0) / 1e3, (kt[7] - k0) / 1e3))
+    print("kernel marks (us from the first tile CTA start): tile pass end %.2f | side products end %.2f | post released (first warp) %.2f, post end %.2f"
+          % ((kt[1] - k0) / 1e3, (kt[3] - k0) / 1e3, (kt[6] - k0) / 1e3, (kt[7] - k0) / 1e3))
 # per-role / per-SM-load breakdown (role = (tile // 148) & 1; SM id in column 15)
 sm = buf[:n, 15].astype(np.int64)
 cnt = np.bincount(sm, minlength=160)
@@ -53,3 +52,23 @@ for key, sel in (("role0", role == 0), ("role1", role == 1), ("lone", load == 1)
     if sel.sum() == 0: continue
     c = (t[sel][:, :len(names)] - t0) / 1e3
     print(key, sel.sum(), " ".join(f"{np.median(c[:, i]):6.1f}" for i in range(len(names))))
+
+# precise cold spans from the kernel marks (globaltimer, 0.26 us resolution): 9 repetitions each
+r = torch.as_tensor(syn.d0, device="cuda")
+def spans(fn, reps=9):
+    out = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        lib.pdst_debug_trace(_b0.ctypes.data_as(ctypes.c_void_p), 8192)
+        flush.fill_(1)
+        fn()
+        torch.cuda.synchronize()
+        lib.pdst_debug_trace(buf.ctypes.data_as(ctypes.c_void_p), 8192)
+        k = buf[8191, :8].astype(np.float64)
+        tt = buf[:n].astype(np.float64)
+        out.append(((k[1] - k[0]) / 1e3, (k[7] - k[0]) / 1e3, np.median(tt[:, len(names) - 1] - tt[:, 0]) / 1e3))
+    a = np.array(out)
+    return np.median(a, axis=0), a.min(axis=0)
+for nm, fn in (("apply", lambda: jac.matvec(x, out=y)), ("defect", lambda: jac.defect(x, r, out=y))):
+    med, mn = spans(fn)
+    print(f"SPAN {nm}: tile pass {med[0]:.2f} us, tile start -> epilogue end {med[1]:.2f} us (min {mn[1]:.2f}), median CTA {med[2]:.2f} us")
