@@ -1471,19 +1471,6 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
     double rv[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};  // rhs of the own 2x2 nodes (defect mode)
     double rp[3] = {0, 0, 0};
     if (valid) {
-      // defect mode: the right-hand side of this cell's own nodes (lower-left
-      // 2x2) and pressures, loaded now for the assembly
-      if (rhs) {
-#pragma unroll
-        for (int n = 0; n < 4; ++n) {
-          const size_t o = (size_t)mu * g.nd + 2 * ((size_t)(2 * cj + (n >> 1)) * g.nnx + 2 * ci + (n & 1));
-          rv[n][0] = __ldg(rhs + o);
-          rv[n][1] = __ldg(rhs + o + 1);
-        }
-        if (!g.th)
-#pragma unroll
-          for (int j = 0; j < 3; ++j) rp[j] = __ldg(rhs + (size_t)mu * g.nd + g.mv + 3 * (size_t)c + j);
-      }
       if (cip) {
         // face matrices: own right / top, the left / bottom neighbours' right / top
         double W[4][6];
@@ -1501,6 +1488,21 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
       if (mu + 1 < K1)  // the next node's first half-columns towards L2
         for (int h = 0; h < PDST_PF_AHEAD; ++h) apc_prefetch_l2(cp + APC_SLOTS * JNT, h, HG);
       TR(3 + 5 * mu);
+    }
+    if (valid) {
+      // defect mode: the right-hand side of this cell's own nodes (lower-left
+      // 2x2) and pressures, loaded behind the face matrices, for the assembly
+      if (rhs) {
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+          const size_t o = (size_t)mu * g.nd + 2 * ((size_t)(2 * cj + (n >> 1)) * g.nnx + 2 * ci + (n & 1));
+          rv[n][0] = __ldg(rhs + o);
+          rv[n][1] = __ldg(rhs + o + 1);
+        }
+        if (!g.th)
+#pragma unroll
+          for (int j = 0; j < 3; ++j) rp[j] = __ldg(rhs + (size_t)mu * g.nd + g.mv + 3 * (size_t)c + j);
+      }
     }
     if (K1 > 1 && mu == 0) {  // the other nodes' planes (staging group 2) for the temporal mass
       cp_async_wait_group<0>();

@@ -67,7 +67,9 @@ def spans(fn, reps=9):
         k = buf[8191, :8].astype(np.float64)
         tt = buf[:n].astype(np.float64)
         out.append(((k[1] - k[0]) / 1e3, (k[7] - k[0]) / 1e3, np.median(tt[:, len(names) - 1] - tt[:, 0]) / 1e3))
+        ph = np.median(tt[:, :len(names)] - tt[:, :1], axis=0) / 1e3
     a = np.array(out)
+    print("   phases (median CTA, last repetition):", " ".join(f"{v:.1f}" for v in ph))
     return np.median(a, axis=0), a.min(axis=0)
 for nm, fn in (("apply", lambda: jac.matvec(x, out=y)), ("defect", lambda: jac.defect(x, r, out=y))):
     med, mn = spans(fn)
