@@ -792,6 +792,11 @@ __device__ unsigned long long g_trace[8192][16];
       unsigned long long t_;                                                                           \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                           \
       g_trace[blockIdx.y * gridDim.x + blockIdx.x][i] = t_;                                            \
+      if ((i) == 0) {                                                                                  \
+        unsigned s_;                                                                                   \
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(s_));                                                \
+        g_trace[blockIdx.y * gridDim.x + blockIdx.x][15] = s_;                                         \
+      }                                                                                                \
     }                                                                                                  \
   } while (0)
 // kernel-level marks: even slots keep the minimum, odd slots the maximum
@@ -839,8 +844,10 @@ constexpr int JNC = 2 * (JT + 2) + 1;
 constexpr int JNC2 = (JNC + 1) / 2;
 constexpr int JRS = 2 * JNC2;
 constexpr int JPLANE = JNC * JRS;
+// The cells' pressure dofs are staged in shared memory with the planes while
+// two CTAs still fit an SM (DG(0), DG(1)); beyond, they are loaded directly.
+__host__ __device__ constexpr bool jac_pstage(int k1) { return k1 <= 2; }
 __host__ __device__ constexpr int jpidx(int r, int c) { return r * JRS + (c & 1) * JNC2 + (c >> 1); }
-using JAcc = SmemAccN<JNT>;
 
 // A staged direction plane addressed by its offset in the kernel's dynamic
 // shared memory (the accesses stay LDS; a pointer array can be demoted to
@@ -982,7 +989,7 @@ struct JTabs {
 // zeros into their own slot) because of the barrier inside.
 template <bool HG, class XA>
 __device__ __forceinline__ void jac_volume_cached(const JTabs& T, const Disc& ds, const double* __restrict__ cp,
-                                                  const XA& XM, int r0, int c0, double* slot, bool sync_first,
+                                                  const XA& XM, int r0, int c0, double2* slot, bool sync_first,
                                                   unsigned long long* sig) {
 #pragma unroll 1
   for (int qx = 0; qx < 4; ++qx) {
@@ -1047,13 +1054,17 @@ __device__ __forceinline__ void jac_volume_cached(const JTabs& T, const Disc& ds
 #pragma unroll
     for (int jy = 0; jy < 3; ++jy)
 #pragma unroll
-      for (int ix = 0; ix < 3; ++ix)
-#pragma unroll
-        for (int d = 0; d < 2; ++d) {
-          const double v = T.Gx[qx][ix] * Pa[jy][d] + T.B[qx][ix] * Qa[jy][d];
-          double* sp = slot + (2 * (3 * jy + ix) + d) * JNT;
-          *sp = qx == 0 ? v : *sp + v;
+      for (int ix = 0; ix < 3; ++ix) {
+        const double v0 = T.Gx[qx][ix] * Pa[jy][0] + T.B[qx][ix] * Qa[jy][0];
+        const double v1 = T.Gx[qx][ix] * Pa[jy][1] + T.B[qx][ix] * Qa[jy][1];
+        double2* sp = slot + (3 * jy + ix) * JNT;  // both components: one 16-byte access
+        if (qx == 0) {
+          *sp = make_double2(v0, v1);
+        } else {
+          const double2 o = *sp;
+          *sp = make_double2(o.x + v0, o.y + v1);
         }
+      }
   }
 }
 
@@ -1390,7 +1401,8 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
                                                   double* __restrict__ out, double* __restrict__ part,
                                                   unsigned long long* __restrict__ done, const JTabs T) {
   double* sacc = g_dsmem + (size_t)K1 * 2 * JPLANE;  // [18][JNT] per-cell node contributions
-  double* spres = sacc + 18 * JNT;                    // [K1][3][JNT] the cells' pressure dofs
+  double* spres = sacc + 18 * JNT;                    // [K1][3][JNT] the cells' pressure dofs (K1 <= 2)
+  constexpr bool PSTAGE = jac_pstage(K1);
   // [K1][2][JPLANE] direction x_nu, all Radau nodes (one-cell ring), in front
   const int bx = blockIdx.x, by = blockIdx.y;
   const int i0 = bx * JT, j0 = by * JT;
@@ -1428,7 +1440,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
   cp_async_commit();
   for (int nu = 1; nu < K1; ++nu) stage_jac_async(g, x + (size_t)nu * g.nd, nu * 2 * JPLANE, X0, Y0);
   // the cell's pressure dofs of every node (read by the own thread with the temporal mass)
-  if (valid && ds.pressure && !g.th)
+  if (PSTAGE && valid && ds.pressure && !g.th)
 #pragma unroll
     for (int nu = 0; nu < K1; ++nu)
 #pragma unroll
@@ -1441,8 +1453,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
   for (int mu = 0; mu < K1; ++mu) {
     const double tw = td.tau_w[mu];
     const double* cp = cbase + (size_t)mu * APC_SLOTS * JNT;
-    double* slot = sacc + threadIdx.x;
-    const JAcc acc{slot};
+    double2* slot = reinterpret_cast<double2*>(sacc) + threadIdx.x;  // [9 nodes][JNT] (both components)
     const PlaneS XM{mu * 2 * JPLANE};
     double accp[3] = {0.0, 0.0, 0.0};
     // CIP, temporal mass and boundary sides accumulate in registers (the
@@ -1549,8 +1560,14 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
       // to 1-D Gauss sums (JTabs pA/pB/pM) and stay out of the volume loop.
       if (ds.pressure && !g.th) {  // Taylor-Hood: the pressure coupling is pdst_th.cu's
         const double WT = g.hx * g.hy * tw;
-        const double* pp = spres + (size_t)mu * 3 * JNT + threadIdx.x;  // staged with the planes
-        const double P0 = WT * pp[0], P1 = WT * pp[JNT], P2 = WT * pp[2 * JNT];
+        double P0, P1, P2;
+        if (PSTAGE) {  // staged with the planes
+          const double* pp = spres + (size_t)mu * 3 * JNT + threadIdx.x;
+          P0 = WT * pp[0], P1 = WT * pp[JNT], P2 = WT * pp[2 * JNT];
+        } else {
+          const double* xp = x + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
+          P0 = WT * __ldg(xp), P1 = WT * __ldg(xp + 1), P2 = WT * __ldg(xp + 2);
+        }
         // -q div u: rows of x_mu against the 1-D sums
         double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll
@@ -1582,9 +1599,11 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
 #pragma unroll
       for (int a = 0; a < 3; ++a)
 #pragma unroll
-        for (int b = 0; b < 3; ++b)
-#pragma unroll
-          for (int d = 0; d < 2; ++d) acc.add(a, b, d, ra[a][b][d]);
+        for (int b = 0; b < 3; ++b) {
+          double2* sp = slot + (3 * a + b) * JNT;
+          const double2 o = *sp;
+          *sp = make_double2(o.x + ra[a][b][0], o.y + ra[a][b][1]);
+        }
       const size_t o = (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
       // boundary cells: raw sum, finished (side terms, rhs) by k_jac_post
       const bool bcell = ci == 0 || cj == 0 || ci == g.nx - 1 || cj == g.ny - 1;
@@ -1603,27 +1622,34 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
       const int me = ty * JT + tx;
       const bool hl = tx > 0, hd = ty > 0;
       // neighbour slots: left, down, down-left cell of this thread's cell
-      const double* sm_ = sacc + me;
-      const double* sl_ = sacc + me - 1;
-      const double* sd_ = sacc + me - JT;
-      const double* sld = sacc + me - JT - 1;
-      auto at = [&](const double* p, int a, int d) { return p[(2 * a + d) * JNT]; };
+      const double2* sm_ = reinterpret_cast<const double2*>(sacc) + me;
+      const double2* sl_ = sm_ - 1;
+      const double2* sd_ = sm_ - JT;
+      const double2* sld = sm_ - JT - 1;
+      auto at = [&](const double2* p, int a, int d) {  // (the two components' loads of a node merge)
+        const double2 v = p[a * JNT];
+        return d == 0 ? v.x : v.y;
+      };
+      const bool oal = (reinterpret_cast<size_t>(out + base) & 15) == 0;
       // n = own-node index (lower-left 2x2, rhs preloaded) or -1 (tile edge row / column)
       auto emit = [&](int lx, int ly, double s0, double s1, int n) {
         const bool shx = (lx == 0 && i0 > 0) || (lx == 2 * JT && i0 + JT < g.nx);
         const bool shy = (ly == 0 && j0 > 0) || (ly == 2 * JT && j0 + JT < g.ny);
         if (shx || shy) {
           double* pp = part + (((size_t)mu * ntiles + tile) * JPER + perim(lx, ly)) * 2;
-          pp[0] = s0;
-          pp[1] = s1;
+          *reinterpret_cast<double2*>(pp) = make_double2(s0, s1);
         } else {
           const size_t o = base + 2 * ((size_t)(2 * j0 + ly) * g.nnx + 2 * i0 + lx);
           if (rhs && !in_strip(g, 2 * i0 + lx, 2 * j0 + ly)) {  // strip nodes: k_jac_post
             s0 = (n >= 0 ? rv[n][0] : __ldg(rhs + o)) - s0;
             s1 = (n >= 0 ? rv[n][1] : __ldg(rhs + o + 1)) - s1;
           }
-          out[o] = s0;  // (nd may be odd: no 16-byte vector store)
-          out[o + 1] = s1;
+          if (oal) {  // both components of the node as one 16-byte store
+            *reinterpret_cast<double2*>(out + o) = make_double2(s0, s1);
+          } else {  // odd nd and an odd Radau node: the block is only 8-byte aligned
+            out[o] = s0;
+            out[o + 1] = s1;
+          }
         }
       };
       const int lx = 2 * tx, ly = 2 * ty;
@@ -2175,7 +2201,7 @@ __global__ void __launch_bounds__(128) k_boundary_matrices(Geom g, Disc ds, Lin 
 
 template <int K1>
 size_t jac_smem() {
-  return ((size_t)2 * K1 * JPLANE + (size_t)JNT * (18 + 3 * K1)) * sizeof(double);
+  return ((size_t)2 * K1 * JPLANE + (size_t)JNT * (18 + (jac_pstage(K1) ? 3 * K1 : 0))) * sizeof(double);
 }
 template <int K1>
 size_t res_smem() {

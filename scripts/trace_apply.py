@@ -74,3 +74,19 @@ def spans(fn, reps=9):
 for nm, fn in (("apply", lambda: jac.matvec(x, out=y)), ("defect", lambda: jac.defect(x, r, out=y))):
     med, mn = spans(fn)
     print(f"SPAN {nm}: tile pass {med[0]:.2f} us, tile start -> epilogue end {med[1]:.2f} us (min {mn[1]:.2f}), median CTA {med[2]:.2f} us")
+
+# the slowest CTAs of the last repetition
+tt = buf[:n].astype(np.float64)
+end = (tt[:, len(names) - 1] - tt[:, 0].min()) / 1e3
+sm = buf[:n, 15].astype(np.int64)
+cnt = np.bincount(sm, minlength=200)
+order = np.argsort(-end)
+ntx = (cfg.nx + 15) // 16
+print("slowest CTAs: (end us, tile x, tile y, sm, CTAs on that sm, started first on sm, staged us)")
+for i in order[:16]:
+    first = all(tt[i, 0] <= tt[j, 0] for j in np.where(sm == sm[i])[0])
+    print(f"  {end[i]:6.2f} {i % ntx:3d} {i // ntx:3d} {sm[i]:4d} {cnt[sm[i]]} {int(first)} {(tt[i,1]-tt[:,0].min())/1e3:6.2f}")
+lone = cnt[sm] == 1
+print("lone CTAs end: median %.2f max %.2f | paired: median %.2f max %.2f" % (np.median(end[lone]), end[lone].max(), np.median(end[~lone]), end[~lone].max()))
+idx = np.arange(n)
+print("second CTA per SM (tile >= 148): median %.2f max %.2f; first: median %.2f max %.2f" % (np.median(end[idx >= 148]), end[idx >= 148].max(), np.median(end[idx < 148]), end[idx < 148].max()))
