@@ -1427,6 +1427,15 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
   TR(0);
   KTR(0);
   // HG == false (Picard, or no viscous term): the a~ slots are zeros and never read
+  // The direction's node rows towards L2 before the wait as well: L2 is the
+  // point of coherence, so lines the predecessor still writes are updated in
+  // place, and a cold x (first apply after other work) lands while we wait.
+  for (int idx = threadIdx.x; idx < K1 * JNC * 5; idx += JNT) {
+    const int nu = idx / (JNC * 5), rem = idx - nu * (JNC * 5);
+    const int r = rem / 5, X = X0 + 8 * (rem - 5 * r), Y = Y0 + r;
+    if (Y >= 0 && Y < g.nny && X < g.nnx)
+      prefetch_l2(x + (size_t)nu * g.nd + 2 * ((size_t)Y * g.nnx + max(X, 0)));
+  }
   if (valid)  // the coefficient stream does not depend on the predecessor
     for (int h = 0; h < PDST_PF_AHEAD; ++h) apc_prefetch_l2(cbase, h, HG);
   // launched with PDL: x (and the scratch the predecessor's epilogue may still
