@@ -220,7 +220,7 @@ def run_distributed(args):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     n_launch0 = L.lib().pdst_launch_count()
     for i in range(args.steps):
-        flush.fill_(float(i))
+        flush_l2(flush, i)
         ev[i][0].record()
         step()
         ev[i][1].record()
@@ -284,7 +284,7 @@ def run_distributed(args):
                                        "x / d halos, defect row and increment reverse-add as pack -> NCCL "
                                        "send/recv (or in-process copy) -> unpack kernels, fused owned-row Vanka "
                                        "update; one stream, no host synchronization)",
-                   "l2": "flushed between timed steps (256 MiB write, outside events)",
+                   "l2": "flushed between timed steps (256 MiB write, then a 256 MiB read of another buffer so no dirty lines remain; outside events)",
                    "parallelism": (f"strip partition x{ws} over NCCL send/recv (libpdst, torch's communicator)"
                                    if ws > 1 else f"{P} virtual ranks on one GPU (pdst_strips_step_local)")},
         "gpu_launches": n_launches,
@@ -360,7 +360,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     n_launch0 = L.lib().pdst_launch_count()
     for i in range(args.steps):
-        flush.fill_(float(i))
+        flush_l2(flush, i)
         ev[i][0].record()
         step()
         ev[i][1].record()
@@ -385,11 +385,12 @@ def run_ours(args):
     L.lib().pdst_profile(h, 1)
     nprof = max(3, min(args.steps, 20))
     for i in range(nprof):
-        flush.fill_(float(i))
+        flush_l2(flush, i)
         step()
     torch.cuda.synchronize()
     kt = {}
-    for kid, name in ((0, "jacobian"), (1, "vanka_gemv"), (2, "vanka_scatter")):
+    # class 0: the Jacobian apply y = J x; class 6: the sweep's defect apply y = r - J x (same kernels + rhs)
+    for kid, name in ((0, "jacobian"), (1, "vanka_gemv"), (2, "vanka_scatter"), (6, "jacobian_defect")):
         ms, cnt = L.C.c_double(), L.C.c_int64()
         L.lib().pdst_profile_read(h, kid, L.C.byref(ms), L.C.byref(cnt))
         kt[name] = (ms.value / max(cnt.value, 1), cnt.value)
@@ -496,10 +497,11 @@ def run_ours(args):
                                f"nu={cfg.nu}, nu_inf={cfg.nu_inf}, modN(sigma_max=nu), surrogate patches at "
                                f"rep_fraction={cfg.rep_fraction}, omega={cfg.omega}",
                    "n_dof": N, "step": "1 Jacobian apply + 1 Vanka sweep (1 smoothing step)",
-                   "l2": "flushed between timed steps (256 MiB write, outside events)",
+                   "l2": "flushed between timed steps (256 MiB write, then a 256 MiB read of another buffer so no dirty lines remain; outside events)",
                    "parallelism": f"replicas x{ws}"},
         "gpu_launches": n_launches,
-        # dominant kernel by time: the Jacobian apply (2 launches per step).  Its
+        # dominant kernel by time: the Jacobian apply (y = J x; the sweep's defect
+        # apply, the same kernels with a right-hand side, is kernels.jacobian_defect).  Its
         # algorithmic bytes are SURVEY §8(d)'s B_apply (the reference algorithm's
         # compulsory traffic: x, y and the per-qp / side / CIP coefficient cache).
         "roofline": {"bound": "hbm", "kernel": "jacobian apply (k_jacobian + k_jac_post)",
@@ -521,12 +523,16 @@ def run_ours(args):
                                "reference_cache_equiv_gbs": b_apply_ref / t_jac / 1e9,
                                "minimal_state_bytes": b_apply_min,
                                "minimal_state_equiv_gbs": b_apply_min / t_jac / 1e9},
+            "jacobian_defect": {"ms": kt["jacobian_defect"][0],
+                                "algorithmic_bytes": b_apply_ref + 8.0 * N,
+                                "frac_hbm": (b_apply_ref + 8.0 * N) / max(kt["jacobian_defect"][0], 1e-9) / 1e6 / peak,
+                                "note": "the sweep's defect apply r - J d: the apply's kernels plus the right-hand side"},
             "vanka_gemv": {"ms": kt["vanka_gemv"][0]},
             "vanka_scatter": {"ms": kt["vanka_scatter"][0]},
             **extra,
         },
         "apply_gdofs": N / t_jac / 1e9,
-        "sweep_gdofs": N / (t_jac + t_gemv + kt["vanka_scatter"][0] * 1e-3) / 1e9,
+        "sweep_gdofs": N / (kt["jacobian_defect"][0] * 1e-3 + t_gemv + kt["vanka_scatter"][0] * 1e-3) / 1e9,
         "setup_s": t_setup,
         "clocks": clk,
         "e2e": e2e,
@@ -566,7 +572,7 @@ def measure_residual_and_build(cfg, ctx, syn, jac, lvl, dev, flush, peak, reps=1
         res()
     ts = []
     for i in range(reps):
-        flush.fill_(float(i))
+        flush_l2(flush, i)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         res()
@@ -635,12 +641,12 @@ def measure_config_kernels(name, peak, steps=5):
     h = jac.dev.h
     L.lib().pdst_profile(h, 1)
     for i in range(steps):
-        flush.fill_(float(i))
+        flush_l2(flush, i)
         jac.matvec(x, out=y)
         lvl.smooth(d, x, 1, cfg.omega, inplace=True)
     torch.cuda.synchronize()
     kt = {}
-    for kid, kn in ((0, "jacobian"), (1, "vanka_gemv"), (2, "vanka_scatter")):
+    for kid, kn in ((0, "jacobian"), (1, "vanka_gemv"), (2, "vanka_scatter"), (6, "jacobian_defect")):
         ms, cnt = L.C.c_double(), L.C.c_int64()
         L.lib().pdst_profile_read(h, kid, L.C.byref(ms), L.C.byref(cnt))
         kt[kn] = ms.value / max(cnt.value, 1)
@@ -652,13 +658,14 @@ def measure_config_kernels(name, peak, steps=5):
     _, nblk, bpp = lvl.patch_info()
     b_gemv = float(nc * bpp) + 8.0 * (N + nc * 21 * k1)
     t_j, t_g = kt["jacobian"] * 1e-3, kt["vanka_gemv"] * 1e-3
-    t_step = t_j + t_j + t_g + kt["vanka_scatter"] * 1e-3  # apply + (defect apply, GEMV, scatter)
+    t_step = t_j + (kt["jacobian_defect"] + kt["vanka_scatter"]) * 1e-3 + t_g  # apply + (defect apply, GEMV, scatter)
     out = {"workload": f"{name}: {cfg.nx}x{cfg.ny} Q2/P1disc, DG({cfg.k}), p={cfg.p}, delta={cfg.delta}, "
                        f"nu_inf={cfg.nu_inf}, modN, surrogate patches", "n_dof": N,
            "apply": {"ms": kt["jacobian"], "gdofs": N / t_j / 1e9, "algorithmic_bytes": b_apply_ref,
                      "achieved_gbs": b_apply_ref / t_j / 1e9, "frac": b_apply_ref / t_j / 1e9 / peak},
            "vanka_gemv": {"ms": kt["vanka_gemv"], "algorithmic_bytes": b_gemv, "achieved_gbs": b_gemv / t_g / 1e9,
                           "frac": b_gemv / t_g / 1e9 / peak},
+           "defect_apply_ms": kt["jacobian_defect"],
            "vanka_scatter_ms": kt["vanka_scatter"],
            "step_gdofs_from_kernels": N / t_step / 1e9,
            "note": "same run as the headline line; libpdst per-launch CUDA events, L2 flushed between steps"}
@@ -944,6 +951,21 @@ def relaunch(n):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(n), "--master-addr",
            "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
     return subprocess.run(cmd, cwd=ROOT).returncode
+
+
+_FLUSH_READ = {}
+
+
+def flush_l2(flush, i):
+    """Cold L2 between timed steps: write a buffer larger than L2 (256 MiB), then read ANOTHER
+    256 MiB buffer so the cache is left holding clean lines -- otherwise the first timed kernel
+    shares HBM with the write-back of the flush's dirty lines (measured: ~2 us on a 44 us apply).
+    Both passes are outside the timed events."""
+    flush.fill_(float(i))
+    rd = _FLUSH_READ.get(flush.device)
+    if rd is None or rd.numel() != flush.numel():
+        rd = _FLUSH_READ[flush.device] = flush.new_zeros(flush.shape)
+    rd.sum()
 
 
 def main():

@@ -202,6 +202,10 @@ int pdst_multidot(pdst_handle* h, const double* A, int64_t lda, int m, const dou
 int pdst_multi_axpy(pdst_handle* h, const double* A, const double* B, int64_t lda, int m, const double* c, double* w,
                     double* w2, int64_t n, int where);
 
+/* Per-launch CUDA events around the handle's kernel groups (measurement only;
+   the events disable PDL overlap between the groups).  Kernel classes:
+   0 Jacobian apply y = J x, 1 patch GEMV, 2 Vanka scatter, 3 residual,
+   4 transfers, 5 coarse level applies, 6 defect apply y = r - J x. */
 int pdst_profile(pdst_handle* h, int enable);
 int pdst_profile_read(pdst_handle* h, int kernel, double* total_ms, int64_t* launches);
 

@@ -231,7 +231,8 @@ int async_used(pdst_handle* h, AsyncSlot& s);
 int async_out(pdst_handle* h, AsyncSlot& s, double* p, size_t n);
 
 // Kernel classes for pdst_profile_read.
-enum { PK_JACOBIAN = 0, PK_VANKA_GEMV = 1, PK_VANKA_SCATTER = 2, PK_RESIDUAL = 3, PK_TRANSFER = 4, PK_LEVEL = 5 };
+enum { PK_JACOBIAN = 0, PK_VANKA_GEMV = 1, PK_VANKA_SCATTER = 2, PK_RESIDUAL = 3, PK_TRANSFER = 4, PK_LEVEL = 5,
+       PK_DEFECT = 6 /* the finest Jacobian apply with a right-hand side: y = r - J x */ };
 
 // Launch `expr` (a cudaError_t expression) bracketed by profiling events when enabled.
 #define PDST_TIMED(h, kid, expr)                                      \

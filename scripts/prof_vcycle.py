@@ -32,7 +32,7 @@ h = pre.dev.h
 L.lib().pdst_profile(h, 1)
 pre.apply(r, out=z)
 torch.cuda.synchronize()
-names = ["jacobian", "vanka_gemv", "vanka_scatter", "residual", "transfer", "level_apply"]
+names = ["jacobian", "vanka_gemv", "vanka_scatter", "residual", "transfer", "level_apply", "defect_apply"]
 for k, n in enumerate(names):
     ms, cnt = C.c_double(), C.c_int64()
     L.lib().pdst_profile_read(h, k, C.byref(ms), C.byref(cnt))
