@@ -427,7 +427,7 @@ static int jac_common(pdst_handle* h, const double* x, const double* r, double* 
     if (err) return err;
     double* part = h->jpart.ensure_zeroed(jacobian_scratch(h->g, h->td.k1));
     if (!part) return fail(PDST_ECUDA, "out of device memory");
-    CK(PDST_TIMED(h, rd ? PK_DEFECT : PK_JACOBIAN, jacobian_apply(h->g, h->td, h->ds, lin_of(h), xd, rd, yd, part, &h->jepoch, h->stream)));
+    CK(PDST_TIMED(h, rd ? PK_DEFECT : PK_JACOBIAN, jacobian_apply(h->g, h->td, h->ds, lin_of(h), xd, rd, yd, part, h->stream)));
     if (h->g.th)
       if (int e = th_add(h, xd, yd)) return e;
     if (int e = async_used(h, h->as_x)) return e;
@@ -449,7 +449,7 @@ static int jac_common(pdst_handle* h, const double* x, const double* r, double* 
   double* part = h->jpart.ensure_zeroed(jacobian_scratch(h->g, h->td.k1));
   if (!part) return fail(PDST_ECUDA, "out of device memory");
   CK(PDST_TIMED(h, rd ? PK_DEFECT : PK_JACOBIAN,
-                jacobian_apply(h->g, h->td, h->ds, lin_of(h), xd, rd, yd, part, &h->jepoch, h->stream)));
+                jacobian_apply(h->g, h->td, h->ds, lin_of(h), xd, rd, yd, part, h->stream)));
   if (h->g.th)
     if (int e = th_add(h, xd, yd)) return e;
   return finish_out(h, y, yd, n, where);

@@ -162,7 +162,6 @@ struct pdst_handle {
   pdst::DeviceBuffer partials;
   pdst::DeviceBuffer kpartials;  // FGMRES multi-dot partial sums
   pdst::DeviceBuffer jpart;  // Jacobian tile-boundary partial sums (+ the tile pass's completion counters)
-  unsigned long long jepoch = 0;  // applies launched with jpart: the counters' target is jepoch * tiles
 
   // surrogate (representative-state) linearization and patch scratch
   pdst::DeviceBuffer state_rep, eta_rep, gam_rep, etaf_rep, gamf_rep;

@@ -11,11 +11,11 @@ cudaError_t set_tables(const Tables& t);
 Tables host_tables();
 
 // y = J x (rhs == null) or y = rhs - J x; `part` holds jacobian_scratch() doubles, zero when
-// first used, and `epoch` counts the applies launched with it (both owned by the handle).
+// first used (its tail holds the apply's completion counters, which every apply leaves at zero).
 size_t jacobian_scratch(const Geom& g, int k1);
 // Requires the linearization's boundary matrices (L.bmat) and apply cache (L.apc).
 cudaError_t jacobian_apply(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* x,
-                           const double* rhs, double* out, double* part, unsigned long long* epoch, cudaStream_t st);
+                           const double* rhs, double* out, double* part, cudaStream_t st);
 
 // Apply cache of the linearization L at velocity state (k1, Mv): the
 // per-quadrature-point coefficients the Jacobian apply streams

@@ -533,14 +533,14 @@ static int level_defect(pdst_handle* h, int l, const double* x, const double* r,
     c->stream = h->stream;
     double* part = c->jpart.ensure_zeroed(jacobian_scratch(c->g, c->td.k1));
     if (!part) return set_error(PDST_ECUDA, "out of device memory");
-    CK(PDST_TIMED(h, PK_LEVEL, jacobian_apply(c->g, c->td, c->ds, lin_of(c), x, r, y, part, &c->jepoch, h->stream)));
+    CK(PDST_TIMED(h, PK_LEVEL, jacobian_apply(c->g, c->td, c->ds, lin_of(c), x, r, y, part, h->stream)));
     return PDST_OK;
   }
   if (l == L - 1) {
     double* part = h->jpart.ensure_zeroed(jacobian_scratch(h->g, h->td.k1));
     if (!part) return set_error(PDST_ECUDA, "out of device memory");
     CK(PDST_TIMED(h, r ? PK_DEFECT : PK_JACOBIAN,
-                  jacobian_apply(h->g, h->td, h->ds, lin_of(h), x, r, y, part, &h->jepoch, h->stream)));
+                  jacobian_apply(h->g, h->td, h->ds, lin_of(h), x, r, y, part, h->stream)));
   } else {
     CK(PDST_TIMED(h, PK_LEVEL, level_apply(level_op(h, l), h->td, x, r, y, level_scratch(h, l), h->stream)));
   }

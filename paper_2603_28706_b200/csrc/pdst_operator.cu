@@ -945,9 +945,12 @@ __device__ __forceinline__ void apc_prefetch_l2(const double* __restrict__ cp, i
 // strip sums) are done — after a CTA barrier, by one thread, behind a
 // device-scope fence — and the epilogue (k_jac_post) of that node polls the
 // counter instead of waiting for the whole grid, so node mu's epilogue runs
-// under the tile pass of node mu + 1.  The counters only grow: apply number e
-// of a handle waits for e * tiles.  No deadlock: the epilogue is launched
-// (PDL) only after every tile CTA has started.
+// under the tile pass of node mu + 1.  The last epilogue CTA to finish sets the
+// counters back to zero (every epilogue CTA is past its waits by then, and the
+// next apply's tile pass signals only after its own grid-dependency wait), so
+// the targets are constants and a captured launch sequence can be replayed.
+// No deadlock: the epilogue is launched (PDL) only after every tile CTA has
+// started.
 __device__ __forceinline__ void tile_signal(unsigned long long* sig) {
   if (threadIdx.x == 0) {
     __threadfence();
@@ -1383,6 +1386,17 @@ __global__ void __launch_bounds__(128, 8) k_jac_post(Geom g, TimeData td, const 
       out[o + j] = rhs ? r[j] - s : s;
     }
     KTRT(7);
+  }
+  // the last epilogue CTA of this apply re-arms the counters (done[5] counts finished epilogue CTAs)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long* cnt = const_cast<unsigned long long*>(done);
+    __threadfence();
+    if (atomicAdd(cnt + 5, 1ull) == (unsigned long long)gridDim.x * gridDim.y - 1) {
+#pragma unroll
+      for (int i = 0; i < 6; ++i) cnt[i] = 0ull;
+      __threadfence();
+    }
   }
 }
 
@@ -2219,7 +2233,7 @@ size_t res_smem() {
 
 template <int K1>
 cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* x,
-                       const double* rhs, double* out, double* part, unsigned long long* epoch, cudaStream_t st) {
+                       const double* rhs, double* out, double* part, cudaStream_t st) {
   static DeviceOnce once;
   const size_t sm = jac_smem<K1>();
   const int dev = current_device();
@@ -2273,8 +2287,7 @@ cudaError_t launch_jac(const Geom& g, const TimeData& td, const Disc& ds, const 
   // completion counters behind the side products (zero in a fresh scratch)
   unsigned long long* done = reinterpret_cast<unsigned long long*>(sp + (size_t)K1 * 21 * ncb);
   const dim3 sgrid((unsigned)((ncb + 3) / 4), K1);
-  const unsigned long long target = ++(*epoch) * (unsigned long long)ntiles;
-  const unsigned long long starget = *epoch * (unsigned long long)(sgrid.x * sgrid.y);
+  const unsigned long long target = ntiles, starget = (unsigned long long)sgrid.x * sgrid.y;
   if (L.has_gamma && ds.viscous)
     PDST_LAUNCH(e = launch_pdl(k_jacobian<K1, true>, grid, dim3(JNT), sm, st, g, td, ds, L, x, rhs, out, part, done, T));
   else  // Picard (or no viscous term): the tangent's a~ slots are zeros, not streamed
@@ -2336,13 +2349,12 @@ size_t jacobian_scratch(const Geom& g, int k1) {
 }
 
 cudaError_t jacobian_apply(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* x,
-                           const double* rhs, double* out, double* part, unsigned long long* epoch,
-                           cudaStream_t st) {
+                           const double* rhs, double* out, double* part, cudaStream_t st) {
   switch (td.k1) {
-    case 1: return launch_jac<1>(g, td, ds, L, x, rhs, out, part, epoch, st);
-    case 2: return launch_jac<2>(g, td, ds, L, x, rhs, out, part, epoch, st);
-    case 3: return launch_jac<3>(g, td, ds, L, x, rhs, out, part, epoch, st);
-    case 4: return launch_jac<4>(g, td, ds, L, x, rhs, out, part, epoch, st);
+    case 1: return launch_jac<1>(g, td, ds, L, x, rhs, out, part, st);
+    case 2: return launch_jac<2>(g, td, ds, L, x, rhs, out, part, st);
+    case 3: return launch_jac<3>(g, td, ds, L, x, rhs, out, part, st);
+    case 4: return launch_jac<4>(g, td, ds, L, x, rhs, out, part, st);
     default: return cudaErrorNotSupported;
   }
 }

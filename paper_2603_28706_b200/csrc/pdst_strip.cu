@@ -296,8 +296,8 @@ int strip_step(pdst_handle* const* hs, int n, double* const* xs, double* const* 
     double* part = h->jpart.ensure_zeroed(jacobian_scratch(h->g, k1));
     defects[r] = h->defect.ensure(nl);
     if (!part || !defects[r]) return set_error(PDST_ECUDA, "out of device memory");
-    CKS(PDST_TIMED(h, PK_JACOBIAN, jacobian_apply(h->g, h->td, h->ds, lin_of(h), xs[r], nullptr, ys[r], part, &h->jepoch, st)));
-    CKS(PDST_TIMED(h, PK_DEFECT, jacobian_apply(h->g, h->td, h->ds, lin_of(h), ds[r], rs[r], defects[r], part, &h->jepoch, st)));
+    CKS(PDST_TIMED(h, PK_JACOBIAN, jacobian_apply(h->g, h->td, h->ds, lin_of(h), xs[r], nullptr, ys[r], part, st)));
+    CKS(PDST_TIMED(h, PK_DEFECT, jacobian_apply(h->g, h->td, h->ds, lin_of(h), ds[r], rs[r], defects[r], part, st)));
   }
   if (int e = exchange(hs, n, defects.data(), KIND_DEFECT)) return e;
   for (int r = 0; r < n; ++r) {

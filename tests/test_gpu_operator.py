@@ -146,3 +146,47 @@ def test_buffer_size_errors():
     # the right sizes still work
     assert np.isfinite(jac.matvec(x)).all()
     assert np.isfinite(lvl.smooth(x, x, 1, 0.7)).all()
+
+
+def test_apply_repeats_and_graph_replay():
+    """The apply's epilogue polls per-node completion counters that the last
+    epilogue CTA re-arms: back-to-back applies / defects on one handle and a
+    captured-and-replayed launch sequence give the same bits as the first call
+    (multi-tile mesh, so tile-line partials and both counters are in play)."""
+    import torch
+
+    from paper_2603_28706_b200 import problem as pb
+    from paper_2603_28706_b200.operators import SlabJacobian
+    from paper_2603_28706_b200.synth import SynthConfig, make_slab_inputs
+
+    cfg = SynthConfig("graph", 40, 24, 1, 1.3, 1.0e-3, 1.0, 0.0, 4, 3)
+    syn = make_slab_inputs(cfg)
+    params = pb.ModelParams(cfg.p, cfg.delta, cfg.nu, cfg.nu_inf)
+    ctx = pb.make_context(cfg.nx, cfg.ny, cfg.k, params, cfg.tau,
+                          config=pb.DiscretizationConfig(cfg.gamma1, cfg.gamma2, cfg.gamma_cip), v_minus=syn.v_minus)
+    U = torch.as_tensor(syn.U, device="cuda")
+    x = torch.as_tensor(syn.x, device="cuda")
+    r = torch.as_tensor(syn.d0, device="cuda")
+    jac = SlabJacobian(ctx, U, pb.modified_newton(cfg.nu))
+    y0 = jac.matvec(x).clone()
+    d0 = jac.defect(x, r).clone()
+    y, d = torch.empty_like(x), torch.empty_like(x)
+    for _ in range(5):
+        jac.matvec(x, out=y)
+        jac.defect(x, r, out=d)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y0) and torch.equal(d, d0)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        jac.matvec(x, out=y)  # warm-up on the side stream
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            jac.matvec(x, out=y)
+            jac.defect(x, r, out=d)
+        for _ in range(3):
+            y.zero_()
+            d.zero_()
+            g.replay()
+        torch.cuda.synchronize()
+    assert torch.equal(y, y0) and torch.equal(d, d0)
