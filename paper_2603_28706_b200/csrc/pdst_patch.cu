@@ -92,10 +92,40 @@ __device__ void cip_weights(const PatchArgs& a, int K, double* cwv, double* cwh)
   }
 }
 
-// Spatial block entry (R_K J R_K')_{ij} of element slot s (cwv / cwh: the
-// patch's face weights, cip_weights).
-__device__ double spatial_entry(const PatchArgs& a, int s, int K, int i, int j, const double* cwv,
-                                const double* cwh) {
+// Per-patch tables of the CIP couplings, filled once per CTA: the jump factors
+// of the patch's three node columns / rows against the four faces per
+// direction that can see them, the faces' validity and the tangential basis
+// values — so an entry's face loop is table lookups in a fixed order instead of
+// index arithmetic, constant-bank gathers and branches per face.
+struct PatchTabs {
+  double jx[4][3];      // jump_factor(2 ki + xn, ki - 2 + f)   vertical faces
+  double jy[4][3];      // jump_factor(2 kj + yn, kj - 2 + f)   horizontal faces
+  double B[4][3];       // c_tab.B
+  unsigned char vv[4][3];  // vertical face (ki - 2 + f, kj - 1 + g) inside the mesh
+  unsigned char vh[4][3];  // horizontal face (ki - 1 + g, kj - 2 + f) inside the mesh
+};
+
+__device__ void patch_tabs(const Geom& g, int K, PatchTabs& T) {
+  const int ki = K % g.nx, kj = K / g.nx;
+  const int t = threadIdx.x;
+  if (t < 12) {
+    const int f = t / 3, n = t % 3;
+    T.jx[f][n] = jump_factor(2 * ki + n, ki - 2 + f);
+    T.jy[f][n] = jump_factor(2 * kj + n, kj - 2 + f);
+    T.B[f][n] = c_tab.B[f][n];
+    const int fi = ki - 2 + f, fj = kj - 1 + n;  // vertical face, its cell row
+    T.vv[f][n] = fi >= 0 && fi <= g.nx - 2 && fj >= 0 && fj <= g.ny - 1;
+    const int hj = kj - 2 + f, hi = ki - 1 + n;  // horizontal face, its cell column
+    T.vh[f][n] = hj >= 0 && hj <= g.ny - 2 && hi >= 0 && hi <= g.nx - 1;
+  }
+}
+
+// Spatial block entry (R_K J R_K')_{ij} of element slot s in two parts (cwv /
+// cwh: the patch's face weights, cip_weights; T: patch_tabs).  The faces are
+// visited in (row, column) order and skipped where a jump factor vanishes.
+// Part 1 (independent of the face weights): the element matrices of every
+// cell containing both dofs.
+__device__ double spatial_entry_cells(const PatchArgs& a, int s, int K, int i, int j) {
   const Geom& g = a.g;
   const int ki = K % g.nx, kj = K / g.nx;
   const double* ET = a.ET + (size_t)s * g.ncells * 441;
@@ -105,41 +135,62 @@ __device__ double spatial_entry(const PatchArgs& a, int s, int K, int i, int j, 
   const int XB = 2 * ki + jb % 3, YB = 2 * kj + jb / 3;
   const int xmin = min(XA, XB), xmax = max(XA, XB), ymin = min(YA, YB), ymax = max(YA, YB);
   double val = 0.0;
-  // element matrices of every cell containing both nodes
   for (int cy = max(0, ceil_half(ymax - 2)); cy <= min(g.ny - 1, floor_half(ymin)); ++cy)
     for (int cx = max(0, ceil_half(xmax - 2)); cx <= min(g.nx - 1, floor_half(xmin)); ++cx) {
       const int c = cy * g.nx + cx;
       const int al = 3 * (YA - 2 * cy) + (XA - 2 * cx), bl = 3 * (YB - 2 * cy) + (XB - 2 * cx);
       val += ET[((size_t)c * 21 + 2 * bl + e) * 21 + 2 * al + d];
     }
+  return val;
+}
+
+// Part 2: + the CIP couplings of the faces that see both nodes (added to val = part 1).
+__device__ double spatial_entry_faces(const PatchArgs& a, int s, int i, int j, double val, const double* cwv,
+                                      const double* cwh, const PatchTabs& T) {
+  const Geom& g = a.g;
+  if (i >= 18 || j >= 18) return val;
+  const int ia = i >> 1, d = i & 1, jb = j >> 1, e = j & 1;
+  const int xa = ia % 3, ya = ia / 3, xb = jb % 3, yb = jb / 3;  // node positions in the patch cell
   if (d != e || !(a.ds.convection && a.ds.gamma_cip > 0.0)) return val;
-  // vertical faces (normal +x) between (fi, fj) and (fi+1, fj)
+  // vertical faces (normal +x) between (fi, fj) and (fi+1, fj): fj = kj - 1 + gr, fi = ki - 2 + f
   {
     const double h = g.hy, coef = a.ds.gamma_cip * h * h / (g.hx * g.hx);
-    for (int fj = max(0, ceil_half(ymax - 2)); fj <= min(g.ny - 1, floor_half(ymin)); ++fj)
-      for (int fi = max(0, ceil_half(xmax - 4)); fi <= min(g.nx - 2, floor_half(xmin)); ++fi) {
-        const double ja = jump_factor(XA, fi), jb2 = jump_factor(XB, fi);
+#pragma unroll
+    for (int gr = 0; gr < 3; ++gr) {
+      const int ta = ya + 2 - 2 * gr, tb = yb + 2 - 2 * gr;  // the nodes' rows in cell row fj
+      if (ta < 0 || ta > 2 || tb < 0 || tb > 2) continue;
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        if (!T.vv[f][gr]) continue;
+        const double ja = T.jx[f][xa], jb2 = T.jx[f][xb];
         if (ja == 0.0 || jb2 == 0.0) continue;
-        const int ta = YA - 2 * fj, tb = YB - 2 * fj;
-        const double* cw = cwv + s * CW_FACE + ((fi - ki + 2) * 3 + (fj - kj + 1)) * 4;
+        const double* cw = cwv + s * CW_FACE + (f * 3 + gr) * 4;
         double sum = 0.0;
-        for (int q = 0; q < 4; ++q) sum += cw[q] * (ja * c_tab.B[q][ta]) * (jb2 * c_tab.B[q][tb]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sum += cw[q] * (ja * T.B[q][ta]) * (jb2 * T.B[q][tb]);
         val += coef * sum;
       }
+    }
   }
-  // horizontal faces (normal +y) between (fi, fj) and (fi, fj+1)
+  // horizontal faces (normal +y) between (fi, fj) and (fi, fj+1): fj = kj - 2 + f, fi = ki - 1 + gc
   {
     const double h = g.hx, coef = a.ds.gamma_cip * h * h / (g.hy * g.hy);
-    for (int fj = max(0, ceil_half(ymax - 4)); fj <= min(g.ny - 2, floor_half(ymin)); ++fj)
-      for (int fi = max(0, ceil_half(xmax - 2)); fi <= min(g.nx - 1, floor_half(xmin)); ++fi) {
-        const double ja = jump_factor(YA, fj), jb2 = jump_factor(YB, fj);
-        if (ja == 0.0 || jb2 == 0.0) continue;
-        const int ta = XA - 2 * fi, tb = XB - 2 * fi;
-        const double* cw = cwh + s * CW_FACE + ((fj - kj + 2) * 3 + (fi - ki + 1)) * 4;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      const double ja = T.jy[f][ya], jb2 = T.jy[f][yb];
+      if (ja == 0.0 || jb2 == 0.0) continue;
+#pragma unroll
+      for (int gc = 0; gc < 3; ++gc) {
+        const int ta = xa + 2 - 2 * gc, tb = xb + 2 - 2 * gc;  // the nodes' columns in cell column fi
+        if (ta < 0 || ta > 2 || tb < 0 || tb > 2) continue;
+        if (!T.vh[f][gc]) continue;
+        const double* cw = cwh + s * CW_FACE + (f * 3 + gc) * 4;
         double sum = 0.0;
-        for (int q = 0; q < 4; ++q) sum += cw[q] * (ja * c_tab.B[q][ta]) * (jb2 * c_tab.B[q][tb]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sum += cw[q] * (ja * T.B[q][ta]) * (jb2 * T.B[q][tb]);
         val += coef * sum;
       }
+    }
   }
   return val;
 }
@@ -148,25 +199,40 @@ __global__ void __launch_bounds__(448) k_patch_fine(PatchArgs a) {
   const int K = blockIdx.x;
   const int t = threadIdx.x;
   __shared__ double cwv[MAXK1 * CW_FACE], cwh[MAXK1 * CW_FACE];
-  if (a.ds.convection && a.ds.gamma_cip > 0.0) cip_weights(a, K, cwv, cwh);
+  __shared__ PatchTabs tabs;
+  __shared__ double sJ[MAXK1][441];  // the slots' spatial blocks, [i][j]
+  const bool cip = a.ds.convection && a.ds.gamma_cip > 0.0;
+  // Entries are evaluated column-major (consecutive threads = consecutive rows
+  // i: the element matrices are stored [cell][j][i], so their loads coalesce)
+  // and the cell sums are issued before the barrier on the face weights.
+  const int ci_ = t % 21, cj_ = t / 21;
+  double Js[MAXK1];
+  if (t < 441)
+    for (int s = 0; s < a.nslot; ++s) Js[s] = spatial_entry_cells(a, s, K, ci_, cj_);
+  if (cip) {
+    cip_weights(a, K, cwv, cwh);
+    patch_tabs(a.g, K, tabs);
+  }
+  __syncthreads();
+  if (t < 441)
+    for (int s = 0; s < a.nslot; ++s) sJ[s][ci_ * 21 + cj_] = spatial_entry_faces(a, s, ci_, cj_, Js[s], cwv, cwh, tabs);
   __syncthreads();
   if (t >= 441) return;
+  // output, row-major: consecutive threads = consecutive columns j
   const Geom& g = a.g;
   const int i = t / 21, j = t % 21;
   const int k1 = a.td.k1, D = 21 * k1;
+  if (a.spatial) a.spatial[(size_t)K * 441 + t] = sJ[0][t];
+  if (!a.mats) return;  // diagonalized path at scale: the spatial block is all the inverse needs
   double M = 0.0;
   if (i < 18 && j < 18 && (i & 1) == (j & 1)) {
     const int ki = K % g.nx, kj = K / g.nx;
     const int ia = i >> 1, jb = j >> 1;
     M = g.hx * g.hy * (m1g(2 * kj + ia / 3, 2 * kj + jb / 3, g.ny) * m1g(2 * ki + ia % 3, 2 * ki + jb % 3, g.nx));
   }
-  double Js[MAXK1];
-  for (int s = 0; s < a.nslot; ++s) Js[s] = spatial_entry(a, s, K, i, j, cwv, cwh);
-  if (a.spatial) a.spatial[(size_t)K * 441 + t] = Js[0];
-  if (!a.mats) return;  // diagonalized path at scale: the spatial block is all the inverse needs
   double* A = a.mats + (size_t)K * D * D;
   for (int mu = 0; mu < k1; ++mu) {
-    const double J = Js[a.nslot == 1 ? 0 : mu];
+    const double J = sJ[a.nslot == 1 ? 0 : mu][t];
     for (int nu = 0; nu < k1; ++nu) {
       double v = (i < 18 && j < 18) ? a.td.K_t[mu * k1 + nu] * M : 0.0;
       if (mu == nu) v += a.td.tau_w[mu] * J;
