@@ -264,6 +264,15 @@ __global__ void __launch_bounds__(128) k_invert_diag(Geom g, TimeDiag td, const 
   const int ki = K % g.nx, kj = K / g.nx;
   const double lr = td.lam_re[b], li = td.lam_im[b];
   const bool row = lane < N;
+  // the patch's assembled 1-D mass factors between its three node columns /
+  // rows, once per warp (they only differ from the interior values next to
+  // the mesh boundary): m1[0..8] x direction, m1[9..17] y direction
+  __shared__ double m1[WPB][18];
+  if (lane < 9)
+    m1[warp][lane] = m1g_d(2 * ki + lane / 3, 2 * ki + lane % 3, g.nx);
+  else if (lane < 18)
+    m1[warp][lane] = m1g_d(2 * kj + (lane - 9) / 3, 2 * kj + (lane - 9) % 3, g.ny);
+  __syncwarp();
   double2 R[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) {
@@ -271,7 +280,7 @@ __global__ void __launch_bounds__(128) k_invert_diag(Geom g, TimeDiag td, const 
     if (row) {
       if (lane < 18 && j < 18 && (lane & 1) == (j & 1)) {
         const int ia = lane >> 1, jb = j >> 1;
-        m = g.hx * g.hy * (m1g_d(2 * kj + ia / 3, 2 * kj + jb / 3, g.ny) * m1g_d(2 * ki + ia % 3, 2 * ki + jb % 3, g.nx));
+        m = g.hx * g.hy * (m1[warp][9 + 3 * (ia / 3) + jb / 3] * m1[warp][3 * (ia % 3) + jb % 3]);
       }
       jv = spatial[(size_t)K * 441 + lane * N + j];
     }
