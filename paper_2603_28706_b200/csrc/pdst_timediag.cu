@@ -252,7 +252,7 @@ __device__ __forceinline__ double cabs1(double2 z) { return fabs(z.x) + fabs(z.y
 // rounding; after all steps lane p_k holds row k of the inverse with its
 // column k' standing for column p_k' (tableau exchange), undone on the store.
 // Output transposed: binvT[K][b][col][row].
-__global__ void __launch_bounds__(128) k_invert_diag(Geom g, TimeDiag td, const double* __restrict__ spatial,
+__global__ void __launch_bounds__(128, 3) k_invert_diag(Geom g, TimeDiag td, const double* __restrict__ spatial,
                                                      double* __restrict__ binvT, int* __restrict__ bad) {
   constexpr int N = 21, WPB = 4;
   __shared__ double2 prow[WPB][N];  // the current pivot row
