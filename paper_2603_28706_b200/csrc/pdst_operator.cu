@@ -1365,6 +1365,16 @@ __global__ void __launch_bounds__(128, 8) k_jac_post(Geom g, TimeData td, const 
   }
   // 3. the tile pass's sums of node mu
   tile_wait(done + mu, target);
+  // The last epilogue CTA past its waits re-arms the counters (done[5] counts
+  // them): nobody polls any more, and the next apply signals only after this
+  // grid has completed.  Off the critical path: the items follow.
+  if (threadIdx.x == 0) {
+    unsigned long long* cnt = const_cast<unsigned long long*>(done);
+    if (atomicAdd(cnt + 5, 1ull) == (unsigned long long)gridDim.x * gridDim.y - 1) {
+#pragma unroll
+      for (int i = 0; i < 6; ++i) cnt[i] = 0ull;
+    }
+  }
   KTRT(6);
   if (kind == 1 || kind == 2) {
     double s[2];
@@ -1386,17 +1396,6 @@ __global__ void __launch_bounds__(128, 8) k_jac_post(Geom g, TimeData td, const 
       out[o + j] = rhs ? r[j] - s : s;
     }
     KTRT(7);
-  }
-  // the last epilogue CTA of this apply re-arms the counters (done[5] counts finished epilogue CTAs)
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long* cnt = const_cast<unsigned long long*>(done);
-    __threadfence();
-    if (atomicAdd(cnt + 5, 1ull) == (unsigned long long)gridDim.x * gridDim.y - 1) {
-#pragma unroll
-      for (int i = 0; i < 6; ++i) cnt[i] = 0ull;
-      __threadfence();
-    }
   }
 }
 
