@@ -927,16 +927,16 @@ constexpr int APC_SLOTS = APC_VOL + 12;
 // L2 prefetch of half h (0..7: Gauss column h/2, points 2(h%2), 2(h%2)+1) of
 // a node's cache block; h == 8 is the CIP block.
 __device__ __forceinline__ void apc_prefetch_l2(const double* __restrict__ cp, int h, bool hasg = true) {
+  // a warp's half-column is 12 slot rows x 256 bytes = 24 lines: lane l < 24 prefetches line l
+  const int lane = threadIdx.x & 31;
+  const int i = lane >> 1;  // slot row 0..11 of the half-column (or of the CIP block)
+  const double* w0 = cp - lane + 16 * (lane & 1);
   if (h < 8) {
     const int qx = h >> 1, qy0 = (h & 1) * 2;
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int k = 0; k < 6; ++k)
-        if (hasg || k == 0 || k > 3) prefetch_l2(cp + (qx * 24 + k * 4 + qy0 + j) * JNT);
+    const int j = i / 6, k = i - 6 * j;
+    if (lane < 24 && (hasg || k == 0 || k > 3)) prefetch_l2(w0 + (qx * 24 + k * 4 + qy0 + j) * JNT);
   } else if (h == 8) {
-#pragma unroll
-    for (int i = 0; i < 12; ++i) prefetch_l2(cp + (APC_VOL + i) * JNT);
+    if (lane < 24) prefetch_l2(w0 + (APC_VOL + i) * JNT);
   }
 }
 
