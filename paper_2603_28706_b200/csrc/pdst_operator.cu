@@ -872,17 +872,33 @@ struct PlaneS {
 __device__ __forceinline__ void stage_jac_async(const Geom& g, const double* __restrict__ v, int o, int X0, int Y0) {
   const bool al16 = (reinterpret_cast<size_t>(v) & 15) == 0;
   double2* pl = reinterpret_cast<double2*>(g_dsmem + o);
-  for (int idx = threadIdx.x; idx < JNC * JNC; idx += JNT) {
-    const int r = idx / JNC, c = idx - r * JNC;
-    const int X = X0 + c, Y = Y0 + r;
-    const bool in = X >= 0 && X < g.nnx && Y >= 0 && Y < g.nny;
-    const double* src = in ? v + 2 * ((size_t)Y * g.nnx + X) : v;
-    double2* dst = pl + jpidx(r, c);
-    if (al16) {
-      cp_async16(dst, src, in);
-    } else {
+  // node (r, c) of the staged square per thread, advanced by JNT nodes per step without divisions
+  int r = threadIdx.x / JNC, c = threadIdx.x - r * JNC;
+  constexpr int DR = JNT / JNC, DC = JNT - DR * JNC;
+  if (al16) {
+    for (; r < JNC; r += DR) {
+      const int X = X0 + c, Y = Y0 + r;
+      const bool in = X >= 0 && X < g.nnx && Y >= 0 && Y < g.nny;
+      cp_async16(pl + jpidx(r, c), in ? v + 2 * ((size_t)Y * g.nnx + X) : v, in);
+      c += DC;
+      if (c >= JNC) {
+        c -= JNC;
+        ++r;
+      }
+    }
+  } else {
+    for (; r < JNC; r += DR) {
+      const int X = X0 + c, Y = Y0 + r;
+      const bool in = X >= 0 && X < g.nnx && Y >= 0 && Y < g.nny;
+      const double* src = in ? v + 2 * ((size_t)Y * g.nnx + X) : v;
+      double2* dst = pl + jpidx(r, c);
       cp_async8(&dst->x, src, in);
       cp_async8(&dst->y, in ? src + 1 : v, in);
+      c += DC;
+      if (c >= JNC) {
+        c -= JNC;
+        ++r;
+      }
     }
   }
 }
