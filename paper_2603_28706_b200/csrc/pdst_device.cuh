@@ -55,6 +55,29 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     pdst_count_launch();   \
   } while (0)
 
+// Step timeline of profiling builds (-DPDST_TRACE): g_steptrace[4 k + j] for
+// kernel class k (0 apply tile pass, 1 apply epilogue, 2 defect tile pass,
+// 3 defect epilogue, 4 patch GEMV, 5 Vanka scatter), j = 0 first start (min),
+// 1 first past its dependency wait (min), 2 last end (max); %globaltimer ns.
+#ifdef PDST_TRACE
+extern __device__ unsigned long long g_steptrace[32];
+#define STEP_MARK(k, j)                                               \
+  do {                                                                \
+    if ((threadIdx.x & 31) == 0) {                                    \
+      unsigned long long t_;                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));          \
+      if ((j) == 2)                                                   \
+        atomicMax(&g_steptrace[4 * (k) + (j)], t_);                   \
+      else                                                            \
+        atomicMin(&g_steptrace[4 * (k) + (j)], t_);                   \
+    }                                                                 \
+  } while (0)
+#else
+#define STEP_MARK(k, j) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace pdst {
 
 // One-time setup of a launch site, kept PER DEVICE: the dynamic shared-memory

@@ -23,6 +23,10 @@
 #include "pdst_device.cuh"
 #include "pdst_internal.h"
 
+#ifdef PDST_TRACE
+__device__ unsigned long long g_steptrace[32];  // step timeline (pdst_device.cuh STEP_MARK)
+#endif
+
 namespace pdst {
 
 __constant__ Tables c_tab;
@@ -1327,6 +1331,7 @@ __global__ void __launch_bounds__(128, 8) k_jac_post(Geom g, TimeData td, const 
                                                  const unsigned long long* __restrict__ done,
                                                  unsigned long long target, unsigned long long starget) {
   pdl_trigger();  // a PDL-launched consumer (the Vanka GEMV) may start its own prologue
+  STEP_MARK(rhs ? 3 : 1, 0);
   const int mu = blockIdx.y;
   const size_t base = (size_t)mu * g.nd;
   // 1. decode the item (nothing here depends on the other kernels)
@@ -1392,6 +1397,7 @@ __global__ void __launch_bounds__(128, 8) k_jac_post(Geom g, TimeData td, const 
     }
   }
   KTRT(6);
+  if (mu == (int)gridDim.y - 1) STEP_MARK(rhs ? 3 : 1, 1);  // the last node's release
   if (kind == 1 || kind == 2) {
     double s[2];
     if (kind == 2 || on_tile_line(g, X, Y)) {
@@ -1413,6 +1419,7 @@ __global__ void __launch_bounds__(128, 8) k_jac_post(Geom g, TimeData td, const 
     }
     KTRT(7);
   }
+  STEP_MARK(rhs ? 3 : 1, 2);
 }
 
 __host__ __device__ inline size_t jac_post_items(const Geom& g) {
@@ -1455,6 +1462,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
 
   TR(0);
   KTR(0);
+  STEP_MARK(rhs ? 2 : 0, 0);
   // HG == false (Picard, or no viscous term): the a~ slots are zeros and never read
   // The direction's node rows towards L2 before the wait as well: L2 is the
   // point of coherence, so lines the predecessor still writes are updated in
@@ -1471,6 +1479,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
   // read) only after the predecessor has completed; then k_side_products may
   // start under this grid (k_jac_post waits for both)
   pdl_wait();
+  STEP_MARK(rhs ? 2 : 0, 1);
   pdl_trigger();
   // node 0's plane in its own group: its volume and CIP (which read only that
   // plane) start while the other planes land; the temporal mass waits for all
@@ -1739,6 +1748,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
   __syncthreads();
   tile_signal(done + K1 - 1);
   KTR(1);
+  STEP_MARK(rhs ? 2 : 0, 2);
 }
 
 // ---------------------------------------------------------------------------
@@ -2351,6 +2361,11 @@ extern "C" int pdst_debug_trace(unsigned long long* out, int n) {
     e = cudaMemcpyFromSymbol(out + (size_t)8191 * 16, g_ktrace, sizeof(g_ktrace));
     const unsigned long long init[8] = {~0ull, 0ull, ~0ull, 0ull, ~0ull, 0ull, ~0ull, 0ull};
     if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_ktrace, init, sizeof(init));
+    // the step timeline rides in the row before, then resets (min slots to ~0, max slots to 0)
+    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(out + (size_t)8190 * 16, g_steptrace, sizeof(g_steptrace));
+    unsigned long long sinit[32];
+    for (int i = 0; i < 32; ++i) sinit[i] = (i % 4 == 2) ? 0ull : ~0ull;
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_steptrace, sinit, sizeof(sinit));
   }
   return (int)e;
 }

@@ -381,7 +381,9 @@ template <bool VEC>
 __global__ void __launch_bounds__(256, 4) k_vanka_scatter(Geom g, int k1, const double* __restrict__ upd, double omega,
                                                        double* __restrict__ d, int row_lo, int row_hi,
                                                        int inc_only, double* __restrict__ inc_row, int inc_Y) {
+  STEP_MARK(5, 0);
   pdl_wait();  // PDL-launched behind the GEMV that writes upd
+  STEP_MARK(5, 1);
   const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int mu = blockIdx.y;
   if (c >= (size_t)g.ncells) return;
@@ -474,6 +476,7 @@ __global__ void __launch_bounds__(256, 4) k_vanka_scatter(Geom g, int k1, const 
     const double v = me ? omega * pv[j] : 0.0;
     op[j] = inc_only ? v : po[j] + v;
   }
+  STEP_MARK(5, 2);
 }
 
 template <int D>

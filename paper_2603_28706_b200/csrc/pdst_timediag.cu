@@ -448,6 +448,7 @@ __global__ void __launch_bounds__(tma_pb<NB>() * NB * 21, TMA_CTAS_PER_SM) k_van
     upd[(size_t)(21 * mu + r) * g.ncells + K] = sacc;
   };
   pdl_trigger();
+  STEP_MARK(4, 0);
   if (threadIdx.x == 0) {
     for (int st = 0; st < STAGES; ++st) mbar_init(&full[st], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -459,6 +460,7 @@ __global__ void __launch_bounds__(tma_pb<NB>() * NB * 21, TMA_CTAS_PER_SM) k_van
   // launched with PDL: the inverse stream above does not depend on the
   // defect; everything below does (and upd may still be read by a predecessor)
   pdl_wait();
+  STEP_MARK(4, 1);
   {
     double f[K1] = {};
     load_defect(blockIdx.x, f);
@@ -527,6 +529,7 @@ __global__ void __launch_bounds__(tma_pb<NB>() * NB * 21, TMA_CTAS_PER_SM) k_van
       }
     }
   }
+  STEP_MARK(4, 2);
 }
 
 template <int K1, int NB>
