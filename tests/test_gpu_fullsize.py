@@ -146,3 +146,30 @@ def test_cfg3_three_linearizations():
         fd = ((Rp - Rm) / (2 * eps)).reshape(-1)
         errs.append(min(_rel(-fd, out["exn"]), _rel(fd, out["exn"])))
     assert min(errs) <= 1e-6, errs
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_repeated_applies_are_bitwise_reproducible(name):
+    """The apply's epilogue runs under the tile pass behind completion counters
+    (one wave at cfg2, many waves at cfg3): back-to-back applies and defects on
+    one handle, without host synchronization in between, reproduce the first
+    result bit for bit."""
+    import torch
+
+    from paper_2603_28706_b200.operators import SlabJacobian
+
+    cfg, ctx, var, syn, dev = _setup(name)
+    U = torch.as_tensor(syn.U, device=dev)
+    x = torch.as_tensor(syn.x, device=dev)
+    r = torch.as_tensor(syn.d0, device=dev)
+    jac = SlabJacobian(ctx, U, var)
+    y0, d0 = jac.matvec(x).clone(), jac.defect(x, r).clone()
+    y, d = torch.empty_like(x), torch.empty_like(x)
+    bad = torch.zeros((), dtype=torch.int64, device=dev)
+    for _ in range(24):
+        y.zero_()
+        d.zero_()
+        jac.matvec(x, out=y)
+        jac.defect(x, r, out=d)
+        bad += (y != y0).any().long() + (d != d0).any().long()
+    assert int(bad.item()) == 0
