@@ -195,7 +195,7 @@ __device__ double spatial_entry_faces(const PatchArgs& a, int s, int i, int j, d
   return val;
 }
 
-__global__ void __launch_bounds__(448) k_patch_fine(PatchArgs a) {
+__global__ void __launch_bounds__(448, 3) k_patch_fine(PatchArgs a) {
   const int K = blockIdx.x;
   const int t = threadIdx.x;
   __shared__ double cwv[MAXK1 * CW_FACE], cwh[MAXK1 * CW_FACE];
