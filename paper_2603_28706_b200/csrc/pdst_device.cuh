@@ -63,7 +63,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 extern __device__ unsigned long long g_steptrace[32];
 #define STEP_MARK(k, j)                                               \
   do {                                                                \
-    if ((threadIdx.x & 31) == 0) {                                    \
+    if (threadIdx.x == 0) {                                           \
       unsigned long long t_;                                          \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));          \
       if ((j) == 2)                                                   \

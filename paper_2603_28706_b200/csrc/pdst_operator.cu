@@ -2361,8 +2361,8 @@ extern "C" int pdst_debug_trace(unsigned long long* out, int n) {
     e = cudaMemcpyFromSymbol(out + (size_t)8191 * 16, g_ktrace, sizeof(g_ktrace));
     const unsigned long long init[8] = {~0ull, 0ull, ~0ull, 0ull, ~0ull, 0ull, ~0ull, 0ull};
     if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_ktrace, init, sizeof(init));
-    // the step timeline rides in the row before, then resets (min slots to ~0, max slots to 0)
-    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(out + (size_t)8190 * 16, g_steptrace, sizeof(g_steptrace));
+    // the step timeline rides in the two rows before, then resets (min slots to ~0, max slots to 0)
+    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(out + (size_t)8189 * 16, g_steptrace, sizeof(g_steptrace));
     unsigned long long sinit[32];
     for (int i = 0; i < 32; ++i) sinit[i] = (i % 4 == 2) ? 0ull : ~0ull;
     if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_steptrace, sinit, sizeof(sinit));

@@ -37,8 +37,7 @@ for rep in range(9):
     a.record(); step(); b.record()
     torch.cuda.synchronize()
     lib.pdst_debug_trace(buf.ctypes.data_as(ctypes.c_void_p), 8192)
-    st = buf[8190].astype(np.float64)
-    st = np.concatenate([st, buf[8191].astype(np.float64)])[:32] if False else np.frombuffer(buf[8190:8192].tobytes(), dtype=np.uint64)[:32].astype(np.float64)
+    st = np.frombuffer(buf[8189:8191].tobytes(), dtype=np.uint64)[:32].astype(np.float64)
     t0 = st[0]
     rows.append([(st[4 * k + j] - t0) / 1e3 for k in range(6) for j in range(3)] + [a.elapsed_time(b) * 1e3])
 m = np.median(np.array(rows), axis=0)
