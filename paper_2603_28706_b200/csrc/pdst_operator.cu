@@ -848,8 +848,9 @@ constexpr int JNC = 2 * (JT + 2) + 1;
 constexpr int JNC2 = (JNC + 1) / 2;
 constexpr int JRS = 2 * JNC2;
 constexpr int JPLANE = JNC * JRS;
-// The cells' pressure dofs are staged in shared memory with the planes while
-// two CTAs still fit an SM (DG(0), DG(1)); beyond, they are loaded directly.
+// The cells' pressure dofs are staged in shared memory: all Radau nodes with
+// the planes while two CTAs still fit an SM (DG(0), DG(1)); beyond, one node
+// at a time, issued at the start of that node's volume phase.
 __host__ __device__ constexpr bool jac_pstage(int k1) { return k1 <= 2; }
 __host__ __device__ constexpr int jpidx(int r, int c) { return r * JRS + (c & 1) * JNC2 + (c >> 1); }
 
@@ -1437,7 +1438,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
                                                   double* __restrict__ out, double* __restrict__ part,
                                                   unsigned long long* __restrict__ done, const JTabs T) {
   double* sacc = g_dsmem + (size_t)K1 * 2 * JPLANE;  // [18][JNT] per-cell node contributions
-  double* spres = sacc + 18 * JNT;                    // [K1][3][JNT] the cells' pressure dofs (K1 <= 2)
+  double* spres = sacc + 18 * JNT;                    // [K1][3][JNT] the cells' pressure dofs (K1 <= 2), else [3][JNT]
   constexpr bool PSTAGE = jac_pstage(K1);
   // [K1][2][JPLANE] direction x_nu, all Radau nodes (one-cell ring), in front
   const int bx = blockIdx.x, by = blockIdx.y;
@@ -1503,6 +1504,12 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
     double2* slot = reinterpret_cast<double2*>(sacc) + threadIdx.x;  // [9 nodes][JNT] (both components)
     const PlaneS XM{mu * 2 * JPLANE};
     double accp[3] = {0.0, 0.0, 0.0};
+    if (!PSTAGE && valid && ds.pressure && !g.th) {  // this node's pressure dofs, landed by the mass phase
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        cp_async8(spres + (size_t)j * JNT + threadIdx.x, x + (size_t)mu * g.nd + g.mv + 3 * (size_t)c + j, true);
+      cp_async_commit();
+    }
     // CIP, temporal mass and boundary sides accumulate in registers (the
     // volume's registers are free by then) and reach the slot in one pass
     double ra[3][3][2];
@@ -1607,14 +1614,9 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
       // to 1-D Gauss sums (JTabs pA/pB/pM) and stay out of the volume loop.
       if (ds.pressure && !g.th) {  // Taylor-Hood: the pressure coupling is pdst_th.cu's
         const double WT = g.hx * g.hy * tw;
-        double P0, P1, P2;
-        if (PSTAGE) {  // staged with the planes
-          const double* pp = spres + (size_t)mu * 3 * JNT + threadIdx.x;
-          P0 = WT * pp[0], P1 = WT * pp[JNT], P2 = WT * pp[2 * JNT];
-        } else {
-          const double* xp = x + (size_t)mu * g.nd + g.mv + 3 * (size_t)c;
-          P0 = WT * __ldg(xp), P1 = WT * __ldg(xp + 1), P2 = WT * __ldg(xp + 2);
-        }
+        if (!PSTAGE) cp_async_wait_group<0>();  // the own thread's copies of this node
+        const double* pp = spres + (size_t)(PSTAGE ? mu : 0) * 3 * JNT + threadIdx.x;
+        const double P0 = WT * pp[0], P1 = WT * pp[JNT], P2 = WT * pp[2 * JNT];
         // -q div u: rows of x_mu against the 1-D sums
         double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll
@@ -2249,7 +2251,7 @@ __global__ void __launch_bounds__(128) k_boundary_matrices(Geom g, Disc ds, Lin 
 
 template <int K1>
 size_t jac_smem() {
-  return ((size_t)2 * K1 * JPLANE + (size_t)JNT * (18 + (jac_pstage(K1) ? 3 * K1 : 0))) * sizeof(double);
+  return ((size_t)2 * K1 * JPLANE + (size_t)JNT * (18 + (jac_pstage(K1) ? 3 * K1 : 3))) * sizeof(double);
 }
 template <int K1>
 size_t res_smem() {
