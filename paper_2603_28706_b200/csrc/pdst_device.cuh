@@ -160,7 +160,7 @@ struct Lin {
   const double* etad;   // [nbf][4]  lifting viscosity (state independent)
   const double* betad;  // [nbf][4]
   const double* dg;     // [nbf][4][3] sym grad of the lifting
-  const double* bmat;   // [k1][21][21][nbf] boundary-side matrices (rows i, cols j), or null
+  const double* bmat;   // [k1][nbf][21 cols][21 rows] boundary-side matrices (column-major), or null
   const double* apc;    // apply cache (pdst_operator.cu, APC_SLOTS), or null
   int has_gamma;        // 0 for Picard (gamma == 0)
 };

@@ -36,7 +36,7 @@ cudaError_t linearize(const Geom& g, const Model& m, int k1, const double* state
 cudaError_t element_matrices(const Geom& g, const Disc& ds, const Lin& L, int mu, const double* state, double* ET,
                              cudaStream_t st);
 
-// Boundary-side matrices [k1][21][21][nbf] of the current linearization (L.bmat ignored).
+// Boundary-side matrices [k1][nbf][col][row] of the current linearization (L.bmat ignored).
 cudaError_t boundary_matrices(const Geom& g, const Disc& ds, const Lin& L, int k1, const double* state, double* bmat,
                               cudaStream_t st);
 

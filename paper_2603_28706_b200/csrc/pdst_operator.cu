@@ -1227,7 +1227,7 @@ __device__ inline int bcell_index(const Geom& g, int ci, int cj) {
 // Side products of the boundary cells: sp[mu][r][cb] = sum over the cell's
 // boundary faces f (side order, cut faces skipped) of tau w_mu (B_f x_loc)[r],
 // B_f the side matrices of forms.py:605-637 probed once per linearization
-// (k_boundary_matrices, face-contiguous [mu][bf][21][21]).  One warp per
+// (k_boundary_matrices, face-contiguous, column-major [mu][bf][col][row]).  One warp per
 // boundary cell, lane r < 21 computes row r; x_loc is loaded once and
 // broadcast by shuffles.  Depends only on x: launched with PDL behind the tile
 // pass (whose CTAs trigger it after their own wait, so x is complete), its
@@ -1258,10 +1258,10 @@ __global__ void __launch_bounds__(128, 8) k_side_products(Geom g, TimeData td, c
       const bool on = side == 0 ? cj == 0 : side == 1 ? ci == g.nx - 1 : side == 2 ? cj == g.ny - 1 : ci == 0;
       const int bf = side_offset(g, side) + ((side == 0 || side == 2) ? ci : cj);
       if (!on || g.dirichlet[bf] == kCutSide) continue;
-      const double* Br = bmat + ((size_t)mu * g.nbf + bf) * 441 + r * 21;
+      const double* Br = bmat + ((size_t)mu * g.nbf + bf) * 441 + r;  // row r of column-major B_f
       double s = 0.0;
 #pragma unroll
-      for (int col = 0; col < 21; ++col) s = fma(__ldg(Br + col), __shfl_sync(0xffffffffu, xj, col), s);
+      for (int col = 0; col < 21; ++col) s = fma(__ldg(Br + 21 * col), __shfl_sync(0xffffffffu, xj, col), s);
       acc += tw * s;
     }
     if (lane < 21) sp[((size_t)mu * 21 + lane) * ncb + cb] = acc;
@@ -2241,12 +2241,14 @@ __global__ void __launch_bounds__(128) k_boundary_matrices(Geom g, Disc ds, Lin 
     for (int b = 0; b < 3; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   double accp[3] = {0.0, 0.0, 0.0};
   jac_boundary_side(g, ds, L, mu, side, bf, X, S, 0, 0, P, RegAcc{acc}, accp, 1.0);
-  double* col = bmat + ((size_t)mu * g.nbf + bf) * 441 + j;  // [mu][bf][row][col]
+  // column-major [mu][bf][col][row]: this thread's column is contiguous, and the
+  // side products' lanes (one row each) read consecutive doubles per column
+  double* col = bmat + ((size_t)mu * g.nbf + bf) * 441 + (size_t)j * 21;
   for (int a = 0; a < 9; ++a) {
-    col[(2 * a) * 21] = acc[a / 3][a % 3][0];
-    col[(2 * a + 1) * 21] = acc[a / 3][a % 3][1];
+    col[2 * a] = acc[a / 3][a % 3][0];
+    col[2 * a + 1] = acc[a / 3][a % 3][1];
   }
-  for (int r = 0; r < 3; ++r) col[(18 + r) * 21] = accp[r];
+  for (int r = 0; r < 3; ++r) col[18 + r] = accp[r];
 }
 
 template <int K1>
