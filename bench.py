@@ -416,9 +416,12 @@ def run_ours(args):
     traffic = traffic_apply = None
     import glob
 
-    tps = sorted(glob.glob(os.path.join(ROOT, "profiles", "traffic_r*.json")))  # the latest round's capture
+    # dram bytes per launch, one ncu capture per config (scripts/ncu_traffic.py): the latest round's file,
+    # profiles/traffic_rNN.json for cfg2 and profiles/traffic_<config>_rNN.json for the others
+    pat = "traffic_r*.json" if args.config == "cfg2" else f"traffic_{args.config}_r*.json"
+    tps = sorted(glob.glob(os.path.join(ROOT, "profiles", pat)))
     tp = tps[-1] if tps else ""
-    if tp and args.config == "cfg2":  # dram bytes per launch, one ncu capture at cfg2 (scripts/ncu_traffic.py)
+    if tp:
         try:
             tr = json.load(open(tp))
             traffic, traffic_apply = tr.get("vanka_gemv"), tr.get("jacobian_apply")

@@ -8,6 +8,12 @@ mkdir -p gpurun_out
 timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
   -k regex:"k_(jac|side|vanka)" --csv python scripts/prof_step.py cfg2 3 > gpurun_out/traffic_$TAG.csv 2> gpurun_out/traffic_$TAG.err
 python scripts/ncu_traffic.py gpurun_out/traffic_$TAG.csv profiles/traffic_$TAG.json > /dev/null && cp profiles/traffic_$TAG.json gpurun_out/traffic_$TAG.json
+for c in cfg3 cfg5; do  # the larger configs' traffic (read by bench.py --config)
+  timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+    -k regex:"k_(jac|side|vanka)" --csv python scripts/prof_step.py $c 2 > gpurun_out/traffic_${c}_$TAG.csv 2> gpurun_out/traffic_${c}_$TAG.err
+  python scripts/ncu_traffic.py gpurun_out/traffic_${c}_$TAG.csv profiles/traffic_${c}_$TAG.json "scripts/prof_step.py $c 2" > /dev/null \
+    && cp profiles/traffic_${c}_$TAG.json gpurun_out/traffic_${c}_$TAG.json
+done
 bash scripts/round_profiles.sh $TAG
 for c in cfg3 cfg5; do
   timeout 900 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${c}_$TAG.log 2>&1
