@@ -1144,7 +1144,8 @@ __device__ __forceinline__ void cip_all_w(const JTabs& T, const Geom& g, const F
 }
 
 // ---------------------------------------------------------------------------
-// Apply epilogue (one kernel, PDL-launched behind k_jacobian): the nodes the
+// Apply epilogue (k_side_products + k_jac_post, PDL-launched behind the tile
+// pass and released per Radau node by its completion counters): the nodes the
 // tile pass cannot finish alone.
 //   * tile-line nodes (shared by 2 or 4 tiles): sum of the tiles' partials;
 //   * boundary-strip nodes (in a cell with a boundary side) and the pressures
@@ -1154,7 +1155,7 @@ __device__ __forceinline__ void cip_all_w(const JTabs& T, const Geom& g, const F
 // The tile pass writes these dofs without the right-hand side; here
 // y = rhs - s or y = s with s = (interior sum) + (side terms), summed in a
 // fixed order, so apply and defect agree bitwise.  The side products depend
-// only on x and are evaluated before the wait on the tile pass.
+// only on x and run under the tile pass.
 // ---------------------------------------------------------------------------
 __host__ __device__ inline bool in_strip(const Geom& g, int X, int Y) {
   return X <= 2 || Y <= 2 || X >= g.nnx - 3 || Y >= g.nny - 3;
@@ -1478,7 +1479,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
     for (int h = 0; h < PDST_PF_AHEAD; ++h) apc_prefetch_l2(cbase, h, HG);
   // launched with PDL: x (and the scratch the predecessor's epilogue may still
   // read) only after the predecessor has completed; then k_side_products may
-  // start under this grid (k_jac_post waits for both)
+  // start under this grid (k_jac_post polls both kernels' completion counters)
   pdl_wait();
   STEP_MARK(rhs ? 2 : 0, 1);
   pdl_trigger();
