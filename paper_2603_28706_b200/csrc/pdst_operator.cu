@@ -1615,7 +1615,7 @@ __global__ void __launch_bounds__(JNT, 65536 / (JNT * 128)) k_jacobian(Geom g, T
       // to 1-D Gauss sums (JTabs pA/pB/pM) and stay out of the volume loop.
       if (ds.pressure && !g.th) {  // Taylor-Hood: the pressure coupling is pdst_th.cu's
         const double WT = g.hx * g.hy * tw;
-        if (!PSTAGE) cp_async_wait_group<0>();  // the own thread's copies of this node
+        cp_async_wait_group<0>();  // the own thread's copies (this node's; DG(0) has no wait on its second staging group)
         const double* pp = spres + (size_t)(PSTAGE ? mu : 0) * 3 * JNT + threadIdx.x;
         const double P0 = WT * pp[0], P1 = WT * pp[JNT], P2 = WT * pp[2 * JNT];
         // -q div u: rows of x_mu against the 1-D sums
