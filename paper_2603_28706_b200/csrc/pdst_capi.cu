@@ -396,6 +396,8 @@ int pdst_linearize(pdst_handle* h, const double* U, int kind, double sigma_max, 
     if (!apc) return fail(PDST_ECUDA, "out of device memory");
     CK(apply_cache(g, h->td, h->ds, L, st, apc, h->stream));
   }
+  if (h->jpart.ptr && h->jpart.cap >= jacobian_scratch(g, k1))  // (allocated by the first apply)
+    CK(jacobian_reset_counters(g, k1, h->jpart.ptr, h->stream));
   h->linearized = true;
   h->patches_valid = false;
   if (where == PDST_HOST) CK(cudaStreamSynchronize(h->stream));

@@ -13,6 +13,8 @@ Tables host_tables();
 // y = J x (rhs == null) or y = rhs - J x; `part` holds jacobian_scratch() doubles, zero when
 // first used (its tail holds the apply's completion counters, which every apply leaves at zero).
 size_t jacobian_scratch(const Geom& g, int k1);
+// Re-zero the completion counters at the tail of `part` (called per linearization).
+cudaError_t jacobian_reset_counters(const Geom& g, int k1, double* part, cudaStream_t st);
 // Requires the linearization's boundary matrices (L.bmat) and apply cache (L.apc).
 cudaError_t jacobian_apply(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* x,
                            const double* rhs, double* out, double* part, cudaStream_t st);

@@ -2383,6 +2383,12 @@ size_t jacobian_scratch(const Geom& g, int k1) {
   return (size_t)k1 * jac_tiles_x(g) * jac_tiles_y(g) * JPER * 2 + (size_t)k1 * 21 * n_bcells(g) + 8;
 }
 
+cudaError_t jacobian_reset_counters(const Geom& g, int k1, double* part, cudaStream_t st) {
+  // the 8 trailing words of the scratch (every completed apply leaves them at zero; an apply cut
+  // short by a device error would not)
+  return cudaMemsetAsync(part + jacobian_scratch(g, k1) - 8, 0, 8 * sizeof(double), st);
+}
+
 cudaError_t jacobian_apply(const Geom& g, const TimeData& td, const Disc& ds, const Lin& L, const double* x,
                            const double* rhs, double* out, double* part, cudaStream_t st) {
   switch (td.k1) {
