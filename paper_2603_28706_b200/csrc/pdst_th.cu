@@ -8,11 +8,14 @@
 //   J:  y_v += tau w_mu G' x_p,   y_p  = tau w_mu G x_v,
 //   R:  R_v -= tau w_mu G' pi,    R_p  = tau w_mu (N(g_hat) - G v),
 // with G the Q1-vertex x Q2-velocity operator of b (oracle/th_oracle.py).
-// Two deterministic kernels: k_th_cell evaluates each cell's 18 + 4
-// contributions (4x4 Gauss volume points, 4 points per Dirichlet side) into a
-// structure-of-arrays buffer, k_th_gather sums the <= 4 cells of every
-// velocity node and pressure vertex in a fixed order.  Pressure vertices are
-// row-major (y, x), (nx+1)(ny+1) per Radau node after the velocity block.
+// On the uniform rectangles of this mesh the volume part of G is ONE 4 x 18
+// cell matrix, separable into 1-D Gauss sums (ThTabs), so no quadrature loop
+// and no per-cell buffer: k_th_gather gives every velocity node and pressure
+// vertex the products of its <= 4 cells directly from x, in a fixed (row,
+// column) order.  Only cells with a Dirichlet side carry more — the boundary
+// terms, evaluated per boundary cell by k_th_sides into a small buffer that
+// the gather adds.  Pressure vertices are row-major (y, x), (nx+1)(ny+1) per
+// Radau node after the velocity block.
 #include <cuda_runtime.h>
 
 #include "../../include/pdst.h"
@@ -33,14 +36,58 @@ __device__ __forceinline__ bool side_on(const Geom& g, int side, int ci, int cj,
   return on && g.dirichlet[bf] == 1;
 }
 
-// cb[(mu * THN + i) * nc + c]: i < 18 the velocity row 2a + d of (G' p)_cell,
-// i >= 18 the vertex row 2 jy + jx of (G u)_cell - N(g_hat)_cell.
-__global__ void k_th_cell(Geom g, int k1, const double* __restrict__ x, const double* __restrict__ ghat,
-                          double* __restrict__ cb) {
+// 1-D Gauss sums of the Q1 x Q2 coupling on the reference interval:
+//   D[j][i] = sum_q w_q psi_j(s_q) L_i'(s_q),  M[j][i] = sum_q w_q psi_j(s_q) L_i(s_q),
+// psi_0 = 1 - s, psi_1 = s.  The cell matrix of -(psi_J, d_d phi_a):
+//   d = 0: -hy D[jx][ix] M[jy][iy],   d = 1: -hx M[jx][ix] D[jy][iy]   (area / h_d).
+struct ThTabs {
+  double G[4][9][2];  // the cell matrix itself, mesh scales folded in (kernel parameter: constant-bank operands)
+};
+__device__ __forceinline__ double th_g(const ThTabs& T, const Geom&, int J, int a, int d) { return T.G[J][a][d]; }
+
+// Boundary cells: bottom row, top row, then the left / right cells of the rows
+// between (every cell when the mesh is one cell wide or tall).
+__host__ __device__ inline size_t th_nbcells(const Geom& g) {
+  return g.nx == 1 || g.ny == 1 ? (size_t)g.ncells : (size_t)2 * g.nx + 2 * (g.ny - 2);
+}
+__device__ inline void th_bcell_of(const Geom& g, size_t t, int& ci, int& cj) {
+  if (g.nx == 1 || g.ny == 1) {
+    ci = (int)(t % g.nx), cj = (int)(t / g.nx);
+  } else if (t < (size_t)g.nx) {
+    ci = (int)t, cj = 0;
+  } else if (t < (size_t)2 * g.nx) {
+    ci = (int)(t - g.nx), cj = g.ny - 1;
+  } else {
+    const size_t u = t - 2 * (size_t)g.nx;
+    cj = 1 + (int)(u / 2), ci = (u & 1) ? g.nx - 1 : 0;
+  }
+}
+__device__ inline int th_bcell_index(const Geom& g, int ci, int cj) {
+  if (g.nx == 1 || g.ny == 1) return cj * g.nx + ci;
+  if (cj == 0) return ci;
+  if (cj == g.ny - 1) return g.nx + ci;
+  if (ci == 0) return 2 * g.nx + 2 * (cj - 1);
+  if (ci == g.nx - 1) return 2 * g.nx + 2 * (cj - 1) + 1;
+  return -1;
+}
+
+// Dirichlet-side terms of boundary cell cb: +<p, phi_a . n> and
+// +<(u - g_hat) . n, psi_j>, 4 Gauss points per side.
+// sb[(mu * THN + i) * ncb + cb]: i < 18 the velocity row 2a + d, i >= 18 the vertex row 2 jy + jx.
+__global__ void k_th_sides(Geom g, int k1, const double* __restrict__ x, const double* __restrict__ ghat,
+                           double* __restrict__ sb) {
+  // PDL-launched behind the velocity apply without a dependency wait: it reads only x (complete since
+  // the apply's tile pass passed its own wait) and writes sb, which the previous gather has released
+  pdl_trigger();
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int mu = blockIdx.y;
-  if (t >= (size_t)g.ncells) return;
-  const int c = (int)t, ci = c % g.nx, cj = c / g.nx;
+  const size_t ncb = th_nbcells(g);
+  if (t >= ncb) {
+    pdl_wait();
+    return;
+  }
+  int ci, cj;
+  th_bcell_of(g, t, ci, cj);
   const double* xm = x + (size_t)mu * g.nd;
   double u[9][2], p[4];
 #pragma unroll
@@ -56,31 +103,6 @@ __global__ void k_th_cell(Geom g, int k1, const double* __restrict__ x, const do
   for (int a = 0; a < 9; ++a) vo[a][0] = vo[a][1] = 0.0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) po[j] = 0.0;
-  const double area = g.hx * g.hy;
-  // ---- volume: -(p, div phi_a) and -(div u, psi_j) ----
-#pragma unroll
-  for (int qx = 0; qx < 4; ++qx) {
-#pragma unroll
-    for (int qy = 0; qy < 4; ++qy) {
-      const double sx = c_tab.s[qx], sy = c_tab.s[qy];
-      const double w = c_tab.w[qx] * c_tab.w[qy] * area;
-      double pq = 0.0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) pq = fma(q1v(j & 1, sx) * q1v(j >> 1, sy), p[j], pq);
-      double div = 0.0;
-#pragma unroll
-      for (int a = 0; a < 9; ++a) {
-        const int ix = a % 3, iy = a / 3;
-        const double dx = c_tab.G[qx][ix] * c_tab.B[qy][iy] * g.ihx, dy = c_tab.B[qx][ix] * c_tab.G[qy][iy] * g.ihy;
-        div = fma(dx, u[a][0], fma(dy, u[a][1], div));
-        vo[a][0] = fma(-w * pq, dx, vo[a][0]);
-        vo[a][1] = fma(-w * pq, dy, vo[a][1]);
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) po[j] = fma(-w * div, q1v(j & 1, sx) * q1v(j >> 1, sy), po[j]);
-    }
-  }
-  // ---- Dirichlet sides: +<p, phi_a . n> and +<(u - g_hat) . n, psi_j> ----
   for (int side = 0; side < 4; ++side) {
     int bf;
     if (!side_on(g, side, ci, cj, bf)) continue;
@@ -116,50 +138,112 @@ __global__ void k_th_cell(Geom g, int k1, const double* __restrict__ x, const do
       for (int j = 0; j < 4; ++j) po[j] = fma(wf * (un - gn), q1v(j & 1, xh) * q1v(j >> 1, yh), po[j]);
     }
   }
-  const size_t nc = g.ncells;
-  double* o = cb + (size_t)mu * THN * nc + c;
+  double* o = sb + (size_t)mu * THN * ncb + t;
 #pragma unroll
   for (int a = 0; a < 9; ++a) {
-    o[(2 * a) * nc] = vo[a][0];
-    o[(2 * a + 1) * nc] = vo[a][1];
+    o[(2 * a) * ncb] = vo[a][0];
+    o[(2 * a + 1) * ncb] = vo[a][1];
   }
 #pragma unroll
-  for (int j = 0; j < 4; ++j) o[(18 + j) * nc] = po[j];
+  for (int j = 0; j < 4; ++j) o[(18 + j) * ncb] = po[j];
+  // this grid completes only after its predecessor (the velocity apply's epilogue) has: the
+  // gather waits for this grid alone and adds to the y that epilogue finishes
+  pdl_wait();
 }
 
-// y_v += sgn tau w_mu sum_cells cb_v (velocity nodes), y_p = sgn tau w_mu
-// sum_cells cb_p (vertices; scale 0 writes zeros), cells in (row, column)
-// order.
-__global__ void k_th_gather(Geom g, TimeData td, const double* __restrict__ cb, double sgn, int on,
-                            double* __restrict__ y) {
+// y_v += sgn tau w_mu sum_cells (G' x_p)_cell (velocity nodes), y_p = sgn tau
+// w_mu sum_cells (G x_v)_cell (vertices; `on` = 0 writes zeros).  One thread
+// per pressure vertex (ci, cj), 0 <= ci <= nx, 0 <= cj <= ny: it finishes the
+// vertex and the <= 4 velocity nodes (2 ci + {0,1}, 2 cj + {0,1}) from the
+// cells (ci - 1 .. ci, cj - 1 .. cj) around it, so every local index below is
+// a compile-time constant; each cell's volume part comes from the separable
+// cell matrix and, for boundary cells, its side terms from sb; cells in (row,
+// column) order.
+__global__ void __launch_bounds__(128) k_th_gather(Geom g, TimeData td, ThTabs T, const double* __restrict__ x,
+                                                   const double* __restrict__ sb, double sgn, int on,
+                                                   double* __restrict__ y) {
+  pdl_trigger();
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int mu = blockIdx.y;
-  const size_t nn = (size_t)g.nnx * g.nny, nv = (size_t)(g.nx + 1) * (g.ny + 1), nc = g.ncells;
+  const size_t nv = (size_t)(g.nx + 1) * (g.ny + 1), ncb = th_nbcells(g);
+  pdl_wait();  // the side terms and, through them, the velocity apply that y already holds
+  if (t >= nv) return;
+  const int ci = (int)(t % (g.nx + 1)), cj = (int)(t / (g.nx + 1));
   const double sc = on ? sgn * td.tau_w[mu] : 0.0;
-  const double* cm = cb + (size_t)mu * THN * nc;
+  const double* xm = x + (size_t)mu * g.nd;
+  const double* sm = sb + (size_t)mu * THN * ncb;
   double* ym = y + (size_t)mu * g.nd;
-  if (t < nn) {
-    if (!on) return;
-    const int X = (int)(t % g.nnx), Y = (int)(t / g.nnx);
-    double s0 = 0.0, s1 = 0.0;
-    for (int cy = max(0, (Y - 1) / 2); cy <= min(g.ny - 1, Y / 2); ++cy)
-      for (int cx = max(0, (X - 1) / 2); cx <= min(g.nx - 1, X / 2); ++cx) {
-        const int a = 3 * (Y - 2 * cy) + (X - 2 * cx);
-        const size_t c = (size_t)cy * g.nx + cx;
-        s0 += cm[(2 * a) * nc + c];
-        s1 += cm[(2 * a + 1) * nc + c];
-      }
-    ym[2 * t] += sc * s0;
-    ym[2 * t + 1] += sc * s1;
-  } else if (t < nn + nv) {
-    const size_t v = t - nn;
-    const int i = (int)(v % (g.nx + 1)), j = (int)(v / (g.nx + 1));
-    double s = 0.0;
-    for (int cy = max(0, j - 1); cy <= min(g.ny - 1, j); ++cy)
-      for (int cx = max(0, i - 1); cx <= min(g.nx - 1, i); ++cx)
-        s += cm[(18 + 2 * (j - cy) + (i - cx)) * nc + (size_t)cy * g.nx + cx];
-    ym[g.mv + v] = sc * s;
+  // the four cells around the vertex: k = 2 dy + dx -> cell (ci - 1 + dx, cj - 1 + dy)
+  bool has[4];
+  int cbi[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int cx = ci - 1 + (k & 1), cy = cj - 1 + (k >> 1);
+    has[k] = cx >= 0 && cx < g.nx && cy >= 0 && cy < g.ny;
+    cbi[k] = has[k] ? th_bcell_index(g, cx, cy) : -1;
   }
+  double pv = 0.0;  // the vertex row, cells in (row, column) order
+  if (on) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (!has[k]) continue;
+      const int cx = ci - 1 + (k & 1), cy = cj - 1 + (k >> 1);
+      const int J = 3 - k;  // the vertex's index in that cell: 2 (cj - cy) + (ci - cx)
+      double c = 0.0;
+#pragma unroll
+      for (int a = 0; a < 9; ++a) {
+        const size_t o = 2 * ((size_t)(2 * cy + a / 3) * g.nnx + 2 * cx + a % 3);
+        c = fma(th_g(T, g, J, a, 0), __ldg(xm + o), c);  // (nd may be odd: no 16-byte load)
+        c = fma(th_g(T, g, J, a, 1), __ldg(xm + o + 1), c);
+      }
+      if (cbi[k] >= 0) c += sm[(size_t)(18 + J) * ncb + cbi[k]];
+      pv += c;
+    }
+  }
+  ym[g.mv + t] = sc * pv;
+  if (!on) return;
+  // pressures of the 3 x 3 vertices around (ci, cj) (0 outside the mesh; never used there)
+  double p[3][3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int vi = ci - 1 + c, vj = cj - 1 + r;
+      p[r][c] = (vi >= 0 && vi <= g.nx && vj >= 0 && vj <= g.ny) ? __ldg(xm + g.mv + (size_t)vj * (g.nx + 1) + vi) : 0.0;
+    }
+  // velocity node (2 ci + ex, 2 cj + ey): the cells containing it among the four, with its local index there
+  auto node = [&](int ex, int ey) {
+    if ((ex && ci == g.nx) || (ey && cj == g.ny)) return;  // beyond the mesh's last node column / row
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int dx = k & 1, dy = k >> 1;
+      if ((ex && !dx) || (ey && !dy)) continue;  // an odd node lies inside the right / upper cells only
+      if (!has[k]) continue;
+      // local node index in cell k: x position 2 - 2 dx + ex, y position 2 - 2 dy + ey
+      const int a = 3 * (2 - 2 * dy + ey) + (2 - 2 * dx + ex);
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int J = 0; J < 4; ++J) {
+        const double pj = p[dy + (J >> 1)][dx + (J & 1)];  // vertex (cx + jx, cy + jy)
+        c0 = fma(th_g(T, g, J, a, 0), pj, c0);
+        c1 = fma(th_g(T, g, J, a, 1), pj, c1);
+      }
+      if (cbi[k] >= 0) {
+        c0 += sm[(size_t)(2 * a) * ncb + cbi[k]];
+        c1 += sm[(size_t)(2 * a + 1) * ncb + cbi[k]];
+      }
+      s0 += c0;
+      s1 += c1;
+    }
+    double* yo = ym + 2 * ((size_t)(2 * cj + ey) * g.nnx + 2 * ci + ex);
+    yo[0] += sc * s0;
+    yo[1] += sc * s1;
+  };
+  node(0, 0);
+  node(1, 0);
+  node(0, 1);
+  node(1, 1);
 }
 
 // y_p = tau w_mu M_p x_p, consistent Q1 mass hx hy M1_y (x) M1_x,
@@ -186,24 +270,56 @@ __global__ void k_th_pmass(Geom g, TimeData td, const double* __restrict__ x, do
 
 }  // namespace
 
+static ThTabs th_tabs(const Geom& g) {
+  // 4-point Gauss sums, the points / weights / Q2 values of the device tables
+  static const Tables tab = host_tables();
+  double D[2][3], M[2][3];
+  for (int j = 0; j < 2; ++j)
+    for (int i = 0; i < 3; ++i) {
+      double d = 0.0, m = 0.0;
+      for (int q = 0; q < 4; ++q) {
+        const double psi = j ? tab.s[q] : 1.0 - tab.s[q];
+        d += tab.w[q] * psi * tab.G[q][i];
+        m += tab.w[q] * psi * tab.B[q][i];
+      }
+      D[j][i] = d;
+      M[j][i] = m;
+    }
+  ThTabs T;
+  for (int J = 0; J < 4; ++J)
+    for (int a = 0; a < 9; ++a) {
+      const int jx = J & 1, jy = J >> 1, ix = a % 3, iy = a / 3;
+      T.G[J][a][0] = -g.hy * (D[jx][ix] * M[jy][iy]);
+      T.G[J][a][1] = -g.hx * (M[jx][ix] * D[jy][iy]);
+    }
+  return T;
+}
+
+static cudaError_t th_coupling(const Geom& g, const TimeData& td, bool on, const double* x, const double* ghat,
+                               double sgn, double* y, double* sb, cudaStream_t st) {
+  const ThTabs T = th_tabs(g);
+  const size_t ncb = th_nbcells(g);
+  cudaError_t e = cudaSuccess;
+  if (on)
+    PDST_LAUNCH(e = launch_pdl(k_th_sides, dim3((unsigned)((ncb + 127) / 128), td.k1), dim3(128), 0, st, g, td.k1, x,
+                               ghat, sb));
+  if (e != cudaSuccess) return e;
+  const size_t nv = (size_t)(g.nx + 1) * (g.ny + 1);
+  PDST_LAUNCH(e = launch_pdl(k_th_gather, dim3((unsigned)((nv + 127) / 128), td.k1), dim3(128), 0, st, g, td, T, x,
+                             (const double*)sb, sgn, on ? 1 : 0, y));
+  return e;
+}
+
 // J: y (velocity rows already J_vel x) += [tau w G' x_p ; tau w G x_v]
 cudaError_t th_apply(const Geom& g, const TimeData& td, bool on, const double* x, double* y, double* cb,
                      cudaStream_t st) {
-  dim3 gc((unsigned)((g.ncells + 127) / 128), td.k1);
-  if (on) PDST_LAUNCH(k_th_cell<<<gc, 128, 0, st>>>(g, td.k1, x, nullptr, cb));
-  const size_t n = (size_t)g.nnx * g.nny + (size_t)(g.nx + 1) * (g.ny + 1);
-  PDST_LAUNCH(k_th_gather<<<dim3((unsigned)((n + 255) / 256), td.k1), 256, 0, st>>>(g, td, cb, 1.0, on ? 1 : 0, y));
-  return cudaGetLastError();
+  return th_coupling(g, td, on, x, nullptr, 1.0, y, cb, st);
 }
 
 // R: R_v -= tau w G' pi, R_p = tau w (N(g_hat) - G v)
 cudaError_t th_residual(const Geom& g, const TimeData& td, bool on, const double* U, const double* ghat, double* R,
                         double* cb, cudaStream_t st) {
-  dim3 gc((unsigned)((g.ncells + 127) / 128), td.k1);
-  if (on) PDST_LAUNCH(k_th_cell<<<gc, 128, 0, st>>>(g, td.k1, U, ghat, cb));
-  const size_t n = (size_t)g.nnx * g.nny + (size_t)(g.nx + 1) * (g.ny + 1);
-  PDST_LAUNCH(k_th_gather<<<dim3((unsigned)((n + 255) / 256), td.k1), 256, 0, st>>>(g, td, cb, -1.0, on ? 1 : 0, R));
-  return cudaGetLastError();
+  return th_coupling(g, td, on, U, ghat, -1.0, R, cb, st);
 }
 
 cudaError_t th_pressure_mass(const Geom& g, const TimeData& td, const double* x, double* y, cudaStream_t st) {
@@ -212,6 +328,6 @@ cudaError_t th_pressure_mass(const Geom& g, const TimeData& td, const double* x,
   return cudaGetLastError();
 }
 
-size_t th_scratch(const Geom& g, int k1) { return (size_t)k1 * THN * g.ncells; }
+size_t th_scratch(const Geom& g, int k1) { return (size_t)k1 * THN * th_nbcells(g); }  // boundary cells' side terms
 
 }  // namespace pdst
