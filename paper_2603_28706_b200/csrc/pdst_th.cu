@@ -159,20 +159,36 @@ __global__ void k_th_sides(Geom g, int k1, const double* __restrict__ x, const d
 // a compile-time constant; each cell's volume part comes from the separable
 // cell matrix and, for boundary cells, its side terms from sb; cells in (row,
 // column) order.
-__global__ void __launch_bounds__(128) k_th_gather(Geom g, TimeData td, ThTabs T, const double* __restrict__ x,
-                                                   const double* __restrict__ sb, double sgn, int on,
-                                                   double* __restrict__ y) {
+constexpr int TG_BW = 32, TG_BH = 4;                             // vertices per CTA (x, y)
+constexpr int TG_NC = 2 * TG_BW + 3, TG_NR = 2 * TG_BH + 3;      // staged velocity nodes: the block's cells' nodes
+__global__ void __launch_bounds__(TG_BW * TG_BH) k_th_gather(Geom g, TimeData td, ThTabs T,
+                                                             const double* __restrict__ x,
+                                                             const double* __restrict__ sb, double sgn, int on,
+                                                             double* __restrict__ y) {
   pdl_trigger();
-  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ __align__(16) double us[TG_NR][2 * TG_NC + 2];  // x's velocity nodes (2 ci0 - 2 .., 2 cj0 - 2 ..), components interleaved
+  const int nbx = (g.nx + 1 + TG_BW - 1) / TG_BW;
+  const int bx = blockIdx.x % nbx, by = blockIdx.x / nbx;
   const int mu = blockIdx.y;
-  const size_t nv = (size_t)(g.nx + 1) * (g.ny + 1), ncb = th_nbcells(g);
-  pdl_wait();  // the side terms and, through them, the velocity apply that y already holds
-  if (t >= nv) return;
-  const int ci = (int)(t % (g.nx + 1)), cj = (int)(t / (g.nx + 1));
+  const int lx = threadIdx.x % TG_BW, ly = threadIdx.x / TG_BW;
+  const int ci = bx * TG_BW + lx, cj = by * TG_BH + ly;
+  const size_t ncb = th_nbcells(g);
   const double sc = on ? sgn * td.tau_w[mu] : 0.0;
   const double* xm = x + (size_t)mu * g.nd;
   const double* sm = sb + (size_t)mu * THN * ncb;
   double* ym = y + (size_t)mu * g.nd;
+  {  // coalesced staging of the node patch (zero outside the mesh); x does not depend on the predecessors
+    const int X0 = 2 * bx * TG_BW - 2, Y0 = 2 * by * TG_BH - 2;
+    for (int idx = threadIdx.x; idx < TG_NR * 2 * TG_NC; idx += TG_BW * TG_BH) {
+      const int r = idx / (2 * TG_NC), c2 = idx - r * (2 * TG_NC);
+      const int X = X0 + (c2 >> 1), Y = Y0 + r;
+      us[r][c2] = (X >= 0 && X < g.nnx && Y >= 0 && Y < g.nny) ? __ldg(xm + 2 * ((size_t)Y * g.nnx + X) + (c2 & 1)) : 0.0;
+    }
+  }
+  __syncthreads();
+  pdl_wait();  // the side terms and, through them, the velocity apply that y already holds
+  if (ci > g.nx || cj > g.ny) return;
+  const size_t t = (size_t)cj * (g.nx + 1) + ci;
   // the four cells around the vertex: k = 2 dy + dx -> cell (ci - 1 + dx, cj - 1 + dy)
   bool has[4];
   int cbi[4];
@@ -187,14 +203,15 @@ __global__ void __launch_bounds__(128) k_th_gather(Geom g, TimeData td, ThTabs T
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       if (!has[k]) continue;
-      const int cx = ci - 1 + (k & 1), cy = cj - 1 + (k >> 1);
       const int J = 3 - k;  // the vertex's index in that cell: 2 (cj - cy) + (ci - cx)
+      // the cell's node (0, 0) in the staged patch: row 2 ly + 2 dy, column 2 lx + 2 dx
+      const int r0 = 2 * ly + 2 * (k >> 1), c0 = 2 * lx + 2 * (k & 1);
       double c = 0.0;
 #pragma unroll
       for (int a = 0; a < 9; ++a) {
-        const size_t o = 2 * ((size_t)(2 * cy + a / 3) * g.nnx + 2 * cx + a % 3);
-        c = fma(th_g(T, g, J, a, 0), __ldg(xm + o), c);  // (nd may be odd: no 16-byte load)
-        c = fma(th_g(T, g, J, a, 1), __ldg(xm + o + 1), c);
+        const double2 uu = *reinterpret_cast<const double2*>(&us[r0 + a / 3][2 * (c0 + a % 3)]);
+        c = fma(th_g(T, g, J, a, 0), uu.x, c);
+        c = fma(th_g(T, g, J, a, 1), uu.y, c);
       }
       if (cbi[k] >= 0) c += sm[(size_t)(18 + J) * ncb + cbi[k]];
       pv += c;
@@ -304,8 +321,8 @@ static cudaError_t th_coupling(const Geom& g, const TimeData& td, bool on, const
     PDST_LAUNCH(e = launch_pdl(k_th_sides, dim3((unsigned)((ncb + 127) / 128), td.k1), dim3(128), 0, st, g, td.k1, x,
                                ghat, sb));
   if (e != cudaSuccess) return e;
-  const size_t nv = (size_t)(g.nx + 1) * (g.ny + 1);
-  PDST_LAUNCH(e = launch_pdl(k_th_gather, dim3((unsigned)((nv + 127) / 128), td.k1), dim3(128), 0, st, g, td, T, x,
+  const unsigned nblk = (unsigned)(((g.nx + 1 + TG_BW - 1) / TG_BW) * ((g.ny + 1 + TG_BH - 1) / TG_BH));
+  PDST_LAUNCH(e = launch_pdl(k_th_gather, dim3(nblk, td.k1), dim3(TG_BW * TG_BH), 0, st, g, td, T, x,
                              (const double*)sb, sgn, on ? 1 : 0, y));
   return e;
 }
