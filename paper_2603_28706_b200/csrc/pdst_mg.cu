@@ -548,11 +548,17 @@ static int level_defect(pdst_handle* h, int l, const double* x, const double* r,
 }
 
 // `steps` Vanka steps on level l, d updated in place (device pointers).
-static int vanka_level(pdst_handle* h, int l, double* d, const double* r, int steps, double omega) {
+// zero_start: d is to be taken as zero whatever it holds (the V-cycle's and
+// the coarse solvers' smoothing from a zero guess, multigrid.py:545-555): the
+// first step's defect r - A 0 is r itself and its update is the increment, so
+// that step needs neither the operator apply nor a cleared d (the same values
+// as the full step up to the sign of zeros).
+static int vanka_level(pdst_handle* h, int l, double* d, const double* r, int steps, double omega,
+                       bool zero_start = false) {
   Level* lv = h->levels[l];
   if (lv->child) {  // rediscretized level: the child's exact patches
     lv->child->stream = h->stream;
-    return vanka_level(lv->child, 0, d, r, steps, omega);
+    return vanka_level(lv->child, 0, d, r, steps, omega, zero_start);
   }
   const Geom& g = lv->g;
   const int k1 = h->td.k1;
@@ -560,14 +566,20 @@ static int vanka_level(pdst_handle* h, int l, double* d, const double* r, int st
   double* defect = h->defect.ensure(std::max(n, (size_t)k1 * h->g.nd));
   double* upd = h->upd.ensure((size_t)h->g.ncells * 21 * k1);
   if (!defect || !upd) return set_error(PDST_ECUDA, "out of device memory");
+  if (zero_start && steps == 0) CK(cudaMemsetAsync(d, 0, n * sizeof(double), h->stream));
   for (int s = 0; s < steps; ++s) {
-    if (int e = level_defect(h, l, d, r, defect)) return e;
+    const bool from_zero = zero_start && s == 0;
+    const double* e_in = defect;
+    if (from_zero)
+      e_in = r;
+    else if (int e = level_defect(h, l, d, r, defect))
+      return e;
     if (lv->diag)
-      CK(PDST_TIMED(h, PK_VANKA_GEMV, vanka_gemv_diag(g, lv->tdiag, lv->binv.ptr,
-                                                       defect, upd, h->stream)));
+      CK(PDST_TIMED(h, PK_VANKA_GEMV, vanka_gemv_diag(g, lv->tdiag, lv->binv.ptr, e_in, upd, h->stream)));
     else
-      CK(PDST_TIMED(h, PK_VANKA_GEMV, vanka_gemv(g, k1, lv->invs.ptr, defect, upd, h->stream)));
-    CK(PDST_TIMED(h, PK_VANKA_SCATTER, vanka_scatter(g, k1, upd, omega, d, h->stream)));
+      CK(PDST_TIMED(h, PK_VANKA_GEMV, vanka_gemv(g, k1, lv->invs.ptr, e_in, upd, h->stream)));
+    // from zero: d = omega sum_K R_K' upd_K (every dof written), else d += ...
+    CK(PDST_TIMED(h, PK_VANKA_SCATTER, vanka_scatter(g, k1, upd, omega, d, h->stream, 0, -1, from_zero)));
   }
   return PDST_OK;
 }
@@ -729,8 +741,7 @@ static int coarse_fgmres(pdst_handle* h, const double* b, double* z) {
   for (int j = 0; j < m; ++j) {
     double* Vj = V + (size_t)j * n;
     double* Zj = Z + (size_t)j * n;
-    CK(cudaMemsetAsync(Zj, 0, n * sizeof(double), h->stream));
-    if (int e = vanka_level(h, 0, Zj, Vj, h->coarse_sweeps, h->coarse_omega)) return e;
+    if (int e = vanka_level(h, 0, Zj, Vj, h->coarse_sweeps, h->coarse_omega, true)) return e;
     // w = A_0 z_j (the matrix-free Jacobian when level 0 is the handle's own mesh)
     if (int e = level_defect(h, 0, Zj, nullptr, w)) return e;
     for (int pass = 0; pass < 2; ++pass) {  // CGS2
@@ -789,8 +800,7 @@ static int vcycle_level(pdst_handle* h, int l, const double* b, double* z, int p
   if (l == 0) {
     if (h->coarse_iterative) {
       if (h->coarse_kind == PDST_COARSE_VANKA) {  // Vanka steps from zero on the coarsest level
-        CK(cudaMemsetAsync(z, 0, n * sizeof(double), h->stream));
-        return vanka_level(h, 0, z, b, h->coarse_sweeps, h->coarse_omega);
+        return vanka_level(h, 0, z, b, h->coarse_sweeps, h->coarse_omega, true);
       }
       return coarse_fgmres(h, b, z);
     }
@@ -801,8 +811,7 @@ static int vcycle_level(pdst_handle* h, int l, const double* b, double* z, int p
   const Geom& gc = lc->g;
   double* r = lv == h->levels.back() ? h->scratch_d.ensure(n) : lv->w1.ptr;
   if (!r) return set_error(PDST_ECUDA, "out of device memory");
-  CK(cudaMemsetAsync(z, 0, n * sizeof(double), h->stream));
-  if (int e = vanka_level(h, l, z, b, pre, omega)) return e;
+  if (int e = vanka_level(h, l, z, b, pre, omega, true)) return e;  // (clears z itself when pre == 0)
   if (int e = level_defect(h, l, z, b, r)) return e;
   CK(PDST_TIMED(h, PK_TRANSFER, restrict_(gc, lv->g, k1, r, lc->w0.ptr, h->stream)));
   if (int e = vcycle_level(h, l - 1, lc->w0.ptr, lc->w2.ptr, pre, post, omega)) return e;
