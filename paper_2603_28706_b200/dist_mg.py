@@ -182,12 +182,18 @@ class DistributedStmg:
 # ---------------------------------------------------------------------------
 
 
-def _vanka_steps(ranks, f, ds, rs, steps, omega, transport):
-    """`steps` additive Vanka steps on level f (multigrid.py:327-340), owner computes."""
+def _vanka_steps(ranks, f, ds, rs, steps, omega, transport, zero_start=False):
+    """`steps` additive Vanka steps on level f (multigrid.py:327-340), owner computes.
+    zero_start: the iterates ds are zero (the V-cycle's and the coarse solver's
+    smoothing from a zero guess), so the first step's defect r - A 0 is r itself:
+    no halo exchange of d and no operator apply for it (as libpdst's vanka_level)."""
     k1 = ranks[0].k1
-    for _ in range(steps):
-        transport.exchange(ds, "halo_recv", k1, level=f)
-        defects = [rk.defect(f, d, r) for rk, d, r in zip(ranks, ds, rs)]
+    for s in range(steps):
+        if zero_start and s == 0:
+            defects = [r.clone() for r in rs]
+        else:
+            transport.exchange(ds, "halo_recv", k1, level=f)
+            defects = [rk.defect(f, d, r) for rk, d, r in zip(ranks, ds, rs)]
         transport.exchange(defects, "defect_recv", k1, level=f)
         incs = [rk.increment(f, df, omega) for rk, df in zip(ranks, defects)]
         transport.exchange(incs, "inc_recv", k1, add=True, level=f)
@@ -229,7 +235,8 @@ def _coarse_fgmres(ranks, bs, transport, comm):
     k = 0
     for j in range(m):
         zj = [rk.zeros(f) for rk in ranks]
-        _vanka_steps(ranks, f, zj, [Vr[j] for Vr in V], ranks[0].coarse_sweeps, ranks[0].coarse_omega, transport)
+        _vanka_steps(ranks, f, zj, [Vr[j] for Vr in V], ranks[0].coarse_sweeps, ranks[0].coarse_omega, transport,
+                     zero_start=True)
         for Zr, z, mk in zip(Z, zj, masks):
             Zr[j] = z * mk
         transport.exchange(zj, "halo_recv", k1, level=f)
@@ -272,7 +279,7 @@ def _cycle(ranks, f, bs, transport, comm, pre, post, omega):
     if f == ranks[0].levels - 1:
         return _coarse_fgmres(ranks, bs, transport, comm)
     zs = [rk.zeros(f) for rk in ranks]
-    _vanka_steps(ranks, f, zs, bs, pre, omega, transport)
+    _vanka_steps(ranks, f, zs, bs, pre, omega, transport, zero_start=True)
     transport.exchange(zs, "halo_recv", k1, level=f)
     res = [rk.defect(f, z, b) * rk.masks[f] for rk, z, b in zip(ranks, zs, bs)]
     rc = [rk.restrict(f, r) for rk, r in zip(ranks, res)]
