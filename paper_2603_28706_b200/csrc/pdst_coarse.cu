@@ -187,67 +187,84 @@ __device__ __forceinline__ double cell_entry(const LevelOp& op, int mu, int c, i
   return op.ecell[base + (size_t)j * 21 + i];
 }
 
+// The four children's local prolongation blocks, the same for every cell:
+// evaluated once per device (k_pm_init) instead of once per CTA.
+__device__ double g_pm[4 * 441];
+__global__ void k_pm_init() {
+  for (int idx = threadIdx.x; idx < 4 * 441; idx += blockDim.x) {
+    const int k = idx / 441, e = idx % 441;
+    g_pm[idx] = ploc(k & 1, k >> 1, e / 21, e % 21);
+  }
+}
+
 // Galerkin coarse cell block: one CTA (448 threads) per (coarse cell, mu).
-__global__ void __launch_bounds__(448) k_galerkin_cells(LevelOp f, Geom gc, double* __restrict__ ecell_c) {
+__global__ void __launch_bounds__(448, 3) k_galerkin_cells(LevelOp f, Geom gc, double* __restrict__ ecell_c) {
   __shared__ double T[21][22];
   __shared__ double Pm[4][21][21];
-  __shared__ double F[9][10];
+  __shared__ double Es[441];  // the child's element block, column-major (staged with coalesced loads)
+  __shared__ double FB[16][9][10];  // the interior fine faces' node blocks
   const int C = blockIdx.x, mu = blockIdx.y;
   const int t = threadIdx.x;
   const int ci = C % gc.nx, cj = C / gc.nx;
-  for (int idx = t; idx < 4 * 441; idx += blockDim.x) {
-    const int k = idx / 441, e = idx % 441;
-    Pm[k][e / 21][e % 21] = ploc(k & 1, k >> 1, e / 21, e % 21);
-  }
+  for (int idx = t; idx < 4 * 441; idx += blockDim.x) (&Pm[0][0][0])[idx] = g_pm[idx];
   const int i = t / 21, j = t % 21;
   double acc = 0.0;
-  __syncthreads();
   for (int k = 0; k < 4; ++k) {
     const int ox = k & 1, oy = k >> 1;
     const int K = (2 * cj + oy) * f.g.nx + 2 * ci + ox;
+    if (t < 441) Es[t] = f.ecell[((size_t)mu * f.g.ncells + K) * 441 + t];
+    __syncthreads();  // (also orders Pm on the first pass and the previous child's reads of T)
     // T = E_K P_K  (rows = child dofs, cols = parent dofs)
     if (t < 441) {
       double s = 0.0;
-      for (int m = 0; m < 21; ++m) s = fma(cell_entry(f, mu, K, i, m), Pm[k][m][j], s);
+#pragma unroll
+      for (int m = 0; m < 21; ++m) s = fma(Es[m * 21 + i], Pm[k][m][j], s);
       T[i][j] = s;
     }
     __syncthreads();
     if (t < 441) {
       double s = 0.0;
+#pragma unroll
       for (int m = 0; m < 21; ++m) s = fma(Pm[k][m][i], T[m][j], s);
       acc += s;
     }
-    __syncthreads();
+    // (the next pass's barrier after staging Es separates these reads of T from its writes)
   }
-  // fine faces interior to C: vertical (children (0,oy)|(1,oy)), horizontal ((ox,0)|(ox,1))
-  for (int fidx = 0; fidx < 4; ++fidx) {
-    const int axis = fidx < 2 ? 0 : 1;
-    const int o = fidx & 1;
-    const int kl = axis == 0 ? (o * 2 + 0) : (0 * 2 + o);  // child index k = ox + 2 oy of the left/lower cell
-    const int kr = axis == 0 ? (o * 2 + 1) : (1 * 2 + o);
+  __syncthreads();
+  // fine faces interior to C: vertical (children (0,oy)|(1,oy)), horizontal ((ox,0)|(ox,1)).
+  // All 16 (face, side, side) node blocks are evaluated first, by all threads, then summed
+  // without further barriers.
+  for (int idx = t; idx < 16 * 81; idx += blockDim.x) {
+    const int blk = idx / 81, e = idx - 81 * blk;
+    const int fidx = blk >> 2, sA = (blk >> 1) & 1, sB = blk & 1;
+    const int axis = fidx < 2 ? 0 : 1, o = fidx & 1;
     const int fi = 2 * ci + (axis == 0 ? 0 : o), fj = 2 * cj + (axis == 0 ? o : 0);
-    for (int sA = 0; sA < 2; ++sA)
-      for (int sB = 0; sB < 2; ++sB) {
-        if (t < 81) F[t / 9][t % 9] = face_entry(f, mu, axis, fi, fj, sA, t / 9, sB, t % 9);
-        __syncthreads();
-        if (t < 441 && i < 18 && j < 18) {
+    FB[blk][e / 9][e % 9] = face_entry(f, mu, axis, fi, fj, sA, e / 9, sB, e % 9);
+  }
+  __syncthreads();
+  if (t < 441 && i < 18 && j < 18 && (i & 1) == (j & 1)) {
+    const int d = i & 1;  // I2: component d of i and j must agree
+    for (int fidx = 0; fidx < 4; ++fidx) {
+      const int axis = fidx < 2 ? 0 : 1;
+      const int o = fidx & 1;
+      const int kl = axis == 0 ? (o * 2 + 0) : (0 * 2 + o);  // child index k = ox + 2 oy of the left/lower cell
+      const int kr = axis == 0 ? (o * 2 + 1) : (1 * 2 + o);
+      for (int sA = 0; sA < 2; ++sA)
+        for (int sB = 0; sB < 2; ++sB) {
           const int kA = sA == 0 ? kl : kr, kB = sB == 0 ? kl : kr;
-          // sum_{a,b} P_kA[2a+d][i] F[a][b] P_kB[2b+d][j]  (I2: component d of i and j must agree)
-          if ((i & 1) == (j & 1)) {
-            const int d = i & 1;
-            double s = 0.0;
-            for (int a = 0; a < 9; ++a) {
-              const double pa = Pm[kA][2 * a + d][i];
-              if (pa == 0.0) continue;
-              double sb = 0.0;
-              for (int b = 0; b < 9; ++b) sb = fma(F[a][b], Pm[kB][2 * b + d][j], sb);
-              s = fma(pa, sb, s);
-            }
-            acc += s;
+          const double (*Fb)[10] = FB[fidx * 4 + sA * 2 + sB];
+          // sum_{a,b} P_kA[2a+d][i] F[a][b] P_kB[2b+d][j]
+          double s = 0.0;
+          for (int a = 0; a < 9; ++a) {
+            const double pa = Pm[kA][2 * a + d][i];
+            if (pa == 0.0) continue;
+            double sb = 0.0;
+            for (int b = 0; b < 9; ++b) sb = fma(Fb[a][b], Pm[kB][2 * b + d][j], sb);
+            s = fma(pa, sb, s);
           }
+          acc += s;
         }
-        __syncthreads();
-      }
+    }
   }
   if (t < 441) ecell_c[((size_t)mu * gc.ncells + C) * 441 + (size_t)j * 21 + i] = acc;  // column-major
 }
@@ -662,23 +679,45 @@ __global__ void k_dense_gemv(const double* __restrict__ Ainv, int n, const doubl
 }
 
 // Remove the mass-weighted mean of the constant pressure mode per node
-// (multigrid.py:557-572); one CTA per Radau node.
-__global__ void k_project_pressure(Geom g, double* __restrict__ z) {
-  __shared__ double sh[1024];
-  const int mu = blockIdx.x;
-  double* p = z + (size_t)mu * g.nd + g.mv;
-  const double area_c = g.hx * g.hy;
-  double s = 0.0;
-  for (int c = threadIdx.x; c < g.ncells; c += blockDim.x) s = fma(area_c, p[3 * (size_t)c], s);
-  sh[threadIdx.x] = s;
+// (multigrid.py:557-572).  Two passes over the cells with a fixed reduction
+// tree (PP_PARTS partial sums per node, summed in order by every CTA of the
+// second pass), so the result does not depend on scheduling.
+constexpr int PP_PARTS = 592, PP_NT = 256;
+__device__ __forceinline__ double pp_block_sum(double v, double* sh) {
+  sh[threadIdx.x] = v;
   __syncthreads();
-  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
-    if (threadIdx.x < off) sh[threadIdx.x] += sh[threadIdx.x + off];
+  for (int off = PP_NT / 2; off > 0; off >>= 1) {
+    if ((int)threadIdx.x < off) sh[threadIdx.x] += sh[threadIdx.x + off];
     __syncthreads();
   }
-  const double mean = sh[0] / (area_c * g.ncells);
+  const double r = sh[0];
   __syncthreads();
-  for (int c = threadIdx.x; c < g.ncells; c += blockDim.x) p[3 * (size_t)c] -= mean;
+  return r;
+}
+__global__ void __launch_bounds__(PP_NT) k_project_partial(Geom g, const double* __restrict__ z,
+                                                          double* __restrict__ partial) {
+  __shared__ double sh[PP_NT];
+  const int mu = blockIdx.y;
+  const double* p = z + (size_t)mu * g.nd + g.mv;
+  const double area_c = g.hx * g.hy;
+  const size_t chunk = ((size_t)g.ncells + PP_PARTS - 1) / PP_PARTS;
+  const size_t c0 = (size_t)blockIdx.x * chunk, c1 = min(c0 + chunk, (size_t)g.ncells);
+  double s = 0.0;
+  for (size_t c = c0 + threadIdx.x; c < c1; c += PP_NT) s = fma(area_c, p[3 * c], s);
+  s = pp_block_sum(s, sh);
+  if (threadIdx.x == 0) partial[(size_t)mu * PP_PARTS + blockIdx.x] = s;
+}
+__global__ void __launch_bounds__(PP_NT) k_project_apply(Geom g, const double* __restrict__ partial,
+                                                        double* __restrict__ z) {
+  __shared__ double sh[PP_NT];
+  const int mu = blockIdx.y;
+  double* p = z + (size_t)mu * g.nd + g.mv;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < PP_PARTS; i += PP_NT) s += partial[(size_t)mu * PP_PARTS + i];
+  s = pp_block_sum(s, sh);
+  const double mean = s / ((g.hx * g.hy) * g.ncells);
+  const size_t c = (size_t)blockIdx.x * PP_NT + threadIdx.x;
+  if (c < (size_t)g.ncells) p[3 * c] -= mean;
 }
 
 __global__ void k_axpy(size_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
@@ -702,6 +741,16 @@ cudaError_t restrict_(const Geom& gc, const Geom& gf, int k1, const double* rf, 
 
 cudaError_t galerkin(const LevelOp& fine, const Geom& gc, int k1, double* ecell_c, double* fv_c, double* fh_c,
                      cudaStream_t st) {
+  {
+    static DeviceOnce once;
+    const int dev = current_device();
+    if (!once.done[dev]) {
+      PDST_LAUNCH(k_pm_init<<<1, 448, 0, st>>>());
+      cudaError_t e0 = cudaStreamSynchronize(st);  // once: other streams' builds may follow at once
+      if (e0 != cudaSuccess) return e0;
+      once.done[dev] = true;
+    }
+  }
   PDST_LAUNCH(k_galerkin_cells<<<dim3(gc.ncells, k1), 448, 0, st>>>(fine, gc, ecell_c));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -757,8 +806,13 @@ cudaError_t dense_solve(const double* Ainv, int n, const double* b, double* y, c
   return cudaGetLastError();
 }
 
-cudaError_t project_pressure(const Geom& g, int k1, double* z, cudaStream_t st) {
-  PDST_LAUNCH(k_project_pressure<<<k1, 1024, 0, st>>>(g, z));
+size_t project_scratch(int k1) { return (size_t)k1 * PP_PARTS; }
+
+cudaError_t project_pressure(const Geom& g, int k1, double* z, double* partial, cudaStream_t st) {
+  PDST_LAUNCH(k_project_partial<<<dim3(PP_PARTS, k1), PP_NT, 0, st>>>(g, z, partial));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  PDST_LAUNCH(k_project_apply<<<dim3((unsigned)((g.ncells + PP_NT - 1) / PP_NT), k1), PP_NT, 0, st>>>(g, partial, z));
   return cudaGetLastError();
 }
 

@@ -35,7 +35,9 @@ cudaError_t patch_assemble_level(const LevelOp& op, const TimeData& td, double* 
 cudaError_t dense_build(const LevelOp& op, const TimeData& td, bool pin, double* A, double* scratch, int* piv,
                         int* bad, cudaStream_t st);
 cudaError_t dense_solve(const double* Ainv, int n, const double* b, double* y, cudaStream_t st);
-cudaError_t project_pressure(const Geom& g, int k1, double* z, cudaStream_t st);
+// `partial`: project_scratch(k1) doubles of scratch.
+size_t project_scratch(int k1);
+cudaError_t project_pressure(const Geom& g, int k1, double* z, double* partial, cudaStream_t st);
 cudaError_t axpy(size_t n, double a, const double* x, double* y, cudaStream_t st);
 // Node injection (multigrid.py:146-153 inject_v, used by coarse_mode
 // "rediscretize", :406-418): coarse node (i, j) <- fine node (2i, 2j), both

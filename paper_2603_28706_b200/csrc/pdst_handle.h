@@ -161,6 +161,7 @@ struct pdst_handle {
   pdst::DeviceBuffer scratch_a, scratch_b, scratch_c, scratch_d, scratch_f;
   pdst::DeviceBuffer partials;
   pdst::DeviceBuffer kpartials;  // FGMRES multi-dot partial sums
+  pdst::DeviceBuffer ppartials;  // mean-pressure projection partial sums
   pdst::DeviceBuffer jpart;  // Jacobian tile-boundary partial sums (+ the tile pass's completion counters)
 
   // surrogate (representative-state) linearization and patch scratch

@@ -861,7 +861,11 @@ int pdst_vcycle(pdst_handle* h, const double* r, double* z, int pre, int post, d
   double* zd = out_ptr(h->scratch_b, z, n, where);
   if (!zd) return set_error(PDST_ECUDA, "out of device memory");
   if (int e = vcycle_level(h, L - 1, rd, zd, pre, post, omega)) return e;
-  if (h->levels.back()->all_dirichlet) CK(project_pressure(h->g, h->td.k1, zd, h->stream));
+  if (h->levels.back()->all_dirichlet) {
+    double* pp = h->ppartials.ensure(project_scratch(h->td.k1));
+    if (!pp) return set_error(PDST_ECUDA, "out of device memory");
+    CK(project_pressure(h->g, h->td.k1, zd, pp, h->stream));
+  }
   return finish_out(h, z, zd, n, where);
 }
 
