@@ -478,13 +478,22 @@ __device__ double level_spatial_entry(const LevelOp& op, int mu, int K, int i, i
 }
 
 // Exact coarse patches: A_K = sum K_t (x) R_K M R_K' + tau w_mu R_K J_mu R_K'.
-__global__ void __launch_bounds__(448) k_patch_level(LevelOp op, TimeData td, double* __restrict__ mats) {
+// The spatial entries are evaluated column-major (consecutive threads =
+// consecutive rows i: the element and face blocks are stored column-major, so
+// their loads coalesce), staged in shared memory, and written row-major.
+__global__ void __launch_bounds__(448, 3) k_patch_level(LevelOp op, TimeData td, double* __restrict__ mats) {
+  __shared__ double sJ[MAXK1][441];  // [mu][i * 21 + j]
   const int K = blockIdx.x;
   const int t = threadIdx.x;
-  if (t >= 441) return;
   const Geom& g = op.g;
-  const int i = t / 21, j = t % 21;
   const int k1 = td.k1, D = 21 * k1;
+  if (t < 441) {
+    const int ci_ = t % 21, cj_ = t / 21;
+    for (int mu = 0; mu < k1; ++mu) sJ[mu][ci_ * 21 + cj_] = level_spatial_entry(op, mu, K, ci_, cj_);
+  }
+  __syncthreads();
+  if (t >= 441) return;
+  const int i = t / 21, j = t % 21;
   double M = 0.0;
   if (i < 18 && j < 18 && (i & 1) == (j & 1)) {
     const int ki = K % g.nx, kj = K / g.nx;
@@ -493,7 +502,7 @@ __global__ void __launch_bounds__(448) k_patch_level(LevelOp op, TimeData td, do
   }
   double* A = mats + (size_t)K * D * D;
   for (int mu = 0; mu < k1; ++mu) {
-    const double J = level_spatial_entry(op, mu, K, i, j);
+    const double J = sJ[mu][t];
     for (int nu = 0; nu < k1; ++nu) {
       double v = (i < 18 && j < 18) ? td.K_t[mu * k1 + nu] * M : 0.0;
       if (mu == nu) v += td.tau_w[mu] * J;
