@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(448, 3) k_galerkin_cells(LevelOp f, Geom gc, d
 
 // Galerkin coarse face blocks from the two fine faces lying on the coarse face.
 // One CTA (324 threads: sA, sB, a, b) per (coarse face, mu); axis via blockIdx.z.
-__global__ void __launch_bounds__(324) k_galerkin_faces(LevelOp f, Geom gc, double* __restrict__ fv_c,
+__global__ void __launch_bounds__(324, 4) k_galerkin_faces(LevelOp f, Geom gc, double* __restrict__ fv_c,
                                                         double* __restrict__ fh_c) {
   __shared__ double Pn[4][9][9];  // node-level prolongation of child k: Pn[k][a_fine][b_coarse]
   __shared__ double F[2][2][9][9];
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(324) k_galerkin_faces(LevelOp f, Geom gc, doub
   const int t = threadIdx.x;
   for (int idx = t; idx < 4 * 81; idx += blockDim.x) {
     const int k = idx / 81, e = idx % 81;
-    Pn[k][e / 9][e % 9] = ploc(k & 1, k >> 1, 2 * (e / 9), 2 * (e % 9));
+    Pn[k][e / 9][e % 9] = g_pm[k * 441 + (2 * (e / 9)) * 21 + 2 * (e % 9)];  // (k_pm_init ran with the cell kernel)
   }
   const int sA = t / 162, sB = (t / 81) % 2, a = (t / 9) % 9, b = t % 9;
   double acc = 0.0;
