@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(448, 3) k_galerkin_cells(LevelOp f, Geom gc, d
   __shared__ double Pm[4][21][21];
   __shared__ double Es[441];  // the child's element block, column-major (staged with coalesced loads)
   __shared__ double FB[16][9][10];  // the interior fine faces' node blocks
+  __shared__ double SB[8][9][18];   // their products with the prolongation, 8 blocks at a time
   const int C = blockIdx.x, mu = blockIdx.y;
   const int t = threadIdx.x;
   const int ci = C % gc.nx, cj = C / gc.nx;
@@ -242,29 +243,39 @@ __global__ void __launch_bounds__(448, 3) k_galerkin_cells(LevelOp f, Geom gc, d
     FB[blk][e / 9][e % 9] = face_entry(f, mu, axis, fi, fj, sA, e / 9, sB, e % 9);
   }
   __syncthreads();
-  if (t < 441 && i < 18 && j < 18 && (i & 1) == (j & 1)) {
-    const int d = i & 1;  // I2: component d of i and j must agree
-    for (int fidx = 0; fidx < 4; ++fidx) {
-      const int axis = fidx < 2 ? 0 : 1;
-      const int o = fidx & 1;
-      const int kl = axis == 0 ? (o * 2 + 0) : (0 * 2 + o);  // child index k = ox + 2 oy of the left/lower cell
-      const int kr = axis == 0 ? (o * 2 + 1) : (1 * 2 + o);
-      for (int sA = 0; sA < 2; ++sA)
-        for (int sB = 0; sB < 2; ++sB) {
-          const int kA = sA == 0 ? kl : kr, kB = sB == 0 ? kl : kr;
-          const double (*Fb)[10] = FB[fidx * 4 + sA * 2 + sB];
-          // sum_{a,b} P_kA[2a+d][i] F[a][b] P_kB[2b+d][j]
-          double s = 0.0;
-          for (int a = 0; a < 9; ++a) {
-            const double pa = Pm[kA][2 * a + d][i];
-            if (pa == 0.0) continue;
-            double sb = 0.0;
-            for (int b = 0; b < 9; ++b) sb = fma(Fb[a][b], Pm[kB][2 * b + d][j], sb);
-            s = fma(pa, sb, s);
-          }
-          acc += s;
-        }
+  // sum_{a,b} P_kA[2a+d][i] F[a][b] P_kB[2b+d][j] per block, factored: the inner sums
+  // SB[a][j] = sum_b F[a][b] P_kB[2b+d][j] do not depend on i, so they are formed once per
+  // (block, a, j) — 8 blocks at a time — and every (i, j) pair then needs 9 terms per block
+  // instead of 90 (same products and order as the unfactored double loop).
+  for (int half = 0; half < 2; ++half) {
+    for (int idx = t; idx < 8 * 9 * 18; idx += blockDim.x) {
+      const int bl = idx / 162, a = (idx / 18) % 9, jv = idx % 18, d = jv & 1;
+      const int blk = 8 * half + bl, fidx = blk >> 2, sB = blk & 1;
+      const int axis = fidx < 2 ? 0 : 1, o = fidx & 1;
+      const int kl = axis == 0 ? (o * 2 + 0) : (0 * 2 + o), kr = axis == 0 ? (o * 2 + 1) : (1 * 2 + o);
+      const int kB = sB == 0 ? kl : kr;
+      double sb = 0.0;
+      for (int b = 0; b < 9; ++b) sb = fma(FB[blk][a][b], Pm[kB][2 * b + d][jv], sb);
+      SB[bl][a][jv] = sb;
     }
+    __syncthreads();
+    if (t < 441 && i < 18 && j < 18 && (i & 1) == (j & 1)) {
+      const int d = i & 1;  // I2: component d of i and j must agree
+      for (int bl = 0; bl < 8; ++bl) {
+        const int blk = 8 * half + bl, fidx = blk >> 2, sA = (blk >> 1) & 1;
+        const int axis = fidx < 2 ? 0 : 1, o = fidx & 1;
+        const int kl = axis == 0 ? (o * 2 + 0) : (0 * 2 + o), kr = axis == 0 ? (o * 2 + 1) : (1 * 2 + o);
+        const int kA = sA == 0 ? kl : kr;  // child index k = ox + 2 oy of the left/lower (sA = 0) or right/upper cell
+        double sacc = 0.0;
+        for (int a = 0; a < 9; ++a) {
+          const double pa = Pm[kA][2 * a + d][i];
+          if (pa == 0.0) continue;
+          sacc = fma(pa, SB[bl][a][j], sacc);
+        }
+        acc += sacc;
+      }
+    }
+    __syncthreads();
   }
   if (t < 441) ecell_c[((size_t)mu * gc.ncells + C) * 441 + (size_t)j * 21 + i] = acc;  // column-major
 }
