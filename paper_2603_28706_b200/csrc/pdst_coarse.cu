@@ -286,6 +286,7 @@ __global__ void __launch_bounds__(324, 4) k_galerkin_faces(LevelOp f, Geom gc, d
                                                         double* __restrict__ fh_c) {
   __shared__ double Pn[4][9][9];  // node-level prolongation of child k: Pn[k][a_fine][b_coarse]
   __shared__ double F[2][2][9][9];
+  __shared__ double SBf[2][2][9][9];
   const int axis = blockIdx.z, mu = blockIdx.y;
   const int nfx = axis == 0 ? gc.nx - 1 : gc.nx;
   const int nface = axis == 0 ? (gc.nx - 1) * gc.ny : gc.nx * (gc.ny - 1);
@@ -307,15 +308,21 @@ __global__ void __launch_bounds__(324, 4) k_galerkin_faces(LevelOp f, Geom gc, d
     __syncthreads();
     if (t < 324) F[sA][sB][a][b] = face_entry(f, mu, axis, ffi, ffj, sA, a, sB, b);
     __syncthreads();
+    // factored: SBf[sA][sB][p][b] = sum_q F[sA][sB][p][q] Pn[kB][q][b] once per (p, b), thread (a, b) playing (p, b)
     if (t < 324) {
-      const int kA = sA == 0 ? kl : kr, kB = sB == 0 ? kl : kr;
+      const int kB = sB == 0 ? kl : kr;
+      double sb = 0.0;
+      for (int q = 0; q < 9; ++q) sb = fma(F[sA][sB][a][q], Pn[kB][q][b], sb);
+      SBf[sA][sB][a][b] = sb;
+    }
+    __syncthreads();
+    if (t < 324) {
+      const int kA = sA == 0 ? kl : kr;
       double s = 0.0;
       for (int p = 0; p < 9; ++p) {
         const double pa = Pn[kA][p][a];
         if (pa == 0.0) continue;
-        double sb = 0.0;
-        for (int q = 0; q < 9; ++q) sb = fma(F[sA][sB][p][q], Pn[kB][q][b], sb);
-        s = fma(pa, sb, s);
+        s = fma(pa, SBf[sA][sB][p][b], s);
       }
       acc += s;
     }
