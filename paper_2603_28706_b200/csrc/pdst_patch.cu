@@ -299,11 +299,17 @@ __global__ void __launch_bounds__(128) k_invert(const double* __restrict__ mats,
     for (int jj = lane; jj < D; jj += 32) A[k * LD + jj] = (jj == k ? 1.0 : A[k * LD + jj]) * pivinv;
     for (int i = lane; i < D; i += 32) col[i] = A[i * LD + k];
     __syncwarp();
-    for (int idx = lane; idx < D * D; idx += 32) {
-      const int i = idx / D, jj = idx - i * D;
-      if (i == k) continue;
-      const double base = (jj == k) ? 0.0 : A[i * LD + jj];
-      A[i * LD + jj] = base - col[i] * A[k * LD + jj];
+    // a lane takes whole columns: the pivot-row entry stays in a register, no index division,
+    // conflict-free column accesses (same arithmetic per entry as an entry-wise sweep)
+    for (int jj = lane; jj < D; jj += 32) {
+      const double pk = A[k * LD + jj];
+      const bool pc = jj == k;
+#pragma unroll 6
+      for (int i = 0; i < D; ++i) {
+        if (i == k) continue;
+        const double base = pc ? 0.0 : A[i * LD + jj];
+        A[i * LD + jj] = base - col[i] * pk;
+      }
     }
     __syncwarp();
   }
