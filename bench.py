@@ -769,7 +769,8 @@ def run_solve(args):
         "config": {"workload": f"{cfg.name}: {cfg.nx}x{cfg.ny} Q2/P1disc, DG({cfg.k}), p={cfg.p}, delta={cfg.delta}, "
                                f"nu_inf={cfg.nu_inf}; {vc.get('levels')} levels (min_cells={min_cells}), 2+2 Vanka "
                                f"(omega={cfg.omega}, surrogate patches at rep_fraction={cfg.rep_fraction}), coarsest "
-                               f"level: dense LU up to 4096 dofs, else {args.coarse_sweeps} Vanka steps, "
+                               f"level: dense LU up to 4096 dofs, else FGMRES(<= 30, rtol 1e-6) preconditioned by "
+                               f"{2 if args.coarse_sweeps is None else args.coarse_sweeps} Vanka steps, "
                                f"FGMRES(restart={args.restart}, budget {args.max_krylov}) in the M-inner product, "
                                f"Eisenstat-Walker eta0=1e-2",
                    "n_dof": N},
@@ -1003,7 +1004,8 @@ def main():
     ap.add_argument("--levels", type=int, default=5)
     ap.add_argument("--restart", type=int, default=20)
     ap.add_argument("--max-krylov", type=int, default=60)
-    ap.add_argument("--coarse-sweeps", type=int, default=30)
+    ap.add_argument("--coarse-sweeps", type=int, default=None,
+                    help="--solve: Vanka steps per coarsest-level preconditioner application (default 2)")
     ap.add_argument("--vcycle", action="store_true", help="distributed V-cycle timing (configs[4] strong scaling)")
     ap.add_argument("--coarse-iters", type=int, default=30)
     ap.add_argument("--secondary", default="cfg5",
