@@ -335,6 +335,123 @@ __global__ void __launch_bounds__(128) k_invert(const double* __restrict__ mats,
   }
 }
 
+// The same inversion for D <= 42 with the matrix in REGISTERS: lane l holds
+// rows l and l + 32 (D = 42: lanes 0-9 two rows), no physical row swaps (the
+// pivot row is the unused row with the largest |entry|, ties to the lower
+// row; lane / slot p_k that pivoted column k ends up holding row k of the
+// inverse with entry j standing for column p_j, undone on the store as in
+// k_invert_diag).  Per step the pivot row goes through shared memory, where
+// lane j scales entry j by 1 / pivot, and every lane eliminates its rows with
+// it: D DFMA per row and step, D / 2 16-byte shared loads per warp and step -
+// the shared-memory kernel above moves three words per DFMA and is bound by
+// that.  Same operations per entry (scaled pivot row, fma(-f, P_j, R_j)).
+template <int D>
+__global__ void __launch_bounds__(128, D > 32 ? 2 : 4) k_invert_rows(const double* __restrict__ mats,
+                                                                   double* __restrict__ invT, int npatch,
+                                                                   int* __restrict__ bad) {
+  constexpr int WPB = 4, NS = (D + 31) / 32, DP = (D + 1) & ~1;
+  __shared__ __align__(16) double prow[WPB][DP];
+  __shared__ int piv[WPB][D];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = blockIdx.x * WPB + warp;
+  if (K >= npatch) return;
+  const double* src = mats + (size_t)K * D * D;
+  double R[NS][D];
+  bool used[NS];
+  int mycol[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int r = lane + 32 * s;
+    used[s] = r >= D;
+    mycol[s] = -1;
+#pragma unroll
+    for (int j = 0; j < D; ++j) R[s][j] = r < D ? __ldg(src + (size_t)r * D + j) : 0.0;
+  }
+  if (lane == 0 && DP > D) prow[warp][DP - 1] = 0.0;
+  bool singular = false;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    double best = -1.0;
+    int bi = 64;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const double v = fabs(R[s][k]);
+      if (!used[s] && v > best) {
+        best = v;
+        bi = lane + 32 * s;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (ov > best || (ov == best && oi < bi)) {
+        best = ov;
+        bi = oi;
+      }
+    }
+    if (!(best > 0.0)) {
+      singular = true;
+      break;
+    }
+    const int pl = bi & 31, ps = bi >> 5;
+    double pv = R[0][k];
+    if (NS > 1 && ps) pv = R[NS - 1][k];
+    const double pinv = 1.0 / __shfl_sync(0xffffffffu, pv, pl);
+    if (lane == pl) {  // the pivot row goes to shared memory as it is
+#pragma unroll
+      for (int s = 0; s < NS; ++s)
+        if (ps == s) {
+#pragma unroll
+          for (int j = 0; j < D; ++j) prow[warp][j] = R[s][j];
+          used[s] = true;
+          mycol[s] = k;
+        }
+      piv[warp][k] = bi;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {  // lane j scales entry j
+      const int j = lane + 32 * s;
+      if (j < D) prow[warp][j] = (j == k ? 1.0 : prow[warp][j]) * pinv;
+    }
+    __syncwarp();
+    double f[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) f[s] = R[s][k];
+#pragma unroll
+    for (int j2 = 0; j2 < DP / 2; ++j2) {
+      if (NS > 1 && j2 % 3 == 0) asm volatile("" ::: "memory");  // keep the row loads from piling up in registers
+      const double2 a = reinterpret_cast<const double2*>(prow[warp])[j2];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        R[s][2 * j2] = fma(-f[s], a.x, 2 * j2 == k ? 0.0 : R[s][2 * j2]);
+        if (2 * j2 + 1 < D) R[s][2 * j2 + 1] = fma(-f[s], a.y, 2 * j2 + 1 == k ? 0.0 : R[s][2 * j2 + 1]);
+      }
+    }
+    if (lane == pl) {  // the pivot lane takes its scaled row back (its own elimination result is discarded)
+#pragma unroll
+      for (int s = 0; s < NS; ++s)
+        if (ps == s) {
+#pragma unroll
+          for (int j = 0; j < D; ++j) R[s][j] = prow[warp][j];
+        }
+    }
+    __syncwarp();
+  }
+  if (singular) {
+    if (lane == 0) atomicMin(bad, K);
+    return;
+  }
+  double* dst = invT + (size_t)K * D * D;
+#pragma unroll
+  for (int s = 0; s < NS; ++s)
+    if (lane + 32 * s < D) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) dst[(size_t)piv[warp][j] * D + mycol[s]] = R[s][j];
+    }
+}
+
 // Slab dof of local patch position l of cell K.
 __device__ __forceinline__ size_t patch_dof(const Geom& g, int K, int l) {
   const int mu = l / 21, s = l % 21;
@@ -487,6 +604,10 @@ __global__ void __launch_bounds__(256, 4) k_vanka_scatter(Geom g, int k1, const 
 
 template <int D>
 cudaError_t launch_invert(const double* mats, double* invT, int np, int* bad, cudaStream_t st) {
+  if constexpr (D <= 42) {
+    PDST_LAUNCH(k_invert_rows<D><<<(np + 3) / 4, 128, 0, st>>>(mats, invT, np, bad));
+    return cudaGetLastError();
+  }
   constexpr int WPB = inv_wpb<D>();
   const size_t smem = (size_t)WPB * (D * (D + 1) + D) * sizeof(double);
   static DeviceOnce once;

@@ -246,10 +246,12 @@ __device__ __forceinline__ double cabs1(double2 z) { return fabs(z.x) + fabs(z.y
 // complex), lane r < 21 holding row r in REGISTERS, Gauss-Jordan by exchange
 // steps with partial pivoting (the pivot row is chosen among the rows not yet
 // used by the largest |Re| + |Im| as izamax / dcabs1 in zgetrf, ties to the
-// lower row) and no physical row swaps: the pivot lane scales its row and
-// broadcasts it through shared memory, the other lanes eliminate.  The same
-// operations as the in-place Gauss-Jordan with row swaps, so the same
-// rounding; after all steps lane p_k holds row k of the inverse with its
+// lower row) and no physical row swaps: the pivot row goes through shared
+// memory, where lane j scales its entry j by 1 / pivot (one complex product
+// per lane instead of 21 on the pivot lane alone), the pivot lane reads the
+// scaled row back and the other lanes eliminate with it (4 DFMA per entry).
+// The in-place Gauss-Jordan with row swaps, operation for operation, up to
+// the fused roundings; after all steps lane p_k holds row k of the inverse with its
 // column k' standing for column p_k' (tableau exchange), undone on the store.
 // Output transposed: binvT[K][b][col][row].
 __global__ void __launch_bounds__(128, 3) k_invert_diag(Geom g, TimeDiag td, const double* __restrict__ spatial,
@@ -306,28 +308,33 @@ __global__ void __launch_bounds__(128, 3) k_invert_diag(Geom g, TimeDiag td, con
       singular = true;
       break;
     }
-    if (lane == bi) {  // the pivot row: R[k] <- 1 / R[k], R[j] <- R[j] / R[k]
-      const double2 p = R[k];
-      const double den = p.x * p.x + p.y * p.y;
-      const double2 pinv = make_double2(p.x / den, -p.y / den);
+    // 1 / pivot on every lane (the pivot value broadcast by shuffle)
+    const double px = __shfl_sync(0xffffffffu, R[k].x, bi), py = __shfl_sync(0xffffffffu, R[k].y, bi);
+    const double den = px * px + py * py;
+    const double2 pinv = make_double2(px / den, -py / den);
+    if (lane == bi) {  // the pivot row goes to shared memory as it is
 #pragma unroll
-      for (int j = 0; j < N; ++j) {
-        const double2 a = (j == k) ? make_double2(1.0, 0.0) : R[j];
-        R[j] = make_double2(a.x * pinv.x - a.y * pinv.y, a.x * pinv.y + a.y * pinv.x);
-        prow[warp][j] = R[j];
-      }
+      for (int j = 0; j < N; ++j) prow[warp][j] = R[j];
       piv[warp][k] = lane;
       used = true;
       mycol = k;
     }
     __syncwarp();
-    if (row && lane != bi) {  // eliminate column k: R[j] -= f P[j], R[k] = -f P[k]
+    if (row) {  // lane j scales entry j: P[k] <- 1 / pivot, P[j] <- P[j] / pivot
+      const double2 a = (lane == k) ? make_double2(1.0, 0.0) : prow[warp][lane];
+      prow[warp][lane] = make_double2(a.x * pinv.x - a.y * pinv.y, a.x * pinv.y + a.y * pinv.x);
+    }
+    __syncwarp();
+    if (lane == bi) {  // the pivot lane takes its scaled row back
+#pragma unroll
+      for (int j = 0; j < N; ++j) R[j] = prow[warp][j];
+    } else if (row) {  // the others eliminate column k: R[j] -= f P[j], R[k] = -f P[k]
       const double2 f = R[k];
 #pragma unroll
       for (int j = 0; j < N; ++j) {
         const double2 base = (j == k) ? make_double2(0.0, 0.0) : R[j];
         const double2 a = prow[warp][j];
-        R[j] = make_double2(base.x - (f.x * a.x - f.y * a.y), base.y - (f.x * a.y + f.y * a.x));
+        R[j] = make_double2(fma(f.y, a.y, fma(-f.x, a.x, base.x)), fma(-f.y, a.x, fma(-f.x, a.y, base.y)));
       }
     }
     __syncwarp();
