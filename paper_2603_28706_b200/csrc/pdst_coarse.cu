@@ -198,39 +198,75 @@ __global__ void k_pm_init() {
 }
 
 // Galerkin coarse cell block: one CTA (448 threads) per (coarse cell, mu).
+// The four children's triple products P_K' E_K P_K run side by side on 196
+// threads, each holding a 3 x 3 register tile of one child's product (six
+// shared-memory operands per nine DFMA; one output per thread needed two per
+// DFMA and was bound by the shared-memory pipe); every entry is still the
+// same m-ordered fma chain and the children are summed in the same order.
 __global__ void __launch_bounds__(448, 3) k_galerkin_cells(LevelOp f, Geom gc, double* __restrict__ ecell_c) {
-  __shared__ double T[21][22];
   __shared__ double Pm[4][21][21];
-  __shared__ double Es[441];  // the child's element block, column-major (staged with coalesced loads)
-  __shared__ double FB[16][9][10];  // the interior fine faces' node blocks
-  __shared__ double SB[8][9][18];   // their products with the prolongation, 8 blocks at a time
+  // Es[4][441] (the children's element blocks, column-major; later their products) and T[4][21][22];
+  // the face part below reuses the space as FB[16][9][10] and SB[8][9][18]
+  __shared__ __align__(16) double W[4 * 441 + 4 * 21 * 22];
+  double* Es = W;
+  double(*T)[21][22] = reinterpret_cast<double(*)[21][22]>(W + 4 * 441);
+  double(*FB)[9][10] = reinterpret_cast<double(*)[9][10]>(W);
+  double(*SB)[9][18] = reinterpret_cast<double(*)[9][18]>(W + 16 * 90);
   const int C = blockIdx.x, mu = blockIdx.y;
   const int t = threadIdx.x;
   const int ci = C % gc.nx, cj = C / gc.nx;
   for (int idx = t; idx < 4 * 441; idx += blockDim.x) (&Pm[0][0][0])[idx] = g_pm[idx];
-  const int i = t / 21, j = t % 21;
-  double acc = 0.0;
-  for (int k = 0; k < 4; ++k) {
-    const int ox = k & 1, oy = k >> 1;
-    const int K = (2 * cj + oy) * f.g.nx + 2 * ci + ox;
-    if (t < 441) Es[t] = f.ecell[((size_t)mu * f.g.ncells + K) * 441 + t];
-    __syncthreads();  // (also orders Pm on the first pass and the previous child's reads of T)
-    // T = E_K P_K  (rows = child dofs, cols = parent dofs)
-    if (t < 441) {
-      double s = 0.0;
-#pragma unroll
-      for (int m = 0; m < 21; ++m) s = fma(Es[m * 21 + i], Pm[k][m][j], s);
-      T[i][j] = s;
-    }
-    __syncthreads();
-    if (t < 441) {
-      double s = 0.0;
-#pragma unroll
-      for (int m = 0; m < 21; ++m) s = fma(Pm[k][m][i], T[m][j], s);
-      acc += s;
-    }
-    // (the next pass's barrier after staging Es separates these reads of T from its writes)
+  for (int idx = t; idx < 4 * 441; idx += blockDim.x) {
+    const int k = idx / 441, e = idx - 441 * k;
+    const int K = (2 * cj + (k >> 1)) * f.g.nx + 2 * ci + (k & 1);
+    Es[idx] = f.ecell[((size_t)mu * f.g.ncells + K) * 441 + e];
   }
+  const int i = t / 21, j = t % 21;
+  const int tk = t / 49, tile = t % 49, i0 = 3 * (tile / 7), j0 = 3 * (tile % 7);
+  __syncthreads();
+  if (t < 196) {  // T_k = E_k P_k  (rows = child dofs, cols = parent dofs)
+    double s[3][3] = {};
+#pragma unroll 3
+    for (int m = 0; m < 21; ++m) {
+      double e[3], pr[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) e[r] = Es[tk * 441 + m * 21 + i0 + r];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) pr[c] = Pm[tk][m][j0 + c];
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) s[r][c] = fma(e[r], pr[c], s[r][c]);
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) T[tk][i0 + r][j0 + c] = s[r][c];
+  }
+  __syncthreads();
+  if (t < 196) {  // P_k' T_k, into the child's (now free) element block space, row-major
+    double s[3][3] = {};
+#pragma unroll 3
+    for (int m = 0; m < 21; ++m) {
+      double pl[3], tr[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) pl[r] = Pm[tk][m][i0 + r];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) tr[c] = T[tk][m][j0 + c];
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) s[r][c] = fma(pl[r], tr[c], s[r][c]);
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) Es[tk * 441 + (i0 + r) * 21 + j0 + c] = s[r][c];
+  }
+  __syncthreads();
+  double acc = 0.0;
+  if (t < 441)
+    for (int k = 0; k < 4; ++k) acc += Es[k * 441 + i * 21 + j];
   __syncthreads();
   // fine faces interior to C: vertical (children (0,oy)|(1,oy)), horizontal ((ox,0)|(ox,1)).
   // All 16 (face, side, side) node blocks are evaluated first, by all threads, then summed
