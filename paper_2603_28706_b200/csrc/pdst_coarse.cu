@@ -492,58 +492,68 @@ __global__ void k_level_gather(LevelOp op, const double* __restrict__ cp, const 
 __device__ __forceinline__ int ceil_half(int v) { return v <= 0 ? -((-v) / 2) : (v + 1) / 2; }
 __device__ __forceinline__ int floor_half(int v) { return v >= 0 ? v / 2 : -((-v + 1) / 2); }
 
-// (R_K J R_K')_{ij} of a level in element form.
-__device__ double level_spatial_entry(const LevelOp& op, int mu, int K, int i, int j) {
+// (R_K J_mu R_K')_{ij} of a level in element form, for every Radau node at once
+// (the cells and faces an entry gathers from do not depend on mu).
+template <int K1>
+__device__ __forceinline__ void level_spatial_entries(const LevelOp& op, int K, int i, int j, double* val) {
   const Geom& g = op.g;
-  if (i >= 18 || j >= 18) return cell_entry(op, mu, K, i, j);
+#pragma unroll
+  for (int mu = 0; mu < K1; ++mu) val[mu] = 0.0;
+  if (i >= 18 || j >= 18) {
+#pragma unroll
+    for (int mu = 0; mu < K1; ++mu) val[mu] = cell_entry(op, mu, K, i, j);
+    return;
+  }
   const int ki = K % g.nx, kj = K / g.nx;
   const int ia = i >> 1, d = i & 1, jb = j >> 1, e = j & 1;
   const int XA = 2 * ki + ia % 3, YA = 2 * kj + ia / 3;
   const int XB = 2 * ki + jb % 3, YB = 2 * kj + jb / 3;
   const int xmin = min(XA, XB), xmax = max(XA, XB), ymin = min(YA, YB), ymax = max(YA, YB);
-  double val = 0.0;
   for (int cy = max(0, ceil_half(ymax - 2)); cy <= min(g.ny - 1, floor_half(ymin)); ++cy)
     for (int cx = max(0, ceil_half(xmax - 2)); cx <= min(g.nx - 1, floor_half(xmin)); ++cx) {
       const int c = cy * g.nx + cx;
       const int al = 3 * (YA - 2 * cy) + (XA - 2 * cx), bl = 3 * (YB - 2 * cy) + (XB - 2 * cx);
-      val += cell_entry(op, mu, c, 2 * al + d, 2 * bl + e);
+#pragma unroll
+      for (int mu = 0; mu < K1; ++mu) val[mu] += cell_entry(op, mu, c, 2 * al + d, 2 * bl + e);
     }
-  if (d != e) return val;
+  if (d != e) return;
   for (int axis = 0; axis < 2; ++axis) {
     const int nfx = axis == 0 ? g.nx - 1 : g.nx, nfy = axis == 0 ? g.ny : g.ny - 1;
     const int xr = axis == 0 ? 4 : 2, yr = axis == 0 ? 2 : 4;
     for (int fj = max(0, ceil_half(ymax - yr)); fj <= min(nfy - 1, floor_half(ymin)); ++fj)
       for (int fi = max(0, ceil_half(xmax - xr)); fi <= min(nfx - 1, floor_half(xmin)); ++fi) {
-        const int cl = fj * g.nx + fi, cr = axis == 0 ? cl + 1 : cl + g.nx;
+        // the face's cells: (fi, fj) and its right / upper neighbour
         for (int sA = 0; sA < 2; ++sA) {
-          const int cA = sA == 0 ? cl : cr;
-          const int ax = XA - 2 * (cA % g.nx), ay = YA - 2 * (cA / g.nx);
+          const int ax = XA - 2 * (fi + (axis == 0 ? sA : 0)), ay = YA - 2 * (fj + (axis == 1 ? sA : 0));
           if (ax < 0 || ax > 2 || ay < 0 || ay > 2) continue;
           for (int sB = 0; sB < 2; ++sB) {
-            const int cB = sB == 0 ? cl : cr;
-            const int bx = XB - 2 * (cB % g.nx), by = YB - 2 * (cB / g.nx);
+            const int bx = XB - 2 * (fi + (axis == 0 ? sB : 0)), by = YB - 2 * (fj + (axis == 1 ? sB : 0));
             if (bx < 0 || bx > 2 || by < 0 || by > 2) continue;
-            val += face_entry(op, mu, axis, fi, fj, sA, 3 * ay + ax, sB, 3 * by + bx);
+#pragma unroll
+            for (int mu = 0; mu < K1; ++mu) val[mu] += face_entry(op, mu, axis, fi, fj, sA, 3 * ay + ax, sB, 3 * by + bx);
           }
         }
       }
   }
-  return val;
 }
 
 // Exact coarse patches: A_K = sum K_t (x) R_K M R_K' + tau w_mu R_K J_mu R_K'.
 // The spatial entries are evaluated column-major (consecutive threads =
 // consecutive rows i: the element and face blocks are stored column-major, so
 // their loads coalesce), staged in shared memory, and written row-major.
+template <int K1>
 __global__ void __launch_bounds__(448, 3) k_patch_level(LevelOp op, TimeData td, double* __restrict__ mats) {
-  __shared__ double sJ[MAXK1][441];  // [mu][i * 21 + j]
+  __shared__ double sJ[K1][441];  // [mu][i * 21 + j]
   const int K = blockIdx.x;
   const int t = threadIdx.x;
   const Geom& g = op.g;
   const int k1 = td.k1, D = 21 * k1;
   if (t < 441) {
     const int ci_ = t % 21, cj_ = t / 21;
-    for (int mu = 0; mu < k1; ++mu) sJ[mu][ci_ * 21 + cj_] = level_spatial_entry(op, mu, K, ci_, cj_);
+    double val[K1];
+    level_spatial_entries<K1>(op, K, ci_, cj_, val);
+#pragma unroll
+    for (int mu = 0; mu < K1; ++mu) sJ[mu][ci_ * 21 + cj_] = val[mu];
   }
   __syncthreads();
   if (t >= 441) return;
@@ -839,7 +849,13 @@ cudaError_t level_apply(const LevelOp& op, const TimeData& td, const double* x, 
 }
 
 cudaError_t patch_assemble_level(const LevelOp& op, const TimeData& td, double* mats, cudaStream_t st) {
-  PDST_LAUNCH(k_patch_level<<<op.g.ncells, 448, 0, st>>>(op, td, mats));
+  switch (td.k1) {  // exact patches exist up to D = 84 (pdst_patch.cu launch_invert)
+    case 1: PDST_LAUNCH(k_patch_level<1><<<op.g.ncells, 448, 0, st>>>(op, td, mats)); break;
+    case 2: PDST_LAUNCH(k_patch_level<2><<<op.g.ncells, 448, 0, st>>>(op, td, mats)); break;
+    case 3: PDST_LAUNCH(k_patch_level<3><<<op.g.ncells, 448, 0, st>>>(op, td, mats)); break;
+    case 4: PDST_LAUNCH(k_patch_level<4><<<op.g.ncells, 448, 0, st>>>(op, td, mats)); break;
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 
