@@ -169,6 +169,31 @@ __device__ double cip_block(const Geom& g, const Disc& ds, const double* v, int 
   return coef * s;
 }
 
+// cip_block in two steps for the Galerkin kernels, which evaluate all 324 entries of a fine
+// face: the point weights (w_q h) |a_L . n| once per (face, q), then the entry from them
+// (the same products in the same order).
+__device__ double cip_point_weight(const Geom& g, const double* v, int axis, int fi, int fj, int q) {
+  const double hface = axis == 0 ? g.hy : g.hx;
+  double tr = 0.0;
+  for (int t = 0; t < 3; ++t) {
+    const size_t node = axis == 0 ? (size_t)(2 * fj + t) * g.nnx + 2 * fi + 2 : (size_t)(2 * fj + 2) * g.nnx + 2 * fi + t;
+    tr = fma(c_tab.B[q][t], v[2 * node + axis], tr);
+  }
+  return (c_tab.w[q] * hface) * fabs(tr);
+}
+__device__ double cip_block_w(const Geom& g, const Disc& ds, const double* wq, int axis, int sA, int a, int sB, int b) {
+  const double hface = axis == 0 ? g.hy : g.hx;
+  const double ihn = axis == 0 ? g.ihx : g.ihy;
+  const double coef = ds.gamma_cip * hface * hface * ihn * ihn;
+  const int na = axis == 0 ? a % 3 : a / 3, ta = axis == 0 ? a / 3 : a % 3;
+  const int nb = axis == 0 ? b % 3 : b / 3, tb = axis == 0 ? b / 3 : b % 3;
+  const double fa = sA == 0 ? c_tab.dE[1][na] : -c_tab.dE[0][na];
+  const double fb = sB == 0 ? c_tab.dE[1][nb] : -c_tab.dE[0][nb];
+  double s = 0.0;
+  for (int q = 0; q < 4; ++q) s += wq[q] * (fa * c_tab.B[q][ta]) * (fb * c_tab.B[q][tb]);
+  return coef * s;
+}
+
 // Face block entry of a level (stored for coarse levels, on the fly for the finest).
 __device__ __forceinline__ double face_entry(const LevelOp& op, int mu, int axis, int fi, int fj, int sA, int a, int sB,
                                              int b) {
@@ -267,6 +292,14 @@ __global__ void __launch_bounds__(448, 3) k_galerkin_cells(LevelOp f, Geom gc, d
   double acc = 0.0;
   if (t < 441)
     for (int k = 0; k < 4; ++k) acc += Es[k * 441 + i * 21 + j];
+  // finest level: the CIP point weights of the four interior fine faces, once per (face, point)
+  __shared__ double Wq[4][4];
+  const bool fine_cip = f.fine && f.ds.convection && f.ds.gamma_cip > 0.0;
+  if (fine_cip && t < 16) {
+    const int fidx = t >> 2, axis = fidx < 2 ? 0 : 1, o = fidx & 1;
+    Wq[fidx][t & 3] = cip_point_weight(f.g, f.state + (size_t)mu * f.g.mv, axis, 2 * ci + (axis == 0 ? 0 : o),
+                                       2 * cj + (axis == 0 ? o : 0), t & 3);
+  }
   __syncthreads();
   // fine faces interior to C: vertical (children (0,oy)|(1,oy)), horizontal ((ox,0)|(ox,1)).
   // All 16 (face, side, side) node blocks are evaluated first, by all threads, then summed
@@ -276,7 +309,9 @@ __global__ void __launch_bounds__(448, 3) k_galerkin_cells(LevelOp f, Geom gc, d
     const int fidx = blk >> 2, sA = (blk >> 1) & 1, sB = blk & 1;
     const int axis = fidx < 2 ? 0 : 1, o = fidx & 1;
     const int fi = 2 * ci + (axis == 0 ? 0 : o), fj = 2 * cj + (axis == 0 ? o : 0);
-    FB[blk][e / 9][e % 9] = face_entry(f, mu, axis, fi, fj, sA, e / 9, sB, e % 9);
+    FB[blk][e / 9][e % 9] = !f.fine      ? face_entry(f, mu, axis, fi, fj, sA, e / 9, sB, e % 9)
+                            : fine_cip ? cip_block_w(f.g, f.ds, Wq[fidx], axis, sA, e / 9, sB, e % 9)
+                                       : 0.0;
   }
   __syncthreads();
   // sum_{a,b} P_kA[2a+d][i] F[a][b] P_kB[2b+d][j] per block, factored: the inner sums
@@ -323,6 +358,8 @@ __global__ void __launch_bounds__(324, 4) k_galerkin_faces(LevelOp f, Geom gc, d
   __shared__ double Pn[4][9][9];  // node-level prolongation of child k: Pn[k][a_fine][b_coarse]
   __shared__ double F[2][2][9][9];
   __shared__ double SBf[2][2][9][9];
+  __shared__ double wq[4];  // finest level: the fine face's CIP point weights
+  const bool fine_cip = f.fine && f.ds.convection && f.ds.gamma_cip > 0.0;
   const int axis = blockIdx.z, mu = blockIdx.y;
   const int nfx = axis == 0 ? gc.nx - 1 : gc.nx;
   const int nface = axis == 0 ? (gc.nx - 1) * gc.ny : gc.nx * (gc.ny - 1);
@@ -341,8 +378,12 @@ __global__ void __launch_bounds__(324, 4) k_galerkin_faces(LevelOp f, Geom gc, d
     const int ffi = axis == 0 ? 2 * fi + 1 : 2 * fi + o, ffj = axis == 0 ? 2 * fj + o : 2 * fj + 1;
     const int kl = axis == 0 ? (1 + 2 * o) : (o + 2 * 1);  // child index in the left/lower coarse cell
     const int kr = axis == 0 ? (0 + 2 * o) : (o + 2 * 0);  // child index in the right/upper coarse cell
+    if (fine_cip && t < 4) wq[t] = cip_point_weight(f.g, f.state + (size_t)mu * f.g.mv, axis, ffi, ffj, t);
     __syncthreads();
-    if (t < 324) F[sA][sB][a][b] = face_entry(f, mu, axis, ffi, ffj, sA, a, sB, b);
+    if (t < 324)
+      F[sA][sB][a][b] = !f.fine      ? face_entry(f, mu, axis, ffi, ffj, sA, a, sB, b)
+                        : fine_cip ? cip_block_w(f.g, f.ds, wq, axis, sA, a, sB, b)
+                                   : 0.0;
     __syncthreads();
     // factored: SBf[sA][sB][p][b] = sum_q F[sA][sB][p][q] Pn[kB][q][b] once per (p, b), thread (a, b) playing (p, b)
     if (t < 324) {

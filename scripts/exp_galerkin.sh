@@ -1,7 +1,7 @@
 #!/bin/bash
 # Galerkin cell kernel change: multigrid parity, then the cfg5 hierarchy build and the kernel's ncu times
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_gpu_multigrid.py tests/test_gpu_solvers.py tests/test_gpu_dist_mg.py -m gpu -x -q > gpurun_out/galerkin_tests.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/galerkin_tests.log 2>&1
 tail -3 gpurun_out/galerkin_tests.log
 python bench.py --solve --config cfg5 > gpurun_out/solve_galerkin.json 2>/dev/null
 python -c "import json;d=json.load(open('gpurun_out/solve_galerkin.json'));print('solve build_s',d['preconditioner_build_s'],'vcycle',d['ms_per_vcycle'],'iters',d['krylov_iterations'],d['newton_message'])"
