@@ -229,7 +229,7 @@ __global__ void k_pm_init() {
 // DFMA and was bound by the shared-memory pipe); every entry is still the
 // same m-ordered fma chain and the children are summed in the same order.
 __global__ void __launch_bounds__(448, 3) k_galerkin_cells(LevelOp f, Geom gc, double* __restrict__ ecell_c) {
-  __shared__ double Pm[4][21][21];
+  __shared__ double Pm[4][21][22];  // row stride 22: rows 2b and 2b + 1 read side by side fall into disjoint banks
   // Es[4][441] (the children's element blocks, column-major; later their products) and T[4][21][22];
   // the face part below reuses the space as FB[16][9][10] and SB[8][9][18]
   __shared__ __align__(16) double W[4 * 441 + 4 * 21 * 22];
@@ -240,7 +240,10 @@ __global__ void __launch_bounds__(448, 3) k_galerkin_cells(LevelOp f, Geom gc, d
   const int C = blockIdx.x, mu = blockIdx.y;
   const int t = threadIdx.x;
   const int ci = C % gc.nx, cj = C / gc.nx;
-  for (int idx = t; idx < 4 * 441; idx += blockDim.x) (&Pm[0][0][0])[idx] = g_pm[idx];
+  for (int idx = t; idx < 4 * 441; idx += blockDim.x) {
+    const int e = idx % 441;
+    Pm[idx / 441][e / 21][e % 21] = g_pm[idx];
+  }
   for (int idx = t; idx < 4 * 441; idx += blockDim.x) {
     const int k = idx / 441, e = idx - 441 * k;
     const int K = (2 * cj + (k >> 1)) * f.g.nx + 2 * ci + (k & 1);
